@@ -1,0 +1,224 @@
+/* tgsx — B200-native (sm_100a) Turbo-GS fit hot path, C ABI.
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (a C++20 static library, /root/reference/proj/core) exposes the path as C++ templates; a
+ * maintainer binds this ABI from C++ through the shim in paper_2412_13547_b200/shim/
+ * (re-implements tgs::render<float> / tgs::backward<float> with the exact reference
+ * signatures) or from any FFI (ctypes stub in INTEGRATION.md).
+ *
+ * Conventions
+ *  - Every function returns int32 status: TGSX_OK or an error code; the message is available
+ *    from tgsx_last_error(ctx). Error codes mirror the reference's exception types:
+ *      TGSX_EINVAL   <-> std::invalid_argument (rasterizer.cpp:222-224, dilation.hpp:18-22,
+ *                        gaussian.hpp:64-68)
+ *      TGSX_ERUNTIME <-> std::runtime_error     (gaussian.hpp:84-86, degenerate covariance)
+ *  - Pointer arguments documented "host or device" are resolved through CUDA unified virtual
+ *    addressing: pass host memory (pinned for async copies) or device memory.
+ *  - All work is enqueued on the context's stream; functions that return data to host memory
+ *    synchronize that stream before returning. One context per host thread; a model may be
+ *    used by one context at a time (the reference is likewise not re-entrant on one model,
+ *    model.hpp:150-151).
+ *  - Arrays are in MODEL (creation/index) order unless stated; "rank" arrays (per active
+ *    pixel) follow the reference's dense rank (dilation.hpp:32, rasterizer.hpp:21-26).
+ */
+#ifndef TGSX_H
+#define TGSX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TGSX_VERSION_MAJOR 0
+#define TGSX_VERSION_MINOR 1
+
+enum {
+    TGSX_OK = 0,
+    TGSX_EINVAL = 1,
+    TGSX_ERUNTIME = 2,
+    TGSX_ECUDA = 3,
+    TGSX_ENOMEM = 4,
+    TGSX_ESTATE = 5
+};
+
+typedef struct tgsx_ctx tgsx_ctx;
+typedef struct tgsx_model tgsx_model;
+typedef struct tgsx_budget tgsx_budget;
+
+/* DilationPattern (dilation.hpp:14-56): pixel (x,y) active iff x%p==ox && y%p==oy. */
+typedef struct {
+    int32_t p, ox, oy, width, height;
+} tgsx_pattern;
+
+/* Host-side scene in model order: the SoA view of GaussianModel<float> (model.hpp:45-152,
+ * Gaussian2D gaussian.hpp:35-44, DensifyStats model.hpp:17-40). Stats / tau_v pointers may be
+ * NULL on upload (zeros / tau_v = 5.0) and are skipped on download when NULL. */
+typedef struct {
+    int64_t n;
+    float *px, *py, *rot, *lsx, *lsy, *rop, *cr, *cg, *cb, *depth;
+    uint64_t* id;
+    uint64_t next_id;
+    float *pos_acc, *col_acc;
+    int32_t* accum;
+    int64_t *visit, *window;
+    double* tau_v;
+} tgsx_host_scene;
+
+/* ---------------------------------------------------------------- context */
+int32_t tgsx_create(int32_t device, tgsx_ctx** out);
+void tgsx_destroy(tgsx_ctx* ctx);
+/* Replaces the context's stream (a cudaStream_t; NULL = the context's own stream). */
+int32_t tgsx_set_stream(tgsx_ctx* ctx, void* stream);
+void* tgsx_get_stream(tgsx_ctx* ctx);
+const char* tgsx_last_error(const tgsx_ctx* ctx);
+int32_t tgsx_synchronize(tgsx_ctx* ctx);
+/* Counters of this library's kernel launches on ctx (for the bench's gpu_launches claim). */
+uint64_t tgsx_launch_count(const tgsx_ctx* ctx);
+/* Live per-stage timing: CUDA events recorded on the context stream around each stage
+ * (0 depth sort, 1 preprocess, 2 scan, 3 duplicate, 4 radix sort, 5 ranges, 6 blend forward,
+ * 7 blend backward, 8 chain+stats+Adam, 9 loss reduce, 10 densify). Enabling resets totals. */
+int32_t tgsx_profile(tgsx_ctx* ctx, int32_t enable);
+/* Accumulated milliseconds and launch counts per stage (n entries). */
+int32_t tgsx_profile_read(tgsx_ctx* ctx, double* ms, int64_t* counts, int32_t n);
+
+/* ---------------------------------------------------------------- model (device SoA) */
+/* Replaces GaussianModel<float> storage: params, ids, DensifyStats, tau_v (model.hpp:140-151)
+ * plus Adam moments live in HBM for the model's lifetime. */
+int32_t tgsx_model_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model** out);
+void tgsx_model_destroy(tgsx_model* m);
+int64_t tgsx_model_size(const tgsx_model* m);
+uint64_t tgsx_model_next_id(const tgsx_model* m);
+/* Upload replaces the whole model (moments zeroed, Adam step counter kept). */
+int32_t tgsx_model_upload(tgsx_ctx* ctx, tgsx_model* m, const tgsx_host_scene* host);
+/* Download copies params, ids, stats, tau_v into caller arrays sized >= tgsx_model_size. */
+int32_t tgsx_model_download(tgsx_ctx* ctx, tgsx_model* m, tgsx_host_scene* host);
+/* Adam moments, component-major [9][n] float, host or device destination. */
+int32_t tgsx_model_download_moments(tgsx_ctx* ctx, tgsx_model* m, float* m1, float* m2);
+int32_t tgsx_model_upload_moments(tgsx_ctx* ctx, tgsx_model* m, const float* m1, const float* m2);
+
+/* ---------------------------------------------------------------- the reference's ops */
+/* tgs::render<float> (rasterizer.hpp:58-60, rasterizer.cpp:144-184). out_rgb [P*3] and out_T
+ * [P] by dense rank (host or device, may be NULL); *out_blend_ops (host, may be NULL).
+ * lowpass_p = RenderOptions::lowpass_p (rasterizer.hpp:48-53; 0 = pattern p). */
+int32_t tgsx_render(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
+                    int32_t lowpass_p, float* out_rgb, float* out_T, uint64_t* out_blend_ops);
+
+/* tgs::backward<float> (rasterizer.hpp:66-69, rasterizer.cpp:218-361). dLdC [P*3] by rank
+ * (host or device); dLdC_count = number of RGB entries, must equal the pattern's active count
+ * (TGSX_EINVAL otherwise, rasterizer.cpp:222-224). out_grads component-major [9][n] (pos x, pos y, rot, ls x, ls y,
+ * raw_opacity, r, g, b), host or device, may be NULL. Updates the model's DensifyStats in
+ * place when update_stats != 0, like the reference (rasterizer.cpp:350-358). */
+int32_t tgsx_backward(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
+                      int32_t lowpass_p, const float* dLdC, int64_t dLdC_count,
+                      float* out_grads, int32_t update_stats);
+
+/* ---------------------------------------------------------------- fit step (fused path) */
+typedef struct {
+    int64_t step;         /* 1-based Adam step t (bias correction) */
+    int64_t total_steps;  /* position-LR decay horizon */
+    double image_diagonal;
+} tgsx_adam_args;
+
+/* Adam + clamp_parameters (gaussian.hpp:105-116) with explicit
+ * gradients [9][n] (host or device). */
+int32_t tgsx_adam_step(tgsx_ctx* ctx, tgsx_model* m, const float* grads,
+                       const tgsx_adam_args* a);
+
+/* One fused fit iteration on one view: render -> L1 loss over active pixels
+ * -> backward -> densify stats -> Adam. target: full-resolution W*H*3 float RGB, host or
+ * device (a host pointer is copied inside the call). *out_loss (host or device, may be NULL).
+ * Equivalent to render + L1 + backward + tgsx_adam_step with the same args. */
+int32_t tgsx_fit_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
+                      const float* target, const tgsx_adam_args* a, float* out_loss);
+
+/* Batched views (SPEC.md:269-277 accumulate; multi-GPU view sharding):
+ * tgsx_view_accumulate adds one view's gradients and densify-stat increments into the
+ * model's per-step buffer (12 floats per Gaussian: 9 gradient sums, pos-norm sum,
+ * colour-norm sum, visit count). The buffer (device pointer, [12][n] floats) may be
+ * all-reduced across ranks before tgsx_apply_step divides by batch_views, applies the
+ * stats and runs Adam. */
+int32_t tgsx_view_accumulate(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat,
+                             const float bg[3], const float* target, float* out_loss);
+float* tgsx_step_buffer(tgsx_model* m, int64_t* out_floats);
+int32_t tgsx_apply_step(tgsx_ctx* ctx, tgsx_model* m, int32_t batch_views,
+                        const tgsx_adam_args* a);
+
+/* ---------------------------------------------------------------- densify */
+typedef struct {
+    float tau_pos;              /* 2e-4 default; tau_color = 0.01 * tau_pos */
+    float opacity_mask_floor;   /* 0.05 */
+    float opacity_prune_floor;  /* 0.005 */
+    float color_branch_prob;    /* 0.2 */
+    double tau_v_init;          /* 5 */
+} tgsx_densify_config;
+
+typedef struct {
+    int64_t candidates, spawned, pruned, count_after;
+    int32_t color_coin;
+} tgsx_densify_report;
+
+void tgsx_densify_config_default(tgsx_densify_config* c);
+/* One densify event: colour coin -> select_candidates -> cap to budget - count (top-k by
+ * averaged positional norm, ties by index) -> spawn -> prune -> reset accumulators.
+ * rng_state[2] = PCG32 (state, inc) (rng.hpp:10-46), advanced in place exactly as the
+ * sequential draw order would. */
+int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* c,
+                     int64_t budget, uint64_t rng_state[2], tgsx_densify_report* out);
+/* update_visit_thresholds. */
+int32_t tgsx_visit_audit(tgsx_ctx* ctx, tgsx_model* m);
+
+/* ---------------------------------------------------------------- budget controller */
+/* BudgetController, host scalar logic. */
+int32_t tgsx_budget_create(double n_init, double m_final, tgsx_budget** out);
+void tgsx_budget_destroy(tgsx_budget* b);
+int32_t tgsx_budget_record_loss(tgsx_budget* b, int64_t t, double loss);
+void tgsx_budget_update(tgsx_budget* b, int64_t t);
+int64_t tgsx_budget_at(const tgsx_budget* b, double t_norm);
+/* out[5] = alpha, alpha_base, m_adaptive, ema, number of fits */
+void tgsx_budget_state(const tgsx_budget* b, double* out);
+double tgsx_budget_t_norm(int64_t step, int64_t warmup, int64_t densify_end);
+int32_t tgsx_fit_power_exponent(const double* t, const double* y, int64_t n, double* out);
+
+/* ---------------------------------------------------------------- utilities */
+/* Seeded synthetic scene, written into caller host arrays (n entries). */
+void tgsx_synthetic_scene(uint64_t seed, int64_t n, int32_t width, int32_t height,
+                          tgsx_host_scene* out);
+/* PCG32 (rng.hpp:10-46) helpers. */
+void tgsx_pcg32_init(uint64_t state_out[2], uint64_t seed, uint64_t stream);
+double tgsx_pcg32_uniform(uint64_t state[2]);
+void tgsx_pcg32_advance(uint64_t state[2], uint64_t delta);
+
+/* ---------------------------------------------------------------- stage access (parity) */
+/* Per-stage outputs for bit-exact parity checks. All write host or device
+ * memory. prepare: 11 float arrays [11][n] (mean x, mean y, inv00, inv01, inv11, alpha, r, g,
+ * b, rx, ry) + orig[n], in blend order (rasterizer.cpp:23-46). */
+int32_t tgsx_stage_prepare(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, float* out,
+                           uint32_t* orig);
+/* Blend order (model.hpp:106-119). */
+int32_t tgsx_stage_sorted_order(tgsx_ctx* ctx, tgsx_model* m, uint32_t* perm);
+/* Per-tile CSR lists (rasterizer.cpp:59-102): offsets[tiles+1]; items up to items_cap; items
+ * are blend-order indices. */
+int32_t tgsx_stage_tile_lists(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, int32_t width,
+                              int32_t height, uint32_t* offsets, uint32_t* items,
+                              int64_t items_cap, int64_t* out_k);
+/* Screen-space per-Gaussian sums of the last backward (rasterizer.cpp:294-319):
+ * [10][n] floats (mean x, mean y, s00, s01, s11, alpha, r, g, b, visited 0/1). */
+int32_t tgsx_stage_screen_grads(tgsx_ctx* ctx, tgsx_model* m, float* out);
+/* Per-pixel last-contributor count and evaluation counters of the last render:
+ * *out_evals = reference-equivalent pixel-splat evaluations. */
+int32_t tgsx_stage_counters(tgsx_ctx* ctx, uint64_t* out_blend_ops, uint64_t* out_evals,
+                            uint64_t* out_pairs);
+/* Device-wide stable LSD radix sort of (u32 key, u32 value) pairs on the low key_bits bits
+ * (the onesweep kernels used for binning), exposed for direct testing. Device pointers. */
+int32_t tgsx_sort_pairs(tgsx_ctx* ctx, uint32_t* keys, uint32_t* vals, int64_t n,
+                        int32_t key_bits);
+/* Device-wide exclusive scan of u32 (single-pass decoupled look-back). Device pointers;
+ * *out_total (host) may be NULL. */
+int32_t tgsx_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n,
+                            uint64_t* out_total);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGSX_H */

@@ -1,0 +1,14 @@
+"""B200-native (sm_100a) Turbo-GS fit hot path: preprocess -> onesweep tile binning ->
+alpha-blend forward/backward (dilated variant first-class) -> densify statistics -> Adam,
+with GPU densification and the convergence-aware budget controller.
+
+The compute path is libtgsx.so (hand-written CUDA, csrc/); this package is its Python mirror
+of the reference interface (api.py). There is no CPU fallback.
+"""
+from .api import (BudgetController, Context, DeviceModel, DilationPattern, GaussianModel,  # noqa: F401
+                  GradientSet, Pcg32, RenderOptions, RenderOutput, backward, budget_t_norm,
+                  densify_config, fit_power_exponent, lowpass_bump, next_offsets, render)
+
+__all__ = ["BudgetController", "Context", "DeviceModel", "DilationPattern", "GaussianModel",
+           "GradientSet", "Pcg32", "RenderOptions", "RenderOutput", "backward", "budget_t_norm",
+           "densify_config", "fit_power_exponent", "lowpass_bump", "next_offsets", "render"]

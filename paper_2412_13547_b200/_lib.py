@@ -1,0 +1,140 @@
+"""ctypes binding of libtgsx.so (include/tgsx.h).
+
+The product path has no CPU fallback: importing this module on a machine without the built
+library raises, and every call that fails on the device raises the exception type the
+reference would have thrown (TGSX_EINVAL -> ValueError (std::invalid_argument),
+TGSX_ERUNTIME -> RuntimeError (std::runtime_error)).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtgsx.so")
+
+P = C.POINTER
+f32p, f64p = P(C.c_float), P(C.c_double)
+u32p, i32p, i64p, u64p = P(C.c_uint32), P(C.c_int32), P(C.c_int64), P(C.c_uint64)
+vp = C.c_void_p
+
+TGSX_OK, TGSX_EINVAL, TGSX_ERUNTIME, TGSX_ECUDA, TGSX_ENOMEM, TGSX_ESTATE = range(6)
+
+
+class Pattern(C.Structure):
+    _fields_ = [("p", C.c_int32), ("ox", C.c_int32), ("oy", C.c_int32), ("width", C.c_int32),
+                ("height", C.c_int32)]
+
+
+class HostScene(C.Structure):
+    _fields_ = [("n", C.c_int64)] + [(f, f32p) for f in (
+        "px", "py", "rot", "lsx", "lsy", "rop", "cr", "cg", "cb", "depth")] + [
+        ("id", u64p), ("next_id", C.c_uint64), ("pos_acc", f32p), ("col_acc", f32p),
+        ("accum", i32p), ("visit", i64p), ("window", i64p), ("tau_v", f64p)]
+
+
+class AdamArgs(C.Structure):
+    _fields_ = [("step", C.c_int64), ("total_steps", C.c_int64), ("image_diagonal", C.c_double)]
+
+
+class DensifyConfig(C.Structure):
+    _fields_ = [("tau_pos", C.c_float), ("opacity_mask_floor", C.c_float),
+                ("opacity_prune_floor", C.c_float), ("color_branch_prob", C.c_float),
+                ("tau_v_init", C.c_double)]
+
+
+class DensifyReport(C.Structure):
+    _fields_ = [("candidates", C.c_int64), ("spawned", C.c_int64), ("pruned", C.c_int64),
+                ("count_after", C.c_int64), ("color_coin", C.c_int32)]
+
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "tgsx_create": (C.c_int32, [C.c_int32, P(vp)]),
+    "tgsx_destroy": (None, [vp]),
+    "tgsx_set_stream": (C.c_int32, [vp, vp]),
+    "tgsx_get_stream": (vp, [vp]),
+    "tgsx_last_error": (C.c_char_p, [vp]),
+    "tgsx_synchronize": (C.c_int32, [vp]),
+    "tgsx_launch_count": (C.c_uint64, [vp]),
+    "tgsx_profile": (C.c_int32, [vp, C.c_int32]),
+    "tgsx_profile_read": (C.c_int32, [vp, f64p, i64p, C.c_int32]),
+    "tgsx_model_create": (C.c_int32, [vp, C.c_int64, P(vp)]),
+    "tgsx_model_destroy": (None, [vp]),
+    "tgsx_model_size": (C.c_int64, [vp]),
+    "tgsx_model_next_id": (C.c_uint64, [vp]),
+    "tgsx_model_upload": (C.c_int32, [vp, vp, P(HostScene)]),
+    "tgsx_model_download": (C.c_int32, [vp, vp, P(HostScene)]),
+    "tgsx_model_download_moments": (C.c_int32, [vp, vp, vp, vp]),
+    "tgsx_model_upload_moments": (C.c_int32, [vp, vp, vp, vp]),
+    "tgsx_render": (C.c_int32, [vp, vp, P(Pattern), f32p, C.c_int32, vp, vp, u64p]),
+    "tgsx_backward": (C.c_int32, [vp, vp, P(Pattern), f32p, C.c_int32, vp, C.c_int64, vp,
+                                  C.c_int32]),
+    "tgsx_adam_step": (C.c_int32, [vp, vp, vp, P(AdamArgs)]),
+    "tgsx_fit_step": (C.c_int32, [vp, vp, P(Pattern), f32p, vp, P(AdamArgs), vp]),
+    "tgsx_view_accumulate": (C.c_int32, [vp, vp, P(Pattern), f32p, vp, vp]),
+    "tgsx_step_buffer": (vp, [vp, i64p]),
+    "tgsx_apply_step": (C.c_int32, [vp, vp, C.c_int32, P(AdamArgs)]),
+    "tgsx_densify_config_default": (None, [P(DensifyConfig)]),
+    "tgsx_densify": (C.c_int32, [vp, vp, P(DensifyConfig), C.c_int64, u64p, P(DensifyReport)]),
+    "tgsx_visit_audit": (C.c_int32, [vp, vp]),
+    "tgsx_budget_create": (C.c_int32, [C.c_double, C.c_double, P(vp)]),
+    "tgsx_budget_destroy": (None, [vp]),
+    "tgsx_budget_record_loss": (C.c_int32, [vp, C.c_int64, C.c_double]),
+    "tgsx_budget_update": (None, [vp, C.c_int64]),
+    "tgsx_budget_at": (C.c_int64, [vp, C.c_double]),
+    "tgsx_budget_state": (None, [vp, f64p]),
+    "tgsx_budget_t_norm": (C.c_double, [C.c_int64, C.c_int64, C.c_int64]),
+    "tgsx_fit_power_exponent": (C.c_int32, [f64p, f64p, C.c_int64, f64p]),
+    "tgsx_synthetic_scene": (None, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, P(HostScene)]),
+    "tgsx_pcg32_init": (None, [u64p, C.c_uint64, C.c_uint64]),
+    "tgsx_pcg32_uniform": (C.c_double, [u64p]),
+    "tgsx_pcg32_advance": (None, [u64p, C.c_uint64]),
+    "tgsx_stage_prepare": (C.c_int32, [vp, vp, C.c_int32, vp, vp]),
+    "tgsx_stage_sorted_order": (C.c_int32, [vp, vp, vp]),
+    "tgsx_stage_tile_lists": (C.c_int32, [vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp,
+                                          C.c_int64, i64p]),
+    "tgsx_stage_screen_grads": (C.c_int32, [vp, vp, vp]),
+    "tgsx_stage_counters": (C.c_int32, [vp, u64p, u64p, u64p]),
+    "tgsx_sort_pairs": (C.c_int32, [vp, vp, vp, C.c_int64, C.c_int32]),
+    "tgsx_exclusive_scan": (C.c_int32, [vp, vp, vp, C.c_int64, u64p]),
+}
+
+_LIB = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libtgsx.so and declare every exported signature. Raises if the library is
+    missing: there is deliberately no fallback implementation."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} not built: run `python -m paper_2412_13547_b200.build` (no CPU fallback)")
+    L = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = L
+    return L
+
+
+class TgsxError(Exception):
+    pass
+
+
+def check(rc: int, ctx=None, what: str = ""):
+    if rc == TGSX_OK:
+        return
+    msg = what
+    if ctx:
+        m = load().tgsx_last_error(ctx)
+        if m:
+            msg = m.decode(errors="replace")
+    if rc == TGSX_EINVAL:
+        raise ValueError(msg)       # std::invalid_argument
+    if rc == TGSX_ERUNTIME:
+        raise RuntimeError(msg)     # std::runtime_error
+    raise TgsxError(f"tgsx status {rc}: {msg}")

@@ -1,0 +1,542 @@
+"""Python mirror of the reference's hot-path interface, backed by libtgsx (CUDA, sm_100a).
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/core/include/tgs/*.hpp):
+
+  GaussianModel   model.hpp:45-152 (+ DensifyStats model.hpp:17-40), host SoA numpy arrays
+  DilationPattern dilation.hpp:14-56;  next_offsets dilation.hpp:60-64; lowpass_bump :67-70
+  RenderOptions   rasterizer.hpp:48-53
+  render          rasterizer.hpp:58-60  -> RenderOutput (rasterizer.hpp:21-26)
+  backward        rasterizer.hpp:66-69  -> GradientSet (rasterizer.hpp:28-46), updates stats
+
+plus the device-resident fast path the C ABI adds (DeviceModel, fit_step, batched views,
+densify, BudgetController).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, load
+
+PARAM_ROWS = ("px", "py", "rot", "lsx", "lsy", "rop", "cr", "cg", "cb", "depth")
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _ptr(a, ct=C.c_void_p):
+    if a is None:
+        return None
+    return a.ctypes.data_as(ct) if ct is not C.c_void_p else C.c_void_p(a.ctypes.data)
+
+
+# ---------------------------------------------------------------- pattern
+class DilationPattern:
+    """Strided sampling pattern (dilation.hpp:14-56)."""
+
+    def __init__(self, pattern_size: int, offset_x: int, offset_y: int, width: int, height: int):
+        if pattern_size < 1:
+            raise ValueError("dilation must be >= 1")
+        if offset_x < 0 or offset_y < 0 or offset_x >= pattern_size or offset_y >= pattern_size:
+            raise ValueError("dilation offsets must lie in [0, p)")
+        if width < 1 or height < 1:
+            raise ValueError("image dimensions must be >= 1")
+        self.p, self.ox, self.oy, self.width, self.height = (
+            pattern_size, offset_x, offset_y, width, height)
+        self.cols = (width - offset_x - 1) // pattern_size + 1 if width > offset_x else 0
+        self.rows = (height - offset_y - 1) // pattern_size + 1 if height > offset_y else 0
+
+    def active(self, x, y):
+        return x % self.p == self.ox and y % self.p == self.oy
+
+    def active_count(self) -> int:
+        return self.cols * self.rows
+
+    def rank_of(self, x, y):
+        return ((y - self.oy) // self.p) * self.cols + (x - self.ox) // self.p
+
+    def pixel_at_rank(self, rank):
+        return self.ox + (rank % self.cols) * self.p, self.oy + (rank // self.cols) * self.p
+
+    def pattern_size(self):
+        return self.p
+
+    def active_pixels(self):
+        """(x, y) integer arrays of the active pixels in rank order."""
+        r = np.arange(self.active_count())
+        return self.ox + (r % self.cols) * self.p, self.oy + (r // self.cols) * self.p
+
+    def c(self) -> _lib.Pattern:
+        return _lib.Pattern(self.p, self.ox, self.oy, self.width, self.height)
+
+
+def next_offsets(p: int, iteration: int):
+    """dilation.hpp:60-64"""
+    if p < 1:
+        raise ValueError("dilation must be >= 1")
+    idx = iteration % (p * p)
+    return idx % p, idx // p
+
+
+def lowpass_bump(p: int) -> float:
+    """dilation.hpp:67-70 (float arithmetic)"""
+    return float(np.float32(0.3) + np.float32(0.5) * np.float32(p - 1))
+
+
+@dataclass
+class RenderOptions:
+    threads: int = 1     # accepted for API parity; the GPU path ignores it
+    lowpass_p: int = 0   # 0 => the pattern's p (rasterizer.cpp:138-140)
+
+
+@dataclass
+class RenderOutput:
+    colors: np.ndarray               # (P, 3) by dense rank
+    final_transmittance: np.ndarray  # (P,)
+    blend_op_count: int = 0
+
+
+@dataclass
+class GradientSet:
+    position: np.ndarray    # (n, 2)
+    rotation: np.ndarray    # (n,)
+    log_scales: np.ndarray  # (n, 2)
+    raw_opacity: np.ndarray
+    color: np.ndarray       # (n, 3)
+
+    def size(self):
+        return self.rotation.shape[0]
+
+    @staticmethod
+    def from_rows(g: np.ndarray) -> "GradientSet":
+        return GradientSet(np.stack([g[0], g[1]], 1), g[2].copy(), np.stack([g[3], g[4]], 1),
+                           g[5].copy(), np.stack([g[6], g[7], g[8]], 1))
+
+    def rows(self) -> np.ndarray:
+        return np.stack([self.position[:, 0], self.position[:, 1], self.rotation,
+                         self.log_scales[:, 0], self.log_scales[:, 1], self.raw_opacity,
+                         self.color[:, 0], self.color[:, 1], self.color[:, 2]]).astype(np.float32)
+
+
+# ---------------------------------------------------------------- host model
+class GaussianModel:
+    """Host-side scene container with the reference's fields (model.hpp:45-152), stored as
+    SoA float32 rows in model (creation) order."""
+
+    def __init__(self, n: int = 0):
+        self.params = np.zeros((10, n), np.float32)
+        self.id = np.arange(n, dtype=np.uint64)
+        self.pos_grad_norm_accum = np.zeros(n, np.float32)
+        self.color_grad_norm_accum = np.zeros(n, np.float32)
+        self.accum_count = np.zeros(n, np.int32)
+        self.visit_count = np.zeros(n, np.int64)
+        self.window_visit_count = np.zeros(n, np.int64)
+        self.visit_thresholds = np.full(n, 5.0, np.float64)
+        self._next_id = n
+
+    # reference accessors
+    def size(self):
+        return self.params.shape[1]
+
+    def __len__(self):
+        return self.size()
+
+    def next_id(self):
+        return self._next_id
+
+    def set_next_id(self, v):
+        self._next_id = int(v)
+
+    def row(self, name):
+        return self.params[PARAM_ROWS.index(name)]
+
+    def add(self, position, rotation, log_scales, raw_opacity, color, depth_key,
+            visit_threshold=5.0) -> int:
+        """GaussianModel::add (model.hpp:66-73): appends with the next creation id."""
+        col = np.array([position[0], position[1], rotation, log_scales[0], log_scales[1],
+                        raw_opacity, color[0], color[1], color[2], depth_key], np.float32)[:, None]
+        self.params = np.concatenate([self.params, col], 1)
+        gid = self._next_id
+        self._next_id += 1
+        self.id = np.append(self.id, np.uint64(gid))
+        self.pos_grad_norm_accum = np.append(self.pos_grad_norm_accum, np.float32(0))
+        self.color_grad_norm_accum = np.append(self.color_grad_norm_accum, np.float32(0))
+        self.accum_count = np.append(self.accum_count, np.int32(0))
+        self.visit_count = np.append(self.visit_count, np.int64(0))
+        self.window_visit_count = np.append(self.window_visit_count, np.int64(0))
+        self.visit_thresholds = np.append(self.visit_thresholds, visit_threshold)
+        return gid
+
+    def compact(self, keep) -> int:
+        """GaussianModel::compact (model.hpp:77-103)."""
+        keep = np.asarray(keep, bool)
+        if keep.shape[0] != self.size():
+            raise ValueError("keep mask size mismatch")
+        removed = int((~keep).sum())
+        self.params = np.ascontiguousarray(self.params[:, keep])
+        for f in ("id", "pos_grad_norm_accum", "color_grad_norm_accum", "accum_count",
+                  "visit_count", "window_visit_count", "visit_thresholds"):
+            setattr(self, f, np.ascontiguousarray(getattr(self, f)[keep]))
+        return removed
+
+    @staticmethod
+    def synthetic(seed: int, n: int, width: int, height: int) -> "GaussianModel":
+        """Seeded synthetic scene generated by libtgsx's host generator."""
+        m = GaussianModel(n)
+        hs = m._host_scene()
+        load().tgsx_synthetic_scene(seed, n, width, height, C.byref(hs))
+        m._next_id = n
+        return m
+
+    def _host_scene(self) -> _lib.HostScene:
+        self.params = np.ascontiguousarray(self.params, np.float32)
+        hs = _lib.HostScene()
+        hs.n = self.size()
+        for i, f in enumerate(PARAM_ROWS):
+            setattr(hs, f, self.params[i].ctypes.data_as(_lib.f32p))
+        self.id = np.ascontiguousarray(self.id, np.uint64)
+        hs.id = self.id.ctypes.data_as(_lib.u64p)
+        hs.next_id = self._next_id
+        for f, attr, ct in (("pos_acc", "pos_grad_norm_accum", _lib.f32p),
+                            ("col_acc", "color_grad_norm_accum", _lib.f32p),
+                            ("accum", "accum_count", _lib.i32p),
+                            ("visit", "visit_count", _lib.i64p),
+                            ("window", "window_visit_count", _lib.i64p),
+                            ("tau_v", "visit_thresholds", _lib.f64p)):
+            a = np.ascontiguousarray(getattr(self, attr))
+            setattr(self, attr, a)
+            setattr(hs, f, a.ctypes.data_as(ct))
+        return hs
+
+    def copy(self) -> "GaussianModel":
+        m = GaussianModel(0)
+        for k, v in self.__dict__.items():
+            setattr(m, k, v.copy() if isinstance(v, np.ndarray) else v)
+        return m
+
+
+# ---------------------------------------------------------------- device objects
+class Context:
+    """A tgsx context: one CUDA stream + reusable workspace (one per host thread)."""
+
+    def __init__(self, device: int = 0):
+        self.L = load()
+        h = C.c_void_p()
+        rc = self.L.tgsx_create(device, C.byref(h))
+        if rc:
+            raise _lib.TgsxError(f"tgsx_create failed ({rc}): no usable CUDA device")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.L.tgsx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc, what=""):
+        check(rc, self.h, what)
+
+    def synchronize(self):
+        self.check(self.L.tgsx_synchronize(self.h))
+
+    def set_stream(self, stream_handle: int):
+        self.check(self.L.tgsx_set_stream(self.h, C.c_void_p(stream_handle)))
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.tgsx_launch_count(self.h))
+
+    STAGES = ("depth_sort", "preprocess", "scan", "duplicate", "radix_sort", "ranges",
+              "blend_forward", "blend_backward", "chain_adam", "loss", "densify")
+
+    def profile(self, enable: bool = True):
+        self.check(self.L.tgsx_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        n = len(self.STAGES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_int64 * n)()
+        self.check(self.L.tgsx_profile_read(self.h, ms, cnt, n))
+        return {s: (ms[i], cnt[i]) for i, s in enumerate(self.STAGES)}
+
+    def counters(self):
+        ops, ev, pairs = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.check(self.L.tgsx_stage_counters(self.h, C.byref(ops), C.byref(ev), C.byref(pairs)))
+        return {"blend_ops": ops.value, "evals": ev.value, "pairs": pairs.value}
+
+
+_DEFAULT_CTX = None
+
+
+def default_context() -> Context:
+    global _DEFAULT_CTX
+    if _DEFAULT_CTX is None:
+        _DEFAULT_CTX = Context(0)
+    return _DEFAULT_CTX
+
+
+class DeviceModel:
+    """Device-resident SoA model (params, ids, stats, tau_v, Adam moments) in HBM."""
+
+    def __init__(self, ctx: Context | None = None, capacity: int = 1):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        self.ctx.check(self.ctx.L.tgsx_model_create(self.ctx.h, max(capacity, 1), C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def from_host(model: GaussianModel, ctx: Context | None = None) -> "DeviceModel":
+        dm = DeviceModel(ctx, model.size())
+        dm.upload(model)
+        return dm
+
+    def upload(self, model: GaussianModel):
+        hs = model._host_scene()
+        self.ctx.check(self.ctx.L.tgsx_model_upload(self.ctx.h, self.h, C.byref(hs)))
+
+    def download(self, into: GaussianModel | None = None) -> GaussianModel:
+        n = self.size()
+        m = into if (into is not None and into.size() == n) else GaussianModel(n)
+        hs = m._host_scene()
+        self.ctx.check(self.ctx.L.tgsx_model_download(self.ctx.h, self.h, C.byref(hs)))
+        m._next_id = int(hs.next_id)
+        return m
+
+    def moments(self):
+        n = self.size()
+        m1 = np.zeros((9, n), np.float32)
+        m2 = np.zeros((9, n), np.float32)
+        self.ctx.check(self.ctx.L.tgsx_model_download_moments(self.ctx.h, self.h, _ptr(m1), _ptr(m2)))
+        return m1, m2
+
+    def set_moments(self, m1, m2):
+        m1 = _f32(m1)
+        m2 = _f32(m2)
+        self.ctx.check(self.ctx.L.tgsx_model_upload_moments(self.ctx.h, self.h, _ptr(m1), _ptr(m2)))
+
+    def size(self) -> int:
+        return int(self.ctx.L.tgsx_model_size(self.h))
+
+    def next_id(self) -> int:
+        return int(self.ctx.L.tgsx_model_next_id(self.h))
+
+    def close(self):
+        if self.h:
+            self.ctx.L.tgsx_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------ ops
+    def render(self, pattern: DilationPattern, background=(0.0, 0.0, 0.0),
+               opts: RenderOptions | None = None) -> RenderOutput:
+        opts = opts or RenderOptions()
+        P = pattern.active_count()
+        rgb = np.zeros((P, 3), np.float32)
+        T = np.zeros(P, np.float32)
+        ops = C.c_uint64()
+        bg = (C.c_float * 3)(*background)
+        self.ctx.check(self.ctx.L.tgsx_render(self.ctx.h, self.h, C.byref(pattern.c()), bg,
+                                              opts.lowpass_p, _ptr(rgb), _ptr(T), C.byref(ops)))
+        return RenderOutput(rgb, T, ops.value)
+
+    def backward(self, pattern: DilationPattern, background, pixel_loss_grads,
+                 opts: RenderOptions | None = None, update_stats=True) -> GradientSet:
+        opts = opts or RenderOptions()
+        g = _f32(pixel_loss_grads).reshape(-1, 3)
+        out = np.zeros((9, self.size()), np.float32)
+        bg = (C.c_float * 3)(*background)
+        self.ctx.check(self.ctx.L.tgsx_backward(self.ctx.h, self.h, C.byref(pattern.c()), bg,
+                                                opts.lowpass_p, _ptr(g), g.shape[0], _ptr(out),
+                                                1 if update_stats else 0))
+        return GradientSet.from_rows(out)
+
+    def screen_grads(self) -> np.ndarray:
+        out = np.zeros((10, self.size()), np.float32)
+        self.ctx.check(self.ctx.L.tgsx_stage_screen_grads(self.ctx.h, self.h, _ptr(out)))
+        return out
+
+    def adam_step(self, grads, step: int, total_steps: int, image_diagonal: float):
+        g = _f32(grads.rows() if isinstance(grads, GradientSet) else grads)
+        a = _lib.AdamArgs(step, total_steps, image_diagonal)
+        self.ctx.check(self.ctx.L.tgsx_adam_step(self.ctx.h, self.h, _ptr(g), C.byref(a)))
+
+    def fit_step(self, pattern: DilationPattern, background, target, step: int,
+                 total_steps: int, image_diagonal: float, loss_out=None) -> float:
+        """render -> L1 -> backward -> stats -> Adam, fused. `target` is a (H, W, 3) float32
+        array (host) or a device pointer (int)."""
+        a = _lib.AdamArgs(step, total_steps, image_diagonal)
+        bg = (C.c_float * 3)(*background)
+        tp = C.c_void_p(target) if isinstance(target, int) else _ptr(_f32(target))
+        loss = np.zeros(1, np.float32)
+        self.ctx.check(self.ctx.L.tgsx_fit_step(self.ctx.h, self.h, C.byref(pattern.c()), bg, tp,
+                                                C.byref(a), _ptr(loss)))
+        return float(loss[0])
+
+    def view_accumulate(self, pattern: DilationPattern, background, target) -> float:
+        bg = (C.c_float * 3)(*background)
+        tp = C.c_void_p(target) if isinstance(target, int) else _ptr(_f32(target))
+        loss = np.zeros(1, np.float32)
+        self.ctx.check(self.ctx.L.tgsx_view_accumulate(self.ctx.h, self.h, C.byref(pattern.c()),
+                                                       bg, tp, _ptr(loss)))
+        return float(loss[0])
+
+    def step_buffer(self):
+        """(device pointer, float count) of the [12][cap] batched step buffer."""
+        n = C.c_int64()
+        p = self.ctx.L.tgsx_step_buffer(self.h, C.byref(n))
+        return int(p), int(n.value)
+
+    def apply_step(self, batch_views: int, step: int, total_steps: int, image_diagonal: float):
+        a = _lib.AdamArgs(step, total_steps, image_diagonal)
+        self.ctx.check(self.ctx.L.tgsx_apply_step(self.ctx.h, self.h, batch_views, C.byref(a)))
+
+    def densify(self, budget: int, rng_state: np.ndarray, config: _lib.DensifyConfig | None = None):
+        cfg = config or densify_config()
+        rep = _lib.DensifyReport()
+        st = np.ascontiguousarray(rng_state, np.uint64)
+        self.ctx.check(self.ctx.L.tgsx_densify(self.ctx.h, self.h, C.byref(cfg), budget,
+                                               st.ctypes.data_as(_lib.u64p), C.byref(rep)))
+        rng_state[:] = st
+        return rep
+
+    def visit_audit(self):
+        self.ctx.check(self.ctx.L.tgsx_visit_audit(self.ctx.h, self.h))
+
+    # ------------------------------------------------ stage access (parity tests)
+    def stage_prepare(self, lowpass_p: int):
+        n = self.size()
+        out = np.zeros((11, n), np.float32)
+        orig = np.zeros(n, np.uint32)
+        self.ctx.check(self.ctx.L.tgsx_stage_prepare(self.ctx.h, self.h, lowpass_p, _ptr(out), _ptr(orig)))
+        return out, orig
+
+    def stage_sorted_order(self):
+        perm = np.zeros(self.size(), np.uint32)
+        self.ctx.check(self.ctx.L.tgsx_stage_sorted_order(self.ctx.h, self.h, _ptr(perm)))
+        return perm
+
+    def stage_tile_lists(self, lowpass_p: int, width: int, height: int):
+        tiles = ((width + 15) // 16) * ((height + 15) // 16)
+        offsets = np.zeros(tiles + 1, np.uint32)
+        k = C.c_int64()
+        self.ctx.check(self.ctx.L.tgsx_stage_tile_lists(self.ctx.h, self.h, lowpass_p, width, height,
+                                                        _ptr(offsets), None, 0, C.byref(k)))
+        items = np.zeros(max(k.value, 1), np.uint32)
+        self.ctx.check(self.ctx.L.tgsx_stage_tile_lists(self.ctx.h, self.h, lowpass_p, width, height,
+                                                        _ptr(offsets), _ptr(items), k.value, C.byref(k)))
+        return offsets, items[:k.value]
+
+
+# ---------------------------------------------------------------- reference-shaped free functions
+def render(model, pattern: DilationPattern, background=(0.0, 0.0, 0.0),
+           opts: RenderOptions | None = None, ctx: Context | None = None) -> RenderOutput:
+    """tgs::render<float> (rasterizer.hpp:58-60). `model` is a GaussianModel (uploaded for the
+    call, like the reference's by-reference host model) or a DeviceModel."""
+    if isinstance(model, DeviceModel):
+        return model.render(pattern, background, opts)
+    dm = DeviceModel.from_host(model, ctx)
+    try:
+        return dm.render(pattern, background, opts)
+    finally:
+        dm.close()
+
+
+def backward(model, pattern: DilationPattern, background, pixel_loss_grads,
+             opts: RenderOptions | None = None, ctx: Context | None = None) -> GradientSet:
+    """tgs::backward<float> (rasterizer.hpp:66-69); updates model's DensifyStats in place."""
+    if isinstance(model, DeviceModel):
+        return model.backward(pattern, background, pixel_loss_grads, opts)
+    g = np.asarray(pixel_loss_grads, np.float32).reshape(-1, 3)
+    if g.shape[0] != pattern.active_count():
+        raise ValueError("backward: loss-gradient count does not match pattern ranks")
+    dm = DeviceModel.from_host(model, ctx)
+    try:
+        gs = dm.backward(pattern, background, g, opts)
+        dm.download(into=model)
+        return gs
+    finally:
+        dm.close()
+
+
+def densify_config(**kw) -> _lib.DensifyConfig:
+    c = _lib.DensifyConfig()
+    load().tgsx_densify_config_default(C.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+class BudgetController:
+    """BudgetController, host C++ in libtgsx."""
+
+    def __init__(self, n_init: float, m_final: float):
+        self.L = load()
+        h = C.c_void_p()
+        check(self.L.tgsx_budget_create(n_init, m_final, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            self.L.tgsx_budget_destroy(self.h)
+        except Exception:
+            pass
+
+    def record_loss(self, t: int, loss: float):
+        if self.L.tgsx_budget_record_loss(self.h, t, loss):
+            raise ValueError("record_loss: loss must be > 0")
+
+    def update(self, t: int):
+        self.L.tgsx_budget_update(self.h, t)
+
+    def budget_at(self, t_norm: float) -> int:
+        return int(self.L.tgsx_budget_at(self.h, t_norm))
+
+    def state(self):
+        out = (C.c_double * 5)()
+        self.L.tgsx_budget_state(self.h, out)
+        return {"alpha": out[0], "alpha_base": out[1], "m_adaptive": out[2], "ema": out[3],
+                "fits": int(out[4])}
+
+
+def budget_t_norm(step, warmup, densify_end) -> float:
+    return float(load().tgsx_budget_t_norm(step, warmup, densify_end))
+
+
+def fit_power_exponent(t, y) -> float:
+    t = np.ascontiguousarray(t, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    out = C.c_double()
+    rc = load().tgsx_fit_power_exponent(t.ctypes.data_as(_lib.f64p), y.ctypes.data_as(_lib.f64p),
+                                        len(t), C.byref(out))
+    if rc:
+        raise ValueError("fit_power_exponent: insufficient data")
+    return out.value
+
+
+class Pcg32:
+    """PCG32 (rng.hpp:10-46) state as used by tgsx_densify."""
+
+    def __init__(self, seed=0x853C49E6748FEA9B, stream=1):
+        self.state = np.zeros(2, np.uint64)
+        load().tgsx_pcg32_init(self.state.ctypes.data_as(_lib.u64p), seed, stream)
+
+    def uniform(self) -> float:
+        return float(load().tgsx_pcg32_uniform(self.state.ctypes.data_as(_lib.u64p)))
+
+    def advance(self, delta: int):
+        load().tgsx_pcg32_advance(self.state.ctypes.data_as(_lib.u64p), delta)

@@ -1,0 +1,791 @@
+// libtgsx C ABI (include/tgsx.h): contexts, device-resident models, and the host-side
+// orchestration of the fit hot path. The product path is CUDA only: there is no CPU fallback —
+// every entry point fails with TGSX_ECUDA if the device work cannot run.
+#include "tgsx_device.cuh"
+#include "tgsx_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace tgsx {
+
+cudaError_t DevBuf::ensure(size_t need) {
+    if (need <= bytes && p) return cudaSuccess;
+    release();
+    size_t nb = std::max<size_t>(need, 256);
+    nb = nb + nb / 4;  // headroom: K and P drift between iterations
+    cudaError_t e = cudaMalloc(&p, nb);
+    if (e) {
+        p = nullptr;
+        bytes = 0;
+        return e;
+    }
+    bytes = nb;
+    return cudaSuccess;
+}
+
+cudaError_t DevBuf::grow_keep(size_t need, size_t keep_bytes, cudaStream_t s) {
+    if (need <= bytes && p) return cudaSuccess;
+    void* np = nullptr;
+    const size_t nb = std::max<size_t>(need, 256);
+    cudaError_t e = cudaMalloc(&np, nb);
+    if (e) return e;
+    if (p && keep_bytes) {
+        e = cudaMemcpyAsync(np, p, std::min(keep_bytes, bytes), cudaMemcpyDeviceToDevice, s);
+        if (e) return e;
+        cudaStreamSynchronize(s);
+    }
+    release();
+    p = np;
+    bytes = nb;
+    return cudaSuccess;
+}
+
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+cudaEvent_t Profiler::get() {
+    if (next >= pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        pool.push_back(e);
+    }
+    return pool[next++];
+}
+
+void Profiler::begin(int stage, cudaStream_t s, cudaEvent_t* out) {
+    (void)stage;
+    *out = get();
+    cudaEventRecord(*out, s);
+}
+
+void Profiler::end(int stage, cudaStream_t s, cudaEvent_t start) {
+    cudaEvent_t e = get();
+    cudaEventRecord(e, s);
+    pending.push_back({stage, {start, e}});
+}
+
+void Profiler::harvest() {
+    for (auto& p : pending) {
+        float ms_ = 0.f;
+        if (cudaEventElapsedTime(&ms_, p.second.first, p.second.second) == cudaSuccess) {
+            ms[p.first] += ms_;
+            count[p.first] += 1;
+        } else {
+            cudaGetLastError();
+        }
+    }
+    pending.clear();
+    next = 0;
+}
+
+}  // namespace tgsx
+
+using namespace tgsx;
+
+namespace {
+
+int32_t fail(tgsx_ctx* ctx, int32_t code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int32_t cuda_fail(tgsx_ctx* ctx, cudaError_t e, const char* where) {
+    return fail(ctx, TGSX_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                              \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr); \
+    } while (0)
+
+constexpr int kParamRows = 10;  // px py rot lsx lsy rop cr cg cb depth
+
+int32_t check_pattern(tgsx_ctx* ctx, const tgsx_pattern* pat) {
+    // DilationPattern constructor checks (dilation.hpp:18-22)
+    if (!pat) return fail(ctx, TGSX_EINVAL, "pattern is null");
+    if (pat->p < 1) return fail(ctx, TGSX_EINVAL, "dilation must be >= 1");
+    if (pat->ox < 0 || pat->oy < 0 || pat->ox >= pat->p || pat->oy >= pat->p)
+        return fail(ctx, TGSX_EINVAL, "dilation offsets must lie in [0, p)");
+    if (pat->width < 1 || pat->height < 1)
+        return fail(ctx, TGSX_EINVAL, "image dimensions must be >= 1");
+    return TGSX_OK;
+}
+
+RenderArgs make_args(const tgsx_pattern* pat, const float bg[3], int lowpass_p) {
+    RenderArgs ra{};
+    ra.p = pat->p;
+    ra.ox = pat->ox;
+    ra.oy = pat->oy;
+    ra.W = pat->width;
+    ra.H = pat->height;
+    ra.cols = pat->width > pat->ox ? (pat->width - pat->ox - 1) / pat->p + 1 : 0;
+    ra.rows = pat->height > pat->oy ? (pat->height - pat->oy - 1) / pat->p + 1 : 0;
+    ra.P = ra.cols * ra.rows;
+    ra.bg[0] = bg ? bg[0] : 0.f;
+    ra.bg[1] = bg ? bg[1] : 0.f;
+    ra.bg[2] = bg ? bg[2] : 0.f;
+    ra.lowpass_p = lowpass_p > 0 ? lowpass_p : pat->p;  // resolve_lowpass rasterizer.cpp:138
+    return ra;
+}
+
+// ---------------------------------------------------------------- model storage
+cudaError_t model_reserve(tgsx_ctx* ctx, tgsx_model* m, int64_t cap) {
+    if (cap <= m->cap) return cudaSuccess;
+    cap = std::max<int64_t>(cap, 1);
+    const int64_t n = m->n, oc = m->cap;
+    cudaStream_t s = ctx->stream;
+    auto regrow_rows = [&](DevBuf& b, int rows, size_t elt) -> cudaError_t {
+        void* np = nullptr;
+        cudaError_t e = cudaMalloc(&np, (size_t)rows * cap * elt);
+        if (e) return e;
+        if ((e = cudaMemsetAsync(np, 0, (size_t)rows * cap * elt, s))) return e;
+        if (b.p && n > 0) {
+            e = cudaMemcpy2DAsync(np, cap * elt, b.p, oc * elt, n * elt, rows, cudaMemcpyDeviceToDevice, s);
+            if (e) return e;
+        }
+        cudaStreamSynchronize(s);
+        b.release();
+        b.p = np;
+        b.bytes = (size_t)rows * cap * elt;
+        return cudaSuccess;
+    };
+    cudaError_t e;
+    if ((e = regrow_rows(m->params, kParamRows, 4))) return e;
+    if ((e = regrow_rows(m->ids, 1, 8))) return e;
+    if ((e = regrow_rows(m->pos_acc, 1, 4))) return e;
+    if ((e = regrow_rows(m->col_acc, 1, 4))) return e;
+    if ((e = regrow_rows(m->accum, 1, 4))) return e;
+    if ((e = regrow_rows(m->visit, 1, 8))) return e;
+    if ((e = regrow_rows(m->window, 1, 8))) return e;
+    if ((e = regrow_rows(m->tau_v, 1, 8))) return e;
+    if ((e = regrow_rows(m->m1, 9, 4))) return e;
+    if ((e = regrow_rows(m->m2, 9, 4))) return e;
+    if ((e = regrow_rows(m->step, kStepFloats, 4))) return e;
+    if ((e = regrow_rows(m->screen, 10, 4))) return e;
+    if ((e = regrow_rows(m->perm, 1, 4))) return e;
+    if ((e = regrow_rows(m->rank_of, 1, 4))) return e;
+    m->cap = cap;
+    return cudaSuccess;
+}
+
+// ---------------------------------------------------------------- error word
+int32_t check_kernel_error(tgsx_ctx* ctx, unsigned long long err) {
+    if (err == kErrNone) return TGSX_OK;
+    const uint32_t code = (uint32_t)(err & 3u);
+    const unsigned long long rank = err >> 2;
+    if (code == 1)
+        return fail(ctx, TGSX_EINVAL,
+                    "covariance_from_params: non-finite input (blend rank " + std::to_string(rank) + ")");
+    return fail(ctx, TGSX_ERUNTIME,
+                "covariance numerically degenerate (det <= 0) (blend rank " + std::to_string(rank) + ")");
+}
+
+cudaError_t reset_counters(tgsx_ctx* ctx) {
+    Workspace& ws = ctx->ws;
+    cudaError_t e = ws.counters.ensure(8 * sizeof(unsigned long long));
+    if (e) return e;
+    if ((e = cudaMemsetAsync(ws.counters.p, 0, 8 * sizeof(unsigned long long), ctx->stream))) return e;
+    return cudaMemsetAsync(ws.counters.p, 0xff, sizeof(unsigned long long), ctx->stream);
+}
+
+// Sort (if dirty) -> preprocess -> scan -> [sync for K] -> duplicate -> onesweep -> ranges.
+// On return ws.K, ws.ranges and `items` (sorted ranks) describe the per-tile lists.
+int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t** items,
+            uint32_t** sorted_keys) {
+    Workspace& ws = ctx->ws;
+    ws.have_forward = false;
+    CK(reset_counters(ctx));
+    if (m->order_dirty) {
+        StageTimer t(ctx, kStDepthSort);
+        CK(launch_sort_depth(ctx, m));
+    }
+    {
+        StageTimer t(ctx, kStPreprocess);
+        CK(launch_preprocess(ctx, m, lowpass_p, W, H));
+    }
+    unsigned long long* counters = ws.counters.as<unsigned long long>();
+    uint32_t* d_total = reinterpret_cast<uint32_t*>(counters + 3);
+    {
+        StageTimer t(ctx, kStScan);
+        CK(launch_exclusive_scan(ctx, ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(), m->n, d_total));
+    }
+    CK(cudaMemcpyAsync(ws.h_scratch, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->prof.enabled) ctx->prof.harvest();  // every event recorded so far has completed
+    int32_t rc = check_kernel_error(ctx, ws.h_scratch[0]);
+    if (rc) return rc;
+    const int64_t K = (int64_t)(uint32_t)(ws.h_scratch[3] & 0xffffffffull);
+    ws.K = K;
+    const int tiles = ws.tiles_x * ws.tiles_y;
+    const int key_bits = key_bits_for(tiles);
+    const int passes = (key_bits + 7) / 8;
+    for (int i = 0; i < 2; ++i) {
+        CK(ws.keys[i].ensure(std::max<int64_t>(K, 1) * 4));
+        CK(ws.vals[i].ensure(std::max<int64_t>(K, 1) * 4));
+    }
+    CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 48));
+    const int64_t sblocks = (K + 4095) / 4096;
+    CK(ws.sort_tmp.ensure(4 * 256 * 4 + 64 + (size_t)std::max(passes, 1) * sblocks * 256 * 4));
+    {
+        StageTimer t(ctx, kStDuplicate);
+        CK(launch_duplicate(ctx, m, W, H, key_bits));
+    }
+    uint32_t* k = ws.keys[0].as<uint32_t>();
+    uint32_t* v = ws.vals[0].as<uint32_t>();
+    {
+        StageTimer t(ctx, kStSort);
+        CK(sort_pairs(ctx, k, v, ws.keys[1].as<uint32_t>(), ws.vals[1].as<uint32_t>(), K, key_bits,
+                      ws.sort_tmp.as<uint32_t>()));
+    }
+    {
+        StageTimer t(ctx, kStRanges);
+        CK(launch_ranges(ctx, k, K, tiles));
+    }
+    *items = v;
+    if (sorted_keys) *sorted_keys = k;
+    return TGSX_OK;
+}
+
+cudaError_t ensure_pixels(tgsx_ctx* ctx, const RenderArgs& ra) {
+    Workspace& ws = ctx->ws;
+    const size_t P = (size_t)std::max(ra.P, 1);
+    cudaError_t e;
+    if ((e = ws.rgb.ensure(P * 12))) return e;
+    if ((e = ws.T.ensure(P * 4))) return e;
+    if ((e = ws.last.ensure(P * 4))) return e;
+    if ((e = ws.dLdC.ensure(P * 12))) return e;
+    const int tiles = ws.tiles_x * ws.tiles_y;
+    if ((e = ws.block_loss.ensure((size_t)std::max(tiles, 1) * 4))) return e;
+    return cudaSuccess;
+}
+
+void fill_adam(AdamCfg& c, const tgsx_adam_args* a) {
+    c.b1 = 0.9f;
+    c.b2 = 0.999f;
+    c.omb1 = 1.0f - c.b1;
+    c.omb2 = 1.0f - c.b2;
+    c.eps = 1e-15f;
+    const double frac = a->total_steps > 0 ? (double)a->step / (double)a->total_steps : 0.0;
+    const float lr_pos = (float)(1.6e-4 * a->image_diagonal * std::pow(0.01, frac));
+    c.lr[0] = c.lr[1] = lr_pos;
+    c.lr[2] = 1e-3f;
+    c.lr[3] = c.lr[4] = 5e-3f;
+    c.lr[5] = 5e-2f;
+    c.lr[6] = c.lr[7] = c.lr[8] = 2.5e-3f;
+    c.bc1 = (float)(1.0 - std::pow(0.9, (double)a->step));
+    c.bc2 = (float)(1.0 - std::pow(0.999, (double)a->step));
+    // clamp_parameters (gaussian.hpp:105-116) bounds, CR logf
+    c.ls_lo = (float)std::log((double)(float)kMinScale);
+    c.ls_hi = (float)std::log((double)(float)a->image_diagonal);
+    c.raw_cap = (float)kRawCap;
+    c.batch = 1.0f;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Host or device source into a device buffer (H2D copy inside the call for host memory).
+int32_t stage_input(tgsx_ctx* ctx, DevBuf& dst, const float* src, size_t bytes, const float** out) {
+    if (is_device_ptr(src)) {
+        *out = src;
+        return TGSX_OK;
+    }
+    CK(dst.ensure(bytes));
+    CK(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyDefault, ctx->stream));
+    *out = dst.as<float>();
+    return TGSX_OK;
+}
+
+int32_t render_core(tgsx_ctx* ctx, tgsx_model* m, const RenderArgs& ra, bool fused_loss,
+                    uint32_t** items_out) {
+    uint32_t* items = nullptr;
+    int32_t rc = bin(ctx, m, ra.lowpass_p, ra.W, ra.H, &items, nullptr);
+    if (rc) return rc;
+    CK(ensure_pixels(ctx, ra));
+    {
+        StageTimer t(ctx, kStForward);
+        CK(launch_forward(ctx, ra, items, fused_loss));
+    }
+    ctx->ws.have_forward = true;
+    ctx->ws.last_P = ra.P;
+    *items_out = items;
+    return TGSX_OK;
+}
+
+__global__ void sum_block_loss(const float* __restrict__ bl, int n, float* out) {
+    // fixed-order reduction: deterministic loss value
+    __shared__ double s[256];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) acc += (double)bl[i];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = (float)s[0];
+}
+
+__global__ void scale_loss(float* v, float scale) { v[0] *= scale; }
+
+int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
+                   const float* target, float* out_loss, ChainMode mode, const AdamCfg* cfg) {
+    int32_t rc = check_pattern(ctx, pat);
+    if (rc) return rc;
+    if (!target) return fail(ctx, TGSX_EINVAL, "target is null");
+    RenderArgs ra = make_args(pat, bg, 0);
+    Workspace& ws = ctx->ws;
+    rc = stage_input(ctx, ws.target, target, (size_t)ra.W * ra.H * 12, &ra.target);
+    if (rc) return rc;
+    uint32_t* items = nullptr;
+    rc = render_core(ctx, m, ra, true, &items);
+    if (rc) return rc;
+    {
+        StageTimer t(ctx, kStBackward);
+        CK(launch_backward(ctx, ra, items));
+    }
+    {
+        StageTimer t(ctx, kStChain);
+        CK(launch_chain(ctx, m, mode, true, nullptr, reinterpret_cast<const float*>(cfg)));
+    }
+    const int tiles = ws.tiles_x * ws.tiles_y;
+    float* dloss = reinterpret_cast<float*>(ws.counters.as<unsigned long long>() + 4);
+    {
+        StageTimer t(ctx, kStLoss);
+        sum_block_loss<<<1, 256, 0, ctx->stream>>>(ws.block_loss.as<float>(), tiles, dloss);
+        scale_loss<<<1, 1, 0, ctx->stream>>>(dloss, ra.P > 0 ? (float)(1.0 / (3.0 * ra.P)) : 0.f);
+        ctx->launches += 2;
+    }
+    CK(cudaGetLastError());
+    if (out_loss) {
+        CK(cudaMemcpyAsync(out_loss, dloss, 4, cudaMemcpyDefault, ctx->stream));
+        if (!is_device_ptr(out_loss)) CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return TGSX_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+int32_t tgsx_create(int32_t device, tgsx_ctx** out) {
+    if (!out) return TGSX_EINVAL;
+    *out = nullptr;
+    tgsx_ctx* ctx = new tgsx_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (!e) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+    if (!e) e = cudaMallocHost(&ctx->ws.h_scratch, 64 * sizeof(uint64_t));
+    if (!e) e = ctx->ws.counters.ensure(8 * sizeof(unsigned long long));
+    if (e) {
+        delete ctx;
+        return TGSX_ECUDA;
+    }
+    ctx->stream = ctx->own_stream;
+    *out = ctx;
+    return TGSX_OK;
+}
+
+void tgsx_destroy(tgsx_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    Workspace& ws = ctx->ws;
+    DevBuf* bufs[] = {&ws.prep, &ws.touched, &ws.pair_off, &ws.scan_tmp, &ws.keys[0], &ws.keys[1],
+                      &ws.vals[0], &ws.vals[1], &ws.sort_tmp, &ws.ranges, &ws.partial, &ws.rgb,
+                      &ws.T, &ws.last, &ws.dLdC, &ws.target, &ws.block_loss, &ws.counters,
+                      &ws.generic};
+    for (DevBuf* b : bufs) b->release();
+    if (ws.h_scratch) cudaFreeHost(ws.h_scratch);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+int32_t tgsx_set_stream(tgsx_ctx* ctx, void* stream) {
+    if (!ctx) return TGSX_EINVAL;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return TGSX_OK;
+}
+
+void* tgsx_get_stream(tgsx_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+const char* tgsx_last_error(const tgsx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int32_t tgsx_synchronize(tgsx_ctx* ctx) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+uint64_t tgsx_launch_count(const tgsx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int32_t tgsx_profile(tgsx_ctx* ctx, int32_t enable) {
+    if (!ctx) return TGSX_EINVAL;
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->prof.harvest();
+    for (int i = 0; i < kNumStages; ++i) {
+        ctx->prof.ms[i] = 0;
+        ctx->prof.count[i] = 0;
+    }
+    ctx->prof.enabled = enable != 0;
+    return TGSX_OK;
+}
+
+int32_t tgsx_profile_read(tgsx_ctx* ctx, double* ms, int64_t* counts, int32_t n) {
+    if (!ctx) return TGSX_EINVAL;
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->prof.harvest();
+    for (int i = 0; i < n && i < kNumStages; ++i) {
+        if (ms) ms[i] = ctx->prof.ms[i];
+        if (counts) counts[i] = ctx->prof.count[i];
+    }
+    return TGSX_OK;
+}
+
+// ---------------------------------------------------------------- model
+int32_t tgsx_model_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model** out) {
+    if (!ctx || !out) return TGSX_EINVAL;
+    tgsx_model* m = new tgsx_model();
+    cudaError_t e = model_reserve(ctx, m, std::max<int64_t>(capacity, 1));
+    if (e) {
+        delete m;
+        return cuda_fail(ctx, e, "tgsx_model_create");
+    }
+    *out = m;
+    return TGSX_OK;
+}
+
+void tgsx_model_destroy(tgsx_model* m) {
+    if (!m) return;
+    DevBuf* bufs[] = {&m->params, &m->ids, &m->pos_acc, &m->col_acc, &m->accum, &m->visit,
+                      &m->window, &m->tau_v, &m->m1, &m->m2, &m->step, &m->perm, &m->rank_of,
+                      &m->screen};
+    for (DevBuf* b : bufs) b->release();
+    delete m;
+}
+
+int64_t tgsx_model_size(const tgsx_model* m) { return m ? m->n : 0; }
+uint64_t tgsx_model_next_id(const tgsx_model* m) { return m ? m->next_id : 0; }
+
+int32_t tgsx_model_upload(tgsx_ctx* ctx, tgsx_model* m, const tgsx_host_scene* h) {
+    if (!ctx || !m || !h || h->n < 0) return fail(ctx, TGSX_EINVAL, "bad upload arguments");
+    const int64_t n = h->n;
+    CK(model_reserve(ctx, m, n));
+    m->n = n;
+    cudaStream_t s = ctx->stream;
+    const int64_t cap = m->cap;
+    float* P = m->params.as<float>();
+    const float* rows[kParamRows] = {h->px, h->py, h->rot, h->lsx, h->lsy, h->rop, h->cr, h->cg, h->cb, h->depth};
+    for (int q = 0; q < kParamRows; ++q) {
+        if (!rows[q] && n) return fail(ctx, TGSX_EINVAL, "null parameter array");
+        if (n) CK(cudaMemcpyAsync(P + q * cap, rows[q], n * 4, cudaMemcpyDefault, s));
+    }
+    std::vector<uint64_t> ids;
+    const uint64_t* idp = h->id;
+    if (!idp) {
+        ids.resize(n);
+        for (int64_t i = 0; i < n; ++i) ids[i] = (uint64_t)i;
+        idp = ids.data();
+    }
+    bool mono = true;
+    uint64_t mx = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (i && idp[i] <= idp[i - 1]) mono = false;
+        mx = std::max(mx, idp[i]);
+    }
+    m->ids_monotone = mono;
+    m->next_id = h->id ? std::max<uint64_t>(h->next_id, n ? mx + 1 : 0) : (uint64_t)n;
+    if (n) CK(cudaMemcpyAsync(m->ids.p, idp, n * 8, cudaMemcpyHostToDevice, s));
+    // stats (zeros when absent), tau_v (5.0 when absent)
+    auto up_or_zero = [&](DevBuf& b, const void* src, size_t elt) -> cudaError_t {
+        if (!n) return cudaSuccess;
+        if (src) return cudaMemcpyAsync(b.p, src, n * elt, cudaMemcpyDefault, s);
+        return cudaMemsetAsync(b.p, 0, n * elt, s);
+    };
+    CK(up_or_zero(m->pos_acc, h->pos_acc, 4));
+    CK(up_or_zero(m->col_acc, h->col_acc, 4));
+    CK(up_or_zero(m->accum, h->accum, 4));
+    CK(up_or_zero(m->visit, h->visit, 8));
+    CK(up_or_zero(m->window, h->window, 8));
+    if (h->tau_v) {
+        if (n) CK(cudaMemcpyAsync(m->tau_v.p, h->tau_v, n * 8, cudaMemcpyDefault, s));
+    } else if (n) {
+        std::vector<double> tv(n, 5.0);
+        CK(cudaMemcpyAsync(m->tau_v.p, tv.data(), n * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    CK(cudaMemsetAsync(m->m1.p, 0, m->m1.bytes, s));
+    CK(cudaMemsetAsync(m->m2.p, 0, m->m2.bytes, s));
+    CK(cudaMemsetAsync(m->step.p, 0, m->step.bytes, s));
+    m->step_views = 0;
+    m->order_dirty = true;
+    CK(cudaStreamSynchronize(s));
+    return TGSX_OK;
+}
+
+int32_t tgsx_model_download(tgsx_ctx* ctx, tgsx_model* m, tgsx_host_scene* h) {
+    if (!ctx || !m || !h) return TGSX_EINVAL;
+    const int64_t n = m->n, cap = m->cap;
+    cudaStream_t s = ctx->stream;
+    float* rows[kParamRows] = {h->px, h->py, h->rot, h->lsx, h->lsy, h->rop, h->cr, h->cg, h->cb, h->depth};
+    const float* P = m->params.as<float>();
+    for (int q = 0; q < kParamRows; ++q)
+        if (rows[q] && n) CK(cudaMemcpyAsync(rows[q], P + q * cap, n * 4, cudaMemcpyDefault, s));
+    if (h->id && n) CK(cudaMemcpyAsync(h->id, m->ids.p, n * 8, cudaMemcpyDefault, s));
+    if (h->pos_acc && n) CK(cudaMemcpyAsync(h->pos_acc, m->pos_acc.p, n * 4, cudaMemcpyDefault, s));
+    if (h->col_acc && n) CK(cudaMemcpyAsync(h->col_acc, m->col_acc.p, n * 4, cudaMemcpyDefault, s));
+    if (h->accum && n) CK(cudaMemcpyAsync(h->accum, m->accum.p, n * 4, cudaMemcpyDefault, s));
+    if (h->visit && n) CK(cudaMemcpyAsync(h->visit, m->visit.p, n * 8, cudaMemcpyDefault, s));
+    if (h->window && n) CK(cudaMemcpyAsync(h->window, m->window.p, n * 8, cudaMemcpyDefault, s));
+    if (h->tau_v && n) CK(cudaMemcpyAsync(h->tau_v, m->tau_v.p, n * 8, cudaMemcpyDefault, s));
+    h->n = n;
+    h->next_id = m->next_id;
+    CK(cudaStreamSynchronize(s));
+    return TGSX_OK;
+}
+
+int32_t tgsx_model_download_moments(tgsx_ctx* ctx, tgsx_model* m, float* m1, float* m2) {
+    const int64_t n = m->n, cap = m->cap;
+    if (n) {
+        if (m1) CK(cudaMemcpy2DAsync(m1, n * 4, m->m1.p, cap * 4, n * 4, 9, cudaMemcpyDefault, ctx->stream));
+        if (m2) CK(cudaMemcpy2DAsync(m2, n * 4, m->m2.p, cap * 4, n * 4, 9, cudaMemcpyDefault, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+int32_t tgsx_model_upload_moments(tgsx_ctx* ctx, tgsx_model* m, const float* m1, const float* m2) {
+    const int64_t n = m->n, cap = m->cap;
+    if (n) {
+        if (m1) CK(cudaMemcpy2DAsync(m->m1.p, cap * 4, m1, n * 4, n * 4, 9, cudaMemcpyDefault, ctx->stream));
+        if (m2) CK(cudaMemcpy2DAsync(m->m2.p, cap * 4, m2, n * 4, n * 4, 9, cudaMemcpyDefault, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+// ---------------------------------------------------------------- render / backward
+int32_t tgsx_render(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
+                    int32_t lowpass_p, float* out_rgb, float* out_T, uint64_t* out_blend_ops) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    int32_t rc = check_pattern(ctx, pat);
+    if (rc) return rc;
+    RenderArgs ra = make_args(pat, bg, lowpass_p);
+    uint32_t* items = nullptr;
+    rc = render_core(ctx, m, ra, false, &items);
+    if (rc) return rc;
+    Workspace& ws = ctx->ws;
+    if (out_rgb && ra.P) CK(cudaMemcpyAsync(out_rgb, ws.rgb.p, (size_t)ra.P * 12, cudaMemcpyDefault, ctx->stream));
+    if (out_T && ra.P) CK(cudaMemcpyAsync(out_T, ws.T.p, (size_t)ra.P * 4, cudaMemcpyDefault, ctx->stream));
+    if (out_blend_ops) {
+        CK(cudaMemcpyAsync(ws.h_scratch + 8, ws.counters.as<unsigned long long>() + 1, 8,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (out_blend_ops) *out_blend_ops = ws.h_scratch[8];
+    return TGSX_OK;
+}
+
+int32_t tgsx_backward(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
+                      int32_t lowpass_p, const float* dLdC, int64_t dLdC_count, float* out_grads,
+                      int32_t update_stats) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    int32_t rc = check_pattern(ctx, pat);
+    if (rc) return rc;
+    RenderArgs ra = make_args(pat, bg, lowpass_p);
+    if (dLdC_count != ra.P)
+        return fail(ctx, TGSX_EINVAL, "backward: loss-gradient count does not match pattern ranks");
+    // the reference recomputes the forward inside backward (rasterizer.cpp:227-263)
+    uint32_t* items = nullptr;
+    rc = render_core(ctx, m, ra, false, &items);
+    if (rc) return rc;
+    Workspace& ws = ctx->ws;
+    if (ra.P) CK(cudaMemcpyAsync(ws.dLdC.p, dLdC, (size_t)ra.P * 12, cudaMemcpyDefault, ctx->stream));
+    CK(launch_backward(ctx, ra, items));
+    float* gout = nullptr;
+    bool host_out = false;
+    if (out_grads && m->n) {
+        if (is_device_ptr(out_grads)) {
+            gout = out_grads;
+        } else {
+            CK(ws.generic.ensure((size_t)m->n * 36));
+            gout = ws.generic.as<float>();
+            host_out = true;
+        }
+    } else if (m->n) {
+        CK(ws.generic.ensure((size_t)m->n * 36));
+        gout = ws.generic.as<float>();
+    }
+    CK(launch_chain(ctx, m, ChainMode::kGrads, update_stats != 0, gout, nullptr));
+    if (host_out) CK(cudaMemcpyAsync(out_grads, gout, (size_t)m->n * 36, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+// ---------------------------------------------------------------- fit step
+int32_t tgsx_adam_step(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const tgsx_adam_args* a) {
+    if (!ctx || !m || !grads || !a) return TGSX_EINVAL;
+    if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
+    AdamCfg c;
+    fill_adam(c, a);
+    const float* g = nullptr;
+    int32_t rc = stage_input(ctx, ctx->ws.generic, grads, (size_t)std::max<int64_t>(m->n, 1) * 36, &g);
+    if (rc) return rc;
+    CK(launch_adam(ctx, m, g, reinterpret_cast<const float*>(&c), 1));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+int32_t tgsx_fit_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
+                      const float* target, const tgsx_adam_args* a, float* out_loss) {
+    if (!ctx || !m || !a) return TGSX_EINVAL;
+    if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
+    AdamCfg c;
+    fill_adam(c, a);
+    return fused_view(ctx, m, pat, bg, target, out_loss, ChainMode::kAdam, &c);
+}
+
+int32_t tgsx_view_accumulate(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat,
+                             const float bg[3], const float* target, float* out_loss) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    int32_t rc = fused_view(ctx, m, pat, bg, target, out_loss, ChainMode::kAccumulate, nullptr);
+    if (!rc) m->step_views++;
+    return rc;
+}
+
+float* tgsx_step_buffer(tgsx_model* m, int64_t* out_floats) {
+    if (!m) return nullptr;
+    if (out_floats) *out_floats = (int64_t)kStepFloats * m->cap;
+    return m->step.as<float>();
+}
+
+int32_t tgsx_apply_step(tgsx_ctx* ctx, tgsx_model* m, int32_t batch_views, const tgsx_adam_args* a) {
+    if (!ctx || !m || !a) return TGSX_EINVAL;
+    if (batch_views < 1) return fail(ctx, TGSX_EINVAL, "accumulate: empty batch");
+    if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
+    AdamCfg c;
+    fill_adam(c, a);
+    CK(launch_adam(ctx, m, nullptr, reinterpret_cast<const float*>(&c), batch_views));
+    m->step_views = 0;
+    return TGSX_OK;
+}
+
+// ---------------------------------------------------------------- stage access
+int32_t tgsx_stage_prepare(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, float* out, uint32_t* orig) {
+    if (!ctx || !m || lowpass_p < 1) return fail(ctx, TGSX_EINVAL, "bad arguments");
+    CK(reset_counters(ctx));
+    if (m->order_dirty) CK(launch_sort_depth(ctx, m));
+    CK(launch_preprocess(ctx, m, lowpass_p, 16, 16));
+    CK(cudaMemcpyAsync(ctx->ws.h_scratch, ctx->ws.counters.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    int32_t rc = check_kernel_error(ctx, ctx->ws.h_scratch[0]);
+    if (rc) return rc;
+    const int64_t n = m->n;
+    if (!n) return TGSX_OK;
+    std::vector<Prepared> hp(n);
+    CK(cudaMemcpy(hp.data(), ctx->ws.prep.p, n * sizeof(Prepared), cudaMemcpyDeviceToHost));
+    std::vector<float> o(11 * n);
+    std::vector<uint32_t> og(n);
+    for (int64_t r = 0; r < n; ++r) {
+        const Prepared& p = hp[r];
+        const float v[11] = {p.a.x, p.a.y, p.a.z, p.a.w, p.b.x, p.b.y, p.c.x, p.c.y, p.c.z, p.b.z, p.b.w};
+        for (int q = 0; q < 11; ++q) o[q * n + r] = v[q];
+        std::memcpy(&og[r], &p.c.w, 4);
+    }
+    if (out) CK(cudaMemcpy(out, o.data(), o.size() * 4, cudaMemcpyDefault));
+    if (orig) CK(cudaMemcpy(orig, og.data(), og.size() * 4, cudaMemcpyDefault));
+    return TGSX_OK;
+}
+
+int32_t tgsx_stage_sorted_order(tgsx_ctx* ctx, tgsx_model* m, uint32_t* perm) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    if (m->order_dirty) CK(launch_sort_depth(ctx, m));
+    if (m->n && perm) CK(cudaMemcpyAsync(perm, m->perm.p, m->n * 4, cudaMemcpyDefault, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+int32_t tgsx_stage_tile_lists(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, int32_t width,
+                              int32_t height, uint32_t* offsets, uint32_t* items,
+                              int64_t items_cap, int64_t* out_k) {
+    if (!ctx || !m || lowpass_p < 1 || width < 1 || height < 1) return fail(ctx, TGSX_EINVAL, "bad arguments");
+    uint32_t* it = nullptr;
+    uint32_t* keys = nullptr;
+    int32_t rc = bin(ctx, m, lowpass_p, width, height, &it, &keys);
+    if (rc) return rc;
+    const int64_t K = ctx->ws.K;
+    if (out_k) *out_k = K;
+    const int tiles = ctx->ws.tiles_x * ctx->ws.tiles_y;
+    std::vector<uint32_t> hk(K);
+    if (K) CK(cudaMemcpy(hk.data(), keys, K * 4, cudaMemcpyDeviceToHost));
+    if (offsets) {
+        std::vector<uint32_t> off(tiles + 1, 0);
+        for (int64_t s = 0; s < K; ++s) off[hk[s] + 1]++;
+        for (int t = 0; t < tiles; ++t) off[t + 1] += off[t];
+        CK(cudaMemcpy(offsets, off.data(), off.size() * 4, cudaMemcpyDefault));
+    }
+    if (items && items_cap >= K && K) CK(cudaMemcpy(items, it, K * 4, cudaMemcpyDefault));
+    return TGSX_OK;
+}
+
+int32_t tgsx_stage_screen_grads(tgsx_ctx* ctx, tgsx_model* m, float* out) {
+    if (!ctx || !m || !out) return TGSX_EINVAL;
+    if (m->n) CK(cudaMemcpy2DAsync(out, m->n * 4, m->screen.p, m->cap * 4, m->n * 4, 10, cudaMemcpyDefault, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+int32_t tgsx_stage_counters(tgsx_ctx* ctx, uint64_t* out_blend_ops, uint64_t* out_evals, uint64_t* out_pairs) {
+    if (!ctx) return TGSX_EINVAL;
+    CK(cudaMemcpyAsync(ctx->ws.h_scratch + 16, ctx->ws.counters.p, 4 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (out_blend_ops) *out_blend_ops = ctx->ws.h_scratch[17];
+    if (out_evals) *out_evals = ctx->ws.h_scratch[18];
+    if (out_pairs) *out_pairs = (uint64_t)ctx->ws.K;
+    return TGSX_OK;
+}
+
+int32_t tgsx_sort_pairs(tgsx_ctx* ctx, uint32_t* keys, uint32_t* vals, int64_t n, int32_t key_bits) {
+    if (!ctx || n < 0 || key_bits < 0 || key_bits > 32) return TGSX_EINVAL;
+    if (n <= 1) return TGSX_OK;
+    DevBuf& a = ctx->ws.generic;
+    CK(a.ensure((size_t)n * 8));
+    uint32_t* k2 = a.as<uint32_t>();
+    uint32_t* v2 = k2 + n;
+    uint32_t* k = keys;
+    uint32_t* v = vals;
+    CK(sort_pairs(ctx, k, v, k2, v2, n, key_bits, nullptr));
+    if (k != keys) {
+        CK(cudaMemcpyAsync(keys, k, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(vals, v, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+int32_t tgsx_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n, uint64_t* out_total) {
+    if (!ctx || n < 0) return TGSX_EINVAL;
+    uint32_t* d_total = reinterpret_cast<uint32_t*>(ctx->ws.counters.as<unsigned long long>() + 5);
+    CK(launch_exclusive_scan(ctx, in, out, n, d_total));
+    CK(cudaMemcpyAsync(ctx->ws.h_scratch + 24, d_total, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (out_total) *out_total = n ? (uint64_t)(uint32_t)ctx->ws.h_scratch[24] : 0;
+    return TGSX_OK;
+}
+
+}  // extern "C"

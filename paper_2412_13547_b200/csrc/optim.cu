@@ -1,0 +1,235 @@
+// Per-Gaussian kernels after the blend backward (sm_100a, HBM-bound streaming):
+//
+//  chain_kernel   merge of the per-(tile, splat) partials in a fixed order (the reference's
+//                 tile-order merge, rasterizer.cpp:301-319), chain rule to raw parameters
+//                 (rasterizer.cpp:321-346), densify statistics (rasterizer.cpp:348-359) and,
+//                 in the fused fit step, the Adam update + clamp_parameters (SPEC.md:258-267,
+//                 gaussian.hpp:105-116) — one pass over the Gaussian state instead of four.
+//  adam_kernel    Adam with explicit gradients (tgsx_adam_step) or the mean of the batched
+//                 step buffer (tgsx_apply_step, SPEC.md:269-277 accumulate).
+//
+// Bit-exactness: given identical screen-space sums / gradients, the chain rule and Adam round
+// exactly like the C oracle (explicit _rn intrinsics, CR transcendentals).
+#include "tgsx_device.cuh"
+#include "tgsx_internal.h"
+
+namespace tgsx {
+
+namespace {
+
+__device__ __forceinline__ float clampf(float v, float lo, float hi) {
+    return v < lo ? lo : (hi < v ? hi : v);
+}
+
+// Adam on one Gaussian's 9 components + clamp (mirrors oracle or_adam_step exactly).
+__device__ __forceinline__ void adam_update(float* __restrict__ params, float* __restrict__ m1,
+                                            float* __restrict__ m2, int64_t cap, int64_t i,
+                                            const float (&g)[9], const AdamCfg& c) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        const int64_t o = (int64_t)q * cap + i;
+        const float mm = fadd(fmul(c.b1, m1[o]), fmul(c.omb1, g[q]));
+        const float vv = fadd(fmul(c.b2, m2[o]), fmul(fmul(c.omb2, g[q]), g[q]));
+        m1[o] = mm;
+        m2[o] = vv;
+        const float mh = fdiv(mm, c.bc1);
+        const float vh = fdiv(vv, c.bc2);
+        float th = params[o];
+        th = fsub(th, fdiv(fmul(c.lr[q], mh), fadd(__fsqrt_rn(vh), c.eps)));
+        if (q == 3 || q == 4) th = clampf(th, c.ls_lo, c.ls_hi);
+        if (q >= 5) th = clampf(th, -c.raw_cap, c.raw_cap);
+        params[o] = th;
+    }
+}
+
+struct ChainParams {
+    const float* params;
+    float* params_w;
+    int64_t cap, n;
+    const uint32_t* rank_of;
+    const Prepared* prep;
+    const float4* partial;
+    float* screen;  // [10][cap] or null
+    // stats
+    float* pos_acc;
+    float* col_acc;
+    int32_t* accum;
+    int64_t* visit;
+    int64_t* window;
+    int update_stats;
+    // outputs
+    int mode;  // 0 grads, 1 adam, 2 accumulate
+    float* grads;   // [9][n] (mode 0)
+    float* m1;
+    float* m2;
+    float* step;    // [12][cap] (mode 2)
+    AdamCfg adam;
+};
+
+__global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cp.n) return;
+    const int64_t cap = cp.cap;
+    const uint32_t r = cp.rank_of[i];
+    const uint4 d = cp.prep[r].d;
+    float s[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) s[k] = 0.f;
+    const float4* src = cp.partial + 3 * (size_t)d.z;
+    for (uint32_t t = 0; t < d.w; ++t) {
+        const float4 a = src[3 * t], b = src[3 * t + 1], c = src[3 * t + 2];
+        s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
+        s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+        s[8] += c.x;
+        s[9] = fmaxf(s[9], c.y);
+    }
+    if (cp.screen) {
+#pragma unroll
+        for (int k = 0; k < 10; ++k) cp.screen[k * cap + i] = s[k];
+    }
+    const bool visited = s[9] > 0.f;
+    // chain rule (rasterizer.cpp:324-346)
+    const float rot = cp.params[2 * cap + i];
+    const float lx = cp.params[3 * cap + i], ly = cp.params[4 * cap + i];
+    float g[9];
+    g[0] = s[0];
+    g[1] = s[1];
+    {
+        float sn, c;
+        cr_sincosf(rot, &sn, &c);
+        const float a = cr_expf(fmul(2.0f, lx));
+        const float b = cr_expf(fmul(2.0f, ly));
+        const float m00 = s[2], m01 = s[3], m11 = s[4];
+        const float cs = fmul(c, sn);
+        const float amb = fsub(a, b);
+        // m00 * (-2 cs amb) + 2 m01 ((c c - s s) amb) + m11 (2 cs amb)
+        g[2] = fadd(fadd(fmul(m00, fmul(fmul(-2.0f, cs), amb)),
+                         fmul(fmul(2.0f, m01), fmul(fsub(fmul(c, c), fmul(sn, sn)), amb))),
+                    fmul(m11, fmul(fmul(2.0f, cs), amb)));
+        // 2 a (m00 c c + 2 m01 cs + m11 s s)
+        g[3] = fmul(fmul(2.0f, a), fadd(fadd(fmul(fmul(m00, c), c), fmul(fmul(2.0f, m01), cs)),
+                                        fmul(fmul(m11, sn), sn)));
+        // 2 b (m00 s s - 2 m01 cs + m11 c c)
+        g[4] = fmul(fmul(2.0f, b), fadd(fsub(fmul(fmul(m00, sn), sn), fmul(fmul(2.0f, m01), cs)),
+                                        fmul(fmul(m11, c), c)));
+        const float al = activate_cr(cp.params[5 * cap + i]);
+        g[5] = fmul(s[5], fmul(al, fsub(1.0f, al)));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float ck = activate_cr(cp.params[(6 + k) * cap + i]);
+            g[6 + k] = fmul(s[6 + k], fmul(ck, fsub(1.0f, ck)));
+        }
+    }
+    // densify statistics (rasterizer.cpp:350-358): norms of the position and raw-colour grads
+    float pn = 0.f, cn = 0.f;
+    if (visited) {
+        pn = __fsqrt_rn(fadd(fmul(g[0], g[0]), fmul(g[1], g[1])));
+        cn = __fsqrt_rn(fadd(fadd(fmul(g[6], g[6]), fmul(g[7], g[7])), fmul(g[8], g[8])));
+    }
+    if (cp.mode == 2) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) cp.step[q * cap + i] += g[q];
+        if (visited) {
+            cp.step[9 * cap + i] += pn;
+            cp.step[10 * cap + i] += cn;
+            cp.step[11 * cap + i] += 1.0f;
+        }
+        return;
+    }
+    if (cp.update_stats && visited) {
+        cp.pos_acc[i] = fadd(cp.pos_acc[i], pn);
+        cp.col_acc[i] = fadd(cp.col_acc[i], cn);
+        cp.accum[i] += 1;
+        cp.visit[i] += 1;
+        cp.window[i] += 1;
+    }
+    if (cp.mode == 0) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) cp.grads[q * cp.n + i] = g[q];
+        return;
+    }
+    adam_update(cp.params_w, cp.m1, cp.m2, cap, i, g, cp.adam);
+}
+
+// mode 0: grads [9][n] given; mode 1: step buffer [12][cap] (mean over batch, stats applied)
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, float* __restrict__ m1,
+                                                   float* __restrict__ m2, int64_t cap, int64_t n,
+                                                   const float* __restrict__ grads,
+                                                   float* __restrict__ step, float* pos_acc,
+                                                   float* col_acc, int32_t* accum, int64_t* visit,
+                                                   int64_t* window, AdamCfg c) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float g[9];
+    if (step) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            g[q] = fdiv(step[q * cap + i], c.batch);
+            step[q * cap + i] = 0.f;
+        }
+        const float v = step[11 * cap + i];
+        if (v > 0.f) {
+            const int32_t cnt = (int32_t)v;
+            pos_acc[i] = fadd(pos_acc[i], step[9 * cap + i]);
+            col_acc[i] = fadd(col_acc[i], step[10 * cap + i]);
+            accum[i] += cnt;
+            visit[i] += cnt;
+            window[i] += cnt;
+        }
+        step[9 * cap + i] = 0.f;
+        step[10 * cap + i] = 0.f;
+        step[11 * cap + i] = 0.f;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) g[q] = grads[q * n + i];
+    }
+    adam_update(params, m1, m2, cap, i, g, c);
+}
+
+inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / bt); }
+
+}  // namespace
+
+cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool update_stats,
+                         float* grads_out, const float* adam_cfg) {
+    if (m->n == 0) return cudaSuccess;
+    ChainParams cp{};
+    cp.params = m->params.as<float>();
+    cp.params_w = m->params.as<float>();
+    cp.cap = m->cap;
+    cp.n = m->n;
+    cp.rank_of = m->rank_of.as<uint32_t>();
+    cp.prep = ctx->ws.prep.as<Prepared>();
+    cp.partial = ctx->ws.partial.as<float4>();
+    cp.screen = m->screen.as<float>();
+    cp.pos_acc = m->pos_acc.as<float>();
+    cp.col_acc = m->col_acc.as<float>();
+    cp.accum = m->accum.as<int32_t>();
+    cp.visit = m->visit.as<int64_t>();
+    cp.window = m->window.as<int64_t>();
+    cp.update_stats = update_stats ? 1 : 0;
+    cp.mode = mode == ChainMode::kGrads ? 0 : (mode == ChainMode::kAdam ? 1 : 2);
+    cp.grads = grads_out;
+    cp.m1 = m->m1.as<float>();
+    cp.m2 = m->m2.as<float>();
+    cp.step = m->step.as<float>();
+    if (adam_cfg) cp.adam = *reinterpret_cast<const AdamCfg*>(adam_cfg);
+    chain_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(cp);
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adam(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const float* adam_cfg,
+                        int batch_views) {
+    if (m->n == 0) return cudaSuccess;
+    AdamCfg c = *reinterpret_cast<const AdamCfg*>(adam_cfg);
+    c.batch = (float)(batch_views > 0 ? batch_views : 1);
+    adam_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(
+        m->params.as<float>(), m->m1.as<float>(), m->m2.as<float>(), m->cap, m->n, grads,
+        grads ? nullptr : m->step.as<float>(), m->pos_acc.as<float>(), m->col_acc.as<float>(),
+        m->accum.as<int32_t>(), m->visit.as<int64_t>(), m->window.as<int64_t>(), c);
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace tgsx

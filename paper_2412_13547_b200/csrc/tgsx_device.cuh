@@ -1,0 +1,138 @@
+// Device-side helpers shared by the tgsx kernels (sm_100a).
+//
+// Bit-exact stages (preprocess, binning, Adam, densify predicates) must round exactly like
+// the reference built with -ffp-contract=off (proj/CMakeLists.txt:12): every float op there
+// is written with an explicit round-to-nearest intrinsic so nvcc can never contract it into
+// an FMA. Transcendentals follow the correctly-rounded contract (oracle/cr_libm.c):
+// f(float x) := round_to_float(f_double((double)x)).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tgsx {
+
+constexpr int kTile = 16;                 // rasterizer.hpp:12
+constexpr float kTermT = 1e-4f;           // rasterizer.hpp:14 (float(1e-4))
+constexpr float kMinVisitW = 1e-4f;       // rasterizer.hpp:17
+constexpr float kCullSigmas = 3.0f;       // rasterizer.hpp:19
+constexpr double kMinScale = 1e-4;        // gaussian.hpp:14
+constexpr double kRawCap = 12.0;          // gaussian.hpp:18
+constexpr int kParams = 9;                // optimised components per Gaussian
+constexpr int kStepFloats = 12;           // step buffer: 9 grads + pos norm + col norm + visits
+
+// Kernel error word: (rank << 2) | code, lowest wins; all-ones = no error.
+constexpr unsigned long long kErrNone = ~0ull;
+
+// ------------------------------------------------------------------ CR transcendentals
+__device__ __forceinline__ float cr_expf(float x) { return __double2float_rn(exp((double)x)); }
+__device__ __forceinline__ float cr_logf(float x) { return __double2float_rn(log((double)x)); }
+__device__ __forceinline__ void cr_sincosf(float x, float* s, float* c) {
+    double sd, cd;
+    sincos((double)x, &sd, &cd);
+    *s = __double2float_rn(sd);
+    *c = __double2float_rn(cd);
+}
+
+// ------------------------------------------------------------------ exact float ops
+__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
+
+// activate (gaussian.hpp:47-49): 1 / (1 + exp(-raw))
+__device__ __forceinline__ float activate_cr(float raw) {
+    return fdiv(1.0f, fadd(1.0f, cr_expf(-raw)));
+}
+
+// static_cast<int>(double) as the reference's x86-64 build executes it (cvttsd2si): values
+// outside int range and NaN become INT_MIN ("integer indefinite"), where the GPU's native
+// conversion would saturate. Keeps off-image / non-finite splats unbinned exactly like the
+// reference.
+__device__ __forceinline__ int x86_double_to_int(double v) {
+    return (v >= -2147483648.0 && v < 2147483648.0) ? (int)v : (int)0x80000000;
+}
+
+// pixel_span (rasterizer.cpp:50-56): float m±r, then double ceil/floor of (value - 0.5).
+__device__ __forceinline__ void pixel_span(float m, float r, int limit, int& lo, int& hi) {
+    lo = x86_double_to_int(ceil(__dsub_rn((double)fsub(m, r), 0.5)));
+    hi = x86_double_to_int(floor(__dsub_rn((double)fadd(m, r), 0.5)));
+    if (lo < 0) lo = 0;
+    if (hi > limit - 1) hi = limit - 1;
+}
+
+// Tile rectangle of a prepared splat (rasterizer.cpp:74-84); false when off-image.
+__device__ __forceinline__ bool tile_rect(float mx, float my, float rx, float ry, int W, int H,
+                                          int& tx0, int& tx1, int& ty0, int& ty1) {
+    int px0, px1, py0, py1;
+    pixel_span(mx, rx, W, px0, px1);
+    pixel_span(my, ry, H, py0, py1);
+    if (px0 > px1 || py0 > py1) return false;
+    tx0 = px0 / kTile;
+    tx1 = px1 / kTile;
+    ty0 = py0 / kTile;
+    ty1 = py1 / kTile;
+    return true;
+}
+
+// DilationPattern::first_active_at_or_after (dilation.hpp:49-53)
+__device__ __forceinline__ int first_active(int v, int offset, int p) {
+    if (v <= offset) return offset;
+    const int k = (v - offset + p - 1) / p;
+    return offset + k * p;
+}
+
+// Orderable u32 of a float depth key (ascending float order; -0 canonicalised to +0 so that
+// -0 == +0 ties fall through to the id order like the reference comparator, model.hpp:111).
+__device__ __forceinline__ uint32_t orderable_key(float f) {
+    uint32_t u = __float_as_uint(f);
+    if (u == 0x80000000u) u = 0u;
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// ------------------------------------------------------------------ prepared splat record
+// 64 B per splat, blend (rank) order:
+//   a = (mean x, mean y, inv00, inv01)   b = (inv11, alpha, rx, ry)
+//   c = (r, g, b, orig as bits)          d = (rect x packed, rect y packed, pair offset, tiles)
+// rect packed = lo | hi << 16 (tile units); tiles == 0 => not binned.
+struct __align__(16) Prepared {
+    float4 a, b, c;
+    uint4 d;
+};
+
+// ------------------------------------------------------------------ blend math
+// log2(e) * -0.5: G = exp(-q/2) = exp2(q * kNegHalfLog2e). Shared by forward and backward so
+// the recomputed sigma is bit-identical (the backward's T recovery relies on it).
+constexpr float kNegHalfLog2e = -0.72134752044448170368f;
+
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// q = inv00 dx^2 + 2 inv01 dx dy + inv11 dy^2 with a fixed FMA schedule; returns G.
+__device__ __forceinline__ float splat_gauss(float i00, float i01x2, float i11, float dx,
+                                             float dy) {
+    const float t = __fmul_rn(i11, dy);
+    const float u = __fmaf_rn(i01x2, dx, t);          // 2 i01 dx + i11 dy
+    const float v = __fmul_rn(u, dy);                 // (2 i01 dx + i11 dy) dy
+    const float q = __fmaf_rn(__fmul_rn(i00, dx), dx, v);
+    return fast_exp2(__fmul_rn(q, kNegHalfLog2e));
+}
+
+// ------------------------------------------------------------------ misc
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ void raise_error(unsigned long long* err, uint32_t rank,
+                                            uint32_t code) {
+    // lowest (rank, code) wins, i.e. the first failing splat in blend order (the reference
+    // throws at the first failure while walking sorted order, rasterizer.cpp:28-32)
+    atomicMin(err, ((unsigned long long)rank << 2) | code);
+}
+
+}  // namespace tgsx

@@ -1,0 +1,155 @@
+// Host-side internals of libtgsx: context, device model, workspace, kernel launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/tgsx.h"
+
+namespace tgsx {
+
+// Growable device allocation (never shrinks; contents are not preserved on growth unless
+// grow_keep is used).
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t need);
+    cudaError_t grow_keep(size_t need, size_t keep_bytes, cudaStream_t s);
+    void release();
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct Status {
+    int32_t code = TGSX_OK;
+    std::string msg;
+};
+
+struct Workspace {
+    // per-render, rank (blend) order
+    DevBuf prep;        // Prepared[n]
+    DevBuf touched;     // u32[n + 1] tiles touched per rank
+    DevBuf pair_off;    // u32[n + 1] exclusive scan of touched
+    DevBuf scan_tmp;    // look-back status
+    // binning
+    DevBuf keys[2], vals[2];  // u32[K] ping-pong
+    DevBuf sort_tmp;          // histograms + block status + tickets
+    DevBuf ranges;            // uint2[tiles]
+    DevBuf partial;           // float4[K * 3] per-(tile, splat) gradient partials
+    // per-pixel
+    DevBuf rgb, T, last, dLdC, target;
+    DevBuf block_loss;        // float[tiles]
+    DevBuf counters;          // u64: [0] err, [1] blend ops, [2] evals, [3..] scratch
+    DevBuf generic;           // misc scratch
+    // pinned host scratch
+    uint64_t* h_scratch = nullptr;
+    int64_t K = 0;
+    int tiles_x = 0, tiles_y = 0;
+    int last_W = 0, last_H = 0, last_P = 0;
+    bool have_forward = false;
+};
+
+}  // namespace tgsx
+
+namespace tgsx {
+// Live per-stage timing with CUDA events on the context stream (enabled by tgsx_profile).
+enum Stage { kStDepthSort, kStPreprocess, kStScan, kStDuplicate, kStSort, kStRanges,
+             kStForward, kStBackward, kStChain, kStLoss, kStDensify, kNumStages };
+struct Profiler {
+    bool enabled = false;
+    std::vector<cudaEvent_t> pool;          // reusable events
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    double ms[kNumStages] = {};
+    int64_t count[kNumStages] = {};
+    size_t next = 0;
+    cudaEvent_t get();
+    void begin(int stage, cudaStream_t s, cudaEvent_t* out);
+    void end(int stage, cudaStream_t s, cudaEvent_t start);
+    void harvest();  // accumulates completed pairs (caller ensures completion)
+};
+}  // namespace tgsx
+
+struct tgsx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    tgsx::Workspace ws;
+    tgsx::Profiler prof;
+};
+
+// Scoped stage timer: no-op unless profiling is enabled.
+namespace tgsx {
+struct StageTimer {
+    tgsx_ctx* ctx;
+    int stage;
+    cudaEvent_t start = nullptr;
+    StageTimer(tgsx_ctx* c, int st) : ctx(c), stage(st) {
+        if (ctx->prof.enabled) ctx->prof.begin(stage, ctx->stream, &start);
+    }
+    ~StageTimer() {
+        if (ctx->prof.enabled && start) ctx->prof.end(stage, ctx->stream, start);
+    }
+};
+}  // namespace tgsx
+
+struct tgsx_model {
+    int64_t n = 0, cap = 0;
+    uint64_t next_id = 0;
+    bool order_dirty = true;
+    bool ids_monotone = true;
+    tgsx::DevBuf params;   // float[10][cap]: px py rot lsx lsy rop cr cg cb depth
+    tgsx::DevBuf ids;      // u64[cap]
+    tgsx::DevBuf pos_acc, col_acc, accum, visit, window, tau_v;
+    tgsx::DevBuf m1, m2;   // float[9][cap] Adam moments
+    tgsx::DevBuf step;     // float[12][cap] batched-view step buffer
+    tgsx::DevBuf perm;     // u32[cap] rank -> index
+    tgsx::DevBuf rank_of;  // u32[cap] index -> rank
+    tgsx::DevBuf screen;   // float[10][cap] screen-space grads of the last backward
+    int64_t step_views = 0;
+};
+
+namespace tgsx {
+
+// Adam hyper-parameters for one step, computed on the host.
+struct AdamCfg {
+    float lr[9];
+    float b1, b2, omb1, omb2, eps, bc1, bc2;
+    float ls_lo, ls_hi, raw_cap;
+    float batch;  // divisor for the batched mean (1 = plain step)
+};
+
+// kernel launchers (defined in the .cu files); all enqueue on ctx->stream
+struct RenderArgs {
+    int p, ox, oy, W, H, cols, rows, P;
+    float bg[3];
+    int lowpass_p;
+    const float* target;  // fused L1 target (device, W*H*3) or null
+};
+
+cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m);
+cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H);
+cudaError_t launch_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n,
+                                  uint32_t* d_total);
+cudaError_t launch_duplicate(tgsx_ctx* ctx, tgsx_model* m, int W, int H, int key_bits);
+cudaError_t sort_pairs(tgsx_ctx* ctx, uint32_t*& keys, uint32_t*& vals, uint32_t* keys_alt,
+                       uint32_t* vals_alt, int64_t n, int key_bits, const uint32_t* d_hist);
+cudaError_t launch_ranges(tgsx_ctx* ctx, const uint32_t* keys, int64_t K, int tiles);
+cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
+                           bool fused_loss);
+cudaError_t launch_backward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items);
+enum class ChainMode { kGrads, kAdam, kAccumulate };
+cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool update_stats,
+                         float* grads_out, const float* adam_cfg);
+cudaError_t launch_adam(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const float* adam_cfg,
+                        int batch_views);
+
+int key_bits_for(int tiles);
+
+}  // namespace tgsx
