@@ -116,7 +116,7 @@ def test_render_empty_and_offimage(P, ctx):
     assert out.blend_op_count == 0
     empty = P.DeviceModel.from_host(P.GaussianModel(0), ctx)
     out = empty.render(P.DilationPattern(2, 1, 0, W, H), (0.0, 0.0, 0.0))
-    assert out.colors.shape == (15 * 15, 3) and np.all(out.colors == 0)
+    assert out.colors.shape == (20 * 15, 3) and np.all(out.colors == 0)
 
 
 def _grad_check(g, r, label):
