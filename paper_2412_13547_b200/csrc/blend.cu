@@ -1,0 +1,543 @@
+// Alpha-blend forward and backward over the per-tile splat lists (sm_100a, FP32 pipe).
+//
+// Work decomposition: one CTA per 16x16 tile; each warp owns an 8x4 block of ACTIVE pixels
+// (for the dilated variant the block spans 8p x 4p image pixels, so the same kernels serve
+// p = 1 and the paper's 4K dilated rendering). Splat batches are staged in shared memory with
+// exact per-tile box-test masks (rasterizer.cpp:116-118 evaluated once per (tile, splat) in
+// float, per active column / row).
+//
+// Per 32-splat chunk a warp builds the 32x32 (splat x pixel) pass matrix: lane j turns splat
+// j's column/row masks into a 32-bit row with one multiply, a 5-stage shuffle bit-transpose
+// hands lane l the column "which of these 32 splats pass my pixel". Each lane then walks only
+// its own passing splats with ffs (forward, front to back) or clz (backward, back to front).
+// This replaces the reference's per-pixel walk over the whole list (walk_pixel,
+// rasterizer.cpp:108-136) without changing a single blended term: the order per pixel is the
+// list order, box-failing splats contribute nothing in the reference either.
+//
+// forward_kernel: walk_pixel + render (rasterizer.cpp:144-184), optional fused L1 epilogue
+//   (SPEC.md:562-570). Records per pixel the final T and the last blended list position.
+// backward_kernel: backward tile phase (rasterizer.cpp:234-292) in two phases per chunk:
+//   1. per pixel, back to front: T_i = T_{i+1} / (1 - sigma_i) with sigma recomputed
+//      bit-identically to the forward, the reference's exact suffix S (rasterizer.cpp:266-287),
+//      dL/dsigma; (w, dL/dsigma) recorded per (splat, pixel) in shared memory;
+//   2. per splat (lane j = splat j), over its contributing pixels: the gradient terms of
+//      rasterizer.cpp:271-285 accumulated in registers — no cross-lane reductions.
+//   Warp partials are combined across warps in a fixed order and written once per (tile,
+//   splat) pair slot (no global atomics, deterministic; merged per Gaussian in optim.cu in
+//   tile order like rasterizer.cpp:301-319).
+#include "tgsx_device.cuh"
+#include "tgsx_internal.h"
+
+#include <algorithm>
+
+namespace tgsx {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+struct BlendParams {
+    const uint2* ranges;
+    const uint32_t* items;
+    const Prepared* prep;
+    int tiles_x, p, ox, oy, W, H, cols;
+    float bg0, bg1, bg2;
+    float* rgb;
+    float* T;
+    uint32_t* last;
+    unsigned long long* counters;  // [1] blend ops, [2] evaluations
+    const float* target;           // fused L1 (forward)
+    float* dLdC;
+    float* block_loss;
+    float loss_scale;
+    float4* partial;               // backward output, 3 float4 per pair slot
+};
+
+// Per-lane pixel of the CTA's tile, in active coordinates.
+template <int NWX>
+struct PixelMap {
+    int tx, ty, x0, y0, ax, ay, acols, arows, bx, by, x, y, rank;
+    float fx, fy;
+    bool valid;
+    __device__ __forceinline__ void init(const BlendParams& prm, int tile) {
+        tx = tile % prm.tiles_x;
+        ty = tile / prm.tiles_x;
+        x0 = tx * kTile;
+        y0 = ty * kTile;
+        const int px1 = min(prm.W, x0 + kTile), py1 = min(prm.H, y0 + kTile);
+        ax = first_active(x0, prm.ox, prm.p);
+        ay = first_active(y0, prm.oy, prm.p);
+        acols = ax < px1 ? (px1 - ax + prm.p - 1) / prm.p : 0;
+        arows = ay < py1 ? (py1 - ay + prm.p - 1) / prm.p : 0;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        bx = warp % NWX;
+        by = warp / NWX;
+        const int lx = bx * 8 + (lane & 7);
+        const int ly = by * 4 + (lane >> 3);
+        valid = lx < acols && ly < arows;
+        x = ax + lx * prm.p;
+        y = ay + ly * prm.p;
+        fx = (float)x + 0.5f;
+        fy = (float)y + 0.5f;
+        rank = valid ? ((y - prm.oy) / prm.p) * prm.cols + (x - prm.ox) / prm.p : 0;
+    }
+};
+
+// Exact box-test mask over the tile's active columns (or rows): bit c set iff
+// |float(a0 + c p) + 0.5 - m| <= r (rasterizer.cpp:116-118, same float rounding).
+__device__ __forceinline__ uint32_t box_mask(float m, float r, int a0, int p, int count) {
+    uint32_t mask = 0;
+#pragma unroll
+    for (int c = 0; c < kTile; ++c) {
+        const float d = __fsub_rn(__fadd_rn((float)(a0 + c * p), 0.5f), m);
+        mask |= (c < count && fabsf(d) <= r) ? (1u << c) : 0u;
+    }
+    return mask;
+}
+
+// Row of the warp's 8x4 pixel block passing a splat: bit l = (l&7, l>>3).
+__device__ __forceinline__ uint32_t warp_rowmask(uint32_t mask, int bx, int by) {
+    const uint32_t xb = (mask >> (bx * 8)) & 0xffu;
+    const uint32_t yb = (mask >> (16 + by * 4)) & 0xfu;
+    const uint32_t s = (yb & 1u) | ((yb & 2u) << 7) | ((yb & 4u) << 14) | ((yb & 8u) << 21);
+    return xb * s;
+}
+
+// 32x32 bit-matrix transpose across the warp: in lane j bit l = M[j][l]; out lane l bit j.
+__device__ __forceinline__ uint32_t transpose32(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t ms[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int k = 16 >> s;
+        const uint32_t m = ms[s];
+        const uint32_t x = __shfl_xor_sync(kFull, v, k);
+        v = (lane & k) ? ((v & ~m) | ((x & ~m) >> k)) : ((v & m) | ((x & m) << k));
+    }
+    return v;
+}
+
+__device__ __forceinline__ void stage_splat(const BlendParams& prm, uint32_t rank,
+                                            const PixelMap<1>& g, int p, float4& sa, float4& sb,
+                                            float2& sc) {
+    const Prepared& P = prm.prep[rank];
+    const float4 a = P.a, b = P.b, c = P.c;
+    const uint32_t mask = box_mask(a.x, b.z, g.ax, p, g.acols) |
+                          (box_mask(a.y, b.w, g.ay, p, g.arows) << 16);
+    sa = make_float4(a.x, a.y, a.z, a.w * 2.0f);
+    sb = make_float4(b.x, b.y, c.x, c.y);
+    sc = make_float2(c.z, __uint_as_float(mask));
+}
+
+template <int NWX>
+__device__ __forceinline__ PixelMap<1> tile_geom(const PixelMap<NWX>& pm) {
+    PixelMap<1> g;
+    g.ax = pm.ax;
+    g.ay = pm.ay;
+    g.acols = pm.acols;
+    g.arows = pm.arows;
+    return g;
+}
+
+// ------------------------------------------------------------------------------- forward
+template <int NWX, int NWY, int BATCH>
+__global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm) {
+    constexpr int NW = NWX * NWY, NT = NW * 32;
+    __shared__ float4 s_a[BATCH];
+    __shared__ float4 s_b[BATCH];
+    __shared__ float2 s_c[BATCH];
+    __shared__ unsigned long long s_red[2][NW];
+    __shared__ float s_loss[NW];
+
+    const int tile = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    PixelMap<NWX> pm;
+    pm.init(prm, tile);
+    const PixelMap<1> geo = tile_geom(pm);
+    const uint2 range = prm.ranges[tile];
+    const int count = (int)(range.y - range.x);
+
+    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
+    uint32_t last = 0, ops = 0;
+    bool done = !pm.valid;
+    bool warp_done = __all_sync(kFull, done);
+
+    for (int bstart = 0; bstart < count; bstart += BATCH) {
+        if (__syncthreads_and(warp_done)) break;
+        const int bcount = min(BATCH, count - bstart);
+        for (int j = threadIdx.x; j < bcount; j += NT) {
+            float4 a, b;
+            float2 c;
+            stage_splat(prm, prm.items[range.x + bstart + j], geo, prm.p, a, b, c);
+            s_a[j] = a;
+            s_b[j] = b;
+            s_c[j] = c;
+        }
+        __syncthreads();
+        if (warp_done) continue;
+        for (int c0 = 0; c0 < bcount; c0 += 32) {
+            const int j = c0 + lane;
+            const uint32_t row = j < bcount ? warp_rowmask(__float_as_uint(s_c[j].y), pm.bx, pm.by) : 0u;
+            uint32_t col = transpose32(row);
+            if (done) col = 0;
+            while (__any_sync(kFull, col)) {
+                if (col) {
+                    const int k = c0 + __ffs(col) - 1;
+                    col &= col - 1;
+                    const float4 a = s_a[k];
+                    const float4 b = s_b[k];
+                    const float cz = s_c[k].x;
+                    const float dx = __fsub_rn(pm.fx, a.x);
+                    const float dy = __fsub_rn(pm.fy, a.y);
+                    const float G = splat_gauss(a.z, a.w, b.x, dx, dy);
+                    const float sigma = __fmul_rn(b.y, G);
+                    const float w = __fmul_rn(sigma, T);
+                    C0 = __fmaf_rn(w, b.z, C0);
+                    C1 = __fmaf_rn(w, b.w, C1);
+                    C2 = __fmaf_rn(w, cz, C2);
+                    T = __fmul_rn(T, __fsub_rn(1.0f, sigma));
+                    ++ops;
+                    last = (uint32_t)(bstart + k + 1);
+                    if (T < kTermT) {
+                        done = true;
+                        col = 0;
+                    }
+                }
+            }
+            if (__all_sync(kFull, done)) {
+                warp_done = true;
+                break;
+            }
+        }
+    }
+
+    float lsum = 0.f;
+    if (pm.valid) {
+        C0 = __fmaf_rn(T, prm.bg0, C0);
+        C1 = __fmaf_rn(T, prm.bg1, C1);
+        C2 = __fmaf_rn(T, prm.bg2, C2);
+        const int r = pm.rank;
+        if (prm.rgb) {
+            prm.rgb[3 * r] = C0;
+            prm.rgb[3 * r + 1] = C1;
+            prm.rgb[3 * r + 2] = C2;
+        }
+        prm.T[r] = T;
+        prm.last[r] = last;
+        if (prm.target) {
+            const float* t = prm.target + 3 * ((int64_t)pm.y * prm.W + pm.x);
+            const float d0 = C0 - t[0], d1 = C1 - t[1], d2 = C2 - t[2];
+            lsum = fabsf(d0) + fabsf(d1) + fabsf(d2);
+            const float s = prm.loss_scale;
+            prm.dLdC[3 * r] = d0 > 0.f ? s : (d0 < 0.f ? -s : 0.f);
+            prm.dLdC[3 * r + 1] = d1 > 0.f ? s : (d1 < 0.f ? -s : 0.f);
+            prm.dLdC[3 * r + 2] = d2 > 0.f ? s : (d2 < 0.f ? -s : 0.f);
+        }
+    }
+    unsigned long long o = ops;
+    unsigned long long ev = pm.valid ? (done ? last : (uint32_t)count) : 0u;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        o += __shfl_xor_sync(kFull, o, s);
+        ev += __shfl_xor_sync(kFull, ev, s);
+        lsum += __shfl_xor_sync(kFull, lsum, s);
+    }
+    if (lane == 0) {
+        s_red[0][warp] = o;
+        s_red[1][warp] = ev;
+        s_loss[warp] = lsum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long to = 0, te = 0;
+        float tl = 0.f;
+        for (int w = 0; w < NW; ++w) {
+            to += s_red[0][w];
+            te += s_red[1][w];
+            tl += s_loss[w];
+        }
+        if (to) atomicAdd(&prm.counters[1], to);
+        if (te) atomicAdd(&prm.counters[2], te);
+        if (prm.block_loss) prm.block_loss[tile] = tl;
+    }
+}
+
+// ------------------------------------------------------------------------------ backward
+__device__ __forceinline__ uint32_t pair_slot(const Prepared& P, int tx, int ty) {
+    const uint4 d = P.d;
+    const int tx0 = d.x & 0xffff, tx1 = d.x >> 16, ty0 = d.y & 0xffff;
+    return d.z + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
+}
+
+template <int NW, int BATCH>
+struct BwdSmem {
+    float4 a[BATCH];
+    float4 b[BATCH];
+    float2 c[BATCH];
+    uint32_t slot[BATCH];
+    uint32_t touch[BATCH];           // bit w: warp w wrote part[w][j]
+    float part[NW][BATCH][10];       // per-warp partials: 9 grads + visited
+    float rec_w[NW][32 * 33];        // phase-1 records [splat][pixel], padded rows
+    float rec_ds[NW][32 * 33];
+    float4 g[NW][32];                // per-pixel dL/dC
+};
+
+template <int NWX, int NWY, int BATCH>
+__global__ void __launch_bounds__(NWX * NWY * 32) backward_kernel(BlendParams prm) {
+    constexpr int NW = NWX * NWY, NT = NW * 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& S = *reinterpret_cast<BwdSmem<NW, BATCH>*>(smem_raw);
+    __shared__ uint32_t s_maxlast;
+
+    const int tile = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    PixelMap<NWX> pm;
+    pm.init(prm, tile);
+    const PixelMap<1> geo = tile_geom(pm);
+    const uint2 range = prm.ranges[tile];
+    const int count = (int)(range.y - range.x);
+    const int p = prm.p;
+
+    float T = 1.f, S0 = 0.f, S1 = 0.f, S2 = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
+    uint32_t last = 0;
+    if (pm.valid) {
+        T = prm.T[pm.rank];
+        last = prm.last[pm.rank];
+        g0 = prm.dLdC[3 * pm.rank];
+        g1 = prm.dLdC[3 * pm.rank + 1];
+        g2 = prm.dLdC[3 * pm.rank + 2];
+        // Vec3 suffix = background * trans_final (rasterizer.cpp:267)
+        S0 = __fmul_rn(prm.bg0, T);
+        S1 = __fmul_rn(prm.bg1, T);
+        S2 = __fmul_rn(prm.bg2, T);
+    }
+    S.g[warp][lane] = make_float4(g0, g1, g2, 0.f);
+    const uint32_t wlast = __reduce_max_sync(kFull, last);
+    if (threadIdx.x == 0) s_maxlast = 0;
+    __syncthreads();
+    if (lane == 0) atomicMax(&s_maxlast, wlast);
+    __syncthreads();
+    const int maxlast = (int)s_maxlast;
+    // pixel centre of lane l of this warp's block (phase 2)
+    const int bx0 = pm.ax + pm.bx * 8 * p, by0 = pm.ay + pm.by * 4 * p;
+
+    // list entries past every pixel's last contributor: zero partials
+    for (int j = maxlast + threadIdx.x; j < count; j += NT) {
+        const uint32_t slot = pair_slot(prm.prep[prm.items[range.x + j]], pm.tx, pm.ty);
+        float4* dst = prm.partial + 3 * (size_t)slot;
+        dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dst[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+
+    float* rec_w = S.rec_w[warp];
+    float* rec_ds = S.rec_ds[warp];
+    const int nb = (maxlast + BATCH - 1) / BATCH;
+    for (int b = nb - 1; b >= 0; --b) {
+        const int bstart = b * BATCH;
+        const int bcount = min(BATCH, maxlast - bstart);
+        __syncthreads();
+        for (int j = threadIdx.x; j < bcount; j += NT) {
+            const uint32_t rank = prm.items[range.x + bstart + j];
+            float4 a, bb;
+            float2 c;
+            stage_splat(prm, rank, geo, p, a, bb, c);
+            S.a[j] = a;
+            S.b[j] = bb;
+            S.c[j] = c;
+            S.slot[j] = pair_slot(prm.prep[rank], pm.tx, pm.ty);
+            S.touch[j] = 0u;
+        }
+        __syncthreads();
+        if (wlast > (uint32_t)bstart) {
+            const int nch = (bcount + 31) / 32;
+            for (int ch = nch - 1; ch >= 0; --ch) {
+                const int c0 = ch * 32;
+                const int cb = bstart + c0;
+                if (wlast <= (uint32_t)cb) continue;
+                const int j = c0 + lane;
+                const uint32_t row = j < bcount ? warp_rowmask(__float_as_uint(S.c[j].y), pm.bx, pm.by) : 0u;
+                uint32_t col = transpose32(row);
+                // only splats before this pixel's last contributor were blended
+                const int span = (int)last - cb;
+                col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
+                uint32_t contrib = col, visb = 0;
+                // phase 1: per pixel, back to front
+                while (__any_sync(kFull, col)) {
+                    if (col) {
+                        const int jj = 31 - __clz(col);
+                        col &= ~(1u << jj);
+                        const int k = c0 + jj;
+                        const float4 a = S.a[k];
+                        const float4 bb = S.b[k];
+                        const float cz = S.c[k].x;
+                        const float dx = __fsub_rn(pm.fx, a.x);
+                        const float dy = __fsub_rn(pm.fy, a.y);
+                        const float G = splat_gauss(a.z, a.w, bb.x, dx, dy);
+                        const float sigma = __fmul_rn(bb.y, G);
+                        const float ir = __frcp_rn(__fsub_rn(1.0f, sigma));  // inv_rest
+                        const float Ti = __fmul_rn(T, ir);
+                        const float w = __fmul_rn(sigma, Ti);
+                        // dC/dsigma_i = T_i c_i - S_i / (1 - sigma_i)   (rasterizer.cpp:272-275)
+                        const float dsig = g0 * (bb.z * Ti - S0 * ir) + g1 * (bb.w * Ti - S1 * ir) +
+                                           g2 * (cz * Ti - S2 * ir);
+                        S0 = __fmaf_rn(bb.z, w, S0);
+                        S1 = __fmaf_rn(bb.w, w, S1);
+                        S2 = __fmaf_rn(cz, w, S2);
+                        T = Ti;
+                        rec_w[jj * 33 + lane] = w;
+                        rec_ds[jj * 33 + lane] = dsig;
+                        if (w > kMinVisitW) visb |= 1u << jj;
+                    }
+                }
+                const uint32_t vism = __reduce_or_sync(kFull, visb);
+                uint32_t rows = transpose32(contrib);
+                __syncwarp();
+                // phase 2: lane = splat j, over its contributing pixels (rasterizer.cpp:271-285)
+                if (rows) {
+                    const float4 a = S.a[j];
+                    const float4 bb = S.b[j];
+                    const float i01 = 0.5f * a.w;
+                    float acc[9];
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) acc[q] = 0.f;
+                    do {
+                        const int l = __ffs(rows) - 1;
+                        rows &= rows - 1;
+                        const float w = rec_w[lane * 33 + l];
+                        const float ds = rec_ds[lane * 33 + l];
+                        const float4 gl = S.g[warp][l];
+                        const float px = __fadd_rn((float)(bx0 + (l & 7) * p), 0.5f);
+                        const float py = __fadd_rn((float)(by0 + (l >> 3) * p), 0.5f);
+                        const float dx = __fsub_rn(px, a.x);
+                        const float dy = __fsub_rn(py, a.y);
+                        const float G = splat_gauss(a.z, a.w, bb.x, dx, dy);
+                        acc[6] = __fmaf_rn(gl.x, w, acc[6]);
+                        acc[7] = __fmaf_rn(gl.y, w, acc[7]);
+                        acc[8] = __fmaf_rn(gl.z, w, acc[8]);
+                        acc[5] = __fmaf_rn(ds, G, acc[5]);
+                        const float dq = ds * bb.y * -0.5f * G;
+                        const float adx = a.z * dx + i01 * dy;
+                        const float ady = i01 * dx + bb.x * dy;
+                        acc[0] = __fmaf_rn(-2.0f * dq, adx, acc[0]);
+                        acc[1] = __fmaf_rn(-2.0f * dq, ady, acc[1]);
+                        const float ndqx = -dq * adx;
+                        acc[2] = __fmaf_rn(ndqx, adx, acc[2]);
+                        acc[3] = __fmaf_rn(ndqx, ady, acc[3]);
+                        acc[4] = __fmaf_rn(-dq * ady, ady, acc[4]);
+                    } while (rows);
+                    float* dst = S.part[warp][j];
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) dst[q] = acc[q];
+                    dst[9] = ((vism >> lane) & 1u) ? 1.0f : 0.0f;
+                    atomicOr(&S.touch[j], 1u << warp);
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        // fixed-order cross-warp combine, one write per (tile, splat) pair slot
+        for (int j = threadIdx.x; j < bcount; j += NT) {
+            float acc[10];
+#pragma unroll
+            for (int k = 0; k < 10; ++k) acc[k] = 0.f;
+            const uint32_t touch = S.touch[j];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                if (touch & (1u << w)) {
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) acc[k] += S.part[w][j][k];
+                    acc[9] = fmaxf(acc[9], S.part[w][j][9]);
+                }
+            }
+            float4* dst = prm.partial + 3 * (size_t)S.slot[j];
+            dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            dst[2] = make_float4(acc[8], acc[9], 0.f, 0.f);
+        }
+    }
+}
+
+BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items) {
+    Workspace& ws = ctx->ws;
+    BlendParams prm{};
+    prm.ranges = ws.ranges.as<uint2>();
+    prm.items = items;
+    prm.prep = ws.prep.as<Prepared>();
+    prm.tiles_x = ws.tiles_x;
+    prm.p = ra.p;
+    prm.ox = ra.ox;
+    prm.oy = ra.oy;
+    prm.W = ra.W;
+    prm.H = ra.H;
+    prm.cols = ra.cols;
+    prm.bg0 = ra.bg[0];
+    prm.bg1 = ra.bg[1];
+    prm.bg2 = ra.bg[2];
+    prm.rgb = ws.rgb.as<float>();
+    prm.T = ws.T.as<float>();
+    prm.last = ws.last.as<uint32_t>();
+    prm.counters = ws.counters.as<unsigned long long>();
+    prm.dLdC = ws.dLdC.as<float>();
+    prm.block_loss = ws.block_loss.as<float>();
+    prm.partial = ws.partial.as<float4>();
+    return prm;
+}
+
+template <int NWX, int NWY, int BATCH>
+cudaError_t run_backward(tgsx_ctx* ctx, const BlendParams& prm, unsigned tiles) {
+    constexpr int NT = NWX * NWY * 32;
+    const size_t smem = sizeof(BwdSmem<NWX * NWY, BATCH>);
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(backward_kernel<NWX, NWY, BATCH>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e) return e;
+        configured = true;
+    }
+    backward_kernel<NWX, NWY, BATCH><<<tiles, NT, smem, ctx->stream>>>(prm);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
+                           bool fused_loss) {
+    Workspace& ws = ctx->ws;
+    BlendParams prm = make_params(ctx, ra, items);
+    if (fused_loss) {
+        prm.target = ra.target;
+        prm.loss_scale = ra.P > 0 ? (float)(1.0 / (3.0 * (double)ra.P)) : 0.f;
+    } else {
+        prm.target = nullptr;
+        prm.block_loss = nullptr;
+    }
+    const unsigned tiles = (unsigned)(ws.tiles_x * ws.tiles_y);
+    if (ra.p == 1) {
+        forward_kernel<2, 4, 256><<<tiles, 256, 0, ctx->stream>>>(prm);
+    } else if (ra.p <= 3) {
+        forward_kernel<1, 2, 128><<<tiles, 64, 0, ctx->stream>>>(prm);
+    } else {
+        forward_kernel<1, 1, 128><<<tiles, 32, 0, ctx->stream>>>(prm);
+    }
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items) {
+    Workspace& ws = ctx->ws;
+    BlendParams prm = make_params(ctx, ra, items);
+    const unsigned tiles = (unsigned)(ws.tiles_x * ws.tiles_y);
+    cudaError_t e;
+    if (ra.p == 1) {
+        e = run_backward<2, 4, 32>(ctx, prm, tiles);
+    } else if (ra.p <= 3) {
+        e = run_backward<1, 2, 64>(ctx, prm, tiles);
+    } else {
+        e = run_backward<1, 1, 64>(ctx, prm, tiles);
+    }
+    ctx->launches++;
+    return e;
+}
+
+}  // namespace tgsx
