@@ -2,29 +2,33 @@
 //
 // Work decomposition: one CTA per 16x16 tile; each warp owns an 8x4 block of ACTIVE pixels
 // (for the dilated variant the block spans 8p x 4p image pixels, so the same kernels serve
-// p = 1 and the paper's 4K dilated rendering). Splat batches are staged in shared memory with
-// exact per-tile box-test masks (rasterizer.cpp:116-118 evaluated once per (tile, splat) in
-// float, per active column / row).
+// p = 1 and the paper's 4K dilated rendering). Splat batches are staged in shared memory
+// (48-byte records) with exact per-tile box-test masks (rasterizer.cpp:116-118 evaluated once
+// per (tile, splat) in float, per active column / row).
 //
 // Per 32-splat chunk a warp builds the 32x32 (splat x pixel) pass matrix: lane j turns splat
 // j's column/row masks into a 32-bit row with one multiply, a 5-stage shuffle bit-transpose
 // hands lane l the column "which of these 32 splats pass my pixel". Each lane then walks only
 // its own passing splats with ffs (forward, front to back) or clz (backward, back to front).
 // This replaces the reference's per-pixel walk over the whole list (walk_pixel,
-// rasterizer.cpp:108-136) without changing a single blended term: the order per pixel is the
-// list order, box-failing splats contribute nothing in the reference either.
+// rasterizer.cpp:108-136) without changing a blended term: per pixel the order is the list
+// order, and box-failing splats contribute nothing in the reference either.
 //
 // forward_kernel: walk_pixel + render (rasterizer.cpp:144-184), optional fused L1 epilogue
 //   (SPEC.md:562-570). Records per pixel the final T and the last blended list position.
-// backward_kernel: backward tile phase (rasterizer.cpp:234-292) in two phases per chunk:
+// backward_kernel: backward tile phase (rasterizer.cpp:234-292), two phases per chunk:
 //   1. per pixel, back to front: T_i = T_{i+1} / (1 - sigma_i) with sigma recomputed
-//      bit-identically to the forward, the reference's exact suffix S (rasterizer.cpp:266-287),
-//      dL/dsigma; (w, dL/dsigma) recorded per (splat, pixel) in shared memory;
-//   2. per splat (lane j = splat j), over its contributing pixels: the gradient terms of
-//      rasterizer.cpp:271-285 accumulated in registers — no cross-lane reductions.
-//   Warp partials are combined across warps in a fixed order and written once per (tile,
-//   splat) pair slot (no global atomics, deterministic; merged per Gaussian in optim.cu in
-//   tile order like rasterizer.cpp:301-319).
+//      bit-identically to the forward; dL/dsigma_i = T_i (g.c_i) - (g.S_i)/(1 - sigma_i) with
+//      the reference's exact suffix S_i (rasterizer.cpp:266-287) carried as the scalar g.S;
+//      records u = dL/dsigma * G and the blend weight w per (splat, pixel) in shared memory.
+//   2. per splat (lane j), dense over the warp's 32 pixels: every position / covariance
+//      gradient of rasterizer.cpp:276-285 is linear in the moments sum(u), sum(u dx),
+//      sum(u dy), sum(u dx^2), sum(u dx dy), sum(u dy^2) and the colour gradient is sum(g w);
+//      with pixel offsets fixed per lane these are FFMA-with-immediate sums — no divergence,
+//      no cross-lane reductions. The moments are turned into the 9 screen-space gradients
+//      per (warp, splat), combined across warps in a fixed order and written once per
+//      (tile, splat) pair slot (no global atomics, deterministic; merged per Gaussian in
+//      optim.cu in tile order like rasterizer.cpp:301-319).
 #include "tgsx_device.cuh"
 #include "tgsx_internal.h"
 
@@ -35,6 +39,7 @@ namespace tgsx {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kRec = 48;  // bytes per staged splat record
 
 struct BlendParams {
     const uint2* ranges;
@@ -53,17 +58,16 @@ struct BlendParams {
     float4* partial;               // backward output, 3 float4 per pair slot
 };
 
-// Per-lane pixel of the CTA's tile, in active coordinates.
+// Tile geometry + this lane's pixel, in active coordinates.
 template <int NWX>
 struct PixelMap {
-    int tx, ty, x0, y0, ax, ay, acols, arows, bx, by, x, y, rank;
+    int tx, ty, ax, ay, acols, arows, bx, by, x, y, rank;
     float fx, fy;
     bool valid;
     __device__ __forceinline__ void init(const BlendParams& prm, int tile) {
         tx = tile % prm.tiles_x;
         ty = tile / prm.tiles_x;
-        x0 = tx * kTile;
-        y0 = ty * kTile;
+        const int x0 = tx * kTile, y0 = ty * kTile;
         const int px1 = min(prm.W, x0 + kTile), py1 = min(prm.H, y0 + kTile);
         ax = first_active(x0, prm.ox, prm.p);
         ay = first_active(y0, prm.oy, prm.p);
@@ -95,7 +99,7 @@ __device__ __forceinline__ uint32_t box_mask(float m, float r, int a0, int p, in
     return mask;
 }
 
-// Row of the warp's 8x4 pixel block passing a splat: bit l = (l&7, l>>3).
+// Row of the warp's 8x4 pixel block passing a splat: bit l <-> pixel (l&7, l>>3).
 __device__ __forceinline__ uint32_t warp_rowmask(uint32_t mask, int bx, int by) {
     const uint32_t xb = (mask >> (bx * 8)) & 0xffu;
     const uint32_t yb = (mask >> (16 + by * 4)) & 0xfu;
@@ -117,35 +121,27 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t v) {
     return v;
 }
 
+// Stages one prepared splat as a 48-byte record:
+//   +0 (mean x, mean y, ka, kb)  +16 (kc, alpha, r, g)  +32 (b, mask bits)
+// (ka, kb, kc) = (inv00, 2 inv01, inv11) * kNegHalfLog2e; mask = active cols | rows << 16.
+template <int NWX>
 __device__ __forceinline__ void stage_splat(const BlendParams& prm, uint32_t rank,
-                                            const PixelMap<1>& g, int p, float4& sa, float4& sb,
-                                            float2& sc) {
+                                            const PixelMap<NWX>& g, uint32_t dst) {
     const Prepared& P = prm.prep[rank];
     const float4 a = P.a, b = P.b, c = P.c;
-    const uint32_t mask = box_mask(a.x, b.z, g.ax, p, g.acols) |
-                          (box_mask(a.y, b.w, g.ay, p, g.arows) << 16);
-    sa = make_float4(a.x, a.y, a.z, a.w * 2.0f);
-    sb = make_float4(b.x, b.y, c.x, c.y);
-    sc = make_float2(c.z, __uint_as_float(mask));
-}
-
-template <int NWX>
-__device__ __forceinline__ PixelMap<1> tile_geom(const PixelMap<NWX>& pm) {
-    PixelMap<1> g;
-    g.ax = pm.ax;
-    g.ay = pm.ay;
-    g.acols = pm.acols;
-    g.arows = pm.arows;
-    return g;
+    const uint32_t mask = box_mask(a.x, b.z, g.ax, prm.p, g.acols) |
+                          (box_mask(a.y, b.w, g.ay, prm.p, g.arows) << 16);
+    sts_f4(dst, make_float4(a.x, a.y, __fmul_rn(a.z, kNegHalfLog2e),
+                            __fmul_rn(a.w * 2.0f, kNegHalfLog2e)));
+    sts_f4(dst + 16, make_float4(__fmul_rn(b.x, kNegHalfLog2e), b.y, c.x, c.y));
+    sts_f4(dst + 32, make_float4(c.z, __uint_as_float(mask), 0.f, 0.f));
 }
 
 // ------------------------------------------------------------------------------- forward
 template <int NWX, int NWY, int BATCH>
 __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm) {
     constexpr int NW = NWX * NWY, NT = NW * 32;
-    __shared__ float4 s_a[BATCH];
-    __shared__ float4 s_b[BATCH];
-    __shared__ float2 s_c[BATCH];
+    __shared__ __align__(16) unsigned char s_rec[BATCH * kRec];
     __shared__ unsigned long long s_red[2][NW];
     __shared__ float s_loss[NW];
 
@@ -153,9 +149,9 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     PixelMap<NWX> pm;
     pm.init(prm, tile);
-    const PixelMap<1> geo = tile_geom(pm);
     const uint2 range = prm.ranges[tile];
     const int count = (int)(range.y - range.x);
+    const uint32_t sbase = smem_addr(s_rec);
 
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
     uint32_t last = 0, ops = 0;
@@ -165,31 +161,27 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
     for (int bstart = 0; bstart < count; bstart += BATCH) {
         if (__syncthreads_and(warp_done)) break;
         const int bcount = min(BATCH, count - bstart);
-        for (int j = threadIdx.x; j < bcount; j += NT) {
-            float4 a, b;
-            float2 c;
-            stage_splat(prm, prm.items[range.x + bstart + j], geo, prm.p, a, b, c);
-            s_a[j] = a;
-            s_b[j] = b;
-            s_c[j] = c;
-        }
+        for (int j = threadIdx.x; j < bcount; j += NT)
+            stage_splat(prm, prm.items[range.x + bstart + j], pm, sbase + j * kRec);
         __syncthreads();
         if (warp_done) continue;
         for (int c0 = 0; c0 < bcount; c0 += 32) {
             const int j = c0 + lane;
-            const uint32_t row = j < bcount ? warp_rowmask(__float_as_uint(s_c[j].y), pm.bx, pm.by) : 0u;
+            const uint32_t row =
+                j < bcount ? warp_rowmask(__float_as_uint(lds_f1(sbase + j * kRec + 36)), pm.bx, pm.by) : 0u;
             uint32_t col = transpose32(row);
             if (done) col = 0;
+            const uint32_t cbase = sbase + c0 * kRec;
+            const uint32_t lbase = (uint32_t)(bstart + c0 + 1);
             while (__any_sync(kFull, col)) {
                 if (col) {
-                    const int k = c0 + __ffs(col) - 1;
+                    const int k = __ffs(col) - 1;
                     col &= col - 1;
-                    const float4 a = s_a[k];
-                    const float4 b = s_b[k];
-                    const float cz = s_c[k].x;
-                    const float dx = __fsub_rn(pm.fx, a.x);
-                    const float dy = __fsub_rn(pm.fy, a.y);
-                    const float G = splat_gauss(a.z, a.w, b.x, dx, dy);
+                    const uint32_t ad = cbase + k * kRec;
+                    const float4 a = lds_f4(ad);
+                    const float4 b = lds_f4(ad + 16);
+                    const float cz = lds_f1(ad + 32);
+                    const float G = conic_gauss(a.z, a.w, b.x, __fsub_rn(pm.fx, a.x), __fsub_rn(pm.fy, a.y));
                     const float sigma = __fmul_rn(b.y, G);
                     const float w = __fmul_rn(sigma, T);
                     C0 = __fmaf_rn(w, b.z, C0);
@@ -197,7 +189,7 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
                     C2 = __fmaf_rn(w, cz, C2);
                     T = __fmul_rn(T, __fsub_rn(1.0f, sigma));
                     ++ops;
-                    last = (uint32_t)(bstart + k + 1);
+                    last = lbase + k;
                     if (T < kTermT) {
                         done = true;
                         col = 0;
@@ -269,17 +261,17 @@ __device__ __forceinline__ uint32_t pair_slot(const Prepared& P, int tx, int ty)
     return d.z + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
 }
 
+constexpr int kRecStride = 33;  // floats per (splat) row of the phase-1 records (bank skew)
+
 template <int NW, int BATCH>
 struct BwdSmem {
-    float4 a[BATCH];
-    float4 b[BATCH];
-    float2 c[BATCH];
+    unsigned char rec[BATCH * kRec];
     uint32_t slot[BATCH];
-    uint32_t touch[BATCH];           // bit w: warp w wrote part[w][j]
-    float part[NW][BATCH][10];       // per-warp partials: 9 grads + visited
-    float rec_w[NW][32 * 33];        // phase-1 records [splat][pixel], padded rows
-    float rec_ds[NW][32 * 33];
-    float4 g[NW][32];                // per-pixel dL/dC
+    uint32_t touch[BATCH];                 // bit w: warp w wrote part[w][j]
+    float part[NW][BATCH][10];             // per-warp partials: 9 grads + visited
+    float rec_u[NW][32 * kRecStride + 4];  // phase-1 records [splat][pixel]
+    float rec_w[NW][32 * kRecStride + 4];
+    float4 g[NW][32];                      // per-pixel dL/dC
 };
 
 template <int NWX, int NWY, int BATCH>
@@ -293,12 +285,14 @@ __global__ void __launch_bounds__(NWX * NWY * 32) backward_kernel(BlendParams pr
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     PixelMap<NWX> pm;
     pm.init(prm, tile);
-    const PixelMap<1> geo = tile_geom(pm);
     const uint2 range = prm.ranges[tile];
     const int count = (int)(range.y - range.x);
     const int p = prm.p;
+    const uint32_t rbase = smem_addr(S.rec);
+    const uint32_t ubase = smem_addr(S.rec_u[warp]);
+    const uint32_t wbase = smem_addr(S.rec_w[warp]);
 
-    float T = 1.f, S0 = 0.f, S1 = 0.f, S2 = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
+    float T = 1.f, gS = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
     uint32_t last = 0;
     if (pm.valid) {
         T = prm.T[pm.rank];
@@ -306,10 +300,8 @@ __global__ void __launch_bounds__(NWX * NWY * 32) backward_kernel(BlendParams pr
         g0 = prm.dLdC[3 * pm.rank];
         g1 = prm.dLdC[3 * pm.rank + 1];
         g2 = prm.dLdC[3 * pm.rank + 2];
-        // Vec3 suffix = background * trans_final (rasterizer.cpp:267)
-        S0 = __fmul_rn(prm.bg0, T);
-        S1 = __fmul_rn(prm.bg1, T);
-        S2 = __fmul_rn(prm.bg2, T);
+        // g . S with S = background * trans_final (rasterizer.cpp:267)
+        gS = g0 * (prm.bg0 * T) + g1 * (prm.bg1 * T) + g2 * (prm.bg2 * T);
     }
     S.g[warp][lane] = make_float4(g0, g1, g2, 0.f);
     const uint32_t wlast = __reduce_max_sync(kFull, last);
@@ -318,8 +310,11 @@ __global__ void __launch_bounds__(NWX * NWY * 32) backward_kernel(BlendParams pr
     if (lane == 0) atomicMax(&s_maxlast, wlast);
     __syncthreads();
     const int maxlast = (int)s_maxlast;
-    // pixel centre of lane l of this warp's block (phase 2)
-    const int bx0 = pm.ax + pm.bx * 8 * p, by0 = pm.ay + pm.by * 4 * p;
+    // block centre (pixel-centre coordinates) for the phase-2 moments: pixel l of this warp is
+    // at (cx + ((l&7) - 3.5) p, cy + ((l>>3) - 1.5) p)
+    const float cx = (float)(pm.ax + pm.bx * 8 * p) + 0.5f + 3.5f * (float)p;
+    const float cy = (float)(pm.ay + pm.by * 4 * p) + 0.5f + 1.5f * (float)p;
+    const float fp = (float)p;
 
     // list entries past every pixel's last contributor: zero partials
     for (int j = maxlast + threadIdx.x; j < count; j += NT) {
@@ -330,8 +325,6 @@ __global__ void __launch_bounds__(NWX * NWY * 32) backward_kernel(BlendParams pr
         dst[2] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
-    float* rec_w = S.rec_w[warp];
-    float* rec_ds = S.rec_ds[warp];
     const int nb = (maxlast + BATCH - 1) / BATCH;
     for (int b = nb - 1; b >= 0; --b) {
         const int bstart = b * BATCH;
@@ -339,12 +332,7 @@ __global__ void __launch_bounds__(NWX * NWY * 32) backward_kernel(BlendParams pr
         __syncthreads();
         for (int j = threadIdx.x; j < bcount; j += NT) {
             const uint32_t rank = prm.items[range.x + bstart + j];
-            float4 a, bb;
-            float2 c;
-            stage_splat(prm, rank, geo, p, a, bb, c);
-            S.a[j] = a;
-            S.b[j] = bb;
-            S.c[j] = c;
+            stage_splat(prm, rank, pm, rbase + j * kRec);
             S.slot[j] = pair_slot(prm.prep[rank], pm.tx, pm.ty);
             S.touch[j] = 0u;
         }
@@ -356,79 +344,96 @@ __global__ void __launch_bounds__(NWX * NWY * 32) backward_kernel(BlendParams pr
                 const int cb = bstart + c0;
                 if (wlast <= (uint32_t)cb) continue;
                 const int j = c0 + lane;
-                const uint32_t row = j < bcount ? warp_rowmask(__float_as_uint(S.c[j].y), pm.bx, pm.by) : 0u;
+                const uint32_t row =
+                    j < bcount ? warp_rowmask(__float_as_uint(lds_f1(rbase + j * kRec + 36)), pm.bx, pm.by) : 0u;
                 uint32_t col = transpose32(row);
                 // only splats before this pixel's last contributor were blended
                 const int span = (int)last - cb;
                 col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
-                uint32_t contrib = col, visb = 0;
+                // zero this warp's records (contiguous; 16-B stores)
+                for (int q = lane; q < (32 * kRecStride + 4) / 4; q += 32) {
+                    sts_f4(ubase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
+                    sts_f4(wbase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
+                }
+                __syncwarp();
+                uint32_t visb = 0;
+                const uint32_t cbase = rbase + c0 * kRec;
                 // phase 1: per pixel, back to front
                 while (__any_sync(kFull, col)) {
                     if (col) {
-                        const int jj = 31 - __clz(col);
-                        col &= ~(1u << jj);
-                        const int k = c0 + jj;
-                        const float4 a = S.a[k];
-                        const float4 bb = S.b[k];
-                        const float cz = S.c[k].x;
-                        const float dx = __fsub_rn(pm.fx, a.x);
-                        const float dy = __fsub_rn(pm.fy, a.y);
-                        const float G = splat_gauss(a.z, a.w, bb.x, dx, dy);
+                        const int k = 31 - __clz(col);
+                        col ^= 1u << k;
+                        const uint32_t ad = cbase + k * kRec;
+                        const float4 a = lds_f4(ad);
+                        const float4 bb = lds_f4(ad + 16);
+                        const float cz = lds_f1(ad + 32);
+                        const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(pm.fx, a.x), __fsub_rn(pm.fy, a.y));
                         const float sigma = __fmul_rn(bb.y, G);
-                        const float ir = __frcp_rn(__fsub_rn(1.0f, sigma));  // inv_rest
-                        const float Ti = __fmul_rn(T, ir);
-                        const float w = __fmul_rn(sigma, Ti);
-                        // dC/dsigma_i = T_i c_i - S_i / (1 - sigma_i)   (rasterizer.cpp:272-275)
-                        const float dsig = g0 * (bb.z * Ti - S0 * ir) + g1 * (bb.w * Ti - S1 * ir) +
-                                           g2 * (cz * Ti - S2 * ir);
-                        S0 = __fmaf_rn(bb.z, w, S0);
-                        S1 = __fmaf_rn(bb.w, w, S1);
-                        S2 = __fmaf_rn(cz, w, S2);
+                        const float ir = fast_rcp(__fsub_rn(1.0f, sigma));  // inv_rest
+                        const float Ti = T * ir;
+                        const float w = sigma * Ti;
+                        const float gc = g0 * bb.z + g1 * bb.w + g2 * cz;
+                        // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
+                        const float dsig = Ti * gc - gS * ir;
+                        gS = __fmaf_rn(gc, w, gS);
                         T = Ti;
-                        rec_w[jj * 33 + lane] = w;
-                        rec_ds[jj * 33 + lane] = dsig;
-                        if (w > kMinVisitW) visb |= 1u << jj;
+                        const uint32_t o = 4u * (uint32_t)(k * kRecStride + lane);
+                        sts_f1(ubase + o, dsig * G);
+                        sts_f1(wbase + o, w);
+                        if (w > kMinVisitW) visb |= 1u << k;
                     }
                 }
                 const uint32_t vism = __reduce_or_sync(kFull, visb);
-                uint32_t rows = transpose32(contrib);
                 __syncwarp();
-                // phase 2: lane = splat j, over its contributing pixels (rasterizer.cpp:271-285)
-                if (rows) {
-                    const float4 a = S.a[j];
-                    const float4 bb = S.b[j];
-                    const float i01 = 0.5f * a.w;
-                    float acc[9];
+                // phase 2: lane = splat j, dense over the warp's 32 pixels
+                float m0 = 0.f, mx1 = 0.f, my1 = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
+                float q0 = 0.f, q1 = 0.f, q2 = 0.f;
+                const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
+                const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
+                const uint32_t gb = smem_addr(S.g[warp]);
 #pragma unroll
-                    for (int q = 0; q < 9; ++q) acc[q] = 0.f;
-                    do {
-                        const int l = __ffs(rows) - 1;
-                        rows &= rows - 1;
-                        const float w = rec_w[lane * 33 + l];
-                        const float ds = rec_ds[lane * 33 + l];
-                        const float4 gl = S.g[warp][l];
-                        const float px = __fadd_rn((float)(bx0 + (l & 7) * p), 0.5f);
-                        const float py = __fadd_rn((float)(by0 + (l >> 3) * p), 0.5f);
-                        const float dx = __fsub_rn(px, a.x);
-                        const float dy = __fsub_rn(py, a.y);
-                        const float G = splat_gauss(a.z, a.w, bb.x, dx, dy);
-                        acc[6] = __fmaf_rn(gl.x, w, acc[6]);
-                        acc[7] = __fmaf_rn(gl.y, w, acc[7]);
-                        acc[8] = __fmaf_rn(gl.z, w, acc[8]);
-                        acc[5] = __fmaf_rn(ds, G, acc[5]);
-                        const float dq = ds * bb.y * -0.5f * G;
-                        const float adx = a.z * dx + i01 * dy;
-                        const float ady = i01 * dx + bb.x * dy;
-                        acc[0] = __fmaf_rn(-2.0f * dq, adx, acc[0]);
-                        acc[1] = __fmaf_rn(-2.0f * dq, ady, acc[1]);
-                        const float ndqx = -dq * adx;
-                        acc[2] = __fmaf_rn(ndqx, adx, acc[2]);
-                        acc[3] = __fmaf_rn(ndqx, ady, acc[3]);
-                        acc[4] = __fmaf_rn(-dq * ady, ady, acc[4]);
-                    } while (rows);
+                for (int l = 0; l < 32; ++l) {
+                    const float xi = (float)(l & 7) - 3.5f;
+                    const float eta = (float)(l >> 3) - 1.5f;
+                    const float u = lds_f1(ur + 4 * l);
+                    const float w = lds_f1(wr + 4 * l);
+                    const float4 gl = lds_f4(gb + 16 * l);
+                    m0 += u;
+                    mx1 = __fmaf_rn(u, xi, mx1);
+                    my1 = __fmaf_rn(u, eta, my1);
+                    mxx = __fmaf_rn(u, xi * xi, mxx);
+                    mxy = __fmaf_rn(u, xi * eta, mxy);
+                    myy = __fmaf_rn(u, eta * eta, myy);
+                    q0 = __fmaf_rn(w, gl.x, q0);
+                    q1 = __fmaf_rn(w, gl.y, q1);
+                    q2 = __fmaf_rn(w, gl.z, q2);
+                }
+                if (j < bcount && (m0 != 0.f || q0 != 0.f || q1 != 0.f || q2 != 0.f || mxx != 0.f ||
+                                   ((vism >> lane) & 1u))) {
+                    const float4 a = lds_f4(rbase + j * kRec);
+                    const float4 bb = lds_f4(rbase + j * kRec + 16);
+                    const float iK = 1.0f / kNegHalfLog2e;
+                    const float ia = a.z * iK, ib = 0.5f * a.w * iK, ic = bb.x * iK;
+                    const float al = bb.y;
+                    // moments about the splat mean: dx = p xi - mxb, dy = p eta - myb
+                    const float mxb = a.x - cx, myb = a.y - cy;
+                    const float sdx = fp * mx1 - mxb * m0;
+                    const float sdy = fp * my1 - myb * m0;
+                    const float sxx = fp * fp * mxx - 2.f * fp * mxb * mx1 + mxb * mxb * m0;
+                    const float sxy = fp * fp * mxy - fp * myb * mx1 - fp * mxb * my1 + mxb * myb * m0;
+                    const float syy = fp * fp * myy - 2.f * fp * myb * my1 + myb * myb * m0;
                     float* dst = S.part[warp][j];
-#pragma unroll
-                    for (int q = 0; q < 9; ++q) dst[q] = acc[q];
+                    // d_mean = alpha u (A delta); d_Sigma' = alpha/2 u (A delta)(A delta)^T
+                    dst[0] = al * (ia * sdx + ib * sdy);
+                    dst[1] = al * (ib * sdx + ic * sdy);
+                    const float ha = 0.5f * al;
+                    dst[2] = ha * (ia * ia * sxx + 2.f * ia * ib * sxy + ib * ib * syy);
+                    dst[3] = ha * (ia * ib * sxx + (ia * ic + ib * ib) * sxy + ib * ic * syy);
+                    dst[4] = ha * (ib * ib * sxx + 2.f * ib * ic * sxy + ic * ic * syy);
+                    dst[5] = m0;
+                    dst[6] = q0;
+                    dst[7] = q1;
+                    dst[8] = q2;
                     dst[9] = ((vism >> lane) & 1u) ? 1.0f : 0.0f;
                     atomicOr(&S.touch[j], 1u << warp);
                 }

@@ -121,6 +121,48 @@ __device__ __forceinline__ float splat_gauss(float i00, float i01x2, float i11, 
     return fast_exp2(__fmul_rn(q, kNegHalfLog2e));
 }
 
+// Same quadratic form with the conic pre-scaled by kNegHalfLog2e (ka = inv00 K, kb = 2 inv01 K,
+// kc = inv11 K): G = exp2(ka dx^2 + kb dx dy + kc dy^2). The blend kernels use this form in
+// both passes (identical instruction sequence => bit-identical sigma for the T recovery).
+__device__ __forceinline__ float conic_gauss(float ka, float kb, float kc, float dx, float dy) {
+    const float v = __fmul_rn(__fmaf_rn(kb, dx, __fmul_rn(kc, dy)), dy);
+    return fast_exp2(__fmaf_rn(__fmul_rn(ka, dx), dx, v));
+}
+
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// 32-bit shared-window loads/stores (keeps address arithmetic out of the hot loops)
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_f1(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f1(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
+}
+__device__ __forceinline__ void sts_f4(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w));
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
 // ------------------------------------------------------------------ misc
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
