@@ -1,34 +1,35 @@
 // Alpha-blend forward and backward over the per-tile splat lists (sm_100a, FP32 pipe).
 //
-// Work decomposition: one CTA per 16x16 tile; each warp owns an 8x4 block of ACTIVE pixels
-// (for the dilated variant the block spans 8p x 4p image pixels, so the same kernels serve
-// p = 1 and the paper's 4K dilated rendering). Splat batches are staged in shared memory
-// (48-byte records) with exact per-tile box-test masks (rasterizer.cpp:116-118 evaluated once
-// per (tile, splat) in float, per active column / row).
+// Work decomposition: ONE WARP PER 16x16 TILE (several independent warps per CTA, no block
+// barriers). The tile's active pixels (the dilated variant keeps only x%p==ox, y%p==oy, so
+// p selects the geometry and the same kernels serve p = 1 and the paper's 4K dilated
+// rendering) form NG groups of 8x4 active pixels; lane l owns pixel l of every group, with the
+// per-pixel state of all groups in registers.
 //
-// Per 32-splat chunk a warp builds the 32x32 (splat x pixel) pass matrix: lane j turns splat
-// j's column/row masks into a 32-bit row with one multiply, a 5-stage shuffle bit-transpose
-// hands lane l the column "which of these 32 splats pass my pixel". Each lane then walks only
-// its own passing splats with ffs (forward, front to back) or clz (backward, back to front).
-// This replaces the reference's per-pixel walk over the whole list (walk_pixel,
-// rasterizer.cpp:108-136) without changing a blended term: per pixel the order is the list
-// order, and box-failing splats contribute nothing in the reference either.
+// The tile's splat list is consumed in chunks of 32: lane j stages splat j as a 48-byte record
+// in the warp's shared memory together with exact per-tile box-test masks (rasterizer.cpp:
+// 116-118, evaluated once per (tile, splat) in float, per active column / row). For each group
+// the warp builds the 32x32 (splat x pixel) pass matrix — lane j turns splat j's masks into a
+// 32-bit row with one multiply, a 5-stage shuffle bit-transpose hands lane l the column "which
+// of these 32 splats pass my pixel" — and each lane walks only its own passing splats with ffs
+// (forward, front to back) or clz (backward, back to front). Per pixel the order is the list
+// order and box-failing splats contribute nothing, exactly as in walk_pixel
+// (rasterizer.cpp:108-136).
 //
 // forward_kernel: walk_pixel + render (rasterizer.cpp:144-184), optional fused L1 epilogue
 //   (SPEC.md:562-570). Records per pixel the final T and the last blended list position.
-// backward_kernel: backward tile phase (rasterizer.cpp:234-292), two phases per chunk:
+// backward_kernel: backward tile phase (rasterizer.cpp:234-292), per chunk and group:
 //   1. per pixel, back to front: T_i = T_{i+1} / (1 - sigma_i) with sigma recomputed
-//      bit-identically to the forward; dL/dsigma_i = T_i (g.c_i) - (g.S_i)/(1 - sigma_i) with
+//      bit-identically to the forward; g.dC/dsigma_i = T_i (g.c_i) - (g.S_i)/(1 - sigma_i) with
 //      the reference's exact suffix S_i (rasterizer.cpp:266-287) carried as the scalar g.S;
-//      records u = dL/dsigma * G and the blend weight w per (splat, pixel) in shared memory.
-//   2. per splat (lane j), dense over the warp's 32 pixels: every position / covariance
-//      gradient of rasterizer.cpp:276-285 is linear in the moments sum(u), sum(u dx),
-//      sum(u dy), sum(u dx^2), sum(u dx dy), sum(u dy^2) and the colour gradient is sum(g w);
-//      with pixel offsets fixed per lane these are FFMA-with-immediate sums — no divergence,
-//      no cross-lane reductions. The moments are turned into the 9 screen-space gradients
-//      per (warp, splat), combined across warps in a fixed order and written once per
-//      (tile, splat) pair slot (no global atomics, deterministic; merged per Gaussian in
-//      optim.cu in tile order like rasterizer.cpp:301-319).
+//      records u = dL/dsigma * G and the blend weight w per (splat, pixel) in shared memory;
+//   2. per splat (lane j), dense over the group's 32 pixels: every position / covariance
+//      gradient of rasterizer.cpp:276-285 is linear in the moments sum(u), sum(u dx), sum(u dy),
+//      sum(u dx^2), sum(u dx dy), sum(u dy^2) and the colour gradient is sum(g w); with fixed
+//      pixel offsets these are FFMA-with-immediate sums, accumulated across groups in lane j's
+//      registers. After the chunk lane j converts them to the 9 screen-space gradients and
+//      writes its (tile, splat) pair slot once — no reductions, no atomics, deterministic; the
+//      per-Gaussian merge in optim.cu walks the slots in tile order like rasterizer.cpp:301-319.
 #include "tgsx_device.cuh"
 #include "tgsx_internal.h"
 
@@ -39,13 +40,15 @@ namespace tgsx {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
-constexpr int kRec = 48;  // bytes per staged splat record
+constexpr int kRec = 48;        // bytes per staged splat record
+constexpr int kRecStride = 33;  // floats per (splat) row of the phase-1 records (bank skew)
+constexpr int kWPB = 4;         // warps (tiles) per CTA
 
 struct BlendParams {
     const uint2* ranges;
     const uint32_t* items;
     const Prepared* prep;
-    int tiles_x, p, ox, oy, W, H, cols;
+    int tiles, tiles_x, p, ox, oy, W, H, cols;
     float bg0, bg1, bg2;
     float* rgb;
     float* T;
@@ -58,12 +61,8 @@ struct BlendParams {
     float4* partial;               // backward output, 3 float4 per pair slot
 };
 
-// Tile geometry + this lane's pixel, in active coordinates.
-template <int NWX>
-struct PixelMap {
-    int tx, ty, ax, ay, acols, arows, bx, by, x, y, rank;
-    float fx, fy;
-    bool valid;
+struct TileGeo {
+    int tx, ty, ax, ay, acols, arows;
     __device__ __forceinline__ void init(const BlendParams& prm, int tile) {
         tx = tile % prm.tiles_x;
         ty = tile / prm.tiles_x;
@@ -73,17 +72,6 @@ struct PixelMap {
         ay = first_active(y0, prm.oy, prm.p);
         acols = ax < px1 ? (px1 - ax + prm.p - 1) / prm.p : 0;
         arows = ay < py1 ? (py1 - ay + prm.p - 1) / prm.p : 0;
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        bx = warp % NWX;
-        by = warp / NWX;
-        const int lx = bx * 8 + (lane & 7);
-        const int ly = by * 4 + (lane >> 3);
-        valid = lx < acols && ly < arows;
-        x = ax + lx * prm.p;
-        y = ay + ly * prm.p;
-        fx = (float)x + 0.5f;
-        fy = (float)y + 0.5f;
-        rank = valid ? ((y - prm.oy) / prm.p) * prm.cols + (x - prm.ox) / prm.p : 0;
     }
 };
 
@@ -99,10 +87,10 @@ __device__ __forceinline__ uint32_t box_mask(float m, float r, int a0, int p, in
     return mask;
 }
 
-// Row of the warp's 8x4 pixel block passing a splat: bit l <-> pixel (l&7, l>>3).
-__device__ __forceinline__ uint32_t warp_rowmask(uint32_t mask, int bx, int by) {
-    const uint32_t xb = (mask >> (bx * 8)) & 0xffu;
-    const uint32_t yb = (mask >> (16 + by * 4)) & 0xfu;
+// Row of the 8x4 group (gx, gy) passing a splat: bit l <-> active pixel (8gx + l&7, 4gy + l>>3).
+__device__ __forceinline__ uint32_t group_rowmask(uint32_t mask, int gx, int gy) {
+    const uint32_t xb = (mask >> (gx * 8)) & 0xffu;
+    const uint32_t yb = (mask >> (16 + gy * 4)) & 0xfu;
     const uint32_t s = (yb & 1u) | ((yb & 2u) << 7) | ((yb & 4u) << 14) | ((yb & 8u) << 21);
     return xb * s;
 }
@@ -121,105 +109,120 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t v) {
     return v;
 }
 
-// Stages one prepared splat as a 48-byte record:
-//   +0 (mean x, mean y, ka, kb)  +16 (kc, alpha, r, g)  +32 (b, mask bits)
+// Stages one prepared splat as a 48-byte record and returns its tile mask:
+//   +0 (mean x, mean y, ka, kb)  +16 (kc, alpha, r, g)  +32 (b, -)
 // (ka, kb, kc) = (inv00, 2 inv01, inv11) * kNegHalfLog2e; mask = active cols | rows << 16.
-template <int NWX>
-__device__ __forceinline__ void stage_splat(const BlendParams& prm, uint32_t rank,
-                                            const PixelMap<NWX>& g, uint32_t dst) {
-    const Prepared& P = prm.prep[rank];
+__device__ __forceinline__ uint32_t stage_splat(const Prepared& P, const TileGeo& g, int p,
+                                                uint32_t dst, float4& a_out, float4& b_out) {
     const float4 a = P.a, b = P.b, c = P.c;
-    const uint32_t mask = box_mask(a.x, b.z, g.ax, prm.p, g.acols) |
-                          (box_mask(a.y, b.w, g.ay, prm.p, g.arows) << 16);
-    sts_f4(dst, make_float4(a.x, a.y, __fmul_rn(a.z, kNegHalfLog2e),
-                            __fmul_rn(a.w * 2.0f, kNegHalfLog2e)));
-    sts_f4(dst + 16, make_float4(__fmul_rn(b.x, kNegHalfLog2e), b.y, c.x, c.y));
-    sts_f4(dst + 32, make_float4(c.z, __uint_as_float(mask), 0.f, 0.f));
+    const uint32_t mask =
+        box_mask(a.x, b.z, g.ax, p, g.acols) | (box_mask(a.y, b.w, g.ay, p, g.arows) << 16);
+    a_out = make_float4(a.x, a.y, __fmul_rn(a.z, kNegHalfLog2e), __fmul_rn(a.w * 2.0f, kNegHalfLog2e));
+    b_out = make_float4(__fmul_rn(b.x, kNegHalfLog2e), b.y, c.x, c.y);
+    sts_f4(dst, a_out);
+    sts_f4(dst + 16, b_out);
+    sts_f1(dst + 32, c.z);
+    return mask;
 }
 
 // ------------------------------------------------------------------------------- forward
-template <int NWX, int NWY, int BATCH>
-__global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm) {
-    constexpr int NW = NWX * NWY, NT = NW * 32;
-    __shared__ __align__(16) unsigned char s_rec[BATCH * kRec];
-    __shared__ unsigned long long s_red[2][NW];
-    __shared__ float s_loss[NW];
-
-    const int tile = blockIdx.x;
+template <int NGX, int NGY>
+__global__ void __launch_bounds__(kWPB * 32) forward_kernel(BlendParams prm) {
+    constexpr int NG = NGX * NGY;
+    __shared__ __align__(16) unsigned char s_rec[kWPB][32 * kRec];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    PixelMap<NWX> pm;
-    pm.init(prm, tile);
+    const int tile = blockIdx.x * kWPB + warp;
+    if (tile >= prm.tiles) return;
+    TileGeo geo;
+    geo.init(prm, tile);
+    const int p = prm.p;
+
+    float fx[NG], fy[NG], T[NG], C0[NG], C1[NG], C2[NG];
+    uint32_t last[NG];
+    bool done[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
+        done[g] = !(lx < geo.acols && ly < geo.arows);
+        fx[g] = (float)(geo.ax + lx * p) + 0.5f;
+        fy[g] = (float)(geo.ay + ly * p) + 0.5f;
+        T[g] = 1.f;
+        C0[g] = C1[g] = C2[g] = 0.f;
+        last[g] = 0;
+    }
+    uint32_t ops = 0;
     const uint2 range = prm.ranges[tile];
     const int count = (int)(range.y - range.x);
-    const uint32_t sbase = smem_addr(s_rec);
+    const uint32_t sbase = smem_addr(s_rec[warp]);
 
-    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-    uint32_t last = 0, ops = 0;
-    bool done = !pm.valid;
-    bool warp_done = __all_sync(kFull, done);
-
-    for (int bstart = 0; bstart < count; bstart += BATCH) {
-        if (__syncthreads_and(warp_done)) break;
-        const int bcount = min(BATCH, count - bstart);
-        for (int j = threadIdx.x; j < bcount; j += NT)
-            stage_splat(prm, prm.items[range.x + bstart + j], pm, sbase + j * kRec);
-        __syncthreads();
-        if (warp_done) continue;
-        for (int c0 = 0; c0 < bcount; c0 += 32) {
-            const int j = c0 + lane;
-            const uint32_t row =
-                j < bcount ? warp_rowmask(__float_as_uint(lds_f1(sbase + j * kRec + 36)), pm.bx, pm.by) : 0u;
-            uint32_t col = transpose32(row);
-            if (done) col = 0;
-            const uint32_t cbase = sbase + c0 * kRec;
-            const uint32_t lbase = (uint32_t)(bstart + c0 + 1);
+    for (int c0 = 0; c0 < count; c0 += 32) {
+        bool alive = false;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) alive |= !done[g];
+        if (!__any_sync(kFull, alive)) break;
+        const int j = c0 + lane;
+        uint32_t mask = 0;
+        __syncwarp();
+        if (j < count) {
+            float4 a, b;
+            mask = stage_splat(prm.prep[prm.items[range.x + j]], geo, p, sbase + lane * kRec, a, b);
+        }
+        __syncwarp();
+        const uint32_t lbase = (uint32_t)(c0 + 1);
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            uint32_t col = transpose32(group_rowmask(mask, g % NGX, g / NGX));
+            if (done[g]) col = 0;
             while (__any_sync(kFull, col)) {
                 if (col) {
                     const int k = __ffs(col) - 1;
                     col &= col - 1;
-                    const uint32_t ad = cbase + k * kRec;
+                    const uint32_t ad = sbase + k * kRec;
                     const float4 a = lds_f4(ad);
                     const float4 b = lds_f4(ad + 16);
                     const float cz = lds_f1(ad + 32);
-                    const float G = conic_gauss(a.z, a.w, b.x, __fsub_rn(pm.fx, a.x), __fsub_rn(pm.fy, a.y));
+                    const float G = conic_gauss(a.z, a.w, b.x, __fsub_rn(fx[g], a.x), __fsub_rn(fy[g], a.y));
                     const float sigma = __fmul_rn(b.y, G);
-                    const float w = __fmul_rn(sigma, T);
-                    C0 = __fmaf_rn(w, b.z, C0);
-                    C1 = __fmaf_rn(w, b.w, C1);
-                    C2 = __fmaf_rn(w, cz, C2);
-                    T = __fmul_rn(T, __fsub_rn(1.0f, sigma));
+                    const float w = __fmul_rn(sigma, T[g]);
+                    C0[g] = __fmaf_rn(w, b.z, C0[g]);
+                    C1[g] = __fmaf_rn(w, b.w, C1[g]);
+                    C2[g] = __fmaf_rn(w, cz, C2[g]);
+                    T[g] = __fmul_rn(T[g], __fsub_rn(1.0f, sigma));
                     ++ops;
-                    last = lbase + k;
-                    if (T < kTermT) {
-                        done = true;
+                    last[g] = lbase + k;
+                    if (T[g] < kTermT) {
+                        done[g] = true;
                         col = 0;
                     }
                 }
-            }
-            if (__all_sync(kFull, done)) {
-                warp_done = true;
-                break;
             }
         }
     }
 
     float lsum = 0.f;
-    if (pm.valid) {
-        C0 = __fmaf_rn(T, prm.bg0, C0);
-        C1 = __fmaf_rn(T, prm.bg1, C1);
-        C2 = __fmaf_rn(T, prm.bg2, C2);
-        const int r = pm.rank;
+    unsigned long long ev = 0;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
+        if (!(lx < geo.acols && ly < geo.arows)) continue;
+        const int x = geo.ax + lx * p, y = geo.ay + ly * p;
+        const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
+        const float c0v = __fmaf_rn(T[g], prm.bg0, C0[g]);
+        const float c1v = __fmaf_rn(T[g], prm.bg1, C1[g]);
+        const float c2v = __fmaf_rn(T[g], prm.bg2, C2[g]);
         if (prm.rgb) {
-            prm.rgb[3 * r] = C0;
-            prm.rgb[3 * r + 1] = C1;
-            prm.rgb[3 * r + 2] = C2;
+            prm.rgb[3 * r] = c0v;
+            prm.rgb[3 * r + 1] = c1v;
+            prm.rgb[3 * r + 2] = c2v;
         }
-        prm.T[r] = T;
-        prm.last[r] = last;
+        prm.T[r] = T[g];
+        prm.last[r] = last[g];
+        // reference-equivalent evaluation count: terminated pixels walked up to `last`
+        ev += (T[g] < kTermT) ? last[g] : (uint32_t)count;
         if (prm.target) {
-            const float* t = prm.target + 3 * ((int64_t)pm.y * prm.W + pm.x);
-            const float d0 = C0 - t[0], d1 = C1 - t[1], d2 = C2 - t[2];
-            lsum = fabsf(d0) + fabsf(d1) + fabsf(d2);
+            const float* t = prm.target + 3 * ((int64_t)y * prm.W + x);
+            const float d0 = c0v - t[0], d1 = c1v - t[1], d2 = c2v - t[2];
+            lsum += fabsf(d0) + fabsf(d1) + fabsf(d2);
             const float s = prm.loss_scale;
             prm.dLdC[3 * r] = d0 > 0.f ? s : (d0 < 0.f ? -s : 0.f);
             prm.dLdC[3 * r + 1] = d1 > 0.f ? s : (d1 < 0.f ? -s : 0.f);
@@ -227,7 +230,6 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
         }
     }
     unsigned long long o = ops;
-    unsigned long long ev = pm.valid ? (done ? last : (uint32_t)count) : 0u;
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
         o += __shfl_xor_sync(kFull, o, s);
@@ -235,22 +237,9 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
         lsum += __shfl_xor_sync(kFull, lsum, s);
     }
     if (lane == 0) {
-        s_red[0][warp] = o;
-        s_red[1][warp] = ev;
-        s_loss[warp] = lsum;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long to = 0, te = 0;
-        float tl = 0.f;
-        for (int w = 0; w < NW; ++w) {
-            to += s_red[0][w];
-            te += s_red[1][w];
-            tl += s_loss[w];
-        }
-        if (to) atomicAdd(&prm.counters[1], to);
-        if (te) atomicAdd(&prm.counters[2], te);
-        if (prm.block_loss) prm.block_loss[tile] = tl;
+        if (o) atomicAdd(&prm.counters[1], o);
+        if (ev) atomicAdd(&prm.counters[2], ev);
+        if (prm.block_loss) prm.block_loss[tile] = lsum;
     }
 }
 
@@ -261,204 +250,178 @@ __device__ __forceinline__ uint32_t pair_slot(const Prepared& P, int tx, int ty)
     return d.z + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
 }
 
-constexpr int kRecStride = 33;  // floats per (splat) row of the phase-1 records (bank skew)
-
-template <int NW, int BATCH>
-struct BwdSmem {
-    unsigned char rec[BATCH * kRec];
-    uint32_t slot[BATCH];
-    uint32_t touch[BATCH];                 // bit w: warp w wrote part[w][j]
-    float part[NW][BATCH][10];             // per-warp partials: 9 grads + visited
-    float rec_u[NW][32 * kRecStride + 4];  // phase-1 records [splat][pixel]
-    float rec_w[NW][32 * kRecStride + 4];
-    float4 g[NW][32];                      // per-pixel dL/dC
+template <int NG>
+struct BwdWarpSmem {
+    float rec_u[32 * kRecStride + 4];  // phase-1 records [splat][pixel]
+    float rec_w[32 * kRecStride + 4];
+    float4 g[NG][32];                  // per-pixel dL/dC
+    unsigned char rec[32 * kRec];
 };
 
-template <int NWX, int NWY, int BATCH>
-__global__ void __launch_bounds__(NWX * NWY * 32) backward_kernel(BlendParams prm) {
-    constexpr int NW = NWX * NWY, NT = NW * 32;
+template <int NGX, int NGY>
+__global__ void __launch_bounds__(kWPB * 32) backward_kernel(BlendParams prm) {
+    constexpr int NG = NGX * NGY;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto& S = *reinterpret_cast<BwdSmem<NW, BATCH>*>(smem_raw);
-    __shared__ uint32_t s_maxlast;
-
-    const int tile = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    PixelMap<NWX> pm;
-    pm.init(prm, tile);
+    auto& S = reinterpret_cast<BwdWarpSmem<NG>*>(smem_raw)[warp];
+    const int tile = blockIdx.x * kWPB + warp;
+    if (tile >= prm.tiles) return;
+    TileGeo geo;
+    geo.init(prm, tile);
+    const int p = prm.p;
     const uint2 range = prm.ranges[tile];
     const int count = (int)(range.y - range.x);
-    const int p = prm.p;
     const uint32_t rbase = smem_addr(S.rec);
-    const uint32_t ubase = smem_addr(S.rec_u[warp]);
-    const uint32_t wbase = smem_addr(S.rec_w[warp]);
+    const uint32_t ubase = smem_addr(S.rec_u);
+    const uint32_t wbase = smem_addr(S.rec_w);
 
-    float T = 1.f, gS = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
-    uint32_t last = 0;
-    if (pm.valid) {
-        T = prm.T[pm.rank];
-        last = prm.last[pm.rank];
-        g0 = prm.dLdC[3 * pm.rank];
-        g1 = prm.dLdC[3 * pm.rank + 1];
-        g2 = prm.dLdC[3 * pm.rank + 2];
-        // g . S with S = background * trans_final (rasterizer.cpp:267)
-        gS = g0 * (prm.bg0 * T) + g1 * (prm.bg1 * T) + g2 * (prm.bg2 * T);
+    float fx[NG], fy[NG], T[NG], gS[NG], g0[NG], g1[NG], g2[NG];
+    uint32_t last[NG];
+    uint32_t maxlast = 0;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
+        const bool valid = lx < geo.acols && ly < geo.arows;
+        const int x = geo.ax + lx * p, y = geo.ay + ly * p;
+        fx[g] = (float)x + 0.5f;
+        fy[g] = (float)y + 0.5f;
+        T[g] = 1.f;
+        gS[g] = g0[g] = g1[g] = g2[g] = 0.f;
+        last[g] = 0;
+        if (valid) {
+            const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
+            T[g] = prm.T[r];
+            last[g] = prm.last[r];
+            g0[g] = prm.dLdC[3 * r];
+            g1[g] = prm.dLdC[3 * r + 1];
+            g2[g] = prm.dLdC[3 * r + 2];
+            // g . S with S = background * trans_final (rasterizer.cpp:267)
+            gS[g] = g0[g] * (prm.bg0 * T[g]) + g1[g] * (prm.bg1 * T[g]) + g2[g] * (prm.bg2 * T[g]);
+        }
+        S.g[g][lane] = make_float4(g0[g], g1[g], g2[g], 0.f);
+        maxlast = max(maxlast, last[g]);
     }
-    S.g[warp][lane] = make_float4(g0, g1, g2, 0.f);
-    const uint32_t wlast = __reduce_max_sync(kFull, last);
-    if (threadIdx.x == 0) s_maxlast = 0;
-    __syncthreads();
-    if (lane == 0) atomicMax(&s_maxlast, wlast);
-    __syncthreads();
-    const int maxlast = (int)s_maxlast;
-    // block centre (pixel-centre coordinates) for the phase-2 moments: pixel l of this warp is
-    // at (cx + ((l&7) - 3.5) p, cy + ((l>>3) - 1.5) p)
-    const float cx = (float)(pm.ax + pm.bx * 8 * p) + 0.5f + 3.5f * (float)p;
-    const float cy = (float)(pm.ay + pm.by * 4 * p) + 0.5f + 1.5f * (float)p;
+    maxlast = __reduce_max_sync(kFull, maxlast);
+    // moments are taken about the tile's active-pixel centre (pixel-centre coordinates):
+    // active pixel (cx, cy) sits at (ctr_x + (cx - hx) p, ctr_y + (cy - hy) p)
+    constexpr float hx = 0.5f * (NGX * 8 - 1), hy = 0.5f * (NGY * 4 - 1);
     const float fp = (float)p;
+    const float ctr_x = (float)geo.ax + 0.5f + hx * fp;
+    const float ctr_y = (float)geo.ay + 0.5f + hy * fp;
 
     // list entries past every pixel's last contributor: zero partials
-    for (int j = maxlast + threadIdx.x; j < count; j += NT) {
-        const uint32_t slot = pair_slot(prm.prep[prm.items[range.x + j]], pm.tx, pm.ty);
+    for (int j = (int)maxlast + lane; j < count; j += 32) {
+        const uint32_t slot = pair_slot(prm.prep[prm.items[range.x + j]], geo.tx, geo.ty);
         float4* dst = prm.partial + 3 * (size_t)slot;
         dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
         dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
         dst[2] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
-    const int nb = (maxlast + BATCH - 1) / BATCH;
-    for (int b = nb - 1; b >= 0; --b) {
-        const int bstart = b * BATCH;
-        const int bcount = min(BATCH, maxlast - bstart);
-        __syncthreads();
-        for (int j = threadIdx.x; j < bcount; j += NT) {
-            const uint32_t rank = prm.items[range.x + bstart + j];
-            stage_splat(prm, rank, pm, rbase + j * kRec);
-            S.slot[j] = pair_slot(prm.prep[rank], pm.tx, pm.ty);
-            S.touch[j] = 0u;
+    const int nch = ((int)maxlast + 31) / 32;
+    for (int ch = nch - 1; ch >= 0; --ch) {
+        const int c0 = ch * 32;
+        const int j = c0 + lane;
+        const bool jvalid = j < (int)maxlast;
+        __syncwarp();
+        uint32_t mask = 0, slot = 0;
+        float4 ja = make_float4(0.f, 0.f, 0.f, 0.f), jb = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (jvalid) {
+            const Prepared& P = prm.prep[prm.items[range.x + j]];
+            mask = stage_splat(P, geo, p, rbase + lane * kRec, ja, jb);
+            slot = pair_slot(P, geo.tx, geo.ty);
         }
-        __syncthreads();
-        if (wlast > (uint32_t)bstart) {
-            const int nch = (bcount + 31) / 32;
-            for (int ch = nch - 1; ch >= 0; --ch) {
-                const int c0 = ch * 32;
-                const int cb = bstart + c0;
-                if (wlast <= (uint32_t)cb) continue;
-                const int j = c0 + lane;
-                const uint32_t row =
-                    j < bcount ? warp_rowmask(__float_as_uint(lds_f1(rbase + j * kRec + 36)), pm.bx, pm.by) : 0u;
-                uint32_t col = transpose32(row);
-                // only splats before this pixel's last contributor were blended
-                const int span = (int)last - cb;
-                col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
-                // zero this warp's records (contiguous; 16-B stores)
-                for (int q = lane; q < (32 * kRecStride + 4) / 4; q += 32) {
-                    sts_f4(ubase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
-                    sts_f4(wbase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
-                }
-                __syncwarp();
-                uint32_t visb = 0;
-                const uint32_t cbase = rbase + c0 * kRec;
-                // phase 1: per pixel, back to front
-                while (__any_sync(kFull, col)) {
-                    if (col) {
-                        const int k = 31 - __clz(col);
-                        col ^= 1u << k;
-                        const uint32_t ad = cbase + k * kRec;
-                        const float4 a = lds_f4(ad);
-                        const float4 bb = lds_f4(ad + 16);
-                        const float cz = lds_f1(ad + 32);
-                        const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(pm.fx, a.x), __fsub_rn(pm.fy, a.y));
-                        const float sigma = __fmul_rn(bb.y, G);
-                        const float ir = fast_rcp(__fsub_rn(1.0f, sigma));  // inv_rest
-                        const float Ti = T * ir;
-                        const float w = sigma * Ti;
-                        const float gc = g0 * bb.z + g1 * bb.w + g2 * cz;
-                        // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
-                        const float dsig = Ti * gc - gS * ir;
-                        gS = __fmaf_rn(gc, w, gS);
-                        T = Ti;
-                        const uint32_t o = 4u * (uint32_t)(k * kRecStride + lane);
-                        sts_f1(ubase + o, dsig * G);
-                        sts_f1(wbase + o, w);
-                        if (w > kMinVisitW) visb |= 1u << k;
-                    }
-                }
-                const uint32_t vism = __reduce_or_sync(kFull, visb);
-                __syncwarp();
-                // phase 2: lane = splat j, dense over the warp's 32 pixels
-                float m0 = 0.f, mx1 = 0.f, my1 = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
-                float q0 = 0.f, q1 = 0.f, q2 = 0.f;
-                const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
-                const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
-                const uint32_t gb = smem_addr(S.g[warp]);
+        __syncwarp();
+        float m0 = 0.f, mx1 = 0.f, my1 = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
+        float q0 = 0.f, q1 = 0.f, q2 = 0.f;
+        uint32_t vism = 0;
 #pragma unroll
-                for (int l = 0; l < 32; ++l) {
-                    const float xi = (float)(l & 7) - 3.5f;
-                    const float eta = (float)(l >> 3) - 1.5f;
-                    const float u = lds_f1(ur + 4 * l);
-                    const float w = lds_f1(wr + 4 * l);
-                    const float4 gl = lds_f4(gb + 16 * l);
-                    m0 += u;
-                    mx1 = __fmaf_rn(u, xi, mx1);
-                    my1 = __fmaf_rn(u, eta, my1);
-                    mxx = __fmaf_rn(u, xi * xi, mxx);
-                    mxy = __fmaf_rn(u, xi * eta, mxy);
-                    myy = __fmaf_rn(u, eta * eta, myy);
-                    q0 = __fmaf_rn(w, gl.x, q0);
-                    q1 = __fmaf_rn(w, gl.y, q1);
-                    q2 = __fmaf_rn(w, gl.z, q2);
-                }
-                if (j < bcount && (m0 != 0.f || q0 != 0.f || q1 != 0.f || q2 != 0.f || mxx != 0.f ||
-                                   ((vism >> lane) & 1u))) {
-                    const float4 a = lds_f4(rbase + j * kRec);
-                    const float4 bb = lds_f4(rbase + j * kRec + 16);
-                    const float iK = 1.0f / kNegHalfLog2e;
-                    const float ia = a.z * iK, ib = 0.5f * a.w * iK, ic = bb.x * iK;
-                    const float al = bb.y;
-                    // moments about the splat mean: dx = p xi - mxb, dy = p eta - myb
-                    const float mxb = a.x - cx, myb = a.y - cy;
-                    const float sdx = fp * mx1 - mxb * m0;
-                    const float sdy = fp * my1 - myb * m0;
-                    const float sxx = fp * fp * mxx - 2.f * fp * mxb * mx1 + mxb * mxb * m0;
-                    const float sxy = fp * fp * mxy - fp * myb * mx1 - fp * mxb * my1 + mxb * myb * m0;
-                    const float syy = fp * fp * myy - 2.f * fp * myb * my1 + myb * myb * m0;
-                    float* dst = S.part[warp][j];
-                    // d_mean = alpha u (A delta); d_Sigma' = alpha/2 u (A delta)(A delta)^T
-                    dst[0] = al * (ia * sdx + ib * sdy);
-                    dst[1] = al * (ib * sdx + ic * sdy);
-                    const float ha = 0.5f * al;
-                    dst[2] = ha * (ia * ia * sxx + 2.f * ia * ib * sxy + ib * ib * syy);
-                    dst[3] = ha * (ia * ib * sxx + (ia * ic + ib * ib) * sxy + ib * ic * syy);
-                    dst[4] = ha * (ib * ib * sxx + 2.f * ib * ic * sxy + ic * ic * syy);
-                    dst[5] = m0;
-                    dst[6] = q0;
-                    dst[7] = q1;
-                    dst[8] = q2;
-                    dst[9] = ((vism >> lane) & 1u) ? 1.0f : 0.0f;
-                    atomicOr(&S.touch[j], 1u << warp);
-                }
-                __syncwarp();
+        for (int g = 0; g < NG; ++g) {
+            uint32_t col = transpose32(group_rowmask(mask, g % NGX, g / NGX));
+            // only splats before this pixel's last contributor were blended
+            const int span = (int)last[g] - c0;
+            col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
+            if (!__any_sync(kFull, col)) continue;
+            for (int q = lane; q < (32 * kRecStride + 4) / 4; q += 32) {
+                sts_f4(ubase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
+                sts_f4(wbase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
             }
-        }
-        __syncthreads();
-        // fixed-order cross-warp combine, one write per (tile, splat) pair slot
-        for (int j = threadIdx.x; j < bcount; j += NT) {
-            float acc[10];
-#pragma unroll
-            for (int k = 0; k < 10; ++k) acc[k] = 0.f;
-            const uint32_t touch = S.touch[j];
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                if (touch & (1u << w)) {
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) acc[k] += S.part[w][j][k];
-                    acc[9] = fmaxf(acc[9], S.part[w][j][9]);
+            __syncwarp();
+            uint32_t visb = 0;
+            // phase 1: per pixel, back to front
+            while (__any_sync(kFull, col)) {
+                if (col) {
+                    const int k = 31 - __clz(col);
+                    col ^= 1u << k;
+                    const uint32_t ad = rbase + k * kRec;
+                    const float4 a = lds_f4(ad);
+                    const float4 bb = lds_f4(ad + 16);
+                    const float cz = lds_f1(ad + 32);
+                    const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(fx[g], a.x), __fsub_rn(fy[g], a.y));
+                    const float sigma = __fmul_rn(bb.y, G);
+                    const float ir = fast_rcp(__fsub_rn(1.0f, sigma));  // inv_rest
+                    const float Ti = T[g] * ir;
+                    const float w = sigma * Ti;
+                    const float gc = g0[g] * bb.z + g1[g] * bb.w + g2[g] * cz;
+                    // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
+                    const float dsig = Ti * gc - gS[g] * ir;
+                    gS[g] = __fmaf_rn(gc, w, gS[g]);
+                    T[g] = Ti;
+                    const uint32_t o = 4u * (uint32_t)(k * kRecStride + lane);
+                    sts_f1(ubase + o, dsig * G);
+                    sts_f1(wbase + o, w);
+                    if (w > kMinVisitW) visb |= 1u << k;
                 }
             }
-            float4* dst = prm.partial + 3 * (size_t)S.slot[j];
-            dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-            dst[2] = make_float4(acc[8], acc[9], 0.f, 0.f);
+            vism |= __reduce_or_sync(kFull, visb);
+            __syncwarp();
+            // phase 2: lane = splat j, dense over the group's 32 pixels
+            const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
+            const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
+            const uint32_t gb = smem_addr(S.g[g]);
+#pragma unroll
+            for (int l = 0; l < 32; ++l) {
+                const float xi = (float)((g % NGX) * 8 + (l & 7)) - hx;
+                const float eta = (float)((g / NGX) * 4 + (l >> 3)) - hy;
+                const float u = lds_f1(ur + 4 * l);
+                const float w = lds_f1(wr + 4 * l);
+                const float4 gl = lds_f4(gb + 16 * l);
+                m0 += u;
+                mx1 = __fmaf_rn(u, xi, mx1);
+                my1 = __fmaf_rn(u, eta, my1);
+                mxx = __fmaf_rn(u, xi * xi, mxx);
+                mxy = __fmaf_rn(u, xi * eta, mxy);
+                myy = __fmaf_rn(u, eta * eta, myy);
+                q0 = __fmaf_rn(w, gl.x, q0);
+                q1 = __fmaf_rn(w, gl.y, q1);
+                q2 = __fmaf_rn(w, gl.z, q2);
+            }
+        }
+        if (jvalid) {
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
+            if (m0 != 0.f || mxx != 0.f || myy != 0.f || q0 != 0.f || q1 != 0.f || q2 != 0.f) {
+                constexpr float iK = 1.0f / kNegHalfLog2e;
+                const float ia = ja.z * iK, ib = 0.5f * ja.w * iK, ic = jb.x * iK;
+                const float al = jb.y;
+                // moments about the splat mean: dx = p xi - mxb, dy = p eta - myb
+                const float mxb = ja.x - ctr_x, myb = ja.y - ctr_y;
+                const float sdx = fp * mx1 - mxb * m0;
+                const float sdy = fp * my1 - myb * m0;
+                const float sxx = fp * fp * mxx - 2.f * fp * mxb * mx1 + mxb * mxb * m0;
+                const float sxy = fp * fp * mxy - fp * myb * mx1 - fp * mxb * my1 + mxb * myb * m0;
+                const float syy = fp * fp * myy - 2.f * fp * myb * my1 + myb * myb * m0;
+                // d_mean = alpha u (A delta); d_Sigma' = alpha/2 u (A delta)(A delta)^T
+                const float ha = 0.5f * al;
+                r0 = make_float4(al * (ia * sdx + ib * sdy), al * (ib * sdx + ic * sdy),
+                                 ha * (ia * ia * sxx + 2.f * ia * ib * sxy + ib * ib * syy),
+                                 ha * (ia * ib * sxx + (ia * ic + ib * ib) * sxy + ib * ic * syy));
+                r1 = make_float4(ha * (ib * ib * sxx + 2.f * ib * ic * sxy + ic * ic * syy), m0, q0, q1);
+            }
+            r2 = make_float4(q2, ((vism >> lane) & 1u) ? 1.0f : 0.0f, 0.f, 0.f);
+            float4* dst = prm.partial + 3 * (size_t)slot;
+            dst[0] = r0;
+            dst[1] = r1;
+            dst[2] = r2;
         }
     }
 }
@@ -469,6 +432,7 @@ BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* ite
     prm.ranges = ws.ranges.as<uint2>();
     prm.items = items;
     prm.prep = ws.prep.as<Prepared>();
+    prm.tiles = ws.tiles_x * ws.tiles_y;
     prm.tiles_x = ws.tiles_x;
     prm.p = ra.p;
     prm.ox = ra.ox;
@@ -489,18 +453,18 @@ BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* ite
     return prm;
 }
 
-template <int NWX, int NWY, int BATCH>
-cudaError_t run_backward(tgsx_ctx* ctx, const BlendParams& prm, unsigned tiles) {
-    constexpr int NT = NWX * NWY * 32;
-    const size_t smem = sizeof(BwdSmem<NWX * NWY, BATCH>);
+template <int NGX, int NGY>
+cudaError_t run_backward(tgsx_ctx* ctx, const BlendParams& prm) {
+    const size_t smem = kWPB * sizeof(BwdWarpSmem<NGX * NGY>);
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(backward_kernel<NWX, NWY, BATCH>,
+        cudaError_t e = cudaFuncSetAttribute(backward_kernel<NGX, NGY>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e) return e;
         configured = true;
     }
-    backward_kernel<NWX, NWY, BATCH><<<tiles, NT, smem, ctx->stream>>>(prm);
+    const unsigned grid = (unsigned)((prm.tiles + kWPB - 1) / kWPB);
+    backward_kernel<NGX, NGY><<<grid, kWPB * 32, smem, ctx->stream>>>(prm);
     return cudaGetLastError();
 }
 
@@ -508,7 +472,6 @@ cudaError_t run_backward(tgsx_ctx* ctx, const BlendParams& prm, unsigned tiles) 
 
 cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
                            bool fused_loss) {
-    Workspace& ws = ctx->ws;
     BlendParams prm = make_params(ctx, ra, items);
     if (fused_loss) {
         prm.target = ra.target;
@@ -517,29 +480,27 @@ cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* 
         prm.target = nullptr;
         prm.block_loss = nullptr;
     }
-    const unsigned tiles = (unsigned)(ws.tiles_x * ws.tiles_y);
+    const unsigned grid = (unsigned)((prm.tiles + kWPB - 1) / kWPB);
     if (ra.p == 1) {
-        forward_kernel<2, 4, 256><<<tiles, 256, 0, ctx->stream>>>(prm);
+        forward_kernel<2, 4><<<grid, kWPB * 32, 0, ctx->stream>>>(prm);
     } else if (ra.p <= 3) {
-        forward_kernel<1, 2, 128><<<tiles, 64, 0, ctx->stream>>>(prm);
+        forward_kernel<1, 2><<<grid, kWPB * 32, 0, ctx->stream>>>(prm);
     } else {
-        forward_kernel<1, 1, 128><<<tiles, 32, 0, ctx->stream>>>(prm);
+        forward_kernel<1, 1><<<grid, kWPB * 32, 0, ctx->stream>>>(prm);
     }
     ctx->launches++;
     return cudaGetLastError();
 }
 
 cudaError_t launch_backward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items) {
-    Workspace& ws = ctx->ws;
     BlendParams prm = make_params(ctx, ra, items);
-    const unsigned tiles = (unsigned)(ws.tiles_x * ws.tiles_y);
     cudaError_t e;
     if (ra.p == 1) {
-        e = run_backward<2, 4, 32>(ctx, prm, tiles);
+        e = run_backward<2, 4>(ctx, prm);
     } else if (ra.p <= 3) {
-        e = run_backward<1, 2, 64>(ctx, prm, tiles);
+        e = run_backward<1, 2>(ctx, prm);
     } else {
-        e = run_backward<1, 1, 64>(ctx, prm, tiles);
+        e = run_backward<1, 1>(ctx, prm);
     }
     ctx->launches++;
     return e;
