@@ -1,24 +1,22 @@
 // Alpha-blend forward and backward over the per-tile splat lists (sm_100a, FP32 pipe).
 //
-// Work decomposition: ONE WARP PER 16x16 TILE (several independent warps per CTA, no block
-// barriers). The tile's active pixels (the dilated variant keeps only x%p==ox, y%p==oy, so
-// p selects the geometry and the same kernels serve p = 1 and the paper's 4K dilated
-// rendering) form NG groups of 8x4 active pixels; lane l owns pixel l of every group, with the
-// per-pixel state of all groups in registers.
-//
-// The tile's splat list is consumed in chunks of 32: lane j stages splat j as a 48-byte record
-// in the warp's shared memory together with exact per-tile box-test masks (rasterizer.cpp:
-// 116-118, evaluated once per (tile, splat) in float, per active column / row). For each group
-// the warp builds the 32x32 (splat x pixel) pass matrix — lane j turns splat j's masks into a
-// 32-bit row with one multiply, a 5-stage shuffle bit-transpose hands lane l the column "which
-// of these 32 splats pass my pixel" — and each lane walks only its own passing splats with ffs
-// (forward, front to back) or clz (backward, back to front). Per pixel the order is the list
-// order and box-failing splats contribute nothing, exactly as in walk_pixel
+// The tile's active pixels (the dilated variant keeps only x%p==ox, y%p==oy, so p selects the
+// geometry and the same kernels serve p = 1 and the paper's 4K dilated rendering) form groups
+// of 8x4 active pixels, one pixel per lane. The tile's splat list is consumed in chunks of 32
+// staged as 48-byte shared-memory records together with exact per-tile box-test masks
+// (rasterizer.cpp:116-118, evaluated once per (tile, splat) in float, per active column / row).
+// For a group the warp builds the 32x32 (splat x pixel) pass matrix — lane j turns splat j's
+// masks into a 32-bit row with one multiply, a 5-stage shuffle bit-transpose hands lane l the
+// column "which of these 32 splats pass my pixel" — and each lane walks only its own passing
+// splats with ffs (forward, front to back) or clz (backward, back to front). Per pixel the
+// order is the list order and box-failing splats contribute nothing, exactly as in walk_pixel
 // (rasterizer.cpp:108-136).
 //
-// forward_kernel: walk_pixel + render (rasterizer.cpp:144-184), optional fused L1 epilogue
-//   (SPEC.md:562-570). Records per pixel the final T and the last blended list position.
-// backward_kernel: backward tile phase (rasterizer.cpp:234-292), per chunk and group:
+// forward_kernel (one CTA per tile, one warp per group): walk_pixel + render
+//   (rasterizer.cpp:144-184), optional fused L1 epilogue. Records per pixel
+//   the final T and the last blended list position.
+// backward_kernel (ONE WARP PER TILE, independent warps, no block barriers): backward tile
+//   phase (rasterizer.cpp:234-292), per chunk and group:
 //   1. per pixel, back to front: T_i = T_{i+1} / (1 - sigma_i) with sigma recomputed
 //      bit-identically to the forward; g.dC/dsigma_i = T_i (g.c_i) - (g.S_i)/(1 - sigma_i) with
 //      the reference's exact suffix S_i (rasterizer.cpp:266-287) carried as the scalar g.S;
@@ -26,10 +24,11 @@
 //   2. per splat (lane j), dense over the group's 32 pixels: every position / covariance
 //      gradient of rasterizer.cpp:276-285 is linear in the moments sum(u), sum(u dx), sum(u dy),
 //      sum(u dx^2), sum(u dx dy), sum(u dy^2) and the colour gradient is sum(g w); with fixed
-//      pixel offsets these are FFMA-with-immediate sums, accumulated across groups in lane j's
-//      registers. After the chunk lane j converts them to the 9 screen-space gradients and
-//      writes its (tile, splat) pair slot once — no reductions, no atomics, deterministic; the
-//      per-Gaussian merge in optim.cu walks the slots in tile order like rasterizer.cpp:301-319.
+//      pixel offsets these are FFMA-with-immediate sums, accumulated across the tile's groups in
+//      lane j's registers. After the chunk lane j converts them to the 9 screen-space gradients
+//      and writes its (tile, splat) pair slot once — no reductions, no atomics, deterministic;
+//      the per-Gaussian merge in optim.cu walks the slots in tile order like
+//      rasterizer.cpp:301-319.
 #include "tgsx_device.cuh"
 #include "tgsx_internal.h"
 
@@ -125,104 +124,131 @@ __device__ __forceinline__ uint32_t stage_splat(const Prepared& P, const TileGeo
     return mask;
 }
 
-// ------------------------------------------------------------------------------- forward
-template <int NGX, int NGY>
-__global__ void __launch_bounds__(kWPB * 32) forward_kernel(BlendParams prm) {
-    constexpr int NG = NGX * NGY;
-    __shared__ __align__(16) unsigned char s_rec[kWPB][32 * kRec];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x * kWPB + warp;
-    if (tile >= prm.tiles) return;
-    TileGeo geo;
-    geo.init(prm, tile);
-    const int p = prm.p;
-
-    float fx[NG], fy[NG], T[NG], C0[NG], C1[NG], C2[NG];
-    uint32_t last[NG];
-    bool done[NG];
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-        const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
-        done[g] = !(lx < geo.acols && ly < geo.arows);
-        fx[g] = (float)(geo.ax + lx * p) + 0.5f;
-        fy[g] = (float)(geo.ay + ly * p) + 0.5f;
-        T[g] = 1.f;
-        C0[g] = C1[g] = C2[g] = 0.f;
-        last[g] = 0;
+// Tile geometry + this lane's pixel, in active coordinates.
+template <int NWX>
+struct PixelMap {
+    int tx, ty, ax, ay, acols, arows, bx, by, x, y, rank;
+    float fx, fy;
+    bool valid;
+    __device__ __forceinline__ void init(const BlendParams& prm, int tile) {
+        tx = tile % prm.tiles_x;
+        ty = tile / prm.tiles_x;
+        const int x0 = tx * kTile, y0 = ty * kTile;
+        const int px1 = min(prm.W, x0 + kTile), py1 = min(prm.H, y0 + kTile);
+        ax = first_active(x0, prm.ox, prm.p);
+        ay = first_active(y0, prm.oy, prm.p);
+        acols = ax < px1 ? (px1 - ax + prm.p - 1) / prm.p : 0;
+        arows = ay < py1 ? (py1 - ay + prm.p - 1) / prm.p : 0;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        bx = warp % NWX;
+        by = warp / NWX;
+        const int lx = bx * 8 + (lane & 7);
+        const int ly = by * 4 + (lane >> 3);
+        valid = lx < acols && ly < arows;
+        x = ax + lx * prm.p;
+        y = ay + ly * prm.p;
+        fx = (float)x + 0.5f;
+        fy = (float)y + 0.5f;
+        rank = valid ? ((y - prm.oy) / prm.p) * prm.cols + (x - prm.ox) / prm.p : 0;
     }
-    uint32_t ops = 0;
+};
+
+template <int NWX>
+__device__ __forceinline__ void stage_splat_cta(const BlendParams& prm, uint32_t rank,
+                                            const PixelMap<NWX>& g, uint32_t dst) {
+    const Prepared& P = prm.prep[rank];
+    const float4 a = P.a, b = P.b, c = P.c;
+    const uint32_t mask = box_mask(a.x, b.z, g.ax, prm.p, g.acols) |
+                          (box_mask(a.y, b.w, g.ay, prm.p, g.arows) << 16);
+    sts_f4(dst, make_float4(a.x, a.y, __fmul_rn(a.z, kNegHalfLog2e),
+                            __fmul_rn(a.w * 2.0f, kNegHalfLog2e)));
+    sts_f4(dst + 16, make_float4(__fmul_rn(b.x, kNegHalfLog2e), b.y, c.x, c.y));
+    sts_f4(dst + 32, make_float4(c.z, __uint_as_float(mask), 0.f, 0.f));
+}
+
+// ------------------------------------------------------------------------------- forward
+template <int NWX, int NWY, int BATCH>
+__global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm) {
+    constexpr int NW = NWX * NWY, NT = NW * 32;
+    __shared__ __align__(16) unsigned char s_rec[BATCH * kRec];
+    __shared__ unsigned long long s_red[2][NW];
+    __shared__ float s_loss[NW];
+
+    const int tile = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    PixelMap<NWX> pm;
+    pm.init(prm, tile);
     const uint2 range = prm.ranges[tile];
     const int count = (int)(range.y - range.x);
-    const uint32_t sbase = smem_addr(s_rec[warp]);
+    const uint32_t sbase = smem_addr(s_rec);
 
-    for (int c0 = 0; c0 < count; c0 += 32) {
-        bool alive = false;
-#pragma unroll
-        for (int g = 0; g < NG; ++g) alive |= !done[g];
-        if (!__any_sync(kFull, alive)) break;
-        const int j = c0 + lane;
-        uint32_t mask = 0;
-        __syncwarp();
-        if (j < count) {
-            float4 a, b;
-            mask = stage_splat(prm.prep[prm.items[range.x + j]], geo, p, sbase + lane * kRec, a, b);
-        }
-        __syncwarp();
-        const uint32_t lbase = (uint32_t)(c0 + 1);
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-            uint32_t col = transpose32(group_rowmask(mask, g % NGX, g / NGX));
-            if (done[g]) col = 0;
+    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
+    uint32_t last = 0, ops = 0;
+    bool done = !pm.valid;
+    bool warp_done = __all_sync(kFull, done);
+
+    for (int bstart = 0; bstart < count; bstart += BATCH) {
+        if (__syncthreads_and(warp_done)) break;
+        const int bcount = min(BATCH, count - bstart);
+        for (int j = threadIdx.x; j < bcount; j += NT)
+            stage_splat_cta(prm, prm.items[range.x + bstart + j], pm, sbase + j * kRec);
+        __syncthreads();
+        if (warp_done) continue;
+        for (int c0 = 0; c0 < bcount; c0 += 32) {
+            const int j = c0 + lane;
+            const uint32_t row =
+                j < bcount ? group_rowmask(__float_as_uint(lds_f1(sbase + j * kRec + 36)), pm.bx, pm.by) : 0u;
+            uint32_t col = transpose32(row);
+            if (done) col = 0;
+            const uint32_t cbase = sbase + c0 * kRec;
+            const uint32_t lbase = (uint32_t)(bstart + c0 + 1);
             while (__any_sync(kFull, col)) {
                 if (col) {
                     const int k = __ffs(col) - 1;
                     col &= col - 1;
-                    const uint32_t ad = sbase + k * kRec;
+                    const uint32_t ad = cbase + k * kRec;
                     const float4 a = lds_f4(ad);
                     const float4 b = lds_f4(ad + 16);
                     const float cz = lds_f1(ad + 32);
-                    const float G = conic_gauss(a.z, a.w, b.x, __fsub_rn(fx[g], a.x), __fsub_rn(fy[g], a.y));
+                    const float G = conic_gauss(a.z, a.w, b.x, __fsub_rn(pm.fx, a.x), __fsub_rn(pm.fy, a.y));
                     const float sigma = __fmul_rn(b.y, G);
-                    const float w = __fmul_rn(sigma, T[g]);
-                    C0[g] = __fmaf_rn(w, b.z, C0[g]);
-                    C1[g] = __fmaf_rn(w, b.w, C1[g]);
-                    C2[g] = __fmaf_rn(w, cz, C2[g]);
-                    T[g] = __fmul_rn(T[g], __fsub_rn(1.0f, sigma));
+                    const float w = __fmul_rn(sigma, T);
+                    C0 = __fmaf_rn(w, b.z, C0);
+                    C1 = __fmaf_rn(w, b.w, C1);
+                    C2 = __fmaf_rn(w, cz, C2);
+                    T = __fmul_rn(T, __fsub_rn(1.0f, sigma));
                     ++ops;
-                    last[g] = lbase + k;
-                    if (T[g] < kTermT) {
-                        done[g] = true;
+                    last = lbase + k;
+                    if (T < kTermT) {
+                        done = true;
                         col = 0;
                     }
                 }
+            }
+            if (__all_sync(kFull, done)) {
+                warp_done = true;
+                break;
             }
         }
     }
 
     float lsum = 0.f;
-    unsigned long long ev = 0;
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-        const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
-        if (!(lx < geo.acols && ly < geo.arows)) continue;
-        const int x = geo.ax + lx * p, y = geo.ay + ly * p;
-        const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
-        const float c0v = __fmaf_rn(T[g], prm.bg0, C0[g]);
-        const float c1v = __fmaf_rn(T[g], prm.bg1, C1[g]);
-        const float c2v = __fmaf_rn(T[g], prm.bg2, C2[g]);
+    if (pm.valid) {
+        C0 = __fmaf_rn(T, prm.bg0, C0);
+        C1 = __fmaf_rn(T, prm.bg1, C1);
+        C2 = __fmaf_rn(T, prm.bg2, C2);
+        const int r = pm.rank;
         if (prm.rgb) {
-            prm.rgb[3 * r] = c0v;
-            prm.rgb[3 * r + 1] = c1v;
-            prm.rgb[3 * r + 2] = c2v;
+            prm.rgb[3 * r] = C0;
+            prm.rgb[3 * r + 1] = C1;
+            prm.rgb[3 * r + 2] = C2;
         }
-        prm.T[r] = T[g];
-        prm.last[r] = last[g];
-        // reference-equivalent evaluation count: terminated pixels walked up to `last`
-        ev += (T[g] < kTermT) ? last[g] : (uint32_t)count;
+        prm.T[r] = T;
+        prm.last[r] = last;
         if (prm.target) {
-            const float* t = prm.target + 3 * ((int64_t)y * prm.W + x);
-            const float d0 = c0v - t[0], d1 = c1v - t[1], d2 = c2v - t[2];
-            lsum += fabsf(d0) + fabsf(d1) + fabsf(d2);
+            const float* t = prm.target + 3 * ((int64_t)pm.y * prm.W + pm.x);
+            const float d0 = C0 - t[0], d1 = C1 - t[1], d2 = C2 - t[2];
+            lsum = fabsf(d0) + fabsf(d1) + fabsf(d2);
             const float s = prm.loss_scale;
             prm.dLdC[3 * r] = d0 > 0.f ? s : (d0 < 0.f ? -s : 0.f);
             prm.dLdC[3 * r + 1] = d1 > 0.f ? s : (d1 < 0.f ? -s : 0.f);
@@ -230,6 +256,7 @@ __global__ void __launch_bounds__(kWPB * 32) forward_kernel(BlendParams prm) {
         }
     }
     unsigned long long o = ops;
+    unsigned long long ev = pm.valid ? (done ? last : (uint32_t)count) : 0u;
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
         o += __shfl_xor_sync(kFull, o, s);
@@ -237,9 +264,22 @@ __global__ void __launch_bounds__(kWPB * 32) forward_kernel(BlendParams prm) {
         lsum += __shfl_xor_sync(kFull, lsum, s);
     }
     if (lane == 0) {
-        if (o) atomicAdd(&prm.counters[1], o);
-        if (ev) atomicAdd(&prm.counters[2], ev);
-        if (prm.block_loss) prm.block_loss[tile] = lsum;
+        s_red[0][warp] = o;
+        s_red[1][warp] = ev;
+        s_loss[warp] = lsum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long to = 0, te = 0;
+        float tl = 0.f;
+        for (int w = 0; w < NW; ++w) {
+            to += s_red[0][w];
+            te += s_red[1][w];
+            tl += s_loss[w];
+        }
+        if (to) atomicAdd(&prm.counters[1], to);
+        if (te) atomicAdd(&prm.counters[2], te);
+        if (prm.block_loss) prm.block_loss[tile] = tl;
     }
 }
 
@@ -254,12 +294,12 @@ template <int NG>
 struct BwdWarpSmem {
     float rec_u[32 * kRecStride + 4];  // phase-1 records [splat][pixel]
     float rec_w[32 * kRecStride + 4];
-    float4 g[NG][32];                  // per-pixel dL/dC
+    float4 g[NG][32];                  // per-pixel dL/dC and last contributor (as bits)
     unsigned char rec[32 * kRec];
 };
 
 template <int NGX, int NGY>
-__global__ void __launch_bounds__(kWPB * 32) backward_kernel(BlendParams prm) {
+__global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm) {
     constexpr int NG = NGX * NGY;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -275,31 +315,31 @@ __global__ void __launch_bounds__(kWPB * 32) backward_kernel(BlendParams prm) {
     const uint32_t ubase = smem_addr(S.rec_u);
     const uint32_t wbase = smem_addr(S.rec_w);
 
-    float fx[NG], fy[NG], T[NG], gS[NG], g0[NG], g1[NG], g2[NG];
-    uint32_t last[NG];
+    float T[NG], gS[NG];
     uint32_t maxlast = 0;
+    const float fxl = (float)(geo.ax + (lane & 7) * p) + 0.5f;   // group (0,0) pixel centre
+    const float fyl = (float)(geo.ay + (lane >> 3) * p) + 0.5f;
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
         const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
         const bool valid = lx < geo.acols && ly < geo.arows;
         const int x = geo.ax + lx * p, y = geo.ay + ly * p;
-        fx[g] = (float)x + 0.5f;
-        fy[g] = (float)y + 0.5f;
         T[g] = 1.f;
-        gS[g] = g0[g] = g1[g] = g2[g] = 0.f;
-        last[g] = 0;
+        gS[g] = 0.f;
+        float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+        uint32_t last = 0;
         if (valid) {
             const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
             T[g] = prm.T[r];
-            last[g] = prm.last[r];
-            g0[g] = prm.dLdC[3 * r];
-            g1[g] = prm.dLdC[3 * r + 1];
-            g2[g] = prm.dLdC[3 * r + 2];
+            last = prm.last[r];
+            g0 = prm.dLdC[3 * r];
+            g1 = prm.dLdC[3 * r + 1];
+            g2 = prm.dLdC[3 * r + 2];
             // g . S with S = background * trans_final (rasterizer.cpp:267)
-            gS[g] = g0[g] * (prm.bg0 * T[g]) + g1[g] * (prm.bg1 * T[g]) + g2[g] * (prm.bg2 * T[g]);
+            gS[g] = g0 * (prm.bg0 * T[g]) + g1 * (prm.bg1 * T[g]) + g2 * (prm.bg2 * T[g]);
         }
-        S.g[g][lane] = make_float4(g0[g], g1[g], g2[g], 0.f);
-        maxlast = max(maxlast, last[g]);
+        S.g[g][lane] = make_float4(g0, g1, g2, __uint_as_float(last));
+        maxlast = max(maxlast, last);
     }
     maxlast = __reduce_max_sync(kFull, maxlast);
     // moments are taken about the tile's active-pixel centre (pixel-centre coordinates):
@@ -338,8 +378,10 @@ __global__ void __launch_bounds__(kWPB * 32) backward_kernel(BlendParams prm) {
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
             uint32_t col = transpose32(group_rowmask(mask, g % NGX, g / NGX));
+            const float4 gv = S.g[g][lane];
+            const float fxg = fxl + (float)((g % NGX) * 8 * p), fyg = fyl + (float)((g / NGX) * 4 * p);
             // only splats before this pixel's last contributor were blended
-            const int span = (int)last[g] - c0;
+            const int span = (int)__float_as_uint(gv.w) - c0;
             col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
             if (!__any_sync(kFull, col)) continue;
             for (int q = lane; q < (32 * kRecStride + 4) / 4; q += 32) {
@@ -357,12 +399,12 @@ __global__ void __launch_bounds__(kWPB * 32) backward_kernel(BlendParams prm) {
                     const float4 a = lds_f4(ad);
                     const float4 bb = lds_f4(ad + 16);
                     const float cz = lds_f1(ad + 32);
-                    const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(fx[g], a.x), __fsub_rn(fy[g], a.y));
+                    const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(fxg, a.x), __fsub_rn(fyg, a.y));
                     const float sigma = __fmul_rn(bb.y, G);
                     const float ir = fast_rcp(__fsub_rn(1.0f, sigma));  // inv_rest
                     const float Ti = T[g] * ir;
                     const float w = sigma * Ti;
-                    const float gc = g0[g] * bb.z + g1[g] * bb.w + g2[g] * cz;
+                    const float gc = gv.x * bb.z + gv.y * bb.w + gv.z * cz;
                     // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
                     const float dsig = Ti * gc - gS[g] * ir;
                     gS[g] = __fmaf_rn(gc, w, gS[g]);
@@ -480,13 +522,13 @@ cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* 
         prm.target = nullptr;
         prm.block_loss = nullptr;
     }
-    const unsigned grid = (unsigned)((prm.tiles + kWPB - 1) / kWPB);
+    const unsigned tiles = (unsigned)prm.tiles;
     if (ra.p == 1) {
-        forward_kernel<2, 4><<<grid, kWPB * 32, 0, ctx->stream>>>(prm);
+        forward_kernel<2, 4, 256><<<tiles, 256, 0, ctx->stream>>>(prm);
     } else if (ra.p <= 3) {
-        forward_kernel<1, 2><<<grid, kWPB * 32, 0, ctx->stream>>>(prm);
+        forward_kernel<1, 2, 128><<<tiles, 64, 0, ctx->stream>>>(prm);
     } else {
-        forward_kernel<1, 1><<<grid, kWPB * 32, 0, ctx->stream>>>(prm);
+        forward_kernel<1, 1, 128><<<tiles, 32, 0, ctx->stream>>>(prm);
     }
     ctx->launches++;
     return cudaGetLastError();
