@@ -40,7 +40,7 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kRec = 48;        // bytes per staged splat record
-constexpr int kRecStride = 33;  // floats per (splat) row of the phase-1 records (bank skew)
+constexpr int kRecStride = 36;  // floats per (splat) row of the phase-1 records (16-B rows, conflict-free LDS.128)
 constexpr int kWPB = 4;         // warps (tiles) per CTA
 
 struct BlendParams {
@@ -292,9 +292,10 @@ __device__ __forceinline__ uint32_t pair_slot(const Prepared& P, int tx, int ty)
 
 template <int NG>
 struct BwdWarpSmem {
-    float rec_u[32 * kRecStride + 4];  // phase-1 records [splat][pixel]
-    float rec_w[32 * kRecStride + 4];
-    float4 g[NG][32];                  // per-pixel dL/dC and last contributor (as bits)
+    float rec_u[32 * kRecStride];  // phase-1 records [splat][pixel], 16-B aligned rows
+    float rec_w[32 * kRecStride];
+    float4 g[NG][32];              // per-pixel dL/dC and last contributor (as bits)
+    float2 st[NG][32];             // per-pixel (T, g.S) carried across chunks
     unsigned char rec[32 * kRec];
 };
 
@@ -315,39 +316,37 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
     const uint32_t ubase = smem_addr(S.rec_u);
     const uint32_t wbase = smem_addr(S.rec_w);
 
-    float T[NG], gS[NG];
     uint32_t maxlast = 0;
-    const float fxl = (float)(geo.ax + (lane & 7) * p) + 0.5f;   // group (0,0) pixel centre
-    const float fyl = (float)(geo.ay + (lane >> 3) * p) + 0.5f;
-#pragma unroll
+#pragma unroll 1
     for (int g = 0; g < NG; ++g) {
         const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
         const bool valid = lx < geo.acols && ly < geo.arows;
         const int x = geo.ax + lx * p, y = geo.ay + ly * p;
-        T[g] = 1.f;
-        gS[g] = 0.f;
-        float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+        float T = 1.f, gS = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
         uint32_t last = 0;
         if (valid) {
             const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
-            T[g] = prm.T[r];
+            T = prm.T[r];
             last = prm.last[r];
             g0 = prm.dLdC[3 * r];
             g1 = prm.dLdC[3 * r + 1];
             g2 = prm.dLdC[3 * r + 2];
             // g . S with S = background * trans_final (rasterizer.cpp:267)
-            gS[g] = g0 * (prm.bg0 * T[g]) + g1 * (prm.bg1 * T[g]) + g2 * (prm.bg2 * T[g]);
+            gS = g0 * (prm.bg0 * T) + g1 * (prm.bg1 * T) + g2 * (prm.bg2 * T);
         }
         S.g[g][lane] = make_float4(g0, g1, g2, __uint_as_float(last));
+        S.st[g][lane] = make_float2(T, gS);
         maxlast = max(maxlast, last);
     }
     maxlast = __reduce_max_sync(kFull, maxlast);
-    // moments are taken about the tile's active-pixel centre (pixel-centre coordinates):
-    // active pixel (cx, cy) sits at (ctr_x + (cx - hx) p, ctr_y + (cy - hy) p)
+    // moments about the tile's active-pixel centre (pixel-centre coordinates): active pixel
+    // (cx, cy) sits at (ctr_x + (cx - hx) p, ctr_y + (cy - hy) p)
     constexpr float hx = 0.5f * (NGX * 8 - 1), hy = 0.5f * (NGY * 4 - 1);
     const float fp = (float)p;
     const float ctr_x = (float)geo.ax + 0.5f + hx * fp;
     const float ctr_y = (float)geo.ay + 0.5f + hy * fp;
+    const float fxl = (float)(geo.ax + (lane & 7) * p) + 0.5f;  // group (0,0) pixel centre
+    const float fyl = (float)(geo.ay + (lane >> 3) * p) + 0.5f;
 
     // list entries past every pixel's last contributor: zero partials
     for (int j = (int)maxlast + lane; j < count; j += 32) {
@@ -375,16 +374,20 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
         float m0 = 0.f, mx1 = 0.f, my1 = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
         float q0 = 0.f, q1 = 0.f, q2 = 0.f;
         uint32_t vism = 0;
-#pragma unroll
+#pragma unroll 1
         for (int g = 0; g < NG; ++g) {
-            uint32_t col = transpose32(group_rowmask(mask, g % NGX, g / NGX));
+            const int gx = g % NGX, gy = g / NGX;
+            uint32_t col = transpose32(group_rowmask(mask, gx, gy));
             const float4 gv = S.g[g][lane];
-            const float fxg = fxl + (float)((g % NGX) * 8 * p), fyg = fyl + (float)((g / NGX) * 4 * p);
             // only splats before this pixel's last contributor were blended
             const int span = (int)__float_as_uint(gv.w) - c0;
             col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
             if (!__any_sync(kFull, col)) continue;
-            for (int q = lane; q < (32 * kRecStride + 4) / 4; q += 32) {
+            float2 st = S.st[g][lane];
+            float T = st.x, gS = st.y;
+            const float fxg = fxl + (float)(gx * 8 * p), fyg = fyl + (float)(gy * 4 * p);
+#pragma unroll
+            for (int q = lane; q < 32 * kRecStride / 4; q += 32) {
                 sts_f4(ubase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
                 sts_f4(wbase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
             }
@@ -402,42 +405,59 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
                     const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(fxg, a.x), __fsub_rn(fyg, a.y));
                     const float sigma = __fmul_rn(bb.y, G);
                     const float ir = fast_rcp(__fsub_rn(1.0f, sigma));  // inv_rest
-                    const float Ti = T[g] * ir;
+                    const float Ti = T * ir;
                     const float w = sigma * Ti;
                     const float gc = gv.x * bb.z + gv.y * bb.w + gv.z * cz;
                     // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
-                    const float dsig = Ti * gc - gS[g] * ir;
-                    gS[g] = __fmaf_rn(gc, w, gS[g]);
-                    T[g] = Ti;
+                    const float dsig = Ti * gc - gS * ir;
+                    gS = __fmaf_rn(gc, w, gS);
+                    T = Ti;
                     const uint32_t o = 4u * (uint32_t)(k * kRecStride + lane);
                     sts_f1(ubase + o, dsig * G);
                     sts_f1(wbase + o, w);
                     if (w > kMinVisitW) visb |= 1u << k;
                 }
             }
+            S.st[g][lane] = make_float2(T, gS);
             vism |= __reduce_or_sync(kFull, visb);
             __syncwarp();
-            // phase 2: lane = splat j, dense over the group's 32 pixels
+            // phase 2: lane = splat j, dense over the group's 32 pixels; moments about the
+            // group centre (compile-time offsets), shifted to the tile centre below
+            float a0 = 0.f, ax1 = 0.f, ay1 = 0.f, axx = 0.f, axy = 0.f, ayy = 0.f;
             const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
             const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
             const uint32_t gb = smem_addr(S.g[g]);
 #pragma unroll
-            for (int l = 0; l < 32; ++l) {
-                const float xi = (float)((g % NGX) * 8 + (l & 7)) - hx;
-                const float eta = (float)((g / NGX) * 4 + (l >> 3)) - hy;
-                const float u = lds_f1(ur + 4 * l);
-                const float w = lds_f1(wr + 4 * l);
-                const float4 gl = lds_f4(gb + 16 * l);
-                m0 += u;
-                mx1 = __fmaf_rn(u, xi, mx1);
-                my1 = __fmaf_rn(u, eta, my1);
-                mxx = __fmaf_rn(u, xi * xi, mxx);
-                mxy = __fmaf_rn(u, xi * eta, mxy);
-                myy = __fmaf_rn(u, eta * eta, myy);
-                q0 = __fmaf_rn(w, gl.x, q0);
-                q1 = __fmaf_rn(w, gl.y, q1);
-                q2 = __fmaf_rn(w, gl.z, q2);
+            for (int l4 = 0; l4 < 8; ++l4) {
+                const float4 u4 = lds_f4(ur + 16 * l4);
+                const float4 w4 = lds_f4(wr + 16 * l4);
+                const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+                const float ww[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int l = 4 * l4 + e;
+                    const float xi = (float)(l & 7) - 3.5f;
+                    const float eta = (float)(l >> 3) - 1.5f;
+                    const float u = uu[e], w = ww[e];
+                    const float4 gl = lds_f4(gb + 16 * l);
+                    a0 += u;
+                    ax1 = __fmaf_rn(u, xi, ax1);
+                    ay1 = __fmaf_rn(u, eta, ay1);
+                    axx = __fmaf_rn(u, xi * xi, axx);
+                    axy = __fmaf_rn(u, xi * eta, axy);
+                    ayy = __fmaf_rn(u, eta * eta, ayy);
+                    q0 = __fmaf_rn(w, gl.x, q0);
+                    q1 = __fmaf_rn(w, gl.y, q1);
+                    q2 = __fmaf_rn(w, gl.z, q2);
+                }
             }
+            const float dx = (float)(gx * 8) + 3.5f - hx, dy = (float)(gy * 4) + 1.5f - hy;
+            m0 += a0;
+            mx1 += ax1 + dx * a0;
+            my1 += ay1 + dy * a0;
+            mxx += axx + 2.f * dx * ax1 + dx * dx * a0;
+            mxy += axy + dy * ax1 + dx * ay1 + dx * dy * a0;
+            myy += ayy + 2.f * dy * ay1 + dy * dy * a0;
         }
         if (jvalid) {
             float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
