@@ -40,7 +40,8 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kRec = 48;        // bytes per staged splat record
-constexpr int kRecStride = 36;  // floats per (splat) row of the phase-1 records (16-B rows, conflict-free LDS.128)
+constexpr int kRecStride = 32;  // floats per (splat) row of the phase-1 records; float4 blocks
+                                // XOR-swizzled by (row & 7) => conflict-free row-wise LDS.128
 constexpr int kWPB = 4;         // warps (tiles) per CTA
 
 struct BlendParams {
@@ -292,12 +293,17 @@ __device__ __forceinline__ uint32_t pair_slot(const Prepared& P, int tx, int ty)
 
 template <int NG>
 struct BwdWarpSmem {
-    float rec_u[32 * kRecStride];  // phase-1 records [splat][pixel], 16-B aligned rows
+    float rec_u[32 * kRecStride];  // phase-1 records [splat][pixel (swizzled)]
     float rec_w[32 * kRecStride];
-    float4 g[NG][32];              // per-pixel dL/dC and last contributor (as bits)
     float2 st[NG][32];             // per-pixel (T, g.S) carried across chunks
+    float4 gcur[32];               // dL/dC of the current group's pixels (phase-2 broadcast)
     unsigned char rec[32 * kRec];
 };
+
+// Swizzled record position of (splat row k, pixel l): float4 block (l>>2) ^ (k&7).
+__device__ __forceinline__ uint32_t rec_off(int k, int l) {
+    return 4u * (uint32_t)(k * kRecStride + ((((l >> 2) ^ (k & 7)) << 2) | (l & 3)));
+}
 
 template <int NGX, int NGY>
 __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm) {
@@ -334,7 +340,6 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             // g . S with S = background * trans_final (rasterizer.cpp:267)
             gS = g0 * (prm.bg0 * T) + g1 * (prm.bg1 * T) + g2 * (prm.bg2 * T);
         }
-        S.g[g][lane] = make_float4(g0, g1, g2, __uint_as_float(last));
         S.st[g][lane] = make_float2(T, gS);
         maxlast = max(maxlast, last);
     }
@@ -378,13 +383,24 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
         for (int g = 0; g < NG; ++g) {
             const int gx = g % NGX, gy = g / NGX;
             uint32_t col = transpose32(group_rowmask(mask, gx, gy));
-            const float4 gv = S.g[g][lane];
+            float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
+            uint32_t glast = 0;
+            {
+                const int lx = gx * 8 + (lane & 7), ly = gy * 4 + (lane >> 3);
+                if (lx < geo.acols && ly < geo.arows) {
+                    const int x = geo.ax + lx * p, y = geo.ay + ly * p;
+                    const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
+                    glast = prm.last[r];
+                    gv = make_float4(prm.dLdC[3 * r], prm.dLdC[3 * r + 1], prm.dLdC[3 * r + 2], 0.f);
+                }
+            }
             // only splats before this pixel's last contributor were blended
-            const int span = (int)__float_as_uint(gv.w) - c0;
+            const int span = (int)glast - c0;
             col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
             if (!__any_sync(kFull, col)) continue;
             float2 st = S.st[g][lane];
             float T = st.x, gS = st.y;
+            S.gcur[lane] = gv;
             const float fxg = fxl + (float)(gx * 8 * p), fyg = fyl + (float)(gy * 4 * p);
 #pragma unroll
             for (int q = lane; q < 32 * kRecStride / 4; q += 32) {
@@ -412,7 +428,7 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
                     const float dsig = Ti * gc - gS * ir;
                     gS = __fmaf_rn(gc, w, gS);
                     T = Ti;
-                    const uint32_t o = 4u * (uint32_t)(k * kRecStride + lane);
+                    const uint32_t o = rec_off(k, lane);
                     sts_f1(ubase + o, dsig * G);
                     sts_f1(wbase + o, w);
                     if (w > kMinVisitW) visb |= 1u << k;
@@ -426,11 +442,12 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             float a0 = 0.f, ax1 = 0.f, ay1 = 0.f, axx = 0.f, axy = 0.f, ayy = 0.f;
             const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
             const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
-            const uint32_t gb = smem_addr(S.g[g]);
+            const uint32_t gb = smem_addr(S.gcur);
 #pragma unroll
             for (int l4 = 0; l4 < 8; ++l4) {
-                const float4 u4 = lds_f4(ur + 16 * l4);
-                const float4 w4 = lds_f4(wr + 16 * l4);
+                const uint32_t sw = 16u * (uint32_t)(l4 ^ (lane & 7));
+                const float4 u4 = lds_f4(ur + sw);
+                const float4 w4 = lds_f4(wr + sw);
                 const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
                 const float ww[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
