@@ -339,6 +339,8 @@ def backward(s: Scene, p, ox, oy, W, H, dLdC, bg=(0, 0, 0), lowpass_p=0, impl="o
     gp = (C.c_void_p * 9)(*[grads[q].ctypes.data for q in range(9)])
     scr = None
     if impl == "oracle":
+        if dLdC.size // 3 != active_count(p, ox, oy, W, H):
+            raise OracleError(1, "backward: loss-gradient count does not match pattern ranks")
         bgv = np.asarray(bg, np.float32)
         gpp = (f32p * 9)(*[_ptr(grads[q], f32p) for q in range(9)])
         sc = None
@@ -367,7 +369,7 @@ def backward(s: Scene, p, ox, oy, W, H, dLdC, bg=(0, 0, 0), lowpass_p=0, impl="o
     vis = np.ascontiguousarray(s.visit, np.int64)
     win = np.ascontiguousarray(s.window, np.int64)
     rc = fn(C.byref(rs), p, ox, oy, W, H, bgv.ctypes.data_as(C.c_void_p),
-            dLdC.ctypes.data_as(C.c_void_p), threads, lowpass_p, gp,
+            dLdC.ctypes.data_as(C.c_void_p), C.c_int64(dLdC.size // 3), threads, lowpass_p, gp,
             pos.ctypes.data_as(C.c_void_p), col.ctypes.data_as(C.c_void_p), _ptr(acc, i32p),
             _ptr(vis, i64p), _ptr(win, i64p), err, 256)
     if rc:
@@ -496,16 +498,35 @@ def cap_candidates(s: Scene, cand, budget_remaining):
 
 
 def densify_event(s: Scene, capacity: int, cfg, budget: int, rng: Pcg32, m=None, v=None):
-    """Runs one event in place on arrays sized >= capacity. Returns (new_scene_view, spawned,
-    pruned, candidates)."""
+    """One densify event (SPEC.md:575(3)). `s` (and the optional Adam moments m, v of shape
+    [9, n]) are copied into capacity-sized arrays; returns (new_scene, spawned, pruned,
+    candidates, (m, v)) with everything truncated to the new count."""
+    s.ensure_stats()
+    n0 = s.n
+    cap = max(capacity, n0, 1)
+    big = Scene.empty(cap, cap)
+    for k, val in s.__dict__.items():
+        if isinstance(val, np.ndarray):
+            getattr(big, k)[:n0] = val
+    big.next_id = s.next_id
+    mm = vv = None
+    if m is not None:
+        mm = np.zeros((9, cap), np.float32)
+        vv = np.zeros((9, cap), np.float32)
+        mm[:, :n0] = m
+        vv[:, :n0] = v
     keep: list = []
-    cs = _c_scene(s, keep)
+    cs = _c_scene(big, keep)
+    cs.n = n0
     sp, pr, nc = C.c_int64(), C.c_int64(), C.c_int64()
-    mp = (f32p * 9)(*[_ptr(m[q], f32p) for q in range(9)]) if m is not None else None
-    vp = (f32p * 9)(*[_ptr(v[q], f32p) for q in range(9)]) if v is not None else None
-    n = lib().or_densify_event(C.byref(cs), C.c_int64(capacity), C.byref(cfg), C.c_int64(budget),
+    mp = (f32p * 9)(*[_ptr(mm[q], f32p) for q in range(9)]) if mm is not None else None
+    vp = (f32p * 9)(*[_ptr(vv[q], f32p) for q in range(9)]) if vv is not None else None
+    n = lib().or_densify_event(C.byref(cs), C.c_int64(cap), C.byref(cfg), C.c_int64(budget),
                                C.byref(rng.c), mp, vp, C.byref(sp), C.byref(pr), C.byref(nc))
-    return n, cs.next_id, sp.value, pr.value, nc.value
+    out = big.truncated(n)
+    out.next_id = cs.next_id
+    mv = (mm[:, :n].copy(), vv[:, :n].copy()) if mm is not None else None
+    return out, sp.value, pr.value, nc.value, mv
 
 
 def visit_audit(s: Scene):

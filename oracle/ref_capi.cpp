@@ -94,7 +94,7 @@ int do_render(const SceneView<T>& s, int p, int ox, int oy, int W, int H, const 
 // stats: in/out (pos_acc, col_acc, accum_count, visit_count, window_visit_count), may be null.
 template <typename T>
 int do_backward(const SceneView<T>& s, int p, int ox, int oy, int W, int H, const T* bg,
-                const T* dLdC, int threads, int lowpass_p, T* const* grads, T* pos_acc,
+                const T* dLdC, int64_t dLdC_count, int threads, int lowpass_p, T* const* grads, T* pos_acc,
                 T* col_acc, int32_t* accum, int64_t* visit, int64_t* window, char* err,
                 int errlen) {
     return guarded(
@@ -114,7 +114,9 @@ int do_backward(const SceneView<T>& s, int p, int ox, int oy, int W, int H, cons
             tgs::RenderOptions opts;
             opts.threads = threads;
             opts.lowpass_p = lowpass_p;
-            std::vector<tgs::Vec3<T>> g(pat.active_count());
+            // the caller's count is passed through so the reference's own size check
+            // (rasterizer.cpp:222-224) decides
+            std::vector<tgs::Vec3<T>> g(dLdC_count < 0 ? pat.active_count() : dLdC_count);
             for (size_t i = 0; i < g.size(); ++i)
                 g[i] = tgs::Vec3<T>(dLdC[3 * i], dLdC[3 * i + 1], dLdC[3 * i + 2]);
             auto gs = tgs::backward<T>(model, pat, tgs::Vec3<T>(bg[0], bg[1], bg[2]), g, opts);
@@ -165,18 +167,18 @@ int ref_render_f64(const RefSceneF64* s, int p, int ox, int oy, int W, int H, co
 }
 
 int ref_backward_f32(const RefSceneF32* s, int p, int ox, int oy, int W, int H, const float* bg,
-                     const float* dLdC, int threads, int lowpass_p, float* const* grads,
+                     const float* dLdC, int64_t dLdC_count, int threads, int lowpass_p, float* const* grads,
                      float* pos_acc, float* col_acc, int32_t* accum, int64_t* visit,
                      int64_t* window, char* err, int errlen) {
-    return do_backward(*s, p, ox, oy, W, H, bg, dLdC, threads, lowpass_p, grads, pos_acc, col_acc,
+    return do_backward(*s, p, ox, oy, W, H, bg, dLdC, dLdC_count, threads, lowpass_p, grads, pos_acc, col_acc,
                        accum, visit, window, err, errlen);
 }
 
 int ref_backward_f64(const RefSceneF64* s, int p, int ox, int oy, int W, int H, const double* bg,
-                     const double* dLdC, int threads, int lowpass_p, double* const* grads,
+                     const double* dLdC, int64_t dLdC_count, int threads, int lowpass_p, double* const* grads,
                      double* pos_acc, double* col_acc, int32_t* accum, int64_t* visit,
                      int64_t* window, char* err, int errlen) {
-    return do_backward(*s, p, ox, oy, W, H, bg, dLdC, threads, lowpass_p, grads, pos_acc, col_acc,
+    return do_backward(*s, p, ox, oy, W, H, bg, dLdC, dLdC_count, threads, lowpass_p, grads, pos_acc, col_acc,
                        accum, visit, window, err, errlen);
 }
 

@@ -1,0 +1,328 @@
+"""SPEC known-answer examples and properties (CPU only).
+
+The reference sources for the optimizer, densifier, budget controller and loss are missing
+(SURVEY.md §0.3); their only pins are the SPEC's examples, which these tests check against
+BOTH the oracle restatement (oracle/tgs_oracle.c) and the product's host-side implementation
+(libtgsx host.cpp, api.py). The product's GPU densify/Adam are compared to the oracle
+bit-for-bit in tests/test_gpu_parity.py.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import bind as B
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2412_13547_b200 as P
+    return P
+
+
+# ------------------------------------------------------------------ splat core / dilation
+def test_covariance_and_lowpass_kats():
+    """SPEC.md:49-51 (covariance), :139-141 (apply_lowpass) via the prepared inverse."""
+    B.set_math(True)
+    cases = [(0.0, 0.0, 0.0, (1.0, 0.0, 1.0)),
+             (math.pi / 2, math.log(2), 0.0, (1.0, 0.0, 4.0)),
+             (math.pi / 4, math.log(2), 0.0, (2.5, 1.5, 2.5))]
+    for p in (1, 3):
+        bump = 0.3 + 0.5 * (p - 1)
+        s = B.Scene.empty(len(cases))
+        for i, (rot, lx, ly, _) in enumerate(cases):
+            s.rot[i], s.lsx[i], s.lsy[i] = rot, lx, ly
+            s.depth[i] = i
+            s.px[i] = s.py[i] = 10.0
+        s.id = np.arange(len(cases), dtype=np.uint64)
+        prep = B.prepare(s, p)
+        for i, (_, _, _, (a, b, c)) in enumerate(cases):
+            A = np.linalg.inv(np.array([[a + bump, b], [b, c + bump]]))
+            got = np.array([[prep["i00"][i], prep["i01"][i]], [prep["i01"][i], prep["i11"][i]]])
+            assert np.allclose(got, A, rtol=2e-6, atol=2e-7)
+            assert abs(prep["rx"][i] - 3 * math.sqrt(a + bump)) < 1e-5
+
+
+def test_activate_kats():
+    """activate(0)=0.5, activate(ln 3)=0.75 (through the prepared alpha)."""
+    s = B.Scene.empty(2)
+    s.rop[:] = [0.0, math.log(3.0)]
+    s.depth[:] = [0, 1]
+    s.id = np.arange(2, dtype=np.uint64)
+    prep = B.prepare(s, 1)
+    assert prep["alpha"][0] == np.float32(0.5)
+    assert abs(prep["alpha"][1] - 0.75) < 1e-7
+
+
+def test_dilation_kats(P):
+    """SPEC.md:119-131 + properties :144-146."""
+    assert P.DilationPattern(1, 0, 0, 4, 4).active_count() == 16
+    pat = P.DilationPattern(2, 0, 0, 4, 4)
+    xs, ys = pat.active_pixels()
+    assert sorted(zip(xs.tolist(), ys.tolist())) == [(0, 0), (0, 2), (2, 0), (2, 2)]
+    pat = P.DilationPattern(3, 1, 2, 5, 5)
+    xs, ys = pat.active_pixels()
+    assert list(zip(xs.tolist(), ys.tolist())) == [(1, 2), (4, 2)]
+    assert [P.next_offsets(2, i) for i in range(4)] == [(0, 0), (1, 0), (0, 1), (1, 1)]
+    assert P.next_offsets(3, 7) == (1, 2)
+    assert P.next_offsets(1, 12345) == (0, 0)
+    for W, H, p in ((7, 5, 2), (33, 17, 3), (16, 16, 4)):
+        tot = sum(P.DilationPattern(p, *P.next_offsets(p, i), W, H).active_count() for i in range(p * p))
+        assert tot == W * H
+        pat = P.DilationPattern(p, 1, 0, W, H)
+        xs, ys = pat.active_pixels()
+        assert all(pat.rank_of(x, y) == r for r, (x, y) in enumerate(zip(xs, ys)))
+    with pytest.raises(ValueError):
+        P.DilationPattern(0, 0, 0, 4, 4)
+    with pytest.raises(ValueError):
+        P.DilationPattern(2, 2, 0, 4, 4)
+    with pytest.raises(ValueError):
+        P.DilationPattern(2, 0, 0, 0, 4)
+    assert P.lowpass_bump(1) == pytest.approx(0.3) and P.lowpass_bump(3) == pytest.approx(1.3)
+
+
+def test_render_kats():
+    """empty model -> background; two-splat front/back example."""
+    s = B.Scene.empty(0)
+    rgb, T, ops, _ = B.render(s, 1, 0, 0, 4, 4, (0.25, 0.5, 0.75))
+    assert np.all(rgb == np.float32([0.25, 0.5, 0.75])) and np.all(T == 1) and ops == 0
+    # front splat sigma ~ 0.5 (white) over an almost opaque black one at the pixel centre
+    s = B.Scene.empty(2)
+    s.px[:] = 0.5
+    s.py[:] = 0.5
+    s.lsx[:] = s.lsy[:] = 3.0
+    s.rop[:] = [0.0, 12.0]
+    s.cr[:] = s.cg[:] = s.cb[:] = [12.0, -12.0]
+    s.depth[:] = [0.0, 1.0]
+    s.id = np.arange(2, dtype=np.uint64)
+    rgb, T, ops, _ = B.render(s, 1, 0, 0, 1, 1)
+    assert np.allclose(rgb[0], 0.5, atol=2e-3) and ops == 2
+
+
+def test_backward_zero_grads_kat():
+    """zero loss grads -> zero gradients; untouched splats -> exactly zero."""
+    s = B.synthetic_scene(2, 50, 20, 20)
+    s.px[0] = 1000.0
+    g, _ = B.backward(s, 1, 0, 0, 20, 20, np.zeros((400, 3), np.float32))
+    assert np.all(g == 0)
+    g, _ = B.backward(s, 1, 0, 0, 20, 20, np.ones((400, 3), np.float32))
+    assert np.all(g[:, 0] == 0)
+
+
+# ------------------------------------------------------------------ loss / Adam
+def test_l1_kats():
+    """identical -> 0; black vs white with lambda_ssim=0 -> 1."""
+    t = np.random.default_rng(0).random((4, 5, 3)).astype(np.float32)
+    loss, g = B.l1_loss(t.reshape(-1, 3), 1, 0, 0, 5, 4, t)
+    assert loss == 0 and np.all(g == 0)
+    loss, g = B.l1_loss(np.zeros((20, 3), np.float32), 1, 0, 0, 5, 4, np.ones((4, 5, 3), np.float32))
+    assert loss == 1.0 and np.all(g < 0)
+
+
+def test_adam_kats():
+    """zero grads -> unchanged; first step g=1 -> delta = -lr; constant g ->
+    |update| -> lr."""
+    s = B.synthetic_scene(1, 10, 16, 16)
+    s0 = s.copy()
+    m = np.zeros((9, 10), np.float32)
+    v = np.zeros((9, 10), np.float32)
+    cfg = B.adam_config(1, 100, math.hypot(16, 16))
+    B.adam_step(s, np.zeros((9, 10), np.float32), m, v, cfg)
+    for f in B.PARAM_FIELDS:
+        assert np.array_equal(getattr(s, f), getattr(s0, f))
+    B.adam_step(s, np.ones((9, 10), np.float32), m, v, cfg)
+    assert np.allclose(s.rot - s0.rot, -1e-3, rtol=1e-4)
+    assert np.allclose(s.cr - s0.cr, -2.5e-3, rtol=1e-4)
+    for t in range(2, 60):
+        prev = s.rot.copy()
+        B.adam_step(s, np.ones((9, 10), np.float32), m, v, B.adam_config(t, 100, math.hypot(16, 16)))
+    assert np.allclose(prev - s.rot, 1e-3, rtol=1e-3)
+
+
+# ------------------------------------------------------------------ budget controller
+def _budgets(P, n, m):
+    return [B.Budget(n, m), P.BudgetController(n, m)]
+
+
+def _ema(b):
+    return b.ema if isinstance(b, B.Budget) else b.state()["ema"]
+
+
+def test_budget_ema_kats(P):
+    """SPEC.md:415-417."""
+    for b in _budgets(P, 100, 1000):
+        for t, x in enumerate((1.0, 2.0, 3.0), 1):
+            b.record_loss(t, x)
+        assert _ema(b) == pytest.approx(1.29)
+        with pytest.raises(ValueError):
+            b.record_loss(4, 0.0)
+    for b in _budgets(P, 100, 1000):
+        for t in range(1, 20):
+            b.record_loss(t, 0.7)
+            assert _ema(b) == pytest.approx(0.7)
+
+
+def test_fit_power_exponent_kats(P):
+    """SPEC.md:425-427 and acceptance #4."""
+    t = np.arange(100, 201, dtype=np.float64)
+    for fn in (B.fit_power_exponent, P.fit_power_exponent):
+        assert abs(fn(t, 2.0 * t ** -0.8) - 0.8) < 1e-9
+        assert abs(fn(t, np.full_like(t, 3.0))) < 1e-12
+        assert abs(fn([1.0, math.e], [1.0, math.exp(-1)]) - 1.0) < 1e-12
+        rng = np.random.default_rng(0)
+        for a in (0.3, 0.8, 1.5):
+            y = t ** -a * np.exp(rng.normal(0, 0.01, t.shape))
+            assert abs(fn(t, y) - a) <= 0.05 * a
+        with pytest.raises(ValueError):
+            fn([1.0], [1.0])
+
+
+def test_budget_at_kats(P):
+    """SPEC.md:445-447 and acceptance #3."""
+    for b in _budgets(P, 100, 1100):
+        assert b.budget_at(1.0) == 100 and b.budget_at(100.0) == 1100 and b.budget_at(50.5) == 600
+        assert b.budget_at(-5.0) == 100 and b.budget_at(1e9) == 1100
+
+
+def test_budget_properties_match_oracle(P):
+    """alpha in [0.1, 2], m_adaptive in [0.5M, 1.5M]; product == oracle on random streams."""
+    rng = np.random.default_rng(3)
+    for trial in range(10):
+        n0, m = 1000.0, float(rng.integers(2000, 50000))
+        ob, pb = B.Budget(n0, m), P.BudgetController(n0, m)
+        loss = 1.0
+        for t in range(1, 1500):
+            loss *= math.exp(rng.normal(-0.002 if trial % 2 else 0.003, 0.05))
+            ob.record_loss(t, loss)
+            pb.record_loss(t, loss)
+            if t % 20 == 0:
+                ob.update(t)
+                pb.update(t)
+                st = pb.state()
+                assert 0.1 <= ob.alpha <= 2.0 and 0.5 * m <= ob.m_adaptive <= 1.5 * m
+                assert st["alpha"] == pytest.approx(ob.alpha, abs=1e-12)
+                assert st["m_adaptive"] == pytest.approx(ob.m_adaptive, abs=1e-9)
+                tn = B.budget_t_norm(t, 300, 3000)
+                assert tn == P.budget_t_norm(t, 300, 3000)
+                assert ob.budget_at(tn) == pb.budget_at(tn)
+    for _ in range(2000):
+        b = P.BudgetController(float(rng.integers(1, 1000)), float(rng.integers(1000, 5000)))
+        ts = np.sort(rng.uniform(1, 100, 5))
+        vals = [b.budget_at(x) for x in ts]
+        assert all(vals[i] <= vals[i + 1] for i in range(4))
+
+
+# ------------------------------------------------------------------ densifier
+def _stat_scene(rng, n):
+    s = B.synthetic_scene(int(rng.integers(1 << 30)), n, 64, 64)
+    s.ensure_stats()
+    s.accum[:] = rng.integers(0, 4, n)
+    s.visit[:] = rng.integers(0, 12, n)
+    s.window[:] = rng.integers(0, 8, n)
+    s.tau_v[:] = rng.choice([1.0, 2.5, 5.0, 8.0], n)
+    s.pos_acc[:] = (rng.random(n) * 6e-4 * s.accum).astype(np.float32)
+    s.col_acc[:] = (rng.random(n) * 6e-2 * s.accum).astype(np.float32)
+    s.rop[:] = rng.uniform(-6, 3, n).astype(np.float32)
+    return s
+
+
+def test_densify_truth_table():
+    """Acceptance #7: gating vs a brute-force predicate, both coin outcomes."""
+    cfg = B.densify_config(2e-4)
+    rng = np.random.default_rng(5)
+    s = _stat_scene(rng, 1000)
+    alpha = 1.0 / (1.0 + np.exp(-s.rop.astype(np.float64)))
+    for coin in (False, True):
+        cand, n = B.select_candidates(s, cfg, coin)
+        cnt = s.accum.astype(np.float32)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            ap = s.pos_acc / cnt
+            ac = s.col_acc / cnt
+        ref = (s.accum > 0) & (s.visit > s.tau_v) & (alpha >= 0.05 - 1e-9) & (
+            (ap > np.float32(2e-4)) | (coin & (ac > np.float32(0.01) * np.float32(2e-4))))
+        assert np.array_equal(cand.astype(bool), ref) and n == ref.sum()
+
+
+def test_spawn_and_prune_kats():
+    """SPEC.md:335-347."""
+    cfg = B.densify_config(2e-4)
+    rng = np.random.default_rng(9)
+    # budget_remaining = 0 -> no spawn, model unchanged apart from the reset
+    s = _stat_scene(rng, 200)
+    s.rop[:] = 2.0
+    out, spawned, pruned, _, _ = B.densify_event(s, 400, cfg, 200, B.Pcg32(3))
+    assert spawned == 0 and pruned == 0 and out.n == 200 and np.array_equal(out.px, s.px)
+    # 10 candidates, budget 4 -> top 4 by averaged positional norm
+    s = _stat_scene(rng, 10)
+    s.accum[:] = 1
+    s.visit[:] = 10
+    s.tau_v[:] = 1.0
+    s.rop[:] = 2.0
+    s.pos_acc[:] = np.linspace(3e-4, 9e-4, 10).astype(np.float32)[rng.permutation(10)]
+    cand, n = B.select_candidates(s, cfg, False)
+    assert n == 10
+    capped = B.cap_candidates(s, cand, 4)
+    assert set(np.nonzero(capped)[0]) == set(np.argsort(-s.pos_acc)[:4])
+    capped0 = B.cap_candidates(s, cand, 0)
+    assert capped0.sum() == 0
+    # 1 candidate, budget 100: child inside the parent's 1-sigma ellipse
+    base = _stat_scene(rng, 1)
+    base.accum[:] = 1
+    base.visit[:] = 10
+    base.tau_v[:] = 1
+    base.rop[:] = 2.0
+    base.pos_acc[:] = 1e-3
+    base.id[:] = 0
+    base.next_id = 1
+    sc, spawned, pruned, ncand, _ = B.densify_event(base, 4, cfg, 100, B.Pcg32(1, 1))
+    assert spawned == 1 and sc.n == 2 and sc.next_id == 2 and sc.id[1] == 1
+    c = 1
+    R = np.array([[math.cos(sc.rot[0]), -math.sin(sc.rot[0])], [math.sin(sc.rot[0]), math.cos(sc.rot[0])]])
+    S = np.diag([math.exp(sc.lsx[0]), math.exp(sc.lsy[0])])
+    d = np.linalg.solve(R @ S, np.array([sc.px[c] - sc.px[0], sc.py[c] - sc.py[0]], np.float64))
+    assert np.linalg.norm(d) <= 1.0 + 1e-5
+    assert sc.lsx[c] == np.float32(sc.lsx[0] - np.float32(math.log(2)))
+    assert abs(1 / (1 + math.exp(-sc.rop[c])) - 0.1) < 1e-6
+    assert sc.accum[0] == 0 and sc.pos_acc[0] == 0  # accumulators reset after the event
+    # prune: all 0.9 -> none removed; all below the floor -> empty
+    s = _stat_scene(rng, 50)
+    s.rop[:] = math.log(0.9 / 0.1)
+    assert B.densify_event(s, 50, cfg, 0, B.Pcg32(2))[2] == 0
+    s = _stat_scene(rng, 50)
+    s.rop[:] = -8.0
+    out, sp, pr, _, _ = B.densify_event(s, 50, cfg, 0, B.Pcg32(2))
+    assert out.n == 0 and pr == 50
+    # mixed: removed count equals an independent scan
+    s = _stat_scene(rng, 300)
+    expect = int((1 / (1 + np.exp(-s.rop.astype(np.float64))) < 0.005).sum())
+    assert B.densify_event(s, 300, cfg, 0, B.Pcg32(2))[2] == expect
+
+
+def test_visit_audit_kats():
+    """SPEC.md:355-357."""
+    s = B.synthetic_scene(1, 3, 8, 8)
+    s.ensure_stats()
+    s.window[:] = [10, 3, 0]
+    s.tau_v[:] = [8.0, 8.0, 1.0]
+    B.visit_audit(s)
+    assert list(s.tau_v) == [8.0, 4.0, 1.0] and list(s.window) == [0, 0, 0]
+
+
+# ------------------------------------------------------------------ product host pieces
+def test_product_pcg_and_generator_match_oracle(P):
+    a, b = B.Pcg32(42, 54), P.Pcg32(42, 54)
+    for _ in range(100):
+        assert a.uniform() == b.uniform()
+    a.advance(1000)
+    b.advance(1000)
+    assert a.uniform() == b.uniform()
+    r1 = B.Pcg32(7)
+    r2 = B.Pcg32(7)
+    for _ in range(37):
+        r1.uniform()
+    r2.advance(37)
+    assert r1.uniform() == r2.uniform()
+    s = B.synthetic_scene(3, 500, 100, 60)
+    m = P.GaussianModel.synthetic(3, 500, 100, 60)
+    for i, f in enumerate(B.ALL_FIELDS):
+        assert np.array_equal(m.params[i], getattr(s, f)), f
