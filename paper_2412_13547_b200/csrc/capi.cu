@@ -733,6 +733,10 @@ int32_t tgsx_stage_tile_lists(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, i
     const int tiles = ctx->ws.tiles_x * ctx->ws.tiles_y;
     std::vector<uint32_t> hk(K);
     if (K) CK(cudaMemcpy(hk.data(), keys, K * 4, cudaMemcpyDeviceToHost));
+    for (int64_t s = 0; s < K; ++s) {
+        if (hk[s] >= (uint32_t)tiles || (s && hk[s] < hk[s - 1]))
+            return fail(ctx, TGSX_ESTATE, "tile keys not sorted / out of range at " + std::to_string(s));
+    }
     if (offsets) {
         std::vector<uint32_t> off(tiles + 1, 0);
         for (int64_t s = 0; s < K; ++s) off[hk[s] + 1]++;
