@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -90,6 +91,14 @@ void Profiler::harvest() {
 using namespace tgsx;
 
 namespace {
+
+bool debug_checks() {
+    static const bool on = [] {
+        const char* e = std::getenv("TGSX_DEBUG_CHECKS");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 
 int32_t fail(tgsx_ctx* ctx, int32_t code, const std::string& msg) {
     if (ctx) ctx->err = msg;
@@ -239,12 +248,60 @@ int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t*
         StageTimer t(ctx, kStDuplicate);
         CK(launch_duplicate(ctx, m, W, H, key_bits));
     }
+    const bool dbg = debug_checks();
+    if (dbg) {
+        // host validation of every binning stage (TGSX_DEBUG_CHECKS=1)
+        const int64_t n = m->n;
+        std::vector<uint32_t> perm(n), rank_of(n), touched(n), off(n), keys(K), hist(4 * 256);
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (n) {
+            CK(cudaMemcpy(perm.data(), m->perm.p, n * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(rank_of.data(), m->rank_of.p, n * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(touched.data(), ws.touched.p, n * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(off.data(), ws.pair_off.p, n * 4, cudaMemcpyDeviceToHost));
+        }
+        if (K) CK(cudaMemcpy(keys.data(), ws.keys[0].p, K * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hist.data(), ws.sort_tmp.p, 4 * 256 * 4, cudaMemcpyDeviceToHost));
+        std::vector<char> seen(n, 0);
+        for (int64_t r = 0; r < n; ++r) {
+            if (perm[r] >= n || seen[perm[r]]) return fail(ctx, TGSX_ESTATE, "debug: perm not a permutation");
+            seen[perm[r]] = 1;
+            if (rank_of[perm[r]] != r) return fail(ctx, TGSX_ESTATE, "debug: rank_of != perm^-1");
+        }
+        uint64_t run = 0;
+        for (int64_t r = 0; r < n; ++r) {
+            if (off[r] != run)
+                return fail(ctx, TGSX_ESTATE, "debug: scan wrong at rank " + std::to_string(r) + " of " +
+                                                  std::to_string(n) + " got " + std::to_string(off[r]) +
+                                                  " want " + std::to_string(run));
+            run += touched[r];
+        }
+        if (run != (uint64_t)K) return fail(ctx, TGSX_ESTATE, "debug: scan total wrong");
+        std::vector<uint32_t> h2(4 * 256, 0);
+        for (int64_t s = 0; s < K; ++s) {
+            if (keys[s] >= (uint32_t)tiles)
+                return fail(ctx, TGSX_ESTATE, "debug: duplicate key out of range at " + std::to_string(s));
+            for (int p = 0; p < passes; ++p) h2[p * 256 + ((keys[s] >> (8 * p)) & 0xff)]++;
+        }
+        for (int i = 0; i < passes * 256; ++i)
+            if (h2[i] != hist[i]) return fail(ctx, TGSX_ESTATE, "debug: digit histogram wrong");
+    }
     uint32_t* k = ws.keys[0].as<uint32_t>();
     uint32_t* v = ws.vals[0].as<uint32_t>();
     {
         StageTimer t(ctx, kStSort);
         CK(sort_pairs(ctx, k, v, ws.keys[1].as<uint32_t>(), ws.vals[1].as<uint32_t>(), K, key_bits,
                       ws.sort_tmp.as<uint32_t>()));
+    }
+    if (dbg && K) {
+        std::vector<uint32_t> keys(K);
+        // the context stream is non-blocking: order the legacy-stream copy after the sort
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaMemcpy(keys.data(), k, K * 4, cudaMemcpyDeviceToHost));
+        for (int64_t s = 1; s < K; ++s)
+            if (keys[s] < keys[s - 1] || keys[s] >= (uint32_t)tiles)
+                return fail(ctx, TGSX_ESTATE, "debug: onesweep output unsorted at " + std::to_string(s) +
+                                                  " of " + std::to_string(K) + " passes " + std::to_string(passes));
     }
     {
         StageTimer t(ctx, kStRanges);
@@ -732,6 +789,8 @@ int32_t tgsx_stage_tile_lists(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, i
     if (out_k) *out_k = K;
     const int tiles = ctx->ws.tiles_x * ctx->ws.tiles_y;
     std::vector<uint32_t> hk(K);
+    // the context stream is non-blocking: order the legacy-stream copies after bin()'s kernels
+    CK(cudaStreamSynchronize(ctx->stream));
     if (K) CK(cudaMemcpy(hk.data(), keys, K * 4, cudaMemcpyDeviceToHost));
     for (int64_t s = 0; s < K; ++s) {
         if (hk[s] >= (uint32_t)tiles || (s && hk[s] < hk[s - 1]))

@@ -265,3 +265,10 @@ def test_errors_mirror_reference(P, ctx):
         dm.backward(P.DilationPattern(1, 0, 0, W, H), (0, 0, 0), np.zeros((5, 3), np.float32))
     with pytest.raises(ValueError):
         P.DilationPattern(2, 2, 0, W, H)
+
+
+def test_binning_stress_random_shapes(P):
+    """Random sizes / patterns / id orders with several live contexts: tile lists bit-exact vs the
+    oracle on every iteration (tests/stress_binning.py)."""
+    from tests import stress_binning
+    assert stress_binning.main(60) == 0
