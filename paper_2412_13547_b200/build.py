@@ -85,6 +85,34 @@ def build(verbose: bool = False, extra=(), force: bool = False) -> str:
     return LIB
 
 
+REF_INCLUDE = "/root/reference/proj/core/include"
+SHIM_BIN = os.path.join(os.path.dirname(HERE), "tests", "_bin", "shim_check")
+
+
+def build_shim(verbose: bool = False) -> str | None:
+    """Builds tests/_bin/shim_check: the C++ drop-in shim (shim/tgs_gpu_rasterizer.cpp) compiled
+    against the reference's public headers + linked to libtgsx. Only where the reference headers
+    exist (this container); the binary travels to the GPU box with the repo snapshot."""
+    if not os.path.isdir(REF_INCLUDE):
+        return None
+    lib = build(verbose)
+    os.makedirs(os.path.dirname(SHIM_BIN), exist_ok=True)
+    srcs = [os.path.join(HERE, "shim", "tgs_gpu_rasterizer.cpp"),
+            os.path.join(os.path.dirname(HERE), "tests", "shim_check.cpp")]
+    if os.path.exists(SHIM_BIN) and os.path.getmtime(SHIM_BIN) > max(
+            os.path.getmtime(s) for s in srcs + [lib]):
+        return SHIM_BIN
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{REF_INCLUDE}", f"-I{INCLUDE}", *srcs,
+           f"-L{HERE}", "-ltgsx", f"-Wl,-rpath,{HERE}", "-Wl,-rpath,$ORIGIN/../../paper_2412_13547_b200",
+           "-o", SHIM_BIN]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"shim build failed:\n{r.stderr}")
+    return SHIM_BIN
+
+
 if __name__ == "__main__":
     build(verbose=True, force="--force" in sys.argv,
           extra=["-Xptxas", "-v"] if "--ptxas" in sys.argv else ())
