@@ -34,9 +34,12 @@ int main(int argc, char** argv) {
     const int P = pat.active_count();
     std::vector<tgs::Vec3<float>> dl(P);
     tgs::Pcg32 r2(9, 1);
-    for (auto& v : dl)
-        v = tgs::Vec3<float>((float)r2.uniform_in(-1e-3, 1e-3), (float)r2.uniform_in(-1e-3, 1e-3),
-                             (float)r2.uniform_in(-1e-3, 1e-3));
+    for (auto& v : dl) {  // explicit draw order (argument evaluation order is unspecified)
+        const float x = (float)r2.uniform_in(-1e-3, 1e-3);
+        const float y = (float)r2.uniform_in(-1e-3, 1e-3);
+        const float z = (float)r2.uniform_in(-1e-3, 1e-3);
+        v = tgs::Vec3<float>(x, y, z);
+    }
     auto gs = tgs::backward<float>(model, pat, tgs::Vec3<float>(0.1f, 0.2f, 0.3f), dl);
     int status = 0;
     try {  // the reference's rank-count check must still throw std::invalid_argument
