@@ -203,28 +203,14 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
             if (done) col = 0;
             const uint32_t cbase = sbase + c0 * kRec;
             const uint32_t lbase = (uint32_t)(bstart + c0 + 1);
-            // per-lane front-to-back walk; the next record is prefetched during the blend
-            int k = col ? __ffs(col) - 1 : 0;
-            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-            float cz = 0.f;
-            if (col) {
-                const uint32_t ad = cbase + k * kRec;
-                a = lds_f4(ad);
-                b = lds_f4(ad + 16);
-                cz = lds_f1(ad + 32);
-            }
             while (__any_sync(kFull, col)) {
-                uint32_t coln = col & (col - 1);
-                const int kn = coln ? __ffs(coln) - 1 : 0;
-                float4 an = a, bn = b;
-                float czn = cz;
-                if (coln) {
-                    const uint32_t ad = cbase + kn * kRec;
-                    an = lds_f4(ad);
-                    bn = lds_f4(ad + 16);
-                    czn = lds_f1(ad + 32);
-                }
                 if (col) {
+                    const int k = __ffs(col) - 1;
+                    col &= col - 1;
+                    const uint32_t ad = cbase + k * kRec;
+                    const float4 a = lds_f4(ad);
+                    const float4 b = lds_f4(ad + 16);
+                    const float cz = lds_f1(ad + 32);
                     const float G = conic_gauss(a.z, a.w, b.x, __fsub_rn(pm.fx, a.x), __fsub_rn(pm.fy, a.y));
                     const float sigma = __fmul_rn(b.y, G);
                     const float w = __fmul_rn(sigma, T);
@@ -236,14 +222,9 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
                     last = lbase + k;
                     if (T < kTermT) {
                         done = true;
-                        coln = 0;
+                        col = 0;
                     }
                 }
-                col = coln;
-                k = kn;
-                a = an;
-                b = bn;
-                cz = czn;
             }
             if (__all_sync(kFull, done)) {
                 warp_done = true;
@@ -428,29 +409,15 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             }
             __syncwarp();
             uint32_t visb = 0;
-            // phase 1: per pixel, back to front; the next splat's record is prefetched while
-            // the current one is processed (hides the shared-memory latency of the chain)
-            int k = col ? 31 - __clz(col) : 0;
-            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bb = a;
-            float cz = 0.f;
-            if (col) {
-                const uint32_t ad = rbase + k * kRec;
-                a = lds_f4(ad);
-                bb = lds_f4(ad + 16);
-                cz = lds_f1(ad + 32);
-            }
+            // phase 1: per pixel, back to front
             while (__any_sync(kFull, col)) {
-                const uint32_t coln = col ? (col ^ (1u << k)) : 0u;
-                const int kn = coln ? 31 - __clz(coln) : 0;
-                float4 an = a, bn = bb;
-                float czn = cz;
-                if (coln) {
-                    const uint32_t ad = rbase + kn * kRec;
-                    an = lds_f4(ad);
-                    bn = lds_f4(ad + 16);
-                    czn = lds_f1(ad + 32);
-                }
                 if (col) {
+                    const int k = 31 - __clz(col);
+                    col ^= 1u << k;
+                    const uint32_t ad = rbase + k * kRec;
+                    const float4 a = lds_f4(ad);
+                    const float4 bb = lds_f4(ad + 16);
+                    const float cz = lds_f1(ad + 32);
                     const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(fxg, a.x), __fsub_rn(fyg, a.y));
                     const float sigma = __fmul_rn(bb.y, G);
                     const float ir = fast_rcp(__fsub_rn(1.0f, sigma));  // inv_rest
@@ -466,11 +433,6 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
                     sts_f1(wbase + o, w);
                     if (w > kMinVisitW) visb |= 1u << k;
                 }
-                col = coln;
-                k = kn;
-                a = an;
-                bb = bn;
-                cz = czn;
             }
             S.st[g][lane] = make_float2(T, gS);
             vism |= __reduce_or_sync(kFull, visb);
