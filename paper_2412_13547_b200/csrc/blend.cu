@@ -443,8 +443,11 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
             const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
             const uint32_t gb = smem_addr(S.gcur);
+#ifndef TGSX_EXP_P2_BLOCKS  // experiment knob (cost attribution); 8 = all 32 pixels
+#define TGSX_EXP_P2_BLOCKS 8
+#endif
 #pragma unroll
-            for (int l4 = 0; l4 < 8; ++l4) {
+            for (int l4 = 0; l4 < TGSX_EXP_P2_BLOCKS; ++l4) {
                 const uint32_t sw = 16u * (uint32_t)(l4 ^ (lane & 7));
                 const float4 u4 = lds_f4(ur + sw);
                 const float4 w4 = lds_f4(wr + sw);
