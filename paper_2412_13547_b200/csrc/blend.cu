@@ -409,30 +409,33 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             }
             __syncwarp();
             uint32_t visb = 0;
-            // phase 1: per pixel, back to front
+            // phase 1: per pixel, back to front. Branch-free body: lanes without work compute on
+            // record 0 and discard (cheaper than divergence + reconvergence per iteration).
             while (__any_sync(kFull, col)) {
-                if (col) {
-                    const int k = 31 - __clz(col);
-                    col ^= 1u << k;
-                    const uint32_t ad = rbase + k * kRec;
-                    const float4 a = lds_f4(ad);
-                    const float4 bb = lds_f4(ad + 16);
-                    const float cz = lds_f1(ad + 32);
-                    const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(fxg, a.x), __fsub_rn(fyg, a.y));
-                    const float sigma = __fmul_rn(bb.y, G);
-                    const float ir = fast_rcp(__fsub_rn(1.0f, sigma));  // inv_rest
-                    const float Ti = T * ir;
-                    const float w = sigma * Ti;
-                    const float gc = gv.x * bb.z + gv.y * bb.w + gv.z * cz;
-                    // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
-                    const float dsig = Ti * gc - gS * ir;
-                    gS = __fmaf_rn(gc, w, gS);
-                    T = Ti;
+                const bool has = col != 0u;
+                const int k = 31 - __clz(col | 1u);
+                col &= ~(1u << k);
+                const uint32_t ad = rbase + k * kRec;
+                const float4 a = lds_f4(ad);
+                const float4 bb = lds_f4(ad + 16);
+                const float cz = lds_f1(ad + 32);
+                const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(fxg, a.x), __fsub_rn(fyg, a.y));
+                const float sigma = __fmul_rn(bb.y, G);
+                const float ir = fast_rcp(__fsub_rn(1.0f, sigma));  // inv_rest
+                const float Ti = T * ir;
+                const float w = sigma * Ti;
+                const float gc = gv.x * bb.z + gv.y * bb.w + gv.z * cz;
+                // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
+                const float dsig = Ti * gc - gS * ir;
+                const float gSn = __fmaf_rn(gc, w, gS);
+                gS = has ? gSn : gS;
+                T = has ? Ti : T;
+                if (has) {
                     const uint32_t o = rec_off(k, lane);
                     sts_f1(ubase + o, dsig * G);
                     sts_f1(wbase + o, w);
-                    if (w > kMinVisitW) visb |= 1u << k;
                 }
+                visb |= (has && w > kMinVisitW) ? (1u << k) : 0u;
             }
             S.st[g][lane] = make_float2(T, gS);
             vism |= __reduce_or_sync(kFull, visb);
@@ -446,30 +449,41 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
 #ifndef TGSX_EXP_P2_BLOCKS  // experiment knob (cost attribution); 8 = all 32 pixels
 #define TGSX_EXP_P2_BLOCKS 8
 #endif
+            // separable moments: per pixel row r (eta_r fixed) accumulate R = sum u,
+            // Rx = sum u xi, Rxx = sum u xi^2 over the row's 8 columns, then fold the row in
+            // with eta_r (3 FFMA per pixel + 6 per row instead of 6 per pixel)
 #pragma unroll
-            for (int l4 = 0; l4 < TGSX_EXP_P2_BLOCKS; ++l4) {
-                const uint32_t sw = 16u * (uint32_t)(l4 ^ (lane & 7));
-                const float4 u4 = lds_f4(ur + sw);
-                const float4 w4 = lds_f4(wr + sw);
-                const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
-                const float ww[4] = {w4.x, w4.y, w4.z, w4.w};
+            for (int row = 0; row < TGSX_EXP_P2_BLOCKS / 2; ++row) {
+                float R = 0.f, Rx = 0.f, Rxx = 0.f;
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int l = 4 * l4 + e;
-                    const float xi = (float)(l & 7) - 3.5f;
-                    const float eta = (float)(l >> 3) - 1.5f;
-                    const float u = uu[e], w = ww[e];
-                    const float4 gl = lds_f4(gb + 16 * l);
-                    a0 += u;
-                    ax1 = __fmaf_rn(u, xi, ax1);
-                    ay1 = __fmaf_rn(u, eta, ay1);
-                    axx = __fmaf_rn(u, xi * xi, axx);
-                    axy = __fmaf_rn(u, xi * eta, axy);
-                    ayy = __fmaf_rn(u, eta * eta, ayy);
-                    q0 = __fmaf_rn(w, gl.x, q0);
-                    q1 = __fmaf_rn(w, gl.y, q1);
-                    q2 = __fmaf_rn(w, gl.z, q2);
+                for (int half = 0; half < 2; ++half) {
+                    const int l4 = 2 * row + half;
+                    const uint32_t sw = 16u * (uint32_t)(l4 ^ (lane & 7));
+                    const float4 u4 = lds_f4(ur + sw);
+                    const float4 w4 = lds_f4(wr + sw);
+                    const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+                    const float ww[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int l = 4 * l4 + e;
+                        const float xi = (float)(l & 7) - 3.5f;
+                        const float u = uu[e], w = ww[e];
+                        const float4 gl = lds_f4(gb + 16 * l);
+                        R += u;
+                        Rx = __fmaf_rn(u, xi, Rx);
+                        Rxx = __fmaf_rn(u, xi * xi, Rxx);
+                        q0 = __fmaf_rn(w, gl.x, q0);
+                        q1 = __fmaf_rn(w, gl.y, q1);
+                        q2 = __fmaf_rn(w, gl.z, q2);
+                    }
                 }
+                const float eta = (float)row - 1.5f;
+                a0 += R;
+                ax1 += Rx;
+                ay1 = __fmaf_rn(R, eta, ay1);
+                axx += Rxx;
+                axy = __fmaf_rn(Rx, eta, axy);
+                ayy = __fmaf_rn(R, eta * eta, ayy);
             }
             const float dx = (float)(gx * 8) + 3.5f - hx, dy = (float)(gy * 4) + 1.5f - hy;
             m0 += a0;
