@@ -203,26 +203,44 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
             if (done) col = 0;
             const uint32_t cbase = sbase + c0 * kRec;
             const uint32_t lbase = (uint32_t)(bstart + c0 + 1);
+            // two passing splats per iteration: their Gaussians are independent (ILP), only the
+            // T / colour update is serial; the second is dropped if the first terminates the ray
             while (__any_sync(kFull, col)) {
                 if (col) {
-                    const int k = __ffs(col) - 1;
+                    const int k1 = __ffs(col) - 1;
                     col &= col - 1;
-                    const uint32_t ad = cbase + k * kRec;
-                    const float4 a = lds_f4(ad);
-                    const float4 b = lds_f4(ad + 16);
-                    const float cz = lds_f1(ad + 32);
-                    const float G = conic_gauss(a.z, a.w, b.x, __fsub_rn(pm.fx, a.x), __fsub_rn(pm.fy, a.y));
-                    const float sigma = __fmul_rn(b.y, G);
-                    const float w = __fmul_rn(sigma, T);
-                    C0 = __fmaf_rn(w, b.z, C0);
-                    C1 = __fmaf_rn(w, b.w, C1);
-                    C2 = __fmaf_rn(w, cz, C2);
-                    T = __fmul_rn(T, __fsub_rn(1.0f, sigma));
+                    const bool h2 = col != 0u;
+                    const int k2 = h2 ? __ffs(col) - 1 : k1;
+                    col &= col - 1;
+                    const uint32_t ad1 = cbase + k1 * kRec, ad2 = cbase + k2 * kRec;
+                    const float4 a1 = lds_f4(ad1), a2 = lds_f4(ad2);
+                    const float4 b1 = lds_f4(ad1 + 16), b2 = lds_f4(ad2 + 16);
+                    const float cz1 = lds_f1(ad1 + 32), cz2 = lds_f1(ad2 + 32);
+                    const float G1 = conic_gauss(a1.z, a1.w, b1.x, __fsub_rn(pm.fx, a1.x), __fsub_rn(pm.fy, a1.y));
+                    const float G2 = conic_gauss(a2.z, a2.w, b2.x, __fsub_rn(pm.fx, a2.x), __fsub_rn(pm.fy, a2.y));
+                    const float s1 = __fmul_rn(b1.y, G1), s2 = __fmul_rn(b2.y, G2);
+                    const float w1 = __fmul_rn(s1, T);
+                    C0 = __fmaf_rn(w1, b1.z, C0);
+                    C1 = __fmaf_rn(w1, b1.w, C1);
+                    C2 = __fmaf_rn(w1, cz1, C2);
+                    T = __fmul_rn(T, __fsub_rn(1.0f, s1));
                     ++ops;
-                    last = lbase + k;
+                    last = lbase + k1;
                     if (T < kTermT) {
                         done = true;
                         col = 0;
+                    } else if (h2) {
+                        const float w2 = __fmul_rn(s2, T);
+                        C0 = __fmaf_rn(w2, b2.z, C0);
+                        C1 = __fmaf_rn(w2, b2.w, C1);
+                        C2 = __fmaf_rn(w2, cz2, C2);
+                        T = __fmul_rn(T, __fsub_rn(1.0f, s2));
+                        ++ops;
+                        last = lbase + k2;
+                        if (T < kTermT) {
+                            done = true;
+                            col = 0;
+                        }
                     }
                 }
             }
@@ -409,33 +427,50 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             }
             __syncwarp();
             uint32_t visb = 0;
-            // phase 1: per pixel, back to front. Branch-free body: lanes without work compute on
-            // record 0 and discard (cheaper than divergence + reconvergence per iteration).
+            // phase 1: per pixel, back to front, two contributions per iteration (k1 > k2): the
+            // Gaussians / reciprocals are independent (ILP); only the T and g.S recursions are
+            // serial. Branch-free: lanes without work compute on record 0 and discard.
             while (__any_sync(kFull, col)) {
-                const bool has = col != 0u;
-                const int k = 31 - __clz(col | 1u);
-                col &= ~(1u << k);
-                const uint32_t ad = rbase + k * kRec;
-                const float4 a = lds_f4(ad);
-                const float4 bb = lds_f4(ad + 16);
-                const float cz = lds_f1(ad + 32);
-                const float G = conic_gauss(a.z, a.w, bb.x, __fsub_rn(fxg, a.x), __fsub_rn(fyg, a.y));
-                const float sigma = __fmul_rn(bb.y, G);
-                const float ir = fast_rcp(__fsub_rn(1.0f, sigma));  // inv_rest
-                const float Ti = T * ir;
-                const float w = sigma * Ti;
-                const float gc = gv.x * bb.z + gv.y * bb.w + gv.z * cz;
+                const bool h1 = col != 0u;
+                const int k1 = 31 - __clz(col | 1u);
+                col &= ~(1u << k1);
+                const bool h2 = col != 0u;
+                const int k2 = 31 - __clz(col | 1u);
+                col &= ~(1u << k2);
+                const uint32_t ad1 = rbase + k1 * kRec, ad2 = rbase + k2 * kRec;
+                const float4 a1 = lds_f4(ad1), a2 = lds_f4(ad2);
+                const float4 b1 = lds_f4(ad1 + 16), b2 = lds_f4(ad2 + 16);
+                const float cz1 = lds_f1(ad1 + 32), cz2 = lds_f1(ad2 + 32);
+                const float G1 = conic_gauss(a1.z, a1.w, b1.x, __fsub_rn(fxg, a1.x), __fsub_rn(fyg, a1.y));
+                const float G2 = conic_gauss(a2.z, a2.w, b2.x, __fsub_rn(fxg, a2.x), __fsub_rn(fyg, a2.y));
+                const float s1 = __fmul_rn(b1.y, G1), s2 = __fmul_rn(b2.y, G2);
+                const float ir1 = fast_rcp(__fsub_rn(1.0f, s1));  // inv_rest
+                const float ir2 = fast_rcp(__fsub_rn(1.0f, s2));
+                const float gc1 = gv.x * b1.z + gv.y * b1.w + gv.z * cz1;
+                const float gc2 = gv.x * b2.z + gv.y * b2.w + gv.z * cz2;
                 // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
-                const float dsig = Ti * gc - gS * ir;
-                const float gSn = __fmaf_rn(gc, w, gS);
-                gS = has ? gSn : gS;
-                T = has ? Ti : T;
-                if (has) {
-                    const uint32_t o = rec_off(k, lane);
-                    sts_f1(ubase + o, dsig * G);
-                    sts_f1(wbase + o, w);
+                const float T1 = T * ir1;
+                const float w1 = s1 * T1;
+                const float ds1 = T1 * gc1 - gS * ir1;
+                const float gS1 = __fmaf_rn(gc1, w1, gS);
+                const float Tb = h1 ? T1 : T, gSb = h1 ? gS1 : gS;
+                const float T2 = Tb * ir2;
+                const float w2 = s2 * T2;
+                const float ds2 = T2 * gc2 - gSb * ir2;
+                const float gS2 = __fmaf_rn(gc2, w2, gSb);
+                T = h2 ? T2 : Tb;
+                gS = h2 ? gS2 : gSb;
+                if (h1) {
+                    const uint32_t o = rec_off(k1, lane);
+                    sts_f1(ubase + o, ds1 * G1);
+                    sts_f1(wbase + o, w1);
                 }
-                visb |= (has && w > kMinVisitW) ? (1u << k) : 0u;
+                if (h2) {
+                    const uint32_t o = rec_off(k2, lane);
+                    sts_f1(ubase + o, ds2 * G2);
+                    sts_f1(wbase + o, w2);
+                }
+                visb |= ((h1 && w1 > kMinVisitW) ? (1u << k1) : 0u) | ((h2 && w2 > kMinVisitW) ? (1u << k2) : 0u);
             }
             S.st[g][lane] = make_float2(T, gS);
             vism |= __reduce_or_sync(kFull, visb);
