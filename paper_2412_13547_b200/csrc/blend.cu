@@ -58,7 +58,7 @@ struct BlendParams {
     float* dLdC;
     float* block_loss;
     float loss_scale;
-    float4* partial;               // backward output, 3 float4 per pair slot
+    Partials partial;              // backward output, one entry per pair slot
 };
 
 struct TileGeo {
@@ -374,10 +374,9 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
     // list entries past every pixel's last contributor: zero partials
     for (int j = (int)maxlast + lane; j < count; j += 32) {
         const uint32_t slot = pair_slot(prm.prep[prm.items[range.x + j]], geo.tx, geo.ty);
-        float4* dst = prm.partial + 3 * (size_t)slot;
-        dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        dst[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+        prm.partial.a[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
+        prm.partial.b[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
+        prm.partial.c[slot] = make_float2(0.f, 0.f);
     }
 
     const int nch = ((int)maxlast + 31) / 32;
@@ -529,7 +528,7 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             myy += ayy + 2.f * dy * ay1 + dy * dy * a0;
         }
         if (jvalid) {
-            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
             if (m0 != 0.f || mxx != 0.f || myy != 0.f || q0 != 0.f || q1 != 0.f || q2 != 0.f) {
                 constexpr float iK = 1.0f / kNegHalfLog2e;
                 const float ia = ja.z * iK, ib = 0.5f * ja.w * iK, ic = jb.x * iK;
@@ -548,11 +547,9 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
                                  ha * (ia * ib * sxx + (ia * ic + ib * ib) * sxy + ib * ic * syy));
                 r1 = make_float4(ha * (ib * ib * sxx + 2.f * ib * ic * sxy + ic * ic * syy), m0, q0, q1);
             }
-            r2 = make_float4(q2, ((vism >> lane) & 1u) ? 1.0f : 0.0f, 0.f, 0.f);
-            float4* dst = prm.partial + 3 * (size_t)slot;
-            dst[0] = r0;
-            dst[1] = r1;
-            dst[2] = r2;
+            prm.partial.a[slot] = r0;
+            prm.partial.b[slot] = r1;
+            prm.partial.c[slot] = make_float2(q2, ((vism >> lane) & 1u) ? 1.0f : 0.0f);
         }
     }
 }
@@ -580,7 +577,7 @@ BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* ite
     prm.counters = ws.counters.as<unsigned long long>();
     prm.dLdC = ws.dLdC.as<float>();
     prm.block_loss = ws.block_loss.as<float>();
-    prm.partial = ws.partial.as<float4>();
+    prm.partial = Partials::at(ws.partial.p, ws.pair_cap);
     return prm;
 }
 

@@ -241,9 +241,11 @@ int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t*
         CK(ws.keys[i].ensure(std::max<int64_t>(K, 1) * 4));
         CK(ws.vals[i].ensure(std::max<int64_t>(K, 1) * 4));
     }
-    CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 48));
-    const int64_t sblocks = (K + 4095) / 4096;
-    CK(ws.sort_tmp.ensure(4 * 256 * 4 + 64 + (size_t)std::max(passes, 1) * sblocks * 256 * 4));
+    CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
+    ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
+    // sized once here: duplicate writes the digit histograms at its head and sort_pairs must
+    // not reallocate it afterwards
+    CK(ws.sort_tmp.ensure(sort_scratch_bytes(K, key_bits)));
     {
         StageTimer t(ctx, kStDuplicate);
         CK(launch_duplicate(ctx, m, W, H, key_bits));

@@ -48,7 +48,7 @@ struct ChainParams {
     int64_t cap, n;
     const uint32_t* rank_of;
     const Prepared* prep;
-    const float4* partial;
+    Partials partial;
     float* screen;  // [10][cap] or null
     // stats
     float* pos_acc;
@@ -70,14 +70,27 @@ __global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cp.n) return;
     const int64_t cap = cp.cap;
-    const uint32_t r = cp.rank_of[i];
-    const uint4 d = cp.prep[r].d;
+    const float* __restrict__ params = cp.params;
+    // independent loads first (memory-level parallelism): the raw parameters the chain rule
+    // needs, then the dependent gather chain rank -> prepared record -> pair partials
+    const float rot = __ldg(params + 2 * cap + i);
+    const float lx = __ldg(params + 3 * cap + i), ly = __ldg(params + 4 * cap + i);
+    const float rop = __ldg(params + 5 * cap + i);
+    float raw_c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) raw_c[k] = __ldg(params + (6 + k) * cap + i);
+    const uint32_t r = __ldg(cp.rank_of + i);
+    const uint4 d = __ldg(&cp.prep[r].d);
     float s[10];
 #pragma unroll
     for (int k = 0; k < 10; ++k) s[k] = 0.f;
-    const float4* src = cp.partial + 3 * (size_t)d.z;
+    // merge in tile order (rasterizer.cpp:301-319): the pair slots of one splat are contiguous
+    const float4* __restrict__ pa = cp.partial.a + d.z;
+    const float4* __restrict__ pb = cp.partial.b + d.z;
+    const float2* __restrict__ pc = cp.partial.c + d.z;
     for (uint32_t t = 0; t < d.w; ++t) {
-        const float4 a = src[3 * t], b = src[3 * t + 1], c = src[3 * t + 2];
+        const float4 a = __ldcs(pa + t), b = __ldcs(pb + t);
+        const float2 c = __ldcs(pc + t);
         s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
         s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
         s[8] += c.x;
@@ -89,8 +102,6 @@ __global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
     }
     const bool visited = s[9] > 0.f;
     // chain rule (rasterizer.cpp:324-346)
-    const float rot = cp.params[2 * cap + i];
-    const float lx = cp.params[3 * cap + i], ly = cp.params[4 * cap + i];
     float g[9];
     g[0] = s[0];
     g[1] = s[1];
@@ -112,11 +123,11 @@ __global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
         // 2 b (m00 s s - 2 m01 cs + m11 c c)
         g[4] = fmul(fmul(2.0f, b), fadd(fsub(fmul(fmul(m00, sn), sn), fmul(fmul(2.0f, m01), cs)),
                                         fmul(fmul(m11, c), c)));
-        const float al = activate_cr(cp.params[5 * cap + i]);
+        const float al = activate_cr(rop);
         g[5] = fmul(s[5], fmul(al, fsub(1.0f, al)));
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            const float ck = activate_cr(cp.params[(6 + k) * cap + i]);
+            const float ck = activate_cr(raw_c[k]);
             g[6 + k] = fmul(s[6 + k], fmul(ck, fsub(1.0f, ck)));
         }
     }
@@ -200,7 +211,7 @@ cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool upda
     cp.n = m->n;
     cp.rank_of = m->rank_of.as<uint32_t>();
     cp.prep = ctx->ws.prep.as<Prepared>();
-    cp.partial = ctx->ws.partial.as<float4>();
+    cp.partial = Partials::at(ctx->ws.partial.p, ctx->ws.pair_cap);
     cp.screen = m->screen.as<float>();
     cp.pos_acc = m->pos_acc.as<float>();
     cp.col_acc = m->col_acc.as<float>();

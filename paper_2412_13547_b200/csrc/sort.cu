@@ -27,7 +27,7 @@ constexpr int kScanIT = 8;
 constexpr int kScanTile = kScanBT * kScanIT;
 
 constexpr int kSortBT = 256;
-constexpr int kSortIT = 16;
+constexpr int kSortIT = 8;  // 2048 keys per block: ~60 registers, 4 blocks per SM
 constexpr int kSortTile = kSortBT * kSortIT;
 constexpr int kRadix = 256;
 
@@ -319,6 +319,13 @@ cudaError_t launch_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* o
                                                                          ticket, d_total);
     ctx->launches++;
     return cudaGetLastError();
+}
+
+// Scratch (histograms + tickets + look-back status) sort_pairs needs for n keys.
+size_t sort_scratch_bytes(int64_t n, int key_bits) {
+    const int passes = std::max((key_bits + 7) / 8, 1);
+    const int64_t blocks = (n + kSortTile - 1) / kSortTile;
+    return 4 * kRadix * sizeof(uint32_t) + 64 + (size_t)passes * blocks * kRadix * sizeof(uint32_t);
 }
 
 // Sorts (keys, vals) on the low key_bits bits. keys/vals are updated to point at whichever

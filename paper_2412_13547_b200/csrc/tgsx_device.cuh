@@ -100,6 +100,24 @@ struct __align__(16) Prepared {
     uint4 d;
 };
 
+// ------------------------------------------------------------------ backward partials
+// One entry per (tile, splat) pair slot, SoA (40 B/pair):
+//   a[s] = (d mean x, d mean y, d Sigma'00, d Sigma'01)
+//   b[s] = (d Sigma'11, d alpha, d r, d g)
+//   c[s] = (d b, visited 0/1)
+struct Partials {
+    float4* a;
+    float4* b;
+    float2* c;
+    __host__ __device__ static Partials at(void* base, int64_t cap) {
+        Partials p;
+        p.a = reinterpret_cast<float4*>(base);
+        p.b = p.a + cap;
+        p.c = reinterpret_cast<float2*>(p.b + cap);
+        return p;
+    }
+};
+
 // ------------------------------------------------------------------ blend math
 // log2(e) * -0.5: G = exp(-q/2) = exp2(q * kNegHalfLog2e). Shared by forward and backward so
 // the recomputed sigma is bit-identical (the backward's T recovery relies on it).

@@ -40,7 +40,8 @@ struct Workspace {
     DevBuf keys[2], vals[2];  // u32[K] ping-pong
     DevBuf sort_tmp;          // histograms + block status + tickets
     DevBuf ranges;            // uint2[tiles]
-    DevBuf partial;           // float4[K * 3] per-(tile, splat) gradient partials
+    DevBuf partial;           // per-(tile, splat) gradient partials, Partials SoA (40 B/pair)
+    int64_t pair_cap = 0;     // pairs the partial buffer holds
     // per-pixel
     DevBuf rgb, T, last, dLdC, target;
     DevBuf block_loss;        // float[tiles]
@@ -138,6 +139,7 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
 cudaError_t launch_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n,
                                   uint32_t* d_total);
 cudaError_t launch_duplicate(tgsx_ctx* ctx, tgsx_model* m, int W, int H, int key_bits);
+size_t sort_scratch_bytes(int64_t n, int key_bits);
 cudaError_t sort_pairs(tgsx_ctx* ctx, uint32_t*& keys, uint32_t*& vals, uint32_t* keys_alt,
                        uint32_t* vals_alt, int64_t n, int key_bits, const uint32_t* d_hist);
 cudaError_t launch_ranges(tgsx_ctx* ctx, const uint32_t* keys, int64_t K, int tiles);
