@@ -204,7 +204,11 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
             const uint32_t cbase = sbase + c0 * kRec;
             const uint32_t lbase = (uint32_t)(bstart + c0 + 1);
             // two passing splats per iteration: their Gaussians are independent (ILP), only the
-            // T / colour update is serial; the second is dropped if the first terminates the ray
+            // T / colour update is serial; the second is masked (select, no branch) when absent
+            // or when the first terminates the ray. Blend count and last contributor are derived
+            // once per chunk from the pass mask; only the (once per pixel) termination branches.
+            const uint32_t col0 = col;
+            int term_k = 32;  // bit of the terminating blend in this chunk, 32 = none
             while (__any_sync(kFull, col)) {
                 if (col) {
                     const int k1 = __ffs(col) - 1;
@@ -220,29 +224,26 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
                     const float G2 = conic_gauss(a2.z, a2.w, b2.x, __fsub_rn(pm.fx, a2.x), __fsub_rn(pm.fy, a2.y));
                     const float s1 = __fmul_rn(b1.y, G1), s2 = __fmul_rn(b2.y, G2);
                     const float w1 = __fmul_rn(s1, T);
-                    C0 = __fmaf_rn(w1, b1.z, C0);
-                    C1 = __fmaf_rn(w1, b1.w, C1);
-                    C2 = __fmaf_rn(w1, cz1, C2);
-                    T = __fmul_rn(T, __fsub_rn(1.0f, s1));
-                    ++ops;
-                    last = lbase + k1;
-                    if (T < kTermT) {
-                        done = true;
+                    const float T1 = __fmul_rn(T, __fsub_rn(1.0f, s1));
+                    const bool t1 = T1 < kTermT;
+                    const bool p2 = h2 && !t1;
+                    const float w2 = p2 ? __fmul_rn(s2, T1) : 0.f;
+                    const float T2 = p2 ? __fmul_rn(T1, __fsub_rn(1.0f, s2)) : T1;
+                    C0 = __fmaf_rn(w2, b2.z, __fmaf_rn(w1, b1.z, C0));
+                    C1 = __fmaf_rn(w2, b2.w, __fmaf_rn(w1, b1.w, C1));
+                    C2 = __fmaf_rn(w2, cz2, __fmaf_rn(w1, cz1, C2));
+                    T = T2;
+                    if (T2 < kTermT) {  // this pixel's ray terminates (break after blending)
+                        term_k = t1 ? k1 : k2;
                         col = 0;
-                    } else if (h2) {
-                        const float w2 = __fmul_rn(s2, T);
-                        C0 = __fmaf_rn(w2, b2.z, C0);
-                        C1 = __fmaf_rn(w2, b2.w, C1);
-                        C2 = __fmaf_rn(w2, cz2, C2);
-                        T = __fmul_rn(T, __fsub_rn(1.0f, s2));
-                        ++ops;
-                        last = lbase + k2;
-                        if (T < kTermT) {
-                            done = true;
-                            col = 0;
-                        }
                     }
                 }
+            }
+            if (col0) {
+                const uint32_t used = term_k < 32 ? (col0 & (kFull >> (31 - term_k))) : col0;
+                ops += __popc(used);
+                last = lbase + 31 - __clz(used);
+                if (term_k < 32) done = true;
             }
             if (__all_sync(kFull, done)) {
                 warp_done = true;

@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
     const float4* __restrict__ pb = cp.partial.b + d.z;
     const float2* __restrict__ pc = cp.partial.c + d.z;
     for (uint32_t t = 0; t < d.w; ++t) {
-        const float4 a = __ldcs(pa + t), b = __ldcs(pb + t);
-        const float2 c = __ldcs(pc + t);
+        const float4 a = pa[t], b = pb[t];
+        const float2 c = pc[t];
         s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
         s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
         s[8] += c.x;
