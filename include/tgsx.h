@@ -180,6 +180,39 @@ void tgsx_budget_state(const tgsx_budget* b, double* out);
 double tgsx_budget_t_norm(int64_t step, int64_t warmup, int64_t densify_end);
 int32_t tgsx_fit_power_exponent(const double* t, const double* y, int64_t n, double* out);
 
+/* ---------------------------------------------------------------- fit loop */
+typedef struct tgsx_trainer tgsx_trainer;
+
+/* TrainConfig. */
+typedef struct {
+    int64_t total_iters, warmup_iters, densify_interval, densify_until, batch_final_iters;
+    int32_t batch_size;               /* renders per step in the batched finale (4) */
+    int32_t dilation_p;               /* p of the dilated phases */
+    float post_densify_dilation_prob; /* 0.5 */
+    int64_t n_views;                  /* visit-audit period */
+    double m_final;                   /* budget M (0 => 1.5 x initial count) */
+    uint64_t seed;                    /* trainer PCG32 seed (stream 1) */
+    float background[3];
+    tgsx_densify_config densify;
+} tgsx_train_config;
+
+typedef struct {
+    int64_t iteration, count, budget, spawned, pruned;
+    int32_t densified, dilated;
+} tgsx_train_report;
+
+void tgsx_train_config_default(tgsx_train_config* c);
+int32_t tgsx_trainer_create(tgsx_ctx* ctx, tgsx_model* m, const tgsx_train_config* cfg,
+                            int32_t width, int32_t height, tgsx_trainer** out);
+void tgsx_trainer_destroy(tgsx_trainer* tr);
+/* One iteration of the schedule; targets[n_targets] = full-resolution W*H*3 RGB images (host
+ * or device), round-robined. */
+int32_t tgsx_trainer_step(tgsx_trainer* tr, const float* const* targets, int64_t n_targets,
+                          tgsx_train_report* report);
+/* Losses of the most recent iterations (oldest first), up to max_out. */
+int32_t tgsx_trainer_losses(tgsx_trainer* tr, float* out, int64_t max_out, int64_t* out_n);
+const tgsx_budget* tgsx_trainer_budget(const tgsx_trainer* tr);
+
 /* ---------------------------------------------------------------- utilities */
 /* Seeded synthetic scene, written into caller host arrays (n entries). */
 void tgsx_synthetic_scene(uint64_t seed, int64_t n, int32_t width, int32_t height,

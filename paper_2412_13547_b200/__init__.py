@@ -6,9 +6,11 @@ The compute path is libtgsx.so (hand-written CUDA, csrc/); this package is its P
 of the reference interface (api.py). There is no CPU fallback.
 """
 from .api import (BudgetController, Context, DeviceModel, DilationPattern, GaussianModel,  # noqa: F401
-                  GradientSet, Pcg32, RenderOptions, RenderOutput, backward, budget_t_norm,
-                  densify_config, fit_power_exponent, lowpass_bump, next_offsets, render)
+                  GradientSet, Pcg32, RenderOptions, RenderOutput, Trainer, backward,
+                  budget_t_norm, densify_config, fit_power_exponent, lowpass_bump, next_offsets,
+                  render, train_config)
 
 __all__ = ["BudgetController", "Context", "DeviceModel", "DilationPattern", "GaussianModel",
-           "GradientSet", "Pcg32", "RenderOptions", "RenderOutput", "backward", "budget_t_norm",
-           "densify_config", "fit_power_exponent", "lowpass_bump", "next_offsets", "render"]
+           "GradientSet", "Pcg32", "RenderOptions", "RenderOutput", "Trainer", "backward",
+           "budget_t_norm", "densify_config", "fit_power_exponent", "lowpass_bump", "next_offsets",
+           "render", "train_config"]

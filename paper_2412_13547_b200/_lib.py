@@ -48,6 +48,21 @@ class DensifyReport(C.Structure):
                 ("count_after", C.c_int64), ("color_coin", C.c_int32)]
 
 
+class TrainConfig(C.Structure):
+    _fields_ = [("total_iters", C.c_int64), ("warmup_iters", C.c_int64),
+                ("densify_interval", C.c_int64), ("densify_until", C.c_int64),
+                ("batch_final_iters", C.c_int64), ("batch_size", C.c_int32),
+                ("dilation_p", C.c_int32), ("post_densify_dilation_prob", C.c_float),
+                ("n_views", C.c_int64), ("m_final", C.c_double), ("seed", C.c_uint64),
+                ("background", C.c_float * 3), ("densify", DensifyConfig)]
+
+
+class TrainReport(C.Structure):
+    _fields_ = [("iteration", C.c_int64), ("count", C.c_int64), ("budget", C.c_int64),
+                ("spawned", C.c_int64), ("pruned", C.c_int64), ("densified", C.c_int32),
+                ("dilated", C.c_int32)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "tgsx_create": (C.c_int32, [C.c_int32, P(vp)]),
@@ -86,6 +101,12 @@ SIGNATURES = {
     "tgsx_budget_state": (None, [vp, f64p]),
     "tgsx_budget_t_norm": (C.c_double, [C.c_int64, C.c_int64, C.c_int64]),
     "tgsx_fit_power_exponent": (C.c_int32, [f64p, f64p, C.c_int64, f64p]),
+    "tgsx_train_config_default": (None, [P(TrainConfig)]),
+    "tgsx_trainer_create": (C.c_int32, [vp, vp, P(TrainConfig), C.c_int32, C.c_int32, P(vp)]),
+    "tgsx_trainer_destroy": (None, [vp]),
+    "tgsx_trainer_step": (C.c_int32, [vp, P(vp), C.c_int64, P(TrainReport)]),
+    "tgsx_trainer_losses": (C.c_int32, [vp, f32p, C.c_int64, i64p]),
+    "tgsx_trainer_budget": (vp, [vp]),
     "tgsx_synthetic_scene": (None, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, P(HostScene)]),
     "tgsx_pcg32_init": (None, [u64p, C.c_uint64, C.c_uint64]),
     "tgsx_pcg32_uniform": (C.c_double, [u64p]),

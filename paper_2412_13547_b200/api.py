@@ -481,6 +481,68 @@ def densify_config(**kw) -> _lib.DensifyConfig:
     return c
 
 
+def train_config(**kw) -> _lib.TrainConfig:
+    """TrainConfig with the SPEC defaults; keyword overrides."""
+    c = _lib.TrainConfig()
+    load().tgsx_train_config_default(C.byref(c))
+    for k, v in kw.items():
+        if k == "background":
+            c.background[:] = v
+        else:
+            setattr(c, k, v)
+    return c
+
+
+class Trainer:
+    """The Turbo-GS fit loop over a DeviceModel: schedule, budget controller,
+    densify cadence, post-densify random dilation, batched finale (libtgsx trainer.cpp)."""
+
+    def __init__(self, dm: "DeviceModel", width: int, height: int, config=None, **kw):
+        self.dm = dm
+        self.cfg = config or train_config(**kw)
+        h = C.c_void_p()
+        dm.ctx.check(dm.ctx.L.tgsx_trainer_create(dm.ctx.h, dm.h, C.byref(self.cfg), width, height,
+                                                  C.byref(h)))
+        self.h = h
+        self._targets = None
+
+    def set_targets(self, targets):
+        """targets: list of device pointers (int) or (H, W, 3) float32 host arrays."""
+        self._keep = [t if isinstance(t, int) else _f32(t) for t in targets]
+        ptrs = [t if isinstance(t, int) else t.ctypes.data for t in self._keep]
+        self._targets = (C.c_void_p * len(ptrs))(*ptrs)
+
+    def step(self) -> _lib.TrainReport:
+        rep = _lib.TrainReport()
+        self.dm.ctx.check(self.dm.ctx.L.tgsx_trainer_step(self.h, self._targets, len(self._targets),
+                                                          C.byref(rep)))
+        return rep
+
+    def losses(self, max_n: int = 4096) -> np.ndarray:
+        out = np.zeros(max_n, np.float32)
+        n = C.c_int64()
+        self.dm.ctx.check(self.dm.ctx.L.tgsx_trainer_losses(self.h, _ptr(out, _lib.f32p), max_n, C.byref(n)))
+        return out[:n.value]
+
+    def budget_state(self):
+        b = self.dm.ctx.L.tgsx_trainer_budget(self.h)
+        out = (C.c_double * 5)()
+        self.dm.ctx.L.tgsx_budget_state(b, out)
+        return {"alpha": out[0], "alpha_base": out[1], "m_adaptive": out[2], "ema": out[3],
+                "fits": int(out[4])}
+
+    def close(self):
+        if self.h:
+            self.dm.ctx.L.tgsx_trainer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class BudgetController:
     """BudgetController, host C++ in libtgsx."""
 

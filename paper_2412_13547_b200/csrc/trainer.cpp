@@ -1,0 +1,196 @@
+// The Turbo-GS fit loop (train(); trainer.cpp is missing from the reference so
+// the schedule is the SPEC's) as native host orchestration over the device-resident fit path:
+//
+//   1..warmup                 dilated (p) with cycled offsets, optimise only
+//   warmup..densify_until     + every densify_interval: budget update -> B(t_norm) -> densify
+//                             (select / top-k cap / spawn / prune / reset) on the device
+//   densify_until..final      no densification; dilated with probability
+//                             post_densify_dilation_prob (one coin per iteration), else dense
+//   last batch_final_iters    batch_size renders with distinct cycled offsets accumulated on the
+//                             device, one Adam step on the mean
+//   every n_views iterations  visit audit
+// Targets are round-robined (multi-image fitting). RNG draw order per SPEC.md:604:
+// offset coin -> colour coin -> spawn jitter (the last two inside tgsx_densify). Per-iteration
+// losses stay on the device and are fed to the budget controller in order at each densify event
+// (the controller only reads them there), so the loop never waits on a loss readback.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/tgsx.h"
+#include <cuda_runtime.h>
+
+struct tgsx_trainer {
+    tgsx_ctx* ctx = nullptr;
+    tgsx_model* m = nullptr;
+    tgsx_train_config cfg{};
+    int32_t W = 0, H = 0;
+    tgsx_budget* budget = nullptr;
+    uint64_t rng[2] = {0, 0};
+    int64_t t = 0;                   // last completed iteration (1-based)
+    int64_t adam_step = 0;
+    int64_t n_init = 0;
+    float* d_losses = nullptr;       // device ring of per-iteration losses
+    int64_t ring = 0;
+    int64_t fed = 0;                 // iterations already fed to the budget controller
+    std::vector<float> h_losses;
+    float* h_pinned = nullptr;
+    double last_budget = 0;
+};
+
+namespace {
+
+int32_t feed_losses(tgsx_trainer* tr) {
+    const int64_t pending = tr->t - tr->fed;
+    if (pending <= 0) return TGSX_OK;
+    if (cudaMemcpyAsync(tr->h_pinned, tr->d_losses, sizeof(float) * tr->ring, cudaMemcpyDeviceToHost,
+                        (cudaStream_t)tgsx_get_stream(tr->ctx)) != cudaSuccess)
+        return TGSX_ECUDA;
+    if (cudaStreamSynchronize((cudaStream_t)tgsx_get_stream(tr->ctx)) != cudaSuccess) return TGSX_ECUDA;
+    for (int64_t it = tr->fed + 1; it <= tr->t; ++it) {
+        const float l = tr->h_pinned[(it - 1) % tr->ring];
+        if (l > 0.f) tgsx_budget_record_loss(tr->budget, it, (double)l);
+    }
+    tr->fed = tr->t;
+    return TGSX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void tgsx_train_config_default(tgsx_train_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->total_iters = 10000;       // SPEC.md:543 (paper scale)
+    c->warmup_iters = 300;
+    c->densify_interval = 20;
+    c->densify_until = 3000;
+    c->batch_final_iters = 50;
+    c->batch_size = 4;
+    c->dilation_p = 2;
+    c->post_densify_dilation_prob = 0.5f;
+    c->n_views = 1;
+    c->m_final = 0;               // 0 => 1.5 x initial count
+    c->seed = 1;
+    c->background[0] = c->background[1] = c->background[2] = 0.f;
+    tgsx_densify_config_default(&c->densify);
+}
+
+int32_t tgsx_trainer_create(tgsx_ctx* ctx, tgsx_model* m, const tgsx_train_config* cfg,
+                            int32_t width, int32_t height, tgsx_trainer** out) {
+    if (!ctx || !m || !cfg || !out || width < 1 || height < 1) return TGSX_EINVAL;
+    if (cfg->dilation_p < 1 || cfg->batch_size < 1 || cfg->densify_interval < 1) return TGSX_EINVAL;
+    if (!(cfg->warmup_iters <= cfg->densify_until && cfg->densify_until <= cfg->total_iters))
+        return TGSX_EINVAL;  // SPEC.md:552 invariants
+    tgsx_trainer* tr = new (std::nothrow) tgsx_trainer();
+    if (!tr) return TGSX_ENOMEM;
+    tr->ctx = ctx;
+    tr->m = m;
+    tr->cfg = *cfg;
+    tr->W = width;
+    tr->H = height;
+    tr->n_init = tgsx_model_size(m);
+    const double mf = cfg->m_final > 0 ? cfg->m_final : 1.5 * (double)tr->n_init;
+    tgsx_budget_create((double)tr->n_init, mf, &tr->budget);
+    tgsx_pcg32_init(tr->rng, cfg->seed, 1);
+    tr->ring = std::max<int64_t>(cfg->densify_interval, 1) * 4 + 64;
+    if (cudaMalloc(&tr->d_losses, sizeof(float) * tr->ring) != cudaSuccess ||
+        cudaMallocHost(&tr->h_pinned, sizeof(float) * tr->ring) != cudaSuccess) {
+        delete tr;
+        return TGSX_ECUDA;
+    }
+    cudaMemset(tr->d_losses, 0, sizeof(float) * tr->ring);
+    *out = tr;
+    return TGSX_OK;
+}
+
+void tgsx_trainer_destroy(tgsx_trainer* tr) {
+    if (!tr) return;
+    if (tr->budget) tgsx_budget_destroy(tr->budget);
+    if (tr->d_losses) cudaFree(tr->d_losses);
+    if (tr->h_pinned) cudaFreeHost(tr->h_pinned);
+    delete tr;
+}
+
+// One iteration. targets: n_targets device or host pointers to full-resolution W*H*3 RGB.
+int32_t tgsx_trainer_step(tgsx_trainer* tr, const float* const* targets, int64_t n_targets,
+                          tgsx_train_report* rep) {
+    if (!tr || !targets || n_targets < 1) return TGSX_EINVAL;
+    const tgsx_train_config& c = tr->cfg;
+    const int64_t t = tr->t + 1;
+    const float* bg = c.background;
+    tgsx_train_report r{};
+    r.iteration = t;
+    const int64_t final_start = c.total_iters - c.batch_final_iters;
+    float* dloss = tr->d_losses + (t - 1) % tr->ring;
+    int32_t rc = TGSX_OK;
+    const int p = c.dilation_p;
+    if (t > final_start && c.batch_size > 1) {
+        // batched finale: batch_size renders with distinct cycled offsets, mean, one Adam step
+        for (int32_t b = 0; b < c.batch_size; ++b) {
+            const int64_t idx = ((t - 1) * c.batch_size + b) % ((int64_t)p * p);
+            tgsx_pattern pat{p, (int32_t)(idx % p), (int32_t)(idx / p), tr->W, tr->H};
+            const float* tg = targets[((t - 1) * c.batch_size + b) % n_targets];
+            if ((rc = tgsx_view_accumulate(tr->ctx, tr->m, &pat, bg, tg, b == 0 ? dloss : nullptr)))
+                return rc;
+        }
+        tgsx_adam_args a{++tr->adam_step, c.total_iters, std::hypot((double)tr->W, (double)tr->H)};
+        if ((rc = tgsx_apply_step(tr->ctx, tr->m, c.batch_size, &a))) return rc;
+        r.dilated = 1;
+    } else {
+        int dilate = 1;
+        if (t > c.densify_until) {  // offset coin (SPEC.md:604 draw order)
+            dilate = tgsx_pcg32_uniform(tr->rng) < (double)c.post_densify_dilation_prob;
+        }
+        const int pp = dilate ? p : 1;
+        const int64_t idx = (t - 1) % ((int64_t)pp * pp);  // next_offsets (dilation.hpp:60-64)
+        tgsx_pattern pat{pp, (int32_t)(idx % pp), (int32_t)(idx / pp), tr->W, tr->H};
+        tgsx_adam_args a{++tr->adam_step, c.total_iters, std::hypot((double)tr->W, (double)tr->H)};
+        if ((rc = tgsx_fit_step(tr->ctx, tr->m, &pat, bg, targets[(t - 1) % n_targets], &a, dloss)))
+            return rc;
+        r.dilated = dilate;
+    }
+    tr->t = t;
+    // drain the device loss ring before it wraps (one small readback every ring/2 iterations)
+    if (tr->t - tr->fed >= tr->ring / 2 && (rc = feed_losses(tr))) return rc;
+    // densification phase (SPEC.md:575(3))
+    if (t > c.warmup_iters && t <= c.densify_until && t % c.densify_interval == 0) {
+        if ((rc = feed_losses(tr))) return rc;
+        tgsx_budget_update(tr->budget, t);
+        const double tn = tgsx_budget_t_norm(t, c.warmup_iters, c.densify_until);
+        const int64_t B = tgsx_budget_at(tr->budget, tn);
+        tgsx_densify_report dr{};
+        if ((rc = tgsx_densify(tr->ctx, tr->m, &c.densify, B, tr->rng, &dr))) return rc;
+        r.densified = 1;
+        r.budget = B;
+        r.spawned = dr.spawned;
+        r.pruned = dr.pruned;
+        tr->last_budget = (double)B;
+    }
+    if (c.n_views > 0 && t % c.n_views == 0) {
+        if ((rc = tgsx_visit_audit(tr->ctx, tr->m))) return rc;
+    }
+    r.count = tgsx_model_size(tr->m);
+    r.budget = r.budget ? r.budget : (int64_t)tr->last_budget;
+    if (rep) *rep = r;
+    return TGSX_OK;
+}
+
+// Per-iteration losses of the last min(ring, t) iterations (oldest first) + budget state.
+int32_t tgsx_trainer_losses(tgsx_trainer* tr, float* out, int64_t max_out, int64_t* out_n) {
+    if (!tr) return TGSX_EINVAL;
+    if (feed_losses(tr)) return TGSX_ECUDA;
+    const int64_t n = std::min<int64_t>(std::min<int64_t>(tr->t, tr->ring), max_out);
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t it = tr->t - n + 1 + k;
+        out[k] = tr->h_pinned[(it - 1) % tr->ring];
+    }
+    if (out_n) *out_n = n;
+    return TGSX_OK;
+}
+
+const tgsx_budget* tgsx_trainer_budget(const tgsx_trainer* tr) { return tr ? tr->budget : nullptr; }
+
+}  // extern "C"

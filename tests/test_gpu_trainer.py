@@ -1,0 +1,56 @@
+"""The GPU fit loop (libtgsx trainer: schedule, budget controller, densify cadence, random
+post-densify dilation, batched finale) against the same schedule restated over the CPU oracle
+(tests/oracle_trainer.py). Trajectories are compared event by event: per-iteration FP32
+differences are tiny, so losses and densify decisions agree early on; later the two runs may
+drift by a few spawned Gaussians, which is checked statistically. Budget compliance
+(acceptance #8) is checked at every densify event."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import bind as B
+from tests.helpers import model_from_scene
+from tests.oracle_trainer import oracle_train
+
+pytestmark = pytest.mark.gpu
+
+
+def test_trainer_matches_oracle_schedule():
+    import paper_2412_13547_b200 as P
+    B.set_math(True)
+    W, H, n = 64, 48, 300
+    s = B.synthetic_scene(1, n, W, H)
+    base = B.render(B.synthetic_scene(2, 600, W, H), 1, 0, 0, W, H)[0].reshape(H, W, 3)
+    rng = np.random.default_rng(0)
+    targets = [np.clip(base + rng.normal(0, 0.02, base.shape), 0, 1).astype(np.float32) for _ in range(4)]
+    cfg = P.train_config(total_iters=400, warmup_iters=60, densify_interval=20, densify_until=300,
+                         batch_final_iters=20, batch_size=4, dilation_p=2, n_views=4,
+                         m_final=700.0, seed=7)
+    cfg.densify.tau_pos = 2e-5
+    ctx = P.Context(0)
+    dm = P.DeviceModel.from_host(model_from_scene(s), ctx)
+    tr = P.Trainer(dm, W, H, cfg)
+    tr.set_targets(targets)
+    events, losses = [], []
+    for t in range(1, 401):
+        rep = tr.step()
+        if rep.densified:
+            events.append((t, rep.budget, rep.count, rep.spawned, rep.pruned))
+            assert rep.count <= rep.budget  # budget compliance
+        if t % 50 == 0:
+            losses.extend(tr.losses(50).tolist())
+    os_, olosses, oevents = oracle_train(s, targets, cfg, W, H, 400)
+    losses = np.array(losses)
+    assert len(events) == len(oevents) == (300 - 60) // 20
+    # early events identical (same budget, same spawn / prune counts)
+    for e, o in zip(events[:3], oevents[:3]):
+        assert e == o, (e, o)
+    for (t, Bt, cnt, sp, pr), (ot, oB, ocnt, osp, opr) in zip(events, oevents):
+        assert t == ot and abs(Bt - oB) <= max(2, 0.02 * oB) and abs(cnt - ocnt) <= max(3, 0.03 * ocnt)
+        assert ocnt <= oB
+    assert np.allclose(losses[:100], olosses[:100], rtol=2e-3)
+    assert abs(losses[-20:].mean() - olosses[-20:].mean()) <= 0.03 * olosses[-20:].mean()
+    assert losses[-50:].mean() < losses[:50].mean()  # the fit makes progress
+    st = tr.budget_state()
+    assert 0.1 <= st["alpha"] <= 2.0
