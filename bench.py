@@ -1,26 +1,32 @@
 """Benchmark: Turbo-GS fit iterations/s on B200 (BASELINE.json metric).
 
-Workload (N=1, BASELINE.json configs[1], "C2"): synthetic 1M Gaussians (seed 1), 1920x1080,
-dense (p=1) single-view fit step = preprocess -> onesweep binning -> blend forward + fused L1
--> blend backward -> chain rule + densify stats + Adam, through libtgsx. The loss target is the
-render of the seed-2 synthetic scene. `--config c3` runs configs[2] (3M Gaussians, 3840x2160,
-dilated p=2 with cycled offsets). With N>1 ranks (torchrun) every rank fits its own view per
-step and the per-Gaussian step buffer (9 grads + densify stats) is all-reduced over NCCL
-before the identical Adam on every rank (view-batch data parallelism).
+Default workload (N=1, BASELINE.json configs[1], "C2"): synthetic 1M Gaussians (seed 1),
+1920x1080, dense (p=1) single-view fit step = preprocess -> onesweep binning -> blend forward +
+fused L1 -> blend backward -> chain rule + densify stats + Adam, through libtgsx. The loss target
+is the render of the seed-2 synthetic scene. With N>1 ranks (torchrun) every rank fits its own
+view per step (target + per-rank noise) and the per-Gaussian step buffer (9 grads + densify stats)
+is all-reduced over NCCL before the identical Adam on every rank (view-batch data parallelism,
+SURVEY.md §8e): weak scaling, value = views*steps/s over all ranks.
 
-Timing: W warm-up steps, then K steps bracketed by barrier + synchronize, timed with CUDA
-events on the library's stream, max over ranks. Working set per step (model state + moments
-+ pairs + partials, >600 MB at C2) exceeds the 126 MB L2, so no explicit flush.
+Other configs (--config): c3 = configs[2] (3M, 3840x2160, dilated p=2 with cycled offsets);
+c4 = configs[3] (the full fit loop — schedule, densify every 20 with the convergence-aware budget —
+over 200 synthetic 1080p views; timed inside the densification phase); c5 = configs[4] (8 views per
+step at 4K p=2 accumulated then one Adam step; with N ranks the 8 views are sharded, strong scaling).
 
-`--impl reference` times the reference CPU path on this host (oracle/_ref: the unmodified
-reference render/backward compiled from /root/reference, + the oracle's restated L1/Adam)
-on the same workload, rank 0 only.
+Timing: W warm-up steps, then K steps bracketed by barrier + synchronize, timed with CUDA events on
+the library's stream, max over ranks. The per-step working set (model state + moments + pairs +
+partials, >600 MB at C2) exceeds the 126 MB L2, so there is no explicit flush.
+
+`--impl reference` times the reference CPU path on this host (oracle/_ref: the unmodified reference
+render/backward compiled from /root/reference, + the oracle's restated L1/Adam) on the same
+workload, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -35,11 +41,16 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     "c2": dict(workload="C2: synthetic 1M Gaussians, 1920x1080, p=1 single-view fit step "
-                        "(fwd + L1 + bwd + densify stats + Adam)",
-               n=1_000_000, W=1920, H=1080, p=1),
+                        "(fwd + L1 + bwd + densify stats + Adam)", n=1_000_000, W=1920, H=1080, p=1),
     "c3": dict(workload="C3: synthetic 3M Gaussians, 3840x2160, dilated p=2 (cycled offsets) "
-                        "fit step (fwd + L1 + bwd + densify stats + Adam)",
-               n=3_000_000, W=3840, H=2160, p=2),
+                        "fit step (fwd + L1 + bwd + densify stats + Adam)", n=3_000_000, W=3840, H=2160, p=2),
+    "c4": dict(workload="C4: full Turbo-GS fit loop, 1M initial Gaussians, 200 synthetic 1080p views, "
+                        "dilated p=2 cycled offsets, densify every 20 iters (tau_pos 5e-8) with the convergence-aware "
+                        "budget (M = 1.5 N0); timed in the densification phase", n=1_000_000, W=1920,
+               H=1080, p=2),
+    "c5": dict(workload="C5: batched-view 4K fitting, 3M Gaussians, 8 views/step (cycled p=2 offsets, "
+                        "distinct targets) accumulated + one Adam step; views sharded across ranks",
+               n=3_000_000, W=3840, H=2160, p=2, views=8),
 }
 METRIC = "fit iters/sec (fwd+bwd+Adam) at 1080p and 4K dilated, 1M–3M Gaussians"
 
@@ -72,7 +83,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self.stop.wait(0.2)
+            self.stop.wait(0.1)
 
     def __enter__(self):
         self.th.start()
@@ -104,35 +115,39 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------------------- reference arm
-def run_reference(args, cfg):
-    rank, world, _ = env_rank()
-    if rank != 0:
-        return
+def _ref_setup(cfg):
     from oracle import bind as B
     threads = os.cpu_count() or 1
-    W, H, n, p = cfg["W"], cfg["H"], cfg["n"], cfg["p"]
+    W, H, n = cfg["W"], cfg["H"], cfg["n"]
     impl = "ref_native" if B.ref_available() else "oracle"
     B.set_math(False)
     s = B.synthetic_scene(1, n, W, H)
     t = B.synthetic_scene(2, n, W, H)
     target, _, _, _ = B.render(t, 1, 0, 0, W, H, impl=impl, threads=threads)
-    target = target.reshape(H, W, 3)
-    m1 = np.zeros((9, n), np.float32)
-    m2 = np.zeros((9, n), np.float32)
-    diag = float(np.hypot(W, H))
+    return B, impl, threads, s, target.reshape(H, W, 3)
 
-    def step(it):
-        ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
-        rgb, _, _, _ = B.render(s, p, ox, oy, W, H, impl=impl, threads=threads)
-        _, dl = B.l1_loss(rgb, p, ox, oy, W, H, target)
-        g, _ = B.backward(s, p, ox, oy, W, H, dl, impl=impl, threads=threads)
-        B.adam_step(s, g, m1, m2, B.adam_config(it + 1, 10000, diag))
 
+def _ref_step(B, impl, threads, s, target, m1, m2, cfg, it):
+    W, H, p = cfg["W"], cfg["H"], cfg["p"]
+    ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
+    rgb, _, _, _ = B.render(s, p, ox, oy, W, H, impl=impl, threads=threads)
+    _, dl = B.l1_loss(rgb, p, ox, oy, W, H, target)
+    g, _ = B.backward(s, p, ox, oy, W, H, dl, impl=impl, threads=threads)
+    B.adam_step(s, g, m1, m2, B.adam_config(it + 1, 10000, math.hypot(W, H)))
+
+
+def run_reference(args, cfg):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    B, impl, threads, s, target = _ref_setup(cfg)
+    m1 = np.zeros((9, s.n), np.float32)
+    m2 = np.zeros((9, s.n), np.float32)
     for i in range(args.warmup):
-        step(i)
+        _ref_step(B, impl, threads, s, target, m1, m2, cfg, i)
     t0 = time.perf_counter()
     for i in range(args.steps):
-        step(args.warmup + i)
+        _ref_step(B, impl, threads, s, target, m1, m2, cfg, args.warmup + i)
     dt = time.perf_counter() - t0
     v = args.steps / dt
     kind = "reference" if impl != "oracle" else "port"
@@ -140,7 +155,8 @@ def run_reference(args, cfg):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "gaussians": n, "width": W, "height": H, "p": p},
+            "config": {"workload": cfg["workload"], "gaussians": cfg["n"], "width": cfg["W"],
+                       "height": cfg["H"], "p": cfg["p"]},
             "cpu_baseline": {"value": v, "unit": "iters/s", "cores": threads, "kind": kind,
                              "sample": f"{args.steps} full fit iterations on {threads} host threads "
                                        "(reference render+backward from oracle/_ref, restated L1+Adam)"},
@@ -150,28 +166,15 @@ def run_reference(args, cfg):
 
 def cpu_baseline_sample(cfg, iters=2):
     """Bounded CPU sample of the same workload (oracle/_ref, all host threads)."""
-    from oracle import bind as B
-    threads = os.cpu_count() or 1
-    W, H, n, p = cfg["W"], cfg["H"], cfg["n"], cfg["p"]
-    impl = "ref_native" if B.ref_available() else "oracle"
-    B.set_math(False)
-    s = B.synthetic_scene(1, n, W, H)
-    t = B.synthetic_scene(2, n, W, H)
-    target, _, _, _ = B.render(t, 1, 0, 0, W, H, impl=impl, threads=threads)
-    target = target.reshape(H, W, 3)
-    m1 = np.zeros((9, n), np.float32)
-    m2 = np.zeros((9, n), np.float32)
-    diag = float(np.hypot(W, H))
+    B, impl, threads, s, target = _ref_setup(cfg)
+    m1 = np.zeros((9, s.n), np.float32)
+    m2 = np.zeros((9, s.n), np.float32)
     times = []
     for it in range(iters + 1):
-        ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
         t0 = time.perf_counter()
-        rgb, _, _, _ = B.render(s, p, ox, oy, W, H, impl=impl, threads=threads)
-        _, dl = B.l1_loss(rgb, p, ox, oy, W, H, target)
-        g, _ = B.backward(s, p, ox, oy, W, H, dl, impl=impl, threads=threads)
-        B.adam_step(s, g, m1, m2, B.adam_config(it + 1, 10000, diag))
+        _ref_step(B, impl, threads, s, target, m1, m2, cfg, it)
         times.append(time.perf_counter() - t0)
-    med = statistics.median(times[1:])  # first iteration absorbs the blend-order sort
+    med = statistics.median(times[1:])  # the first iteration absorbs the blend-order sort
     return {"value": 1.0 / med, "unit": "iters/s", "cores": threads,
             "kind": "reference" if impl != "oracle" else "port",
             "sample": f"median of {iters} full fit iterations after 1 warm-up, same config "
@@ -179,9 +182,63 @@ def cpu_baseline_sample(cfg, iters=2):
 
 
 # ---------------------------------------------------------------------------- tgsx arm
+class Timer:
+    """CUDA events on the library stream around a timed region; max over ranks."""
+
+    def __init__(self, torch, stream, dist):
+        self.torch, self.stream, self.dist = torch, stream, dist
+
+    def run(self, fn, steps, base, ctx):
+        torch = self.torch
+        if self.dist:
+            self.dist.barrier()
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(self.stream)
+        for i in range(steps):
+            fn(base + i)
+        e1.record(self.stream)
+        e1.synchronize()
+        ctx.synchronize()
+        ms = e0.elapsed_time(e1)
+        if self.dist:
+            t = torch.tensor([ms], device="cuda")
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+
+def roofline(stages, counters, clocks, n):
+    peaks = measured_peaks()
+    per = {k: (v[0] / max(v[1], 1), v[1]) for k, v in stages.items() if v[1]}
+    dom = max(per, key=lambda k: per[k][0] * per[k][1])
+    dom_ms = per[dom][0]
+    E, Bl, K = counters["evals"], counters["blend_ops"], counters["pairs"]
+    f_mhz = clocks.get("sm_mhz") or peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1342.0)
+    fp32_peak = 148 * 128 * 2 * f_mhz * 1e6 / 1e12  # TFLOP/s at the sampled SM clock
+    if dom in ("blend_backward", "blend_forward"):
+        per_blend = 77 if dom == "blend_backward" else 20
+        achieved = (2 * E + per_blend * Bl) / (dom_ms / 1e3) / 1e12
+        return {"kernel": dom, "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
+                "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+                "ms_per_launch": dom_ms,
+                "peak_note": "148 SM x 128 FP32 lanes x 2 x median sampled SM clock "
+                             "(MEASURED_PEAKS.json has no FP32 figure)",
+                "work_note": f"algorithmic flops per launch 2E+{per_blend}Bl with E={E} evaluations, "
+                             f"Bl={Bl} blends (SURVEY.md §8d)"}
+    nb = {"chain_adam": 400 * n, "preprocess": 108 * n, "radix_sort": 32 * K,
+          "duplicate": 8 * K + 20 * n}.get(dom, 0)
+    achieved = nb / (dom_ms / 1e3) / 1e9
+    return {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None, "ms_per_launch": dom_ms}
+
+
 def run_tgsx(args, cfg):
     import torch
     import paper_2412_13547_b200 as P
+    from paper_2412_13547_b200 import dist as D
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
@@ -195,125 +252,144 @@ def run_tgsx(args, cfg):
     stream = torch.cuda.ExternalStream(ctx.L.tgsx_get_stream(ctx.h))
     host = P.GaussianModel.synthetic(1, n, W, H)
     dm = P.DeviceModel.from_host(host, ctx)
-    # target: render of the seed-2 scene on the GPU (+ per-rank noise for N>1 distinct views)
     tm = P.DeviceModel.from_host(P.GaussianModel.synthetic(2, n, W, H), ctx)
     tgt = tm.render(P.DilationPattern(1, 0, 0, W, H)).colors.reshape(H, W, 3)
     tm.close()
-    target = torch.from_numpy(tgt).cuda()
-    if world > 1:
-        g = torch.Generator(device="cuda").manual_seed(1000 + rank)
-        target = target + 0.02 * torch.randn(target.shape, generator=g, device="cuda")
-    target = target.contiguous()
-    loss_dev = torch.zeros(1, device="cuda")
-    torch.cuda.synchronize()
-    step_ptr, step_floats = dm.step_buffer()
-
-    class _CudaArray:
-        # zero-copy torch view of the library's [12][cap] step buffer, all-reduced by NCCL
-        __cuda_array_interface__ = {"shape": (step_floats,), "typestr": "<f4",
-                                    "data": (step_ptr, False), "version": 3, "stream": None}
-
-    step_tensor = torch.as_tensor(_CudaArray(), device="cuda") if world > 1 else None
+    base = torch.from_numpy(tgt).cuda()
+    timer = Timer(torch, stream, dist)
     bg = (C.c_float * 3)(0, 0, 0)
 
-    def one_step(it, tptr, lptr):
-        ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
-        pat = P.DilationPattern(p, ox, oy, W, H).c()
-        a = P._lib.AdamArgs(it + 1, 10000, diag)
-        if world == 1:
-            ctx.check(ctx.L.tgsx_fit_step(ctx.h, dm.h, C.byref(pat), bg, tptr, C.byref(a), lptr))
-        else:
-            ctx.check(ctx.L.tgsx_view_accumulate(ctx.h, dm.h, C.byref(pat), bg, tptr, lptr))
-            with torch.cuda.stream(stream):
-                dist.all_reduce(step_tensor)
-            ctx.check(ctx.L.tgsx_apply_step(ctx.h, dm.h, world, C.byref(a)))
+    def noisy(view_id):
+        g = torch.Generator(device="cuda").manual_seed(1000 + view_id)
+        return (base + 0.02 * torch.randn(base.shape, generator=g, device="cuda")).contiguous()
 
-    tptr = C.c_void_p(target.data_ptr())
-    lptr = C.c_void_p(loss_dev.data_ptr())
-    for i in range(args.warmup):
-        one_step(i, tptr, lptr)
-    ctx.synchronize()
-
-    def timed(fn, steps, base):
-        if dist:
-            dist.barrier()
+    extra = {}
+    if args.config in ("c2", "c3"):
+        target = noisy(rank) if world > 1 else base.contiguous()
+        loss_dev = torch.zeros(1, device="cuda")
         torch.cuda.synchronize()
-        ctx.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(steps):
-            fn(base + i)
-        e1.record(stream)
-        e1.synchronize()
-        ctx.synchronize()
-        ms = e0.elapsed_time(e1)
-        if dist:
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        sharded = D.ViewShardedFit(dm, rank, world)
 
-    # device-resident run (the `value`), with live per-stage CUDA events
+        def one_step(it, tptr, lptr):
+            ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
+            pat = P.DilationPattern(p, ox, oy, W, H).c()
+            a = P._lib.AdamArgs(it + 1, 10000, diag)
+            if world == 1:
+                ctx.check(ctx.L.tgsx_fit_step(ctx.h, dm.h, C.byref(pat), bg, tptr, C.byref(a), lptr))
+            else:
+                ctx.check(ctx.L.tgsx_view_accumulate(ctx.h, dm.h, C.byref(pat), bg, tptr, lptr))
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(sharded._tensor())
+                ctx.check(ctx.L.tgsx_apply_step(ctx.h, dm.h, world, C.byref(a)))
+
+        tptr, lptr = C.c_void_p(target.data_ptr()), C.c_void_p(loss_dev.data_ptr())
+        step_fn = lambda it: one_step(it, tptr, lptr)  # noqa: E731
+        views_per_step = world
+        h_target = target.cpu().pin_memory()
+        h_loss = torch.zeros(1).pin_memory()
+        e2e_fn = lambda it: one_step(it, C.c_void_p(h_target.data_ptr()), C.c_void_p(h_loss.data_ptr()))  # noqa: E731
+        e2e_bytes = (W * H * 12, 4)
+        units = world  # views per step over all ranks
+    elif args.config == "c4":
+        n_targets = 200
+        targets = [noisy(v) for v in range(n_targets)]
+        torch.cuda.synchronize()
+        tcfg = P.train_config(total_iters=10000, warmup_iters=300, densify_interval=20,
+                              densify_until=3000, batch_final_iters=50, batch_size=4,
+                              dilation_p=p, n_views=n_targets, m_final=1.5 * n, seed=1)
+        # SPEC's tau_pos = 2e-4 is calibrated for NDC-scale gradients; with the per-pixel
+        # normalised L1 at 1080p the mean position-gradient norms sit near 1e-8..2e-7, so the
+        # bench uses the ~93rd percentile (measured after warm-up) to make densify do real work.
+        tcfg.densify.tau_pos = 5e-8
+        trainer = P.Trainer(dm, W, H, tcfg)
+        trainer.set_targets([t.data_ptr() for t in targets])
+        for _ in range(tcfg.warmup_iters):  # warm-up phase of the schedule (untimed)
+            trainer.step()
+        reports = []
+        step_fn = lambda it: reports.append(trainer.step())  # noqa: E731
+        h_targets = [targets[v].cpu().pin_memory() for v in range(min(n_targets, 8))]
+        e2e_fn = None
+        e2e_bytes = (W * H * 12, 4)
+        units = 1
+        extra["trainer"] = trainer
+        extra["reports"] = reports
+        args.steps = max(args.steps, 100)
+        args.warmup = max(args.warmup, tcfg.warmup_iters)
+    else:  # c5
+        views = cfg["views"]
+        targets = [noisy(v) for v in range(views)]
+        torch.cuda.synchronize()
+        sharded = D.ViewShardedFit(dm, rank, world)
+        mine = D.views_for_rank(views, rank, world)
+        pats = [P.DilationPattern(p, (v % (p * p)) % p, (v % (p * p)) // p, W, H).c() for v in range(views)]
+        loss_dev = torch.zeros(views, device="cuda")
+        h_targets = [targets[v].cpu().pin_memory() for v in range(views)]
+        h_loss = torch.zeros(views).pin_memory()
+
+        def batched_step(it, tptrs, lbase, lstride):
+            for v in mine:
+                ctx.check(ctx.L.tgsx_view_accumulate(ctx.h, dm.h, C.byref(pats[v]), bg, C.c_void_p(tptrs[v]),
+                                                     C.c_void_p(lbase + 4 * v)))
+            if world > 1:
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(sharded._tensor())
+            a = P._lib.AdamArgs(it + 1, 10000, diag)
+            ctx.check(ctx.L.tgsx_apply_step(ctx.h, dm.h, views, C.byref(a)))
+
+        d_ptrs = [t.data_ptr() for t in targets]
+        h_ptrs = [t.data_ptr() for t in h_targets]
+        step_fn = lambda it: batched_step(it, d_ptrs, loss_dev.data_ptr(), 4)  # noqa: E731
+        e2e_fn = lambda it: batched_step(it, h_ptrs, h_loss.data_ptr(), 4)  # noqa: E731
+        e2e_bytes = (W * H * 12 * len(mine), 4 * len(mine))
+        units = 1  # one batched step = one fit iteration of the whole job (strong scaling)
+
+    if args.config != "c4":
+        for i in range(args.warmup):
+            step_fn(i)
+        ctx.synchronize()
+
     launches0 = ctx.launches
     ctx.profile(True)
     with ClockSampler(local) as clk:
-        ms = timed(lambda it: one_step(it, tptr, lptr), args.steps, args.warmup)
+        ms = timer.run(step_fn, args.steps, args.warmup, ctx)
     stages = ctx.profile_read()
     ctx.profile(False)
     launches = ctx.launches - launches0
     counters = ctx.counters()
-    # e2e through the public API with host buffers: pinned target H2D + loss D2H every step
-    h_target = torch.from_numpy(tgt).pin_memory() if world == 1 else target.cpu().pin_memory()
-    h_loss = torch.zeros(1).pin_memory()
-    e2e_ms = timed(lambda it: one_step(it, C.c_void_p(h_target.data_ptr()),
-                                       C.c_void_p(h_loss.data_ptr())), args.steps,
-                   args.warmup + args.steps)
+    e2e_ms = timer.run(e2e_fn, args.steps, args.warmup + args.steps, ctx) if e2e_fn else None
     if rank != 0:
         dist.barrier()
         dist.destroy_process_group()
         return
-    value = world * args.steps / (ms / 1e3)
-    e2e = world * args.steps / (e2e_ms / 1e3)
+    value = units * args.steps / (ms / 1e3)
     clocks = clk.summary()
-    peaks = measured_peaks()
-    # roofline of the dominant kernel (per launch: stage ms / launch count)
-    per = {k: (v[0] / max(v[1], 1), v[1]) for k, v in stages.items() if v[1]}
-    dom = max(per, key=lambda k: per[k][0] * per[k][1])
-    dom_ms = per[dom][0]
-    E, Bl, K = counters["evals"], counters["blend_ops"], counters["pairs"]
-    f_mhz = clocks["sm_mhz"] or peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1342.0)
-    fp32_peak = 148 * 128 * 2 * f_mhz * 1e6 / 1e12  # TFLOP/s at the sampled SM clock
-    if dom in ("blend_backward", "blend_forward"):
-        flops = (2 * E + 77 * Bl) if dom == "blend_backward" else (2 * E + 20 * Bl)
-        achieved = flops / (dom_ms / 1e3) / 1e12
-        roof = {"kernel": dom, "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
-                "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
-                "peak_note": "148 SM x 128 FP32 lanes x 2 x median sampled SM clock "
-                             "(MEASURED_PEAKS.json has no FP32 figure)",
-                "work_note": f"algorithmic flops per launch 2E+{77 if dom == 'blend_backward' else 20}Bl "
-                             f"with E={E} evaluations, Bl={Bl} blends (SURVEY.md §8d)"}
-    else:
-        nb = {"chain_adam": 400 * n, "preprocess": 108 * n, "radix_sort": 32 * K,
-              "duplicate": 8 * K + 20 * n}.get(dom, 0)
-        achieved = nb / (dom_ms / 1e3) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None}
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": cfg["workload"], "gaussians": n, "width": W, "height": H,
-                       "p": p, "views_per_step": world,
+            "higher_is_better": True, "scaling": "strong" if args.config == "c5" else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "gaussians": n, "width": W, "height": H, "p": p,
+                       "views_per_step": units if args.config in ("c2", "c3") else cfg.get("views", 1),
                        "l2": "per-step working set > 126 MB L2 (no explicit flush)"},
             "clocks": clocks,
-            "e2e": {"value": e2e, "unit": "iters/s", "h2d_bytes_per_step": W * H * 12,
-                    "d2h_bytes_per_step": 4},
             "gpu_launches": launches,
-            "roofline": roof,
+            "roofline": roofline(stages, counters, clocks, n),
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},
-            "counters": {"pairs": K, "evals": E, "blend_ops": Bl}}
-    if world == 1 and not args.no_cpu_baseline:
+            "counters": counters}
+    if e2e_ms is not None:
+        line["e2e"] = {"value": units * args.steps / (e2e_ms / 1e3), "unit": "iters/s",
+                       "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1]}
+    else:
+        line["e2e"] = {"value": None, "unit": "iters/s", "note": "fit loop runs device-resident targets"}
+    if args.config == "c4":
+        reps = extra["reports"]
+        line["fit_loop"] = {"iterations": [reps[0].iteration, reps[-1].iteration],
+                            "densify_events": sum(r.densified for r in reps),
+                            "spawned": int(sum(r.spawned for r in reps)),
+                            "pruned": int(sum(r.pruned for r in reps)),
+                            "count_start": int(n), "count_end": int(reps[-1].count),
+                            "budget_end": int(reps[-1].budget),
+                            "loss_last": float(extra["trainer"].losses(1)[-1])}
+    if world == 1 and not args.no_cpu_baseline and args.config in ("c2", "c3"):
         try:
             line["cpu_baseline"] = cpu_baseline_sample(cfg)
         except Exception as e:  # the baseline is reported, never required
@@ -333,7 +409,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "tgsx" else args.warmup
+    if args.impl == "tgsx":
+        args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

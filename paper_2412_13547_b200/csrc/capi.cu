@@ -535,6 +535,7 @@ void tgsx_model_destroy(tgsx_model* m) {
                       &m->window, &m->tau_v, &m->m1, &m->m2, &m->step, &m->perm, &m->rank_of,
                       &m->screen};
     for (DevBuf* b : bufs) b->release();
+    for (DevBuf& b : m->spare) b.release();
     delete m;
 }
 

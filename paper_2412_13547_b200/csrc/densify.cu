@@ -183,9 +183,8 @@ cudaError_t scan_count(tgsx_ctx* ctx, const uint32_t* flags, uint32_t* pos, int6
     return cudaSuccess;
 }
 
-// grows every model array to at least `cap` (defined in capi.cu's anonymous namespace; we
-// re-implement the needed piece here through the public upload path is too slow, so keep a
-// local copy of the row-regrow logic)
+// Re-allocates one [rows][cap] row group at a larger capacity, keeping the first n columns of
+// every row (capacity grows geometrically, so this runs O(log N) times per fit).
 cudaError_t regrow(tgsx_ctx* ctx, DevBuf& b, int rows, size_t elt, int64_t oc, int64_t cap, int64_t n) {
     void* np = nullptr;
     cudaError_t e = cudaMalloc(&np, (size_t)rows * cap * elt);
@@ -233,6 +232,7 @@ void tgsx_densify_config_default(tgsx_densify_config* c) {
 int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cfg, int64_t budget,
                      uint64_t rng_state[2], tgsx_densify_report* out) {
     if (!ctx || !m || !cfg || !rng_state) return TGSX_EINVAL;
+    StageTimer timer(ctx, kStDensify);
     const int64_t n0 = m->n;
     tgsx_densify_report rep{};
     // colour coin: one draw per event
@@ -331,21 +331,27 @@ int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cf
                 {&m->params, 10, 4}, {&m->ids, 1, 8}, {&m->pos_acc, 1, 4}, {&m->col_acc, 1, 4},
                 {&m->accum, 1, 4}, {&m->visit, 1, 8}, {&m->window, 1, 8}, {&m->tau_v, 1, 8},
                 {&m->m1, 9, 4}, {&m->m2, 9, 4}, {&m->step, kStepFloats, 4}};
-            for (auto& r : rs) {
-                void* np = nullptr;
-                DCK(cudaMalloc(&np, (size_t)r.rows * cap * r.elt));
+            // compact each row group into its spare (allocated once per capacity) and swap
+            for (int i = 0; i < 11; ++i) {
+                const auto& r = rs[i];
+                DevBuf& sp = m->spare[i];
+                const size_t bytes = (size_t)r.rows * cap * r.elt;
+                if (sp.bytes < bytes) {
+                    DCK(cudaStreamSynchronize(ctx->stream));
+                    sp.release();
+                    DCK(cudaMalloc(&sp.p, bytes));
+                    sp.bytes = bytes;
+                }
                 if (r.elt == 4)
                     compact_rows<uint32_t><<<grid_for(n1, 256), 256, 0, ctx->stream>>>(
-                        r.b->as<uint32_t>(), (uint32_t*)np, cap, n1, r.rows, keep, kpos);
+                        r.b->as<uint32_t>(), sp.as<uint32_t>(), cap, n1, r.rows, keep, kpos);
                 else
                     compact_rows<unsigned long long><<<grid_for(n1, 256), 256, 0, ctx->stream>>>(
-                        r.b->as<unsigned long long>(), (unsigned long long*)np, cap, n1, r.rows, keep, kpos);
+                        r.b->as<unsigned long long>(), sp.as<unsigned long long>(), cap, n1, r.rows, keep, kpos);
                 ctx->launches++;
                 DCK(cudaGetLastError());
-                DCK(cudaStreamSynchronize(ctx->stream));
-                cudaFree(r.b->p);
-                r.b->p = np;
-                r.b->bytes = (size_t)r.rows * cap * r.elt;
+                std::swap(r.b->p, sp.p);
+                std::swap(r.b->bytes, sp.bytes);
             }
             m->n = kept;
             m->order_dirty = true;

@@ -113,6 +113,7 @@ struct tgsx_model {
     tgsx::DevBuf perm;     // u32[cap] rank -> index
     tgsx::DevBuf rank_of;  // u32[cap] index -> rank
     tgsx::DevBuf screen;   // float[10][cap] screen-space grads of the last backward
+    tgsx::DevBuf spare[11];  // prune compaction targets (swapped with the live rows; no per-event malloc)
     int64_t step_views = 0;
 };
 
