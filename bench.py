@@ -210,7 +210,16 @@ class Timer:
         return ms
 
 
-def roofline(stages, counters, clocks, n):
+def measured_traffic(config, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_r01.json")) as f:
+            return json.load(f).get(config, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def roofline(stages, counters, clocks, n, config):
     peaks = measured_peaks()
     per = {k: (v[0] / max(v[1], 1), v[1]) for k, v in stages.items() if v[1]}
     dom = max(per, key=lambda k: per[k][0] * per[k][1])
@@ -222,7 +231,8 @@ def roofline(stages, counters, clocks, n):
         per_blend = 77 if dom == "blend_backward" else 20
         achieved = (2 * E + per_blend * Bl) / (dom_ms / 1e3) / 1e12
         return {"kernel": dom, "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
-                "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+                "traffic": measured_traffic(config, dom),
                 "ms_per_launch": dom_ms,
                 "peak_note": "148 SM x 128 FP32 lanes x 2 x median sampled SM clock "
                              "(MEASURED_PEAKS.json has no FP32 figure)",
@@ -232,7 +242,8 @@ def roofline(stages, counters, clocks, n):
           "duplicate": 8 * K + 20 * n}.get(dom, 0)
     achieved = nb / (dom_ms / 1e3) / 1e9
     return {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-            "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None, "ms_per_launch": dom_ms}
+            "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+            "traffic": measured_traffic(config, dom), "ms_per_launch": dom_ms}
 
 
 def run_tgsx(args, cfg):
@@ -372,7 +383,7 @@ def run_tgsx(args, cfg):
                        "l2": "per-step working set > 126 MB L2 (no explicit flush)"},
             "clocks": clocks,
             "gpu_launches": launches,
-            "roofline": roofline(stages, counters, clocks, n),
+            "roofline": roofline(stages, counters, clocks, n, args.config),
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},
             "counters": counters}
     if e2e_ms is not None:
