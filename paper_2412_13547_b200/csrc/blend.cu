@@ -40,8 +40,9 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kRec = 48;        // bytes per staged splat record
-constexpr int kRecStride = 32;  // floats per (splat) row of the phase-1 records; float4 blocks
-                                // XOR-swizzled by (row & 7) => conflict-free row-wise LDS.128
+constexpr int kRecStride = 36;  // floats per row of the phase-1 records: 32 pixels + 4 pad, so
+                                // row writes (fixed row, lane = pixel) and row-per-lane LDS.128
+                                // reads (lane i reads row i) are both bank-conflict-free
 constexpr int kWPB = 4;         // warps (tiles) per CTA
 
 struct BlendParams {
@@ -312,17 +313,13 @@ __device__ __forceinline__ uint32_t pair_slot(const Prepared& P, int tx, int ty)
 
 template <int NG>
 struct BwdWarpSmem {
-    float rec_u[32 * kRecStride];  // phase-1 records [splat][pixel (swizzled)]
+    float rec_u[32 * kRecStride];  // phase-1 records [union row][pixel]
     float rec_w[32 * kRecStride];
     float2 st[NG][32];             // per-pixel (T, g.S) carried across chunks
-    float4 gcur[32];               // dL/dC of the current group's pixels (phase-2 broadcast)
+    float g[3][32];                // dL/dC of the current group's pixels, planar (phase-2 broadcast)
     unsigned char rec[32 * kRec];
 };
 
-// Swizzled record position of (splat row k, pixel l): float4 block (l>>2) ^ (k&7).
-__device__ __forceinline__ uint32_t rec_off(int k, int l) {
-    return 4u * (uint32_t)(k * kRecStride + ((((l >> 2) ^ (k & 7)) << 2) | (l & 3)));
-}
 
 template <int NGX, int NGY>
 __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm) {
@@ -415,28 +412,34 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             // only splats before this pixel's last contributor were blended
             const int span = (int)glast - c0;
             col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
-            if (!__any_sync(kFull, col)) continue;
+            // The union of the group's walked splats (warp-uniform) is visited back to front with
+            // all lanes on the same splat: record reads are broadcasts, and every visited splat
+            // gets a DENSE record row (row r = r-th highest union splat; pixels that do not blend
+            // it store 0), so no row is ever cleared and phase 2 reads only U = |union| rows.
+            const uint32_t un = __reduce_or_sync(kFull, col);
+            if (!un) continue;
+            const int U = __popc(un);
             float2 st = S.st[g][lane];
             float T = st.x, gS = st.y;
-            S.gcur[lane] = gv;
             const float fxg = fxl + (float)(gx * 8 * p), fyg = fyl + (float)(gy * 4 * p);
-#pragma unroll
-            for (int q = lane; q < 32 * kRecStride / 4; q += 32) {
-                sts_f4(ubase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
-                sts_f4(wbase + 16 * q, make_float4(0.f, 0.f, 0.f, 0.f));
-            }
-            __syncwarp();
+            __syncwarp();  // the previous group's phase 2 is done with the rows and g
+            S.g[0][lane] = gv.x;
+            S.g[1][lane] = gv.y;
+            S.g[2][lane] = gv.z;
             uint32_t visb = 0;
-            // phase 1: per pixel, back to front, two contributions per iteration (k1 > k2): the
+            // phase 1: per pixel, back to front, two union splats per iteration (k1 > k2): the
             // Gaussians / reciprocals are independent (ILP); only the T and g.S recursions are
-            // serial. Branch-free: lanes without work compute on record 0 and discard.
-            while (__any_sync(kFull, col)) {
-                const bool h1 = col != 0u;
-                const int k1 = 31 - __clz(col | 1u);
-                col &= ~(1u << k1);
-                const bool h2 = col != 0u;
-                const int k2 = 31 - __clz(col | 1u);
-                col &= ~(1u << k2);
+            // serial. A lane whose pixel does not blend a splat computes on it and discards.
+            uint32_t rem = un;
+            uint32_t rowp = 4u * (uint32_t)lane;  // byte offset of (row r, this pixel)
+            while (rem) {
+                const int k1 = 31 - __clz(rem);
+                rem &= ~(1u << k1);
+                const bool two = rem != 0u;
+                const int k2 = 31 - __clz(rem | 1u);
+                rem &= ~(1u << k2);
+                const bool h1 = (col >> k1) & 1u;
+                const bool h2 = two && ((col >> k2) & 1u);
                 const uint32_t ad1 = rbase + k1 * kRec, ad2 = rbase + k2 * kRec;
                 const float4 a1 = lds_f4(ad1), a2 = lds_f4(ad2);
                 const float4 b1 = lds_f4(ad1 + 16), b2 = lds_f4(ad2 + 16);
@@ -460,73 +463,96 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
                 const float gS2 = __fmaf_rn(gc2, w2, gSb);
                 T = h2 ? T2 : Tb;
                 gS = h2 ? gS2 : gSb;
-                if (h1) {
-                    const uint32_t o = rec_off(k1, lane);
-                    sts_f1(ubase + o, ds1 * G1);
-                    sts_f1(wbase + o, w1);
-                }
-                if (h2) {
-                    const uint32_t o = rec_off(k2, lane);
-                    sts_f1(ubase + o, ds2 * G2);
-                    sts_f1(wbase + o, w2);
+                sts_f1(ubase + rowp, h1 ? ds1 * G1 : 0.f);
+                sts_f1(wbase + rowp, h1 ? w1 : 0.f);
+                if (two) {
+                    sts_f1(ubase + rowp + 4 * kRecStride, h2 ? ds2 * G2 : 0.f);
+                    sts_f1(wbase + rowp + 4 * kRecStride, h2 ? w2 : 0.f);
                 }
                 visb |= ((h1 && w1 > kMinVisitW) ? (1u << k1) : 0u) | ((h2 && w2 > kMinVisitW) ? (1u << k2) : 0u);
+                rowp += 8 * kRecStride;
             }
             S.st[g][lane] = make_float2(T, gS);
             vism |= __reduce_or_sync(kFull, visb);
             __syncwarp();
-            // phase 2: lane = splat j, dense over the group's 32 pixels; moments about the
-            // group centre (compile-time offsets), shifted to the tile centre below
+            // phase 2: lane i < U = row i (the i-th highest union splat), dense over the group's
+            // 32 pixels; moments about the group centre (compile-time offsets)
             float a0 = 0.f, ax1 = 0.f, ay1 = 0.f, axx = 0.f, axy = 0.f, ayy = 0.f;
-            const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
-            const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
-            const uint32_t gb = smem_addr(S.gcur);
-#ifndef TGSX_EXP_P2_BLOCKS  // experiment knob (cost attribution); 8 = all 32 pixels
-#define TGSX_EXP_P2_BLOCKS 8
-#endif
-            // separable moments: per pixel row r (eta_r fixed) accumulate R = sum u,
-            // Rx = sum u xi, Rxx = sum u xi^2 over the row's 8 columns, then fold the row in
-            // with eta_r (3 FFMA per pixel + 6 per row instead of 6 per pixel)
+            float c0s = 0.f, c1s = 0.f, c2s = 0.f;
+            if (lane < U) {
+                const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
+                const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
+                const uint32_t gb = smem_addr(S.g);
+                // separable moments: per pixel row (eta fixed) accumulate R = sum u,
+                // Rx = sum u xi, Rxx = sum u xi^2 over the row's 8 columns, then fold the row in
+                // with eta (3 FFMA per pixel + 6 per row instead of 6 per pixel). Pixel pairs
+                // (2c, 2c+1) sit in register pairs, so R and the colour sums use the packed
+                // FADD2 / FFMA2 (two lanes of FP32 per instruction).
+                float2 c0p = make_float2(0.f, 0.f), c1p = c0p, c2p = c0p;
 #pragma unroll
-            for (int row = 0; row < TGSX_EXP_P2_BLOCKS / 2; ++row) {
-                float R = 0.f, Rx = 0.f, Rxx = 0.f;
+                for (int row = 0; row < 4; ++row) {
+                    float2 Rp = make_float2(0.f, 0.f);
+                    float Rx = 0.f, Rxx = 0.f;
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    const int l4 = 2 * row + half;
-                    const uint32_t sw = 16u * (uint32_t)(l4 ^ (lane & 7));
-                    const float4 u4 = lds_f4(ur + sw);
-                    const float4 w4 = lds_f4(wr + sw);
-                    const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
-                    const float ww[4] = {w4.x, w4.y, w4.z, w4.w};
+                    for (int half = 0; half < 2; ++half) {
+                        const int l4 = 2 * row + half;
+                        const float4 u4 = lds_f4(ur + 16 * l4);
+                        const float4 w4 = lds_f4(wr + 16 * l4);
+                        const float4 g0 = lds_f4(gb + 16 * l4);  // broadcasts
+                        const float4 g1 = lds_f4(gb + 128 + 16 * l4);
+                        const float4 g2 = lds_f4(gb + 256 + 16 * l4);
+                        const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int l = 4 * l4 + e;
-                        const float xi = (float)(l & 7) - 3.5f;
-                        const float u = uu[e], w = ww[e];
-                        const float4 gl = lds_f4(gb + 16 * l);
-                        R += u;
-                        Rx = __fmaf_rn(u, xi, Rx);
-                        Rxx = __fmaf_rn(u, xi * xi, Rxx);
-                        q0 = __fmaf_rn(w, gl.x, q0);
-                        q1 = __fmaf_rn(w, gl.y, q1);
-                        q2 = __fmaf_rn(w, gl.z, q2);
+                        for (int e = 0; e < 4; ++e) {
+                            const float xi = (float)(4 * half + e) - 3.5f;
+                            Rx = __fmaf_rn(uu[e], xi, Rx);
+                            Rxx = __fmaf_rn(uu[e], xi * xi, Rxx);
+                        }
+                        Rp = __fadd2_rn(Rp, make_float2(u4.x, u4.y));
+                        Rp = __fadd2_rn(Rp, make_float2(u4.z, u4.w));
+                        c0p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g0.x, g0.y), c0p);
+                        c0p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g0.z, g0.w), c0p);
+                        c1p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g1.x, g1.y), c1p);
+                        c1p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g1.z, g1.w), c1p);
+                        c2p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g2.x, g2.y), c2p);
+                        c2p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g2.z, g2.w), c2p);
                     }
+                    const float R = Rp.x + Rp.y;
+                    const float eta = (float)row - 1.5f;
+                    a0 += R;
+                    ax1 += Rx;
+                    ay1 = __fmaf_rn(R, eta, ay1);
+                    axx += Rxx;
+                    axy = __fmaf_rn(Rx, eta, axy);
+                    ayy = __fmaf_rn(R, eta * eta, ayy);
                 }
-                const float eta = (float)row - 1.5f;
-                a0 += R;
-                ax1 += Rx;
-                ay1 = __fmaf_rn(R, eta, ay1);
-                axx += Rxx;
-                axy = __fmaf_rn(Rx, eta, axy);
-                ayy = __fmaf_rn(R, eta * eta, ayy);
+                c0s = c0p.x + c0p.y;
+                c1s = c1p.x + c1p.y;
+                c2s = c2p.x + c2p.y;
             }
-            const float dx = (float)(gx * 8) + 3.5f - hx, dy = (float)(gy * 4) + 1.5f - hy;
-            m0 += a0;
-            mx1 += ax1 + dx * a0;
-            my1 += ay1 + dy * a0;
-            mxx += axx + 2.f * dx * ax1 + dx * dx * a0;
-            mxy += axy + dy * ax1 + dx * ay1 + dx * dy * a0;
-            myy += ayy + 2.f * dy * ay1 + dy * dy * a0;
+            // hand row i's sums to lane j = its splat (row of j = union bits above j)
+            const int src = __popc(un & (0xfffffffeu << lane));
+            a0 = __shfl_sync(kFull, a0, src);
+            ax1 = __shfl_sync(kFull, ax1, src);
+            ay1 = __shfl_sync(kFull, ay1, src);
+            axx = __shfl_sync(kFull, axx, src);
+            axy = __shfl_sync(kFull, axy, src);
+            ayy = __shfl_sync(kFull, ayy, src);
+            c0s = __shfl_sync(kFull, c0s, src);
+            c1s = __shfl_sync(kFull, c1s, src);
+            c2s = __shfl_sync(kFull, c2s, src);
+            if ((un >> lane) & 1u) {
+                const float dx = (float)(gx * 8) + 3.5f - hx, dy = (float)(gy * 4) + 1.5f - hy;
+                m0 += a0;
+                mx1 += ax1 + dx * a0;
+                my1 += ay1 + dy * a0;
+                mxx += axx + 2.f * dx * ax1 + dx * dx * a0;
+                mxy += axy + dy * ax1 + dx * ay1 + dx * dy * a0;
+                myy += ayy + 2.f * dy * ay1 + dy * dy * a0;
+                q0 += c0s;
+                q1 += c1s;
+                q2 += c2s;
+            }
         }
         if (jvalid) {
             float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
