@@ -316,9 +316,21 @@ struct BwdWarpSmem {
     float rec_u[32 * kRecStride];  // phase-1 records [union row][pixel]
     float rec_w[32 * kRecStride];
     float2 st[NG][32];             // per-pixel (T, g.S) carried across chunks
-    float g[3][32];                // dL/dC of the current group's pixels, planar (phase-2 broadcast)
+    float lg[2][4][32];            // (last, dL/dC) of the current / next group, planar; filled by
+                                   // cp.async one group ahead (phase 2 broadcasts dL/dC from here)
     unsigned char rec[32 * kRec];
 };
+
+// 4-byte global -> shared async copy (zero-fill when src_bytes == 0)
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 
 template <int NGX, int NGY>
@@ -377,6 +389,27 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
         prm.partial.c[slot] = make_float2(0.f, 0.f);
     }
 
+    // per-group (last, dL/dC) prefetch, one group ahead, cyclic over the groups of every chunk
+    const uint32_t lgbase = smem_addr(S.lg);
+    auto prefetch = [&](int g, int buf) {
+        const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
+        const bool valid = lx < geo.acols && ly < geo.arows;
+        int r = 0;
+        if (valid) {
+            const int x = geo.ax + lx * p, y = geo.ay + ly * p;
+            r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
+        }
+        const uint32_t nb = valid ? 4u : 0u;
+        const uint32_t d = lgbase + 512u * (uint32_t)buf + 4u * (uint32_t)lane;
+        cp_async4(d, prm.last + r, nb);
+        cp_async4(d + 128, prm.dLdC + 3 * r, nb);
+        cp_async4(d + 256, prm.dLdC + 3 * r + 1, nb);
+        cp_async4(d + 384, prm.dLdC + 3 * r + 2, nb);
+        cp_async_commit();
+    };
+    int buf = 0;
+    prefetch(0, 0);
+
     const int nch = ((int)maxlast + 31) / 32;
     for (int ch = nch - 1; ch >= 0; --ch) {
         const int c0 = ch * 32;
@@ -397,18 +430,15 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
 #pragma unroll 1
         for (int g = 0; g < NG; ++g) {
             const int gx = g % NGX, gy = g / NGX;
+            const int cur = buf;
+            buf ^= 1;
+            __syncwarp();  // the previous group's phase 2 is done with the rows and lg[buf]
+            prefetch(g + 1 < NG ? g + 1 : 0, buf);
             uint32_t col = transpose32(group_rowmask(mask, gx, gy));
-            float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
-            uint32_t glast = 0;
-            {
-                const int lx = gx * 8 + (lane & 7), ly = gy * 4 + (lane >> 3);
-                if (lx < geo.acols && ly < geo.arows) {
-                    const int x = geo.ax + lx * p, y = geo.ay + ly * p;
-                    const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
-                    glast = prm.last[r];
-                    gv = make_float4(prm.dLdC[3 * r], prm.dLdC[3 * r + 1], prm.dLdC[3 * r + 2], 0.f);
-                }
-            }
+            cp_async_wait<1>();
+            __syncwarp();
+            const uint32_t glast = __float_as_uint(S.lg[cur][0][lane]);
+            const float4 gv = make_float4(S.lg[cur][1][lane], S.lg[cur][2][lane], S.lg[cur][3][lane], 0.f);
             // only splats before this pixel's last contributor were blended
             const int span = (int)glast - c0;
             col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
@@ -422,10 +452,6 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             float2 st = S.st[g][lane];
             float T = st.x, gS = st.y;
             const float fxg = fxl + (float)(gx * 8 * p), fyg = fyl + (float)(gy * 4 * p);
-            __syncwarp();  // the previous group's phase 2 is done with the rows and g
-            S.g[0][lane] = gv.x;
-            S.g[1][lane] = gv.y;
-            S.g[2][lane] = gv.z;
             uint32_t visb = 0;
             // phase 1: per pixel, back to front, two union splats per iteration (k1 > k2): the
             // Gaussians / reciprocals are independent (ILP); only the T and g.S recursions are
@@ -482,7 +508,7 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             if (lane < U) {
                 const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
                 const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
-                const uint32_t gb = smem_addr(S.g);
+                const uint32_t gb = lgbase + 512u * (uint32_t)cur + 128u;  // lg[cur][1..3]
                 // separable moments: per pixel row (eta fixed) accumulate R = sum u,
                 // Rx = sum u xi, Rxx = sum u xi^2 over the row's 8 columns, then fold the row in
                 // with eta (3 FFMA per pixel + 6 per row instead of 6 per pixel). Pixel pairs
@@ -579,6 +605,7 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             prm.partial.c[slot] = make_float2(q2, ((vism >> lane) & 1u) ? 1.0f : 0.0f);
         }
     }
+    cp_async_wait<0>();  // drain the last (unused) prefetch
 }
 
 BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items) {
