@@ -127,7 +127,11 @@ int32_t tgsx_adam_step(tgsx_ctx* ctx, tgsx_model* m, const float* grads,
 
 /* One fused fit iteration on one view: render -> L1 loss over active pixels
  * -> backward -> densify stats -> Adam. target: full-resolution W*H*3 float RGB, host or
- * device (a host pointer is copied inside the call). *out_loss (host or device, may be NULL).
+ * device. A host target is copied on the context's copy stream into one of two staging
+ * buffers, overlapping the previous call's kernels; the caller may reuse a pinned target
+ * buffer after the next tgsx_synchronize (pageable buffers are consumed before returning).
+ * *out_loss may be NULL, device, pinned host (written in stream order: read it after
+ * tgsx_synchronize) or pageable host (written before returning).
  * Equivalent to render + L1 + backward + tgsx_adam_step with the same args. */
 int32_t tgsx_fit_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
                       const float* target, const tgsx_adam_args* a, float* out_loss);

@@ -370,6 +370,57 @@ int32_t stage_input(tgsx_ctx* ctx, DevBuf& dst, const float* src, size_t bytes, 
     return TGSX_OK;
 }
 
+bool is_pinned_host_ptr(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// View target: device pointers are used in place; host targets go through two staging buffers
+// filled on the copy stream, so the H2D of this view overlaps the previous view's kernels (the
+// compute stream waits for the copy; the next copy into a buffer waits for the forward that
+// read it, see mark_target_consumed).
+int32_t stage_target(tgsx_ctx* ctx, const float* src, size_t bytes, const float** out) {
+    if (is_device_ptr(src)) {
+        *out = src;
+        return TGSX_OK;
+    }
+    if (!ctx->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&ctx->staged[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->consumed[i], cudaEventDisableTiming));
+        }
+    }
+    const int k = ctx->stage_next;
+    ctx->stage_next ^= 1;
+    DevBuf& b = ctx->stage_buf[k];
+    if (b.bytes < bytes) {
+        CK(cudaStreamSynchronize(ctx->copy_stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(b.ensure(bytes));
+    }
+    if (ctx->stage_used[k]) CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->consumed[k], 0));
+    CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+    CK(cudaEventRecord(ctx->staged[k], ctx->copy_stream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->staged[k], 0));
+    ctx->stage_pending = k;
+    *out = b.as<float>();
+    return TGSX_OK;
+}
+
+int32_t mark_target_consumed(tgsx_ctx* ctx) {
+    if (ctx->stage_pending >= 0) {
+        CK(cudaEventRecord(ctx->consumed[ctx->stage_pending], ctx->stream));
+        ctx->stage_used[ctx->stage_pending] = true;
+        ctx->stage_pending = -1;
+    }
+    return TGSX_OK;
+}
+
 int32_t render_core(tgsx_ctx* ctx, tgsx_model* m, const RenderArgs& ra, bool fused_loss,
                     uint32_t** items_out) {
     uint32_t* items = nullptr;
@@ -409,11 +460,12 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
     if (!target) return fail(ctx, TGSX_EINVAL, "target is null");
     RenderArgs ra = make_args(pat, bg, 0);
     Workspace& ws = ctx->ws;
-    rc = stage_input(ctx, ws.target, target, (size_t)ra.W * ra.H * 12, &ra.target);
+    rc = stage_target(ctx, target, (size_t)ra.W * ra.H * 12, &ra.target);
     if (rc) return rc;
     uint32_t* items = nullptr;
     rc = render_core(ctx, m, ra, true, &items);
     if (rc) return rc;
+    if ((rc = mark_target_consumed(ctx))) return rc;  // the fused L1 is the target's only reader
     {
         StageTimer t(ctx, kStBackward);
         CK(launch_backward(ctx, ra, items));
@@ -432,8 +484,11 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
     }
     CK(cudaGetLastError());
     if (out_loss) {
+        // device and pinned host destinations are written in stream order (read the pinned
+        // value after tgsx_synchronize); pageable host memory is written before returning
         CK(cudaMemcpyAsync(out_loss, dloss, 4, cudaMemcpyDefault, ctx->stream));
-        if (!is_device_ptr(out_loss)) CK(cudaStreamSynchronize(ctx->stream));
+        if (!is_device_ptr(out_loss) && !is_pinned_host_ptr(out_loss))
+            CK(cudaStreamSynchronize(ctx->stream));
     }
     return TGSX_OK;
 }
@@ -471,6 +526,15 @@ void tgsx_destroy(tgsx_ctx* ctx) {
                       &ws.T, &ws.last, &ws.dLdC, &ws.target, &ws.block_loss, &ws.counters,
                       &ws.generic};
     for (DevBuf* b : bufs) b->release();
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+        for (int i = 0; i < 2; ++i) {
+            ctx->stage_buf[i].release();
+            cudaEventDestroy(ctx->staged[i]);
+            cudaEventDestroy(ctx->consumed[i]);
+        }
+    }
     if (ws.h_scratch) cudaFreeHost(ws.h_scratch);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;

@@ -83,6 +83,13 @@ struct tgsx_ctx {
     uint64_t launches = 0;
     tgsx::Workspace ws;
     tgsx::Profiler prof;
+    // host-resident view targets: double-buffered H2D on a copy stream so the copy of view i+1
+    // overlaps the kernels of view i (events order buffer reuse against the compute stream)
+    cudaStream_t copy_stream = nullptr;
+    tgsx::DevBuf stage_buf[2];
+    cudaEvent_t staged[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    bool stage_used[2] = {false, false};
+    int stage_next = 0, stage_pending = -1;
 };
 
 // Scoped stage timer: no-op unless profiling is enabled.
