@@ -205,8 +205,18 @@ cudaError_t reset_counters(tgsx_ctx* ctx) {
     return cudaMemsetAsync(ws.counters.p, 0xff, sizeof(unsigned long long), ctx->stream);
 }
 
-// Sort (if dirty) -> preprocess -> scan -> [sync for K] -> duplicate -> onesweep -> ranges.
-// On return ws.K, ws.ranges and `items` (sorted ranks) describe the per-tile lists.
+bool force_onesweep() {
+    static const bool v = [] {
+        const char* s = std::getenv("TGSX_BINNING");
+        return s && std::string(s) == "onesweep";
+    }();
+    return v;
+}
+
+// Sort (if dirty) -> preprocess (+ per-tile lengths) -> scans -> [sync for K, longest list] ->
+// scatter + per-tile sort, or (a list longer than kSegCap, or TGSX_BINNING=onesweep)
+// duplicate -> onesweep radix sort -> ranges.
+// On return ws.K, ws.ranges and `items` (per-tile ranks in blend order) describe the lists.
 int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t** items,
             uint32_t** sorted_keys) {
     Workspace& ws = ctx->ws;
@@ -222,27 +232,42 @@ int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t*
     }
     unsigned long long* counters = ws.counters.as<unsigned long long>();
     uint32_t* d_total = reinterpret_cast<uint32_t*>(counters + 3);
+    const int tiles = ws.tiles_x * ws.tiles_y;
     {
         StageTimer t(ctx, kStScan);
         CK(launch_exclusive_scan(ctx, ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(), m->n, d_total));
+        CK(launch_tile_finalize(ctx, tiles));
     }
-    CK(cudaMemcpyAsync(ws.h_scratch, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(ws.h_scratch, counters, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof.enabled) ctx->prof.harvest();  // every event recorded so far has completed
     int32_t rc = check_kernel_error(ctx, ws.h_scratch[0]);
     if (rc) return rc;
     const int64_t K = (int64_t)(uint32_t)(ws.h_scratch[3] & 0xffffffffull);
+    const uint64_t max_list = ws.h_scratch[5];
     ws.K = K;
-    const int tiles = ws.tiles_x * ws.tiles_y;
-    const int key_bits = key_bits_for(tiles);
-    const int passes = (key_bits + 7) / 8;
-    for (int i = 0; i < 2; ++i) {
-        CK(ws.keys[i].ensure(std::max<int64_t>(K, 1) * 4));
-        CK(ws.vals[i].ensure(std::max<int64_t>(K, 1) * 4));
-    }
+    for (int i = 0; i < 2; ++i) CK(ws.vals[i].ensure(std::max<int64_t>(K, 1) * 4));
     CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
     ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
+    if (max_list <= (uint64_t)kSegCap && !force_onesweep()) {
+        // scatter binning: tile lists claimed with atomics, then sorted per tile in shared memory
+        uint32_t* v = ws.vals[0].as<uint32_t>();
+        {
+            StageTimer t(ctx, kStDuplicate);
+            CK(launch_scatter(ctx, m, v));
+        }
+        {
+            StageTimer t(ctx, kStSort);
+            CK(launch_seg_sort(ctx, v, tiles));
+        }
+        *items = v;
+        if (sorted_keys) *sorted_keys = nullptr;
+        return TGSX_OK;
+    }
+    const int key_bits = key_bits_for(tiles);
+    const int passes = (key_bits + 7) / 8;
+    for (int i = 0; i < 2; ++i) CK(ws.keys[i].ensure(std::max<int64_t>(K, 1) * 4));
     // sized once here: duplicate writes the digit histograms at its head and sort_pairs must
     // not reallocate it afterwards
     CK(ws.sort_tmp.ensure(sort_scratch_bytes(K, key_bits)));
@@ -524,7 +549,7 @@ void tgsx_destroy(tgsx_ctx* ctx) {
     DevBuf* bufs[] = {&ws.prep, &ws.touched, &ws.pair_off, &ws.scan_tmp, &ws.keys[0], &ws.keys[1],
                       &ws.vals[0], &ws.vals[1], &ws.sort_tmp, &ws.ranges, &ws.partial, &ws.rgb,
                       &ws.T, &ws.last, &ws.dLdC, &ws.target, &ws.block_loss, &ws.counters,
-                      &ws.generic};
+                      &ws.generic, &ws.tile_count, &ws.tile_off, &ws.tile_fill};
     for (DevBuf* b : bufs) b->release();
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);
@@ -855,20 +880,25 @@ int32_t tgsx_stage_tile_lists(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, i
     const int64_t K = ctx->ws.K;
     if (out_k) *out_k = K;
     const int tiles = ctx->ws.tiles_x * ctx->ws.tiles_y;
-    std::vector<uint32_t> hk(K);
+    std::vector<uint2> rg(tiles);
+    std::vector<uint32_t> hi(K);
     // the context stream is non-blocking: order the legacy-stream copies after bin()'s kernels
     CK(cudaStreamSynchronize(ctx->stream));
-    if (K) CK(cudaMemcpy(hk.data(), keys, K * 4, cudaMemcpyDeviceToHost));
-    for (int64_t s = 0; s < K; ++s) {
-        if (hk[s] >= (uint32_t)tiles || (s && hk[s] < hk[s - 1]))
-            return fail(ctx, TGSX_ESTATE, "tile keys not sorted / out of range at " + std::to_string(s));
+    if (tiles) CK(cudaMemcpy(rg.data(), ctx->ws.ranges.p, (size_t)tiles * sizeof(uint2), cudaMemcpyDeviceToHost));
+    if (K) CK(cudaMemcpy(hi.data(), it, K * 4, cudaMemcpyDeviceToHost));
+    // validate the lists: contiguous in tile order, ranks strictly ascending inside each tile
+    std::vector<uint32_t> off(tiles + 1, 0);
+    for (int t = 0; t < tiles; ++t) {
+        const uint32_t c = rg[t].y - rg[t].x;
+        if (rg[t].y < rg[t].x || (c && rg[t].x != off[t]))
+            return fail(ctx, TGSX_ESTATE, "tile ranges not contiguous at tile " + std::to_string(t));
+        for (uint32_t s = rg[t].x + 1; s < rg[t].y; ++s)
+            if (hi[s] <= hi[s - 1])
+                return fail(ctx, TGSX_ESTATE, "tile list not in blend order at " + std::to_string(s));
+        off[t + 1] = off[t] + c;
     }
-    if (offsets) {
-        std::vector<uint32_t> off(tiles + 1, 0);
-        for (int64_t s = 0; s < K; ++s) off[hk[s] + 1]++;
-        for (int t = 0; t < tiles; ++t) off[t + 1] += off[t];
-        CK(cudaMemcpy(offsets, off.data(), off.size() * 4, cudaMemcpyDefault));
-    }
+    if (off[tiles] != (uint64_t)K) return fail(ctx, TGSX_ESTATE, "tile ranges do not cover the pairs");
+    if (offsets) CK(cudaMemcpy(offsets, off.data(), off.size() * 4, cudaMemcpyDefault));
     if (items && items_cap >= K && K) CK(cudaMemcpy(items, it, K * 4, cudaMemcpyDefault));
     return TGSX_OK;
 }

@@ -23,7 +23,8 @@ namespace {
 __global__ void __launch_bounds__(256) preprocess_kernel(
     const float* __restrict__ params, int64_t cap, int64_t n,
     const uint32_t* __restrict__ rank_of, int lowpass_p, int W, int H, int tiles_x,
-    Prepared* __restrict__ prep, uint32_t* __restrict__ touched, unsigned long long* err) {
+    Prepared* __restrict__ prep, uint32_t* __restrict__ touched, uint32_t* __restrict__ tile_count,
+    unsigned long long* err) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t rank = rank_of[i];
@@ -66,6 +67,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
         o.d = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16),
                          0u, tiles);
+        if (tile_count)  // per-tile list lengths for the scatter binning (fire-and-forget RED)
+            for (int ty = ty0; ty <= ty1; ++ty)
+                for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&tile_count[ty * tiles_x + tx], 1u);
     } else {
         o.d = make_uint4(0u, 0u, 0u, 0u);
     }
@@ -115,9 +119,149 @@ __global__ void ranges_kernel(const uint32_t* __restrict__ keys, int64_t K, uint
     if (s == K - 1 || keys[s + 1] != t) ranges[t].y = (uint32_t)(s + 1);
 }
 
+// ------------------------------------------------------------------ scatter binning
+// Per-tile lists from the per-tile lengths (counted by preprocess): tile t's list occupies
+// [off[t], off[t] + cnt[t]) == TileGrid::offsets (rasterizer.cpp:92-100). fill[t] starts at
+// off[t]; the scatter claims slots with atomics (arbitrary order inside a tile) and the
+// per-tile sort restores blend (rank) order, so the result is deterministic.
+__global__ void tile_finalize_kernel(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
+                                     int tiles, uint2* __restrict__ ranges, uint32_t* __restrict__ fill,
+                                     unsigned long long* __restrict__ max_cnt) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t c = 0;
+    if (t < tiles) {
+        c = cnt[t];
+        const uint32_t o = off[t];
+        ranges[t] = make_uint2(o, o + c);
+        fill[t] = o;
+    }
+    c = __reduce_max_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicMax(max_cnt, (unsigned long long)c);
+}
+
+__global__ void __launch_bounds__(256) scatter_kernel(
+    Prepared* __restrict__ prep, const uint32_t* __restrict__ pair_off, int64_t n, int tiles_x,
+    uint32_t* __restrict__ fill, uint32_t* __restrict__ items) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint4 d = prep[r].d;
+    if (!d.w) return;
+    prep[r].d.z = pair_off[r];  // partial-slot base of this splat (rank-major pair order)
+    const int tx0 = d.x & 0xffff, tx1 = d.x >> 16, ty0 = d.y & 0xffff;
+    const int w = tx1 - tx0 + 1, cnt = (int)d.w;
+    // four independent slot claims in flight per iteration (the atomics' latency dominates)
+    for (int i = 0; i < cnt; i += 4) {
+        uint32_t pos[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i + u < cnt) {
+                const int q = i + u, ty = ty0 + q / w, tx = tx0 + q % w;
+                pos[u] = atomicAdd(&fill[ty * tiles_x + tx], 1u);
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i + u < cnt) items[pos[u]] = (uint32_t)r;
+    }
+}
+
+// Bitonic sort of 32*E keys held by one warp, lane L owning positions L*E .. L*E+E-1:
+// partners closer than E are in-register compare-exchanges, farther ones one shuffle.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&x)[E], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= E) {
+                const int lm = j / E;
+                const bool lower = (lane & lm) == 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const uint32_t y = __shfl_xor_sync(0xffffffffu, x[e], lm);
+                    const bool asc = ((lane * E + e) & k) == 0;
+                    x[e] = (asc == lower) ? min(x[e], y) : max(x[e], y);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if ((e & j) == 0) {
+                        const bool asc = ((lane * E + e) & k) == 0;
+                        const uint32_t a = x[e], b = x[e | j];
+                        x[e] = asc ? min(a, b) : max(a, b);
+                        x[e | j] = asc ? max(a, b) : min(a, b);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void warp_sort_list(uint32_t* __restrict__ list, int n, int lane) {
+    uint32_t x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = lane * E + e < n ? list[lane * E + e] : 0xffffffffu;
+    warp_bitonic<E>(x, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        if (lane * E + e < n) list[lane * E + e] = x[e];
+}
+
+// One warp per tile: the tile's ranks (claimed in arbitrary order by the scatter) sorted back
+// into blend order in registers (lists <= kSegCap = 1024).
+__global__ void __launch_bounds__(256) seg_sort_kernel(const uint2* __restrict__ ranges, int tiles,
+                                                       uint32_t* __restrict__ items) {
+    const int lane = threadIdx.x & 31;
+    const int tile = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (tile >= tiles) return;
+    const uint2 rg = ranges[tile];
+    const int n = (int)(rg.y - rg.x);
+    uint32_t* list = items + rg.x;
+    if (n <= 1) return;
+    if (n <= 32) warp_sort_list<1>(list, n, lane);
+    else if (n <= 64) warp_sort_list<2>(list, n, lane);
+    else if (n <= 128) warp_sort_list<4>(list, n, lane);
+    else if (n <= 256) warp_sort_list<8>(list, n, lane);
+    else if (n <= 512) warp_sort_list<16>(list, n, lane);
+    else warp_sort_list<32>(list, n, lane);
+}
+
 inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / bt); }
 
 }  // namespace
+
+cudaError_t launch_tile_finalize(tgsx_ctx* ctx, int tiles) {
+    Workspace& ws = ctx->ws;
+    cudaError_t e;
+    if ((e = ws.ranges.ensure((size_t)std::max(tiles, 1) * sizeof(uint2)))) return e;
+    if ((e = ws.tile_fill.ensure((size_t)std::max(tiles, 1) * 4))) return e;
+    unsigned long long* counters = ws.counters.as<unsigned long long>();
+    if ((e = launch_exclusive_scan(ctx, ws.tile_count.as<uint32_t>(), ws.tile_off.as<uint32_t>(), tiles,
+                                   nullptr)))
+        return e;
+    tile_finalize_kernel<<<grid_for(tiles, 256), 256, 0, ctx->stream>>>(
+        ws.tile_count.as<uint32_t>(), ws.tile_off.as<uint32_t>(), tiles, ws.ranges.as<uint2>(),
+        ws.tile_fill.as<uint32_t>(), counters + 5);
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(tgsx_ctx* ctx, tgsx_model* m, uint32_t* items) {
+    Workspace& ws = ctx->ws;
+    const int64_t n = m->n;
+    if (n == 0 || ws.K == 0) return cudaSuccess;
+    scatter_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+        ws.prep.as<Prepared>(), ws.pair_off.as<uint32_t>(), n, ws.tiles_x, ws.tile_fill.as<uint32_t>(), items);
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles) {
+    if (ctx->ws.K == 0 || tiles == 0) return cudaSuccess;
+    seg_sort_kernel<<<grid_for(tiles, 8), 256, 0, ctx->stream>>>(ctx->ws.ranges.as<uint2>(), tiles, items);
+    ctx->launches++;
+    return cudaGetLastError();
+}
 
 int key_bits_for(int tiles) {
     int b = 0;
@@ -134,10 +278,15 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
     if ((e = ws.pair_off.ensure((n + 1) * 4))) return e;
     ws.tiles_x = (W + kTile - 1) / kTile;
     ws.tiles_y = (H + kTile - 1) / kTile;
+    const size_t tb = (size_t)std::max(ws.tiles_x * ws.tiles_y, 1) * 4;
+    if ((e = ws.tile_count.ensure(tb))) return e;
+    if ((e = ws.tile_off.ensure(tb))) return e;
+    if ((e = cudaMemsetAsync(ws.tile_count.p, 0, tb, ctx->stream))) return e;
     if (n == 0) return cudaSuccess;
     preprocess_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
         m->params.as<float>(), m->cap, n, m->rank_of.as<uint32_t>(), lowpass_p, W, H, ws.tiles_x,
-        ws.prep.as<Prepared>(), ws.touched.as<uint32_t>(), ws.counters.as<unsigned long long>());
+        ws.prep.as<Prepared>(), ws.touched.as<uint32_t>(), ws.tile_count.as<uint32_t>(),
+        ws.counters.as<unsigned long long>());
     ctx->launches++;
     return cudaGetLastError();
 }

@@ -40,6 +40,7 @@ struct Workspace {
     DevBuf keys[2], vals[2];  // u32[K] ping-pong
     DevBuf sort_tmp;          // histograms + block status + tickets
     DevBuf ranges;            // uint2[tiles]
+    DevBuf tile_count, tile_off, tile_fill;  // u32[tiles] scatter binning (lengths, offsets, cursors)
     DevBuf partial;           // per-(tile, splat) gradient partials, Partials SoA (40 B/pair)
     int64_t pair_cap = 0;     // pairs the partial buffer holds
     // per-pixel
@@ -151,6 +152,12 @@ size_t sort_scratch_bytes(int64_t n, int key_bits);
 cudaError_t sort_pairs(tgsx_ctx* ctx, uint32_t*& keys, uint32_t*& vals, uint32_t* keys_alt,
                        uint32_t* vals_alt, int64_t n, int key_bits, const uint32_t* d_hist);
 cudaError_t launch_ranges(tgsx_ctx* ctx, const uint32_t* keys, int64_t K, int tiles);
+// scatter binning: per-tile lengths counted by preprocess -> offsets/ranges -> atomic scatter ->
+// per-tile warp register sort (lists up to kSegCap; longer lists take the onesweep path)
+constexpr int kSegCap = 1024;
+cudaError_t launch_tile_finalize(tgsx_ctx* ctx, int tiles);
+cudaError_t launch_scatter(tgsx_ctx* ctx, tgsx_model* m, uint32_t* items);
+cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles);
 cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
                            bool fused_loss);
 cudaError_t launch_backward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items);

@@ -80,6 +80,46 @@ def test_tile_lists_bitexact(P, ctx, W, H, n, lowpass):
     assert np.array_equal(items, ritems)
 
 
+def test_tile_lists_long_list_fallback(P, ctx):
+    """A tile list longer than the per-tile warp sort (kSegCap = 1024) takes the
+    onesweep radix-sort path; the lists must still equal the reference's."""
+    W, H, n = 64, 64, 6000
+    s = B.synthetic_scene(11, n, W, H)
+    rng = np.random.default_rng(1)
+    s.px[:] = (8.0 + rng.uniform(-2, 2, n)).astype(np.float32)
+    s.py[:] = (8.0 + rng.uniform(-2, 2, n)).astype(np.float32)
+    s.lsx[:] = np.float32(0.0)
+    s.lsy[:] = np.float32(0.0)
+    dm = P.DeviceModel.from_host(model_from_scene(s), ctx)
+    off, items = dm.stage_tile_lists(1, W, H)
+    roff, ritems = B.tile_grid(s, 1, W, H)
+    assert np.diff(roff.astype(np.int64)).max() > 1024
+    assert np.array_equal(off, roff)
+    assert np.array_equal(items, ritems)
+
+
+def test_tile_lists_forced_onesweep():
+    """TGSX_BINNING=onesweep forces the radix-sort binning for every view: same lists."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, paper_2412_13547_b200 as P\n"
+        "from oracle import bind as B\n"
+        "from tests.helpers import model_from_scene\n"
+        "B.set_math(True)\n"
+        "s = B.synthetic_scene(5, 20000, 400, 300)\n"
+        "dm = P.DeviceModel.from_host(model_from_scene(s), P.Context(0))\n"
+        "off, items = dm.stage_tile_lists(1, 400, 300)\n"
+        "roff, ritems = B.tile_grid(s, 1, 400, 300)\n"
+        "assert np.array_equal(off, roff) and np.array_equal(items, ritems)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TGSX_BINNING="onesweep")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+
+
 def _render_check(got, ref):
     rgb, T, ops = got.colors, got.final_transmittance, got.blend_op_count
     rrgb, rT, rops, _ = ref
