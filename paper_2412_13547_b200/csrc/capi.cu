@@ -185,6 +185,73 @@ cudaError_t model_reserve(tgsx_ctx* ctx, tgsx_model* m, int64_t cap) {
     return cudaSuccess;
 }
 
+// ---------------------------------------------------------------- physical row order
+// Between depth sorts the blend order is fixed (depth_key is not optimised), so the model rows
+// are kept physically in blend (rank) order: preprocess, the partial merge and Adam then stream
+// every per-Gaussian array contiguously instead of gathering through rank_of. Densify, download
+// and the explicit-gradient APIs see the logical (creation) order; permute_model converts.
+template <typename T>
+__global__ void permute_rows_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t cap,
+                                    int64_t n, int rows, const uint32_t* __restrict__ idx) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int64_t q = idx[p];
+    for (int r = 0; r < rows; ++r) dst[(int64_t)r * cap + p] = src[(int64_t)r * cap + q];
+}
+
+// every row group: new[p] = old[idx[p]] (through the model's spare buffers, pointer swap)
+cudaError_t permute_model(tgsx_ctx* ctx, tgsx_model* m, const uint32_t* idx) {
+    const int64_t n = m->n, cap = m->cap;
+    if (n == 0) return cudaSuccess;
+    struct R { DevBuf* b; int rows; int elt; } rs[] = {
+        {&m->params, kParamRows, 4}, {&m->ids, 1, 8}, {&m->pos_acc, 1, 4}, {&m->col_acc, 1, 4},
+        {&m->accum, 1, 4}, {&m->visit, 1, 8}, {&m->window, 1, 8}, {&m->tau_v, 1, 8},
+        {&m->m1, 9, 4}, {&m->m2, 9, 4}, {&m->step, kStepFloats, 4}};
+    static_assert(sizeof(rs) / sizeof(rs[0]) == sizeof(m->spare) / sizeof(m->spare[0]), "spares");
+    cudaError_t e;
+    for (int i = 0; i < 11; ++i) {
+        const R& r = rs[i];
+        DevBuf& sp = m->spare[i];
+        const size_t bytes = (size_t)r.rows * cap * r.elt;
+        if (sp.bytes < bytes) {
+            if ((e = cudaStreamSynchronize(ctx->stream))) return e;
+            sp.release();
+            if ((e = cudaMalloc(&sp.p, bytes))) return e;
+            sp.bytes = bytes;
+        }
+        const unsigned grid = (unsigned)((n + 255) / 256);
+        if (r.elt == 4)
+            permute_rows_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(r.b->as<uint32_t>(), sp.as<uint32_t>(),
+                                                                        cap, n, r.rows, idx);
+        else
+            permute_rows_kernel<unsigned long long><<<grid, 256, 0, ctx->stream>>>(
+                r.b->as<unsigned long long>(), sp.as<unsigned long long>(), cap, n, r.rows, idx);
+        ctx->launches++;
+        if ((e = cudaGetLastError())) return e;
+        std::swap(r.b->p, sp.p);
+        std::swap(r.b->bytes, sp.bytes);
+    }
+    return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t model_to_blend_order(tgsx_ctx* ctx, tgsx_model* m) {
+    if (m->blend_phys || m->order_dirty) return cudaSuccess;
+    cudaError_t e = permute_model(ctx, m, m->perm.as<uint32_t>());
+    if (!e) m->blend_phys = true;
+    return e;
+}
+
+cudaError_t model_to_logical_order(tgsx_ctx* ctx, tgsx_model* m) {
+    if (!m->blend_phys) return cudaSuccess;
+    cudaError_t e = permute_model(ctx, m, m->rank_of.as<uint32_t>());
+    if (!e) m->blend_phys = false;
+    return e;
+}
+
+namespace {
+
 // ---------------------------------------------------------------- error word
 int32_t check_kernel_error(tgsx_ctx* ctx, unsigned long long err) {
     if (err == kErrNone) return TGSX_OK;
@@ -222,9 +289,10 @@ int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t*
     Workspace& ws = ctx->ws;
     ws.have_forward = false;
     CK(reset_counters(ctx));
-    if (m->order_dirty) {
+    if (m->order_dirty || !m->blend_phys) {
         StageTimer t(ctx, kStDepthSort);
-        CK(launch_sort_depth(ctx, m));
+        if (m->order_dirty) CK(launch_sort_depth(ctx, m));
+        CK(model_to_blend_order(ctx, m));
     }
     {
         StageTimer t(ctx, kStPreprocess);
@@ -636,6 +704,7 @@ int32_t tgsx_model_upload(tgsx_ctx* ctx, tgsx_model* m, const tgsx_host_scene* h
     const int64_t n = h->n;
     CK(model_reserve(ctx, m, n));
     m->n = n;
+    m->blend_phys = false;  // uploaded rows are in logical order
     cudaStream_t s = ctx->stream;
     const int64_t cap = m->cap;
     float* P = m->params.as<float>();
@@ -689,6 +758,7 @@ int32_t tgsx_model_upload(tgsx_ctx* ctx, tgsx_model* m, const tgsx_host_scene* h
 
 int32_t tgsx_model_download(tgsx_ctx* ctx, tgsx_model* m, tgsx_host_scene* h) {
     if (!ctx || !m || !h) return TGSX_EINVAL;
+    CK(model_to_logical_order(ctx, m));
     const int64_t n = m->n, cap = m->cap;
     cudaStream_t s = ctx->stream;
     float* rows[kParamRows] = {h->px, h->py, h->rot, h->lsx, h->lsy, h->rop, h->cr, h->cg, h->cb, h->depth};
@@ -709,6 +779,8 @@ int32_t tgsx_model_download(tgsx_ctx* ctx, tgsx_model* m, tgsx_host_scene* h) {
 }
 
 int32_t tgsx_model_download_moments(tgsx_ctx* ctx, tgsx_model* m, float* m1, float* m2) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    CK(model_to_logical_order(ctx, m));
     const int64_t n = m->n, cap = m->cap;
     if (n) {
         if (m1) CK(cudaMemcpy2DAsync(m1, n * 4, m->m1.p, cap * 4, n * 4, 9, cudaMemcpyDefault, ctx->stream));
@@ -719,6 +791,8 @@ int32_t tgsx_model_download_moments(tgsx_ctx* ctx, tgsx_model* m, float* m1, flo
 }
 
 int32_t tgsx_model_upload_moments(tgsx_ctx* ctx, tgsx_model* m, const float* m1, const float* m2) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    CK(model_to_logical_order(ctx, m));
     const int64_t n = m->n, cap = m->cap;
     if (n) {
         if (m1) CK(cudaMemcpy2DAsync(m->m1.p, cap * 4, m1, n * 4, n * 4, 9, cudaMemcpyDefault, ctx->stream));
@@ -792,6 +866,7 @@ int32_t tgsx_adam_step(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const t
     if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
     AdamCfg c;
     fill_adam(c, a);
+    CK(model_to_logical_order(ctx, m));  // explicit gradients are in logical order
     const float* g = nullptr;
     int32_t rc = stage_input(ctx, ctx->ws.generic, grads, (size_t)std::max<int64_t>(m->n, 1) * 36, &g);
     if (rc) return rc;

@@ -233,6 +233,8 @@ int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cf
                      uint64_t rng_state[2], tgsx_densify_report* out) {
     if (!ctx || !m || !cfg || !rng_state) return TGSX_EINVAL;
     StageTimer timer(ctx, kStDensify);
+    // selection ties, spawn order and compaction follow the logical (creation) order
+    DCK(model_to_logical_order(ctx, m));
     const int64_t n0 = m->n;
     tgsx_densify_report rep{};
     // colour coin: one draw per event

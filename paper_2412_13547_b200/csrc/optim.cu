@@ -47,6 +47,7 @@ struct ChainParams {
     float* params_w;
     int64_t cap, n;
     const uint32_t* rank_of;
+    const uint32_t* perm;  // non-null: rows stored in blend order (perm[rank] = logical index)
     const Prepared* prep;
     Partials partial;
     float* screen;  // [10][cap] or null
@@ -79,7 +80,10 @@ __global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
     float raw_c[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) raw_c[k] = __ldg(params + (6 + k) * cap + i);
-    const uint32_t r = __ldg(cp.rank_of + i);
+    // blend-ordered rows: row i is rank i and its pair slots follow row i-1's (streaming reads);
+    // logical rows gather through rank_of. Outputs in logical order go to index `li`.
+    const uint32_t r = cp.perm ? (uint32_t)i : __ldg(cp.rank_of + i);
+    const int64_t li = cp.perm ? (int64_t)__ldg(cp.perm + i) : i;
     const uint4 d = __ldg(&cp.prep[r].d);
     float s[10];
 #pragma unroll
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
     }
     if (cp.screen) {
 #pragma unroll
-        for (int k = 0; k < 10; ++k) cp.screen[k * cap + i] = s[k];
+        for (int k = 0; k < 10; ++k) cp.screen[k * cap + li] = s[k];
     }
     const bool visited = s[9] > 0.f;
     // chain rule (rasterizer.cpp:324-346)
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
     }
     if (cp.mode == 0) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) cp.grads[q * cp.n + i] = g[q];
+        for (int q = 0; q < 9; ++q) cp.grads[q * cp.n + li] = g[q];
         return;
     }
     adam_update(cp.params_w, cp.m1, cp.m2, cap, i, g, cp.adam);
@@ -210,9 +214,11 @@ cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool upda
     cp.cap = m->cap;
     cp.n = m->n;
     cp.rank_of = m->rank_of.as<uint32_t>();
+    cp.perm = m->blend_phys ? m->perm.as<uint32_t>() : nullptr;
     cp.prep = ctx->ws.prep.as<Prepared>();
     cp.partial = Partials::at(ctx->ws.partial.p, ctx->ws.pair_cap);
-    cp.screen = m->screen.as<float>();
+    // screen-space sums are kept only for the explicit backward (tgsx_stage_screen_grads)
+    cp.screen = mode == ChainMode::kGrads ? m->screen.as<float>() : nullptr;
     cp.pos_acc = m->pos_acc.as<float>();
     cp.col_acc = m->col_acc.as<float>();
     cp.accum = m->accum.as<int32_t>();

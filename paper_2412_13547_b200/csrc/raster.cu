@@ -22,12 +22,15 @@ namespace {
 // ------------------------------------------------------------------ preprocess
 __global__ void __launch_bounds__(256) preprocess_kernel(
     const float* __restrict__ params, int64_t cap, int64_t n,
-    const uint32_t* __restrict__ rank_of, int lowpass_p, int W, int H, int tiles_x,
+    const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ perm, int blend_phys,
+    int lowpass_p, int W, int H, int tiles_x,
     Prepared* __restrict__ prep, uint32_t* __restrict__ touched, uint32_t* __restrict__ tile_count,
     unsigned long long* err) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t rank = rank_of[i];
+    // row i is rank i when the model is stored in blend order (logical index perm[i])
+    const uint32_t rank = blend_phys ? (uint32_t)i : rank_of[i];
+    const uint32_t orig = blend_phys ? perm[i] : (uint32_t)i;
     const float px = params[i], py = params[cap + i], rot = params[2 * cap + i];
     const float lx = params[3 * cap + i], ly = params[4 * cap + i], rop = params[5 * cap + i];
     const float cr = params[6 * cap + i], cg = params[7 * cap + i], cb = params[8 * cap + i];
@@ -60,7 +63,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     const float rx = fmul(kCullSigmas, __fsqrt_rn(s00));
     const float ry = fmul(kCullSigmas, __fsqrt_rn(s11));
     o.b = make_float4(fdiv(s00, det), activate_cr(rop), rx, ry);
-    o.c = make_float4(activate_cr(cr), activate_cr(cg), activate_cr(cb), __uint_as_float((uint32_t)i));
+    o.c = make_float4(activate_cr(cr), activate_cr(cg), activate_cr(cb), __uint_as_float(orig));
     int tx0, tx1, ty0, ty1;
     uint32_t tiles = 0;
     if (tile_rect(px, py, rx, ry, W, H, tx0, tx1, ty0, ty1)) {
@@ -284,7 +287,8 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
     if ((e = cudaMemsetAsync(ws.tile_count.p, 0, tb, ctx->stream))) return e;
     if (n == 0) return cudaSuccess;
     preprocess_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-        m->params.as<float>(), m->cap, n, m->rank_of.as<uint32_t>(), lowpass_p, W, H, ws.tiles_x,
+        m->params.as<float>(), m->cap, n, m->rank_of.as<uint32_t>(), m->perm.as<uint32_t>(),
+        m->blend_phys ? 1 : 0, lowpass_p, W, H, ws.tiles_x,
         ws.prep.as<Prepared>(), ws.touched.as<uint32_t>(), ws.tile_count.as<uint32_t>(),
         ws.counters.as<unsigned long long>());
     ctx->launches++;

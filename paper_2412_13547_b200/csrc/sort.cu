@@ -374,6 +374,8 @@ cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m) {
     }
     Workspace& ws = ctx->ws;
     cudaError_t e;
+    // ties are broken by id in logical order: sort the logical layout
+    if ((e = model_to_logical_order(ctx, m))) return e;
     for (int i = 0; i < 2; ++i) {
         if ((e = ws.keys[i].ensure(n * 4))) return e;
         if ((e = ws.vals[i].ensure(n * 4))) return e;

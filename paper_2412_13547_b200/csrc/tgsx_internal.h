@@ -113,6 +113,7 @@ struct tgsx_model {
     uint64_t next_id = 0;
     bool order_dirty = true;
     bool ids_monotone = true;
+    bool blend_phys = false;  // rows physically in blend (rank) order (perm maps rank -> logical)
     tgsx::DevBuf params;   // float[10][cap]: px py rot lsx lsy rop cr cg cb depth
     tgsx::DevBuf ids;      // u64[cap]
     tgsx::DevBuf pos_acc, col_acc, accum, visit, window, tau_v;
@@ -124,6 +125,11 @@ struct tgsx_model {
     tgsx::DevBuf spare[11];  // prune compaction targets (swapped with the live rows; no per-event malloc)
     int64_t step_views = 0;
 };
+
+// physical row order of the model (capi.cu): blend order for the hot path, logical (creation)
+// order for densify / download / explicit-gradient APIs
+cudaError_t model_to_blend_order(tgsx_ctx* ctx, tgsx_model* m);
+cudaError_t model_to_logical_order(tgsx_ctx* ctx, tgsx_model* m);
 
 namespace tgsx {
 
