@@ -61,29 +61,56 @@ def env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled every 10 ms during the timed region (NVML; the
+    nvidia-smi CLI as a fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []   # (sm_mhz, max_mhz, [reasons])
         self.stop = threading.Event()
         self.th = threading.Thread(target=self.run, daemon=True)
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self.nvml = None
+
+    def sample_nvml(self):
+        N = self.nvml
+        sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+        mx = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        bits = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        rs = [name for name, attr in self.REASONS if bits & getattr(N, attr, 0)]
+        return sm, mx, rs
+
+    def sample_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rs = [names[i] for i in range(4) if len(f) > 2 + i and f[2 + i].lower().startswith("active")]
+        return float(f[0]), float(f[1]), rs
 
     def run(self):
         while not self.stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self.sample_nvml() if self.nvml else self.sample_smi())
             except Exception:
                 pass
-            self.stop.wait(0.1)
+            self.stop.wait(0.01 if self.nvml else 0.1)
 
     def __enter__(self):
         self.th.start()
@@ -95,15 +122,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted({r for s in self.samples for r in s[2]}),
+                "samples": len(self.samples), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def measured_peaks():
@@ -354,26 +377,41 @@ def run_tgsx(args, cfg):
         e2e_bytes = (W * H * 12 * len(mine), 4 * len(mine))
         units = 1  # one batched step = one fit iteration of the whole job (strong scaling)
 
-    if args.config != "c4":
+    # The fit changes the model (and so the per-step work) every iteration: each timed phase
+    # below restarts from the same initial model, W warm-up steps, then K timed steps, so the
+    # device-resident and the end-to-end numbers measure the same trajectory.
+    def restart():
+        if args.config == "c4":
+            return
+        dm.upload(host)
+        ctx.synchronize()
         for i in range(args.warmup):
             step_fn(i)
         ctx.synchronize()
 
+    restart()
+
     launches0 = ctx.launches
-    ctx.profile(True)
     with ClockSampler(local) as clk:
         ms = timer.run(step_fn, args.steps, args.warmup, ctx)
-    stages = ctx.profile_read()
-    ctx.profile(False)
     launches = ctx.launches - launches0
     counters = ctx.counters()
+    # per-stage CUDA-event timing in a separate run (the event records and their readback add
+    # host work between the launches, so they stay out of the timed region above)
+    prof_steps = min(args.steps, 20)
+    restart()
+    ctx.profile(True)
+    timer.run(step_fn, prof_steps, args.warmup, ctx)
+    stages = ctx.profile_read()
+    ctx.profile(False)
     e2e_ms = None
     if e2e_fn:
         # the host-input path has its own warm-up (staging buffers, copy stream) before timing
+        dm.upload(host)
         for i in range(args.warmup):
-            e2e_fn(args.warmup + args.steps + i)
+            e2e_fn(i)
         ctx.synchronize()
-        e2e_ms = timer.run(e2e_fn, args.steps, 2 * args.warmup + args.steps, ctx)
+        e2e_ms = timer.run(e2e_fn, args.steps, args.warmup, ctx)
     if rank != 0:
         dist.barrier()
         dist.destroy_process_group()
@@ -390,7 +428,7 @@ def run_tgsx(args, cfg):
             "clocks": clocks,
             "gpu_launches": launches,
             "roofline": roofline(stages, counters, clocks, n, args.config),
-            "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},
+            "stages_ms_per_step": {k: v[0] / prof_steps for k, v in stages.items() if v[1]},
             "counters": counters}
     if e2e_ms is not None:
         line["e2e"] = {"value": units * args.steps / (e2e_ms / 1e3), "unit": "iters/s",
