@@ -316,6 +316,7 @@ struct BwdWarpSmem {
     float rec_u[32 * kRecStride];  // phase-1 records [union row][pixel]
     float rec_w[32 * kRecStride];
     float2 st[NG][32];             // per-pixel (T, g.S) carried across chunks
+    uint8_t klist[32];             // union splats of the current group in visiting order
     float lg[2][4][32];            // (last, dL/dC) of the current / next group, planar; filled by
                                    // cp.async one group ahead (phase 2 broadcasts dL/dC from here)
     unsigned char rec[32 * kRec];
@@ -456,25 +457,27 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             // phase 1: per pixel, back to front, two union splats per iteration (k1 > k2): the
             // Gaussians / reciprocals are independent (ILP); only the T and g.S recursions are
             // serial. A lane whose pixel does not blend a splat computes on it and discards.
-            uint32_t rem = un;
+            // union splats in visiting order: row r <- splat k_r (lane j owns row popc(un >> j+1))
+            if ((un >> lane) & 1u) S.klist[__popc(un & (0xfffffffeu << lane))] = (uint8_t)lane;
+            __syncwarp();
             uint32_t rowp = 4u * (uint32_t)lane;  // byte offset of (row r, this pixel)
-            while (rem) {
-                const int k1 = 31 - __clz(rem);
-                rem &= ~(1u << k1);
-                const bool two = rem != 0u;
-                const int k2 = 31 - __clz(rem | 1u);
-                rem &= ~(1u << k2);
+            for (int r = 0; r < U; r += 2) {
+                const bool two = r + 1 < U;
+                const int k1 = S.klist[r];
+                const int k2 = two ? S.klist[r + 1] : k1;
                 const bool h1 = (col >> k1) & 1u;
                 const bool h2 = two && ((col >> k2) & 1u);
                 const uint32_t ad1 = rbase + k1 * kRec, ad2 = rbase + k2 * kRec;
                 const float4 a1 = lds_f4(ad1), a2 = lds_f4(ad2);
                 const float4 b1 = lds_f4(ad1 + 16), b2 = lds_f4(ad2 + 16);
                 const float cz1 = lds_f1(ad1 + 32), cz2 = lds_f1(ad2 + 32);
-                const float G1 = conic_gauss(a1.z, a1.w, b1.x, __fsub_rn(fxg, a1.x), __fsub_rn(fyg, a1.y));
-                const float G2 = conic_gauss(a2.z, a2.w, b2.x, __fsub_rn(fxg, a2.x), __fsub_rn(fyg, a2.y));
+                // a pixel that does not blend a splat sees G = 0: sigma = 0, inv_rest = 1, so
+                // T, g.S pass through unchanged and the records u, w are 0 (no selects needed)
+                const float G1 = h1 ? conic_gauss(a1.z, a1.w, b1.x, __fsub_rn(fxg, a1.x), __fsub_rn(fyg, a1.y)) : 0.f;
+                const float G2 = h2 ? conic_gauss(a2.z, a2.w, b2.x, __fsub_rn(fxg, a2.x), __fsub_rn(fyg, a2.y)) : 0.f;
                 const float s1 = __fmul_rn(b1.y, G1), s2 = __fmul_rn(b2.y, G2);
-                const float ir1 = fast_rcp(__fsub_rn(1.0f, s1));  // inv_rest
-                const float ir2 = fast_rcp(__fsub_rn(1.0f, s2));
+                const float ir1 = h1 ? fast_rcp(__fsub_rn(1.0f, s1)) : 1.0f;  // inv_rest
+                const float ir2 = h2 ? fast_rcp(__fsub_rn(1.0f, s2)) : 1.0f;
                 const float gc1 = gv.x * b1.z + gv.y * b1.w + gv.z * cz1;
                 const float gc2 = gv.x * b2.z + gv.y * b2.w + gv.z * cz2;
                 // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
@@ -482,20 +485,18 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
                 const float w1 = s1 * T1;
                 const float ds1 = T1 * gc1 - gS * ir1;
                 const float gS1 = __fmaf_rn(gc1, w1, gS);
-                const float Tb = h1 ? T1 : T, gSb = h1 ? gS1 : gS;
-                const float T2 = Tb * ir2;
+                const float T2 = T1 * ir2;
                 const float w2 = s2 * T2;
-                const float ds2 = T2 * gc2 - gSb * ir2;
-                const float gS2 = __fmaf_rn(gc2, w2, gSb);
-                T = h2 ? T2 : Tb;
-                gS = h2 ? gS2 : gSb;
-                sts_f1(ubase + rowp, h1 ? ds1 * G1 : 0.f);
-                sts_f1(wbase + rowp, h1 ? w1 : 0.f);
+                const float ds2 = T2 * gc2 - gS1 * ir2;
+                T = T2;
+                gS = __fmaf_rn(gc2, w2, gS1);
+                sts_f1(ubase + rowp, ds1 * G1);
+                sts_f1(wbase + rowp, w1);
                 if (two) {
-                    sts_f1(ubase + rowp + 4 * kRecStride, h2 ? ds2 * G2 : 0.f);
-                    sts_f1(wbase + rowp + 4 * kRecStride, h2 ? w2 : 0.f);
+                    sts_f1(ubase + rowp + 4 * kRecStride, ds2 * G2);
+                    sts_f1(wbase + rowp + 4 * kRecStride, w2);
                 }
-                visb |= ((h1 && w1 > kMinVisitW) ? (1u << k1) : 0u) | ((h2 && w2 > kMinVisitW) ? (1u << k2) : 0u);
+                visb |= (w1 > kMinVisitW ? (1u << k1) : 0u) | (w2 > kMinVisitW ? (1u << k2) : 0u);
                 rowp += 8 * kRecStride;
             }
             S.st[g][lane] = make_float2(T, gS);
