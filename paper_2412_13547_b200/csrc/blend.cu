@@ -316,7 +316,8 @@ struct BwdWarpSmem {
     float rec_u[32 * kRecStride];  // phase-1 records [union row][pixel]
     float rec_w[32 * kRecStride];
     float2 st[NG][32];             // per-pixel (T, g.S) carried across chunks
-    uint8_t klist[32];             // union splats of the current group in visiting order
+    uint8_t klist[48];             // union splats of the current group in visiting order (+pad,
+                                   // keeps the float4-read members below 16-byte aligned)
     float lg[2][4][32];            // (last, dL/dC) of the current / next group, planar; filled by
                                    // cp.async one group ahead (phase 2 broadcasts dL/dC from here)
     unsigned char rec[32 * kRec];
@@ -337,6 +338,9 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int NGX, int NGY>
 __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm) {
     constexpr int NG = NGX * NGY;
+    static_assert(sizeof(BwdWarpSmem<NG>) % 16 == 0 && offsetof(BwdWarpSmem<NG>, lg) % 16 == 0 &&
+                      offsetof(BwdWarpSmem<NG>, rec) % 16 == 0,
+                  "float4 shared-memory reads need 16-byte alignment");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto& S = reinterpret_cast<BwdWarpSmem<NG>*>(smem_raw)[warp];
@@ -461,10 +465,13 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             if ((un >> lane) & 1u) S.klist[__popc(un & (0xfffffffeu << lane))] = (uint8_t)lane;
             __syncwarp();
             uint32_t rowp = 4u * (uint32_t)lane;  // byte offset of (row r, this pixel)
+            int k1n = S.klist[0], k2n = S.klist[1];  // next pair, loaded one iteration ahead
             for (int r = 0; r < U; r += 2) {
                 const bool two = r + 1 < U;
-                const int k1 = S.klist[r];
-                const int k2 = two ? S.klist[r + 1] : k1;
+                const int k1 = k1n;
+                const int k2 = two ? k2n : k1;
+                k1n = S.klist[r + 2];
+                k2n = S.klist[r + 3];
                 const bool h1 = (col >> k1) & 1u;
                 const bool h2 = two && ((col >> k2) & 1u);
                 const uint32_t ad1 = rbase + k1 * kRec, ad2 = rbase + k2 * kRec;
