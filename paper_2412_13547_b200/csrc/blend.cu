@@ -305,6 +305,8 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
 }
 
 // ------------------------------------------------------------------------------ backward
+// partial slot of (splat, tile): the splat's first slot (d.z = exclusive scan of tiles touched,
+// in rank order) + the tile's row-major index inside the splat's tile rectangle
 __device__ __forceinline__ uint32_t pair_slot(const Prepared& P, int tx, int ty) {
     const uint4 d = P.d;
     const int tx0 = d.x & 0xffff, tx1 = d.x >> 16, ty0 = d.y & 0xffff;

@@ -48,7 +48,8 @@ struct ChainParams {
     int64_t cap, n;
     const uint32_t* rank_of;
     const uint32_t* perm;  // non-null: rows stored in blend order (perm[rank] = logical index)
-    const Prepared* prep;
+    const uint32_t* pair_off;  // per rank: first partial slot
+    const uint32_t* touched;   // per rank: tiles touched (= partial slots)
     Partials partial;
     float* screen;  // [10][cap] or null
     // stats
@@ -67,7 +68,9 @@ struct ChainParams {
     AdamCfg adam;
 };
 
-__global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
+// 6 blocks of 256 per SM (<= 40 registers): the slot loop and the moment / parameter streams
+// are latency-bound, so occupancy buys memory-level parallelism
+__global__ void __launch_bounds__(256, 6) chain_kernel(ChainParams cp) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cp.n) return;
     const int64_t cap = cp.cap;
@@ -84,15 +87,15 @@ __global__ void __launch_bounds__(256) chain_kernel(ChainParams cp) {
     // logical rows gather through rank_of. Outputs in logical order go to index `li`.
     const uint32_t r = cp.perm ? (uint32_t)i : __ldg(cp.rank_of + i);
     const int64_t li = cp.perm ? (int64_t)__ldg(cp.perm + i) : i;
-    const uint4 d = __ldg(&cp.prep[r].d);
+    const uint32_t base = __ldg(cp.pair_off + r), cnt = __ldg(cp.touched + r);
     float s[10];
 #pragma unroll
     for (int k = 0; k < 10; ++k) s[k] = 0.f;
     // merge in tile order (rasterizer.cpp:301-319): the pair slots of one splat are contiguous
-    const float4* __restrict__ pa = cp.partial.a + d.z;
-    const float4* __restrict__ pb = cp.partial.b + d.z;
-    const float2* __restrict__ pc = cp.partial.c + d.z;
-    for (uint32_t t = 0; t < d.w; ++t) {
+    const float4* __restrict__ pa = cp.partial.a + base;
+    const float4* __restrict__ pb = cp.partial.b + base;
+    const float2* __restrict__ pc = cp.partial.c + base;
+    for (uint32_t t = 0; t < cnt; ++t) {
         const float4 a = pa[t], b = pb[t];
         const float2 c = pc[t];
         s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
@@ -215,7 +218,8 @@ cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool upda
     cp.n = m->n;
     cp.rank_of = m->rank_of.as<uint32_t>();
     cp.perm = m->blend_phys ? m->perm.as<uint32_t>() : nullptr;
-    cp.prep = ctx->ws.prep.as<Prepared>();
+    cp.pair_off = ctx->ws.pair_off.as<uint32_t>();
+    cp.touched = ctx->ws.touched.as<uint32_t>();
     cp.partial = Partials::at(ctx->ws.partial.p, ctx->ws.pair_cap);
     // screen-space sums are kept only for the explicit backward (tgsx_stage_screen_grads)
     cp.screen = mode == ChainMode::kGrads ? m->screen.as<float>() : nullptr;

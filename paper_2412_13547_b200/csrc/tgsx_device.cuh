@@ -94,6 +94,7 @@ __device__ __forceinline__ uint32_t orderable_key(float f) {
 // 64 B per splat, blend (rank) order:
 //   a = (mean x, mean y, inv00, inv01)   b = (inv11, alpha, rx, ry)
 //   c = (r, g, b, orig as bits)          d = (rect x packed, rect y packed, pair offset, tiles)
+// (pair offset = the splat's first partial slot = pair_off[rank], written by the binning)
 // rect packed = lo | hi << 16 (tile units); tiles == 0 => not binned.
 struct __align__(16) Prepared {
     float4 a, b, c;
