@@ -617,7 +617,7 @@ void tgsx_destroy(tgsx_ctx* ctx) {
     DevBuf* bufs[] = {&ws.prep, &ws.touched, &ws.pair_off, &ws.scan_tmp, &ws.keys[0], &ws.keys[1],
                       &ws.vals[0], &ws.vals[1], &ws.sort_tmp, &ws.ranges, &ws.partial, &ws.rgb,
                       &ws.T, &ws.last, &ws.dLdC, &ws.target, &ws.block_loss, &ws.counters,
-                      &ws.generic, &ws.tile_count, &ws.tile_off, &ws.tile_fill};
+                      &ws.generic, &ws.tile_count, &ws.tile_off, &ws.tile_fill, &ws.tile_dense};
     for (DevBuf* b : bufs) b->release();
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);

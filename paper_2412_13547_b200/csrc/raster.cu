@@ -17,7 +17,8 @@ namespace tgsx {
 
 namespace {
 
-
+// per-tile counters one per 128-B line: neighbouring tiles' atomics do not serialise on one L2 line
+constexpr int kFillStride = 32;
 
 // ------------------------------------------------------------------ preprocess
 __global__ void __launch_bounds__(256) preprocess_kernel(
@@ -72,7 +73,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                          0u, tiles);
         if (tile_count)  // per-tile list lengths for the scatter binning (fire-and-forget RED)
             for (int ty = ty0; ty <= ty1; ++ty)
-                for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&tile_count[ty * tiles_x + tx], 1u);
+                for (int tx = tx0; tx <= tx1; ++tx)
+                    atomicAdd(&tile_count[(size_t)(ty * tiles_x + tx) * kFillStride], 1u);
     } else {
         o.d = make_uint4(0u, 0u, 0u, 0u);
     }
@@ -127,6 +129,12 @@ __global__ void ranges_kernel(const uint32_t* __restrict__ keys, int64_t K, uint
 // [off[t], off[t] + cnt[t]) == TileGrid::offsets (rasterizer.cpp:92-100). fill[t] starts at
 // off[t]; the scatter claims slots with atomics (arbitrary order inside a tile) and the
 // per-tile sort restores blend (rank) order, so the result is deterministic.
+__global__ void tile_counts_kernel(const uint32_t* __restrict__ padded, int tiles,
+                                   uint32_t* __restrict__ dense) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < tiles) dense[t] = padded[(size_t)t * kFillStride];
+}
+
 __global__ void tile_finalize_kernel(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
                                      int tiles, uint2* __restrict__ ranges, uint32_t* __restrict__ fill,
                                      unsigned long long* __restrict__ max_cnt) {
@@ -136,7 +144,7 @@ __global__ void tile_finalize_kernel(const uint32_t* __restrict__ cnt, const uin
         c = cnt[t];
         const uint32_t o = off[t];
         ranges[t] = make_uint2(o, o + c);
-        fill[t] = o;
+        fill[(size_t)t * kFillStride] = o;
     }
     c = __reduce_max_sync(0xffffffffu, c);
     if ((threadIdx.x & 31) == 0 && c) atomicMax(max_cnt, (unsigned long long)c);
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(256) scatter_kernel(
         for (int u = 0; u < 4; ++u)
             if (i + u < cnt) {
                 const int q = i + u, ty = ty0 + q / w, tx = tx0 + q % w;
-                pos[u] = atomicAdd(&fill[ty * tiles_x + tx], 1u);
+                pos[u] = atomicAdd(&fill[(size_t)(ty * tiles_x + tx) * kFillStride], 1u);
             }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -237,13 +245,17 @@ cudaError_t launch_tile_finalize(tgsx_ctx* ctx, int tiles) {
     Workspace& ws = ctx->ws;
     cudaError_t e;
     if ((e = ws.ranges.ensure((size_t)std::max(tiles, 1) * sizeof(uint2)))) return e;
-    if ((e = ws.tile_fill.ensure((size_t)std::max(tiles, 1) * 4))) return e;
+    if ((e = ws.tile_fill.ensure((size_t)std::max(tiles, 1) * 4 * kFillStride))) return e;
     unsigned long long* counters = ws.counters.as<unsigned long long>();
-    if ((e = launch_exclusive_scan(ctx, ws.tile_count.as<uint32_t>(), ws.tile_off.as<uint32_t>(), tiles,
+    if ((e = ws.tile_dense.ensure((size_t)std::max(tiles, 1) * 4))) return e;
+    tile_counts_kernel<<<grid_for(tiles, 256), 256, 0, ctx->stream>>>(ws.tile_count.as<uint32_t>(), tiles,
+                                                                      ws.tile_dense.as<uint32_t>());
+    ctx->launches++;
+    if ((e = launch_exclusive_scan(ctx, ws.tile_dense.as<uint32_t>(), ws.tile_off.as<uint32_t>(), tiles,
                                    nullptr)))
         return e;
     tile_finalize_kernel<<<grid_for(tiles, 256), 256, 0, ctx->stream>>>(
-        ws.tile_count.as<uint32_t>(), ws.tile_off.as<uint32_t>(), tiles, ws.ranges.as<uint2>(),
+        ws.tile_dense.as<uint32_t>(), ws.tile_off.as<uint32_t>(), tiles, ws.ranges.as<uint2>(),
         ws.tile_fill.as<uint32_t>(), counters + 5);
     ctx->launches++;
     return cudaGetLastError();
@@ -282,9 +294,9 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
     ws.tiles_x = (W + kTile - 1) / kTile;
     ws.tiles_y = (H + kTile - 1) / kTile;
     const size_t tb = (size_t)std::max(ws.tiles_x * ws.tiles_y, 1) * 4;
-    if ((e = ws.tile_count.ensure(tb))) return e;
+    if ((e = ws.tile_count.ensure(tb * kFillStride))) return e;
     if ((e = ws.tile_off.ensure(tb))) return e;
-    if ((e = cudaMemsetAsync(ws.tile_count.p, 0, tb, ctx->stream))) return e;
+    if ((e = cudaMemsetAsync(ws.tile_count.p, 0, tb * kFillStride, ctx->stream))) return e;
     if (n == 0) return cudaSuccess;
     preprocess_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
         m->params.as<float>(), m->cap, n, m->rank_of.as<uint32_t>(), m->perm.as<uint32_t>(),

@@ -40,7 +40,9 @@ struct Workspace {
     DevBuf keys[2], vals[2];  // u32[K] ping-pong
     DevBuf sort_tmp;          // histograms + block status + tickets
     DevBuf ranges;            // uint2[tiles]
-    DevBuf tile_count, tile_off, tile_fill;  // u32[tiles] scatter binning (lengths, offsets, cursors)
+    // scatter binning: per-tile lengths and slot cursors (one per 128-B line), dense lengths,
+    // offsets
+    DevBuf tile_count, tile_fill, tile_dense, tile_off;
     DevBuf partial;           // per-(tile, splat) gradient partials, Partials SoA (40 B/pair)
     int64_t pair_cap = 0;     // pairs the partial buffer holds
     // per-pixel
