@@ -1,27 +1,26 @@
 // Alpha-blend forward and backward over the per-tile splat lists (sm_100a, FP32 pipe).
 //
 // The tile's active pixels (the dilated variant keeps only x%p==ox, y%p==oy, so p selects the
-// geometry and the same kernels serve p = 1 and the paper's 4K dilated rendering) form groups
-// of 8x4 active pixels, one pixel per lane. The tile's splat list is consumed in chunks of 32
-// staged as 48-byte shared-memory records together with exact per-tile box-test masks
-// (rasterizer.cpp:116-118, evaluated once per (tile, splat) in float, per active column / row).
-// For a group the warp builds the 32x32 (splat x pixel) pass matrix — lane j turns splat j's
-// masks into a 32-bit row with one multiply, a 5-stage shuffle bit-transpose hands lane l the
-// column "which of these 32 splats pass my pixel" — and each lane walks only its own passing
-// splats with ffs (forward, front to back) or clz (backward, back to front). Per pixel the
-// order is the list order and box-failing splats contribute nothing, exactly as in walk_pixel
-// (rasterizer.cpp:108-136).
+// geometry and the same kernels serve p = 1 and the paper's 4K dilated rendering) are covered
+// by warps. The tile's splat list is consumed in chunks of 32 staged as 48-byte shared-memory
+// records together with exact per-tile box-test masks (rasterizer.cpp:116-118, evaluated once
+// per (tile, splat) in float, per active column / row). Per chunk the warp builds the 32x32
+// (splat x pixel) pass matrix — lane j turns splat j's masks into a 32-bit row with one
+// multiply, a 5-stage shuffle bit-transpose hands lane l the column "which of these 32 splats
+// pass my pixel". Per pixel the order is the list order and box-failing splats contribute
+// nothing, exactly as in walk_pixel (rasterizer.cpp:108-136).
 //
-// forward_kernel (one CTA per tile, one warp per group): walk_pixel + render
-//   (rasterizer.cpp:144-184), optional fused L1 epilogue. Records per pixel
-//   the final T and the last blended list position.
+// forward_pairs_kernel (one CTA per tile, one warp per 8x8 block, two pixels per lane as packed
+//   FP32x2): walk_pixel + render (rasterizer.cpp:144-184), optional fused L1 epilogue
+//   (SPEC.md:562-570). Records per pixel the final T and the last blended list position.
 // backward_kernel (ONE WARP PER TILE, independent warps, no block barriers): backward tile
-//   phase (rasterizer.cpp:234-292), per chunk and group:
-//   1. per pixel, back to front: T_i = T_{i+1} / (1 - sigma_i) with sigma recomputed
-//      bit-identically to the forward; g.dC/dsigma_i = T_i (g.c_i) - (g.S_i)/(1 - sigma_i) with
-//      the reference's exact suffix S_i (rasterizer.cpp:266-287) carried as the scalar g.S;
-//      records u = dL/dsigma * G and the blend weight w per (splat, pixel) in shared memory;
-//   2. per splat (lane j), dense over the group's 32 pixels: every position / covariance
+//   phase (rasterizer.cpp:234-292), per chunk and 8x4 pixel group:
+//   1. per pixel, back to front over the union of the group's walked splats (all lanes on the
+//      same splat): T_i = T_{i+1} / (1 - sigma_i) with sigma recomputed bit-identically to the
+//      forward; g.dC/dsigma_i = T_i (g.c_i) - (g.S_i)/(1 - sigma_i) with the reference's exact
+//      suffix S_i (rasterizer.cpp:266-287) carried as the scalar g.S; records u = dL/dsigma * G
+//      and the blend weight w per (splat, pixel) in a dense shared-memory row per splat;
+//   2. per splat (lane = row), dense over the group's 32 pixels: every position / covariance
 //      gradient of rasterizer.cpp:276-285 is linear in the moments sum(u), sum(u dx), sum(u dy),
 //      sum(u dx^2), sum(u dx dy), sum(u dy^2) and the colour gradient is sum(g w); with fixed
 //      pixel offsets these are FFMA-with-immediate sums, accumulated across the tile's groups in
@@ -126,51 +125,20 @@ __device__ __forceinline__ uint32_t stage_splat(const Prepared& P, const TileGeo
     return mask;
 }
 
-// Tile geometry + this lane's pixel, in active coordinates.
-template <int NWX>
-struct PixelMap {
-    int tx, ty, ax, ay, acols, arows, bx, by, x, y, rank;
-    float fx, fy;
-    bool valid;
-    __device__ __forceinline__ void init(const BlendParams& prm, int tile) {
-        tx = tile % prm.tiles_x;
-        ty = tile / prm.tiles_x;
-        const int x0 = tx * kTile, y0 = ty * kTile;
-        const int px1 = min(prm.W, x0 + kTile), py1 = min(prm.H, y0 + kTile);
-        ax = first_active(x0, prm.ox, prm.p);
-        ay = first_active(y0, prm.oy, prm.p);
-        acols = ax < px1 ? (px1 - ax + prm.p - 1) / prm.p : 0;
-        arows = ay < py1 ? (py1 - ay + prm.p - 1) / prm.p : 0;
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        bx = warp % NWX;
-        by = warp / NWX;
-        const int lx = bx * 8 + (lane & 7);
-        const int ly = by * 4 + (lane >> 3);
-        valid = lx < acols && ly < arows;
-        x = ax + lx * prm.p;
-        y = ay + ly * prm.p;
-        fx = (float)x + 0.5f;
-        fy = (float)y + 0.5f;
-        rank = valid ? ((y - prm.oy) / prm.p) * prm.cols + (x - prm.ox) / prm.p : 0;
-    }
-};
-
-template <int NWX>
-__device__ __forceinline__ void stage_splat_cta(const BlendParams& prm, uint32_t rank,
-                                            const PixelMap<NWX>& g, uint32_t dst) {
-    const Prepared& P = prm.prep[rank];
-    const float4 a = P.a, b = P.b, c = P.c;
-    const uint32_t mask = box_mask(a.x, b.z, g.ax, prm.p, g.acols) |
-                          (box_mask(a.y, b.w, g.ay, prm.p, g.arows) << 16);
-    sts_f4(dst, make_float4(a.x, a.y, __fmul_rn(a.z, kNegHalfLog2e),
-                            __fmul_rn(a.w * 2.0f, kNegHalfLog2e)));
-    sts_f4(dst + 16, make_float4(__fmul_rn(b.x, kNegHalfLog2e), b.y, c.x, c.y));
-    sts_f4(dst + 32, make_float4(c.z, __uint_as_float(mask), 0.f, 0.f));
+// ------------------------------------------------------------------------ forward (pairs)
+// Row bits 0,2,4,6 of an 8-bit row mask spread to bytes 0..3 (one byte per lane row-pair).
+__device__ __forceinline__ uint32_t spread_even4(uint32_t yb) {
+    return (yb & 1u) | ((yb & 4u) << 6) | ((yb & 16u) << 12) | ((yb & 64u) << 18);
 }
 
-// ------------------------------------------------------------------------------- forward
+// One CTA per tile, one warp per 8x8 block of active pixels, TWO vertically adjacent pixels per
+// lane (rows 2r and 2r+1 of the block). The lane walks the union of its two pixels' passing
+// splats front to back; the two Gaussians / blends of a splat run as packed FP32x2 (FMUL2 /
+// FFMA2 with the splat's scalars broadcast), so one record read and one instruction stream
+// serve two pixels. Every per-pixel quantity rounds exactly like walk_pixel
+// (rasterizer.cpp:108-136) and like conic_gauss (the backward recomputes sigma from it).
 template <int NWX, int NWY, int BATCH>
-__global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm) {
+__global__ void __launch_bounds__(NWX * NWY * 32) forward_pairs_kernel(BlendParams prm) {
     constexpr int NW = NWX * NWY, NT = NW * 32;
     __shared__ __align__(16) unsigned char s_rec[BATCH * kRec];
     __shared__ unsigned long long s_red[2][NW];
@@ -178,75 +146,109 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
 
     const int tile = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    PixelMap<NWX> pm;
-    pm.init(prm, tile);
+    TileGeo geo;
+    geo.init(prm, tile);
+    const int p = prm.p;
+    const int bx = warp % NWX, by = warp / NWX;
+    const int lx = bx * 8 + (lane & 7), lyA = by * 8 + 2 * (lane >> 3);
+    const bool vA = lx < geo.acols && lyA < geo.arows;
+    const bool vB = lx < geo.acols && lyA + 1 < geo.arows;
+    const int x = geo.ax + lx * p, yA = geo.ay + lyA * p, yB = yA + p;
+    const float fx = (float)x + 0.5f, fyA = (float)yA + 0.5f, fyB = (float)yB + 0.5f;
     const uint2 range = prm.ranges[tile];
     const int count = (int)(range.y - range.x);
     const uint32_t sbase = smem_addr(s_rec);
 
-    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-    uint32_t last = 0, ops = 0;
-    bool done = !pm.valid;
-    bool warp_done = __all_sync(kFull, done);
+    float2 T = make_float2(1.0f, 1.0f);
+    float2 C0 = make_float2(0.f, 0.f), C1 = C0, C2 = C0;
+    uint32_t lastA = 0, lastB = 0, ops = 0;
+    bool doneA = !vA, doneB = !vB;
+    bool warp_done = __all_sync(kFull, doneA && doneB);
 
     for (int bstart = 0; bstart < count; bstart += BATCH) {
         if (__syncthreads_and(warp_done)) break;
         const int bcount = min(BATCH, count - bstart);
-        for (int j = threadIdx.x; j < bcount; j += NT)
-            stage_splat_cta(prm, prm.items[range.x + bstart + j], pm, sbase + j * kRec);
+        for (int j = threadIdx.x; j < bcount; j += NT) {
+            const Prepared& P = prm.prep[prm.items[range.x + bstart + j]];
+            const float4 a = P.a, b = P.b, c = P.c;
+            const uint32_t mask = box_mask(a.x, b.z, geo.ax, p, geo.acols) |
+                                  (box_mask(a.y, b.w, geo.ay, p, geo.arows) << 16);
+            const uint32_t dst = sbase + j * kRec;
+            sts_f4(dst, make_float4(a.x, a.y, __fmul_rn(a.z, kNegHalfLog2e),
+                                    __fmul_rn(a.w * 2.0f, kNegHalfLog2e)));
+            sts_f4(dst + 16, make_float4(__fmul_rn(b.x, kNegHalfLog2e), b.y, c.x, c.y));
+            sts_f4(dst + 32, make_float4(c.z, __uint_as_float(mask), 0.f, 0.f));
+        }
         __syncthreads();
         if (warp_done) continue;
         for (int c0 = 0; c0 < bcount; c0 += 32) {
             const int j = c0 + lane;
-            const uint32_t row =
-                j < bcount ? group_rowmask(__float_as_uint(lds_f1(sbase + j * kRec + 36)), pm.bx, pm.by) : 0u;
-            uint32_t col = transpose32(row);
-            if (done) col = 0;
+            uint32_t rowA = 0, rowB = 0;
+            if (j < bcount) {
+                const uint32_t m = __float_as_uint(lds_f1(sbase + j * kRec + 36));
+                const uint32_t xb = (m >> (bx * 8)) & 0xffu, yb = (m >> (16 + by * 8)) & 0xffu;
+                rowA = xb * spread_even4(yb);
+                rowB = xb * spread_even4(yb >> 1);
+            }
+            uint32_t colA = transpose32(rowA), colB = transpose32(rowB);
+            if (doneA) colA = 0;
+            if (doneB) colB = 0;
+            const uint32_t colA0 = colA, colB0 = colB;
             const uint32_t cbase = sbase + c0 * kRec;
             const uint32_t lbase = (uint32_t)(bstart + c0 + 1);
-            // two passing splats per iteration: their Gaussians are independent (ILP), only the
-            // T / colour update is serial; the second is masked (select, no branch) when absent
-            // or when the first terminates the ray. Blend count and last contributor are derived
-            // once per chunk from the pass mask; only the (once per pixel) termination branches.
-            const uint32_t col0 = col;
-            int term_k = 32;  // bit of the terminating blend in this chunk, 32 = none
-            while (__any_sync(kFull, col)) {
-                if (col) {
-                    const int k1 = __ffs(col) - 1;
-                    col &= col - 1;
-                    const bool h2 = col != 0u;
-                    const int k2 = h2 ? __ffs(col) - 1 : k1;
-                    col &= col - 1;
-                    const uint32_t ad1 = cbase + k1 * kRec, ad2 = cbase + k2 * kRec;
-                    const float4 a1 = lds_f4(ad1), a2 = lds_f4(ad2);
-                    const float4 b1 = lds_f4(ad1 + 16), b2 = lds_f4(ad2 + 16);
-                    const float cz1 = lds_f1(ad1 + 32), cz2 = lds_f1(ad2 + 32);
-                    const float G1 = conic_gauss(a1.z, a1.w, b1.x, __fsub_rn(pm.fx, a1.x), __fsub_rn(pm.fy, a1.y));
-                    const float G2 = conic_gauss(a2.z, a2.w, b2.x, __fsub_rn(pm.fx, a2.x), __fsub_rn(pm.fy, a2.y));
-                    const float s1 = __fmul_rn(b1.y, G1), s2 = __fmul_rn(b2.y, G2);
-                    const float w1 = __fmul_rn(s1, T);
-                    const float T1 = __fmul_rn(T, __fsub_rn(1.0f, s1));
-                    const bool t1 = T1 < kTermT;
-                    const bool p2 = h2 && !t1;
-                    const float w2 = p2 ? __fmul_rn(s2, T1) : 0.f;
-                    const float T2 = p2 ? __fmul_rn(T1, __fsub_rn(1.0f, s2)) : T1;
-                    C0 = __fmaf_rn(w2, b2.z, __fmaf_rn(w1, b1.z, C0));
-                    C1 = __fmaf_rn(w2, b2.w, __fmaf_rn(w1, b1.w, C1));
-                    C2 = __fmaf_rn(w2, cz2, __fmaf_rn(w1, cz1, C2));
-                    T = T2;
-                    if (T2 < kTermT) {  // this pixel's ray terminates (break after blending)
-                        term_k = t1 ? k1 : k2;
-                        col = 0;
+            int termA = 32, termB = 32;  // bit of each pixel's terminating blend, 32 = none
+            uint32_t colU = colA | colB;
+            while (__any_sync(kFull, colU)) {
+                if (colU) {
+                    const int k = __ffs(colU) - 1;
+                    const uint32_t bit = 1u << k;
+                    const bool hA = (colA & bit) != 0u, hB = (colB & bit) != 0u;
+                    colA &= ~bit;
+                    colB &= ~bit;
+                    const uint32_t ad = cbase + k * kRec;
+                    const float4 a = lds_f4(ad), b = lds_f4(ad + 16);
+                    const float cz = lds_f1(ad + 32);
+                    // conic_gauss for both pixels, same op sequence
+                    const float dx = __fsub_rn(fx, a.x);
+                    const float2 dy = make_float2(__fsub_rn(fyA, a.y), __fsub_rn(fyB, a.y));
+                    const float2 t = __fmul2_rn(make_float2(b.x, b.x), dy);
+                    const float2 u = __ffma2_rn(make_float2(a.w, a.w), make_float2(dx, dx), t);
+                    const float2 v = __fmul2_rn(u, dy);
+                    const float kadx = __fmul_rn(a.z, dx);
+                    const float2 q = __ffma2_rn(make_float2(kadx, kadx), make_float2(dx, dx), v);
+                    // a pixel that does not pass the splat gets sigma = 0 (T, colour unchanged)
+                    const float2 s = make_float2(hA ? __fmul_rn(b.y, fast_exp2(q.x)) : 0.f,
+                                                 hB ? __fmul_rn(b.y, fast_exp2(q.y)) : 0.f);
+                    const float2 w = __fmul2_rn(s, T);
+                    // 1 - sigma with one rounding, exactly as the scalar subtraction
+                    T = __fmul2_rn(T, __ffma2_rn(s, make_float2(-1.0f, -1.0f), make_float2(1.0f, 1.0f)));
+                    C0 = __ffma2_rn(w, make_float2(b.z, b.z), C0);
+                    C1 = __ffma2_rn(w, make_float2(b.w, b.w), C1);
+                    C2 = __ffma2_rn(w, make_float2(cz, cz), C2);
+                    if (hA && T.x < kTermT) {  // ray A terminates (break after blending)
+                        termA = k;
+                        colA = 0;
                     }
+                    if (hB && T.y < kTermT) {
+                        termB = k;
+                        colB = 0;
+                    }
+                    colU = colA | colB;
                 }
             }
-            if (col0) {
-                const uint32_t used = term_k < 32 ? (col0 & (kFull >> (31 - term_k))) : col0;
+            if (colA0) {
+                const uint32_t used = termA < 32 ? (colA0 & (kFull >> (31 - termA))) : colA0;
                 ops += __popc(used);
-                last = lbase + 31 - __clz(used);
-                if (term_k < 32) done = true;
+                lastA = lbase + 31 - __clz(used);
+                if (termA < 32) doneA = true;
             }
-            if (__all_sync(kFull, done)) {
+            if (colB0) {
+                const uint32_t used = termB < 32 ? (colB0 & (kFull >> (31 - termB))) : colB0;
+                ops += __popc(used);
+                lastB = lbase + 31 - __clz(used);
+                if (termB < 32) doneB = true;
+            }
+            if (__all_sync(kFull, doneA && doneB)) {
                 warp_done = true;
                 break;
             }
@@ -254,35 +256,39 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_kernel(BlendParams prm
     }
 
     float lsum = 0.f;
-    if (pm.valid) {
-        C0 = __fmaf_rn(T, prm.bg0, C0);
-        C1 = __fmaf_rn(T, prm.bg1, C1);
-        C2 = __fmaf_rn(T, prm.bg2, C2);
-        const int r = pm.rank;
+    unsigned long long ev = 0;
+    auto finish = [&](bool valid, int y, float Tp, float c0, float c1, float c2, uint32_t last, bool done) {
+        if (!valid) return;
+        c0 = __fmaf_rn(Tp, prm.bg0, c0);
+        c1 = __fmaf_rn(Tp, prm.bg1, c1);
+        c2 = __fmaf_rn(Tp, prm.bg2, c2);
+        const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
         if (prm.rgb) {
-            prm.rgb[3 * r] = C0;
-            prm.rgb[3 * r + 1] = C1;
-            prm.rgb[3 * r + 2] = C2;
+            prm.rgb[3 * r] = c0;
+            prm.rgb[3 * r + 1] = c1;
+            prm.rgb[3 * r + 2] = c2;
         }
-        prm.T[r] = T;
+        prm.T[r] = Tp;
         prm.last[r] = last;
+        ev += done ? last : (uint32_t)count;
         if (prm.target) {
-            const float* t = prm.target + 3 * ((int64_t)pm.y * prm.W + pm.x);
-            const float d0 = C0 - t[0], d1 = C1 - t[1], d2 = C2 - t[2];
-            lsum = fabsf(d0) + fabsf(d1) + fabsf(d2);
-            const float s = prm.loss_scale;
-            prm.dLdC[3 * r] = d0 > 0.f ? s : (d0 < 0.f ? -s : 0.f);
-            prm.dLdC[3 * r + 1] = d1 > 0.f ? s : (d1 < 0.f ? -s : 0.f);
-            prm.dLdC[3 * r + 2] = d2 > 0.f ? s : (d2 < 0.f ? -s : 0.f);
+            const float* tg = prm.target + 3 * ((int64_t)y * prm.W + x);
+            const float d0 = c0 - tg[0], d1 = c1 - tg[1], d2 = c2 - tg[2];
+            lsum += fabsf(d0) + fabsf(d1) + fabsf(d2);
+            const float sc = prm.loss_scale;
+            prm.dLdC[3 * r] = d0 > 0.f ? sc : (d0 < 0.f ? -sc : 0.f);
+            prm.dLdC[3 * r + 1] = d1 > 0.f ? sc : (d1 < 0.f ? -sc : 0.f);
+            prm.dLdC[3 * r + 2] = d2 > 0.f ? sc : (d2 < 0.f ? -sc : 0.f);
         }
-    }
+    };
+    finish(vA, yA, T.x, C0.x, C1.x, C2.x, lastA, doneA);
+    finish(vB, yB, T.y, C0.y, C1.y, C2.y, lastB, doneB);
     unsigned long long o = ops;
-    unsigned long long ev = pm.valid ? (done ? last : (uint32_t)count) : 0u;
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-        o += __shfl_xor_sync(kFull, o, s);
-        ev += __shfl_xor_sync(kFull, ev, s);
-        lsum += __shfl_xor_sync(kFull, lsum, s);
+    for (int sft = 16; sft > 0; sft >>= 1) {
+        o += __shfl_xor_sync(kFull, o, sft);
+        ev += __shfl_xor_sync(kFull, ev, sft);
+        lsum += __shfl_xor_sync(kFull, lsum, sft);
     }
     if (lane == 0) {
         s_red[0][warp] = o;
@@ -674,11 +680,9 @@ cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* 
     }
     const unsigned tiles = (unsigned)prm.tiles;
     if (ra.p == 1) {
-        forward_kernel<2, 4, 256><<<tiles, 256, 0, ctx->stream>>>(prm);
-    } else if (ra.p <= 3) {
-        forward_kernel<1, 2, 128><<<tiles, 64, 0, ctx->stream>>>(prm);
+        forward_pairs_kernel<2, 2, 256><<<tiles, 128, 0, ctx->stream>>>(prm);
     } else {
-        forward_kernel<1, 1, 128><<<tiles, 32, 0, ctx->stream>>>(prm);
+        forward_pairs_kernel<1, 1, 128><<<tiles, 32, 0, ctx->stream>>>(prm);
     }
     ctx->launches++;
     return cudaGetLastError();
