@@ -533,8 +533,11 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
                 float2 c0p = make_float2(0.f, 0.f), c1p = c0p, c2p = c0p;
 #pragma unroll
                 for (int row = 0; row < 4; ++row) {
-                    float2 Rp = make_float2(0.f, 0.f);
-                    float Rx = 0.f, Rxx = 0.f;
+                    // column pairs (2k, 2k+1): xi_{2k+1} = xi_{2k} + 1, so with the pair sums
+                    // P = sum u, X = sum xi_{2k} u, Q = sum xi_{2k}^2 u (one FADD2 / FFMA2 each,
+                    // scalar weights broadcast): R = P.x+P.y, Rx = X.x+X.y+P.y,
+                    // Rxx = Q.x+Q.y+2 X.y+P.y
+                    float2 Rp = make_float2(0.f, 0.f), Xp = Rp, Qp = Rp;
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
                         const int l4 = 2 * row + half;
@@ -543,15 +546,14 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
                         const float4 g0 = lds_f4(gb + 16 * l4);  // broadcasts
                         const float4 g1 = lds_f4(gb + 128 + 16 * l4);
                         const float4 g2 = lds_f4(gb + 256 + 16 * l4);
-                        const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float xi = (float)(4 * half + e) - 3.5f;
-                            Rx = __fmaf_rn(uu[e], xi, Rx);
-                            Rxx = __fmaf_rn(uu[e], xi * xi, Rxx);
-                        }
-                        Rp = __fadd2_rn(Rp, make_float2(u4.x, u4.y));
-                        Rp = __fadd2_rn(Rp, make_float2(u4.z, u4.w));
+                        const float xa = (float)(4 * half) - 3.5f, xb = xa + 2.0f;  // xi of cols 4h, 4h+2
+                        const float2 ua = make_float2(u4.x, u4.y), ub = make_float2(u4.z, u4.w);
+                        Rp = __fadd2_rn(Rp, ua);
+                        Rp = __fadd2_rn(Rp, ub);
+                        Xp = __ffma2_rn(ua, make_float2(xa, xa), Xp);
+                        Xp = __ffma2_rn(ub, make_float2(xb, xb), Xp);
+                        Qp = __ffma2_rn(ua, make_float2(xa * xa, xa * xa), Qp);
+                        Qp = __ffma2_rn(ub, make_float2(xb * xb, xb * xb), Qp);
                         c0p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g0.x, g0.y), c0p);
                         c0p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g0.z, g0.w), c0p);
                         c1p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g1.x, g1.y), c1p);
@@ -560,6 +562,8 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
                         c2p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g2.z, g2.w), c2p);
                     }
                     const float R = Rp.x + Rp.y;
+                    const float Rx = Xp.x + Xp.y + Rp.y;
+                    const float Rxx = Qp.x + Qp.y + 2.0f * Xp.y + Rp.y;
                     const float eta = (float)row - 1.5f;
                     a0 += R;
                     ax1 += Rx;
