@@ -342,6 +342,60 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// Phase-2 sums of one record row over NPR pixel rows of an 8x4 group, starting at pixel row
+// eta0 + 1.5 (u, w at ur / wr, dL/dC planar at gb; all pre-offset to that pixel row):
+// acc += (sum u, sum u xi, sum u eta, sum u xi^2, sum u xi eta, sum u eta^2, sum w g0..g2),
+// xi / eta the pixel offsets from the group centre. Separable: per pixel row accumulate
+// R = sum u, Rx = sum u xi, Rxx = sum u xi^2 over its 8 columns, then fold the row in with eta.
+// Column pairs (2k, 2k+1) sit in register pairs: with xi_{2k+1} = xi_{2k} + 1 and the pair sums
+// P = sum u, X = sum xi_{2k} u, Q = sum xi_{2k}^2 u (FADD2 / FFMA2, scalar weights broadcast),
+// R = P.x+P.y, Rx = X.x+X.y+P.y, Rxx = Q.x+Q.y+2 X.y+P.y; the colour sums are FFMA2 as well.
+template <int NPR>
+__device__ __forceinline__ void row_sums(uint32_t ur, uint32_t wr, uint32_t gb, float prow0,
+                                         float (&acc)[9]) {
+    float2 c0p = make_float2(0.f, 0.f), c1p = c0p, c2p = c0p;
+#pragma unroll
+    for (int row = 0; row < NPR; ++row) {
+        float2 Rp = make_float2(0.f, 0.f), Xp = Rp, Qp = Rp;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const int l4 = 2 * row + half;
+            const float4 u4 = lds_f4(ur + 16 * l4);
+            const float4 w4 = lds_f4(wr + 16 * l4);
+            const float4 g0 = lds_f4(gb + 16 * l4);  // broadcasts
+            const float4 g1 = lds_f4(gb + 128 + 16 * l4);
+            const float4 g2 = lds_f4(gb + 256 + 16 * l4);
+            const float xa = (float)(4 * half) - 3.5f, xb = xa + 2.0f;  // xi of cols 4h, 4h+2
+            const float2 ua = make_float2(u4.x, u4.y), ub = make_float2(u4.z, u4.w);
+            Rp = __fadd2_rn(Rp, ua);
+            Rp = __fadd2_rn(Rp, ub);
+            Xp = __ffma2_rn(ua, make_float2(xa, xa), Xp);
+            Xp = __ffma2_rn(ub, make_float2(xb, xb), Xp);
+            Qp = __ffma2_rn(ua, make_float2(xa * xa, xa * xa), Qp);
+            Qp = __ffma2_rn(ub, make_float2(xb * xb, xb * xb), Qp);
+            c0p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g0.x, g0.y), c0p);
+            c0p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g0.z, g0.w), c0p);
+            c1p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g1.x, g1.y), c1p);
+            c1p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g1.z, g1.w), c1p);
+            c2p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g2.x, g2.y), c2p);
+            c2p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g2.z, g2.w), c2p);
+        }
+        const float R = Rp.x + Rp.y;
+        const float Rx = Xp.x + Xp.y + Rp.y;
+        const float Rxx = Qp.x + Qp.y + 2.0f * Xp.y + Rp.y;
+        const float eta = prow0 + (float)row - 1.5f;
+        acc[0] += R;
+        acc[1] += Rx;
+        acc[2] = __fmaf_rn(R, eta, acc[2]);
+        acc[3] += Rxx;
+        acc[4] = __fmaf_rn(Rx, eta, acc[4]);
+        acc[5] = __fmaf_rn(R, eta * eta, acc[5]);
+    }
+    acc[6] += c0p.x + c0p.y;
+    acc[7] += c1p.x + c1p.y;
+    acc[8] += c2p.x + c2p.y;
+}
+
 
 template <int NGX, int NGY>
 __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm) {
@@ -517,76 +571,30 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
             S.st[g][lane] = make_float2(T, gS);
             vism |= __reduce_or_sync(kFull, visb);
             __syncwarp();
-            // phase 2: lane i < U = row i (the i-th highest union splat), dense over the group's
-            // 32 pixels; moments about the group centre (compile-time offsets)
-            float a0 = 0.f, ax1 = 0.f, ay1 = 0.f, axx = 0.f, axy = 0.f, ayy = 0.f;
-            float c0s = 0.f, c1s = 0.f, c2s = 0.f;
-            if (lane < U) {
-                const uint32_t ur = ubase + 4u * (uint32_t)(lane * kRecStride);
-                const uint32_t wr = wbase + 4u * (uint32_t)(lane * kRecStride);
-                const uint32_t gb = lgbase + 512u * (uint32_t)cur + 128u;  // lg[cur][1..3]
-                // separable moments: per pixel row (eta fixed) accumulate R = sum u,
-                // Rx = sum u xi, Rxx = sum u xi^2 over the row's 8 columns, then fold the row in
-                // with eta (3 FFMA per pixel + 6 per row instead of 6 per pixel). Pixel pairs
-                // (2c, 2c+1) sit in register pairs, so R and the colour sums use the packed
-                // FADD2 / FFMA2 (two lanes of FP32 per instruction).
-                float2 c0p = make_float2(0.f, 0.f), c1p = c0p, c2p = c0p;
-#pragma unroll
-                for (int row = 0; row < 4; ++row) {
-                    // column pairs (2k, 2k+1): xi_{2k+1} = xi_{2k} + 1, so with the pair sums
-                    // P = sum u, X = sum xi_{2k} u, Q = sum xi_{2k}^2 u (one FADD2 / FFMA2 each,
-                    // scalar weights broadcast): R = P.x+P.y, Rx = X.x+X.y+P.y,
-                    // Rxx = Q.x+Q.y+2 X.y+P.y
-                    float2 Rp = make_float2(0.f, 0.f), Xp = Rp, Qp = Rp;
-#pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        const int l4 = 2 * row + half;
-                        const float4 u4 = lds_f4(ur + 16 * l4);
-                        const float4 w4 = lds_f4(wr + 16 * l4);
-                        const float4 g0 = lds_f4(gb + 16 * l4);  // broadcasts
-                        const float4 g1 = lds_f4(gb + 128 + 16 * l4);
-                        const float4 g2 = lds_f4(gb + 256 + 16 * l4);
-                        const float xa = (float)(4 * half) - 3.5f, xb = xa + 2.0f;  // xi of cols 4h, 4h+2
-                        const float2 ua = make_float2(u4.x, u4.y), ub = make_float2(u4.z, u4.w);
-                        Rp = __fadd2_rn(Rp, ua);
-                        Rp = __fadd2_rn(Rp, ub);
-                        Xp = __ffma2_rn(ua, make_float2(xa, xa), Xp);
-                        Xp = __ffma2_rn(ub, make_float2(xb, xb), Xp);
-                        Qp = __ffma2_rn(ua, make_float2(xa * xa, xa * xa), Qp);
-                        Qp = __ffma2_rn(ub, make_float2(xb * xb, xb * xb), Qp);
-                        c0p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g0.x, g0.y), c0p);
-                        c0p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g0.z, g0.w), c0p);
-                        c1p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g1.x, g1.y), c1p);
-                        c1p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g1.z, g1.w), c1p);
-                        c2p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g2.x, g2.y), c2p);
-                        c2p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g2.z, g2.w), c2p);
-                    }
-                    const float R = Rp.x + Rp.y;
-                    const float Rx = Xp.x + Xp.y + Rp.y;
-                    const float Rxx = Qp.x + Qp.y + 2.0f * Xp.y + Rp.y;
-                    const float eta = (float)row - 1.5f;
-                    a0 += R;
-                    ax1 += Rx;
-                    ay1 = __fmaf_rn(R, eta, ay1);
-                    axx += Rxx;
-                    axy = __fmaf_rn(Rx, eta, axy);
-                    ayy = __fmaf_rn(R, eta * eta, ayy);
+            // phase 2: dense over the group's 32 pixels per record row (row i = the i-th highest
+            // union splat); moments about the group centre. Up to 16 rows: two lanes per row,
+            // two pixel rows each, halves added with one shuffle; otherwise one lane per row.
+            float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            const uint32_t gb = lgbase + 512u * (uint32_t)cur + 128u;  // lg[cur][1..3]
+            int src = __popc(un & (0xfffffffeu << lane));  // row of splat `lane`
+            if (U <= 16) {
+                const int row = lane >> 1, prow0 = 2 * (lane & 1);
+                if (row < U) {
+                    const uint32_t ro = 4u * (uint32_t)(row * kRecStride) + 32u * (uint32_t)prow0;
+                    row_sums<2>(ubase + ro, wbase + ro, gb + 32u * (uint32_t)prow0, (float)prow0, acc);
                 }
-                c0s = c0p.x + c0p.y;
-                c1s = c1p.x + c1p.y;
-                c2s = c2p.x + c2p.y;
+#pragma unroll
+                for (int q = 0; q < 9; ++q) acc[q] += __shfl_xor_sync(kFull, acc[q], 1);
+                src *= 2;
+            } else if (lane < U) {
+                const uint32_t ro = 4u * (uint32_t)(lane * kRecStride);
+                row_sums<4>(ubase + ro, wbase + ro, gb, 0.f, acc);
             }
-            // hand row i's sums to lane j = its splat (row of j = union bits above j)
-            const int src = __popc(un & (0xfffffffeu << lane));
-            a0 = __shfl_sync(kFull, a0, src);
-            ax1 = __shfl_sync(kFull, ax1, src);
-            ay1 = __shfl_sync(kFull, ay1, src);
-            axx = __shfl_sync(kFull, axx, src);
-            axy = __shfl_sync(kFull, axy, src);
-            ayy = __shfl_sync(kFull, ayy, src);
-            c0s = __shfl_sync(kFull, c0s, src);
-            c1s = __shfl_sync(kFull, c1s, src);
-            c2s = __shfl_sync(kFull, c2s, src);
+            // hand row i's sums to lane j = its splat
+#pragma unroll
+            for (int q = 0; q < 9; ++q) acc[q] = __shfl_sync(kFull, acc[q], src);
+            const float a0 = acc[0], ax1 = acc[1], ay1 = acc[2], axx = acc[3], axy = acc[4],
+                        ayy = acc[5], c0s = acc[6], c1s = acc[7], c2s = acc[8];
             if ((un >> lane) & 1u) {
                 const float dx = (float)(gx * 8) + 3.5f - hx, dy = (float)(gy * 4) + 1.5f - hy;
                 m0 += a0;
