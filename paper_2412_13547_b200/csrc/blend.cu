@@ -485,11 +485,15 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
         __syncwarp();
         uint32_t mask = 0, slot = 0;
         float4 ja = make_float4(0.f, 0.f, 0.f, 0.f), jb = make_float4(0.f, 0.f, 0.f, 0.f);
+        // the next (earlier) chunk's list entry, loaded alongside this chunk's: its prepared
+        // record is prefetched into L2 below, hiding the DRAM latency of the next staging
+        const uint32_t nxt = ch > 0 ? prm.items[range.x + j - 32] : 0u;
         if (jvalid) {
             const Prepared& P = prm.prep[prm.items[range.x + j]];
             mask = stage_splat(P, geo, p, rbase + lane * kRec, ja, jb);
             slot = pair_slot(P, geo.tx, geo.ty);
         }
+        if (ch > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(prm.prep + nxt));
         __syncwarp();
         float m0 = 0.f, mx1 = 0.f, my1 = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
         float q0 = 0.f, q1 = 0.f, q2 = 0.f;
