@@ -87,6 +87,10 @@ int32_t tgsx_profile_read(tgsx_ctx* ctx, double* ms, int64_t* counts, int32_t n)
  * plus Adam moments live in HBM for the model's lifetime. */
 int32_t tgsx_model_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model** out);
 void tgsx_model_destroy(tgsx_model* m);
+/* Grows the model's capacity (contents kept) and the context's per-Gaussian workspace to at
+ * least `capacity` Gaussians, so densification up to that size allocates nothing (the
+ * trainer reserves its maximal budget up front). */
+int32_t tgsx_model_reserve(tgsx_ctx* ctx, tgsx_model* m, int64_t capacity);
 int64_t tgsx_model_size(const tgsx_model* m);
 uint64_t tgsx_model_next_id(const tgsx_model* m);
 /* Upload replaces the whole model (moments zeroed, Adam step counter kept). */

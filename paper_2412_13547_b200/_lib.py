@@ -76,6 +76,7 @@ SIGNATURES = {
     "tgsx_profile_read": (C.c_int32, [vp, f64p, i64p, C.c_int32]),
     "tgsx_model_create": (C.c_int32, [vp, C.c_int64, P(vp)]),
     "tgsx_model_destroy": (None, [vp]),
+    "tgsx_model_reserve": (C.c_int32, [vp, vp, C.c_int64]),
     "tgsx_model_size": (C.c_int64, [vp]),
     "tgsx_model_next_id": (C.c_uint64, [vp]),
     "tgsx_model_upload": (C.c_int32, [vp, vp, P(HostScene)]),

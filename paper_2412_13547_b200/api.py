@@ -300,6 +300,11 @@ class DeviceModel:
         dm.upload(model)
         return dm
 
+    def reserve(self, capacity: int):
+        """Grow capacity and workspace to `capacity` Gaussians (no allocation while densifying
+        up to that size)."""
+        self.ctx.check(self.ctx.L.tgsx_model_reserve(self.ctx.h, self.h, int(capacity)))
+
     def upload(self, model: GaussianModel):
         hs = model._host_scene()
         self.ctx.check(self.ctx.L.tgsx_model_upload(self.ctx.h, self.h, C.byref(hs)))

@@ -236,6 +236,25 @@ cudaError_t permute_model(tgsx_ctx* ctx, tgsx_model* m, const uint32_t* idx) {
 
 }  // namespace
 
+// Capacity growth (contents kept) with the spare row buffers sized alongside, so neither
+// permutation nor prune compaction allocates later.
+cudaError_t model_grow(tgsx_ctx* ctx, tgsx_model* m, int64_t cap) {
+    if (cap <= m->cap) return cudaSuccess;
+    cudaError_t e = model_reserve(ctx, m, cap);
+    if (e) return e;
+    const int rows[11] = {kParamRows, 1, 1, 1, 1, 1, 1, 1, 9, 9, kStepFloats};
+    const int elt[11] = {4, 8, 4, 4, 4, 8, 8, 8, 4, 4, 4};
+    for (int i = 0; i < 11; ++i) {
+        DevBuf& sp = m->spare[i];
+        const size_t bytes = (size_t)rows[i] * m->cap * elt[i];
+        if (sp.bytes >= bytes) continue;
+        sp.release();
+        if ((e = cudaMalloc(&sp.p, bytes))) return e;
+        sp.bytes = bytes;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t model_to_blend_order(tgsx_ctx* ctx, tgsx_model* m) {
     if (m->blend_phys || m->order_dirty) return cudaSuccess;
     cudaError_t e = permute_model(ctx, m, m->perm.as<uint32_t>());
@@ -694,6 +713,21 @@ void tgsx_model_destroy(tgsx_model* m) {
     for (DevBuf* b : bufs) b->release();
     for (DevBuf& b : m->spare) b.release();
     delete m;
+}
+
+int32_t tgsx_model_reserve(tgsx_ctx* ctx, tgsx_model* m, int64_t capacity) {
+    if (!ctx || !m || capacity < 0) return TGSX_EINVAL;
+    CK(model_grow(ctx, m, capacity));
+    // per-Gaussian workspace (prepared records, counts, offsets, depth-sort and densify scratch)
+    Workspace& ws = ctx->ws;
+    const int64_t c = std::max<int64_t>(m->cap, 1);
+    CK(ws.prep.ensure(c * sizeof(Prepared)));
+    CK(ws.touched.ensure((c + 1) * 4));
+    CK(ws.pair_off.ensure((c + 1) * 4));
+    for (int i = 0; i < 2; ++i) CK(ws.keys[i].ensure(c * 4));
+    CK(ws.generic.ensure((size_t)c * 4 * 7));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
 }
 
 int64_t tgsx_model_size(const tgsx_model* m) { return m ? m->n : 0; }

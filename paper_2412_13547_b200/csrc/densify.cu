@@ -183,39 +183,6 @@ cudaError_t scan_count(tgsx_ctx* ctx, const uint32_t* flags, uint32_t* pos, int6
     return cudaSuccess;
 }
 
-// Re-allocates one [rows][cap] row group at a larger capacity, keeping the first n columns of
-// every row (capacity grows geometrically, so this runs O(log N) times per fit).
-cudaError_t regrow(tgsx_ctx* ctx, DevBuf& b, int rows, size_t elt, int64_t oc, int64_t cap, int64_t n) {
-    void* np = nullptr;
-    cudaError_t e = cudaMalloc(&np, (size_t)rows * cap * elt);
-    if (e) return e;
-    if ((e = cudaMemsetAsync(np, 0, (size_t)rows * cap * elt, ctx->stream))) return e;
-    if (b.p && n > 0)
-        if ((e = cudaMemcpy2DAsync(np, cap * elt, b.p, oc * elt, n * elt, rows, cudaMemcpyDeviceToDevice, ctx->stream)))
-            return e;
-    if ((e = cudaStreamSynchronize(ctx->stream))) return e;
-    b.release();
-    b.p = np;
-    b.bytes = (size_t)rows * cap * elt;
-    return cudaSuccess;
-}
-
-cudaError_t reserve(tgsx_ctx* ctx, tgsx_model* m, int64_t need) {
-    if (need <= m->cap) return cudaSuccess;
-    const int64_t cap = std::max<int64_t>(need, m->cap + m->cap / 2);
-    const int64_t oc = m->cap, n = m->n;
-    cudaError_t e;
-    struct R { DevBuf* b; int rows; size_t elt; } rs[] = {
-        {&m->params, 10, 4}, {&m->ids, 1, 8}, {&m->pos_acc, 1, 4}, {&m->col_acc, 1, 4},
-        {&m->accum, 1, 4}, {&m->visit, 1, 8}, {&m->window, 1, 8}, {&m->tau_v, 1, 8},
-        {&m->m1, 9, 4}, {&m->m2, 9, 4}, {&m->step, kStepFloats, 4}, {&m->screen, 10, 4},
-        {&m->perm, 1, 4}, {&m->rank_of, 1, 4}};
-    for (auto& r : rs)
-        if ((e = regrow(ctx, *r.b, r.rows, r.elt, oc, cap, n))) return e;
-    m->cap = cap;
-    return cudaSuccess;
-}
-
 }  // namespace
 
 extern "C" {
@@ -290,7 +257,8 @@ int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cf
     }
     // spawn
     if (nsel > 0) {
-        DCK(reserve(ctx, m, n0 + nsel));
+        // geometric capacity growth (x1.5) when the children do not fit
+        if (n0 + nsel > m->cap) DCK(model_grow(ctx, m, std::max<int64_t>(n0 + nsel, m->cap + m->cap / 2)));
         PcgDev base{rng_state[0], rng_state[1]};
         spawn_kernel<<<grid_for(n0, 256), 256, 0, ctx->stream>>>(
             m->params.as<float>(), m->cap, n0, m->ids.as<unsigned long long>(), m->next_id,

@@ -132,6 +132,8 @@ struct tgsx_model {
 // order for densify / download / explicit-gradient APIs
 cudaError_t model_to_blend_order(tgsx_ctx* ctx, tgsx_model* m);
 cudaError_t model_to_logical_order(tgsx_ctx* ctx, tgsx_model* m);
+// capacity growth keeping contents, spare row buffers sized alongside (capi.cu)
+cudaError_t model_grow(tgsx_ctx* ctx, tgsx_model* m, int64_t cap);
 
 namespace tgsx {
 

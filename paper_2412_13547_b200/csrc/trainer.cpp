@@ -94,6 +94,16 @@ int32_t tgsx_trainer_create(tgsx_ctx* ctx, tgsx_model* m, const tgsx_train_confi
     tr->n_init = tgsx_model_size(m);
     const double mf = cfg->m_final > 0 ? cfg->m_final : 1.5 * (double)tr->n_init;
     tgsx_budget_create((double)tr->n_init, mf, &tr->budget);
+    // the budget never exceeds the adaptive maximum 1.5 M: reserve it up front so
+    // densify events allocate nothing
+    if (cfg->densify_until > cfg->warmup_iters) {
+        const int32_t rc = tgsx_model_reserve(ctx, m, (int64_t)std::ceil(1.5 * mf) + 1024);
+        if (rc) {
+            tgsx_budget_destroy(tr->budget);
+            delete tr;
+            return rc;
+        }
+    }
     tgsx_pcg32_init(tr->rng, cfg->seed, 1);
     tr->ring = std::max<int64_t>(cfg->densify_interval, 1) * 4 + 64;
     if (cudaMalloc(&tr->d_losses, sizeof(float) * tr->ring) != cudaSuccess ||
