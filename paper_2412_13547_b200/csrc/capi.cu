@@ -5,6 +5,7 @@
 #include "tgsx_internal.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -201,6 +202,7 @@ __global__ void permute_rows_kernel(const T* __restrict__ src, T* __restrict__ d
 
 // every row group: new[p] = old[idx[p]] (through the model's spare buffers, pointer swap)
 cudaError_t permute_model(tgsx_ctx* ctx, tgsx_model* m, const uint32_t* idx) {
+    ctx->bin_valid = false;
     const int64_t n = m->n, cap = m->cap;
     if (n == 0) return cudaSuccess;
     struct R { DevBuf* b; int rows; int elt; } rs[] = {
@@ -303,8 +305,8 @@ bool force_onesweep() {
 // scatter + per-tile sort, or (a list longer than kSegCap, or TGSX_BINNING=onesweep)
 // duplicate -> onesweep radix sort -> ranges.
 // On return ws.K, ws.ranges and `items` (per-tile ranks in blend order) describe the lists.
-int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t** items,
-            uint32_t** sorted_keys) {
+int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t** items,
+                    uint32_t** sorted_keys) {
     Workspace& ws = ctx->ws;
     ws.have_forward = false;
     CK(reset_counters(ctx));
@@ -423,6 +425,32 @@ int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t*
     }
     *items = v;
     if (sorted_keys) *sorted_keys = k;
+    return TGSX_OK;
+}
+
+// Binning with reuse: a second view of the same, unchanged model at the same resolution and
+// low-pass (every view of a batched step; render followed by backward) keeps the previous
+// prepared records and tile lists — pixel_span works on the full-resolution image, so the lists
+// do not depend on the dilation offset (rasterizer.cpp:74-100).
+int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t** items,
+            uint32_t** sorted_keys) {
+    if (!sorted_keys && ctx->bin_valid && ctx->bin_model == m->uid && ctx->bin_lowpass == lowpass_p &&
+        ctx->bin_W == W && ctx->bin_H == H && ctx->bin_n == m->n && !m->order_dirty && m->blend_phys) {
+        ctx->ws.have_forward = false;
+        CK(reset_counters(ctx));  // blend-op / evaluation counters are per render
+        *items = ctx->bin_items;
+        return TGSX_OK;
+    }
+    ctx->bin_valid = false;
+    const int32_t rc = bin_compute(ctx, m, lowpass_p, W, H, items, sorted_keys);
+    if (rc) return rc;
+    ctx->bin_valid = true;
+    ctx->bin_model = m->uid;
+    ctx->bin_lowpass = lowpass_p;
+    ctx->bin_W = W;
+    ctx->bin_H = H;
+    ctx->bin_n = m->n;
+    ctx->bin_items = *items;
     return TGSX_OK;
 }
 
@@ -586,6 +614,7 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
         StageTimer t(ctx, kStChain);
         CK(launch_chain(ctx, m, mode, true, nullptr, reinterpret_cast<const float*>(cfg)));
     }
+    if (mode == ChainMode::kAdam) ctx->bin_valid = false;  // the parameters moved
     const int tiles = ws.tiles_x * ws.tiles_y;
     float* dloss = reinterpret_cast<float*>(ws.counters.as<unsigned long long>() + 4);
     {
@@ -696,6 +725,8 @@ int32_t tgsx_profile_read(tgsx_ctx* ctx, double* ms, int64_t* counts, int32_t n)
 int32_t tgsx_model_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model** out) {
     if (!ctx || !out) return TGSX_EINVAL;
     tgsx_model* m = new tgsx_model();
+    static std::atomic<uint64_t> next_uid{1};
+    m->uid = next_uid.fetch_add(1);
     cudaError_t e = model_reserve(ctx, m, std::max<int64_t>(capacity, 1));
     if (e) {
         delete m;
@@ -717,6 +748,7 @@ void tgsx_model_destroy(tgsx_model* m) {
 
 int32_t tgsx_model_reserve(tgsx_ctx* ctx, tgsx_model* m, int64_t capacity) {
     if (!ctx || !m || capacity < 0) return TGSX_EINVAL;
+    ctx->bin_valid = false;
     CK(model_grow(ctx, m, capacity));
     // per-Gaussian workspace (prepared records, counts, offsets, depth-sort and densify scratch)
     Workspace& ws = ctx->ws;
@@ -735,6 +767,7 @@ uint64_t tgsx_model_next_id(const tgsx_model* m) { return m ? m->next_id : 0; }
 
 int32_t tgsx_model_upload(tgsx_ctx* ctx, tgsx_model* m, const tgsx_host_scene* h) {
     if (!ctx || !m || !h || h->n < 0) return fail(ctx, TGSX_EINVAL, "bad upload arguments");
+    ctx->bin_valid = false;
     const int64_t n = h->n;
     CK(model_reserve(ctx, m, n));
     m->n = n;
@@ -898,6 +931,7 @@ int32_t tgsx_backward(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, con
 int32_t tgsx_adam_step(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const tgsx_adam_args* a) {
     if (!ctx || !m || !grads || !a) return TGSX_EINVAL;
     if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
+    ctx->bin_valid = false;
     AdamCfg c;
     fill_adam(c, a);
     CK(model_to_logical_order(ctx, m));  // explicit gradients are in logical order
@@ -935,6 +969,7 @@ float* tgsx_step_buffer(tgsx_model* m, int64_t* out_floats) {
 int32_t tgsx_apply_step(tgsx_ctx* ctx, tgsx_model* m, int32_t batch_views, const tgsx_adam_args* a) {
     if (!ctx || !m || !a) return TGSX_EINVAL;
     if (batch_views < 1) return fail(ctx, TGSX_EINVAL, "accumulate: empty batch");
+    ctx->bin_valid = false;  // parameters change
     if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
     AdamCfg c;
     fill_adam(c, a);
@@ -946,6 +981,7 @@ int32_t tgsx_apply_step(tgsx_ctx* ctx, tgsx_model* m, int32_t batch_views, const
 // ---------------------------------------------------------------- stage access
 int32_t tgsx_stage_prepare(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, float* out, uint32_t* orig) {
     if (!ctx || !m || lowpass_p < 1) return fail(ctx, TGSX_EINVAL, "bad arguments");
+    ctx->bin_valid = false;
     CK(reset_counters(ctx));
     if (m->order_dirty) CK(launch_sort_depth(ctx, m));
     CK(launch_preprocess(ctx, m, lowpass_p, 16, 16));
@@ -972,6 +1008,7 @@ int32_t tgsx_stage_prepare(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, floa
 
 int32_t tgsx_stage_sorted_order(tgsx_ctx* ctx, tgsx_model* m, uint32_t* perm) {
     if (!ctx || !m) return TGSX_EINVAL;
+    ctx->bin_valid = false;
     if (m->order_dirty) CK(launch_sort_depth(ctx, m));
     if (m->n && perm) CK(cudaMemcpyAsync(perm, m->perm.p, m->n * 4, cudaMemcpyDefault, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1031,6 +1068,7 @@ int32_t tgsx_stage_counters(tgsx_ctx* ctx, uint64_t* out_blend_ops, uint64_t* ou
 
 int32_t tgsx_sort_pairs(tgsx_ctx* ctx, uint32_t* keys, uint32_t* vals, int64_t n, int32_t key_bits) {
     if (!ctx || n < 0 || key_bits < 0 || key_bits > 32) return TGSX_EINVAL;
+    ctx->bin_valid = false;  // shares the binning scratch
     if (n <= 1) return TGSX_OK;
     DevBuf& a = ctx->ws.generic;
     CK(a.ensure((size_t)n * 8));
@@ -1049,6 +1087,7 @@ int32_t tgsx_sort_pairs(tgsx_ctx* ctx, uint32_t* keys, uint32_t* vals, int64_t n
 
 int32_t tgsx_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n, uint64_t* out_total) {
     if (!ctx || n < 0) return TGSX_EINVAL;
+    ctx->bin_valid = false;  // shares the binning scratch
     uint32_t* d_total = reinterpret_cast<uint32_t*>(ctx->ws.counters.as<unsigned long long>() + 5);
     CK(launch_exclusive_scan(ctx, in, out, n, d_total));
     CK(cudaMemcpyAsync(ctx->ws.h_scratch + 24, d_total, 4, cudaMemcpyDeviceToHost, ctx->stream));

@@ -202,6 +202,7 @@ int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cf
     StageTimer timer(ctx, kStDensify);
     // selection ties, spawn order and compaction follow the logical (creation) order
     DCK(model_to_logical_order(ctx, m));
+    ctx->bin_valid = false;  // the model changes (and the scratch below overlaps the binning's)
     const int64_t n0 = m->n;
     tgsx_densify_report rep{};
     // colour coin: one draw per event

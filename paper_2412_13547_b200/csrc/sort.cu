@@ -376,6 +376,7 @@ cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m) {
     cudaError_t e;
     // ties are broken by id in logical order: sort the logical layout
     if ((e = model_to_logical_order(ctx, m))) return e;
+    ctx->bin_valid = false;  // the sort reuses the binning buffers
     for (int i = 0; i < 2; ++i) {
         if ((e = ws.keys[i].ensure(n * 4))) return e;
         if ((e = ws.vals[i].ensure(n * 4))) return e;

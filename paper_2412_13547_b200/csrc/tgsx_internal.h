@@ -93,6 +93,14 @@ struct tgsx_ctx {
     cudaEvent_t staged[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
     bool stage_used[2] = {false, false};
     int stage_next = 0, stage_pending = -1;
+    // binning reuse: views of an unchanged model with the same geometry share one binning (the
+    // tile lists do not depend on the dilation offset). Any entry point that changes the
+    // parameters, the row order or the binning workspace clears bin_valid.
+    bool bin_valid = false;
+    uint64_t bin_model = 0;
+    int bin_lowpass = 0, bin_W = 0, bin_H = 0;
+    int64_t bin_n = -1;
+    uint32_t* bin_items = nullptr;
 };
 
 // Scoped stage timer: no-op unless profiling is enabled.
@@ -111,6 +119,7 @@ struct StageTimer {
 }  // namespace tgsx
 
 struct tgsx_model {
+    uint64_t uid = 0;  // unique per created model (binning-reuse key)
     int64_t n = 0, cap = 0;
     uint64_t next_id = 0;
     bool order_dirty = true;
