@@ -458,14 +458,12 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
 
     // per-group (last, dL/dC) prefetch, one group ahead, cyclic over the groups of every chunk
     const uint32_t lgbase = smem_addr(S.lg);
+    // dense rank of active pixel (lx, ly) = rank0 + ly * cols + lx (ax, ay are active pixels)
+    const int rank0 = ((geo.ay - prm.oy) / p) * prm.cols + (geo.ax - prm.ox) / p;
     auto prefetch = [&](int g, int buf) {
         const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
         const bool valid = lx < geo.acols && ly < geo.arows;
-        int r = 0;
-        if (valid) {
-            const int x = geo.ax + lx * p, y = geo.ay + ly * p;
-            r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
-        }
+        const int r = valid ? rank0 + ly * prm.cols + lx : 0;
         const uint32_t nb = valid ? 4u : 0u;
         const uint32_t d = lgbase + 512u * (uint32_t)buf + 4u * (uint32_t)lane;
         cp_async4(d, prm.last + r, nb);
