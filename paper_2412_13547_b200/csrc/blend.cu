@@ -198,10 +198,12 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_pairs_kernel(BlendPara
             const uint32_t lbase = (uint32_t)(bstart + c0 + 1);
             int termA = 32, termB = 32;  // bit of each pixel's terminating blend, 32 = none
             uint32_t colU = colA | colB;
+            // branch-free: a lane whose walk is over runs on record 0 with both pixels masked
+            // (sigma = 0 changes nothing)
             while (__any_sync(kFull, colU)) {
-                if (colU) {
-                    const int k = __ffs(colU) - 1;
-                    const uint32_t bit = 1u << k;
+                {
+                    const int k = colU ? __ffs(colU) - 1 : 0;
+                    const uint32_t bit = colU ? 1u << k : 0u;
                     const bool hA = (colA & bit) != 0u, hB = (colB & bit) != 0u;
                     colA &= ~bit;
                     colB &= ~bit;
