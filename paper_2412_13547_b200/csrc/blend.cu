@@ -126,6 +126,18 @@ __device__ __forceinline__ uint32_t stage_splat(const Prepared& P, const TileGeo
 }
 
 // ------------------------------------------------------------------------ forward (pairs)
+// Exponent of conic_gauss for two pixels in the same column (rows fyA, fyB) as packed FP32x2,
+// the same op sequence (and rounding) per pixel as conic_gauss: a = (mx, my, ka, kb), kc.
+__device__ __forceinline__ float2 pair_quad(const float4& a, float kc, float fx, float fyA, float fyB) {
+    const float dx = __fsub_rn(fx, a.x);
+    const float2 dy = make_float2(__fsub_rn(fyA, a.y), __fsub_rn(fyB, a.y));
+    const float2 t = __fmul2_rn(make_float2(kc, kc), dy);
+    const float2 u = __ffma2_rn(make_float2(a.w, a.w), make_float2(dx, dx), t);
+    const float2 v = __fmul2_rn(u, dy);
+    const float kadx = __fmul_rn(a.z, dx);
+    return __ffma2_rn(make_float2(kadx, kadx), make_float2(dx, dx), v);
+}
+
 // Row bits 0,2,4,6 of an 8-bit row mask spread to bytes 0..3 (one byte per lane row-pair).
 __device__ __forceinline__ uint32_t spread_even4(uint32_t yb) {
     return (yb & 1u) | ((yb & 4u) << 6) | ((yb & 16u) << 12) | ((yb & 64u) << 18);
@@ -200,43 +212,52 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_pairs_kernel(BlendPara
             uint32_t colU = colA | colB;
             // branch-free: a lane whose walk is over runs on record 0 with both pixels masked
             // (sigma = 0 changes nothing)
+            // Two splats (k1 < k2) per iteration: their Gaussians are independent (ILP), the
+            // blends are applied in order and a ray that terminates at k1 does not blend k2.
             while (__any_sync(kFull, colU)) {
-                {
-                    const int k = colU ? __ffs(colU) - 1 : 0;
-                    const uint32_t bit = colU ? 1u << k : 0u;
-                    const bool hA = (colA & bit) != 0u, hB = (colB & bit) != 0u;
-                    colA &= ~bit;
-                    colB &= ~bit;
-                    const uint32_t ad = cbase + k * kRec;
-                    const float4 a = lds_f4(ad), b = lds_f4(ad + 16);
-                    const float cz = lds_f1(ad + 32);
-                    // conic_gauss for both pixels, same op sequence
-                    const float dx = __fsub_rn(fx, a.x);
-                    const float2 dy = make_float2(__fsub_rn(fyA, a.y), __fsub_rn(fyB, a.y));
-                    const float2 t = __fmul2_rn(make_float2(b.x, b.x), dy);
-                    const float2 u = __ffma2_rn(make_float2(a.w, a.w), make_float2(dx, dx), t);
-                    const float2 v = __fmul2_rn(u, dy);
-                    const float kadx = __fmul_rn(a.z, dx);
-                    const float2 q = __ffma2_rn(make_float2(kadx, kadx), make_float2(dx, dx), v);
-                    // a pixel that does not pass the splat gets sigma = 0 (T, colour unchanged)
-                    const float2 s = make_float2(hA ? __fmul_rn(b.y, fast_exp2(q.x)) : 0.f,
-                                                 hB ? __fmul_rn(b.y, fast_exp2(q.y)) : 0.f);
-                    const float2 w = __fmul2_rn(s, T);
-                    // 1 - sigma with one rounding, exactly as the scalar subtraction
-                    T = __fmul2_rn(T, __ffma2_rn(s, make_float2(-1.0f, -1.0f), make_float2(1.0f, 1.0f)));
-                    C0 = __ffma2_rn(w, make_float2(b.z, b.z), C0);
-                    C1 = __ffma2_rn(w, make_float2(b.w, b.w), C1);
-                    C2 = __ffma2_rn(w, make_float2(cz, cz), C2);
-                    if (hA && T.x < kTermT) {  // ray A terminates (break after blending)
-                        termA = k;
-                        colA = 0;
-                    }
-                    if (hB && T.y < kTermT) {
-                        termB = k;
-                        colB = 0;
-                    }
-                    colU = colA | colB;
+                const int k1 = colU ? __ffs(colU) - 1 : 0;
+                const uint32_t bit1 = colU ? 1u << k1 : 0u;
+                const uint32_t rem = colU & ~bit1;
+                const int k2 = rem ? __ffs(rem) - 1 : 0;
+                const uint32_t bit2 = rem ? 1u << k2 : 0u;
+                const bool hA1 = (colA & bit1) != 0u, hB1 = (colB & bit1) != 0u;
+                const bool hA2 = (colA & bit2) != 0u, hB2 = (colB & bit2) != 0u;
+                const uint32_t ad1 = cbase + k1 * kRec, ad2 = cbase + k2 * kRec;
+                const float4 a1 = lds_f4(ad1), b1 = lds_f4(ad1 + 16);
+                const float4 a2 = lds_f4(ad2), b2 = lds_f4(ad2 + 16);
+                const float cz1 = lds_f1(ad1 + 32), cz2 = lds_f1(ad2 + 32);
+                const float2 q1 = pair_quad(a1, b1.x, fx, fyA, fyB);
+                const float2 q2 = pair_quad(a2, b2.x, fx, fyA, fyB);
+                const float2 e1 = make_float2(fast_exp2(q1.x), fast_exp2(q1.y));
+                const float2 e2 = make_float2(fast_exp2(q2.x), fast_exp2(q2.y));
+                // a pixel that does not pass the splat gets sigma = 0 (T, colour unchanged)
+                const float2 s1 = make_float2(hA1 ? __fmul_rn(b1.y, e1.x) : 0.f, hB1 ? __fmul_rn(b1.y, e1.y) : 0.f);
+                const float2 w1 = __fmul2_rn(s1, T);
+                // 1 - sigma with one rounding, exactly as the scalar subtraction
+                T = __fmul2_rn(T, __ffma2_rn(s1, make_float2(-1.0f, -1.0f), make_float2(1.0f, 1.0f)));
+                C0 = __ffma2_rn(w1, make_float2(b1.z, b1.z), C0);
+                C1 = __ffma2_rn(w1, make_float2(b1.w, b1.w), C1);
+                C2 = __ffma2_rn(w1, make_float2(cz1, cz1), C2);
+                const bool tA1 = hA1 && T.x < kTermT, tB1 = hB1 && T.y < kTermT;  // ray ends at k1
+                const bool gA2 = hA2 && !tA1, gB2 = hB2 && !tB1;
+                const float2 s2 = make_float2(gA2 ? __fmul_rn(b2.y, e2.x) : 0.f, gB2 ? __fmul_rn(b2.y, e2.y) : 0.f);
+                const float2 w2 = __fmul2_rn(s2, T);
+                T = __fmul2_rn(T, __ffma2_rn(s2, make_float2(-1.0f, -1.0f), make_float2(1.0f, 1.0f)));
+                C0 = __ffma2_rn(w2, make_float2(b2.z, b2.z), C0);
+                C1 = __ffma2_rn(w2, make_float2(b2.w, b2.w), C1);
+                C2 = __ffma2_rn(w2, make_float2(cz2, cz2), C2);
+                const bool tA2 = gA2 && T.x < kTermT, tB2 = gB2 && T.y < kTermT;
+                colA &= ~(bit1 | bit2);
+                colB &= ~(bit1 | bit2);
+                if (tA1 || tA2) {  // ray A terminates (break after blending)
+                    termA = tA1 ? k1 : k2;
+                    colA = 0;
                 }
+                if (tB1 || tB2) {
+                    termB = tB1 ? k1 : k2;
+                    colB = 0;
+                }
+                colU = colA | colB;
             }
             if (colA0) {
                 const uint32_t used = termA < 32 ? (colA0 & (kFull >> (31 - termA))) : colA0;
