@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import bind as B
-from tests.helpers import frac_close, model_from_scene, target_image
+from tests.helpers import frac_close, model_from_scene, scene_from_model, target_image
 
 pytestmark = pytest.mark.gpu
 
@@ -113,6 +113,54 @@ def test_batched_views_match_oracle(P, ctx):
     for i, f in enumerate(B.PARAM_FIELDS):
         assert frac_close(h.params[i], getattr(s, f), 1e-6, 1e-6) >= 0.995, f
     assert np.allclose(h.pos_grad_norm_accum, s.pos_acc, rtol=2e-3, atol=1e-9)
+
+
+def test_binning_reuse_invalidated_by_every_model_change(P, ctx):
+    """Views of an unchanged model share one binning; each parameter / order change must drop it.
+    After render -> adam_step / apply_step / densify / upload, the next render equals the oracle
+    render of the changed scene."""
+    W, H, n = 80, 64, 1200
+    s = B.synthetic_scene(4, n, W, H).ensure_stats()
+    dm = P.DeviceModel.from_host(model_from_scene(s), ctx)
+    diag = math.hypot(W, H)
+    pat = P.DilationPattern(2, 1, 0, W, H)
+    m1 = np.zeros((9, n), np.float32)
+    m2 = np.zeros((9, n), np.float32)
+
+    def check():
+        # render first (a stale binning would be used here), then compare with the oracle
+        # render of the device's current parameters
+        got = dm.render(pat, (0.1, 0.2, 0.3)).colors
+        ref = B.render(scene_from_model(dm.download()), 2, 1, 0, W, H, (0.1, 0.2, 0.3))[0]
+        assert np.abs(got - ref).max() <= 2e-3 and (np.abs(got - ref).max(axis=1) > 1e-5).mean() <= 1e-3
+
+    dm.render(pat, (0.1, 0.2, 0.3))  # binning cached
+    check()
+    # explicit-gradient Adam (large steps so that tile rectangles change)
+    g = np.random.default_rng(0).normal(size=(9, n)).astype(np.float32) * 50
+    dm.render(pat, (0.1, 0.2, 0.3))
+    dm.adam_step(g, 1, 100, diag)
+    B.adam_step(s, g, m1, m2, B.adam_config(1, 100, diag))
+    check()
+    # batched views + apply_step
+    target = target_image(5, n, W, H)
+    gsum = np.zeros((9, n), np.float32)
+    for v in range(2):
+        ox, oy = P.next_offsets(2, v)
+        dm.view_accumulate(P.DilationPattern(2, ox, oy, W, H), (0, 0, 0), target)
+        rgb = B.render(s, 2, ox, oy, W, H)[0]
+        _, dl = B.l1_loss(rgb, 2, ox, oy, W, H, target)
+        gsum += B.backward(s, 2, ox, oy, W, H, dl)[0]
+    dm.apply_step(2, 2, 100, diag)
+    check()
+    # densify (spawn + prune change n and the blend order)
+    dm.render(pat, (0.1, 0.2, 0.3))
+    dm.densify(dm.size() + 200, P.Pcg32(3, 1).state, P.densify_config(tau_pos=1e-9))
+    check()
+    # upload of a different scene
+    dm.render(pat, (0.1, 0.2, 0.3))
+    dm.upload(model_from_scene(B.synthetic_scene(9, n, W, H)))
+    check()
 
 
 # ------------------------------------------------------------------ full-size properties
