@@ -59,6 +59,7 @@ struct BlendParams {
     float* block_loss;
     float loss_scale;
     Partials partial;              // backward output, one entry per pair slot
+    unsigned int* tile_queue;      // backward: next tile to take (zeroed before the launch)
 };
 
 struct TileGeo {
@@ -421,16 +422,9 @@ __device__ __forceinline__ void row_sums(uint32_t ur, uint32_t wr, uint32_t gb, 
 
 
 template <int NGX, int NGY>
-__global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm) {
+__device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSmem<NGX * NGY>& S,
+                                              int tile, int lane) {
     constexpr int NG = NGX * NGY;
-    static_assert(sizeof(BwdWarpSmem<NG>) % 16 == 0 && offsetof(BwdWarpSmem<NG>, lg) % 16 == 0 &&
-                      offsetof(BwdWarpSmem<NG>, rec) % 16 == 0,
-                  "float4 shared-memory reads need 16-byte alignment");
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    auto& S = reinterpret_cast<BwdWarpSmem<NG>*>(smem_raw)[warp];
-    const int tile = blockIdx.x * kWPB + warp;
-    if (tile >= prm.tiles) return;
     TileGeo geo;
     geo.init(prm, tile);
     const int p = prm.p;
@@ -661,6 +655,28 @@ __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm)
     cp_async_wait<0>();  // drain the last (unused) prefetch
 }
 
+// One warp per tile, tiles taken from a queue: a warp starts its next tile as soon as it has
+// finished one, so no warp idles until its CTA siblings finish (per-tile work varies) and the
+// tail of the launch is at most one tile.
+template <int NGX, int NGY>
+__global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm) {
+    constexpr int NG = NGX * NGY;
+    static_assert(sizeof(BwdWarpSmem<NG>) % 16 == 0 && offsetof(BwdWarpSmem<NG>, lg) % 16 == 0 &&
+                      offsetof(BwdWarpSmem<NG>, rec) % 16 == 0,
+                  "float4 shared-memory reads need 16-byte alignment");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto& S = reinterpret_cast<BwdWarpSmem<NG>*>(smem_raw)[warp];
+    for (;;) {
+        int tile = 0;
+        if (lane == 0) tile = (int)atomicAdd(prm.tile_queue, 1u);
+        tile = __shfl_sync(kFull, tile, 0);
+        if (tile >= prm.tiles) break;
+        backward_tile<NGX, NGY>(prm, S, tile, lane);
+        __syncwarp();
+    }
+}
+
 BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items) {
     Workspace& ws = ctx->ws;
     BlendParams prm{};
@@ -685,6 +701,8 @@ BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* ite
     prm.dLdC = ws.dLdC.as<float>();
     prm.block_loss = ws.block_loss.as<float>();
     prm.partial = Partials::at(ws.partial.p, ws.pair_cap);
+    // counters slot 7 (u32): the backward's tile queue
+    prm.tile_queue = reinterpret_cast<unsigned int*>(ws.counters.as<unsigned long long>() + 7);
     return prm;
 }
 
@@ -692,13 +710,24 @@ template <int NGX, int NGY>
 cudaError_t run_backward(tgsx_ctx* ctx, const BlendParams& prm) {
     const size_t smem = kWPB * sizeof(BwdWarpSmem<NGX * NGY>);
     static bool configured = false;
+    static int resident = 0;  // CTAs resident at once (SMs x CTAs per SM)
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(backward_kernel<NGX, NGY>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e) return e;
+        int sms = 0, per_sm = 0;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device))) return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, backward_kernel<NGX, NGY>,
+                                                               kWPB * 32, smem)))
+            return e;
+        resident = std::max(1, sms * std::max(per_sm, 1));
         configured = true;
     }
-    const unsigned grid = (unsigned)((prm.tiles + kWPB - 1) / kWPB);
+    cudaError_t e = cudaMemsetAsync(prm.tile_queue, 0, sizeof(unsigned int), ctx->stream);
+    if (e) return e;
+    const unsigned grid =
+        (unsigned)std::min<int64_t>((prm.tiles + kWPB - 1) / kWPB, (int64_t)resident);
+    if (grid == 0) return cudaSuccess;
     backward_kernel<NGX, NGY><<<grid, kWPB * 32, smem, ctx->stream>>>(prm);
     return cudaGetLastError();
 }
