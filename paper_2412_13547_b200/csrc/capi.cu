@@ -325,7 +325,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
     {
         StageTimer t(ctx, kStScan);
         CK(launch_exclusive_scan(ctx, ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(), m->n, d_total));
-        CK(launch_tile_finalize(ctx, tiles));
+        CK(launch_slab_finalize(ctx, tiles));
     }
     CK(cudaMemcpyAsync(ws.h_scratch, counters, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -336,15 +336,15 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
     const int64_t K = (int64_t)(uint32_t)(ws.h_scratch[3] & 0xffffffffull);
     const uint64_t max_list = ws.h_scratch[5];
     ws.K = K;
-    for (int i = 0; i < 2; ++i) CK(ws.vals[i].ensure(std::max<int64_t>(K, 1) * 4));
     CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
     ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
     if (max_list <= (uint64_t)kSegCap && !force_onesweep()) {
-        // scatter binning: tile lists claimed with atomics, then sorted per tile in shared memory
-        uint32_t* v = ws.vals[0].as<uint32_t>();
+        // slab binning: every tile's list was claimed by preprocess into its slab; sort each slab
+        // back into blend order (one warp per tile)
+        uint32_t* v = ws.tile_slab.as<uint32_t>();
         {
             StageTimer t(ctx, kStDuplicate);
-            CK(launch_scatter(ctx, m, v));
+            CK(launch_pair_base(ctx, m));
         }
         {
             StageTimer t(ctx, kStSort);
@@ -354,6 +354,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
         if (sorted_keys) *sorted_keys = nullptr;
         return TGSX_OK;
     }
+    for (int i = 0; i < 2; ++i) CK(ws.vals[i].ensure(std::max<int64_t>(K, 1) * 4));
     const int key_bits = key_bits_for(tiles);
     const int passes = (key_bits + 7) / 8;
     for (int i = 0; i < 2; ++i) CK(ws.keys[i].ensure(std::max<int64_t>(K, 1) * 4));
@@ -665,7 +666,7 @@ void tgsx_destroy(tgsx_ctx* ctx) {
     DevBuf* bufs[] = {&ws.prep, &ws.touched, &ws.pair_off, &ws.scan_tmp, &ws.keys[0], &ws.keys[1],
                       &ws.vals[0], &ws.vals[1], &ws.sort_tmp, &ws.ranges, &ws.partial, &ws.rgb,
                       &ws.T, &ws.last, &ws.dLdC, &ws.target, &ws.block_loss, &ws.counters,
-                      &ws.generic, &ws.tile_count, &ws.tile_off, &ws.tile_fill, &ws.tile_dense};
+                      &ws.generic, &ws.tile_fill, &ws.tile_slab};
     for (DevBuf* b : bufs) b->release();
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);
@@ -1027,25 +1028,31 @@ int32_t tgsx_stage_tile_lists(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, i
     if (out_k) *out_k = K;
     const int tiles = ctx->ws.tiles_x * ctx->ws.tiles_y;
     std::vector<uint2> rg(tiles);
-    std::vector<uint32_t> hi(K);
     // the context stream is non-blocking: order the legacy-stream copies after bin()'s kernels
     CK(cudaStreamSynchronize(ctx->stream));
     if (tiles) CK(cudaMemcpy(rg.data(), ctx->ws.ranges.p, (size_t)tiles * sizeof(uint2), cudaMemcpyDeviceToHost));
-    if (K) CK(cudaMemcpy(hi.data(), it, K * 4, cudaMemcpyDeviceToHost));
-    // validate the lists: contiguous in tile order, ranks strictly ascending inside each tile
+    // per-tile ranges index the items buffer (per-tile slabs, or one contiguous array for the
+    // onesweep path): gather them in tile order, checking blend order inside every tile
+    size_t span = 0;
+    for (int t = 0; t < tiles; ++t) {
+        if (rg[t].y < rg[t].x) return fail(ctx, TGSX_ESTATE, "bad tile range at tile " + std::to_string(t));
+        if (rg[t].y > rg[t].x) span = std::max<size_t>(span, rg[t].y);
+    }
+    std::vector<uint32_t> hi(span), flat;
+    flat.reserve(K);
+    if (span) CK(cudaMemcpy(hi.data(), it, span * 4, cudaMemcpyDeviceToHost));
     std::vector<uint32_t> off(tiles + 1, 0);
     for (int t = 0; t < tiles; ++t) {
-        const uint32_t c = rg[t].y - rg[t].x;
-        if (rg[t].y < rg[t].x || (c && rg[t].x != off[t]))
-            return fail(ctx, TGSX_ESTATE, "tile ranges not contiguous at tile " + std::to_string(t));
-        for (uint32_t s = rg[t].x + 1; s < rg[t].y; ++s)
-            if (hi[s] <= hi[s - 1])
-                return fail(ctx, TGSX_ESTATE, "tile list not in blend order at " + std::to_string(s));
-        off[t + 1] = off[t] + c;
+        for (uint32_t s = rg[t].x; s < rg[t].y; ++s) {
+            if (s > rg[t].x && hi[s] <= hi[s - 1])
+                return fail(ctx, TGSX_ESTATE, "tile list not in blend order at tile " + std::to_string(t));
+            flat.push_back(hi[s]);
+        }
+        off[t + 1] = off[t] + (rg[t].y - rg[t].x);
     }
     if (off[tiles] != (uint64_t)K) return fail(ctx, TGSX_ESTATE, "tile ranges do not cover the pairs");
     if (offsets) CK(cudaMemcpy(offsets, off.data(), off.size() * 4, cudaMemcpyDefault));
-    if (items && items_cap >= K && K) CK(cudaMemcpy(items, it, K * 4, cudaMemcpyDefault));
+    if (items && items_cap >= K && K) CK(cudaMemcpy(items, flat.data(), K * 4, cudaMemcpyDefault));
     return TGSX_OK;
 }
 

@@ -25,8 +25,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     const float* __restrict__ params, int64_t cap, int64_t n,
     const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ perm, int blend_phys,
     int lowpass_p, int W, int H, int tiles_x,
-    Prepared* __restrict__ prep, uint32_t* __restrict__ touched, uint32_t* __restrict__ tile_count,
-    unsigned long long* err) {
+    Prepared* __restrict__ prep, uint32_t* __restrict__ touched, uint32_t* __restrict__ fill,
+    uint32_t* __restrict__ slab, unsigned long long* err) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     // row i is rank i when the model is stored in blend order (logical index perm[i])
@@ -71,10 +71,26 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
         o.d = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16),
                          0u, tiles);
-        if (tile_count)  // per-tile list lengths for the scatter binning (fire-and-forget RED)
-            for (int ty = ty0; ty <= ty1; ++ty)
-                for (int tx = tx0; tx <= tx1; ++tx)
-                    atomicAdd(&tile_count[(size_t)(ty * tiles_x + tx) * kFillStride], 1u);
+        if (fill) {
+            // slab binning: claim a slot in every touched tile's slab (kSegCap entries per tile,
+            // arbitrary order inside a tile; the per-tile sort restores blend order). Four claims
+            // in flight per step: the returning atomics' latency dominates.
+            const int w = tx1 - tx0 + 1, cnt = (int)tiles;
+            for (int q0 = 0; q0 < cnt; q0 += 4) {
+                uint32_t pos[4], tt[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (q0 + u < cnt) {
+                        const int q = q0 + u;
+                        tt[u] = (uint32_t)((ty0 + q / w) * tiles_x + tx0 + q % w);
+                        pos[u] = atomicAdd(&fill[(size_t)tt[u] * kFillStride], 1u);
+                    }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (q0 + u < cnt && pos[u] < (uint32_t)kSegCap)
+                        slab[(size_t)tt[u] * kSegCap + pos[u]] = rank;
+            }
+        }
     } else {
         o.d = make_uint4(0u, 0u, 0u, 0u);
     }
@@ -124,55 +140,29 @@ __global__ void ranges_kernel(const uint32_t* __restrict__ keys, int64_t K, uint
     if (s == K - 1 || keys[s + 1] != t) ranges[t].y = (uint32_t)(s + 1);
 }
 
-// ------------------------------------------------------------------ scatter binning
-// Per-tile lists from the per-tile lengths (counted by preprocess): tile t's list occupies
-// [off[t], off[t] + cnt[t]) == TileGrid::offsets (rasterizer.cpp:92-100). fill[t] starts at
-// off[t]; the scatter claims slots with atomics (arbitrary order inside a tile) and the
-// per-tile sort restores blend (rank) order, so the result is deterministic.
-__global__ void tile_counts_kernel(const uint32_t* __restrict__ padded, int tiles,
-                                   uint32_t* __restrict__ dense) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < tiles) dense[t] = padded[(size_t)t * kFillStride];
-}
-
-__global__ void tile_finalize_kernel(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
-                                     int tiles, uint2* __restrict__ ranges, uint32_t* __restrict__ fill,
-                                     unsigned long long* __restrict__ max_cnt) {
+// ------------------------------------------------------------------ slab binning
+// Preprocess claims every (tile, splat) slot in the tile's fixed-size slab (kSegCap entries,
+// claim order arbitrary); the per-tile sort restores blend (rank) order, so the lists are
+// deterministic and equal TileGrid's (rasterizer.cpp:92-100). A tile whose list exceeds the
+// slab makes the view take the onesweep path.
+__global__ void slab_finalize_kernel(const uint32_t* __restrict__ fill, int tiles,
+                                     uint2* __restrict__ ranges, unsigned long long* __restrict__ max_cnt) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t c = 0;
     if (t < tiles) {
-        c = cnt[t];
-        const uint32_t o = off[t];
-        ranges[t] = make_uint2(o, o + c);
-        fill[(size_t)t * kFillStride] = o;
+        c = fill[(size_t)t * kFillStride];
+        const uint32_t o = (uint32_t)t * (uint32_t)kSegCap;
+        ranges[t] = make_uint2(o, o + min(c, (uint32_t)kSegCap));
     }
     c = __reduce_max_sync(0xffffffffu, c);
     if ((threadIdx.x & 31) == 0 && c) atomicMax(max_cnt, (unsigned long long)c);
 }
 
-__global__ void __launch_bounds__(256) scatter_kernel(
-    Prepared* __restrict__ prep, const uint32_t* __restrict__ pair_off, int64_t n, int tiles_x,
-    uint32_t* __restrict__ fill, uint32_t* __restrict__ items) {
+// first partial slot of each splat (rank-major pair order) into its prepared record
+__global__ void pair_base_kernel(Prepared* __restrict__ prep, const uint32_t* __restrict__ pair_off,
+                                 int64_t n) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const uint4 d = prep[r].d;
-    if (!d.w) return;
-    prep[r].d.z = pair_off[r];  // partial-slot base of this splat (rank-major pair order)
-    const int tx0 = d.x & 0xffff, tx1 = d.x >> 16, ty0 = d.y & 0xffff;
-    const int w = tx1 - tx0 + 1, cnt = (int)d.w;
-    // four independent slot claims in flight per iteration (the atomics' latency dominates)
-    for (int i = 0; i < cnt; i += 4) {
-        uint32_t pos[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (i + u < cnt) {
-                const int q = i + u, ty = ty0 + q / w, tx = tx0 + q % w;
-                pos[u] = atomicAdd(&fill[(size_t)(ty * tiles_x + tx) * kFillStride], 1u);
-            }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (i + u < cnt) items[pos[u]] = (uint32_t)r;
-    }
+    if (r < n) prep[r].d.z = pair_off[r];
 }
 
 // Bitonic sort of 32*E keys held by one warp, lane L owning positions L*E .. L*E+E-1:
@@ -241,32 +231,23 @@ inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / b
 
 }  // namespace
 
-cudaError_t launch_tile_finalize(tgsx_ctx* ctx, int tiles) {
+cudaError_t launch_slab_finalize(tgsx_ctx* ctx, int tiles) {
     Workspace& ws = ctx->ws;
     cudaError_t e;
     if ((e = ws.ranges.ensure((size_t)std::max(tiles, 1) * sizeof(uint2)))) return e;
-    if ((e = ws.tile_fill.ensure((size_t)std::max(tiles, 1) * 4 * kFillStride))) return e;
-    unsigned long long* counters = ws.counters.as<unsigned long long>();
-    if ((e = ws.tile_dense.ensure((size_t)std::max(tiles, 1) * 4))) return e;
-    tile_counts_kernel<<<grid_for(tiles, 256), 256, 0, ctx->stream>>>(ws.tile_count.as<uint32_t>(), tiles,
-                                                                      ws.tile_dense.as<uint32_t>());
-    ctx->launches++;
-    if ((e = launch_exclusive_scan(ctx, ws.tile_dense.as<uint32_t>(), ws.tile_off.as<uint32_t>(), tiles,
-                                   nullptr)))
-        return e;
-    tile_finalize_kernel<<<grid_for(tiles, 256), 256, 0, ctx->stream>>>(
-        ws.tile_dense.as<uint32_t>(), ws.tile_off.as<uint32_t>(), tiles, ws.ranges.as<uint2>(),
-        ws.tile_fill.as<uint32_t>(), counters + 5);
+    if (tiles == 0) return cudaSuccess;
+    slab_finalize_kernel<<<grid_for(tiles, 256), 256, 0, ctx->stream>>>(
+        ws.tile_fill.as<uint32_t>(), tiles, ws.ranges.as<uint2>(), ws.counters.as<unsigned long long>() + 5);
     ctx->launches++;
     return cudaGetLastError();
 }
 
-cudaError_t launch_scatter(tgsx_ctx* ctx, tgsx_model* m, uint32_t* items) {
+cudaError_t launch_pair_base(tgsx_ctx* ctx, tgsx_model* m) {
     Workspace& ws = ctx->ws;
     const int64_t n = m->n;
     if (n == 0 || ws.K == 0) return cudaSuccess;
-    scatter_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-        ws.prep.as<Prepared>(), ws.pair_off.as<uint32_t>(), n, ws.tiles_x, ws.tile_fill.as<uint32_t>(), items);
+    pair_base_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(ws.prep.as<Prepared>(),
+                                                                ws.pair_off.as<uint32_t>(), n);
     ctx->launches++;
     return cudaGetLastError();
 }
@@ -293,16 +274,16 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
     if ((e = ws.pair_off.ensure((n + 1) * 4))) return e;
     ws.tiles_x = (W + kTile - 1) / kTile;
     ws.tiles_y = (H + kTile - 1) / kTile;
-    const size_t tb = (size_t)std::max(ws.tiles_x * ws.tiles_y, 1) * 4;
-    if ((e = ws.tile_count.ensure(tb * kFillStride))) return e;
-    if ((e = ws.tile_off.ensure(tb))) return e;
-    if ((e = cudaMemsetAsync(ws.tile_count.p, 0, tb * kFillStride, ctx->stream))) return e;
+    const size_t tiles = (size_t)std::max(ws.tiles_x * ws.tiles_y, 1);
+    if ((e = ws.tile_fill.ensure(tiles * 4 * kFillStride))) return e;
+    if ((e = ws.tile_slab.ensure(tiles * 4 * kSegCap))) return e;
+    if ((e = cudaMemsetAsync(ws.tile_fill.p, 0, tiles * 4 * kFillStride, ctx->stream))) return e;
     if (n == 0) return cudaSuccess;
     preprocess_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
         m->params.as<float>(), m->cap, n, m->rank_of.as<uint32_t>(), m->perm.as<uint32_t>(),
         m->blend_phys ? 1 : 0, lowpass_p, W, H, ws.tiles_x,
-        ws.prep.as<Prepared>(), ws.touched.as<uint32_t>(), ws.tile_count.as<uint32_t>(),
-        ws.counters.as<unsigned long long>());
+        ws.prep.as<Prepared>(), ws.touched.as<uint32_t>(), ws.tile_fill.as<uint32_t>(),
+        ws.tile_slab.as<uint32_t>(), ws.counters.as<unsigned long long>());
     ctx->launches++;
     return cudaGetLastError();
 }

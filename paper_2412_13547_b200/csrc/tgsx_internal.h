@@ -40,9 +40,8 @@ struct Workspace {
     DevBuf keys[2], vals[2];  // u32[K] ping-pong
     DevBuf sort_tmp;          // histograms + block status + tickets
     DevBuf ranges;            // uint2[tiles]
-    // scatter binning: per-tile lengths and slot cursors (one per 128-B line), dense lengths,
-    // offsets
-    DevBuf tile_count, tile_fill, tile_dense, tile_off;
+    // slab binning: per-tile slot cursors (one per 128-B line) and kSegCap-entry slabs
+    DevBuf tile_fill, tile_slab;
     DevBuf partial;           // per-(tile, splat) gradient partials, Partials SoA (40 B/pair)
     int64_t pair_cap = 0;     // pairs the partial buffer holds
     // per-pixel
@@ -174,8 +173,8 @@ cudaError_t launch_ranges(tgsx_ctx* ctx, const uint32_t* keys, int64_t K, int ti
 // scatter binning: per-tile lengths counted by preprocess -> offsets/ranges -> atomic scatter ->
 // per-tile warp register sort (lists up to kSegCap; longer lists take the onesweep path)
 constexpr int kSegCap = 1024;
-cudaError_t launch_tile_finalize(tgsx_ctx* ctx, int tiles);
-cudaError_t launch_scatter(tgsx_ctx* ctx, tgsx_model* m, uint32_t* items);
+cudaError_t launch_slab_finalize(tgsx_ctx* ctx, int tiles);
+cudaError_t launch_pair_base(tgsx_ctx* ctx, tgsx_model* m);
 cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles);
 cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
                            bool fused_loss);
