@@ -348,7 +348,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
         }
         {
             StageTimer t(ctx, kStSort);
-            CK(launch_seg_sort(ctx, v, tiles));
+            CK(launch_seg_sort(ctx, v, tiles, (int64_t)max_list));
         }
         *items = v;
         if (sorted_keys) *sorted_keys = nullptr;

@@ -210,6 +210,9 @@ __device__ __forceinline__ void warp_sort_list(uint32_t* __restrict__ list, int 
 
 // One warp per tile: the tile's ranks (claimed in arbitrary order by the scatter) sorted back
 // into blend order in registers (lists <= kSegCap = 1024).
+// MAXE: largest per-lane width instantiated (lists <= 32 * MAXE); chosen on the host from the
+// longest list, so the common case does not pay the registers of the 1024-entry network
+template <int MAXE>
 __global__ void __launch_bounds__(256) seg_sort_kernel(const uint2* __restrict__ ranges, int tiles,
                                                        uint32_t* __restrict__ items) {
     const int lane = threadIdx.x & 31;
@@ -222,9 +225,9 @@ __global__ void __launch_bounds__(256) seg_sort_kernel(const uint2* __restrict__
     if (n <= 32) warp_sort_list<1>(list, n, lane);
     else if (n <= 64) warp_sort_list<2>(list, n, lane);
     else if (n <= 128) warp_sort_list<4>(list, n, lane);
-    else if (n <= 256) warp_sort_list<8>(list, n, lane);
-    else if (n <= 512) warp_sort_list<16>(list, n, lane);
-    else warp_sort_list<32>(list, n, lane);
+    else if (MAXE <= 8 || n <= 256) warp_sort_list<MAXE < 8 ? MAXE : 8>(list, n, lane);
+    else if (MAXE <= 16 || n <= 512) warp_sort_list<MAXE < 16 ? MAXE : 16>(list, n, lane);
+    else warp_sort_list<MAXE>(list, n, lane);
 }
 
 inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / bt); }
@@ -252,9 +255,16 @@ cudaError_t launch_pair_base(tgsx_ctx* ctx, tgsx_model* m) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles) {
+cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles, int64_t max_list) {
     if (ctx->ws.K == 0 || tiles == 0) return cudaSuccess;
-    seg_sort_kernel<<<grid_for(tiles, 8), 256, 0, ctx->stream>>>(ctx->ws.ranges.as<uint2>(), tiles, items);
+    const uint2* rg = ctx->ws.ranges.as<uint2>();
+    const unsigned grid = grid_for(tiles, 8);
+    if (max_list <= 256)
+        seg_sort_kernel<8><<<grid, 256, 0, ctx->stream>>>(rg, tiles, items);
+    else if (max_list <= 512)
+        seg_sort_kernel<16><<<grid, 256, 0, ctx->stream>>>(rg, tiles, items);
+    else
+        seg_sort_kernel<32><<<grid, 256, 0, ctx->stream>>>(rg, tiles, items);
     ctx->launches++;
     return cudaGetLastError();
 }

@@ -170,12 +170,12 @@ size_t sort_scratch_bytes(int64_t n, int key_bits);
 cudaError_t sort_pairs(tgsx_ctx* ctx, uint32_t*& keys, uint32_t*& vals, uint32_t* keys_alt,
                        uint32_t* vals_alt, int64_t n, int key_bits, const uint32_t* d_hist);
 cudaError_t launch_ranges(tgsx_ctx* ctx, const uint32_t* keys, int64_t K, int tiles);
-// scatter binning: per-tile lengths counted by preprocess -> offsets/ranges -> atomic scatter ->
+// slab binning: preprocess claims slots in per-tile slabs of kSegCap entries -> ranges ->
 // per-tile warp register sort (lists up to kSegCap; longer lists take the onesweep path)
 constexpr int kSegCap = 1024;
 cudaError_t launch_slab_finalize(tgsx_ctx* ctx, int tiles);
 cudaError_t launch_pair_base(tgsx_ctx* ctx, tgsx_model* m);
-cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles);
+cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles, int64_t max_list);
 cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
                            bool fused_loss);
 cudaError_t launch_backward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items);
