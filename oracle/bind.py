@@ -189,6 +189,8 @@ def lib():
         L.or_pcg32_next.restype = C.c_uint32
         L.or_pcg32_uniform.restype = C.c_double
         L.or_l1_loss.restype = C.c_double
+        L.or_loss.restype = C.c_double
+        L.or_loss.argtypes = [f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, f32p, C.c_float, f32p]
         for fn in ("or_select_candidates", "or_cap_candidates", "or_spawn", "or_prune",
                    "or_densify_event", "or_budget_at"):
             getattr(L, fn).restype = C.c_int64
@@ -458,6 +460,18 @@ def l1_loss(rgb, p, ox, oy, W, H, target):
     g = np.zeros_like(rgb)
     loss = lib().or_l1_loss(_ptr(rgb, f32p), p, ox, oy, W, H, _ptr(target, f32p), _ptr(g, f32p))
     return loss, g
+
+
+def loss(rgb, p, ox, oy, W, H, target, ssim_weight=0.0):
+    """compute_loss: dense (p = 1) (1-w) L1 + w (1 - SSIM), dilated L1 only.
+    Returns (loss, dL/dC per active pixel)."""
+    rgb = np.ascontiguousarray(rgb, np.float32)
+    target = np.ascontiguousarray(target, np.float32)
+    g = np.zeros_like(rgb)
+    v = lib().or_loss(_ptr(rgb, f32p), p, ox, oy, W, H, _ptr(target, f32p), float(ssim_weight), _ptr(g, f32p))
+    if v < 0:
+        raise OracleError(1, "loss: bad pattern")
+    return v, g
 
 
 def adam_config(step, total_steps, diag) -> OrAdamCfg:

@@ -529,6 +529,104 @@ double or_l1_loss(const float* rgb, int p, int ox, int oy, int W, int H, const f
     return sum / (3.0 * (double)P);
 }
 
+/* ---------------------------------------------------------------- L1 + SSIM (dense) */
+/* compute_loss (loss.cpp is missing from the reference, restated): dense
+ * iterations (p = 1) use L = (1 - lam) L1 + lam (1 - SSIM), dilated ones L1 only. SSIM is the
+ * mean over pixels and channels of the 11x11 Gaussian-window (sigma 1.5, normalised) SSIM map
+ * with zero padding and C1 = 0.01^2, C2 = 0.03^2 (the 3DGS convention the SPEC names for
+ * lam = 0.2, DESIGN DECISIONS). Gradient (analytic, pinned by finite differences in
+ * tests/test_spec_kats.py): with the local statistics mu, sigma^2, sigma_xy of the window at
+ * pixel p and S = A1 A2 / (B1 B2),
+ *   dSSIM/dx_q = (1/3P) [ (G*a)(q) + 2 x_q (G*b)(q) + y_q (G*c)(q) ]
+ *   a = dS/dmu_x - 2 mu_x dS/dsxx - mu_y dS/dsxy,  b = dS/dsxx,  c = dS/dsxy.
+ * Double precision throughout (this is the checker); float in / out. */
+#define SSIM_R 5
+static void ssim_window(double g[2 * SSIM_R + 1]) {
+    double s = 0.0;
+    for (int i = -SSIM_R; i <= SSIM_R; ++i) {
+        g[i + SSIM_R] = exp(-(double)(i * i) / (2.0 * 1.5 * 1.5));
+        s += g[i + SSIM_R];
+    }
+    for (int i = 0; i < 2 * SSIM_R + 1; ++i) g[i] /= s;
+}
+
+/* separable "same" convolution with zero padding */
+static void ssim_conv(const double* in, double* out, double* tmp, int W, int H, const double* g) {
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            double acc = 0.0;
+            for (int k = -SSIM_R; k <= SSIM_R; ++k) {
+                const int xx = x + k;
+                if (xx >= 0 && xx < W) acc += g[k + SSIM_R] * in[(int64_t)y * W + xx];
+            }
+            tmp[(int64_t)y * W + x] = acc;
+        }
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            double acc = 0.0;
+            for (int k = -SSIM_R; k <= SSIM_R; ++k) {
+                const int yy = y + k;
+                if (yy >= 0 && yy < H) acc += g[k + SSIM_R] * tmp[(int64_t)yy * W + x];
+            }
+            out[(int64_t)y * W + x] = acc;
+        }
+}
+
+double or_loss(const float* rgb, int p, int ox, int oy, int W, int H, const float* target,
+               float lam, float* dLdC) {
+    if (p != 1 || !(lam > 0.0f)) return or_l1_loss(rgb, p, ox, oy, W, H, target, dLdC);
+    if (ox != 0 || oy != 0 || W < 1 || H < 1) return -1.0;
+    const int64_t P = (int64_t)W * H;
+    const double l1 = or_l1_loss(rgb, 1, 0, 0, W, H, target, dLdC);
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03, inv = 1.0 / (3.0 * (double)P);
+    double g[2 * SSIM_R + 1];
+    ssim_window(g);
+    double* buf = (double*)malloc(sizeof(double) * (size_t)P * 14);
+    double *x = buf, *y = x + P, *t = y + P, *mx = t + P, *my = mx + P, *exx = my + P, *eyy = exx + P,
+           *exy = eyy + P, *a = exy + P, *b = a + P, *c = b + P, *ga = c + P, *gb = ga + P, *gc = gb + P;
+    double ssim_sum = 0.0;
+    for (int ch = 0; ch < 3; ++ch) {
+        for (int64_t i = 0; i < P; ++i) {
+            x[i] = rgb[3 * i + ch];
+            y[i] = target[3 * i + ch];
+        }
+        ssim_conv(x, mx, t, W, H, g);
+        ssim_conv(y, my, t, W, H, g);
+        for (int64_t i = 0; i < P; ++i) a[i] = x[i] * x[i];
+        ssim_conv(a, exx, t, W, H, g);
+        for (int64_t i = 0; i < P; ++i) a[i] = y[i] * y[i];
+        ssim_conv(a, eyy, t, W, H, g);
+        for (int64_t i = 0; i < P; ++i) a[i] = x[i] * y[i];
+        ssim_conv(a, exy, t, W, H, g);
+        for (int64_t i = 0; i < P; ++i) {
+            const double sxx = exx[i] - mx[i] * mx[i], syy = eyy[i] - my[i] * my[i];
+            const double sxy = exy[i] - mx[i] * my[i];
+            const double A1 = 2.0 * mx[i] * my[i] + C1, A2 = 2.0 * sxy + C2;
+            const double B1 = mx[i] * mx[i] + my[i] * my[i] + C1, B2 = sxx + syy + C2;
+            const double S = A1 * A2 / (B1 * B2);
+            ssim_sum += S;
+            const double dmu = 2.0 * my[i] * A2 / (B1 * B2) - 2.0 * mx[i] * S / B1;
+            const double dsxx = -S / B2, dsxy = 2.0 * A1 / (B1 * B2);
+            a[i] = dmu - 2.0 * mx[i] * dsxx - my[i] * dsxy;
+            b[i] = dsxx;
+            c[i] = dsxy;
+        }
+        if (dLdC) {
+            ssim_conv(a, ga, t, W, H, g);
+            ssim_conv(b, gb, t, W, H, g);
+            ssim_conv(c, gc, t, W, H, g);
+            for (int64_t i = 0; i < P; ++i) {
+                const double dssim = inv * (ga[i] + 2.0 * x[i] * gb[i] + y[i] * gc[i]);
+                const double d = (double)rgb[3 * i + ch] - (double)target[3 * i + ch];
+                const double sgn = d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0);
+                dLdC[3 * i + ch] = (float)((1.0 - lam) * sgn * inv - lam * dssim);
+            }
+        }
+    }
+    free(buf);
+    return (1.0 - lam) * l1 + lam * (1.0 - ssim_sum * inv);
+}
+
 /* ---------------------------------------------------------------- Adam */
 /* optimizer step, SPEC.md:258-267,283-285 (source missing; restated), clamp_parameters
  * gaussian.hpp:105-116. Float arithmetic in this exact order (the GPU kernel mirrors it):

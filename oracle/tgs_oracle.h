@@ -83,6 +83,9 @@ int or_backward(or_scene* s, int p, int ox, int oy, int W, int H, const float* b
                 const float* dLdC, int lowpass_p, float* const* grads, or_screen_grads* screen,
                 int update_stats);
 
+/* compute_loss: dense (p = 1, lam > 0) (1-lam) L1 + lam (1 - SSIM), else L1 */
+double or_loss(const float* rgb, int p, int ox, int oy, int W, int H, const float* target,
+               float lam, float* dLdC);
 double or_l1_loss(const float* rgb, int p, int ox, int oy, int W, int H, const float* target,
                   float* dLdC);
 
