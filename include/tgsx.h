@@ -129,7 +129,19 @@ typedef struct {
 int32_t tgsx_adam_step(tgsx_ctx* ctx, tgsx_model* m, const float* grads,
                        const tgsx_adam_args* a);
 
-/* One fused fit iteration on one view: render -> L1 loss over active pixels
+/* compute_loss (loss.cpp is missing from the reference): for a dense pattern
+ * (p = 1) L = (1 - w) L1 + w (1 - SSIM) with the 11x11 Gaussian-window SSIM, for a dilated one
+ * L1 over the active pixels. rgb: colours by rank (active_count x 3), target: full-resolution
+ * W*H*3 (host or device). Writes the loss and dL/dC by rank (host or device, may be NULL).
+ * EINVAL on a bad pattern or w outside [0, 1]. */
+int32_t tgsx_loss(tgsx_ctx* ctx, const tgsx_pattern* pat, const float* rgb, const float* target,
+                  float ssim_weight, float* out_loss, float* out_dLdC);
+/* lambda_ssim of the fused fit views below on dense patterns (default 0: L1 only; the trainer
+ * uses its config's value, SPEC.md DESIGN DECISIONS 0.2). */
+int32_t tgsx_set_ssim_weight(tgsx_ctx* ctx, float ssim_weight);
+
+/* One fused fit iteration on one view: render -> loss (L1 over active pixels; plus the SSIM
+ * term on dense views when tgsx_set_ssim_weight > 0)
  * -> backward -> densify stats -> Adam. target: full-resolution W*H*3 float RGB, host or
  * device. A host target is copied on the context's copy stream into one of two staging
  * buffers, overlapping the previous call's kernels; the caller may reuse a pinned target

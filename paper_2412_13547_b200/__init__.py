@@ -7,10 +7,10 @@ of the reference interface (api.py). There is no CPU fallback.
 """
 from .api import (BudgetController, Context, DeviceModel, DilationPattern, GaussianModel,  # noqa: F401
                   GradientSet, Pcg32, RenderOptions, RenderOutput, Trainer, backward,
-                  budget_t_norm, densify_config, fit_power_exponent, lowpass_bump, next_offsets,
-                  render, train_config)
+                  budget_t_norm, compute_loss, densify_config, fit_power_exponent, lowpass_bump,
+                  next_offsets, render, train_config)
 
 __all__ = ["BudgetController", "Context", "DeviceModel", "DilationPattern", "GaussianModel",
            "GradientSet", "Pcg32", "RenderOptions", "RenderOutput", "Trainer", "backward",
-           "budget_t_norm", "densify_config", "fit_power_exponent", "lowpass_bump", "next_offsets",
+           "budget_t_norm", "compute_loss", "densify_config", "fit_power_exponent", "lowpass_bump", "next_offsets",
            "render", "train_config"]

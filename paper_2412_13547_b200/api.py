@@ -262,6 +262,10 @@ class Context:
     def profile(self, enable: bool = True):
         self.check(self.L.tgsx_profile(self.h, 1 if enable else 0))
 
+    def set_ssim_weight(self, weight: float):
+        """lambda_ssim of dense fused fit views (0 = L1 only)."""
+        self.check(self.L.tgsx_set_ssim_weight(self.h, float(weight)))
+
     def profile_read(self):
         n = len(self.STAGES)
         ms = (C.c_double * n)()
@@ -448,6 +452,24 @@ class DeviceModel:
 
 
 # ---------------------------------------------------------------- reference-shaped free functions
+def compute_loss(ctx: "Context", colors, target, pattern: DilationPattern, ssim_weight: float = 0.2):
+    """compute_loss(render, target, pattern, ssim_weight): dense patterns
+    (1-w) L1 + w (1 - SSIM), dilated ones L1 over the active pixels. colors: (active, 3) by
+    rank; target: (H, W, 3). Returns (loss, dL/dC by rank). ValueError on a dimension mismatch
+    or a weight outside [0, 1]."""
+    colors = _f32(colors)
+    target = _f32(target)
+    if colors.reshape(-1, 3).shape[0] != pattern.active_count():
+        raise ValueError("compute_loss: colour count does not match the pattern's ranks")
+    if target.size != pattern.width * pattern.height * 3:
+        raise ValueError("compute_loss: target size does not match the pattern's image")
+    loss = np.zeros(1, np.float32)
+    grad = np.zeros((pattern.active_count(), 3), np.float32)
+    ctx.check(ctx.L.tgsx_loss(ctx.h, C.byref(pattern.c()), _ptr(colors), _ptr(target),
+                              float(ssim_weight), _ptr(loss), _ptr(grad)))
+    return float(loss[0]), grad
+
+
 def render(model, pattern: DilationPattern, background=(0.0, 0.0, 0.0),
            opts: RenderOptions | None = None, ctx: Context | None = None) -> RenderOutput:
     """tgs::render<float> (rasterizer.hpp:58-60). `model` is a GaussianModel (uploaded for the

@@ -739,7 +739,7 @@ cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* 
     BlendParams prm = make_params(ctx, ra, items);
     if (fused_loss) {
         prm.target = ra.target;
-        prm.loss_scale = ra.P > 0 ? (float)(1.0 / (3.0 * (double)ra.P)) : 0.f;
+        prm.loss_scale = ra.P > 0 ? (float)((double)ra.l1_weight / (3.0 * (double)ra.P)) : 0.f;
     } else {
         prm.target = nullptr;
         prm.block_loss = nullptr;

@@ -143,6 +143,7 @@ RenderArgs make_args(const tgsx_pattern* pat, const float bg[3], int lowpass_p) 
     ra.bg[1] = bg ? bg[1] : 0.f;
     ra.bg[2] = bg ? bg[2] : 0.f;
     ra.lowpass_p = lowpass_p > 0 ? lowpass_p : pat->p;  // resolve_lowpass rasterizer.cpp:138
+    ra.l1_weight = 1.0f;
     return ra;
 }
 
@@ -578,21 +579,6 @@ int32_t render_core(tgsx_ctx* ctx, tgsx_model* m, const RenderArgs& ra, bool fus
     return TGSX_OK;
 }
 
-__global__ void sum_block_loss(const float* __restrict__ bl, int n, float* out) {
-    // fixed-order reduction: deterministic loss value
-    __shared__ double s[256];
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < n; i += 256) acc += (double)bl[i];
-    s[threadIdx.x] = acc;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) out[0] = (float)s[0];
-}
-
-__global__ void scale_loss(float* v, float scale) { v[0] *= scale; }
 
 int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
                    const float* target, float* out_loss, ChainMode mode, const AdamCfg* cfg) {
@@ -600,13 +586,25 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
     if (rc) return rc;
     if (!target) return fail(ctx, TGSX_EINVAL, "target is null");
     RenderArgs ra = make_args(pat, bg, 0);
+    // compute_loss: dense views add the SSIM term, dilated views are L1 only
+    const float lam = (pat->p == 1 && ctx->ssim_weight > 0.f) ? ctx->ssim_weight : 0.f;
+    ra.l1_weight = 1.0f - lam;
     Workspace& ws = ctx->ws;
     rc = stage_target(ctx, target, (size_t)ra.W * ra.H * 12, &ra.target);
     if (rc) return rc;
     uint32_t* items = nullptr;
-    rc = render_core(ctx, m, ra, true, &items);
+    rc = render_core(ctx, m, ra, true, &items);  // forward + fused (1 - lam) L1
     if (rc) return rc;
-    if ((rc = mark_target_consumed(ctx))) return rc;  // the fused L1 is the target's only reader
+    int nsb = 0;
+    if (lam > 0.f && ra.P > 0) {
+        StageTimer t(ctx, kStLoss);
+        nsb = (int)ssim_blocks(ra.W, ra.H);
+        CK(ws.ssim_abc.ensure((size_t)ra.P * 36));
+        CK(ws.ssim_part.ensure((size_t)nsb * 4));
+        CK(launch_ssim(ctx, ws.rgb.as<float>(), ra.target, ra.W, ra.H, lam, ws.ssim_abc.as<float>(),
+                       ws.ssim_part.as<float>(), ws.dLdC.as<float>()));
+    }
+    if ((rc = mark_target_consumed(ctx))) return rc;  // the loss kernels are the target's readers
     {
         StageTimer t(ctx, kStBackward);
         CK(launch_backward(ctx, ra, items));
@@ -620,9 +618,9 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
     float* dloss = reinterpret_cast<float*>(ws.counters.as<unsigned long long>() + 4);
     {
         StageTimer t(ctx, kStLoss);
-        sum_block_loss<<<1, 256, 0, ctx->stream>>>(ws.block_loss.as<float>(), tiles, dloss);
-        scale_loss<<<1, 1, 0, ctx->stream>>>(dloss, ra.P > 0 ? (float)(1.0 / (3.0 * ra.P)) : 0.f);
-        ctx->launches += 2;
+        const double inv = ra.P > 0 ? 1.0 / (3.0 * (double)ra.P) : 0.0;
+        CK(launch_loss_finalize(ctx, ws.block_loss.as<float>(), tiles, (float)((1.0 - lam) * inv),
+                                ws.ssim_part.as<float>(), nsb, lam, inv, dloss));
     }
     CK(cudaGetLastError());
     if (out_loss) {
@@ -666,7 +664,8 @@ void tgsx_destroy(tgsx_ctx* ctx) {
     DevBuf* bufs[] = {&ws.prep, &ws.touched, &ws.pair_off, &ws.scan_tmp, &ws.keys[0], &ws.keys[1],
                       &ws.vals[0], &ws.vals[1], &ws.sort_tmp, &ws.ranges, &ws.partial, &ws.rgb,
                       &ws.T, &ws.last, &ws.dLdC, &ws.target, &ws.block_loss, &ws.counters,
-                      &ws.generic, &ws.tile_fill, &ws.tile_slab};
+                      &ws.generic, &ws.tile_fill, &ws.tile_slab, &ws.ssim_abc, &ws.ssim_part,
+                      &ws.loss_grad};
     for (DevBuf* b : bufs) b->release();
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);
@@ -965,6 +964,48 @@ float* tgsx_step_buffer(tgsx_model* m, int64_t* out_floats) {
     if (!m) return nullptr;
     if (out_floats) *out_floats = (int64_t)kStepFloats * m->cap;
     return m->step.as<float>();
+}
+
+int32_t tgsx_set_ssim_weight(tgsx_ctx* ctx, float ssim_weight) {
+    if (!ctx) return TGSX_EINVAL;
+    if (!(ssim_weight >= 0.f && ssim_weight <= 1.f)) return fail(ctx, TGSX_EINVAL, "ssim weight must lie in [0, 1]");
+    ctx->ssim_weight = ssim_weight;
+    return TGSX_OK;
+}
+
+int32_t tgsx_loss(tgsx_ctx* ctx, const tgsx_pattern* pat, const float* rgb, const float* target,
+                  float ssim_weight, float* out_loss, float* out_dLdC) {
+    if (!ctx || !rgb || !target) return fail(ctx, TGSX_EINVAL, "loss: null input");
+    int32_t rc = check_pattern(ctx, pat);
+    if (rc) return rc;
+    if (!(ssim_weight >= 0.f && ssim_weight <= 1.f)) return fail(ctx, TGSX_EINVAL, "ssim weight must lie in [0, 1]");
+    RenderArgs ra = make_args(pat, nullptr, 0);
+    const float lam = pat->p == 1 ? ssim_weight : 0.f;  // dilated iterations: L1 only
+    Workspace& ws = ctx->ws;
+    ws.have_forward = false;
+    const float* d_rgb = nullptr;
+    if ((rc = stage_input(ctx, ws.rgb, rgb, (size_t)std::max(ra.P, 1) * 12, &d_rgb))) return rc;
+    if ((rc = stage_input(ctx, ws.target, target, (size_t)ra.W * ra.H * 12, &ra.target))) return rc;
+    CK(ws.loss_grad.ensure((size_t)std::max(ra.P, 1) * 12));
+    float* grad = ws.loss_grad.as<float>();
+    const double inv = ra.P > 0 ? 1.0 / (3.0 * (double)ra.P) : 0.0;
+    int n1 = 0, n2 = 0;
+    CK(ws.block_loss.ensure((size_t)std::max<int64_t>((ra.P + 255) / 256, 1) * 4));
+    CK(launch_l1(ctx, ra, d_rgb, (float)((1.0 - lam) * inv), grad, ws.block_loss.as<float>(), &n1));
+    if (lam > 0.f && ra.P > 0) {
+        n2 = (int)ssim_blocks(ra.W, ra.H);
+        CK(ws.ssim_abc.ensure((size_t)ra.P * 36));
+        CK(ws.ssim_part.ensure((size_t)n2 * 4));
+        CK(launch_ssim(ctx, d_rgb, ra.target, ra.W, ra.H, lam, ws.ssim_abc.as<float>(),
+                       ws.ssim_part.as<float>(), grad));
+    }
+    float* dloss = reinterpret_cast<float*>(ws.counters.as<unsigned long long>() + 4);
+    CK(launch_loss_finalize(ctx, ws.block_loss.as<float>(), n1, (float)((1.0 - lam) * inv),
+                            ws.ssim_part.as<float>(), n2, lam, inv, dloss));
+    if (out_loss) CK(cudaMemcpyAsync(out_loss, dloss, 4, cudaMemcpyDefault, ctx->stream));
+    if (out_dLdC && ra.P) CK(cudaMemcpyAsync(out_dLdC, grad, (size_t)ra.P * 12, cudaMemcpyDefault, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
 }
 
 int32_t tgsx_apply_step(tgsx_ctx* ctx, tgsx_model* m, int32_t batch_views, const tgsx_adam_args* a) {

@@ -47,6 +47,7 @@ struct Workspace {
     // per-pixel
     DevBuf rgb, T, last, dLdC, target;
     DevBuf block_loss;        // float[tiles]
+    DevBuf ssim_abc, ssim_part, loss_grad;  // dense SSIM adjoint weights [P][3][3], block sums
     DevBuf counters;          // u64: [0] err, [1] blend ops, [2] evals, [3..] scratch
     DevBuf generic;           // misc scratch
     // pinned host scratch
@@ -95,6 +96,7 @@ struct tgsx_ctx {
     // binning reuse: views of an unchanged model with the same geometry share one binning (the
     // tile lists do not depend on the dilation offset). Any entry point that changes the
     // parameters, the row order or the binning workspace clears bin_valid.
+    float ssim_weight = 0.f;  // lambda_ssim of dense fused views (tgsx_set_ssim_weight)
     bool bin_valid = false;
     uint64_t bin_model = 0;
     int bin_lowpass = 0, bin_W = 0, bin_H = 0;
@@ -159,6 +161,7 @@ struct RenderArgs {
     float bg[3];
     int lowpass_p;
     const float* target;  // fused L1 target (device, W*H*3) or null
+    float l1_weight;      // weight of the L1 term (1 - lambda_ssim on dense SSIM iterations)
 };
 
 cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m);
@@ -179,6 +182,14 @@ cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles, int64_t m
 cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
                            bool fused_loss);
 cudaError_t launch_backward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items);
+// compute_loss pieces (loss.cu): L1 over given colours, dense SSIM term, loss value
+cudaError_t launch_l1(tgsx_ctx* ctx, const RenderArgs& ra, const float* rgb, float scale, float* dLdC,
+                      float* block_sum, int* nblocks);
+size_t ssim_blocks(int W, int H);
+cudaError_t launch_ssim(tgsx_ctx* ctx, const float* rgb, const float* target, int W, int H, float lam,
+                        float* abc, float* block_sum, float* dLdC);
+cudaError_t launch_loss_finalize(tgsx_ctx* ctx, const float* l1_part, int n1, float w1, const float* s_part,
+                                 int n2, float lam, double inv, float* out);
 enum class ChainMode { kGrads, kAdam, kAccumulate };
 cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool update_stats,
                          float* grads_out, const float* adam_cfg);
