@@ -214,6 +214,7 @@ typedef struct {
     uint64_t seed;                    /* trainer PCG32 seed (stream 1) */
     float background[3];
     tgsx_densify_config densify;
+    float ssim_weight;                /* lambda_ssim of dense iterations (0.2, SPEC.md DESIGN) */
 } tgsx_train_config;
 
 typedef struct {

@@ -54,7 +54,7 @@ class TrainConfig(C.Structure):
                 ("batch_final_iters", C.c_int64), ("batch_size", C.c_int32),
                 ("dilation_p", C.c_int32), ("post_densify_dilation_prob", C.c_float),
                 ("n_views", C.c_int64), ("m_final", C.c_double), ("seed", C.c_uint64),
-                ("background", C.c_float * 3), ("densify", DensifyConfig)]
+                ("background", C.c_float * 3), ("densify", DensifyConfig), ("ssim_weight", C.c_float)]
 
 
 class TrainReport(C.Structure):

@@ -71,6 +71,7 @@ void tgsx_train_config_default(tgsx_train_config* c) {
     c->batch_size = 4;
     c->dilation_p = 2;
     c->post_densify_dilation_prob = 0.5f;
+    c->ssim_weight = 0.2f;                 // SPEC.md DESIGN DECISIONS (dense iterations only)
     c->n_views = 1;
     c->m_final = 0;               // 0 => 1.5 x initial count
     c->seed = 1;
@@ -82,6 +83,7 @@ int32_t tgsx_trainer_create(tgsx_ctx* ctx, tgsx_model* m, const tgsx_train_confi
                             int32_t width, int32_t height, tgsx_trainer** out) {
     if (!ctx || !m || !cfg || !out || width < 1 || height < 1) return TGSX_EINVAL;
     if (cfg->dilation_p < 1 || cfg->batch_size < 1 || cfg->densify_interval < 1) return TGSX_EINVAL;
+    if (!(cfg->ssim_weight >= 0.f && cfg->ssim_weight <= 1.f)) return TGSX_EINVAL;
     if (!(cfg->warmup_iters <= cfg->densify_until && cfg->densify_until <= cfg->total_iters))
         return TGSX_EINVAL;  // SPEC.md:552 invariants
     tgsx_trainer* tr = new (std::nothrow) tgsx_trainer();
@@ -158,8 +160,11 @@ int32_t tgsx_trainer_step(tgsx_trainer* tr, const float* const* targets, int64_t
         const int64_t idx = (t - 1) % ((int64_t)pp * pp);  // next_offsets (dilation.hpp:60-64)
         tgsx_pattern pat{pp, (int32_t)(idx % pp), (int32_t)(idx / pp), tr->W, tr->H};
         tgsx_adam_args a{++tr->adam_step, c.total_iters, std::hypot((double)tr->W, (double)tr->H)};
-        if ((rc = tgsx_fit_step(tr->ctx, tr->m, &pat, bg, targets[(t - 1) % n_targets], &a, dloss)))
-            return rc;
+        // compute_loss: dense iterations add the SSIM term
+        if ((rc = tgsx_set_ssim_weight(tr->ctx, pp == 1 ? c.ssim_weight : 0.f))) return rc;
+        rc = tgsx_fit_step(tr->ctx, tr->m, &pat, bg, targets[(t - 1) % n_targets], &a, dloss);
+        tgsx_set_ssim_weight(tr->ctx, 0.f);
+        if (rc) return rc;
         r.dilated = dilate;
     }
     tr->t = t;

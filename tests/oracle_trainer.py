@@ -48,7 +48,9 @@ def oracle_train(s, targets, cfg, W, H, iters, on_iter=None):
             idx = (t - 1) % (pp * pp)
             ox, oy = idx % pp, idx // pp
             rgb = B.render(s, pp, ox, oy, W, H, bg)[0]
-            loss, dl = B.l1_loss(rgb, pp, ox, oy, W, H, targets[(t - 1) % len(targets)])
+            # compute_loss: dense iterations add the SSIM term
+            loss, dl = B.loss(rgb, pp, ox, oy, W, H, targets[(t - 1) % len(targets)],
+                              float(np.float32(cfg.ssim_weight)) if pp == 1 else 0.0)
             g, _ = B.backward(s, pp, ox, oy, W, H, dl, bg)
             adam_t += 1
             B.adam_step(s, g, m1, m2, B.adam_config(adam_t, cfg.total_iters, diag))
