@@ -57,30 +57,42 @@ __global__ void __launch_bounds__(256) l1_kernel(const float* __restrict__ rgb, 
 }
 
 // Separable windowed sums of NM maps over a haloed tile: in[m][kHH][kHW] -> out[m][kTH][kTW].
+// Register blocking: a horizontal work item produces 4 consecutive outputs from 14 loads, a
+// thread's vertical pass produces 2 consecutive rows from 12 loads (the shared-memory pipe, not
+// the FMA pipe, bounds the naive one-load-per-tap form).
 template <int NM>
 __device__ __forceinline__ void window_sums(const float (*in)[kHH][kHW], float (*hs)[kHH][kTW],
                                             int tid, float (&out)[2][NM]) {
-    for (int i = tid; i < kHH * kTW; i += 256) {
-        const int yy = i / kTW, xx = i % kTW;
+    constexpr int kQ = kTW / 4;  // 4-wide column groups per row
+    for (int i = tid; i < kHH * kQ; i += 256) {
+        const int yy = i / kQ, x0 = 4 * (i % kQ);
 #pragma unroll
         for (int m = 0; m < NM; ++m) {
-            float acc = 0.f;
+            float v[4 + 2 * kR];
 #pragma unroll
-            for (int k = 0; k <= 2 * kR; ++k) acc = fmaf(c_win[k], in[m][yy][xx + k], acc);
-            hs[m][yy][xx] = acc;
+            for (int j = 0; j < 4 + 2 * kR; ++j) v[j] = in[m][yy][x0 + j];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                float acc = 0.f;
+#pragma unroll
+                for (int k = 0; k <= 2 * kR; ++k) acc = fmaf(c_win[k], v[o + k], acc);
+                hs[m][yy][x0 + o] = acc;
+            }
         }
     }
     __syncthreads();
-    // each thread: two output pixels (rows ty and ty + 8)
+    // each thread: two vertically consecutive output pixels (rows 2 ty, 2 ty + 1)
     const int tx = tid % kTW, ty = tid / kTW;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int oy = ty + 8 * h;
+    for (int m = 0; m < NM; ++m) {
+        float v[2 + 2 * kR];
 #pragma unroll
-        for (int m = 0; m < NM; ++m) {
+        for (int j = 0; j < 2 + 2 * kR; ++j) v[j] = hs[m][2 * ty + j][tx];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
             float acc = 0.f;
 #pragma unroll
-            for (int k = 0; k <= 2 * kR; ++k) acc = fmaf(c_win[k], hs[m][oy + k][tx], acc);
+            for (int k = 0; k <= 2 * kR; ++k) acc = fmaf(c_win[k], v[h + k], acc);
             out[h][m] = acc;
         }
     }
@@ -117,7 +129,7 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict
         const int tx = tid % kTW, ty = tid / kTW;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int gx = blockIdx.x * kTW + tx, gy = blockIdx.y * kTH + ty + 8 * h;
+            const int gx = blockIdx.x * kTW + tx, gy = blockIdx.y * kTH + 2 * ty + h;
             if (gx >= W || gy >= H) continue;
             const float mx = st[h][0], my = st[h][1];
             const float sxx = st[h][2] - mx * mx, syy = st[h][3] - my * my, sxy = st[h][4] - mx * my;
@@ -174,7 +186,7 @@ __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict_
         const int tx = tid % kTW, ty = tid / kTW;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int gx = blockIdx.x * kTW + tx, gy = blockIdx.y * kTH + ty + 8 * h;
+            const int gx = blockIdx.x * kTW + tx, gy = blockIdx.y * kTH + 2 * ty + h;
             if (gx >= W || gy >= H) continue;
             const int64_t q = 3 * ((int64_t)gy * W + gx) + ch;
             dLdC[q] -= scale * (g[h][0] + 2.f * rgb[q] * g[h][1] + target[q] * g[h][2]);
