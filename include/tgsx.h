@@ -234,6 +234,16 @@ int32_t tgsx_trainer_step(tgsx_trainer* tr, const float* const* targets, int64_t
 int32_t tgsx_trainer_losses(tgsx_trainer* tr, float* out, int64_t max_out, int64_t* out_n);
 const tgsx_budget* tgsx_trainer_budget(const tgsx_trainer* tr);
 
+/* ---------------------------------------------------------------- TGS1 checkpoint */
+/* "TGS1", u32 version, u64 count, u64 next_id, the parameter arrays in declared field order,
+ * ids, DensifyStats, Adam moments, then (when a trainer is given) the training state: iteration,
+ * Adam step, RNG, loss ring, BudgetController. Load validates magic, version and lengths:
+ * a corrupt or truncated file returns TGSX_ERUNTIME (the reference's corrupt-checkpoint
+ * error); a file carrying training state needs a trainer (created with the same config).
+ * Round trip: saving a loaded state reproduces the file byte for byte. */
+int32_t tgsx_checkpoint_save(tgsx_ctx* ctx, tgsx_model* m, const tgsx_trainer* tr, const char* path);
+int32_t tgsx_checkpoint_load(tgsx_ctx* ctx, tgsx_model* m, tgsx_trainer* tr, const char* path);
+
 /* ---------------------------------------------------------------- utilities */
 /* Seeded synthetic scene, written into caller host arrays (n entries). */
 void tgsx_synthetic_scene(uint64_t seed, int64_t n, int32_t width, int32_t height,

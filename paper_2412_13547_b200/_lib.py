@@ -110,6 +110,8 @@ SIGNATURES = {
     "tgsx_trainer_step": (C.c_int32, [vp, P(vp), C.c_int64, P(TrainReport)]),
     "tgsx_trainer_losses": (C.c_int32, [vp, f32p, C.c_int64, i64p]),
     "tgsx_trainer_budget": (vp, [vp]),
+    "tgsx_checkpoint_save": (C.c_int32, [vp, vp, vp, C.c_char_p]),
+    "tgsx_checkpoint_load": (C.c_int32, [vp, vp, vp, C.c_char_p]),
     "tgsx_synthetic_scene": (None, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, P(HostScene)]),
     "tgsx_pcg32_init": (None, [u64p, C.c_uint64, C.c_uint64]),
     "tgsx_pcg32_uniform": (C.c_double, [u64p]),

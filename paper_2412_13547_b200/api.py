@@ -15,6 +15,7 @@ densify, BudgetController).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -303,6 +304,18 @@ class DeviceModel:
         dm = DeviceModel(ctx, model.size())
         dm.upload(model)
         return dm
+
+    def save_checkpoint(self, path: str, trainer: "Trainer | None" = None):
+        """save_checkpoint: TGS1 file of the model, its moments and (with a
+        trainer) the training state."""
+        self.ctx.check(self.ctx.L.tgsx_checkpoint_save(self.ctx.h, self.h, trainer.h if trainer else None,
+                                                       os.fsencode(path)))
+
+    def load_checkpoint(self, path: str, trainer: "Trainer | None" = None):
+        """load_checkpoint: RuntimeError on a corrupt / truncated file (bad magic, version or
+        lengths); a file with training state needs the trainer to restore into."""
+        self.ctx.check(self.ctx.L.tgsx_checkpoint_load(self.ctx.h, self.h, trainer.h if trainer else None,
+                                                       os.fsencode(path)))
 
     def reserve(self, capacity: int):
         """Grow capacity and workspace to `capacity` Gaussians (no allocation while densifying

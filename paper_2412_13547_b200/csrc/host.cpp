@@ -208,3 +208,47 @@ void tgsx_synthetic_scene(uint64_t seed, int64_t n, int32_t W, int32_t H, tgsx_h
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- checkpoint state
+#include "host_state.h"
+
+namespace tgsx {
+
+void budget_write(const tgsx_budget* b, ByteWriter& w) {
+    w.put(b->n_init);
+    w.put(b->m_final);
+    w.put(b->m_adaptive);
+    w.put(b->alpha);
+    w.put(b->alpha_base);
+    w.put(b->ema);
+    w.put((uint8_t)(b->has_ema ? 1 : 0));
+    w.put(b->warmup_steps);
+    w.put(b->window_size);
+    w.put(b->refit_interval);
+    w.put(b->ma_depth);
+    w.put(b->last_refit);
+    w.put(b->lambda);
+    for (const std::vector<double>* v : {&b->log_t, &b->log_ema, &b->fits}) {
+        w.put((uint64_t)v->size());
+        w.bytes(v->data(), v->size() * sizeof(double));
+    }
+}
+
+bool budget_read(tgsx_budget* b, ByteReader& r) {
+    uint8_t has = 0;
+    if (!(r.get(b->n_init) && r.get(b->m_final) && r.get(b->m_adaptive) && r.get(b->alpha) &&
+          r.get(b->alpha_base) && r.get(b->ema) && r.get(has) && r.get(b->warmup_steps) &&
+          r.get(b->window_size) && r.get(b->refit_interval) && r.get(b->ma_depth) &&
+          r.get(b->last_refit) && r.get(b->lambda)))
+        return false;
+    b->has_ema = has != 0;
+    for (std::vector<double>* v : {&b->log_t, &b->log_ema, &b->fits}) {
+        uint64_t n = 0;
+        if (!r.get(n) || n > (uint64_t)(r.end - r.p) / sizeof(double)) return false;
+        v->resize(n);
+        if (!r.bytes(v->data(), n * sizeof(double))) return false;
+    }
+    return true;
+}
+
+}  // namespace tgsx

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/tgsx.h"
+#include "host_state.h"
 #include <cuda_runtime.h>
 
 struct tgsx_trainer {
@@ -209,3 +210,42 @@ int32_t tgsx_trainer_losses(tgsx_trainer* tr, float* out, int64_t max_out, int64
 const tgsx_budget* tgsx_trainer_budget(const tgsx_trainer* tr) { return tr ? tr->budget : nullptr; }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- checkpoint state
+namespace tgsx {
+
+void trainer_write(const tgsx_trainer* tr, ByteWriter& w) {
+    w.put(tr->t);
+    w.put(tr->adam_step);
+    w.put(tr->n_init);
+    w.put(tr->fed);
+    w.put(tr->rng[0]);
+    w.put(tr->rng[1]);
+    w.put(tr->last_budget);
+    // the device loss ring (losses not yet fed to the controller)
+    std::vector<float> ring((size_t)tr->ring);
+    cudaStream_t s = (cudaStream_t)tgsx_get_stream(tr->ctx);
+    cudaMemcpyAsync(ring.data(), tr->d_losses, sizeof(float) * ring.size(), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    w.put(tr->ring);
+    w.bytes(ring.data(), ring.size() * sizeof(float));
+    budget_write(tr->budget, w);
+}
+
+int32_t trainer_read(tgsx_trainer* tr, ByteReader& r) {
+    int64_t ring = 0;
+    if (!(r.get(tr->t) && r.get(tr->adam_step) && r.get(tr->n_init) && r.get(tr->fed) && r.get(tr->rng[0]) &&
+          r.get(tr->rng[1]) && r.get(tr->last_budget) && r.get(ring)))
+        return TGSX_ERUNTIME;
+    if (ring != tr->ring) return TGSX_ERUNTIME;  // trainer created with another densify interval
+    std::vector<float> h((size_t)ring);
+    if (!r.bytes(h.data(), h.size() * sizeof(float))) return TGSX_ERUNTIME;
+    cudaStream_t s = (cudaStream_t)tgsx_get_stream(tr->ctx);
+    if (cudaMemcpyAsync(tr->d_losses, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, s) ||
+        cudaStreamSynchronize(s))
+        return TGSX_ECUDA;
+    std::memcpy(tr->h_pinned, h.data(), sizeof(float) * h.size());
+    return budget_read(tr->budget, r) ? TGSX_OK : TGSX_ERUNTIME;
+}
+
+}  // namespace tgsx
