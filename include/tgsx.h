@@ -244,6 +244,28 @@ const tgsx_budget* tgsx_trainer_budget(const tgsx_trainer* tr);
 int32_t tgsx_checkpoint_save(tgsx_ctx* ctx, tgsx_model* m, const tgsx_trainer* tr, const char* path);
 int32_t tgsx_checkpoint_load(tgsx_ctx* ctx, tgsx_model* m, tgsx_trainer* tr, const char* path);
 
+/* ---------------------------------------------------------------- initializer */
+/* Exact k nearest neighbours (1 <= k <= 8) of every host point xy[n][2], self excluded, in
+ * ascending (dist2, index) order: KdTree2<float>::knn (kdtree.hpp:30-38) for every point, on the
+ * device (uniform-grid hash). Missing neighbours (n - 1 < k) are UINT32_MAX / +inf. out_d2 may
+ * be null. */
+int32_t tgsx_knn(tgsx_ctx* ctx, const float* xy, int64_t n, int32_t k, uint32_t* out_idx, float* out_d2);
+/* sample_seed_points: count/2 uniform points, the rest importance-sampled on the image's
+ * luminance-gradient magnitude (uniform for a flat image), jittered in their pixel; colours
+ * read at the point's pixel. image = host W*H*3 RGB; PCG32 (seed, stream 2). */
+int32_t tgsx_seed_points(const float* image, int32_t W, int32_t H, int64_t count, uint64_t seed,
+                         float* out_xy, float* out_rgb);
+/* kdtree_upsample: `rounds` times, append the midpoint of every unique {i, nearest(i)} pair
+ * (ascending pair order, exact-duplicate positions skipped). Outputs hold up to capacity
+ * points (TGSX_EINVAL when exceeded); *out_n = the final count. */
+int32_t tgsx_upsample(tgsx_ctx* ctx, const float* xy, const float* rgb, int64_t n, int32_t rounds,
+                      int64_t capacity, float* out_xy, float* out_rgb, int64_t* out_n);
+/* init_model: one Gaussian per point; isotropic log-scale of the mean 3-NN distance (image
+ * diagonal / 16 below 4 points), opacity 0.1, rotation 0, colour logit, PCG32 (seed, stream 3)
+ * depth keys. Replaces m's contents. */
+int32_t tgsx_init_model(tgsx_ctx* ctx, tgsx_model* m, const float* xy, const float* rgb, int64_t n,
+                        int32_t W, int32_t H, uint64_t seed);
+
 /* ---------------------------------------------------------------- utilities */
 /* Seeded synthetic scene, written into caller host arrays (n entries). */
 void tgsx_synthetic_scene(uint64_t seed, int64_t n, int32_t width, int32_t height,

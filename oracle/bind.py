@@ -453,6 +453,31 @@ def sorted_order(s: Scene, impl="oracle"):
     return out[:s.n]
 
 
+def knn(xy, k, impl="ref_native"):
+    """k nearest neighbours of every point, self excluded, ascending (dist2, index).
+    impl "ref_*": the reference KdTree2<float>::knn (kdtree.hpp:30-38, 96-116) per point;
+    "brute": numpy restatement of the same ordering (float32 dist2, unfused)."""
+    xy = np.ascontiguousarray(xy, np.float32).reshape(-1, 2)
+    n = xy.shape[0]
+    out = np.zeros((n, k), np.uint32)
+    if impl == "brute":
+        for i in range(n):
+            dx = xy[i, 0] - xy[:, 0]
+            dy = xy[i, 1] - xy[:, 1]
+            d2 = (dx * dx).astype(np.float32) + (dy * dy).astype(np.float32)
+            order = np.lexsort((np.arange(n), d2))
+            order = order[order != i][:k]
+            out[i, :len(order)] = order
+            out[i, len(order):] = 0xFFFFFFFF
+        return out
+    L = ref_lib(impl.split("_", 1)[1])
+    err = C.create_string_buffer(256)
+    rc = L.ref_knn_f32(_ptr(xy, f32p), C.c_int64(n), int(k), _ptr(out, u32p), err, 256)
+    if rc:
+        raise OracleError(rc)
+    return out
+
+
 # ------------------------------------------------------------------ loss / adam / densify
 def l1_loss(rgb, p, ox, oy, W, H, target):
     rgb = np.ascontiguousarray(rgb, np.float32)

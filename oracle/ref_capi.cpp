@@ -10,6 +10,7 @@
 //   tgs::backward<T> rasterizer.hpp:66-69 / rasterizer.cpp:218-361
 // Exceptions are mapped to status codes: 1 = std::invalid_argument, 2 = std::runtime_error.
 #include REF_RASTERIZER_CPP  // "/root/reference/proj/core/src/rasterizer.cpp"
+#include "tgs/kdtree.hpp"    // header-only KdTree2 (kdtree.hpp:15-139), for the initializer's kNN
 
 #include <cstdint>
 #include <cstring>
@@ -233,6 +234,22 @@ int ref_sorted_order_f32(const RefSceneF32* s, uint32_t* out, char* err, int err
             auto model = build_model(*s);
             const auto& o = model.sorted_order();
             for (size_t i = 0; i < o.size(); ++i) out[i] = o[i];
+        },
+        err, errlen);
+}
+
+// KdTree2<float>::knn (kdtree.hpp) of every point, excluding itself: out[i*k + j] = the j-th
+// nearest (ascending (dist2, index)); missing neighbours (n - 1 < k) are UINT32_MAX.
+int ref_knn_f32(const float* xy, int64_t n, int k, uint32_t* out, char* err, int errlen) {
+    return guarded(
+        [&] {
+            std::vector<tgs::Vec2<float>> pts((size_t)n);
+            for (int64_t i = 0; i < n; ++i) pts[(size_t)i] = {xy[2 * i], xy[2 * i + 1]};
+            tgs::KdTree2<float> tree(pts);
+            for (int64_t i = 0; i < n; ++i) {
+                const auto nn = tree.knn(pts[(size_t)i], k, (uint32_t)i);
+                for (int j = 0; j < k; ++j) out[i * k + j] = j < (int)nn.size() ? nn[(size_t)j] : UINT32_MAX;
+            }
         },
         err, errlen);
 }

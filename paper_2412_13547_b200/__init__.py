@@ -8,9 +8,11 @@ of the reference interface (api.py). There is no CPU fallback.
 from .api import (BudgetController, Context, DeviceModel, DilationPattern, GaussianModel,  # noqa: F401
                   GradientSet, Pcg32, RenderOptions, RenderOutput, Trainer, backward,
                   budget_t_norm, compute_loss, densify_config, fit_power_exponent, lowpass_bump,
-                  next_offsets, render, train_config)
+                  init_model, kdtree_upsample, knn, load_seed_points, next_offsets, render, sample_seed_points,
+                  train_config)
 
 __all__ = ["BudgetController", "Context", "DeviceModel", "DilationPattern", "GaussianModel",
            "GradientSet", "Pcg32", "RenderOptions", "RenderOutput", "Trainer", "backward",
            "budget_t_norm", "compute_loss", "densify_config", "fit_power_exponent", "lowpass_bump", "next_offsets",
-           "render", "train_config"]
+           "render", "train_config", "knn", "sample_seed_points", "kdtree_upsample", "init_model",
+           "load_seed_points"]

@@ -112,7 +112,12 @@ SIGNATURES = {
     "tgsx_trainer_budget": (vp, [vp]),
     "tgsx_checkpoint_save": (C.c_int32, [vp, vp, vp, C.c_char_p]),
     "tgsx_checkpoint_load": (C.c_int32, [vp, vp, vp, C.c_char_p]),
-    "tgsx_synthetic_scene": (None, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, P(HostScene)]),
+    "tgsx_knn": (C.c_int32, [vp, vp, C.c_int64, C.c_int32, vp, vp]),
+    "tgsx_seed_points": (C.c_int32, [vp, C.c_int32, C.c_int32, C.c_int64, C.c_uint64, vp, vp]),
+    "tgsx_upsample": (C.c_int32, [vp, vp, vp, C.c_int64, C.c_int32, C.c_int64, vp, vp, i64p]),
+    "tgsx_init_model": (C.c_int32, [vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32,
+                                    C.c_uint64]),
+    "tgsx_synthetic_scene":(None, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, P(HostScene)]),
     "tgsx_pcg32_init": (None, [u64p, C.c_uint64, C.c_uint64]),
     "tgsx_pcg32_uniform": (C.c_double, [u64p]),
     "tgsx_pcg32_advance": (None, [u64p, C.c_uint64]),

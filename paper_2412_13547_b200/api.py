@@ -483,6 +483,65 @@ def compute_loss(ctx: "Context", colors, target, pattern: DilationPattern, ssim_
     return float(loss[0]), grad
 
 
+# ---------------------------------------------------------------- initializer
+def knn(ctx: "Context", points, k: int):
+    """k nearest neighbours of every point (self excluded), ascending (dist2, index) like
+    KdTree2::knn (kdtree.hpp:30-38); computed on the device. Returns (idx (n, k) uint32 with
+    UINT32_MAX for missing, dist2 (n, k) float32)."""
+    pts = _f32(points).reshape(-1, 2)
+    n = pts.shape[0]
+    if not 1 <= k <= 8:
+        raise ValueError("knn: k must be in [1, 8]")
+    idx = np.zeros((n, k), np.uint32)
+    d2 = np.zeros((n, k), np.float32)
+    ctx.check(ctx.L.tgsx_knn(ctx.h, _ptr(pts), n, int(k), _ptr(idx), _ptr(d2)))
+    return idx, d2
+
+
+def sample_seed_points(image, count: int, seed: int = 0):
+    """sample_seed_points(target, count, seed): half uniform, half gradient-importance points
+    with the colour under each. image: (H, W, 3) float. Returns (xy (count, 2), rgb (count, 3))."""
+    img = _f32(image)
+    H, W = img.shape[0], img.shape[1]
+    xy = np.zeros((count, 2), np.float32)
+    rgb = np.zeros((count, 3), np.float32)
+    rc = _lib.load().tgsx_seed_points(_ptr(img), W, H, int(count), int(seed), _ptr(xy), _ptr(rgb))
+    if rc:
+        raise ValueError("sample_seed_points: invalid image or count")
+    return xy, rgb
+
+
+def load_seed_points(path: str):
+    """External seed-point file: one "x y r g b" line per point."""
+    a = np.loadtxt(path, dtype=np.float64, ndmin=2)
+    if a.shape[1] != 5:
+        raise ValueError("seed-point file: expected 5 columns (x y r g b)")
+    return a[:, :2].astype(np.float32), a[:, 2:].astype(np.float32)
+
+
+def kdtree_upsample(ctx: "Context", points, colors, rounds: int, capacity: int | None = None):
+    """kdtree_upsample(points, colors, rounds): appends nearest-neighbour midpoints per round."""
+    pts = _f32(points).reshape(-1, 2)
+    cols = _f32(colors).reshape(-1, 3)
+    n = pts.shape[0]
+    cap = capacity if capacity is not None else n << max(0, int(rounds))
+    oxy = np.zeros((max(cap, n), 2), np.float32)
+    orgb = np.zeros((max(cap, n), 3), np.float32)
+    on = C.c_int64(0)
+    ctx.check(ctx.L.tgsx_upsample(ctx.h, _ptr(pts), _ptr(cols), n, int(rounds), int(max(cap, n)),
+                                  _ptr(oxy), _ptr(orgb), C.byref(on)))
+    return oxy[:on.value].copy(), orgb[:on.value].copy()
+
+
+def init_model(dm: "DeviceModel", points, colors, width: int, height: int, seed: int = 0):
+    """init_model(points, colors, W, H, seed) into a DeviceModel (replacing its contents)."""
+    pts = _f32(points).reshape(-1, 2)
+    cols = _f32(colors).reshape(-1, 3)
+    dm.ctx.check(dm.ctx.L.tgsx_init_model(dm.ctx.h, dm.h, _ptr(pts), _ptr(cols), pts.shape[0],
+                                          int(width), int(height), int(seed)))
+    return dm
+
+
 def render(model, pattern: DilationPattern, background=(0.0, 0.0, 0.0),
            opts: RenderOptions | None = None, ctx: Context | None = None) -> RenderOutput:
     """tgs::render<float> (rasterizer.hpp:58-60). `model` is a GaussianModel (uploaded for the
