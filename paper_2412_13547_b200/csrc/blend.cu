@@ -39,9 +39,6 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kRec = 48;        // bytes per staged splat record
-constexpr int kRecStride = 36;  // floats per row of the phase-1 records: 32 pixels + 4 pad, so
-                                // row writes (fixed row, lane = pixel) and row-per-lane LDS.128
-                                // reads (lane i reads row i) are both bank-conflict-free
 constexpr int kWPB = 4;         // warps (tiles) per CTA
 
 struct BlendParams {
@@ -110,20 +107,17 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t v) {
     return v;
 }
 
-// Stages one prepared splat as a 48-byte record and returns its tile mask:
-//   +0 (mean x, mean y, ka, kb)  +16 (kc, alpha, r, g)  +32 (b, -)
+// Stages one prepared splat (and its pair slot) as a 48-byte record:
+//   +0 (mean x, mean y, ka, kb)  +16 (kc, alpha, r, g)  +32 (b, tile mask, pair slot, -)
 // (ka, kb, kc) = (inv00, 2 inv01, inv11) * kNegHalfLog2e; mask = active cols | rows << 16.
-__device__ __forceinline__ uint32_t stage_splat(const Prepared& P, const TileGeo& g, int p,
-                                                uint32_t dst, float4& a_out, float4& b_out) {
+__device__ __forceinline__ void stage_splat(const Prepared& P, const TileGeo& g, int p, uint32_t slot,
+                                            uint32_t dst) {
     const float4 a = P.a, b = P.b, c = P.c;
     const uint32_t mask =
         box_mask(a.x, b.z, g.ax, p, g.acols) | (box_mask(a.y, b.w, g.ay, p, g.arows) << 16);
-    a_out = make_float4(a.x, a.y, __fmul_rn(a.z, kNegHalfLog2e), __fmul_rn(a.w * 2.0f, kNegHalfLog2e));
-    b_out = make_float4(__fmul_rn(b.x, kNegHalfLog2e), b.y, c.x, c.y);
-    sts_f4(dst, a_out);
-    sts_f4(dst + 16, b_out);
-    sts_f1(dst + 32, c.z);
-    return mask;
+    sts_f4(dst, make_float4(a.x, a.y, __fmul_rn(a.z, kNegHalfLog2e), __fmul_rn(a.w * 2.0f, kNegHalfLog2e)));
+    sts_f4(dst + 16, make_float4(__fmul_rn(b.x, kNegHalfLog2e), b.y, c.x, c.y));
+    sts_f4(dst + 32, make_float4(c.z, __uint_as_float(mask), __uint_as_float(slot), 0.f));
 }
 
 // ------------------------------------------------------------------------ forward (pairs)
@@ -343,16 +337,23 @@ __device__ __forceinline__ uint32_t pair_slot(const Prepared& P, int tx, int ty)
     return d.z + (uint32_t)((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
 }
 
+constexpr int kSubRows = 16;  // union rows per phase-1 / phase-2 round
+
+// Per-warp shared memory of the backward. Pixel layout of an 8x8 group: lane l owns the two
+// vertically adjacent pixels (col l&7, rows 2(l>>3), 2(l>>3)+1) = pixel slots 2l (A), 2l+1 (B).
+// Record rows hold the 64 pixel slots as 16 chunks of 16 B; chunk c of row r sits at physical
+// chunk c ^ (r & 3) (XOR swizzle: phase-1 row writes and the phase-2 row-per-lane-pair reads
+// are both bank-conflict-free without padding).
 template <int NG>
 struct BwdWarpSmem {
-    float rec_u[32 * kRecStride];  // phase-1 records [union row][pixel]
-    float rec_w[32 * kRecStride];
-    float2 st[NG][32];             // per-pixel (T, g.S) carried across chunks
-    uint8_t klist[48];             // union splats of the current group in visiting order (+pad,
-                                   // keeps the float4-read members below 16-byte aligned)
-    float lg[2][4][32];            // (last, dL/dC) of the current / next group, planar; filled by
-                                   // cp.async one group ahead (phase 2 broadcasts dL/dC from here)
+    float rec_u[kSubRows * 64];  // phase-1 records u = dL/dsigma * G   [row][slot]
+    float rec_w[kSubRows * 64];  //                  w = blend weight
+    float4 st[NG][32];           // per lane (T_A, g.S_A, T_B, g.S_B) carried across chunks
+    float lg[2][4][64];          // (last, dL/dC r, g, b) per slot of the current / next group,
+                                 // filled by cp.async one group ahead
     unsigned char rec[32 * kRec];
+    uint8_t klist[2][48];        // per half (lanes 0-15 / 16-31): union splats in visiting order,
+                                 // padded to the longer half with a splat outside the union
 };
 
 // 4-byte global -> shared async copy (zero-fill when src_bytes == 0)
@@ -366,60 +367,60 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Phase-2 sums of one record row over NPR pixel rows of an 8x4 group, starting at pixel row
-// eta0 + 1.5 (u, w at ur / wr, dL/dC planar at gb; all pre-offset to that pixel row):
+__device__ __forceinline__ float2 neg2(float2 v) { return make_float2(-v.x, -v.y); }
+
+// Phase-2 sums of one record row over half of an 8x8 group (lane half h: pixel rows 4h..4h+3),
+// u / w row at rowp (byte address of the row's first chunk), dL/dC planar at gbase:
 // acc += (sum u, sum u xi, sum u eta, sum u xi^2, sum u xi eta, sum u eta^2, sum w g0..g2),
-// xi / eta the pixel offsets from the group centre. Separable: per pixel row accumulate
-// R = sum u, Rx = sum u xi, Rxx = sum u xi^2 over its 8 columns, then fold the row in with eta.
-// Column pairs (2k, 2k+1) sit in register pairs: with xi_{2k+1} = xi_{2k} + 1 and the pair sums
-// P = sum u, X = sum xi_{2k} u, Q = sum xi_{2k}^2 u (FADD2 / FFMA2, scalar weights broadcast),
-// R = P.x+P.y, Rx = X.x+X.y+P.y, Rxx = Q.x+Q.y+2 X.y+P.y; the colour sums are FFMA2 as well.
-template <int NPR>
-__device__ __forceinline__ void row_sums(uint32_t ur, uint32_t wr, uint32_t gb, float prow0,
-                                         float (&acc)[9]) {
+// xi / eta = pixel offsets from the group centre (3.5, 3.5). Step s reads logical chunk
+// 8h + (s ^ 4h) (row pair 2h + ((s>>2) ^ h), columns 2(s&3), 2(s&3)+1); a chunk holds
+// (col c, row y), (c, y+1), (c+1, y), (c+1, y+1). Separable: per row pair accumulate packed
+// (rows y, y+1) R = sum u, X = sum xi u, Q = sum xi^2 u over the columns, then fold with eta.
+__device__ __forceinline__ void half_sums(uint32_t rowp, int ukey, uint32_t gbase, int h,
+                                          float (&acc)[9]) {
     float2 c0p = make_float2(0.f, 0.f), c1p = c0p, c2p = c0p;
 #pragma unroll
-    for (int row = 0; row < NPR; ++row) {
+    for (int rp = 0; rp < 2; ++rp) {
         float2 Rp = make_float2(0.f, 0.f), Xp = Rp, Qp = Rp;
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int l4 = 2 * row + half;
-            const float4 u4 = lds_f4(ur + 16 * l4);
-            const float4 w4 = lds_f4(wr + 16 * l4);
-            const float4 g0 = lds_f4(gb + 16 * l4);  // broadcasts
-            const float4 g1 = lds_f4(gb + 128 + 16 * l4);
-            const float4 g2 = lds_f4(gb + 256 + 16 * l4);
-            const float xa = (float)(4 * half) - 3.5f, xb = xa + 2.0f;  // xi of cols 4h, 4h+2
-            const float2 ua = make_float2(u4.x, u4.y), ub = make_float2(u4.z, u4.w);
-            Rp = __fadd2_rn(Rp, ua);
-            Rp = __fadd2_rn(Rp, ub);
-            Xp = __ffma2_rn(ua, make_float2(xa, xa), Xp);
-            Xp = __ffma2_rn(ub, make_float2(xb, xb), Xp);
-            Qp = __ffma2_rn(ua, make_float2(xa * xa, xa * xa), Qp);
-            Qp = __ffma2_rn(ub, make_float2(xb * xb, xb * xb), Qp);
-            c0p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g0.x, g0.y), c0p);
-            c0p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g0.z, g0.w), c0p);
-            c1p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g1.x, g1.y), c1p);
-            c1p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g1.z, g1.w), c1p);
-            c2p = __ffma2_rn(make_float2(w4.x, w4.y), make_float2(g2.x, g2.y), c2p);
-            c2p = __ffma2_rn(make_float2(w4.z, w4.w), make_float2(g2.z, g2.w), c2p);
+        for (int cs = 0; cs < 4; ++cs) {
+            const int s = 4 * rp + cs;
+            const uint32_t ua = rowp + (uint32_t)((s ^ ukey) << 4);
+            const float4 u4 = lds_f4(ua);
+            const float4 w4 = lds_f4(ua + kSubRows * 64 * 4);
+            const uint32_t ga = gbase + (uint32_t)((s ^ (4 * h)) << 4);
+            const float4 g0 = lds_f4(ga);  // two distinct addresses per quarter warp (broadcast)
+            const float4 g1 = lds_f4(ga + 256);
+            const float4 g2 = lds_f4(ga + 512);
+            const float xa = (float)(2 * cs) - 3.5f, xb = xa + 1.0f;
+            const float2 uA = make_float2(u4.x, u4.y), uB = make_float2(u4.z, u4.w);
+            Rp = __fadd2_rn(Rp, uA);
+            Rp = __fadd2_rn(Rp, uB);
+            Xp = __ffma2_rn(uA, make_float2(xa, xa), Xp);
+            Xp = __ffma2_rn(uB, make_float2(xb, xb), Xp);
+            Qp = __ffma2_rn(uA, make_float2(xa * xa, xa * xa), Qp);
+            Qp = __ffma2_rn(uB, make_float2(xb * xb, xb * xb), Qp);
+            const float2 wA = make_float2(w4.x, w4.y), wB = make_float2(w4.z, w4.w);
+            c0p = __ffma2_rn(wA, make_float2(g0.x, g0.y), c0p);
+            c0p = __ffma2_rn(wB, make_float2(g0.z, g0.w), c0p);
+            c1p = __ffma2_rn(wA, make_float2(g1.x, g1.y), c1p);
+            c1p = __ffma2_rn(wB, make_float2(g1.z, g1.w), c1p);
+            c2p = __ffma2_rn(wA, make_float2(g2.x, g2.y), c2p);
+            c2p = __ffma2_rn(wB, make_float2(g2.z, g2.w), c2p);
         }
-        const float R = Rp.x + Rp.y;
-        const float Rx = Xp.x + Xp.y + Rp.y;
-        const float Rxx = Qp.x + Qp.y + 2.0f * Xp.y + Rp.y;
-        const float eta = prow0 + (float)row - 1.5f;
+        const float eta = (float)(4 * h + 2 * (rp ^ h)) - 3.5f;  // row y; Rp.y is row y + 1
+        const float R = Rp.x + Rp.y, X = Xp.x + Xp.y;
         acc[0] += R;
-        acc[1] += Rx;
-        acc[2] = __fmaf_rn(R, eta, acc[2]);
-        acc[3] += Rxx;
-        acc[4] = __fmaf_rn(Rx, eta, acc[4]);
-        acc[5] = __fmaf_rn(R, eta * eta, acc[5]);
+        acc[1] += X;
+        acc[2] += __fmaf_rn(R, eta, Rp.y);
+        acc[3] += Qp.x + Qp.y;
+        acc[4] += __fmaf_rn(X, eta, Xp.y);
+        acc[5] += __fmaf_rn(Rp.x, eta * eta, Rp.y * ((eta + 1.f) * (eta + 1.f)));
     }
     acc[6] += c0p.x + c0p.y;
     acc[7] += c1p.x + c1p.y;
     acc[8] += c2p.x + c2p.y;
 }
-
 
 template <int NGX, int NGY>
 __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSmem<NGX * NGY>& S,
@@ -433,37 +434,39 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
     const uint32_t rbase = smem_addr(S.rec);
     const uint32_t ubase = smem_addr(S.rec_u);
     const uint32_t wbase = smem_addr(S.rec_w);
+    const int cxl = lane & 7, ryl = 2 * (lane >> 3);  // lane's column / first row in a group
 
     uint32_t maxlast = 0;
 #pragma unroll 1
     for (int g = 0; g < NG; ++g) {
-        const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
-        const bool valid = lx < geo.acols && ly < geo.arows;
-        const int x = geo.ax + lx * p, y = geo.ay + ly * p;
-        float T = 1.f, gS = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
-        uint32_t last = 0;
-        if (valid) {
-            const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
-            T = prm.T[r];
-            last = prm.last[r];
-            g0 = prm.dLdC[3 * r];
-            g1 = prm.dLdC[3 * r + 1];
-            g2 = prm.dLdC[3 * r + 2];
-            // g . S with S = background * trans_final (rasterizer.cpp:267)
-            gS = g0 * (prm.bg0 * T) + g1 * (prm.bg1 * T) + g2 * (prm.bg2 * T);
+        const int lx = (g % NGX) * 8 + cxl, lyA = (g / NGX) * 8 + ryl;
+        float4 st = make_float4(1.f, 0.f, 1.f, 0.f);
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int ly = lyA + b;
+            if (lx < geo.acols && ly < geo.arows) {
+                const int x = geo.ax + lx * p, y = geo.ay + ly * p;
+                const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
+                const float T = prm.T[r];
+                // g . S with S = background * trans_final (rasterizer.cpp:267)
+                const float gS = prm.dLdC[3 * r] * (prm.bg0 * T) + prm.dLdC[3 * r + 1] * (prm.bg1 * T) +
+                                 prm.dLdC[3 * r + 2] * (prm.bg2 * T);
+                if (b == 0) st.x = T, st.y = gS;
+                else st.z = T, st.w = gS;
+                maxlast = max(maxlast, prm.last[r]);
+            }
         }
-        S.st[g][lane] = make_float2(T, gS);
-        maxlast = max(maxlast, last);
+        S.st[g][lane] = st;
     }
     maxlast = __reduce_max_sync(kFull, maxlast);
     // moments about the tile's active-pixel centre (pixel-centre coordinates): active pixel
     // (cx, cy) sits at (ctr_x + (cx - hx) p, ctr_y + (cy - hy) p)
-    constexpr float hx = 0.5f * (NGX * 8 - 1), hy = 0.5f * (NGY * 4 - 1);
+    constexpr float hx = 0.5f * (NGX * 8 - 1), hy = 0.5f * (NGY * 8 - 1);
     const float fp = (float)p;
     const float ctr_x = (float)geo.ax + 0.5f + hx * fp;
     const float ctr_y = (float)geo.ay + 0.5f + hy * fp;
-    const float fxl = (float)(geo.ax + (lane & 7) * p) + 0.5f;  // group (0,0) pixel centre
-    const float fyl = (float)(geo.ay + (lane >> 3) * p) + 0.5f;
+    const float fxl = (float)(geo.ax + cxl * p) + 0.5f;  // group (0,0) pixel centres (A, B)
+    const float fyl = (float)(geo.ay + ryl * p) + 0.5f;
 
     // list entries past every pixel's last contributor: zero partials
     for (int j = (int)maxlast + lane; j < count; j += 32) {
@@ -478,19 +481,29 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
     // dense rank of active pixel (lx, ly) = rank0 + ly * cols + lx (ax, ay are active pixels)
     const int rank0 = ((geo.ay - prm.oy) / p) * prm.cols + (geo.ax - prm.ox) / p;
     auto prefetch = [&](int g, int buf) {
-        const int lx = (g % NGX) * 8 + (lane & 7), ly = (g / NGX) * 4 + (lane >> 3);
-        const bool valid = lx < geo.acols && ly < geo.arows;
-        const int r = valid ? rank0 + ly * prm.cols + lx : 0;
-        const uint32_t nb = valid ? 4u : 0u;
-        const uint32_t d = lgbase + 512u * (uint32_t)buf + 4u * (uint32_t)lane;
-        cp_async4(d, prm.last + r, nb);
-        cp_async4(d + 128, prm.dLdC + 3 * r, nb);
-        cp_async4(d + 256, prm.dLdC + 3 * r + 1, nb);
-        cp_async4(d + 384, prm.dLdC + 3 * r + 2, nb);
+        const int lx = (g % NGX) * 8 + cxl, lyA = (g / NGX) * 8 + ryl;
+        const bool vA = lx < geo.acols && lyA < geo.arows, vB = lx < geo.acols && lyA + 1 < geo.arows;
+        const int rA = vA ? rank0 + lyA * prm.cols + lx : 0;
+        const int rB = vB ? rA + prm.cols : 0;
+        const uint32_t nA = vA ? 4u : 0u, nB = vB ? 4u : 0u;
+        const uint32_t d = lgbase + 1024u * (uint32_t)buf + 8u * (uint32_t)lane;
+        cp_async4(d, prm.last + rA, nA);
+        cp_async4(d + 4, prm.last + rB, nB);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            cp_async4(d + 256 * (c + 1), prm.dLdC + 3 * rA + c, nA);
+            cp_async4(d + 256 * (c + 1) + 4, prm.dLdC + 3 * rB + c, nB);
+        }
         cp_async_commit();
     };
     int buf = 0;
     prefetch(0, 0);
+
+    // phase-1 record offsets of this lane's slot pair in a row r: chunk (lane >> 1) ^ (r & 3)
+    const uint32_t soff0 = (uint32_t)((lane >> 1) << 4) + (uint32_t)((lane & 1) << 3);
+    // phase-2 role: lane = 2 i + h reads row i, half h
+    const int p2row = lane >> 1, p2h = lane & 1;
+    const int ukey = (4 * p2h) | (p2row & 3);
 
     const int nch = ((int)maxlast + 31) / 32;
     for (int ch = nch - 1; ch >= 0; --ch) {
@@ -498,15 +511,15 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
         const int j = c0 + lane;
         const bool jvalid = j < (int)maxlast;
         __syncwarp();
-        uint32_t mask = 0, slot = 0;
-        float4 ja = make_float4(0.f, 0.f, 0.f, 0.f), jb = make_float4(0.f, 0.f, 0.f, 0.f);
         // the next (earlier) chunk's list entry, loaded alongside this chunk's: its prepared
         // record is prefetched into L2 below, hiding the DRAM latency of the next staging
         const uint32_t nxt = ch > 0 ? prm.items[range.x + j - 32] : 0u;
+        const uint32_t myrec = rbase + lane * kRec;  // lane j's splat: mask, slot re-read from here
         if (jvalid) {
             const Prepared& P = prm.prep[prm.items[range.x + j]];
-            mask = stage_splat(P, geo, p, rbase + lane * kRec, ja, jb);
-            slot = pair_slot(P, geo.tx, geo.ty);
+            stage_splat(P, geo, p, pair_slot(P, geo.tx, geo.ty), myrec);
+        } else {
+            sts_f4(myrec + 32, make_float4(0.f, 0.f, 0.f, 0.f));  // empty mask
         }
         if (ch > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(prm.prep + nxt));
         __syncwarp();
@@ -520,116 +533,141 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
             buf ^= 1;
             __syncwarp();  // the previous group's phase 2 is done with the rows and lg[buf]
             prefetch(g + 1 < NG ? g + 1 : 0, buf);
-            uint32_t col = transpose32(group_rowmask(mask, gx, gy));
+            // pass matrix of the group (rasterizer.cpp:116-118): lane l, pixel A / B
+            const uint32_t mask = __float_as_uint(lds_f1(myrec + 36));
+            const uint32_t xb = (mask >> (gx * 8)) & 0xffu, yb = (mask >> (16 + gy * 8)) & 0xffu;
+            uint32_t colA = transpose32(xb * spread_even4(yb));
+            uint32_t colB = transpose32(xb * spread_even4(yb >> 1));
             cp_async_wait<1>();
             __syncwarp();
-            const uint32_t glast = __float_as_uint(S.lg[cur][0][lane]);
-            const float4 gv = make_float4(S.lg[cur][1][lane], S.lg[cur][2][lane], S.lg[cur][3][lane], 0.f);
-            // only splats before this pixel's last contributor were blended
-            const int span = (int)glast - c0;
-            col &= span <= 0 ? 0u : (span >= 32 ? kFull : ((1u << span) - 1u));
-            // The union of the group's walked splats (warp-uniform) is visited back to front with
-            // all lanes on the same splat: record reads are broadcasts, and every visited splat
-            // gets a DENSE record row (row r = r-th highest union splat; pixels that do not blend
-            // it store 0), so no row is ever cleared and phase 2 reads only U = |union| rows.
-            const uint32_t un = __reduce_or_sync(kFull, col);
-            if (!un) continue;
-            const int U = __popc(un);
-            float2 st = S.st[g][lane];
-            float T = st.x, gS = st.y;
-            const float fxg = fxl + (float)(gx * 8 * p), fyg = fyl + (float)(gy * 4 * p);
+            const uint32_t lgc = lgbase + 1024u * (uint32_t)cur + 8u * (uint32_t)lane;
+            const float2 lastp = lds_f2(lgc);
+            // only splats before each pixel's last contributor were blended
+            const int spA = (int)__float_as_uint(lastp.x) - c0, spB = (int)__float_as_uint(lastp.y) - c0;
+            colA &= spA <= 0 ? 0u : (spA >= 32 ? kFull : ((1u << spA) - 1u));
+            colB &= spB <= 0 ? 0u : (spB >= 32 ? kFull : ((1u << spB) - 1u));
+            // Each half of the group (8x4 pixels, lanes 0-15 / 16-31) visits the union of its
+            // pixels' walked splats back to front, both halves in lockstep (row r = the r-th
+            // splat of each half's union): record reads are broadcasts per half, and every row
+            // is DENSE (pixels that do not blend the row's splat store 0), so phase 2 reads only
+            // max(U0, U1) rows. The shorter half runs on a splat outside its union (G = 0).
+            const uint32_t cu = colA | colB;
+            const uint32_t un0 = __reduce_or_sync(kFull, lane < 16 ? cu : 0u);
+            const uint32_t un1 = __reduce_or_sync(kFull, lane < 16 ? 0u : cu);
+            if (!(un0 | un1)) continue;
+            const int U0 = __popc(un0), U1 = __popc(un1);
+            const int U = max(U0, U1);
+            const float2 g0p = lds_f2(lgc + 256), g1p = lds_f2(lgc + 512), g2p = lds_f2(lgc + 768);
+            const float4 st = S.st[g][lane];
+            float2 T = make_float2(st.x, st.z), gS = make_float2(st.y, st.w);
+            const float fx = fxl + (float)(gx * 8 * p), fyA = fyl + (float)(gy * 8 * p), fyB = fyA + fp;
             uint32_t visb = 0;
-            // phase 1: per pixel, back to front, two union splats per iteration (k1 > k2): the
-            // Gaussians / reciprocals are independent (ILP); only the T and g.S recursions are
-            // serial. A lane whose pixel does not blend a splat computes on it and discards.
             // union splats in visiting order: row r <- splat k_r (lane j owns row popc(un >> j+1))
-            if ((un >> lane) & 1u) S.klist[__popc(un & (0xfffffffeu << lane))] = (uint8_t)lane;
+            const int row0 = __popc(un0 & (0xfffffffeu << lane)), row1 = __popc(un1 & (0xfffffffeu << lane));
+            const bool in0 = (un0 >> lane) & 1u, in1 = (un1 >> lane) & 1u;
+            if (in0) S.klist[0][row0] = (uint8_t)lane;
+            if (in1) S.klist[1][row1] = (uint8_t)lane;
+            if (U0 + lane < U) S.klist[0][U0 + lane] = (uint8_t)(__ffs(~un0) - 1);
+            if (U1 + lane < U) S.klist[1][U1 + lane] = (uint8_t)(__ffs(~un1) - 1);
             __syncwarp();
-            uint32_t rowp = 4u * (uint32_t)lane;  // byte offset of (row r, this pixel)
-            int k1n = S.klist[0], k2n = S.klist[1];  // next pair, loaded one iteration ahead
-            for (int r = 0; r < U; r += 2) {
-                const bool two = r + 1 < U;
-                const int k1 = k1n;
-                const int k2 = two ? k2n : k1;
-                k1n = S.klist[r + 2];
-                k2n = S.klist[r + 3];
-                const bool h1 = (col >> k1) & 1u;
-                const bool h2 = two && ((col >> k2) & 1u);
-                const uint32_t ad1 = rbase + k1 * kRec, ad2 = rbase + k2 * kRec;
-                const float4 a1 = lds_f4(ad1), a2 = lds_f4(ad2);
-                const float4 b1 = lds_f4(ad1 + 16), b2 = lds_f4(ad2 + 16);
-                const float cz1 = lds_f1(ad1 + 32), cz2 = lds_f1(ad2 + 32);
-                // a pixel that does not blend a splat sees G = 0: sigma = 0, inv_rest = 1, so
-                // T, g.S pass through unchanged and the records u, w are 0 (no selects needed)
-                const float G1 = h1 ? conic_gauss(a1.z, a1.w, b1.x, __fsub_rn(fxg, a1.x), __fsub_rn(fyg, a1.y)) : 0.f;
-                const float G2 = h2 ? conic_gauss(a2.z, a2.w, b2.x, __fsub_rn(fxg, a2.x), __fsub_rn(fyg, a2.y)) : 0.f;
-                const float s1 = __fmul_rn(b1.y, G1), s2 = __fmul_rn(b2.y, G2);
-                const float ir1 = h1 ? fast_rcp(__fsub_rn(1.0f, s1)) : 1.0f;  // inv_rest
-                const float ir2 = h2 ? fast_rcp(__fsub_rn(1.0f, s2)) : 1.0f;
-                const float gc1 = gv.x * b1.z + gv.y * b1.w + gv.z * cz1;
-                const float gc2 = gv.x * b2.z + gv.y * b2.w + gv.z * cz2;
-                // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
-                const float T1 = T * ir1;
-                const float w1 = s1 * T1;
-                const float ds1 = T1 * gc1 - gS * ir1;
-                const float gS1 = __fmaf_rn(gc1, w1, gS);
-                const float T2 = T1 * ir2;
-                const float w2 = s2 * T2;
-                const float ds2 = T2 * gc2 - gS1 * ir2;
-                T = T2;
-                gS = __fmaf_rn(gc2, w2, gS1);
-                sts_f1(ubase + rowp, ds1 * G1);
-                sts_f1(wbase + rowp, w1);
-                if (two) {
-                    sts_f1(ubase + rowp + 4 * kRecStride, ds2 * G2);
-                    sts_f1(wbase + rowp + 4 * kRecStride, w2);
+            const uint8_t* kl = S.klist[lane >> 4];
+            const float dxg = (float)(gx * 8) + 3.5f - hx, dyg = (float)(gy * 8) + 3.5f - hy;
+            const uint32_t gb = lgbase + 1024u * (uint32_t)cur + 256u + 128u * (uint32_t)p2h;
+            for (int rb = 0; rb < U; rb += kSubRows) {
+                const int re = min(U, rb + kSubRows);
+                // phase 1: per pixel pair, back to front, two union splats per iteration (k1 > k2):
+                // Gaussians / reciprocals are independent (ILP); only the T and g.S recursions are
+                // serial. A pixel that does not blend a splat computes on it with G = 0
+                // (sigma = 0, 1 / (1 - sigma) = 1: T, g.S pass through; records u = w = 0).
+                int k1n = kl[rb], k2n = kl[rb + 1];  // next pair, one iteration ahead
+                uint32_t rowb = 0;  // byte offset of row (r - rb)
+                for (int r = rb; r < re; r += 2) {
+                    const bool two = r + 1 < re;
+                    const int k1 = k1n;
+                    const int k2 = two ? k2n : k1;
+                    k1n = kl[r + 2];
+                    k2n = kl[r + 3];
+                    const bool hA1 = (colA >> k1) & 1u, hB1 = (colB >> k1) & 1u;
+                    const bool hA2 = two && ((colA >> k2) & 1u), hB2 = two && ((colB >> k2) & 1u);
+                    const uint32_t ad1 = rbase + k1 * kRec, ad2 = rbase + k2 * kRec;
+                    const float4 a1 = lds_f4(ad1), a2 = lds_f4(ad2);
+                    const float4 b1 = lds_f4(ad1 + 16), b2 = lds_f4(ad2 + 16);
+                    const float cz1 = lds_f1(ad1 + 32), cz2 = lds_f1(ad2 + 32);
+                    const float2 e1 = pair_quad(a1, b1.x, fx, fyA, fyB);
+                    const float2 e2 = pair_quad(a2, b2.x, fx, fyA, fyB);
+                    const float2 G1 = make_float2(hA1 ? fast_exp2(e1.x) : 0.f, hB1 ? fast_exp2(e1.y) : 0.f);
+                    const float2 G2 = make_float2(hA2 ? fast_exp2(e2.x) : 0.f, hB2 ? fast_exp2(e2.y) : 0.f);
+                    const float2 s1 = __fmul2_rn(make_float2(b1.y, b1.y), G1);
+                    const float2 s2 = __fmul2_rn(make_float2(b2.y, b2.y), G2);
+                    // 1 - sigma with one rounding, exactly as the scalar subtraction
+                    const float2 o1 = __ffma2_rn(s1, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
+                    const float2 o2 = __ffma2_rn(s2, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
+                    const float2 ir1 = make_float2(fast_rcp(o1.x), fast_rcp(o1.y));  // inv_rest
+                    const float2 ir2 = make_float2(fast_rcp(o2.x), fast_rcp(o2.y));
+                    const float2 gc1 = __ffma2_rn(g2p, make_float2(cz1, cz1),
+                                                  __ffma2_rn(g1p, make_float2(b1.w, b1.w),
+                                                             __fmul2_rn(g0p, make_float2(b1.z, b1.z))));
+                    const float2 gc2 = __ffma2_rn(g2p, make_float2(cz2, cz2),
+                                                  __ffma2_rn(g1p, make_float2(b2.w, b2.w),
+                                                             __fmul2_rn(g0p, make_float2(b2.z, b2.z))));
+                    // g . dC/dsigma_i = T_i (g.c_i) - (g.S_i) / (1 - sigma_i)  (rasterizer.cpp:272-275)
+                    const float2 T1 = __fmul2_rn(T, ir1);
+                    const float2 w1 = __fmul2_rn(s1, T1);
+                    const float2 ds1 = __ffma2_rn(T1, gc1, neg2(__fmul2_rn(gS, ir1)));
+                    const float2 gS1 = __ffma2_rn(gc1, w1, gS);
+                    const float2 T2 = __fmul2_rn(T1, ir2);
+                    const float2 w2 = __fmul2_rn(s2, T2);
+                    const float2 ds2 = __ffma2_rn(T2, gc2, neg2(__fmul2_rn(gS1, ir2)));
+                    T = T2;
+                    gS = __ffma2_rn(gc2, w2, gS1);
+                    const uint32_t o1b = rowb + (soff0 ^ (((uint32_t)(r - rb) & 3u) << 4));
+                    sts_f2(ubase + o1b, __fmul2_rn(ds1, G1));
+                    sts_f2(wbase + o1b, w1);
+                    if (two) {
+                        const uint32_t o2b = rowb + 256u + (soff0 ^ (((uint32_t)(r + 1 - rb) & 3u) << 4));
+                        sts_f2(ubase + o2b, __fmul2_rn(ds2, G2));
+                        sts_f2(wbase + o2b, w2);
+                    }
+                    visb |= (fmaxf(w1.x, w1.y) > kMinVisitW ? (1u << k1) : 0u) |
+                            (fmaxf(w2.x, w2.y) > kMinVisitW ? (1u << k2) : 0u);
+                    rowb += 512u;
                 }
-                visb |= (w1 > kMinVisitW ? (1u << k1) : 0u) | (w2 > kMinVisitW ? (1u << k2) : 0u);
-                rowp += 8 * kRecStride;
+                __syncwarp();
+                // phase 2: dense over each half's 32 pixels per record row; lane 2i + h takes
+                // half h of row i (splat k^h_i)
+                float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if (p2row < re - rb)
+                    half_sums(ubase + 256u * (uint32_t)p2row + 128u * (uint32_t)p2h, ukey, gb, p2h, acc);
+                // hand each half-row's sums to lane j = its splat (from up to two lanes)
+                const bool m0h = in0 && row0 >= rb && row0 < re, m1h = in1 && row1 >= rb && row1 < re;
+                const int src0 = m0h ? 2 * (row0 - rb) : 0, src1 = m1h ? 2 * (row1 - rb) + 1 : 1;
+#pragma unroll
+                for (int q = 0; q < 9; ++q) {
+                    const float v0 = __shfl_sync(kFull, acc[q], src0), v1 = __shfl_sync(kFull, acc[q], src1);
+                    acc[q] = (m0h ? v0 : 0.f) + (m1h ? v1 : 0.f);
+                }
+                if (m0h || m1h) {
+                    const float a0 = acc[0], ax1 = acc[1], ay1 = acc[2];
+                    m0 += a0;
+                    mx1 += ax1 + dxg * a0;
+                    my1 += ay1 + dyg * a0;
+                    mxx += acc[3] + 2.f * dxg * ax1 + dxg * dxg * a0;
+                    mxy += acc[4] + dyg * ax1 + dxg * ay1 + dxg * dyg * a0;
+                    myy += acc[5] + 2.f * dyg * ay1 + dyg * dyg * a0;
+                    q0 += acc[6];
+                    q1 += acc[7];
+                    q2 += acc[8];
+                }
+                __syncwarp();  // rows are rewritten by the next round
             }
-            S.st[g][lane] = make_float2(T, gS);
+            S.st[g][lane] = make_float4(T.x, gS.x, T.y, gS.y);
             vism |= __reduce_or_sync(kFull, visb);
-            __syncwarp();
-            // phase 2: dense over the group's 32 pixels per record row (row i = the i-th highest
-            // union splat); moments about the group centre. Up to 16 rows: two lanes per row,
-            // two pixel rows each, halves added with one shuffle; otherwise one lane per row.
-            float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            const uint32_t gb = lgbase + 512u * (uint32_t)cur + 128u;  // lg[cur][1..3]
-            int src = __popc(un & (0xfffffffeu << lane));  // row of splat `lane`
-            if (U <= 16) {
-                const int row = lane >> 1, prow0 = 2 * (lane & 1);
-                if (row < U) {
-                    const uint32_t ro = 4u * (uint32_t)(row * kRecStride) + 32u * (uint32_t)prow0;
-                    row_sums<2>(ubase + ro, wbase + ro, gb + 32u * (uint32_t)prow0, (float)prow0, acc);
-                }
-#pragma unroll
-                for (int q = 0; q < 9; ++q) acc[q] += __shfl_xor_sync(kFull, acc[q], 1);
-                src *= 2;
-            } else if (lane < U) {
-                const uint32_t ro = 4u * (uint32_t)(lane * kRecStride);
-                row_sums<4>(ubase + ro, wbase + ro, gb, 0.f, acc);
-            }
-            // hand row i's sums to lane j = its splat
-#pragma unroll
-            for (int q = 0; q < 9; ++q) acc[q] = __shfl_sync(kFull, acc[q], src);
-            const float a0 = acc[0], ax1 = acc[1], ay1 = acc[2], axx = acc[3], axy = acc[4],
-                        ayy = acc[5], c0s = acc[6], c1s = acc[7], c2s = acc[8];
-            if ((un >> lane) & 1u) {
-                const float dx = (float)(gx * 8) + 3.5f - hx, dy = (float)(gy * 4) + 1.5f - hy;
-                m0 += a0;
-                mx1 += ax1 + dx * a0;
-                my1 += ay1 + dy * a0;
-                mxx += axx + 2.f * dx * ax1 + dx * dx * a0;
-                mxy += axy + dy * ax1 + dx * ay1 + dx * dy * a0;
-                myy += ayy + 2.f * dy * ay1 + dy * dy * a0;
-                q0 += c0s;
-                q1 += c1s;
-                q2 += c2s;
-            }
         }
         if (jvalid) {
             float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+            const uint32_t slot = __float_as_uint(lds_f1(myrec + 40));
             if (m0 != 0.f || mxx != 0.f || myy != 0.f || q0 != 0.f || q1 != 0.f || q2 != 0.f) {
+                const float4 ja = lds_f4(myrec), jb = lds_f4(myrec + 16);
                 constexpr float iK = 1.0f / kNegHalfLog2e;
                 const float ia = ja.z * iK, ib = 0.5f * ja.w * iK, ic = jb.x * iK;
                 const float al = jb.y;
@@ -661,8 +699,8 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
 template <int NGX, int NGY>
 __global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm) {
     constexpr int NG = NGX * NGY;
-    static_assert(sizeof(BwdWarpSmem<NG>) % 16 == 0 && offsetof(BwdWarpSmem<NG>, lg) % 16 == 0 &&
-                      offsetof(BwdWarpSmem<NG>, rec) % 16 == 0,
+    static_assert(sizeof(BwdWarpSmem<NG>) % 16 == 0 && offsetof(BwdWarpSmem<NG>, st) % 16 == 0 &&
+                      offsetof(BwdWarpSmem<NG>, lg) % 16 == 0 && offsetof(BwdWarpSmem<NG>, rec) % 16 == 0,
                   "float4 shared-memory reads need 16-byte alignment");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -758,9 +796,7 @@ cudaError_t launch_backward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t*
     BlendParams prm = make_params(ctx, ra, items);
     cudaError_t e;
     if (ra.p == 1) {
-        e = run_backward<2, 4>(ctx, prm);
-    } else if (ra.p <= 3) {
-        e = run_backward<1, 2>(ctx, prm);
+        e = run_backward<2, 2>(ctx, prm);
     } else {
         e = run_backward<1, 1>(ctx, prm);
     }

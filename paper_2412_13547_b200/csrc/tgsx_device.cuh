@@ -174,6 +174,9 @@ __device__ __forceinline__ float lds_f1(uint32_t a) {
 __device__ __forceinline__ void sts_f1(uint32_t a, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
 }
+__device__ __forceinline__ void sts_f2(uint32_t a, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(a), "f"(v.x), "f"(v.y));
+}
 __device__ __forceinline__ void sts_f4(uint32_t a, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
                  "f"(v.w));
