@@ -85,14 +85,6 @@ __device__ __forceinline__ uint32_t box_mask(float m, float r, int a0, int p, in
     return mask;
 }
 
-// Row of the 8x4 group (gx, gy) passing a splat: bit l <-> active pixel (8gx + l&7, 4gy + l>>3).
-__device__ __forceinline__ uint32_t group_rowmask(uint32_t mask, int gx, int gy) {
-    const uint32_t xb = (mask >> (gx * 8)) & 0xffu;
-    const uint32_t yb = (mask >> (16 + gy * 4)) & 0xfu;
-    const uint32_t s = (yb & 1u) | ((yb & 2u) << 7) | ((yb & 4u) << 14) | ((yb & 8u) << 21);
-    return xb * s;
-}
-
 // 32x32 bit-matrix transpose across the warp: in lane j bit l = M[j][l]; out lane l bit j.
 __device__ __forceinline__ uint32_t transpose32(uint32_t v) {
     const int lane = threadIdx.x & 31;
@@ -125,7 +117,7 @@ __device__ __forceinline__ void stage_splat(const Prepared& P, const TileGeo& g,
 // the same op sequence (and rounding) per pixel as conic_gauss: a = (mx, my, ka, kb), kc.
 __device__ __forceinline__ float2 pair_quad(const float4& a, float kc, float fx, float fyA, float fyB) {
     const float dx = __fsub_rn(fx, a.x);
-    const float2 dy = make_float2(__fsub_rn(fyA, a.y), __fsub_rn(fyB, a.y));
+    const float2 dy = __fadd2_rn(make_float2(fyA, fyB), make_float2(-a.y, -a.y));  // exact negation
     const float2 t = __fmul2_rn(make_float2(kc, kc), dy);
     const float2 u = __ffma2_rn(make_float2(a.w, a.w), make_float2(dx, dx), t);
     const float2 v = __fmul2_rn(u, dy);
@@ -518,8 +510,10 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
         if (jvalid) {
             const Prepared& P = prm.prep[prm.items[range.x + j]];
             stage_splat(P, geo, p, pair_slot(P, geo.tx, geo.ty), myrec);
-        } else {
-            sts_f4(myrec + 32, make_float4(0.f, 0.f, 0.f, 0.f));  // empty mask
+        } else {  // empty mask; a zero record (finite) for filler rows that land here
+            sts_f4(myrec, make_float4(0.f, 0.f, 0.f, 0.f));
+            sts_f4(myrec + 16, make_float4(0.f, 0.f, 0.f, 0.f));
+            sts_f4(myrec + 32, make_float4(0.f, 0.f, 0.f, 0.f));
         }
         if (ch > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(prm.prep + nxt));
         __syncwarp();
@@ -556,7 +550,9 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
             const uint32_t un1 = __reduce_or_sync(kFull, lane < 16 ? 0u : cu);
             if (!(un0 | un1)) continue;
             const int U0 = __popc(un0), U1 = __popc(un1);
-            const int U = max(U0, U1);
+            // rows are visited in pairs: an odd count is padded with a filler row (each half then
+            // has a splat outside its union, as U <= 31)
+            const int U = (max(U0, U1) + 1) & ~1;
             const float2 g0p = lds_f2(lgc + 256), g1p = lds_f2(lgc + 512), g2p = lds_f2(lgc + 768);
             const float4 st = S.st[g][lane];
             float2 T = make_float2(st.x, st.z), gS = make_float2(st.y, st.w);
@@ -582,13 +578,11 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
                 int k1n = kl[rb], k2n = kl[rb + 1];  // next pair, one iteration ahead
                 uint32_t rowb = 0;  // byte offset of row (r - rb)
                 for (int r = rb; r < re; r += 2) {
-                    const bool two = r + 1 < re;
-                    const int k1 = k1n;
-                    const int k2 = two ? k2n : k1;
+                    const int k1 = k1n, k2 = k2n;
                     k1n = kl[r + 2];
                     k2n = kl[r + 3];
                     const bool hA1 = (colA >> k1) & 1u, hB1 = (colB >> k1) & 1u;
-                    const bool hA2 = two && ((colA >> k2) & 1u), hB2 = two && ((colB >> k2) & 1u);
+                    const bool hA2 = (colA >> k2) & 1u, hB2 = (colB >> k2) & 1u;
                     const uint32_t ad1 = rbase + k1 * kRec, ad2 = rbase + k2 * kRec;
                     const float4 a1 = lds_f4(ad1), a2 = lds_f4(ad2);
                     const float4 b1 = lds_f4(ad1 + 16), b2 = lds_f4(ad2 + 16);
@@ -623,11 +617,9 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
                     const uint32_t o1b = rowb + (soff0 ^ (((uint32_t)(r - rb) & 3u) << 4));
                     sts_f2(ubase + o1b, __fmul2_rn(ds1, G1));
                     sts_f2(wbase + o1b, w1);
-                    if (two) {
-                        const uint32_t o2b = rowb + 256u + (soff0 ^ (((uint32_t)(r + 1 - rb) & 3u) << 4));
-                        sts_f2(ubase + o2b, __fmul2_rn(ds2, G2));
-                        sts_f2(wbase + o2b, w2);
-                    }
+                    const uint32_t o2b = rowb + 256u + (soff0 ^ (((uint32_t)(r + 1 - rb) & 3u) << 4));
+                    sts_f2(ubase + o2b, __fmul2_rn(ds2, G2));
+                    sts_f2(wbase + o2b, w2);
                     visb |= (fmaxf(w1.x, w1.y) > kMinVisitW ? (1u << k1) : 0u) |
                             (fmaxf(w2.x, w2.y) > kMinVisitW ? (1u << k2) : 0u);
                     rowb += 512u;

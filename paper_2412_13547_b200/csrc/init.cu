@@ -165,6 +165,7 @@ cudaError_t launch_knn(tgsx_ctx* ctx, const float* d_xy, int64_t n, int k, uint3
 
 // ============================================================================ C ABI
 #include <cstring>
+#include <string>
 #include <unordered_set>
 
 using namespace tgsx;
@@ -176,6 +177,11 @@ struct PcgInit {
     explicit PcgInit(uint64_t seed, uint64_t stream) { tgsx_pcg32_init(s, seed, stream); }
     double uniform() { return tgsx_pcg32_uniform(s); }
 };
+
+int32_t cuda_err(tgsx_ctx* ctx, cudaError_t e, const char* where) {
+    ctx->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return TGSX_ECUDA;
+}
 
 int32_t knn_host(tgsx_ctx* ctx, const float* xy, int64_t n, int k, uint32_t* out_idx, float* out_d2) {
     if (n <= 0) return TGSX_OK;
@@ -193,15 +199,15 @@ int32_t knn_host(tgsx_ctx* ctx, const float* xy, int64_t n, int k, uint32_t* out
     cudaError_t e;
     // device buffers: points, indices, distances (the loss-gradient buffer is free here)
     const size_t pts = (size_t)n * 8, idx = (size_t)n * k * 4;
-    if ((e = ws.loss_grad.ensure(pts + 2 * idx))) return TGSX_ECUDA;
+    if ((e = ws.loss_grad.ensure(pts + 2 * idx))) return cuda_err(ctx, e, "tgsx_knn: allocate");
     float* d_xy = ws.loss_grad.as<float>();
     uint32_t* d_idx = reinterpret_cast<uint32_t*>(ws.loss_grad.as<char>() + pts);
     float* d_d2 = reinterpret_cast<float*>(ws.loss_grad.as<char>() + pts + idx);
-    if ((e = cudaMemcpyAsync(d_xy, xy, pts, cudaMemcpyHostToDevice, ctx->stream))) return TGSX_ECUDA;
-    if ((e = launch_knn(ctx, d_xy, n, k, d_idx, d_d2, bb))) return TGSX_ECUDA;
-    if ((e = cudaMemcpyAsync(out_idx, d_idx, idx, cudaMemcpyDeviceToHost, ctx->stream))) return TGSX_ECUDA;
-    if (out_d2 && (e = cudaMemcpyAsync(out_d2, d_d2, idx, cudaMemcpyDeviceToHost, ctx->stream))) return TGSX_ECUDA;
-    if ((e = cudaStreamSynchronize(ctx->stream))) return TGSX_ECUDA;
+    if ((e = cudaMemcpyAsync(d_xy, xy, pts, cudaMemcpyHostToDevice, ctx->stream))) return cuda_err(ctx, e, "tgsx_knn: upload");
+    if ((e = launch_knn(ctx, d_xy, n, k, d_idx, d_d2, bb))) return cuda_err(ctx, e, "tgsx_knn: kernels");
+    if ((e = cudaMemcpyAsync(out_idx, d_idx, idx, cudaMemcpyDeviceToHost, ctx->stream))) return cuda_err(ctx, e, "tgsx_knn: download");
+    if (out_d2 && (e = cudaMemcpyAsync(out_d2, d_d2, idx, cudaMemcpyDeviceToHost, ctx->stream))) return cuda_err(ctx, e, "tgsx_knn: download");
+    if ((e = cudaStreamSynchronize(ctx->stream))) return cuda_err(ctx, e, "tgsx_knn: synchronize");
     return TGSX_OK;
 }
 
