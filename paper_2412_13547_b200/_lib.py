@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtgsx.so")
+LIB_PATH = os.environ.get("TGSX_LIB") or os.path.join(HERE, "libtgsx.so")  # TGSX_LIB: A/B builds
 
 P = C.POINTER
 f32p, f64p = P(C.c_float), P(C.c_double)
@@ -117,7 +117,7 @@ SIGNATURES = {
     "tgsx_upsample": (C.c_int32, [vp, vp, vp, C.c_int64, C.c_int32, C.c_int64, vp, vp, i64p]),
     "tgsx_init_model": (C.c_int32, [vp, vp, vp, vp, C.c_int64, C.c_int32, C.c_int32,
                                     C.c_uint64]),
-    "tgsx_synthetic_scene":(None, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, P(HostScene)]),
+    "tgsx_synthetic_scene": (None, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, P(HostScene)]),
     "tgsx_pcg32_init": (None, [u64p, C.c_uint64, C.c_uint64]),
     "tgsx_pcg32_uniform": (C.c_double, [u64p]),
     "tgsx_pcg32_advance": (None, [u64p, C.c_uint64]),

@@ -40,6 +40,9 @@ namespace {
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kRec = 48;        // bytes per staged splat record
 constexpr int kWPB = 4;         // warps (tiles) per CTA
+#ifndef TGSX_BWD_MINB
+#define TGSX_BWD_MINB 4
+#endif
 
 struct BlendParams {
     const uint2* ranges;
@@ -577,6 +580,7 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
                 // (sigma = 0, 1 / (1 - sigma) = 1: T, g.S pass through; records u = w = 0).
                 int k1n = kl[rb], k2n = kl[rb + 1];  // next pair, one iteration ahead
                 uint32_t rowb = 0;  // byte offset of row (r - rb)
+#pragma unroll 2
                 for (int r = rb; r < re; r += 2) {
                     const int k1 = k1n, k2 = k2n;
                     k1n = kl[r + 2];
@@ -689,7 +693,7 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
 // finished one, so no warp idles until its CTA siblings finish (per-tile work varies) and the
 // tail of the launch is at most one tile.
 template <int NGX, int NGY>
-__global__ void __launch_bounds__(kWPB * 32, 4) backward_kernel(BlendParams prm) {
+__global__ void __launch_bounds__(kWPB * 32, TGSX_BWD_MINB) backward_kernel(BlendParams prm) {
     constexpr int NG = NGX * NGY;
     static_assert(sizeof(BwdWarpSmem<NG>) % 16 == 0 && offsetof(BwdWarpSmem<NG>, st) % 16 == 0 &&
                       offsetof(BwdWarpSmem<NG>, lg) % 16 == 0 && offsetof(BwdWarpSmem<NG>, rec) % 16 == 0,
