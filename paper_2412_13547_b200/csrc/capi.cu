@@ -302,14 +302,36 @@ bool force_onesweep() {
     return v;
 }
 
-// Sort (if dirty) -> preprocess (+ per-tile lengths) -> scans -> [sync for K, longest list] ->
-// scatter + per-tile sort, or (a list longer than kSegCap, or TGSX_BINNING=onesweep)
-// duplicate -> onesweep radix sort -> ranges.
+// Per-tile sort of the slabs for lists up to `cap` entries (the template is chosen from it).
+int32_t slab_sort(tgsx_ctx* ctx, tgsx_model* m, int tiles, uint64_t cap) {
+    {
+        StageTimer t(ctx, kStDuplicate);
+        CK(launch_pair_base(ctx, m));
+    }
+    {
+        StageTimer t(ctx, kStSort);
+        CK(launch_seg_sort(ctx, ctx->ws.tile_slab.as<uint32_t>(), tiles, (int64_t)cap));
+    }
+    ctx->bin_sort_cap = cap <= 256 ? 256 : (cap <= 512 ? 512 : kSegCap);
+    return TGSX_OK;
+}
+
+int32_t bin_onesweep(tgsx_ctx* ctx, tgsx_model* m, int W, int H, int64_t K, uint32_t** items,
+                     uint32_t** sorted_keys);
+
+// Sort (if dirty) -> preprocess (+ per-tile lengths) -> scans -> [read-back of K, errors, the
+// longest list] -> per-tile sort of the slabs, or (a list longer than kSegCap, or
+// TGSX_BINNING=onesweep) duplicate -> onesweep radix sort -> ranges.
+// With `defer` (fused views) the read-back is not waited for here: the per-tile sort is
+// launched speculatively for lists up to the previous binning's longest (x1.25), the caller
+// queues its forward and then bin_settle() checks the counters (normally long complete),
+// redoing the sort (or taking the onesweep path) when the guess was short.
 // On return ws.K, ws.ranges and `items` (per-tile ranks in blend order) describe the lists.
 int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t** items,
-                    uint32_t** sorted_keys) {
+                    uint32_t** sorted_keys, bool defer = false) {
     Workspace& ws = ctx->ws;
     ws.have_forward = false;
+    ctx->bin_pending = false;
     CK(reset_counters(ctx));
     if (m->order_dirty || !m->blend_phys) {
         StageTimer t(ctx, kStDepthSort);
@@ -330,6 +352,17 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
     }
     CK(cudaMemcpyAsync(ws.h_scratch, counters, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        ctx->stream));
+    if (defer && !sorted_keys && !force_onesweep() && !debug_checks()) {
+        if (!ctx->bin_event) CK(cudaEventCreateWithFlags(&ctx->bin_event, cudaEventDisableTiming));
+        CK(cudaEventRecord(ctx->bin_event, ctx->stream));
+        const uint64_t guess = std::min<uint64_t>(kSegCap, ctx->bin_max_hint + ctx->bin_max_hint / 4);
+        int32_t rc = slab_sort(ctx, m, tiles, guess);
+        if (rc) return rc;
+        ctx->bin_pending = true;
+        *items = ws.tile_slab.as<uint32_t>();
+        if (sorted_keys) *sorted_keys = nullptr;
+        return TGSX_OK;
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->prof.enabled) ctx->prof.harvest();  // every event recorded so far has completed
     int32_t rc = check_kernel_error(ctx, ws.h_scratch[0]);
@@ -337,24 +370,61 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
     const int64_t K = (int64_t)(uint32_t)(ws.h_scratch[3] & 0xffffffffull);
     const uint64_t max_list = ws.h_scratch[5];
     ws.K = K;
+    ctx->bin_max_hint = max_list;
     CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
     ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
     if (max_list <= (uint64_t)kSegCap && !force_onesweep()) {
         // slab binning: every tile's list was claimed by preprocess into its slab; sort each slab
         // back into blend order (one warp per tile)
-        uint32_t* v = ws.tile_slab.as<uint32_t>();
-        {
-            StageTimer t(ctx, kStDuplicate);
-            CK(launch_pair_base(ctx, m));
-        }
-        {
-            StageTimer t(ctx, kStSort);
-            CK(launch_seg_sort(ctx, v, tiles, (int64_t)max_list));
-        }
-        *items = v;
+        rc = slab_sort(ctx, m, tiles, max_list);
+        if (rc) return rc;
+        *items = ws.tile_slab.as<uint32_t>();
         if (sorted_keys) *sorted_keys = nullptr;
         return TGSX_OK;
     }
+    return bin_onesweep(ctx, m, W, H, K, items, sorted_keys);
+}
+
+// Completes a deferred binning: waits for the counters, reports kernel errors, sizes the
+// per-pair partials and, when the speculative per-tile sort was too short for the longest list
+// (or a list overflowed its slab), redoes the lists; *redo tells the caller to rerun its forward.
+int32_t bin_settle(tgsx_ctx* ctx, tgsx_model* m, int W, int H, uint32_t** items, bool* redo) {
+    *redo = false;
+    if (!ctx->bin_pending) return TGSX_OK;
+    ctx->bin_pending = false;
+    Workspace& ws = ctx->ws;
+    CK(cudaEventSynchronize(ctx->bin_event));
+    int32_t rc = check_kernel_error(ctx, ws.h_scratch[0]);
+    if (rc) {
+        ctx->bin_valid = false;
+        return rc;
+    }
+    const int64_t K = (int64_t)(uint32_t)(ws.h_scratch[3] & 0xffffffffull);
+    const uint64_t max_list = ws.h_scratch[5];
+    ws.K = K;
+    ctx->bin_max_hint = max_list;
+    CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
+    ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
+    if (max_list <= (uint64_t)ctx->bin_sort_cap) return TGSX_OK;
+    *redo = true;
+    if (max_list <= (uint64_t)kSegCap) {
+        rc = slab_sort(ctx, m, ws.tiles_x * ws.tiles_y, max_list);
+        if (rc) return rc;
+        *items = ws.tile_slab.as<uint32_t>();
+    } else {
+        rc = bin_onesweep(ctx, m, W, H, K, items, nullptr);
+        if (rc) return rc;
+    }
+    if (ctx->bin_valid) ctx->bin_items = *items;
+    return TGSX_OK;
+}
+
+// Onesweep path (a list longer than the slab, or TGSX_BINNING=onesweep): duplicate keys,
+// radix sort by tile (stable: blend order inside a tile), ranges.
+int32_t bin_onesweep(tgsx_ctx* ctx, tgsx_model* m, int W, int H, int64_t K, uint32_t** items,
+                     uint32_t** sorted_keys) {
+    Workspace& ws = ctx->ws;
+    const int tiles = ws.tiles_x * ws.tiles_y;
     for (int i = 0; i < 2; ++i) CK(ws.vals[i].ensure(std::max<int64_t>(K, 1) * 4));
     const int key_bits = key_bits_for(tiles);
     const int passes = (key_bits + 7) / 8;
@@ -435,7 +505,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
 // prepared records and tile lists — pixel_span works on the full-resolution image, so the lists
 // do not depend on the dilation offset (rasterizer.cpp:74-100).
 int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t** items,
-            uint32_t** sorted_keys) {
+            uint32_t** sorted_keys, bool defer = false) {
     if (!sorted_keys && ctx->bin_valid && ctx->bin_model == m->uid && ctx->bin_lowpass == lowpass_p &&
         ctx->bin_W == W && ctx->bin_H == H && ctx->bin_n == m->n && !m->order_dirty && m->blend_phys) {
         ctx->ws.have_forward = false;
@@ -444,7 +514,7 @@ int32_t bin(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t*
         return TGSX_OK;
     }
     ctx->bin_valid = false;
-    const int32_t rc = bin_compute(ctx, m, lowpass_p, W, H, items, sorted_keys);
+    const int32_t rc = bin_compute(ctx, m, lowpass_p, W, H, items, sorted_keys, defer);
     if (rc) return rc;
     ctx->bin_valid = true;
     ctx->bin_model = m->uid;
@@ -564,12 +634,19 @@ int32_t mark_target_consumed(tgsx_ctx* ctx) {
 }
 
 int32_t render_core(tgsx_ctx* ctx, tgsx_model* m, const RenderArgs& ra, bool fused_loss,
-                    uint32_t** items_out) {
+                    uint32_t** items_out, bool defer = false) {
     uint32_t* items = nullptr;
-    int32_t rc = bin(ctx, m, ra.lowpass_p, ra.W, ra.H, &items, nullptr);
+    int32_t rc = bin(ctx, m, ra.lowpass_p, ra.W, ra.H, &items, nullptr, defer);
     if (rc) return rc;
     CK(ensure_pixels(ctx, ra));
     {
+        StageTimer t(ctx, kStForward);
+        CK(launch_forward(ctx, ra, items, fused_loss));
+    }
+    bool redo = false;
+    if ((rc = bin_settle(ctx, m, ra.W, ra.H, &items, &redo))) return rc;
+    if (redo) {  // the speculative lists were short: forward again on the settled ones
+        CK(reset_counters(ctx));
         StageTimer t(ctx, kStForward);
         CK(launch_forward(ctx, ra, items, fused_loss));
     }
@@ -593,7 +670,7 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
     rc = stage_target(ctx, target, (size_t)ra.W * ra.H * 12, &ra.target);
     if (rc) return rc;
     uint32_t* items = nullptr;
-    rc = render_core(ctx, m, ra, true, &items);  // forward + fused (1 - lam) L1
+    rc = render_core(ctx, m, ra, true, &items, true);  // forward + fused (1 - lam) L1
     if (rc) return rc;
     int nsb = 0;
     if (lam > 0.f && ra.P > 0) {

@@ -248,7 +248,7 @@ cudaError_t launch_slab_finalize(tgsx_ctx* ctx, int tiles) {
 cudaError_t launch_pair_base(tgsx_ctx* ctx, tgsx_model* m) {
     Workspace& ws = ctx->ws;
     const int64_t n = m->n;
-    if (n == 0 || ws.K == 0) return cudaSuccess;
+    if (n == 0) return cudaSuccess;
     pair_base_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(ws.prep.as<Prepared>(),
                                                                 ws.pair_off.as<uint32_t>(), n);
     ctx->launches++;
@@ -256,7 +256,7 @@ cudaError_t launch_pair_base(tgsx_ctx* ctx, tgsx_model* m) {
 }
 
 cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles, int64_t max_list) {
-    if (ctx->ws.K == 0 || tiles == 0) return cudaSuccess;
+    if (tiles == 0) return cudaSuccess;
     const uint2* rg = ctx->ws.ranges.as<uint2>();
     const unsigned grid = grid_for(tiles, 8);
     if (max_list <= 256)

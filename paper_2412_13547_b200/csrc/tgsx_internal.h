@@ -102,6 +102,12 @@ struct tgsx_ctx {
     int bin_lowpass = 0, bin_W = 0, bin_H = 0;
     int64_t bin_n = -1;
     uint32_t* bin_items = nullptr;
+    // deferred binning read-back (fused views): the counters copy is waited for after the
+    // forward has been queued, so the GPU never idles on the host's decision
+    cudaEvent_t bin_event = nullptr;
+    bool bin_pending = false;
+    int bin_sort_cap = 0;           // longest list the speculative per-tile sort handled
+    uint64_t bin_max_hint = 0;      // longest list of the previous binning
 };
 
 // Scoped stage timer: no-op unless profiling is enabled.
