@@ -1,7 +1,7 @@
 """Summarise ncu captures into the text files committed under profiles/.
 
     python profiles/summarize.py launches <launches.csv> <out.txt>
-    python profiles/summarize.py kernel <capture.ncu-rep> <out.txt> [algorithmic_bytes]
+    python profiles/summarize.py kernel <capture.ncu-rep> <out.txt> [algorithmic_bytes] [kernel_regex]
 
 `launches` aggregates a `--metrics gpu__time_duration.sum` launch list into per-kernel counts,
 total / mean device time and share of the captured time (cold-cache, serialised: compare
@@ -71,13 +71,14 @@ def launches(path, out):
     print("\n".join(lines))
 
 
-def kernel(rep, out, algo_bytes=None):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def kernel(rep, out, algo_bytes=None, name=None):
+    filt = ["-k", f"regex:{name}"] if name else []
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"] + filt, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, u, v = rows[0], rows[1], rows[2]
     get = {name: (v[i], u[i]) for i, name in enumerate(h)}
-    name = get.get("Kernel Name", ("?", ""))[0]
-    lines = [f"# {rep.split('/')[-1]}: {name}"]
+    kname = get.get("Kernel Name", ("?", ""))[0]
+    lines = [f"# {rep.split('/')[-1]}: {kname}"]
     for m in KEY_METRICS:
         if m in get:
             lines.append(f"{m:70s} {get[m][0]:>18s} {get[m][1]}")
@@ -95,7 +96,7 @@ def kernel(rep, out, algo_bytes=None):
         m = f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"
         if m in get and get[m][0] not in ("", "0"):
             lines.append(f"  {s:24s} {get[m][0]}")
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + filt,
                          capture_output=True, text=True).stdout
     srows = list(csv.reader(io.StringIO(src)))
     if len(srows) > 2:
@@ -118,4 +119,5 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
-        kernel(sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 else None)
+        kernel(sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4] else None,
+               sys.argv[5] if len(sys.argv) > 5 else None)
