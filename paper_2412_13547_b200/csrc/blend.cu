@@ -76,18 +76,6 @@ struct TileGeo {
     }
 };
 
-// Exact box-test mask over the tile's active columns (or rows): bit c set iff
-// |float(a0 + c p) + 0.5 - m| <= r (rasterizer.cpp:116-118, same float rounding).
-__device__ __forceinline__ uint32_t box_mask(float m, float r, int a0, int p, int count) {
-    uint32_t mask = 0;
-#pragma unroll
-    for (int c = 0; c < kTile; ++c) {
-        const float d = __fsub_rn(__fadd_rn((float)(a0 + c * p), 0.5f), m);
-        mask |= (c < count && fabsf(d) <= r) ? (1u << c) : 0u;
-    }
-    return mask;
-}
-
 // 32x32 bit-matrix transpose across the warp: in lane j bit l = M[j][l]; out lane l bit j.
 __device__ __forceinline__ uint32_t transpose32(uint32_t v) {
     const int lane = threadIdx.x & 31;

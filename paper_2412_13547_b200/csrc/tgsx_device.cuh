@@ -148,6 +148,30 @@ __device__ __forceinline__ float conic_gauss(float ka, float kb, float kc, float
     return fast_exp2(__fmaf_rn(__fmul_rn(ka, dx), dx, v));
 }
 
+// Exact box-test mask over the tile's active columns (or rows): bit c set iff
+// |float(a0 + c p) + 0.5 - m| <= r (rasterizer.cpp:116-118, same float rounding). The centres
+// increase with c and the rounded difference is monotonic in the centre, so the passing
+// columns form one interval: its ends are estimated in real arithmetic (off by at most one
+// column) and then settled with the exact test itself.
+__device__ __forceinline__ bool box_pass(float m, float r, int a0, int p, int c) {
+    const float d = __fsub_rn(__fadd_rn((float)(a0 + c * p), 0.5f), m);
+    return fabsf(d) <= r;
+}
+__device__ __forceinline__ uint32_t box_mask(float m, float r, int a0, int p, int count) {
+    if (count <= 0) return 0u;
+    const float base = (float)a0 + 0.5f, inv_p = 1.0f / (float)p;
+    float lo = ceilf(((m - r) - base) * inv_p), hi = floorf(((m + r) - base) * inv_p);
+    lo = fminf(fmaxf(lo, 0.f), (float)count);
+    hi = fminf(fmaxf(hi, -1.f), (float)(count - 1));
+    int cl = (int)lo, ch = (int)hi;
+    if (cl > 0 && box_pass(m, r, a0, p, cl - 1)) --cl;
+    else if (cl < count && !box_pass(m, r, a0, p, cl)) ++cl;
+    if (ch < count - 1 && box_pass(m, r, a0, p, ch + 1)) ++ch;
+    else if (ch >= 0 && !box_pass(m, r, a0, p, ch)) --ch;
+    if (cl > ch) return 0u;
+    return (uint32_t)((2ull << ch) - (1ull << cl));
+}
+
 __device__ __forceinline__ float fast_rcp(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
