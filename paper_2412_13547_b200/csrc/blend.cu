@@ -4,11 +4,12 @@
 // geometry and the same kernels serve p = 1 and the paper's 4K dilated rendering) are covered
 // by warps. The tile's splat list is consumed in chunks of 32 staged as 48-byte shared-memory
 // records together with exact per-tile box-test masks (rasterizer.cpp:116-118, evaluated once
-// per (tile, splat) in float, per active column / row). Per chunk the warp builds the 32x32
-// (splat x pixel) pass matrix — lane j turns splat j's masks into a 32-bit row with one
-// multiply, a 5-stage shuffle bit-transpose hands lane l the column "which of these 32 splats
-// pass my pixel". Per pixel the order is the list order and box-failing splats contribute
-// nothing, exactly as in walk_pixel (rasterizer.cpp:108-136).
+// per (tile, splat) in float: the passing active columns / rows form one interval, settled by
+// the exact test at its two ends). Per chunk one 5-stage shuffle bit-transpose of the 32 masks
+// hands lane c the set of splats passing active column c and lane 16 + r those passing row r;
+// a pixel's pass set is one AND of a column and a row set (two shuffles). Per pixel the order is
+// the list order and box-failing splats contribute nothing, exactly as in walk_pixel
+// (rasterizer.cpp:108-136).
 //
 // forward_pairs_kernel (one CTA per tile, one warp per 8x8 block, two pixels per lane as packed
 //   FP32x2): walk_pixel + render (rasterizer.cpp:144-184), optional fused L1 epilogue
@@ -116,10 +117,6 @@ __device__ __forceinline__ float2 pair_quad(const float4& a, float kc, float fx,
     return __ffma2_rn(make_float2(kadx, kadx), make_float2(dx, dx), v);
 }
 
-// Row bits 0,2,4,6 of an 8-bit row mask spread to bytes 0..3 (one byte per lane row-pair).
-__device__ __forceinline__ uint32_t spread_even4(uint32_t yb) {
-    return (yb & 1u) | ((yb & 4u) << 6) | ((yb & 16u) << 12) | ((yb & 64u) << 18);
-}
 
 // One CTA per tile, one warp per 8x8 block of active pixels, TWO vertically adjacent pixels per
 // lane (rows 2r and 2r+1 of the block). The lane walks the union of its two pixels' passing
@@ -173,14 +170,12 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_pairs_kernel(BlendPara
         if (warp_done) continue;
         for (int c0 = 0; c0 < bcount; c0 += 32) {
             const int j = c0 + lane;
-            uint32_t rowA = 0, rowB = 0;
-            if (j < bcount) {
-                const uint32_t m = __float_as_uint(lds_f1(sbase + j * kRec + 36));
-                const uint32_t xb = (m >> (bx * 8)) & 0xffu, yb = (m >> (16 + by * 8)) & 0xffu;
-                rowA = xb * spread_even4(yb);
-                rowB = xb * spread_even4(yb >> 1);
-            }
-            uint32_t colA = transpose32(rowA), colB = transpose32(rowB);
+            // masks transposed: lane c < 16 holds the chunk's splats passing active column c,
+            // lane 16 + r those passing row r; a pixel's pass set is column & row
+            const uint32_t bits = transpose32(j < bcount ? __float_as_uint(lds_f1(sbase + j * kRec + 36)) : 0u);
+            const uint32_t X = __shfl_sync(kFull, bits, bx * 8 + (lane & 7));
+            uint32_t colA = X & __shfl_sync(kFull, bits, 16 + by * 8 + 2 * (lane >> 3));
+            uint32_t colB = X & __shfl_sync(kFull, bits, 17 + by * 8 + 2 * (lane >> 3));
             if (doneA) colA = 0;
             if (doneB) colB = 0;
             const uint32_t colA0 = colA, colB0 = colB;
@@ -508,6 +503,9 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
         }
         if (ch > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(prm.prep + nxt));
         __syncwarp();
+        // masks transposed: lane c < 16 holds the chunk's splats passing active column c, lane
+        // 16 + r those passing row r (rasterizer.cpp:116-118); a pixel's pass set is column & row
+        const uint32_t bits = transpose32(__float_as_uint(lds_f1(myrec + 36)));
         float m0 = 0.f, mx1 = 0.f, my1 = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
         float q0 = 0.f, q1 = 0.f, q2 = 0.f;
         uint32_t vism = 0;
@@ -518,11 +516,10 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
             buf ^= 1;
             __syncwarp();  // the previous group's phase 2 is done with the rows and lg[buf]
             prefetch(g + 1 < NG ? g + 1 : 0, buf);
-            // pass matrix of the group (rasterizer.cpp:116-118): lane l, pixel A / B
-            const uint32_t mask = __float_as_uint(lds_f1(myrec + 36));
-            const uint32_t xb = (mask >> (gx * 8)) & 0xffu, yb = (mask >> (16 + gy * 8)) & 0xffu;
-            uint32_t colA = transpose32(xb * spread_even4(yb));
-            uint32_t colB = transpose32(xb * spread_even4(yb >> 1));
+            // pass sets of the lane's pixels A / B in this group
+            const uint32_t X = __shfl_sync(kFull, bits, gx * 8 + cxl);
+            uint32_t colA = X & __shfl_sync(kFull, bits, 16 + gy * 8 + ryl);
+            uint32_t colB = X & __shfl_sync(kFull, bits, 17 + gy * 8 + ryl);
             cp_async_wait<1>();
             __syncwarp();
             const uint32_t lgc = lgbase + 1024u * (uint32_t)cur + 8u * (uint32_t)lane;
