@@ -304,6 +304,70 @@ int32_t tgsx_sort_pairs(tgsx_ctx* ctx, uint32_t* keys, uint32_t* vals, int64_t n
 int32_t tgsx_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n,
                             uint64_t* out_total);
 
+/* ---------------------------------------------------------------- 3-D front end
+ * SURVEY.md §8a row A3b / BASELINE.json north_star item (1): per-Gaussian EWA projection to a
+ * 2-D covariance, SH-degree-3 colour and near-plane / tile-rect culling in front of the same
+ * binning, blend and backward kernels as the 2-D path, and the chain rule back to the 3-D
+ * parameters fused with Adam. The reference is a 2-D analog with NO 3-D code:
+ * these entry points have no reference counterpart to replace; they follow the published 3DGS
+ * algorithm (restated in FP64 by oracle/ewa3d.c) and reuse the 2-D conventions: the low-pass
+ * bump 0.3 + 0.5 (p - 1) (dilation.hpp:67-80), 3-sigma box extents (rasterizer.cpp:40-41),
+ * pixel centres at (x + 0.5, y + 0.5) (rasterizer.cpp:114), the reference's blend.
+ *
+ * Parameters: float[59][n] (row-major, one row per component, n columns): mean xyz (world),
+ * quaternion w x y z (normalised in the forward), log-scales xyz, raw opacity (sigmoid),
+ * SH coefficients sh[k][c] at row 11 + 3k + c (k = 0..15, c = r g b); colour = SH + 0.5
+ * clamped at 0. Blend order: ascending camera depth, ties by row. Gaussians at depth <= znear
+ * are culled. Non-finite parameters / zero quaternion -> TGSX_EINVAL. */
+typedef struct tgsx_model3d tgsx_model3d;
+#define TGSX_3D_PARAMS 59
+/* Pinhole camera: p_cam = R p_world + t (R row-major), u = fx x/z + cx, v = fy y/z + cy in
+ * pixel units of a width x height image (OpenCV axes: x right, y down, z forward). */
+typedef struct {
+    float R[9];
+    float t[3];
+    float fx, fy, cx, cy, znear;
+    int32_t width, height;
+} tgsx_camera;
+/* 3DGS learning rates: mean 1.6e-4 * scene_extent * 0.01^(step/total) (as SPEC.md:284's
+ * position schedule), rotation 1e-3, log-scale 5e-3, opacity 5e-2, SH DC 2.5e-3, SH rest
+ * 2.5e-3 / 20; Adam beta (0.9, 0.999), eps 1e-15; raw opacity in [-12, 12]. */
+typedef struct {
+    int64_t step, total_steps;
+    double scene_extent;
+} tgsx_adam3d_args;
+
+int32_t tgsx_model3d_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model3d** out);
+void tgsx_model3d_destroy(tgsx_model3d* m);
+int64_t tgsx_model3d_size(const tgsx_model3d* m);
+/* params host or device float[59][n]; zeroes the Adam moments and statistics. */
+int32_t tgsx_model3d_upload(tgsx_ctx* ctx, tgsx_model3d* m, const float* params, int64_t n);
+/* Any pointer may be NULL. Statistics: screen-space position-gradient norm sum, SH-DC
+ * colour-gradient norm sum and visit count per Gaussian (the 2-D DensifyStats analogues,
+ * rasterizer.cpp:348-359). */
+int32_t tgsx_model3d_download(tgsx_ctx* ctx, tgsx_model3d* m, float* params, float* pos_acc,
+                              float* col_acc, int32_t* visits);
+int32_t tgsx_model3d_download_moments(tgsx_ctx* ctx, tgsx_model3d* m, float* m1, float* m2);
+/* render<float> (rasterizer.hpp:58-60) with the 3-D front end; camera size == pattern size. */
+int32_t tgsx_render3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                      const float bg[3], int32_t lowpass_p, float* out_rgb, float* out_T,
+                      uint64_t* out_blend_ops);
+/* backward<float> (rasterizer.hpp:66-69) with the 3-D chain rule: out_grads float[59][n] (zero for
+ * Gaussians this view does not touch), out_screen float[10][n] the merged screen-space sums
+ * (d mean xy, d Sigma' 00 01 11, d alpha, d rgb, visited), both host or device, may be NULL. */
+int32_t tgsx_backward3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                        const float bg[3], int32_t lowpass_p, const float* dLdC, int64_t dLdC_count,
+                        float* out_grads, float* out_screen, int32_t update_stats);
+/* Adam with explicit gradients float[59][n] (host or device). */
+int32_t tgsx_adam3d_step(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, const tgsx_adam3d_args* a);
+/* One fused fit iteration of the 3-D model on one view (tgsx_fit_step with the 3-D front end). */
+int32_t tgsx_fit_step3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                        const float bg[3], const float* target, const tgsx_adam3d_args* a, float* out_loss);
+/* Parity stage: the blend-ordered 64-B records (Prepared layout, raster.cu) of all n ranks and
+ * the sorted depth keys (culled rows last with key 0xffffffff). */
+int32_t tgsx_stage_prepare3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, int32_t lowpass_p,
+                             float* out_records, uint32_t* out_keys);
+
 #ifdef __cplusplus
 }
 #endif

@@ -623,3 +623,137 @@ def fit_power_exponent(t, y):
 
 def budget_t_norm(step, warmup, densify_end):
     return lib().or_budget_t_norm(step, warmup, densify_end)
+
+
+# ------------------------------------------------------------------ 3-D front end (ewa3d.c)
+# parity unpinned at the reference (no 3-D code exists there); the
+# restatement is pinned by formula KATs and FP64 finite differences (tests/test_oracle3d.py).
+N3D = 59
+
+
+class OrCamera(C.Structure):
+    _fields_ = [("R", C.c_double * 9), ("t", C.c_double * 3), ("fx", C.c_double),
+                ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("znear", C.c_double), ("W", C.c_int), ("H", C.c_int)]
+
+
+class OrAdam3dCfg(C.Structure):
+    _fields_ = [(f, C.c_float) for f in ("beta1", "beta2", "eps", "lr_pos", "lr_rot", "lr_scale",
+                                          "lr_opacity", "lr_dc", "lr_rest", "bc1", "bc2",
+                                          "raw_cap")]
+
+
+def camera_struct(cam) -> OrCamera:
+    """`cam`: any object with R (3x3), t (3), fx, fy, cx, cy, znear, width, height."""
+    c = OrCamera()
+    R = np.asarray(cam.R, np.float64).reshape(9)
+    for i in range(9):
+        c.R[i] = float(R[i])
+    for i in range(3):
+        c.t[i] = float(cam.t[i])
+    c.fx, c.fy, c.cx, c.cy, c.znear = (float(cam.fx), float(cam.fy), float(cam.cx),
+                                       float(cam.cy), float(cam.znear))
+    c.W, c.H = int(cam.width), int(cam.height)
+    return c
+
+
+def sh_basis(d):
+    b = np.zeros(16, np.float64)
+    db = np.zeros((16, 3), np.float64)
+    lib().or3d_sh_basis(C.c_double(d[0]), C.c_double(d[1]), C.c_double(d[2]), _ptr(b, f64p),
+                        _ptr(db, f64p))
+    return b, db
+
+
+def project3d(theta, cam, bump):
+    """(status, out[12]) for one Gaussian in FP64: u v s00 s01 s11 alpha r g b depth rx ry."""
+    th = np.ascontiguousarray(theta, np.float64)
+    out = np.zeros(12, np.float64)
+    cs = camera_struct(cam)
+    rc = lib().or3d_project(_ptr(th, f64p), C.byref(cs), C.c_double(bump), _ptr(out, f64p))
+    return rc, out
+
+
+def chain3d(theta, cam, bump, screen):
+    th = np.ascontiguousarray(theta, np.float64)
+    sc = np.ascontiguousarray(screen, np.float64)
+    g = np.zeros(N3D, np.float64)
+    cs = camera_struct(cam)
+    lib().or3d_chain(_ptr(th, f64p), C.byref(cs), C.c_double(bump), _ptr(sc, f64p), _ptr(g, f64p))
+    return g
+
+
+def _prep_arrays(n):
+    nn = max(n, 1)
+    arrs = {f: np.zeros(nn, np.float32) for f in ("mx", "my", "i00", "i01", "i11", "alpha", "c0",
+                                                  "c1", "c2", "rx", "ry")}
+    arrs["orig"] = np.zeros(nn, np.uint32)
+    sp = OrPrepared(**{k: _ptr(v, f32p if v.dtype == np.float32 else u32p) for k, v in arrs.items()})
+    return arrs, sp
+
+
+def prepare3d(params, cam, lowpass_p):
+    """Blend-ordered records of the visible Gaussians: dict of arrays (+ 'depth'), length nv."""
+    params = np.ascontiguousarray(params, np.float32)
+    n = params.shape[1]
+    arrs, sp = _prep_arrays(n)
+    depth = np.zeros(max(n, 1), np.float32)
+    nv = C.c_int64(0)
+    cs = camera_struct(cam)
+    rc = lib().or3d_prepare(_ptr(params, f32p), C.c_int64(n), C.byref(cs), lowpass_p, C.byref(sp),
+                            _ptr(depth, f32p), C.byref(nv))
+    if rc:
+        raise OracleError(rc)
+    arrs["depth"] = depth
+    return {k: v[:nv.value] for k, v in arrs.items()}
+
+
+def render3d(params, cam, p, ox, oy, bg=(0, 0, 0), lowpass_p=0):
+    params = np.ascontiguousarray(params, np.float32)
+    n = params.shape[1]
+    Pn = active_count(p, ox, oy, cam.width, cam.height)
+    rgb = np.zeros((Pn, 3), np.float32)
+    T = np.zeros(Pn, np.float32)
+    ops, ev = C.c_uint64(0), C.c_uint64(0)
+    bgv = np.asarray(bg, np.float32)
+    cs = camera_struct(cam)
+    rc = lib().or3d_render(_ptr(params, f32p), C.c_int64(n), C.byref(cs), p, ox, oy, _ptr(bgv, f32p),
+                           lowpass_p, _ptr(rgb, f32p), _ptr(T, f32p), C.byref(ops), C.byref(ev))
+    if rc:
+        raise OracleError(rc)
+    return rgb, T, ops.value, ev.value
+
+
+def backward3d(params, cam, p, ox, oy, dLdC, bg=(0, 0, 0), lowpass_p=0):
+    """(grads[59, n], screen[10, n], touched[n]) in row order."""
+    params = np.ascontiguousarray(params, np.float32)
+    n = params.shape[1]
+    nn = max(n, 1)
+    grads = np.zeros((N3D, nn), np.float32)
+    scr = np.zeros((10, nn), np.float32)
+    touched = np.zeros(nn, np.uint8)
+    sg = OrScreen(*[_ptr(scr[q], f32p) for q in range(10)], _ptr(touched, u8p))
+    dl = np.ascontiguousarray(dLdC, np.float32)
+    bgv = np.asarray(bg, np.float32)
+    cs = camera_struct(cam)
+    rc = lib().or3d_backward(_ptr(params, f32p), C.c_int64(n), C.byref(cs), p, ox, oy,
+                             _ptr(bgv, f32p), _ptr(dl, f32p), lowpass_p, _ptr(grads, f32p),
+                             C.byref(sg))
+    if rc:
+        raise OracleError(rc)
+    return grads[:, :n], scr[:, :n], touched[:n].astype(bool)
+
+
+def adam3d_config(step, total_steps, extent) -> OrAdam3dCfg:
+    c = OrAdam3dCfg()
+    lib().or3d_adam_config(C.byref(c), C.c_int64(step), C.c_int64(total_steps), C.c_double(extent))
+    return c
+
+
+def adam3d_step(params, grads, m, v, cfg: OrAdam3dCfg):
+    """In place on float32 [59, n] arrays."""
+    n = params.shape[1]
+    for a in (params, grads, m, v):
+        assert a.dtype == np.float32 and a.flags.c_contiguous
+    lib().or3d_adam_step(_ptr(params, f32p), _ptr(grads, f32p), _ptr(m, f32p), _ptr(v, f32p),
+                         C.c_int64(n), C.byref(cfg))

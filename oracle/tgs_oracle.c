@@ -276,20 +276,41 @@ static int build_stage(const or_scene* s, int lowpass_p, int W, int H, stage_t* 
     return 0;
 }
 
+/* Stage over splats that are already prepared and in blend order (the 3-D front end, ewa3d.c). */
+static void stage_from_prepared(const or_prepared* src, int64_t n, int W, int H, stage_t* st) {
+    memset(st, 0, sizeof(*st));
+    const size_t nn = (size_t)(n ? n : 1);
+    st->n = n;
+    st->buf = (float*)malloc(sizeof(float) * 11 * nn);
+    st->orig = (uint32_t*)malloc(sizeof(uint32_t) * nn);
+    float* b = st->buf;
+    or_prepared* sp = &st->sp;
+    sp->mx = b; sp->my = b + nn; sp->i00 = b + 2 * nn; sp->i01 = b + 3 * nn;
+    sp->i11 = b + 4 * nn; sp->alpha = b + 5 * nn; sp->c0 = b + 6 * nn; sp->c1 = b + 7 * nn;
+    sp->c2 = b + 8 * nn; sp->rx = b + 9 * nn; sp->ry = b + 10 * nn; sp->orig = st->orig;
+    const float* s[11] = {src->mx, src->my, src->i00, src->i01, src->i11, src->alpha,
+                          src->c0, src->c1, src->c2, src->rx, src->ry};
+    for (int q = 0; q < 11; ++q) memcpy(b + q * nn, s[q], sizeof(float) * (size_t)n);
+    memcpy(st->orig, src->orig, sizeof(uint32_t) * (size_t)n);
+    st->tiles_x = (W + TILE - 1) / TILE;
+    st->tiles_y = (H + TILE - 1) / TILE;
+    st->offsets = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(st->tiles_x * st->tiles_y + 1));
+    or_tile_grid(sp, n, W, H, st->offsets, NULL, 0, &st->k);
+    st->items = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(st->k ? st->k : 1));
+    or_tile_grid(sp, n, W, H, st->offsets, st->items, st->k, &st->k);
+}
+
 static void free_stage(stage_t* st) {
     free(st->buf); free(st->orig); free(st->offsets); free(st->items);
 }
 
 /* ---------------------------------------------------------------- render */
 /* walk_pixel rasterizer.cpp:108-136 + render rasterizer.cpp:144-184. */
-int or_render(const or_scene* s, int p, int ox, int oy, int W, int H, const float* bg,
-              int lowpass_p, float* out_rgb, float* out_T, uint64_t* out_ops,
-              uint64_t* out_evals) {
-    pattern_t pt;
-    if (make_pattern(p, ox, oy, W, H, &pt)) return 1;
-    stage_t st;
-    int rc = build_stage(s, lowpass_p > 0 ? lowpass_p : p, W, H, &st);
-    if (rc) { free_stage(&st); return rc; }
+static void render_stage(const stage_t* stp, const pattern_t* ptp, const float* bg, float* out_rgb,
+                         float* out_T, uint64_t* out_ops, uint64_t* out_evals) {
+    const stage_t st = *stp;
+    const pattern_t pt = *ptp;
+    const int p = pt.p, ox = pt.ox, oy = pt.oy, W = pt.W, H = pt.H;
     const or_prepared* sp = &st.sp;
     const int P = pt.cols * pt.rows;
     for (int i = 0; i < P; ++i) {
@@ -341,6 +362,29 @@ int or_render(const or_scene* s, int p, int ox, int oy, int W, int H, const floa
     }
     if (out_ops) *out_ops = ops;
     if (out_evals) *out_evals = evals;
+}
+
+int or_render(const or_scene* s, int p, int ox, int oy, int W, int H, const float* bg,
+              int lowpass_p, float* out_rgb, float* out_T, uint64_t* out_ops,
+              uint64_t* out_evals) {
+    pattern_t pt;
+    if (make_pattern(p, ox, oy, W, H, &pt)) return 1;
+    stage_t st;
+    int rc = build_stage(s, lowpass_p > 0 ? lowpass_p : p, W, H, &st);
+    if (rc) { free_stage(&st); return rc; }
+    render_stage(&st, &pt, bg, out_rgb, out_T, out_ops, out_evals);
+    free_stage(&st);
+    return 0;
+}
+
+int or_render_prepared(const or_prepared* sp, int64_t n, int p, int ox, int oy, int W, int H,
+                       const float* bg, float* out_rgb, float* out_T, uint64_t* out_ops,
+                       uint64_t* out_evals) {
+    pattern_t pt;
+    if (make_pattern(p, ox, oy, W, H, &pt)) return 1;
+    stage_t st;
+    stage_from_prepared(sp, n, W, H, &st);
+    render_stage(&st, &pt, bg, out_rgb, out_T, out_ops, out_evals);
     free_stage(&st);
     return 0;
 }
@@ -353,20 +397,14 @@ typedef struct {
     float dx, dy, g, sigma, trans, w;
 } contrib_t;
 
-int or_backward(or_scene* s, int p, int ox, int oy, int W, int H, const float* bg,
-                const float* dLdC, int lowpass_p, float* const* grads, or_screen_grads* screen,
-                int update_stats) {
-    pattern_t pt;
-    if (make_pattern(p, ox, oy, W, H, &pt)) return 1;
-    stage_t st;
-    int rc = build_stage(s, lowpass_p > 0 ? lowpass_p : p, W, H, &st);
-    if (rc) { free_stage(&st); return rc; }
+/* Tile phase + tile-order merge over a built stage: acc[10][nn] (gmx gmy s00 s01 s11 alpha c0 c1
+ * c2 maxw) and touched[nn], indexed by the splats' orig index, zero-initialised by the caller. */
+static void backward_stage(const stage_t* stp, const pattern_t* ptp, const float* bg,
+                           const float* dLdC, float* acc, uint8_t* touched, size_t nn) {
+    const stage_t st = *stp;
+    const pattern_t pt = *ptp;
+    const int p = pt.p, ox = pt.ox, oy = pt.oy, W = pt.W, H = pt.H;
     const or_prepared* sp = &st.sp;
-    const int64_t n = s->n;
-    const size_t nn = (size_t)(n ? n : 1);
-    /* per-Gaussian merged sums: gmx gmy s00 s01 s11 alpha c0 c1 c2 maxw */
-    float* acc = (float*)calloc(10 * nn, sizeof(float));
-    uint8_t* touched = (uint8_t*)calloc(nn, 1);
     /* tile-local accumulators, sized to the longest list */
     uint32_t maxc = 0;
     for (int t = 0; t < st.tiles_x * st.tiles_y; ++t) {
@@ -454,6 +492,42 @@ int or_backward(or_scene* s, int p, int ox, int oy, int W, int H, const float* b
         }
     }
     free(loc); free(ltouch); free(cb);
+}
+
+int or_backward_prepared(const or_prepared* sp, int64_t n, int64_t n_orig, int p, int ox, int oy,
+                         int W, int H, const float* bg, const float* dLdC, or_screen_grads* screen) {
+    pattern_t pt;
+    if (make_pattern(p, ox, oy, W, H, &pt)) return 1;
+    stage_t st;
+    stage_from_prepared(sp, n, W, H, &st);
+    const size_t nn = (size_t)(n_orig ? n_orig : 1);
+    float* acc = (float*)calloc(10 * nn, sizeof(float));
+    uint8_t* touched = (uint8_t*)calloc(nn, 1);
+    backward_stage(&st, &pt, bg, dLdC, acc, touched, nn);
+    float* dst[10] = {screen->gmx, screen->gmy, screen->gs00, screen->gs01, screen->gs11,
+                      screen->galpha, screen->gc0, screen->gc1, screen->gc2, screen->maxw};
+    for (int q = 0; q < 10; ++q)
+        if (dst[q]) memcpy(dst[q], acc + q * nn, sizeof(float) * (size_t)n_orig);
+    if (screen->touched) memcpy(screen->touched, touched, (size_t)n_orig);
+    free(acc); free(touched);
+    free_stage(&st);
+    return 0;
+}
+
+int or_backward(or_scene* s, int p, int ox, int oy, int W, int H, const float* bg,
+                const float* dLdC, int lowpass_p, float* const* grads, or_screen_grads* screen,
+                int update_stats) {
+    pattern_t pt;
+    if (make_pattern(p, ox, oy, W, H, &pt)) return 1;
+    stage_t st;
+    int rc = build_stage(s, lowpass_p > 0 ? lowpass_p : p, W, H, &st);
+    if (rc) { free_stage(&st); return rc; }
+    const int64_t n = s->n;
+    const size_t nn = (size_t)(n ? n : 1);
+    /* per-Gaussian merged sums: gmx gmy s00 s01 s11 alpha c0 c1 c2 maxw */
+    float* acc = (float*)calloc(10 * nn, sizeof(float));
+    uint8_t* touched = (uint8_t*)calloc(nn, 1);
+    backward_stage(&st, &pt, bg, dLdC, acc, touched, nn);
 
     for (int q = 0; q < 9; ++q)
         for (int64_t i = 0; i < n; ++i) grads[q][i] = 0.f;

@@ -125,6 +125,47 @@ void or_budget_update(or_budget* b, int64_t t);
 int64_t or_budget_at(const or_budget* b, double t_norm);
 double or_budget_t_norm(int64_t step, int64_t warmup, int64_t densify_end);
 
+
+/* Blend stages over splats already prepared in blend order (orig = index into n_orig). */
+int or_render_prepared(const or_prepared* sp, int64_t n, int p, int ox, int oy, int W, int H,
+                       const float* bg, float* out_rgb, float* out_T, uint64_t* out_ops,
+                       uint64_t* out_evals);
+int or_backward_prepared(const or_prepared* sp, int64_t n, int64_t n_orig, int p, int ox, int oy,
+                         int W, int H, const float* bg, const float* dLdC, or_screen_grads* screen);
+
+/* ---------------- 3-D front end (ewa3d.c; SURVEY.md §8a A3b — parity unpinned at the
+ * reference, which has no 3-D code; pinned by formula KATs and FP64 finite differences) */
+#define OR3D_PARAMS 59
+typedef struct {
+    double R[9]; /* world -> camera rotation, row-major */
+    double t[3];
+    double fx, fy, cx, cy, znear;
+    int W, H;
+} or_camera;
+void or3d_sh_basis(double x, double y, double z, double* b, double* db);
+/* out[12]: u v s00 s01 s11 (Σ' incl. bump) alpha r g b depth rx ry; 1 visible, 0 culled, -1 invalid */
+int or3d_project(const double* theta, const or_camera* cam, double bump, double* out);
+/* screen[9]: d(u, v), dΣ'(00, 01, 11; symmetric convention), d alpha, d rgb -> grad[59] */
+void or3d_chain(const double* theta, const or_camera* cam, double bump, const double* screen,
+                double* grad);
+int or3d_prepare(const float* params, int64_t n, const or_camera* cam, int lowpass_p,
+                 or_prepared* out, float* depth_out, int64_t* out_visible);
+int or3d_render(const float* params, int64_t n, const or_camera* cam, int p, int ox, int oy,
+                const float* bg, int lowpass_p, float* out_rgb, float* out_T, uint64_t* out_ops,
+                uint64_t* out_evals);
+int or3d_backward(const float* params, int64_t n, const or_camera* cam, int p, int ox, int oy,
+                  const float* bg, const float* dLdC, int lowpass_p, float* grads,
+                  or_screen_grads* screen);
+typedef struct {
+    float beta1, beta2, eps;
+    float lr_pos, lr_rot, lr_scale, lr_opacity, lr_dc, lr_rest;
+    float bc1, bc2, raw_cap;
+} or3d_adam_cfg;
+void or3d_adam_config(or3d_adam_cfg* c, int64_t step, int64_t total_steps, double extent);
+float or3d_lr(const or3d_adam_cfg* c, int k);
+void or3d_adam_step(float* params, const float* grads, float* m, float* v, int64_t n,
+                    const or3d_adam_cfg* c);
+
 #ifdef __cplusplus
 }
 #endif

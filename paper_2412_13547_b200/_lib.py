@@ -63,6 +63,16 @@ class TrainReport(C.Structure):
                 ("dilated", C.c_int32)]
 
 
+class Camera3(C.Structure):
+    _fields_ = [("R", C.c_float * 9), ("t", C.c_float * 3), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("znear", C.c_float), ("width", C.c_int32),
+                ("height", C.c_int32)]
+
+
+class Adam3dArgs(C.Structure):
+    _fields_ = [("step", C.c_int64), ("total_steps", C.c_int64), ("scene_extent", C.c_double)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "tgsx_create": (C.c_int32, [C.c_int32, P(vp)]),
@@ -129,6 +139,19 @@ SIGNATURES = {
     "tgsx_stage_counters": (C.c_int32, [vp, u64p, u64p, u64p]),
     "tgsx_sort_pairs": (C.c_int32, [vp, vp, vp, C.c_int64, C.c_int32]),
     "tgsx_exclusive_scan": (C.c_int32, [vp, vp, vp, C.c_int64, u64p]),
+    # 3-D front end
+    "tgsx_model3d_create": (C.c_int32, [vp, C.c_int64, P(vp)]),
+    "tgsx_model3d_destroy": (None, [vp]),
+    "tgsx_model3d_size": (C.c_int64, [vp]),
+    "tgsx_model3d_upload": (C.c_int32, [vp, vp, vp, C.c_int64]),
+    "tgsx_model3d_download": (C.c_int32, [vp, vp, vp, vp, vp, vp]),
+    "tgsx_model3d_download_moments": (C.c_int32, [vp, vp, vp, vp]),
+    "tgsx_render3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, C.c_int32, vp, vp, u64p]),
+    "tgsx_backward3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, C.c_int32, vp, C.c_int64,
+                                    vp, vp, C.c_int32]),
+    "tgsx_adam3d_step": (C.c_int32, [vp, vp, vp, P(Adam3dArgs)]),
+    "tgsx_fit_step3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, vp, P(Adam3dArgs), vp]),
+    "tgsx_stage_prepare3d": (C.c_int32, [vp, vp, P(Camera3), C.c_int32, vp, vp]),
 }
 
 _LIB = None

@@ -303,10 +303,10 @@ bool force_onesweep() {
 }
 
 // Per-tile sort of the slabs for lists up to `cap` entries (the template is chosen from it).
-int32_t slab_sort(tgsx_ctx* ctx, tgsx_model* m, int tiles, uint64_t cap) {
+int32_t slab_sort(tgsx_ctx* ctx, int64_t n, int tiles, uint64_t cap) {
     {
         StageTimer t(ctx, kStDuplicate);
-        CK(launch_pair_base(ctx, m));
+        CK(launch_pair_base(ctx, n));
     }
     {
         StageTimer t(ctx, kStSort);
@@ -316,7 +316,7 @@ int32_t slab_sort(tgsx_ctx* ctx, tgsx_model* m, int tiles, uint64_t cap) {
     return TGSX_OK;
 }
 
-int32_t bin_onesweep(tgsx_ctx* ctx, tgsx_model* m, int W, int H, int64_t K, uint32_t** items,
+int32_t bin_onesweep(tgsx_ctx* ctx, tgsx_model* m, int64_t n, int W, int H, int64_t K, uint32_t** items,
                      uint32_t** sorted_keys);
 
 // Sort (if dirty) -> preprocess (+ per-tile lengths) -> scans -> [read-back of K, errors, the
@@ -356,7 +356,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
         if (!ctx->bin_event) CK(cudaEventCreateWithFlags(&ctx->bin_event, cudaEventDisableTiming));
         CK(cudaEventRecord(ctx->bin_event, ctx->stream));
         const uint64_t guess = std::min<uint64_t>(kSegCap, ctx->bin_max_hint + ctx->bin_max_hint / 4);
-        int32_t rc = slab_sort(ctx, m, tiles, guess);
+        int32_t rc = slab_sort(ctx, m->n, tiles, guess);
         if (rc) return rc;
         ctx->bin_pending = true;
         *items = ws.tile_slab.as<uint32_t>();
@@ -376,13 +376,13 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
     if (max_list <= (uint64_t)kSegCap && !force_onesweep()) {
         // slab binning: every tile's list was claimed by preprocess into its slab; sort each slab
         // back into blend order (one warp per tile)
-        rc = slab_sort(ctx, m, tiles, max_list);
+        rc = slab_sort(ctx, m->n, tiles, max_list);
         if (rc) return rc;
         *items = ws.tile_slab.as<uint32_t>();
         if (sorted_keys) *sorted_keys = nullptr;
         return TGSX_OK;
     }
-    return bin_onesweep(ctx, m, W, H, K, items, sorted_keys);
+    return bin_onesweep(ctx, m, m->n, W, H, K, items, sorted_keys);
 }
 
 // Completes a deferred binning: waits for the counters, reports kernel errors, sizes the
@@ -408,11 +408,11 @@ int32_t bin_settle(tgsx_ctx* ctx, tgsx_model* m, int W, int H, uint32_t** items,
     if (max_list <= (uint64_t)ctx->bin_sort_cap) return TGSX_OK;
     *redo = true;
     if (max_list <= (uint64_t)kSegCap) {
-        rc = slab_sort(ctx, m, ws.tiles_x * ws.tiles_y, max_list);
+        rc = slab_sort(ctx, m->n, ws.tiles_x * ws.tiles_y, max_list);
         if (rc) return rc;
         *items = ws.tile_slab.as<uint32_t>();
     } else {
-        rc = bin_onesweep(ctx, m, W, H, K, items, nullptr);
+        rc = bin_onesweep(ctx, m, m->n, W, H, K, items, nullptr);
         if (rc) return rc;
     }
     if (ctx->bin_valid) ctx->bin_items = *items;
@@ -421,7 +421,8 @@ int32_t bin_settle(tgsx_ctx* ctx, tgsx_model* m, int W, int H, uint32_t** items,
 
 // Onesweep path (a list longer than the slab, or TGSX_BINNING=onesweep): duplicate keys,
 // radix sort by tile (stable: blend order inside a tile), ranges.
-int32_t bin_onesweep(tgsx_ctx* ctx, tgsx_model* m, int W, int H, int64_t K, uint32_t** items,
+// m may be null (3-D front end): the debug checks of the blend permutation are then skipped.
+int32_t bin_onesweep(tgsx_ctx* ctx, tgsx_model* m, int64_t n_splats, int W, int H, int64_t K, uint32_t** items,
                      uint32_t** sorted_keys) {
     Workspace& ws = ctx->ws;
     const int tiles = ws.tiles_x * ws.tiles_y;
@@ -434,9 +435,9 @@ int32_t bin_onesweep(tgsx_ctx* ctx, tgsx_model* m, int W, int H, int64_t K, uint
     CK(ws.sort_tmp.ensure(sort_scratch_bytes(K, key_bits)));
     {
         StageTimer t(ctx, kStDuplicate);
-        CK(launch_duplicate(ctx, m, W, H, key_bits));
+        CK(launch_duplicate(ctx, n_splats, key_bits));
     }
-    const bool dbg = debug_checks();
+    const bool dbg = debug_checks() && m;
     if (dbg) {
         // host validation of every binning stage (TGSX_DEBUG_CHECKS=1)
         const int64_t n = m->n;
@@ -708,6 +709,156 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
             CK(cudaStreamSynchronize(ctx->stream));
     }
     return TGSX_OK;
+}
+
+// ============================================================================ 3-D front end
+// preprocess3d -> depth sort (onesweep, 32-bit keys) -> rank-order
+// gather + slab claims -> the 2-D path's scan / per-tile sort / blend kernels -> chain3d.
+
+int32_t make_cam3(tgsx_ctx* ctx, const tgsx_camera* c, const tgsx_pattern* pat, Cam3* out) {
+    if (!c) return fail(ctx, TGSX_EINVAL, "camera is null");
+    if (pat && (c->width != pat->width || c->height != pat->height))
+        return fail(ctx, TGSX_EINVAL, "camera size does not match the pattern size");
+    if (!(c->fx > 0.f) || !(c->fy > 0.f) || !(c->znear > 0.f) || !std::isfinite(c->fx) ||
+        !std::isfinite(c->fy) || !std::isfinite(c->cx) || !std::isfinite(c->cy) || c->width < 1 ||
+        c->height < 1)
+        return fail(ctx, TGSX_EINVAL, "camera: fx, fy, znear must be positive and finite");
+    Cam3 k{};
+    for (int i = 0; i < 9; ++i) k.R[i] = c->R[i];
+    for (int i = 0; i < 3; ++i) k.t[i] = c->t[i];
+    k.fx = c->fx; k.fy = c->fy; k.cx = c->cx; k.cy = c->cy; k.znear = c->znear;
+    k.limx = (float)(1.3 * 0.5 * (double)c->width / (double)c->fx);
+    k.limy = (float)(1.3 * 0.5 * (double)c->height / (double)c->fy);
+    for (int j = 0; j < 3; ++j)
+        k.C[j] = (float)(-((double)c->R[j] * c->t[0] + (double)c->R[3 + j] * c->t[1] +
+                           (double)c->R[6 + j] * c->t[2]));
+    *out = k;
+    return TGSX_OK;
+}
+
+int32_t check_kernel_error3d(tgsx_ctx* ctx, unsigned long long err) {
+    if (err == kErrNone) return TGSX_OK;
+    const uint32_t code = (uint32_t)(err & 3u);
+    const unsigned long long row = err >> 2;
+    if (code == 1)
+        return fail(ctx, TGSX_EINVAL, "3-D Gaussian with non-finite parameters or a zero quaternion (row " +
+                                          std::to_string(row) + ")");
+    return fail(ctx, TGSX_ERUNTIME, "projected covariance numerically degenerate (row " + std::to_string(row) + ")");
+}
+
+int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int W, int H,
+              uint32_t** items) {
+    Workspace& ws = ctx->ws;
+    ctx->bin_valid = false;  // the 2-D path's binning reuse never sees these buffers as its own
+    ctx->bin_pending = false;
+    ws.have_forward = false;
+    const int64_t n = m->n;
+    CK(reset_counters(ctx));
+    {
+        StageTimer t(ctx, kStPreprocess);
+        CK(launch_preprocess3d(ctx, m, cam, lowpass_p, W, H));
+    }
+    uint32_t* k = ws.keys[0].as<uint32_t>();
+    uint32_t* v = ws.vals[0].as<uint32_t>();
+    {
+        // blend order of this view: ascending camera depth, ties by row (stable LSD passes)
+        StageTimer t(ctx, kStDepthSort);
+        CK(sort_pairs(ctx, k, v, ws.keys[1].as<uint32_t>(), ws.vals[1].as<uint32_t>(), n, 32, nullptr));
+        CK(launch_bin3d(ctx, m, k, v, W, H));
+    }
+    unsigned long long* counters = ws.counters.as<unsigned long long>();
+    uint32_t* d_total = reinterpret_cast<uint32_t*>(counters + 3);
+    const int tiles = ws.tiles_x * ws.tiles_y;
+    {
+        StageTimer t(ctx, kStScan);
+        CK(launch_exclusive_scan(ctx, ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(), n, d_total));
+        CK(launch_slab_finalize(ctx, tiles));
+    }
+    CK(cudaMemcpyAsync(ws.h_scratch, counters, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->prof.enabled) ctx->prof.harvest();
+    int32_t rc = check_kernel_error3d(ctx, ws.h_scratch[0]);
+    if (rc) return rc;
+    const int64_t K = (int64_t)(uint32_t)(ws.h_scratch[3] & 0xffffffffull);
+    const uint64_t max_list = ws.h_scratch[5];
+    ws.K = K;
+    CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
+    ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
+    if (max_list <= (uint64_t)kSegCap && !force_onesweep()) {
+        rc = slab_sort(ctx, n, tiles, max_list);
+        if (rc) return rc;
+        *items = ws.tile_slab.as<uint32_t>();
+        return TGSX_OK;
+    }
+    return bin_onesweep(ctx, nullptr, n, W, H, K, items, nullptr);
+}
+
+int32_t render3d_core(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, const RenderArgs& ra,
+                      bool fused_loss, uint32_t** items_out) {
+    uint32_t* items = nullptr;
+    int32_t rc = bin3d(ctx, m, cam, ra.lowpass_p, ra.W, ra.H, &items);
+    if (rc) return rc;
+    CK(ensure_pixels(ctx, ra));
+    {
+        StageTimer t(ctx, kStForward);
+        CK(launch_forward(ctx, ra, items, fused_loss));
+    }
+    ctx->ws.have_forward = true;
+    ctx->ws.last_P = ra.P;
+    *items_out = items;
+    return TGSX_OK;
+}
+
+void fill_adam3d(Adam3dCfg& c, const tgsx_adam3d_args* a) {
+    // or3d_adam_config (oracle/ewa3d.c): 3DGS learning rates, SPEC.md:258-267 update
+    c.b1 = 0.9f;
+    c.b2 = 0.999f;
+    c.omb1 = 1.0f - c.b1;
+    c.omb2 = 1.0f - c.b2;
+    c.eps = 1e-15f;
+    const double frac = a->total_steps > 0 ? (double)a->step / (double)a->total_steps : 0.0;
+    c.lr[0] = (float)(1.6e-4 * a->scene_extent * std::pow(0.01, frac));
+    c.lr[1] = 1e-3f;
+    c.lr[2] = 5e-3f;
+    c.lr[3] = 5e-2f;
+    c.lr[4] = 2.5e-3f;
+    c.lr[5] = 2.5e-3f / 20.0f;
+    c.bc1 = (float)(1.0 - std::pow(0.9, (double)a->step));
+    c.bc2 = (float)(1.0 - std::pow(0.999, (double)a->step));
+    c.raw_cap = (float)kRawCap;
+}
+
+cudaError_t model3d_reserve(tgsx_ctx* ctx, tgsx_model3d* m, int64_t cap, bool keep) {
+    if (cap <= m->cap && m->params.p) return cudaSuccess;
+    const int64_t nc = std::max<int64_t>(cap, 1);
+    cudaError_t e;
+    auto regrow = [&](DevBuf& b, int rows, size_t elt) -> cudaError_t {
+        DevBuf nb;
+        cudaError_t er = nb.ensure((size_t)rows * nc * elt);
+        if (er) return er;
+        if (keep && b.p && m->n) {
+            er = cudaMemcpy2DAsync(nb.p, nc * elt, b.p, m->cap * elt, m->n * elt, rows, cudaMemcpyDeviceToDevice,
+                                   ctx->stream);
+            if (er) return er;
+            er = cudaStreamSynchronize(ctx->stream);
+            if (er) return er;
+        }
+        b.release();
+        b = nb;
+        return cudaSuccess;
+    };
+    if ((e = regrow(m->params, k3dParams, 4))) return e;
+    if ((e = regrow(m->m1, k3dParams, 4))) return e;
+    if ((e = regrow(m->m2, k3dParams, 4))) return e;
+    if ((e = regrow(m->pos_acc, 1, 4))) return e;
+    if ((e = regrow(m->col_acc, 1, 4))) return e;
+    if ((e = regrow(m->visit, 1, 4))) return e;
+    if ((e = m->perm.ensure(nc * 4))) return e;
+    if ((e = m->rank_of.ensure(nc * 4))) return e;
+    if ((e = m->prep_row.ensure(nc * sizeof(Prepared)))) return e;
+    m->cap = nc;
+    return cudaSuccess;
 }
 
 }  // namespace
@@ -1218,6 +1369,213 @@ int32_t tgsx_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* out, in
     CK(cudaMemcpyAsync(ctx->ws.h_scratch + 24, d_total, 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (out_total) *out_total = n ? (uint64_t)(uint32_t)ctx->ws.h_scratch[24] : 0;
+    return TGSX_OK;
+}
+
+// ---------------------------------------------------------------- 3-D front end (A3b)
+int32_t tgsx_model3d_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model3d** out) {
+    if (!ctx || !out || capacity < 0) return TGSX_EINVAL;
+    tgsx_model3d* m = new tgsx_model3d();
+    cudaError_t e = model3d_reserve(ctx, m, std::max<int64_t>(capacity, 1), false);
+    if (e) {
+        delete m;
+        return cuda_fail(ctx, e, "tgsx_model3d_create");
+    }
+    *out = m;
+    return TGSX_OK;
+}
+
+void tgsx_model3d_destroy(tgsx_model3d* m) {
+    if (!m) return;
+    DevBuf* bufs[] = {&m->params, &m->m1, &m->m2, &m->pos_acc, &m->col_acc, &m->visit,
+                      &m->perm, &m->rank_of, &m->prep_row};
+    for (DevBuf* b : bufs) b->release();
+    delete m;
+}
+
+int64_t tgsx_model3d_size(const tgsx_model3d* m) { return m ? m->n : 0; }
+
+int32_t tgsx_model3d_upload(tgsx_ctx* ctx, tgsx_model3d* m, const float* params, int64_t n) {
+    if (!ctx || !m || n < 0 || (n && !params)) return fail(ctx, TGSX_EINVAL, "bad 3-D upload arguments");
+    ctx->bin_valid = false;
+    CK(model3d_reserve(ctx, m, n, false));
+    m->n = n;
+    cudaStream_t s = ctx->stream;
+    const int64_t cap = m->cap;
+    if (n) CK(cudaMemcpy2DAsync(m->params.p, cap * 4, params, n * 4, n * 4, k3dParams, cudaMemcpyDefault, s));
+    CK(cudaMemsetAsync(m->m1.p, 0, m->m1.bytes, s));
+    CK(cudaMemsetAsync(m->m2.p, 0, m->m2.bytes, s));
+    CK(cudaMemsetAsync(m->pos_acc.p, 0, m->pos_acc.bytes, s));
+    CK(cudaMemsetAsync(m->col_acc.p, 0, m->col_acc.bytes, s));
+    CK(cudaMemsetAsync(m->visit.p, 0, m->visit.bytes, s));
+    CK(cudaStreamSynchronize(s));
+    return TGSX_OK;
+}
+
+int32_t tgsx_model3d_download(tgsx_ctx* ctx, tgsx_model3d* m, float* params, float* pos_acc,
+                              float* col_acc, int32_t* visits) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    const int64_t n = m->n, cap = m->cap;
+    cudaStream_t s = ctx->stream;
+    if (n) {
+        if (params) CK(cudaMemcpy2DAsync(params, n * 4, m->params.p, cap * 4, n * 4, k3dParams, cudaMemcpyDefault, s));
+        if (pos_acc) CK(cudaMemcpyAsync(pos_acc, m->pos_acc.p, n * 4, cudaMemcpyDefault, s));
+        if (col_acc) CK(cudaMemcpyAsync(col_acc, m->col_acc.p, n * 4, cudaMemcpyDefault, s));
+        if (visits) CK(cudaMemcpyAsync(visits, m->visit.p, n * 4, cudaMemcpyDefault, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return TGSX_OK;
+}
+
+int32_t tgsx_model3d_download_moments(tgsx_ctx* ctx, tgsx_model3d* m, float* m1, float* m2) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    const int64_t n = m->n, cap = m->cap;
+    if (n) {
+        if (m1) CK(cudaMemcpy2DAsync(m1, n * 4, m->m1.p, cap * 4, n * 4, k3dParams, cudaMemcpyDefault, ctx->stream));
+        if (m2) CK(cudaMemcpy2DAsync(m2, n * 4, m->m2.p, cap * 4, n * 4, k3dParams, cudaMemcpyDefault, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+int32_t tgsx_render3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                      const float bg[3], int32_t lowpass_p, float* out_rgb, float* out_T,
+                      uint64_t* out_blend_ops) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    int32_t rc = check_pattern(ctx, pat);
+    if (rc) return rc;
+    Cam3 c3;
+    if ((rc = make_cam3(ctx, cam, pat, &c3))) return rc;
+    RenderArgs ra = make_args(pat, bg, lowpass_p);
+    uint32_t* items = nullptr;
+    if ((rc = render3d_core(ctx, m, c3, ra, false, &items))) return rc;
+    Workspace& ws = ctx->ws;
+    if (out_rgb && ra.P) CK(cudaMemcpyAsync(out_rgb, ws.rgb.p, (size_t)ra.P * 12, cudaMemcpyDefault, ctx->stream));
+    if (out_T && ra.P) CK(cudaMemcpyAsync(out_T, ws.T.p, (size_t)ra.P * 4, cudaMemcpyDefault, ctx->stream));
+    if (out_blend_ops)
+        CK(cudaMemcpyAsync(ws.h_scratch + 8, ws.counters.as<unsigned long long>() + 1, 8,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (out_blend_ops) *out_blend_ops = ws.h_scratch[8];
+    return TGSX_OK;
+}
+
+int32_t tgsx_backward3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                        const float bg[3], int32_t lowpass_p, const float* dLdC, int64_t dLdC_count,
+                        float* out_grads, float* out_screen, int32_t update_stats) {
+    if (!ctx || !m || !dLdC) return TGSX_EINVAL;
+    int32_t rc = check_pattern(ctx, pat);
+    if (rc) return rc;
+    Cam3 c3;
+    if ((rc = make_cam3(ctx, cam, pat, &c3))) return rc;
+    RenderArgs ra = make_args(pat, bg, lowpass_p);
+    if (dLdC_count != ra.P)
+        return fail(ctx, TGSX_EINVAL, "backward3d: loss-gradient count does not match pattern ranks");
+    uint32_t* items = nullptr;
+    if ((rc = render3d_core(ctx, m, c3, ra, false, &items))) return rc;
+    Workspace& ws = ctx->ws;
+    if (ra.P) CK(cudaMemcpyAsync(ws.dLdC.p, dLdC, (size_t)ra.P * 12, cudaMemcpyDefault, ctx->stream));
+    {
+        StageTimer t(ctx, kStBackward);
+        CK(launch_backward(ctx, ra, items));
+    }
+    const int64_t n = m->n;
+    const size_t gbytes = (size_t)std::max<int64_t>(n, 1) * k3dParams * 4;
+    const size_t sbytes = (size_t)std::max<int64_t>(n, 1) * 10 * 4;
+    CK(ws.generic.ensure(gbytes + sbytes));
+    float* gdev = (out_grads && is_device_ptr(out_grads)) ? out_grads : ws.generic.as<float>();
+    float* sdev = out_screen ? (is_device_ptr(out_screen) ? out_screen : ws.generic.as<float>() + gbytes / 4)
+                             : nullptr;
+    {
+        StageTimer t(ctx, kStChain);
+        CK(launch_chain3d(ctx, m, c3, ra.lowpass_p, false, update_stats != 0, gdev, sdev, nullptr));
+    }
+    if (out_grads && gdev != out_grads && n)
+        CK(cudaMemcpyAsync(out_grads, gdev, (size_t)n * k3dParams * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out_screen && sdev != out_screen && n)
+        CK(cudaMemcpyAsync(out_screen, sdev, (size_t)n * 40, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+int32_t tgsx_adam3d_step(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, const tgsx_adam3d_args* a) {
+    if (!ctx || !m || !grads || !a) return TGSX_EINVAL;
+    if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
+    Adam3dCfg c;
+    fill_adam3d(c, a);
+    const float* g = nullptr;
+    int32_t rc = stage_input(ctx, ctx->ws.generic, grads, (size_t)std::max<int64_t>(m->n, 1) * k3dParams * 4, &g);
+    if (rc) return rc;
+    CK(launch_adam3d(ctx, m, g, c));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+int32_t tgsx_fit_step3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                        const float bg[3], const float* target, const tgsx_adam3d_args* a, float* out_loss) {
+    if (!ctx || !m || !a) return TGSX_EINVAL;
+    if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
+    int32_t rc = check_pattern(ctx, pat);
+    if (rc) return rc;
+    if (!target) return fail(ctx, TGSX_EINVAL, "target is null");
+    Cam3 c3;
+    if ((rc = make_cam3(ctx, cam, pat, &c3))) return rc;
+    Adam3dCfg cfg;
+    fill_adam3d(cfg, a);
+    RenderArgs ra = make_args(pat, bg, 0);
+    const float lam = (pat->p == 1 && ctx->ssim_weight > 0.f) ? ctx->ssim_weight : 0.f;
+    ra.l1_weight = 1.0f - lam;
+    Workspace& ws = ctx->ws;
+    if ((rc = stage_target(ctx, target, (size_t)ra.W * ra.H * 12, &ra.target))) return rc;
+    uint32_t* items = nullptr;
+    if ((rc = render3d_core(ctx, m, c3, ra, true, &items))) return rc;
+    int nsb = 0;
+    if (lam > 0.f && ra.P > 0) {
+        StageTimer t(ctx, kStLoss);
+        nsb = (int)ssim_blocks(ra.W, ra.H);
+        CK(ws.ssim_abc.ensure((size_t)ra.P * 36));
+        CK(ws.ssim_part.ensure((size_t)nsb * 4));
+        CK(launch_ssim(ctx, ws.rgb.as<float>(), ra.target, ra.W, ra.H, lam, ws.ssim_abc.as<float>(),
+                       ws.ssim_part.as<float>(), ws.dLdC.as<float>()));
+    }
+    if ((rc = mark_target_consumed(ctx))) return rc;
+    {
+        StageTimer t(ctx, kStBackward);
+        CK(launch_backward(ctx, ra, items));
+    }
+    {
+        StageTimer t(ctx, kStChain);
+        CK(launch_chain3d(ctx, m, c3, ra.lowpass_p, true, true, nullptr, nullptr, &cfg));
+    }
+    const int tiles = ws.tiles_x * ws.tiles_y;
+    float* dloss = reinterpret_cast<float*>(ws.counters.as<unsigned long long>() + 4);
+    {
+        StageTimer t(ctx, kStLoss);
+        const double inv = ra.P > 0 ? 1.0 / (3.0 * (double)ra.P) : 0.0;
+        CK(launch_loss_finalize(ctx, ws.block_loss.as<float>(), tiles, (float)((1.0 - lam) * inv),
+                                ws.ssim_part.as<float>(), nsb, lam, inv, dloss));
+    }
+    if (out_loss) {
+        CK(cudaMemcpyAsync(out_loss, dloss, 4, cudaMemcpyDefault, ctx->stream));
+        if (!is_device_ptr(out_loss) && !is_pinned_host_ptr(out_loss)) CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return TGSX_OK;
+}
+
+int32_t tgsx_stage_prepare3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, int32_t lowpass_p,
+                             float* out_records, uint32_t* out_keys) {
+    if (!ctx || !m || lowpass_p < 1) return TGSX_EINVAL;
+    Cam3 c3;
+    int32_t rc = make_cam3(ctx, cam, nullptr, &c3);
+    if (rc) return rc;
+    uint32_t* items = nullptr;
+    if ((rc = bin3d(ctx, m, c3, lowpass_p, cam->width, cam->height, &items))) return rc;
+    const int64_t n = m->n;
+    if (n && out_records) CK(cudaMemcpyAsync(out_records, ctx->ws.prep.p, (size_t)n * sizeof(Prepared),
+                                             cudaMemcpyDefault, ctx->stream));
+    // sorted depth keys of the blend order (culled rows last, key 0xffffffff)
+    if (n && out_keys) CK(cudaMemcpyAsync(out_keys, ctx->ws.keys[0].p, (size_t)n * 4, cudaMemcpyDefault, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return TGSX_OK;
 }
 

@@ -245,9 +245,8 @@ cudaError_t launch_slab_finalize(tgsx_ctx* ctx, int tiles) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_pair_base(tgsx_ctx* ctx, tgsx_model* m) {
+cudaError_t launch_pair_base(tgsx_ctx* ctx, int64_t n) {
     Workspace& ws = ctx->ws;
-    const int64_t n = m->n;
     if (n == 0) return cudaSuccess;
     pair_base_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(ws.prep.as<Prepared>(),
                                                                 ws.pair_off.as<uint32_t>(), n);
@@ -298,11 +297,8 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
     return cudaGetLastError();
 }
 
-cudaError_t launch_duplicate(tgsx_ctx* ctx, tgsx_model* m, int W, int H, int key_bits) {
+cudaError_t launch_duplicate(tgsx_ctx* ctx, int64_t n, int key_bits) {
     Workspace& ws = ctx->ws;
-    const int64_t n = m->n;
-    (void)W;
-    (void)H;
     const int passes = (key_bits + 7) / 8;
     cudaError_t e;
     // histogram lives at the head of sort_tmp (sort_pairs reads it from there)

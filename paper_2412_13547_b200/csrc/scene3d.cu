@@ -1,0 +1,564 @@
+// 3-D front end of the fit hot path (BASELINE.json north_star item 1):
+// per-Gaussian EWA projection to a 2-D covariance, SH-degree-3 colour, near-plane / tile-rect
+// culling, and the chain rule from the blend's screen-space sums back to the 3-D parameters,
+// fused with Adam. Everything between the 2-D record and the screen-space sums — tile binning,
+// blend forward / backward, L1 — is the 2-D path's own kernels unchanged (raster.cu, sort.cu,
+// blend.cu): the 3-D front end produces the same 64-B Prepared records in blend order.
+//
+// The reference is 2-D only: this row follows the published 3DGS algorithm,
+// restated in FP64 by oracle/ewa3d.c (parity unpinned at the reference; the oracle is pinned
+// by formula known-answers and finite differences, tests/test_oracle3d.py).
+//
+//  preprocess3d_kernel  one thread per Gaussian, SoA [59][cap] reads (coalesced), writes the
+//                       record in row order + the (depth key, row) pair for the blend sort
+//  bin3d_kernel         one thread per blend rank after the depth sort: gathers the row's
+//                       record into rank order, tile rectangle + slab slot claims (as the 2-D
+//                       preprocess does), perm / rank_of
+//  chain3d_kernel       one thread per Gaussian (row order): tile-order merge of the pair
+//                       partials, chain rule to mean / quaternion / log-scales / opacity / 48 SH
+//                       coefficients, densify statistics, fused Adam (or gradients out)
+//
+// FP32 throughout (contraction allowed): no bit-exactness claim except Adam given equal
+// gradients (explicit _rn ops, the oracle's order).
+#include "tgsx_device.cuh"
+#include "tgsx_internal.h"
+
+#include <algorithm>
+
+namespace tgsx {
+
+namespace {
+
+constexpr int kFillStride = 32;  // as raster.cu: one slot cursor per 128-B line
+constexpr uint32_t kCulledKey = 0xffffffffu;
+
+constexpr float SH_C0 = 0.28209479177387814f;
+constexpr float SH_C1 = 0.4886025119029199f;
+constexpr float SH_C2_0 = 1.0925484305920792f, SH_C2_1 = -1.0925484305920792f,
+                SH_C2_2 = 0.31539156525252005f, SH_C2_3 = -1.0925484305920792f,
+                SH_C2_4 = 0.5462742152960396f;
+constexpr float SH_C3_0 = -0.5900435899266435f, SH_C3_1 = 2.890611442640554f,
+                SH_C3_2 = -0.4570457994644658f, SH_C3_3 = 0.3731763325901154f,
+                SH_C3_4 = -0.4570457994644658f, SH_C3_5 = 1.445305721320277f,
+                SH_C3_6 = -0.5900435899266435f;
+
+__device__ __forceinline__ void sh_basis(float x, float y, float z, float (&b)[16]) {
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    b[0] = SH_C0;
+    b[1] = -SH_C1 * y;
+    b[2] = SH_C1 * z;
+    b[3] = -SH_C1 * x;
+    b[4] = SH_C2_0 * xy;
+    b[5] = SH_C2_1 * yz;
+    b[6] = SH_C2_2 * (2.f * zz - xx - yy);
+    b[7] = SH_C2_3 * xz;
+    b[8] = SH_C2_4 * (xx - yy);
+    b[9] = SH_C3_0 * y * (3.f * xx - yy);
+    b[10] = SH_C3_1 * xy * z;
+    b[11] = SH_C3_2 * y * (4.f * zz - xx - yy);
+    b[12] = SH_C3_3 * z * (2.f * zz - 3.f * xx - 3.f * yy);
+    b[13] = SH_C3_4 * x * (4.f * zz - xx - yy);
+    b[14] = SH_C3_5 * z * (xx - yy);
+    b[15] = SH_C3_6 * x * (xx - 3.f * yy);
+}
+
+// d/d(dir) of sum_k w_k b_k(dir) (dir components treated as independent)
+__device__ __forceinline__ void sh_basis_grad(float x, float y, float z, const float (&w)[16],
+                                              float& gx, float& gy, float& gz) {
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    gx = -SH_C1 * w[3] + SH_C2_0 * y * w[4] - 2.f * SH_C2_2 * x * w[6] + SH_C2_3 * z * w[7] +
+         2.f * SH_C2_4 * x * w[8] + 6.f * SH_C3_0 * xy * w[9] + SH_C3_1 * yz * w[10] -
+         2.f * SH_C3_2 * xy * w[11] - 6.f * SH_C3_3 * xz * w[12] +
+         SH_C3_4 * (4.f * zz - 3.f * xx - yy) * w[13] + 2.f * SH_C3_5 * xz * w[14] +
+         SH_C3_6 * (3.f * xx - 3.f * yy) * w[15];
+    gy = -SH_C1 * w[1] + SH_C2_0 * x * w[4] + SH_C2_1 * z * w[5] - 2.f * SH_C2_2 * y * w[6] -
+         2.f * SH_C2_4 * y * w[8] + SH_C3_0 * (3.f * xx - 3.f * yy) * w[9] + SH_C3_1 * xz * w[10] +
+         SH_C3_2 * (4.f * zz - xx - 3.f * yy) * w[11] - 6.f * SH_C3_3 * yz * w[12] -
+         2.f * SH_C3_4 * xy * w[13] - 2.f * SH_C3_5 * yz * w[14] - 6.f * SH_C3_6 * xy * w[15];
+    gz = SH_C1 * w[2] + SH_C2_1 * y * w[5] + 4.f * SH_C2_2 * z * w[6] + SH_C2_3 * x * w[7] +
+         SH_C3_1 * xy * w[10] + 8.f * SH_C3_2 * yz * w[11] +
+         SH_C3_3 * (6.f * zz - 3.f * xx - 3.f * yy) * w[12] + 8.f * SH_C3_4 * xz * w[13] +
+         SH_C3_5 * (xx - yy) * w[14];
+}
+
+// Geometry of one Gaussian (everything the chain rule needs again).
+struct Geo3 {
+    float tc[3], iz, cxz, cyz;
+    bool clx, cly;
+    float T[2][3];
+    float qn[4], qinv;
+    float Rq[3][3], s[3], M[3][3];
+    float S3[3][3];
+    float s00, s01, s11;
+};
+
+// Returns false when culled by the near plane. Requires finite inputs.
+__device__ __forceinline__ bool geometry(const Cam3& cam, float bump, const float (&mu)[3],
+                                         const float (&q)[4], const float (&ls)[3], Geo3& g) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        g.tc[i] = cam.R[3 * i] * mu[0] + cam.R[3 * i + 1] * mu[1] + cam.R[3 * i + 2] * mu[2] + cam.t[i];
+    if (!(g.tc[2] > cam.znear)) return false;
+    g.iz = 1.0f / g.tc[2];
+    const float rx = g.tc[0] * g.iz, ry = g.tc[1] * g.iz;
+    g.clx = rx < -cam.limx || rx > cam.limx;
+    g.cly = ry < -cam.limy || ry > cam.limy;
+    g.cxz = fminf(fmaxf(rx, -cam.limx), cam.limx);
+    g.cyz = fminf(fmaxf(ry, -cam.limy), cam.limy);
+    const float J00 = cam.fx * g.iz, J02 = -cam.fx * g.cxz * g.iz;
+    const float J11 = cam.fy * g.iz, J12 = -cam.fy * g.cyz * g.iz;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        g.T[0][j] = J00 * cam.R[j] + J02 * cam.R[6 + j];
+        g.T[1][j] = J11 * cam.R[3 + j] + J12 * cam.R[6 + j];
+    }
+    const float qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
+    g.qinv = rsqrtf(qq);
+    const float r = q[0] * g.qinv, x = q[1] * g.qinv, y = q[2] * g.qinv, z = q[3] * g.qinv;
+    g.qn[0] = r; g.qn[1] = x; g.qn[2] = y; g.qn[3] = z;
+    g.Rq[0][0] = 1.f - 2.f * (y * y + z * z); g.Rq[0][1] = 2.f * (x * y - r * z); g.Rq[0][2] = 2.f * (x * z + r * y);
+    g.Rq[1][0] = 2.f * (x * y + r * z); g.Rq[1][1] = 1.f - 2.f * (x * x + z * z); g.Rq[1][2] = 2.f * (y * z - r * x);
+    g.Rq[2][0] = 2.f * (x * z - r * y); g.Rq[2][1] = 2.f * (y * z + r * x); g.Rq[2][2] = 1.f - 2.f * (x * x + y * y);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) g.s[j] = expf(ls[j]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) g.M[i][j] = g.Rq[i][j] * g.s[j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            g.S3[i][j] = g.M[i][0] * g.M[j][0] + g.M[i][1] * g.M[j][1] + g.M[i][2] * g.M[j][2];
+    float U[2][3];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            U[i][j] = g.T[i][0] * g.S3[0][j] + g.T[i][1] * g.S3[1][j] + g.T[i][2] * g.S3[2][j];
+    g.s00 = U[0][0] * g.T[0][0] + U[0][1] * g.T[0][1] + U[0][2] * g.T[0][2] + bump;
+    g.s01 = U[0][0] * g.T[1][0] + U[0][1] * g.T[1][1] + U[0][2] * g.T[1][2];
+    g.s11 = U[1][0] * g.T[1][0] + U[1][1] * g.T[1][1] + U[1][2] * g.T[1][2] + bump;
+    return true;
+}
+
+__device__ __forceinline__ void view_dir(const Cam3& cam, const float (&mu)[3], float (&d)[3],
+                                         float& ilen) {
+    const float dx = mu[0] - cam.C[0], dy = mu[1] - cam.C[1], dz = mu[2] - cam.C[2];
+    ilen = rsqrtf(dx * dx + dy * dy + dz * dz);
+    d[0] = dx * ilen;
+    d[1] = dy * ilen;
+    d[2] = dz * ilen;
+}
+
+__device__ __forceinline__ float sigmoidf(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+// ------------------------------------------------------------------ preprocess
+__global__ void __launch_bounds__(256) preprocess3d_kernel(
+    const float* __restrict__ params, int64_t cap, int64_t n, Cam3 cam, float bump,
+    Prepared* __restrict__ prep_row, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+    unsigned long long* err) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    vals[i] = (uint32_t)i;
+    float mu[3], q[4], ls[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mu[k] = __ldg(params + k * cap + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = __ldg(params + (3 + k) * cap + i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ls[k] = __ldg(params + (7 + k) * cap + i);
+    const float rop = __ldg(params + 10 * cap + i);
+    float sh[48];
+    bool finite = isfinite(rop);
+#pragma unroll
+    for (int k = 0; k < 48; ++k) {
+        sh[k] = __ldg(params + (11 + k) * cap + i);
+        finite &= isfinite(sh[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) finite &= isfinite(mu[k]) && isfinite(ls[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) finite &= isfinite(q[k]);
+    finite &= (q[0] != 0.f || q[1] != 0.f || q[2] != 0.f || q[3] != 0.f);
+    if (!finite) {
+        raise_error(err, (uint32_t)i, 1);
+        keys[i] = kCulledKey;
+        return;
+    }
+    Geo3 g;
+    if (!geometry(cam, bump, mu, q, ls, g)) {
+        keys[i] = kCulledKey;
+        return;
+    }
+    const float det = g.s00 * g.s11 - g.s01 * g.s01;
+    if (!(det > 0.0f) || !isfinite(det)) {
+        raise_error(err, (uint32_t)i, 2);
+        keys[i] = kCulledKey;
+        return;
+    }
+    float d[3], ilen;
+    view_dir(cam, mu, d, ilen);
+    float b[16];
+    sh_basis(d[0], d[1], d[2], b);
+    float rgb[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        float acc = 0.5f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc += b[k] * sh[3 * k + c];
+        rgb[c] = fmaxf(acc, 0.0f);
+    }
+    const float idet = 1.0f / det;
+    Prepared o;
+    o.a = make_float4(cam.fx * g.tc[0] * g.iz + cam.cx, cam.fy * g.tc[1] * g.iz + cam.cy,
+                      g.s11 * idet, -g.s01 * idet);
+    o.b = make_float4(g.s00 * idet, sigmoidf(rop), kCullSigmas * sqrtf(g.s00),
+                      kCullSigmas * sqrtf(g.s11));
+    o.c = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float((uint32_t)i));
+    o.d = make_uint4(0u, 0u, 0u, 0u);
+    prep_row[i] = o;
+    keys[i] = __float_as_uint(g.tc[2]) | 0x80000000u;  // positive depth: orderable key
+}
+
+// ------------------------------------------------------------------ rank-order gather + binning
+__global__ void __launch_bounds__(256) bin3d_kernel(
+    const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals, int64_t n,
+    const Prepared* __restrict__ prep_row, int W, int H, int tiles_x, Prepared* __restrict__ prep,
+    uint32_t* __restrict__ touched, uint32_t* __restrict__ fill, uint32_t* __restrict__ slab,
+    uint32_t* __restrict__ perm, uint32_t* __restrict__ rank_of) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t row = svals[r];
+    perm[r] = row;
+    rank_of[row] = (uint32_t)r;
+    if (skeys[r] == kCulledKey) {
+        touched[r] = 0;
+        prep[r].d = make_uint4(0u, 0u, 0u, 0u);
+        return;
+    }
+    Prepared o = prep_row[row];
+    int tx0, tx1, ty0, ty1;
+    uint32_t tiles = 0;
+    if (tile_rect(o.a.x, o.a.y, o.b.z, o.b.w, W, H, tx0, tx1, ty0, ty1)) {
+        tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+        o.d = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16),
+                         0u, tiles);
+        const int w = tx1 - tx0 + 1, cnt = (int)tiles;
+        for (int q0 = 0; q0 < cnt; q0 += 4) {
+            uint32_t pos[4], tt[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (q0 + u < cnt) {
+                    const int q = q0 + u;
+                    tt[u] = (uint32_t)((ty0 + q / w) * tiles_x + tx0 + q % w);
+                    pos[u] = atomicAdd(&fill[(size_t)tt[u] * kFillStride], 1u);
+                }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (q0 + u < cnt && pos[u] < (uint32_t)kSegCap) slab[(size_t)tt[u] * kSegCap + pos[u]] = (uint32_t)r;
+        }
+    } else {
+        o.d = make_uint4(0u, 0u, 0u, 0u);
+    }
+    prep[r] = o;
+    touched[r] = tiles;
+}
+
+// ------------------------------------------------------------------ chain rule (+ Adam)
+__device__ __forceinline__ int adam3d_group(int k) {
+    return k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k == 10 ? 3 : (k < 14 ? 4 : 5))));
+}
+
+// Adam on one component (the oracle's or3d_adam_step order, explicit _rn ops).
+__device__ __forceinline__ void adam3d_one(float* __restrict__ params, float* __restrict__ m1,
+                                           float* __restrict__ m2, int64_t o, float g, float lr,
+                                           bool clamp, const Adam3dCfg& c) {
+    const float mm = fadd(fmul(c.b1, m1[o]), fmul(c.omb1, g));
+    const float vv = fadd(fmul(c.b2, m2[o]), fmul(fmul(c.omb2, g), g));
+    m1[o] = mm;
+    m2[o] = vv;
+    const float mh = fdiv(mm, c.bc1);
+    const float vh = fdiv(vv, c.bc2);
+    float th = fsub(params[o], fdiv(fmul(lr, mh), fadd(__fsqrt_rn(vh), c.eps)));
+    if (clamp) th = th < -c.raw_cap ? -c.raw_cap : (c.raw_cap < th ? c.raw_cap : th);
+    params[o] = th;
+}
+
+struct Chain3Params {
+    float* params;
+    int64_t cap, n;
+    Cam3 cam;
+    float bump;
+    const uint32_t* rank_of;
+    const uint32_t* pair_off;
+    const uint32_t* touched;
+    Partials partial;
+    int mode;       // 0 gradients out, 1 fused Adam
+    float* grads;   // [59][n] (mode 0)
+    float* screen;  // [10][n] or null
+    float* pos_acc;
+    float* col_acc;
+    int32_t* visit;
+    int update_stats;
+    float* m1;
+    float* m2;
+    Adam3dCfg adam;
+};
+
+__device__ __forceinline__ void emit3d(const Chain3Params& cp, int64_t i, int k, float g) {
+    if (cp.mode == 0) {
+        cp.grads[(int64_t)k * cp.n + i] = g;
+    } else {
+        adam3d_one(cp.params, cp.m1, cp.m2, (int64_t)k * cp.cap + i, g, cp.adam.lr[adam3d_group(k)],
+                   k == 10, cp.adam);
+    }
+}
+
+__global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cp.n) return;
+    const int64_t cap = cp.cap;
+    const float* __restrict__ P = cp.params;
+    const uint32_t r = __ldg(cp.rank_of + i);
+    const uint32_t cnt = __ldg(cp.touched + r);
+    float s[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) s[k] = 0.f;
+    if (cnt) {
+        // tile-order merge (rasterizer.cpp:301-319): the splat's pair slots are contiguous
+        const uint32_t base = __ldg(cp.pair_off + r);
+        const float4* __restrict__ pa = cp.partial.a + base;
+        const float4* __restrict__ pb = cp.partial.b + base;
+        const float2* __restrict__ pc = cp.partial.c + base;
+        for (uint32_t t = 0; t < cnt; ++t) {
+            const float4 a = pa[t], b = pb[t];
+            const float2 c = pc[t];
+            s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
+            s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+            s[8] += c.x;
+            s[9] = fmaxf(s[9], c.y);
+        }
+    }
+    if (cp.screen) {
+#pragma unroll
+        for (int k = 0; k < 10; ++k) cp.screen[(int64_t)k * cp.n + i] = s[k];
+    }
+    float mu[3], q[4], ls[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mu[k] = __ldg(P + k * cap + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = __ldg(P + (3 + k) * cap + i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ls[k] = __ldg(P + (7 + k) * cap + i);
+    const float rop = __ldg(P + 10 * cap + i);
+    Geo3 g;
+    const bool seen = cnt != 0 && geometry(cp.cam, cp.bump, mu, q, ls, g);
+    if (!seen) {
+        // untouched by this view: zero gradient (Adam still advances its moments)
+        for (int k = 0; k < 59; ++k) emit3d(cp, i, k, 0.f);
+        return;
+    }
+    const Cam3& cam = cp.cam;
+    // ---- colour: SH basis, raw colour, clamp mask, SH gradients, direction gradient
+    float d[3], ilen;
+    view_dir(cam, mu, d, ilen);
+    float b[16];
+    sh_basis(d[0], d[1], d[2], b);
+    float sh[48];
+#pragma unroll
+    for (int k = 0; k < 48; ++k) sh[k] = __ldg(P + (11 + k) * cap + i);
+    float dcol[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        float acc = 0.5f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc += b[k] * sh[3 * k + c];
+        dcol[c] = acc < 0.f ? 0.f : s[6 + c];
+    }
+    float w[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) w[k] = dcol[0] * sh[3 * k] + dcol[1] * sh[3 * k + 1] + dcol[2] * sh[3 * k + 2];
+    float gdx, gdy, gdz;
+    sh_basis_grad(d[0], d[1], d[2], w, gdx, gdy, gdz);
+    const float dd = gdx * d[0] + gdy * d[1] + gdz * d[2];
+    float dmu[3] = {(gdx - d[0] * dd) * ilen, (gdy - d[1] * dd) * ilen, (gdz - d[2] * dd) * ilen};
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) emit3d(cp, i, 11 + 3 * k + c, b[k] * dcol[c]);
+    // ---- opacity
+    const float al = sigmoidf(rop);
+    emit3d(cp, i, 10, s[5] * al * (1.f - al));
+    // ---- mean projection + EWA covariance
+    const float fx = cam.fx, fy = cam.fy, iz = g.iz, iz2 = iz * iz;
+    float dt[3];
+    dt[0] = s[0] * fx * iz;
+    dt[1] = s[1] * fy * iz;
+    dt[2] = -(s[0] * fx * g.tc[0] + s[1] * fy * g.tc[1]) * iz2;
+    const float G00 = s[2], G01 = s[3], G11 = s[4];
+    float GT[2][3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        GT[0][j] = G00 * g.T[0][j] + G01 * g.T[1][j];
+        GT[1][j] = G01 * g.T[0][j] + G11 * g.T[1][j];
+    }
+    float dS3[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dS3[a][c] = g.T[0][a] * GT[0][c] + g.T[1][a] * GT[1][c];
+    float dT[2][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            dT[a][j] = 2.f * (GT[a][0] * g.S3[0][j] + GT[a][1] * g.S3[1][j] + GT[a][2] * g.S3[2][j]);
+    const float* R = cam.R;
+    const float dJ00 = dT[0][0] * R[0] + dT[0][1] * R[1] + dT[0][2] * R[2];
+    const float dJ02 = dT[0][0] * R[6] + dT[0][1] * R[7] + dT[0][2] * R[8];
+    const float dJ11 = dT[1][0] * R[3] + dT[1][1] * R[4] + dT[1][2] * R[5];
+    const float dJ12 = dT[1][0] * R[6] + dT[1][1] * R[7] + dT[1][2] * R[8];
+    dt[2] += -fx * iz2 * dJ00 - fy * iz2 * dJ11;
+    if (g.clx) {
+        dt[2] += dJ02 * fx * g.cxz * iz2;
+    } else {
+        dt[0] -= dJ02 * fx * iz2;
+        dt[2] += dJ02 * 2.f * fx * g.cxz * iz2;
+    }
+    if (g.cly) {
+        dt[2] += dJ12 * fy * g.cyz * iz2;
+    } else {
+        dt[1] -= dJ12 * fy * iz2;
+        dt[2] += dJ12 * 2.f * fy * g.cyz * iz2;
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) emit3d(cp, i, j, R[j] * dt[0] + R[3 + j] * dt[1] + R[6 + j] * dt[2] + dmu[j]);
+    // ---- Σ3 = M Mᵀ, M = Rq diag(s)
+    float dR[3][3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        float ds = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float dM = 2.f * (dS3[a][0] * g.M[0][j] + dS3[a][1] * g.M[1][j] + dS3[a][2] * g.M[2][j]);
+            dR[a][j] = dM * g.s[j];
+            ds += dM * g.Rq[a][j];
+        }
+        emit3d(cp, i, 7 + j, ds * g.s[j]);
+    }
+    const float qr = g.qn[0], qx = g.qn[1], qy = g.qn[2], qz = g.qn[3];
+    float dq[4];
+    dq[0] = 2.f * (-qz * dR[0][1] + qy * dR[0][2] + qz * dR[1][0] - qx * dR[1][2] - qy * dR[2][0] + qx * dR[2][1]);
+    dq[1] = 2.f * (qy * dR[0][1] + qz * dR[0][2] + qy * dR[1][0] - 2.f * qx * dR[1][1] - qr * dR[1][2] +
+                   qz * dR[2][0] + qr * dR[2][1] - 2.f * qx * dR[2][2]);
+    dq[2] = 2.f * (-2.f * qy * dR[0][0] + qx * dR[0][1] + qr * dR[0][2] + qx * dR[1][0] + qz * dR[1][2] -
+                   qr * dR[2][0] + qz * dR[2][1] - 2.f * qy * dR[2][2]);
+    dq[3] = 2.f * (-2.f * qz * dR[0][0] - qr * dR[0][1] + qx * dR[0][2] + qr * dR[1][0] - 2.f * qz * dR[1][1] +
+                   qy * dR[1][2] + qx * dR[2][0] + qy * dR[2][1]);
+    const float qd = qr * dq[0] + qx * dq[1] + qy * dq[2] + qz * dq[3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) emit3d(cp, i, 3 + k, (dq[k] - g.qn[k] * qd) * g.qinv);
+    // ---- densify statistics: screen-space position norm, DC colour-gradient norm
+    if (cp.update_stats && s[9] > 0.f) {
+        cp.pos_acc[i] += sqrtf(s[0] * s[0] + s[1] * s[1]);
+        cp.col_acc[i] += SH_C0 * sqrtf(dcol[0] * dcol[0] + dcol[1] * dcol[1] + dcol[2] * dcol[2]);
+        cp.visit[i] += 1;
+    }
+}
+
+// Adam with explicit gradients [59][n] (tgsx_adam3d_step)
+__global__ void __launch_bounds__(256) adam3d_kernel(float* __restrict__ params, float* __restrict__ m1,
+                                                     float* __restrict__ m2, int64_t cap, int64_t n,
+                                                     const float* __restrict__ grads, Adam3dCfg c) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+#pragma unroll
+    for (int k = 0; k < 59; ++k)
+        adam3d_one(params, m1, m2, (int64_t)k * cap + i, grads[(int64_t)k * n + i], c.lr[adam3d_group(k)],
+                   k == 10, c);
+}
+
+inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / bt); }
+
+}  // namespace
+
+cudaError_t launch_adam3d(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, const Adam3dCfg& cfg) {
+    if (m->n == 0) return cudaSuccess;
+    adam3d_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(m->params.as<float>(), m->m1.as<float>(),
+                                                                m->m2.as<float>(), m->cap, m->n, grads, cfg);
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p,
+                                int W, int H) {
+    Workspace& ws = ctx->ws;
+    const int64_t n = m->n;
+    cudaError_t e;
+    const int64_t c = std::max<int64_t>(n, 1);
+    if ((e = ws.prep.ensure(c * sizeof(Prepared)))) return e;
+    if ((e = m->prep_row.ensure(c * sizeof(Prepared)))) return e;
+    if ((e = ws.touched.ensure((c + 1) * 4))) return e;
+    if ((e = ws.pair_off.ensure((c + 1) * 4))) return e;
+    for (int k = 0; k < 2; ++k) {
+        if ((e = ws.keys[k].ensure(c * 4))) return e;
+        if ((e = ws.vals[k].ensure(c * 4))) return e;
+    }
+    ws.tiles_x = (W + kTile - 1) / kTile;
+    ws.tiles_y = (H + kTile - 1) / kTile;
+    const size_t tiles = (size_t)std::max(ws.tiles_x * ws.tiles_y, 1);
+    if ((e = ws.tile_fill.ensure(tiles * 4 * kFillStride))) return e;
+    if ((e = ws.tile_slab.ensure(tiles * 4 * kSegCap))) return e;
+    if ((e = cudaMemsetAsync(ws.tile_fill.p, 0, tiles * 4 * kFillStride, ctx->stream))) return e;
+    if (n == 0) return cudaSuccess;
+    const float bump = 0.3f + 0.5f * (float)(lowpass_p - 1);
+    preprocess3d_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+        m->params.as<float>(), m->cap, n, cam, bump, m->prep_row.as<Prepared>(),
+        ws.keys[0].as<uint32_t>(), ws.vals[0].as<uint32_t>(), ws.counters.as<unsigned long long>());
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const uint32_t* skeys, const uint32_t* svals,
+                         int W, int H) {
+    Workspace& ws = ctx->ws;
+    const int64_t n = m->n;
+    if (n == 0) return cudaSuccess;
+    bin3d_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+        skeys, svals, n, m->prep_row.as<Prepared>(), W, H, ws.tiles_x, ws.prep.as<Prepared>(),
+        ws.touched.as<uint32_t>(), ws.tile_fill.as<uint32_t>(), ws.tile_slab.as<uint32_t>(),
+        m->perm.as<uint32_t>(), m->rank_of.as<uint32_t>());
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, bool adam,
+                           bool update_stats, float* grads, float* screen, const Adam3dCfg* cfg) {
+    if (m->n == 0) return cudaSuccess;
+    Chain3Params cp{};
+    cp.params = m->params.as<float>();
+    cp.cap = m->cap;
+    cp.n = m->n;
+    cp.cam = cam;
+    cp.bump = 0.3f + 0.5f * (float)(lowpass_p - 1);
+    cp.rank_of = m->rank_of.as<uint32_t>();
+    cp.pair_off = ctx->ws.pair_off.as<uint32_t>();
+    cp.touched = ctx->ws.touched.as<uint32_t>();
+    cp.partial = Partials::at(ctx->ws.partial.p, ctx->ws.pair_cap);
+    cp.mode = adam ? 1 : 0;
+    cp.grads = grads;
+    cp.screen = screen;
+    cp.pos_acc = m->pos_acc.as<float>();
+    cp.col_acc = m->col_acc.as<float>();
+    cp.visit = m->visit.as<int32_t>();
+    cp.update_stats = update_stats ? 1 : 0;
+    cp.m1 = m->m1.as<float>();
+    cp.m2 = m->m2.as<float>();
+    if (cfg) cp.adam = *cfg;
+    chain3d_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(cp);
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace tgsx

@@ -144,6 +144,18 @@ struct tgsx_model {
     int64_t step_views = 0;
 };
 
+// 3-D front end model (scene3d.cu): params float[59][cap] = mean(3),
+// quaternion wxyz(4), log-scales(3), raw opacity, SH coefficients [16][3]; row (creation) order.
+struct tgsx_model3d {
+    int64_t n = 0, cap = 0;
+    tgsx::DevBuf params;            // float[59][cap]
+    tgsx::DevBuf m1, m2;            // float[59][cap] Adam moments
+    tgsx::DevBuf pos_acc, col_acc;  // float[cap] densify statistics
+    tgsx::DevBuf visit;             // i32[cap]
+    tgsx::DevBuf perm, rank_of;     // u32[cap] blend order of the last view
+    tgsx::DevBuf prep_row;          // Prepared[cap] records in row order (before the depth sort)
+};
+
 // physical row order of the model (capi.cu): blend order for the hot path, logical (creation)
 // order for densify / download / explicit-gradient APIs
 cudaError_t model_to_blend_order(tgsx_ctx* ctx, tgsx_model* m);
@@ -174,7 +186,7 @@ cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m);
 cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H);
 cudaError_t launch_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n,
                                   uint32_t* d_total);
-cudaError_t launch_duplicate(tgsx_ctx* ctx, tgsx_model* m, int W, int H, int key_bits);
+cudaError_t launch_duplicate(tgsx_ctx* ctx, int64_t n, int key_bits);
 size_t sort_scratch_bytes(int64_t n, int key_bits);
 cudaError_t sort_pairs(tgsx_ctx* ctx, uint32_t*& keys, uint32_t*& vals, uint32_t* keys_alt,
                        uint32_t* vals_alt, int64_t n, int key_bits, const uint32_t* d_hist);
@@ -183,7 +195,7 @@ cudaError_t launch_ranges(tgsx_ctx* ctx, const uint32_t* keys, int64_t K, int ti
 // per-tile warp register sort (lists up to kSegCap; longer lists take the onesweep path)
 constexpr int kSegCap = 1024;
 cudaError_t launch_slab_finalize(tgsx_ctx* ctx, int tiles);
-cudaError_t launch_pair_base(tgsx_ctx* ctx, tgsx_model* m);
+cudaError_t launch_pair_base(tgsx_ctx* ctx, int64_t n);
 cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles, int64_t max_list);
 cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
                            bool fused_loss);
@@ -203,5 +215,24 @@ cudaError_t launch_adam(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const 
                         int batch_views);
 
 int key_bits_for(int tiles);
+
+// 3-D front end (scene3d.cu)
+struct Cam3 {
+    float R[9], t[3];
+    float fx, fy, cx, cy, znear;
+    float limx, limy;  // 1.3 tan(fov / 2) clamp of the EWA Jacobian
+    float C[3];        // camera centre -R^T t
+};
+struct Adam3dCfg {
+    float lr[6];  // mean, rotation, log-scale, opacity, SH DC, SH rest
+    float b1, b2, omb1, omb2, eps, bc1, bc2, raw_cap;
+};
+constexpr int k3dParams = 59;
+cudaError_t launch_preprocess3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int W, int H);
+cudaError_t launch_bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const uint32_t* skeys, const uint32_t* svals,
+                         int W, int H);
+cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, bool adam,
+                           bool update_stats, float* grads, float* screen, const Adam3dCfg* cfg);
+cudaError_t launch_adam3d(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, const Adam3dCfg& cfg);
 
 }  // namespace tgsx
