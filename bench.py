@@ -51,6 +51,10 @@ CONFIGS = {
     "c5": dict(workload="C5: batched-view 4K fitting, 3M Gaussians, 8 views/step (cycled p=2 offsets, "
                         "distinct targets) accumulated + one Adam step; views sharded across ranks",
                n=3_000_000, W=3840, H=2160, p=2, views=8),
+    "c6": dict(workload="C2-3D: synthetic 1M 3-D Gaussians (mean, quaternion, 3 log-scales, SH degree 3), "
+                        "EWA + SH-3 front end (SURVEY.md §8a A3b), 1920x1080 p=1 single-view fit step "
+                        "(preprocess3d + depth sort + binning + fwd + L1 + bwd + chain3d + Adam over 59 params)",
+               n=1_000_000, W=1920, H=1080, p=1, three_d=True),
 }
 METRIC = "fit iters/sec (fwd+bwd+Adam) at 1080p and 4K dilated, 1M–3M Gaussians"
 
@@ -265,8 +269,12 @@ def roofline(stages, counters, clocks, n, config):
                              "(MEASURED_PEAKS.json has no FP32 figure)",
                 "work_note": f"algorithmic flops per launch 2E+{per_blend}Bl with E={E} evaluations, "
                              f"Bl={Bl} blends (SURVEY.md §8d)"}
-    nb = {"chain_adam": 400 * n, "preprocess": 108 * n, "radix_sort": 32 * K,
-          "duplicate": 8 * K + 20 * n}.get(dom, 0)
+    if config == "c6":  # 3-D: chain3d + Adam streams 59 params, 2 moments (r+w), partials
+        nb = {"chain_adam": (59 * 4 * 6 + 24) * n + 40 * K, "preprocess": (59 * 4 + 64 + 8) * n,
+              "depth_sort": 4 * 24 * n + (64 + 64 + 16) * n}.get(dom, 0)
+    else:
+        nb = {"chain_adam": 400 * n, "preprocess": 108 * n, "radix_sort": 32 * K,
+              "duplicate": 8 * K + 20 * n}.get(dom, 0)
     achieved = nb / (dom_ms / 1e3) / 1e9
     return {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
@@ -290,12 +298,13 @@ def run_tgsx(args, cfg):
     if args.ssim > 0:
         ctx.set_ssim_weight(args.ssim)
     stream = torch.cuda.ExternalStream(ctx.L.tgsx_get_stream(ctx.h))
-    host = P.GaussianModel.synthetic(1, n, W, H)
-    dm = P.DeviceModel.from_host(host, ctx)
-    tm = P.DeviceModel.from_host(P.GaussianModel.synthetic(2, n, W, H), ctx)
-    tgt = tm.render(P.DilationPattern(1, 0, 0, W, H)).colors.reshape(H, W, 3)
-    tm.close()
-    base = torch.from_numpy(tgt).cuda()
+    if not cfg.get("three_d"):
+        host = P.GaussianModel.synthetic(1, n, W, H)
+        dm = P.DeviceModel.from_host(host, ctx)
+        tm = P.DeviceModel.from_host(P.GaussianModel.synthetic(2, n, W, H), ctx)
+        tgt = tm.render(P.DilationPattern(1, 0, 0, W, H)).colors.reshape(H, W, 3)
+        tm.close()
+        base = torch.from_numpy(tgt).cuda()
     timer = Timer(torch, stream, dist)
     bg = (C.c_float * 3)(0, 0, 0)
 
@@ -304,7 +313,35 @@ def run_tgsx(args, cfg):
         return (base + 0.02 * torch.randn(base.shape, generator=g, device="cuda")).contiguous()
 
     extra = {}
-    if args.config in ("c2", "c3"):
+    if cfg.get("three_d"):
+        from paper_2412_13547_b200 import scene3d as S3
+        if world > 1:
+            raise SystemExit("c6 (3-D front end) is single-view: run it with --gpus 1")
+        cam = S3.Camera(np.eye(3), np.zeros(3), 0.5 * W / math.tan(math.radians(30)),
+                        0.5 * W / math.tan(math.radians(30)), W / 2, H / 2, W, H)
+        host = S3.GaussianModel3D.synthetic(1, n, cam)
+        dm = S3.DeviceModel3D.from_host(host, ctx)
+        tm3 = S3.DeviceModel3D.from_host(S3.GaussianModel3D.synthetic(2, n, cam), ctx)
+        target = torch.from_numpy(tm3.render(cam).colors.reshape(H, W, 3).copy()).cuda().contiguous()
+        tm3.close()
+        loss_dev = torch.zeros(1, device="cuda")
+        torch.cuda.synchronize()
+        camc = cam.c()
+        extent = 3.0
+
+        def one_step(it, tptr, lptr):
+            pat = P.DilationPattern(1, 0, 0, W, H).c()
+            a = P._lib.Adam3dArgs(it + 1, 10000, extent)
+            ctx.check(ctx.L.tgsx_fit_step3d(ctx.h, dm.h, C.byref(camc), C.byref(pat), bg, tptr, C.byref(a), lptr))
+
+        tptr, lptr = C.c_void_p(target.data_ptr()), C.c_void_p(loss_dev.data_ptr())
+        step_fn = lambda it: one_step(it, tptr, lptr)  # noqa: E731
+        h_target = target.cpu().pin_memory()
+        h_loss = torch.zeros(1).pin_memory()
+        e2e_fn = lambda it: one_step(it, C.c_void_p(h_target.data_ptr()), C.c_void_p(h_loss.data_ptr()))  # noqa: E731
+        e2e_bytes = (W * H * 12, 4)
+        units = 1
+    elif args.config in ("c2", "c3"):
         target = noisy(rank) if world > 1 else base.contiguous()
         loss_dev = torch.zeros(1, device="cuda")
         torch.cuda.synchronize()
@@ -431,7 +468,7 @@ def run_tgsx(args, cfg):
             "config": {"workload": cfg["workload"] + (f"; dense loss (1-{args.ssim}) L1 + {args.ssim} (1-SSIM)"
                                                       if args.ssim > 0 and p == 1 else ""),
                        "gaussians": n, "width": W, "height": H, "p": p,
-                       "views_per_step": units if args.config in ("c2", "c3") else cfg.get("views", 1),
+                       "views_per_step": units if args.config in ("c2", "c3", "c6") else cfg.get("views", 1),
                        "l2": "per-step working set > 126 MB L2 (no explicit flush)"},
             "clocks": clocks,
             "gpu_launches": launches,

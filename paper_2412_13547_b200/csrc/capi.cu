@@ -1388,7 +1388,7 @@ int32_t tgsx_model3d_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model3d** out)
 void tgsx_model3d_destroy(tgsx_model3d* m) {
     if (!m) return;
     DevBuf* bufs[] = {&m->params, &m->m1, &m->m2, &m->pos_acc, &m->col_acc, &m->visit,
-                      &m->perm, &m->rank_of, &m->prep_row};
+                      &m->perm, &m->rank_of, &m->prep_row, &m->gbuf};
     for (DevBuf* b : bufs) b->release();
     delete m;
 }

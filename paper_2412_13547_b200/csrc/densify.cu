@@ -45,8 +45,8 @@ __global__ void select_kernel(const float* __restrict__ params, int64_t cap, int
     float ap = 0.f;
     if (cnt > 0 && (double)visit[i] > tau_v[i] && activate_cr(params[5 * cap + i]) >= c.mask_floor) {
         const float cf = (float)cnt;
-        ap = fdiv(pos_acc[i], cf);
-        const float ac = fdiv(col_acc[i], cf);
+        ap = fdiv_pos(pos_acc[i], cf);
+        const float ac = fdiv_pos(col_acc[i], cf);
         ok = (ap > c.tau_pos) || (coin && ac > c.tau_color);
     }
     flag[i] = ok;

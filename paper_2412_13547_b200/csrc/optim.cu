@@ -32,10 +32,10 @@ __device__ __forceinline__ void adam_update(float* __restrict__ params, float* _
         const float vv = fadd(fmul(c.b2, m2[o]), fmul(fmul(c.omb2, g[q]), g[q]));
         m1[o] = mm;
         m2[o] = vv;
-        const float mh = fdiv(mm, c.bc1);
-        const float vh = fdiv(vv, c.bc2);
+        const float mh = fdiv_pos(mm, c.bc1);
+        const float vh = fdiv_pos(vv, c.bc2);
         float th = params[o];
-        th = fsub(th, fdiv(fmul(c.lr[q], mh), fadd(__fsqrt_rn(vh), c.eps)));
+        th = fsub(th, fdiv_pos(fmul(c.lr[q], mh), fadd(fsqrt_nz(vh), c.eps)));
         if (q == 3 || q == 4) th = clampf(th, c.ls_lo, c.ls_hi);
         if (q >= 5) th = clampf(th, -c.raw_cap, c.raw_cap);
         params[o] = th;
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, f
     if (step) {
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
-            g[q] = fdiv(step[q * cap + i], c.batch);
+            g[q] = fdiv_pos(step[q * cap + i], c.batch);
             step[q * cap + i] = 0.f;
         }
         const float v = step[11 * cap + i];

@@ -60,10 +60,10 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         return;
     }
     Prepared o;
-    o.a = make_float4(px, py, fdiv(s11, det), fdiv(-s01, det));
+    o.a = make_float4(px, py, fdiv_pos(s11, det), fdiv_pos(-s01, det));
     const float rx = fmul(kCullSigmas, __fsqrt_rn(s00));
     const float ry = fmul(kCullSigmas, __fsqrt_rn(s11));
-    o.b = make_float4(fdiv(s00, det), activate_cr(rop), rx, ry);
+    o.b = make_float4(fdiv_pos(s00, det), activate_cr(rop), rx, ry);
     o.c = make_float4(activate_cr(cr), activate_cr(cg), activate_cr(cb), __uint_as_float(orig));
     int tx0, tx1, ty0, ty1;
     uint32_t tiles = 0;

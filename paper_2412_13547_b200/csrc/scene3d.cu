@@ -42,24 +42,27 @@ constexpr float SH_C3_0 = -0.5900435899266435f, SH_C3_1 = 2.890611442640554f,
                 SH_C3_4 = -0.4570457994644658f, SH_C3_5 = 1.445305721320277f,
                 SH_C3_6 = -0.5900435899266435f;
 
+// Explicit _rn products / sums: the basis is evaluated by two kernels of the fused step
+// (chain rule and Adam) and by the explicit-gradient path; no FMA contraction keeps them bitwise equal.
 __device__ __forceinline__ void sh_basis(float x, float y, float z, float (&b)[16]) {
-    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    const float xx = fmul(x, x), yy = fmul(y, y), zz = fmul(z, z);
+    const float xy = fmul(x, y), yz = fmul(y, z), xz = fmul(x, z);
     b[0] = SH_C0;
-    b[1] = -SH_C1 * y;
-    b[2] = SH_C1 * z;
-    b[3] = -SH_C1 * x;
-    b[4] = SH_C2_0 * xy;
-    b[5] = SH_C2_1 * yz;
-    b[6] = SH_C2_2 * (2.f * zz - xx - yy);
-    b[7] = SH_C2_3 * xz;
-    b[8] = SH_C2_4 * (xx - yy);
-    b[9] = SH_C3_0 * y * (3.f * xx - yy);
-    b[10] = SH_C3_1 * xy * z;
-    b[11] = SH_C3_2 * y * (4.f * zz - xx - yy);
-    b[12] = SH_C3_3 * z * (2.f * zz - 3.f * xx - 3.f * yy);
-    b[13] = SH_C3_4 * x * (4.f * zz - xx - yy);
-    b[14] = SH_C3_5 * z * (xx - yy);
-    b[15] = SH_C3_6 * x * (xx - 3.f * yy);
+    b[1] = fmul(-SH_C1, y);
+    b[2] = fmul(SH_C1, z);
+    b[3] = fmul(-SH_C1, x);
+    b[4] = fmul(SH_C2_0, xy);
+    b[5] = fmul(SH_C2_1, yz);
+    b[6] = fmul(SH_C2_2, fsub(fsub(fmul(2.f, zz), xx), yy));
+    b[7] = fmul(SH_C2_3, xz);
+    b[8] = fmul(SH_C2_4, fsub(xx, yy));
+    b[9] = fmul(fmul(SH_C3_0, y), fsub(fmul(3.f, xx), yy));
+    b[10] = fmul(fmul(SH_C3_1, xy), z);
+    b[11] = fmul(fmul(SH_C3_2, y), fsub(fsub(fmul(4.f, zz), xx), yy));
+    b[12] = fmul(fmul(SH_C3_3, z), fsub(fsub(fmul(2.f, zz), fmul(3.f, xx)), fmul(3.f, yy)));
+    b[13] = fmul(fmul(SH_C3_4, x), fsub(fsub(fmul(4.f, zz), xx), yy));
+    b[14] = fmul(fmul(SH_C3_5, z), fsub(xx, yy));
+    b[15] = fmul(fmul(SH_C3_6, x), fsub(xx, fmul(3.f, yy)));
 }
 
 // d/d(dir) of sum_k w_k b_k(dir) (dir components treated as independent)
@@ -270,19 +273,49 @@ __device__ __forceinline__ int adam3d_group(int k) {
     return k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k == 10 ? 3 : (k < 14 ? 4 : 5))));
 }
 
-// Adam on one component (the oracle's or3d_adam_step order, explicit _rn ops).
+// Adam on one component from loaded state (the oracle's or3d_adam_step order, explicit _rn ops).
+__device__ __forceinline__ void adam3d_math(float& th, float& m, float& v, float g, float lr, bool clamp,
+                                            const Adam3dCfg& c) {
+    m = fadd(fmul(c.b1, m), fmul(c.omb1, g));
+    v = fadd(fmul(c.b2, v), fmul(fmul(c.omb2, g), g));
+    const float mh = fdiv_pos(m, c.bc1);
+    const float vh = fdiv_pos(v, c.bc2);
+    th = fsub(th, fdiv_pos(fmul(lr, mh), fadd(fsqrt_nz(vh), c.eps)));
+    if (clamp) th = th < -c.raw_cap ? -c.raw_cap : (c.raw_cap < th ? c.raw_cap : th);
+}
+
 __device__ __forceinline__ void adam3d_one(float* __restrict__ params, float* __restrict__ m1,
                                            float* __restrict__ m2, int64_t o, float g, float lr,
                                            bool clamp, const Adam3dCfg& c) {
-    const float mm = fadd(fmul(c.b1, m1[o]), fmul(c.omb1, g));
-    const float vv = fadd(fmul(c.b2, m2[o]), fmul(fmul(c.omb2, g), g));
-    m1[o] = mm;
-    m2[o] = vv;
-    const float mh = fdiv(mm, c.bc1);
-    const float vh = fdiv(vv, c.bc2);
-    float th = fsub(params[o], fdiv(fmul(lr, mh), fadd(__fsqrt_rn(vh), c.eps)));
-    if (clamp) th = th < -c.raw_cap ? -c.raw_cap : (c.raw_cap < th ? c.raw_cap : th);
+    float th = params[o], m = m1[o], v = m2[o];
+    adam3d_math(th, m, v, g, lr, clamp, c);
+    m1[o] = m;
+    m2[o] = v;
     params[o] = th;
+}
+
+// Adam over components K0 .. K0+NK-1 of row i: all 3*NK loads issued before any store (the
+// streams are independent; the restrict pointers let the loads run ahead).
+template <int K0, int NK, typename GradFn>
+__device__ __forceinline__ void adam3d_chunk(float* __restrict__ P, float* __restrict__ M1,
+                                             float* __restrict__ M2, int64_t cap, int64_t i,
+                                             GradFn grad, const Adam3dCfg& c) {
+    float th[NK], m[NK], v[NK];
+#pragma unroll
+    for (int j = 0; j < NK; ++j) {
+        const int64_t o = (int64_t)(K0 + j) * cap + i;
+        th[j] = P[o];
+        m[j] = M1[o];
+        v[j] = M2[o];
+    }
+#pragma unroll
+    for (int j = 0; j < NK; ++j) {
+        adam3d_math(th[j], m[j], v[j], grad(K0 + j), c.lr[adam3d_group(K0 + j)], K0 + j == 10, c);
+        const int64_t o = (int64_t)(K0 + j) * cap + i;
+        P[o] = th[j];
+        M1[o] = m[j];
+        M2[o] = v[j];
+    }
 }
 
 struct Chain3Params {
@@ -301,74 +334,23 @@ struct Chain3Params {
     float* col_acc;
     int32_t* visit;
     int update_stats;
-    float* m1;
-    float* m2;
-    Adam3dCfg adam;
+    float* gbuf;    // [17][n] (mode 1): gradients 0..10, masked colour gradient, view direction
 };
 
-__device__ __forceinline__ void emit3d(const Chain3Params& cp, int64_t i, int k, float g) {
-    if (cp.mode == 0) {
-        cp.grads[(int64_t)k * cp.n + i] = g;
-    } else {
-        adam3d_one(cp.params, cp.m1, cp.m2, (int64_t)k * cp.cap + i, g, cp.adam.lr[adam3d_group(k)],
-                   k == 10, cp.adam);
-    }
-}
-
-__global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= cp.n) return;
-    const int64_t cap = cp.cap;
-    const float* __restrict__ P = cp.params;
-    const uint32_t r = __ldg(cp.rank_of + i);
-    const uint32_t cnt = __ldg(cp.touched + r);
-    float s[10];
-#pragma unroll
-    for (int k = 0; k < 10; ++k) s[k] = 0.f;
-    if (cnt) {
-        // tile-order merge (rasterizer.cpp:301-319): the splat's pair slots are contiguous
-        const uint32_t base = __ldg(cp.pair_off + r);
-        const float4* __restrict__ pa = cp.partial.a + base;
-        const float4* __restrict__ pb = cp.partial.b + base;
-        const float2* __restrict__ pc = cp.partial.c + base;
-        for (uint32_t t = 0; t < cnt; ++t) {
-            const float4 a = pa[t], b = pb[t];
-            const float2 c = pc[t];
-            s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
-            s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
-            s[8] += c.x;
-            s[9] = fmaxf(s[9], c.y);
-        }
-    }
-    if (cp.screen) {
-#pragma unroll
-        for (int k = 0; k < 10; ++k) cp.screen[(int64_t)k * cp.n + i] = s[k];
-    }
-    float mu[3], q[4], ls[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) mu[k] = __ldg(P + k * cap + i);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = __ldg(P + (3 + k) * cap + i);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) ls[k] = __ldg(P + (7 + k) * cap + i);
-    const float rop = __ldg(P + 10 * cap + i);
-    Geo3 g;
-    const bool seen = cnt != 0 && geometry(cp.cam, cp.bump, mu, q, ls, g);
-    if (!seen) {
-        // untouched by this view: zero gradient (Adam still advances its moments)
-        for (int k = 0; k < 59; ++k) emit3d(cp, i, k, 0.f);
-        return;
-    }
-    const Cam3& cam = cp.cam;
-    // ---- colour: SH basis, raw colour, clamp mask, SH gradients, direction gradient
-    float d[3], ilen;
+// Gradients of one Gaussian from its merged screen-space sums s[0..8]: the 11 geometric /
+// opacity components into gg (rows 0..10), the SH gradients as b[k] * dcol[c] (rows 11+3k+c).
+// Mirrors or3d_chain (oracle/ewa3d.c).
+__device__ __forceinline__ void chain3d_grads(const Cam3& cam, const Geo3& g, const float (&mu)[3],
+                                              float rop, const float* __restrict__ P, int64_t cap, int64_t i,
+                                              const float (&s)[10], float (&gg)[11], float (&b)[16],
+                                              float (&dcol)[3], float (&d)[3]) {
+    // ---- colour: SH basis, raw colour, clamp mask, direction gradient
+    float ilen;
     view_dir(cam, mu, d, ilen);
-    float b[16];
     sh_basis(d[0], d[1], d[2], b);
     float sh[48];
 #pragma unroll
     for (int k = 0; k < 48; ++k) sh[k] = __ldg(P + (11 + k) * cap + i);
-    float dcol[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         float acc = 0.5f;
@@ -382,14 +364,10 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
     float gdx, gdy, gdz;
     sh_basis_grad(d[0], d[1], d[2], w, gdx, gdy, gdz);
     const float dd = gdx * d[0] + gdy * d[1] + gdz * d[2];
-    float dmu[3] = {(gdx - d[0] * dd) * ilen, (gdy - d[1] * dd) * ilen, (gdz - d[2] * dd) * ilen};
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) emit3d(cp, i, 11 + 3 * k + c, b[k] * dcol[c]);
+    const float dmu[3] = {(gdx - d[0] * dd) * ilen, (gdy - d[1] * dd) * ilen, (gdz - d[2] * dd) * ilen};
     // ---- opacity
     const float al = sigmoidf(rop);
-    emit3d(cp, i, 10, s[5] * al * (1.f - al));
+    gg[10] = s[5] * al * (1.f - al);
     // ---- mean projection + EWA covariance
     const float fx = cam.fx, fy = cam.fy, iz = g.iz, iz2 = iz * iz;
     float dt[3];
@@ -433,7 +411,7 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
         dt[2] += dJ12 * 2.f * fy * g.cyz * iz2;
     }
 #pragma unroll
-    for (int j = 0; j < 3; ++j) emit3d(cp, i, j, R[j] * dt[0] + R[3 + j] * dt[1] + R[6 + j] * dt[2] + dmu[j]);
+    for (int j = 0; j < 3; ++j) gg[j] = R[j] * dt[0] + R[3 + j] * dt[1] + R[6 + j] * dt[2] + dmu[j];
     // ---- Σ3 = M Mᵀ, M = Rq diag(s)
     float dR[3][3];
 #pragma unroll
@@ -445,7 +423,7 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
             dR[a][j] = dM * g.s[j];
             ds += dM * g.Rq[a][j];
         }
-        emit3d(cp, i, 7 + j, ds * g.s[j]);
+        gg[7 + j] = ds * g.s[j];
     }
     const float qr = g.qn[0], qx = g.qn[1], qy = g.qn[2], qz = g.qn[3];
     float dq[4];
@@ -458,25 +436,151 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
                    qy * dR[1][2] + qx * dR[2][0] + qy * dR[2][1]);
     const float qd = qr * dq[0] + qx * dq[1] + qy * dq[2] + qz * dq[3];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) emit3d(cp, i, 3 + k, (dq[k] - g.qn[k] * qd) * g.qinv);
-    // ---- densify statistics: screen-space position norm, DC colour-gradient norm
-    if (cp.update_stats && s[9] > 0.f) {
-        cp.pos_acc[i] += sqrtf(s[0] * s[0] + s[1] * s[1]);
-        cp.col_acc[i] += SH_C0 * sqrtf(dcol[0] * dcol[0] + dcol[1] * dcol[1] + dcol[2] * dcol[2]);
-        cp.visit[i] += 1;
+    for (int k = 0; k < 4; ++k) gg[3 + k] = (dq[k] - g.qn[k] * qd) * g.qinv;
+}
+
+__global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cp.n) return;
+    const int64_t cap = cp.cap;
+    const float* __restrict__ P = cp.params;
+    const uint32_t r = __ldg(cp.rank_of + i);
+    const uint32_t cnt = __ldg(cp.touched + r);
+    float s[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) s[k] = 0.f;
+    if (cnt) {
+        // tile-order merge (rasterizer.cpp:301-319): the splat's pair slots are contiguous
+        const uint32_t base = __ldg(cp.pair_off + r);
+        const float4* __restrict__ pa = cp.partial.a + base;
+        const float4* __restrict__ pb = cp.partial.b + base;
+        const float2* __restrict__ pc = cp.partial.c + base;
+        for (uint32_t t = 0; t < cnt; ++t) {
+            const float4 a = pa[t], b = pb[t];
+            const float2 c = pc[t];
+            s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
+            s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+            s[8] += c.x;
+            s[9] = fmaxf(s[9], c.y);
+        }
+    }
+    if (cp.screen) {
+#pragma unroll
+        for (int k = 0; k < 10; ++k) cp.screen[(int64_t)k * cp.n + i] = s[k];
+    }
+    float mu[3], q[4], ls[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mu[k] = __ldg(P + k * cap + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = __ldg(P + (3 + k) * cap + i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ls[k] = __ldg(P + (7 + k) * cap + i);
+    const float rop = __ldg(P + 10 * cap + i);
+    Geo3 g;
+    float gg[11], b[16], dcol[3], dir[3] = {0.f, 0.f, 1.f};
+    // untouched by this view: zero gradient (Adam still advances its moments)
+    if (cnt != 0 && geometry(cp.cam, cp.bump, mu, q, ls, g)) {
+        chain3d_grads(cp.cam, g, mu, rop, P, cap, i, s, gg, b, dcol, dir);
+        // densify statistics: screen-space position norm, DC colour-gradient norm
+        if (cp.update_stats && s[9] > 0.f) {
+            cp.pos_acc[i] += sqrtf(s[0] * s[0] + s[1] * s[1]);
+            cp.col_acc[i] += SH_C0 * sqrtf(dcol[0] * dcol[0] + dcol[1] * dcol[1] + dcol[2] * dcol[2]);
+            cp.visit[i] += 1;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 11; ++k) gg[k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) b[k] = 0.f;
+        dcol[0] = dcol[1] = dcol[2] = 0.f;
+    }
+    if (cp.mode == 0) {
+        auto grad = [&](int k) -> float { return k < 11 ? gg[k] : fmul(b[(k - 11) / 3], dcol[(k - 11) % 3]); };
+        float* __restrict__ G = cp.grads;
+#pragma unroll
+        for (int k = 0; k < 59; ++k) G[(int64_t)k * cp.n + i] = grad(k);
+        return;
+    }
+    // fused step: 17 floats per Gaussian (11 gradients, the clamp-masked colour gradient, the
+    // view direction) for the elementwise Adam kernel, which recomputes the SH basis
+    float* __restrict__ GB = cp.gbuf;
+#pragma unroll
+    for (int k = 0; k < 11; ++k) GB[(int64_t)k * cp.n + i] = gg[k];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) GB[(int64_t)(11 + c) * cp.n + i] = dcol[c];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) GB[(int64_t)(14 + c) * cp.n + i] = dir[c];
+}
+
+// Adam over one group of components of every Gaussian (grid.y = group, kAdamGroups groups):
+// group 0 = rows 0..5 (mean, quaternion w x y), group 1 = rows 6..10 (quaternion z, log-scales,
+// opacity), group 2 + j = SH functions 2j, 2j+1, all three channels (rows 11 + 6j ..). <= 6
+// components per thread: small register footprint, full occupancy for the streams.
+constexpr int kAdamGroups = 10;
+
+template <int G>
+__device__ __forceinline__ void adam3d_group_apply(float* __restrict__ P, float* __restrict__ M1,
+                                                   float* __restrict__ M2, int64_t cap, int64_t n,
+                                                   int64_t i, const float* __restrict__ GB,
+                                                   const Adam3dCfg& c) {
+    if (G < 2) {
+        constexpr int K0 = G == 0 ? 0 : 6, NK = G == 0 ? 6 : 5;
+        float gg[NK];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) gg[k] = GB[(int64_t)(K0 + k) * n + i];
+        adam3d_chunk<K0, NK>(P, M1, M2, cap, i, [&](int k) { return gg[k - K0]; }, c);
+    } else {
+        float dcol[3], d[3], b[16];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            dcol[k] = GB[(int64_t)(11 + k) * n + i];
+            d[k] = GB[(int64_t)(14 + k) * n + i];
+        }
+        sh_basis(d[0], d[1], d[2], b);
+        constexpr int K0 = 11 + 6 * (G - 2);
+        adam3d_chunk<K0, 6>(P, M1, M2, cap, i,
+                            [&](int k) { return fmul(b[(k - 11) / 3], dcol[(k - 11) % 3]); }, c);
     }
 }
 
-// Adam with explicit gradients [59][n] (tgsx_adam3d_step)
+__global__ void __launch_bounds__(256, 3) adam3d_apply_kernel(float* __restrict__ P, float* __restrict__ M1,
+                                                           float* __restrict__ M2, int64_t cap, int64_t n,
+                                                           const float* __restrict__ GB, Adam3dCfg c) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    switch (blockIdx.y) {
+        case 0: adam3d_group_apply<0>(P, M1, M2, cap, n, i, GB, c); break;
+        case 1: adam3d_group_apply<1>(P, M1, M2, cap, n, i, GB, c); break;
+        case 2: adam3d_group_apply<2>(P, M1, M2, cap, n, i, GB, c); break;
+        case 3: adam3d_group_apply<3>(P, M1, M2, cap, n, i, GB, c); break;
+        case 4: adam3d_group_apply<4>(P, M1, M2, cap, n, i, GB, c); break;
+        case 5: adam3d_group_apply<5>(P, M1, M2, cap, n, i, GB, c); break;
+        case 6: adam3d_group_apply<6>(P, M1, M2, cap, n, i, GB, c); break;
+        case 7: adam3d_group_apply<7>(P, M1, M2, cap, n, i, GB, c); break;
+        case 8: adam3d_group_apply<8>(P, M1, M2, cap, n, i, GB, c); break;
+        default: adam3d_group_apply<9>(P, M1, M2, cap, n, i, GB, c); break;
+    }
+}
+
+// Adam with explicit gradients [59][n] (tgsx_adam3d_step): grid.y = group of components as above
 __global__ void __launch_bounds__(256) adam3d_kernel(float* __restrict__ params, float* __restrict__ m1,
                                                      float* __restrict__ m2, int64_t cap, int64_t n,
                                                      const float* __restrict__ grads, Adam3dCfg c) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-#pragma unroll
-    for (int k = 0; k < 59; ++k)
-        adam3d_one(params, m1, m2, (int64_t)k * cap + i, grads[(int64_t)k * n + i], c.lr[adam3d_group(k)],
-                   k == 10, c);
+    auto grad = [&](int k) -> float { return grads[(int64_t)k * n + i]; };
+    switch (blockIdx.y) {
+        case 0: adam3d_chunk<0, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 1: adam3d_chunk<6, 5>(params, m1, m2, cap, i, grad, c); break;
+        case 2: adam3d_chunk<11, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 3: adam3d_chunk<17, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 4: adam3d_chunk<23, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 5: adam3d_chunk<29, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 6: adam3d_chunk<35, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 7: adam3d_chunk<41, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 8: adam3d_chunk<47, 6>(params, m1, m2, cap, i, grad, c); break;
+        default: adam3d_chunk<53, 6>(params, m1, m2, cap, i, grad, c); break;
+    }
 }
 
 inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / bt); }
@@ -485,7 +589,7 @@ inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / b
 
 cudaError_t launch_adam3d(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, const Adam3dCfg& cfg) {
     if (m->n == 0) return cudaSuccess;
-    adam3d_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(m->params.as<float>(), m->m1.as<float>(),
+    adam3d_kernel<<<dim3(grid_for(m->n, 256), kAdamGroups), 256, 0, ctx->stream>>>(m->params.as<float>(), m->m1.as<float>(),
                                                                 m->m2.as<float>(), m->cap, m->n, grads, cfg);
     ctx->launches++;
     return cudaGetLastError();
@@ -553,11 +657,18 @@ cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int 
     cp.col_acc = m->col_acc.as<float>();
     cp.visit = m->visit.as<int32_t>();
     cp.update_stats = update_stats ? 1 : 0;
-    cp.m1 = m->m1.as<float>();
-    cp.m2 = m->m2.as<float>();
-    if (cfg) cp.adam = *cfg;
+    cudaError_t e;
+    if (adam) {
+        if ((e = m->gbuf.ensure((size_t)std::max<int64_t>(m->n, 1) * 17 * 4))) return e;
+        cp.gbuf = m->gbuf.as<float>();
+    }
     chain3d_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(cp);
     ctx->launches++;
+    if (adam) {
+        adam3d_apply_kernel<<<dim3(grid_for(m->n, 256), kAdamGroups), 256, 0, ctx->stream>>>(
+            m->params.as<float>(), m->m1.as<float>(), m->m2.as<float>(), m->cap, m->n, cp.gbuf, *cfg);
+        ctx->launches++;
+    }
     return cudaGetLastError();
 }
 

@@ -40,6 +40,20 @@ __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b)
 __device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
 
+// a / b correctly rounded (== __fdiv_rn) for b > 0, without the division's slow-path subroutine
+// for a zero dividend: FCHK sends any lane with a zero / denormal operand there, and one such lane
+// makes the whole warp pay (Adam moments of components that never saw a gradient are exactly 0).
+// +-0 / b = +-0 for b > 0, so the substitution is exact.
+__device__ __forceinline__ float fdiv_pos(float a, float b) {
+    const float q = __fdiv_rn(a == 0.0f ? 1.0f : a, b);
+    return a == 0.0f ? a : q;
+}
+// sqrt correctly rounded (== __fsqrt_rn) without the slow path for a zero argument.
+__device__ __forceinline__ float fsqrt_nz(float a) {
+    const float r = __fsqrt_rn(a == 0.0f ? 1.0f : a);
+    return a == 0.0f ? a : r;
+}
+
 // activate (gaussian.hpp:47-49): 1 / (1 + exp(-raw))
 __device__ __forceinline__ float activate_cr(float raw) {
     return fdiv(1.0f, fadd(1.0f, cr_expf(-raw)));

@@ -154,6 +154,7 @@ struct tgsx_model3d {
     tgsx::DevBuf visit;             // i32[cap]
     tgsx::DevBuf perm, rank_of;     // u32[cap] blend order of the last view
     tgsx::DevBuf prep_row;          // Prepared[cap] records in row order (before the depth sort)
+    tgsx::DevBuf gbuf;              // float[17][n] chain-rule output of the fused step (scene3d.cu)
 };
 
 // physical row order of the model (capi.cu): blend order for the hot path, logical (creation)
