@@ -21,6 +21,29 @@ __device__ __forceinline__ float clampf(float v, float lo, float hi) {
     return v < lo ? lo : (hi < v ? hi : v);
 }
 
+// Adam on one Gaussian's 9 components from preloaded state (theta, m, v loaded before the
+// partial merge so their latency overlaps it); same rounding as adam_update.
+__device__ __forceinline__ void adam_update_pre(float* __restrict__ params, float* __restrict__ m1,
+                                                float* __restrict__ m2, int64_t cap, int64_t i,
+                                                const float (&g)[9], const float (&th0)[9],
+                                                const float (&mm0)[9], const float (&vv0)[9],
+                                                const AdamCfg& c) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        const int64_t o = (int64_t)q * cap + i;
+        const float mm = fadd(fmul(c.b1, mm0[q]), fmul(c.omb1, g[q]));
+        const float vv = fadd(fmul(c.b2, vv0[q]), fmul(fmul(c.omb2, g[q]), g[q]));
+        m1[o] = mm;
+        m2[o] = vv;
+        const float mh = fdiv_pos(mm, c.bc1);
+        const float vh = fdiv_pos(vv, c.bc2);
+        float th = fsub(th0[q], fdiv_pos(fmul(c.lr[q], mh), fadd(fsqrt_nz(vh), c.eps)));
+        if (q == 3 || q == 4) th = clampf(th, c.ls_lo, c.ls_hi);
+        if (q >= 5) th = clampf(th, -c.raw_cap, c.raw_cap);
+        params[o] = th;
+    }
+}
+
 // Adam on one Gaussian's 9 components + clamp (mirrors oracle or_adam_step exactly).
 __device__ __forceinline__ void adam_update(float* __restrict__ params, float* __restrict__ m1,
                                             float* __restrict__ m2, int64_t cap, int64_t i,
@@ -70,7 +93,7 @@ struct ChainParams {
 
 // 6 blocks of 256 per SM (<= 40 registers): the slot loop and the moment / parameter streams
 // are latency-bound, so occupancy buys memory-level parallelism
-__global__ void __launch_bounds__(256, 6) chain_kernel(ChainParams cp) {
+__global__ void __launch_bounds__(256, 4) chain_kernel(ChainParams cp) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cp.n) return;
     const int64_t cap = cp.cap;
@@ -95,7 +118,32 @@ __global__ void __launch_bounds__(256, 6) chain_kernel(ChainParams cp) {
     const float4* __restrict__ pa = cp.partial.a + base;
     const float4* __restrict__ pb = cp.partial.b + base;
     const float2* __restrict__ pc = cp.partial.c + base;
-    for (uint32_t t = 0; t < cnt; ++t) {
+    // fused Adam: its state streams (theta, m, v) do not depend on the merge; issue them first
+    float th0[9], mm0[9], vv0[9];
+    if (cp.mode == 1) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            const int64_t o = (int64_t)q * cap + i;
+            th0[q] = __ldg(params + o);
+            mm0[q] = cp.m1[o];
+            vv0[q] = cp.m2[o];
+        }
+    }
+    // two slots per step (the loads of both in flight together); sums in slot order
+    uint32_t t = 0;
+    for (; t + 1 < cnt; t += 2) {
+        const float4 a0 = pa[t], b0 = pb[t], a1 = pa[t + 1], b1 = pb[t + 1];
+        const float2 c0 = pc[t], c1 = pc[t + 1];
+        s[0] += a0.x; s[1] += a0.y; s[2] += a0.z; s[3] += a0.w;
+        s[4] += b0.x; s[5] += b0.y; s[6] += b0.z; s[7] += b0.w;
+        s[8] += c0.x;
+        s[9] = fmaxf(s[9], c0.y);
+        s[0] += a1.x; s[1] += a1.y; s[2] += a1.z; s[3] += a1.w;
+        s[4] += b1.x; s[5] += b1.y; s[6] += b1.z; s[7] += b1.w;
+        s[8] += c1.x;
+        s[9] = fmaxf(s[9], c1.y);
+    }
+    if (t < cnt) {
         const float4 a = pa[t], b = pb[t];
         const float2 c = pc[t];
         s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
@@ -166,7 +214,7 @@ __global__ void __launch_bounds__(256, 6) chain_kernel(ChainParams cp) {
         for (int q = 0; q < 9; ++q) cp.grads[q * cp.n + li] = g[q];
         return;
     }
-    adam_update(cp.params_w, cp.m1, cp.m2, cap, i, g, cp.adam);
+    adam_update_pre(cp.params_w, cp.m1, cp.m2, cap, i, g, th0, mm0, vv0, cp.adam);
 }
 
 // mode 0: grads [9][n] given; mode 1: step buffer [12][cap] (mean over batch, stats applied)
