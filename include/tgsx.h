@@ -363,6 +363,14 @@ int32_t tgsx_adam3d_step(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, con
 /* One fused fit iteration of the 3-D model on one view (tgsx_fit_step with the 3-D front end). */
 int32_t tgsx_fit_step3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
                         const float bg[3], const float* target, const tgsx_adam3d_args* a, float* out_loss);
+/* Batched views (SPEC.md:269-277 accumulate): each view adds its 59 gradients, the
+ * position / colour norms and a visit count into the model's step buffer float[62][capacity]
+ * (device; all-reduce it across ranks with NCCL), then tgsx_apply_step3d applies the mean over
+ * batch_views (all ranks' views), the statistics and Adam, and zeroes the buffer. */
+int32_t tgsx_view_accumulate3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                               const float bg[3], const float* target, float* out_loss);
+float* tgsx_step_buffer3d(tgsx_model3d* m, int64_t* out_floats);
+int32_t tgsx_apply_step3d(tgsx_ctx* ctx, tgsx_model3d* m, int32_t batch_views, const tgsx_adam3d_args* a);
 /* Parity stage: the blend-ordered 64-B records (Prepared layout, raster.cu) of all n ranks and
  * the sorted depth keys (culled rows last with key 0xffffffff). */
 int32_t tgsx_stage_prepare3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, int32_t lowpass_p,

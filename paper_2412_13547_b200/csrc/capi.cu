@@ -854,6 +854,7 @@ cudaError_t model3d_reserve(tgsx_ctx* ctx, tgsx_model3d* m, int64_t cap, bool ke
     if ((e = regrow(m->pos_acc, 1, 4))) return e;
     if ((e = regrow(m->col_acc, 1, 4))) return e;
     if ((e = regrow(m->visit, 1, 4))) return e;
+    if ((e = regrow(m->step, k3dStepRows, 4))) return e;
     if ((e = m->perm.ensure(nc * 4))) return e;
     if ((e = m->rank_of.ensure(nc * 4))) return e;
     if ((e = m->prep_row.ensure(nc * sizeof(Prepared)))) return e;
@@ -1388,7 +1389,7 @@ int32_t tgsx_model3d_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model3d** out)
 void tgsx_model3d_destroy(tgsx_model3d* m) {
     if (!m) return;
     DevBuf* bufs[] = {&m->params, &m->m1, &m->m2, &m->pos_acc, &m->col_acc, &m->visit,
-                      &m->perm, &m->rank_of, &m->prep_row, &m->gbuf};
+                      &m->perm, &m->rank_of, &m->prep_row, &m->gbuf, &m->step};
     for (DevBuf* b : bufs) b->release();
     delete m;
 }
@@ -1408,6 +1409,8 @@ int32_t tgsx_model3d_upload(tgsx_ctx* ctx, tgsx_model3d* m, const float* params,
     CK(cudaMemsetAsync(m->pos_acc.p, 0, m->pos_acc.bytes, s));
     CK(cudaMemsetAsync(m->col_acc.p, 0, m->col_acc.bytes, s));
     CK(cudaMemsetAsync(m->visit.p, 0, m->visit.bytes, s));
+    CK(cudaMemsetAsync(m->step.p, 0, m->step.bytes, s));
+    m->step_views = 0;
     CK(cudaStreamSynchronize(s));
     return TGSX_OK;
 }
@@ -1488,7 +1491,7 @@ int32_t tgsx_backward3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, 
                              : nullptr;
     {
         StageTimer t(ctx, kStChain);
-        CK(launch_chain3d(ctx, m, c3, ra.lowpass_p, false, update_stats != 0, gdev, sdev, nullptr));
+        CK(launch_chain3d(ctx, m, c3, ra.lowpass_p, 0, update_stats != 0, gdev, sdev, nullptr));
     }
     if (out_grads && gdev != out_grads && n)
         CK(cudaMemcpyAsync(out_grads, gdev, (size_t)n * k3dParams * 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1511,17 +1514,55 @@ int32_t tgsx_adam3d_step(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, con
     return TGSX_OK;
 }
 
+static int32_t fused_view3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                            const float bg[3], const float* target, const tgsx_adam3d_args* a, float* out_loss,
+                            int mode);
+
 int32_t tgsx_fit_step3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
                         const float bg[3], const float* target, const tgsx_adam3d_args* a, float* out_loss) {
     if (!ctx || !m || !a) return TGSX_EINVAL;
     if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
+    return fused_view3d(ctx, m, cam, pat, bg, target, a, out_loss, 1);
+}
+
+int32_t tgsx_view_accumulate3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                               const float bg[3], const float* target, float* out_loss) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    const int32_t rc = fused_view3d(ctx, m, cam, pat, bg, target, nullptr, out_loss, 2);
+    if (!rc) m->step_views++;
+    return rc;
+}
+
+float* tgsx_step_buffer3d(tgsx_model3d* m, int64_t* out_floats) {
+    if (!m) return nullptr;
+    if (out_floats) *out_floats = (int64_t)k3dStepRows * m->cap;
+    return m->step.as<float>();
+}
+
+int32_t tgsx_apply_step3d(tgsx_ctx* ctx, tgsx_model3d* m, int32_t batch_views, const tgsx_adam3d_args* a) {
+    if (!ctx || !m || !a) return TGSX_EINVAL;
+    if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
+    if (batch_views < 1) return fail(ctx, TGSX_EINVAL, "batch_views must be >= 1");
+    Adam3dCfg cfg;
+    fill_adam3d(cfg, a);
+    CK(launch_adam3d_step(ctx, m, batch_views, cfg));
+    m->step_views = 0;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TGSX_OK;
+}
+
+// One 3-D view: render + fused L1 (+ SSIM on dense views) + backward + chain3d in `mode`
+// (1 fused Adam, 2 accumulate into the step buffer).
+static int32_t fused_view3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
+                            const float bg[3], const float* target, const tgsx_adam3d_args* a, float* out_loss,
+                            int mode) {
     int32_t rc = check_pattern(ctx, pat);
     if (rc) return rc;
     if (!target) return fail(ctx, TGSX_EINVAL, "target is null");
     Cam3 c3;
     if ((rc = make_cam3(ctx, cam, pat, &c3))) return rc;
-    Adam3dCfg cfg;
-    fill_adam3d(cfg, a);
+    Adam3dCfg cfg{};
+    if (a) fill_adam3d(cfg, a);
     RenderArgs ra = make_args(pat, bg, 0);
     const float lam = (pat->p == 1 && ctx->ssim_weight > 0.f) ? ctx->ssim_weight : 0.f;
     ra.l1_weight = 1.0f - lam;
@@ -1545,7 +1586,7 @@ int32_t tgsx_fit_step3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, 
     }
     {
         StageTimer t(ctx, kStChain);
-        CK(launch_chain3d(ctx, m, c3, ra.lowpass_p, true, true, nullptr, nullptr, &cfg));
+        CK(launch_chain3d(ctx, m, c3, ra.lowpass_p, mode, true, nullptr, nullptr, &cfg));
     }
     const int tiles = ws.tiles_x * ws.tiles_y;
     float* dloss = reinterpret_cast<float*>(ws.counters.as<unsigned long long>() + 4);

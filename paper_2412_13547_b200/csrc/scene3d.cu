@@ -327,7 +327,7 @@ struct Chain3Params {
     const uint32_t* pair_off;
     const uint32_t* touched;
     Partials partial;
-    int mode;       // 0 gradients out, 1 fused Adam
+    int mode;       // 0 gradients out, 1 fused Adam, 2 accumulate into the batched step buffer
     float* grads;   // [59][n] (mode 0)
     float* screen;  // [10][n] or null
     float* pos_acc;
@@ -335,6 +335,7 @@ struct Chain3Params {
     int32_t* visit;
     int update_stats;
     float* gbuf;    // [17][n] (mode 1): gradients 0..10, masked colour gradient, view direction
+    float* step;    // [62][cap] (mode 2): 59 gradient sums, position-norm sum, colour-norm sum, visits
 };
 
 // Gradients of one Gaussian from its merged screen-space sums s[0..8]: the 11 geometric /
@@ -478,13 +479,20 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
     const float rop = __ldg(P + 10 * cap + i);
     Geo3 g;
     float gg[11], b[16], dcol[3], dir[3] = {0.f, 0.f, 1.f};
+    bool visited = false;
+    float pn = 0.f, cn = 0.f;
     // untouched by this view: zero gradient (Adam still advances its moments)
     if (cnt != 0 && geometry(cp.cam, cp.bump, mu, q, ls, g)) {
         chain3d_grads(cp.cam, g, mu, rop, P, cap, i, s, gg, b, dcol, dir);
         // densify statistics: screen-space position norm, DC colour-gradient norm
-        if (cp.update_stats && s[9] > 0.f) {
-            cp.pos_acc[i] += sqrtf(s[0] * s[0] + s[1] * s[1]);
-            cp.col_acc[i] += SH_C0 * sqrtf(dcol[0] * dcol[0] + dcol[1] * dcol[1] + dcol[2] * dcol[2]);
+        visited = s[9] > 0.f;
+        if (visited) {
+            pn = sqrtf(s[0] * s[0] + s[1] * s[1]);
+            cn = SH_C0 * sqrtf(dcol[0] * dcol[0] + dcol[1] * dcol[1] + dcol[2] * dcol[2]);
+        }
+        if (cp.update_stats && visited && cp.mode != 2) {
+            cp.pos_acc[i] += pn;
+            cp.col_acc[i] += cn;
             cp.visit[i] += 1;
         }
     } else {
@@ -494,11 +502,31 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
         for (int k = 0; k < 16; ++k) b[k] = 0.f;
         dcol[0] = dcol[1] = dcol[2] = 0.f;
     }
-    if (cp.mode == 0) {
+    if (cp.mode != 1) {
         auto grad = [&](int k) -> float { return k < 11 ? gg[k] : fmul(b[(k - 11) / 3], dcol[(k - 11) % 3]); };
-        float* __restrict__ G = cp.grads;
+        if (cp.mode == 0) {
+            float* __restrict__ G = cp.grads;
 #pragma unroll
-        for (int k = 0; k < 59; ++k) G[(int64_t)k * cp.n + i] = grad(k);
+            for (int k = 0; k < 59; ++k) G[(int64_t)k * cp.n + i] = grad(k);
+            return;
+        }
+        // batched views: sums in view order (tgsx_view_accumulate3d)
+        float* __restrict__ ST = cp.step;
+#pragma unroll
+        for (int k0 = 0; k0 < 59; k0 += 8) {  // 8 loads in flight, then 8 stores
+            float old[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < 59) old[k] = ST[(int64_t)(k0 + k) * cap + i];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < 59) ST[(int64_t)(k0 + k) * cap + i] = old[k] + grad(k0 + k);
+        }
+        if (cp.update_stats && visited) {
+            ST[59 * cap + i] += pn;
+            ST[60 * cap + i] += cn;
+            ST[61 * cap + i] += 1.0f;
+        }
         return;
     }
     // fused step: 17 floats per Gaussian (11 gradients, the clamp-masked colour gradient, the
@@ -583,9 +611,60 @@ __global__ void __launch_bounds__(256) adam3d_kernel(float* __restrict__ params,
     }
 }
 
+// Batched step (tgsx_apply_step3d): gradient = step sum / views (SPEC.md:269-277 accumulate),
+// statistics from the summed increments, Adam; the step buffer is zeroed for the next batch.
+__global__ void __launch_bounds__(256) adam3d_step_kernel(float* __restrict__ params, float* __restrict__ m1,
+                                                          float* __restrict__ m2, int64_t cap, int64_t n,
+                                                          float* __restrict__ step, float batch,
+                                                          float* __restrict__ pos_acc, float* __restrict__ col_acc,
+                                                          int32_t* __restrict__ visit, Adam3dCfg c) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    auto grad = [&](int k) -> float {
+        float* p = step + (int64_t)k * cap + i;
+        const float v = *p;
+        *p = 0.f;
+        return fdiv_pos(v, batch);
+    };
+    switch (blockIdx.y) {
+        case 0: {
+            adam3d_chunk<0, 6>(params, m1, m2, cap, i, grad, c);
+            const float v = step[61 * cap + i];
+            if (v > 0.f) {
+                pos_acc[i] += step[59 * cap + i];
+                col_acc[i] += step[60 * cap + i];
+                visit[i] += (int32_t)v;
+            }
+            step[59 * cap + i] = 0.f;
+            step[60 * cap + i] = 0.f;
+            step[61 * cap + i] = 0.f;
+            break;
+        }
+        case 1: adam3d_chunk<6, 5>(params, m1, m2, cap, i, grad, c); break;
+        case 2: adam3d_chunk<11, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 3: adam3d_chunk<17, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 4: adam3d_chunk<23, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 5: adam3d_chunk<29, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 6: adam3d_chunk<35, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 7: adam3d_chunk<41, 6>(params, m1, m2, cap, i, grad, c); break;
+        case 8: adam3d_chunk<47, 6>(params, m1, m2, cap, i, grad, c); break;
+        default: adam3d_chunk<53, 6>(params, m1, m2, cap, i, grad, c); break;
+    }
+}
+
 inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / bt); }
 
 }  // namespace
+
+cudaError_t launch_adam3d_step(tgsx_ctx* ctx, tgsx_model3d* m, int batch_views, const Adam3dCfg& cfg) {
+    if (m->n == 0) return cudaSuccess;
+    adam3d_step_kernel<<<dim3(grid_for(m->n, 256), kAdamGroups), 256, 0, ctx->stream>>>(
+        m->params.as<float>(), m->m1.as<float>(), m->m2.as<float>(), m->cap, m->n, m->step.as<float>(),
+        (float)(batch_views > 0 ? batch_views : 1), m->pos_acc.as<float>(), m->col_acc.as<float>(),
+        m->visit.as<int32_t>(), cfg);
+    ctx->launches++;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_adam3d(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, const Adam3dCfg& cfg) {
     if (m->n == 0) return cudaSuccess;
@@ -637,8 +716,9 @@ cudaError_t launch_bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const uint32_t* skeys, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, bool adam,
+cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int mode,
                            bool update_stats, float* grads, float* screen, const Adam3dCfg* cfg) {
+    const bool adam = mode == 1;
     if (m->n == 0) return cudaSuccess;
     Chain3Params cp{};
     cp.params = m->params.as<float>();
@@ -650,7 +730,8 @@ cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int 
     cp.pair_off = ctx->ws.pair_off.as<uint32_t>();
     cp.touched = ctx->ws.touched.as<uint32_t>();
     cp.partial = Partials::at(ctx->ws.partial.p, ctx->ws.pair_cap);
-    cp.mode = adam ? 1 : 0;
+    cp.mode = mode;
+    cp.step = m->step.as<float>();
     cp.grads = grads;
     cp.screen = screen;
     cp.pos_acc = m->pos_acc.as<float>();

@@ -155,6 +155,8 @@ struct tgsx_model3d {
     tgsx::DevBuf perm, rank_of;     // u32[cap] blend order of the last view
     tgsx::DevBuf prep_row;          // Prepared[cap] records in row order (before the depth sort)
     tgsx::DevBuf gbuf;              // float[17][n] chain-rule output of the fused step (scene3d.cu)
+    tgsx::DevBuf step;              // float[62][cap] batched-view step buffer (all-reduced across ranks)
+    int64_t step_views = 0;
 };
 
 // physical row order of the model (capi.cu): blend order for the hot path, logical (creation)
@@ -232,8 +234,11 @@ constexpr int k3dParams = 59;
 cudaError_t launch_preprocess3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int W, int H);
 cudaError_t launch_bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const uint32_t* skeys, const uint32_t* svals,
                          int W, int H);
-cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, bool adam,
+// mode: 0 gradients out, 1 fused Adam, 2 accumulate into the batched step buffer
+cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int mode,
                            bool update_stats, float* grads, float* screen, const Adam3dCfg* cfg);
+cudaError_t launch_adam3d_step(tgsx_ctx* ctx, tgsx_model3d* m, int batch_views, const Adam3dCfg& cfg);
+constexpr int k3dStepRows = 62;  // 59 gradient sums, position-norm sum, colour-norm sum, visits
 cudaError_t launch_adam3d(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, const Adam3dCfg& cfg);
 
 }  // namespace tgsx

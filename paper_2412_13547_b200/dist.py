@@ -22,6 +22,10 @@ ROW_POS_NORM = 9          # sum of |dL/dmu| over the views that visited the Gaus
 ROW_COL_NORM = 10         # sum of |dL/d raw colour|
 ROW_VISITS = 11           # number of views that visited it
 
+# 3-D step buffer, [STEP3D_ROWS][capacity] (csrc/scene3d.cu chain3d mode 2): 59 gradient sums,
+# screen-space position-norm sum, SH-DC colour-norm sum, visits
+STEP3D_ROWS = 62
+
 
 def views_for_rank(views_per_step: int, rank: int, world: int) -> list[int]:
     """Round-robin view assignment: rank r renders views r, r + world, ..."""
@@ -65,10 +69,12 @@ class ViewShardedFit:
         return self._t
 
     def step(self, views, background, step: int, total_steps: int, image_diagonal: float):
+        """`views[v]` = (pattern, target) for a 2-D DeviceModel, (camera, pattern, target) for a
+        3-D DeviceModel3D (then `image_diagonal` is the scene extent of the 3-D learning rates)."""
         losses = []
         for v in views_for_rank(len(views), self.rank, self.world):
-            pat, target = views[v]
-            losses.append(self.dm.view_accumulate(pat, background, target))
+            *geom, target = views[v]
+            losses.append(self.dm.view_accumulate(*geom, background, target))
         if self.world > 1:
             import torch
             import torch.distributed as dist

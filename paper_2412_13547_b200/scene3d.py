@@ -223,6 +223,27 @@ class DeviceModel3D:
                                                   bg, tp, C.byref(a), _ptr(loss)))
         return float(loss[0])
 
+    def view_accumulate(self, cam: Camera, pattern: DilationPattern | None, background, target) -> float:
+        """One view of a batched step: render -> L1 -> backward -> chain rule, summed into the step
+        buffer (no parameter update)."""
+        pattern = pattern or cam.pattern()
+        bg = (C.c_float * 3)(*background)
+        tp = C.c_void_p(target) if isinstance(target, int) else _ptr(_f32(target))
+        loss = np.zeros(1, np.float32)
+        self.ctx.check(self.ctx.L.tgsx_view_accumulate3d(self.ctx.h, self.h, C.byref(cam.c()),
+                                                         C.byref(pattern.c()), bg, tp, _ptr(loss)))
+        return float(loss[0])
+
+    def step_buffer(self):
+        """(device pointer, float count) of the [62][capacity] step buffer (for the all-reduce)."""
+        n = C.c_int64()
+        ptr = self.ctx.L.tgsx_step_buffer3d(self.h, C.byref(n))
+        return int(ptr), int(n.value)
+
+    def apply_step(self, batch_views: int, step: int, total_steps: int, scene_extent: float):
+        a = _lib.Adam3dArgs(step, total_steps, scene_extent)
+        self.ctx.check(self.ctx.L.tgsx_apply_step3d(self.ctx.h, self.h, batch_views, C.byref(a)))
+
     def stage_prepare(self, cam: Camera, lowpass_p: int = 1):
         """Blend-ordered records of the visible Gaussians: dict of arrays (mx, my, i00, i01, i11,
         alpha, c0, c1, c2, rx, ry, orig, depth)."""

@@ -180,3 +180,39 @@ def test_errors(S, ctx):
     bad_cam = S.Camera(cam.R, cam.t, -1.0, cam.fy, cam.cx, cam.cy, 64, 48)
     with pytest.raises(ValueError):
         dm.render(bad_cam)
+
+
+def test_batched_views_equal_mean_of_per_view_gradients(S, ctx):
+    """Batched multi-camera step (view_accumulate3d x V + apply_step3d, driven through
+    dist.ViewShardedFit as one rank) == the mean of the per-view backward3d gradients (summed in
+    view order) followed by the oracle's Adam: bit-exact; statistics = summed increments."""
+    from paper_2412_13547_b200 import dist as D
+    W, H = 96, 72
+    cams = [S.Camera.look_at((0.4 * np.cos(a), 0.3 * np.sin(a), -0.5), (0.0, 0.0, 4.5), (0, -1, 0), 60.0, W, H)
+            for a in np.linspace(0, 2 * np.pi, 4, endpoint=False)]
+    m = S.GaussianModel3D.synthetic(9, 3000, cams[0])
+    rng = np.random.default_rng(5)
+    targets = [rng.uniform(0, 1, (H, W, 3)).astype(np.float32) for _ in cams]
+    ref = S.DeviceModel3D.from_host(m, ctx)
+    total = np.zeros((59, m.size()), np.float32)
+    visits = np.zeros(m.size(), np.int64)
+    for cam, tgt in zip(cams, targets):
+        pat = cam.pattern(1)
+        c = ref.render(cam, pat).colors.reshape(H, W, 3)
+        dl = (np.sign(c - tgt) * np.float32(1.0 / (3.0 * pat.active_count()))).astype(np.float32).reshape(-1, 3)
+        g, scr = ref.backward(cam, pat, (0, 0, 0), dl, update_stats=False, screen=True)
+        total = (total + g).astype(np.float32)
+        visits += scr[9] > 0
+    mean = (total / np.float32(len(cams))).astype(np.float32)
+    p = m.params.copy()
+    mom1, mom2 = np.zeros_like(p), np.zeros_like(p)
+    B.adam3d_step(p, mean, mom1, mom2, B.adam3d_config(1, 100, 3.0))
+    dm = S.DeviceModel3D.from_host(m, ctx)
+    fit = D.ViewShardedFit(dm, 0, 1)
+    losses = fit.step([(cam, cam.pattern(1), t) for cam, t in zip(cams, targets)], (0, 0, 0), 1, 100, 3.0)
+    assert len(losses) == 4 and all(np.isfinite(losses))
+    assert np.array_equal(dm.download().params.view(np.uint32), p.view(np.uint32))
+    _, _, vis = dm.stats()
+    assert np.array_equal(vis, visits)
+    ptr, count = dm.step_buffer()
+    assert ptr != 0 and count % D.STEP3D_ROWS == 0 and count // D.STEP3D_ROWS >= m.size()
