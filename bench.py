@@ -55,6 +55,10 @@ CONFIGS = {
                         "EWA + SH-3 front end (SURVEY.md §8a A3b), 1920x1080 p=1 single-view fit step "
                         "(preprocess3d + depth sort + binning + fwd + L1 + bwd + chain3d + Adam over 59 params)",
                n=1_000_000, W=1920, H=1080, p=1, three_d=True),
+    "c7": dict(workload="C7-3D: batched multi-camera fitting, 1M 3-D Gaussians SH3, 8 distinct 1080p cameras "
+                        "per step accumulated + one Adam step; cameras sharded across ranks with an NCCL "
+                        "all-reduce of the [62][N] step buffer", n=1_000_000, W=1920, H=1080, p=1,
+               three_d=True, views=8),
 }
 METRIC = "fit iters/sec (fwd+bwd+Adam) at 1080p and 4K dilated, 1M–3M Gaussians"
 
@@ -269,7 +273,7 @@ def roofline(stages, counters, clocks, n, config):
                              "(MEASURED_PEAKS.json has no FP32 figure)",
                 "work_note": f"algorithmic flops per launch 2E+{per_blend}Bl with E={E} evaluations, "
                              f"Bl={Bl} blends (SURVEY.md §8d)"}
-    if config == "c6":  # 3-D: chain3d + Adam streams 59 params, 2 moments (r+w), partials
+    if config in ("c6", "c7"):  # 3-D: chain3d + Adam streams 59 params, 2 moments (r+w), partials
         nb = {"chain_adam": (59 * 4 * 6 + 24) * n + 40 * K, "preprocess": (59 * 4 + 64 + 8) * n,
               "depth_sort": 4 * 24 * n + (64 + 64 + 16) * n}.get(dom, 0)
     else:
@@ -313,7 +317,7 @@ def run_tgsx(args, cfg):
         return (base + 0.02 * torch.randn(base.shape, generator=g, device="cuda")).contiguous()
 
     extra = {}
-    if cfg.get("three_d"):
+    if cfg.get("three_d") and args.config == "c6":
         from paper_2412_13547_b200 import scene3d as S3
         if world > 1:
             raise SystemExit("c6 (3-D front end) is single-view: run it with --gpus 1")
@@ -340,6 +344,43 @@ def run_tgsx(args, cfg):
         h_loss = torch.zeros(1).pin_memory()
         e2e_fn = lambda it: one_step(it, C.c_void_p(h_target.data_ptr()), C.c_void_p(h_loss.data_ptr()))  # noqa: E731
         e2e_bytes = (W * H * 12, 4)
+        units = 1
+    elif args.config == "c7":
+        from paper_2412_13547_b200 import scene3d as S3
+        views = cfg["views"]
+        fx = 0.5 * W / math.tan(math.radians(30))
+        cams = [S3.Camera.look_at((0.3 * math.cos(a), 0.2 * math.sin(a), 0.0), (0.0, 0.0, 4.5), (0, -1, 0),
+                                  60.0, W, H) for a in np.linspace(0, 2 * math.pi, views, endpoint=False)]
+        cam0 = S3.Camera(np.eye(3), np.zeros(3), fx, fx, W / 2, H / 2, W, H)
+        host = S3.GaussianModel3D.synthetic(1, n, cam0)
+        dm = S3.DeviceModel3D.from_host(host, ctx)
+        tm3 = S3.DeviceModel3D.from_host(S3.GaussianModel3D.synthetic(2, n, cam0), ctx)
+        targets = [torch.from_numpy(tm3.render(c).colors.reshape(H, W, 3).copy()).cuda().contiguous() for c in cams]
+        tm3.close()
+        torch.cuda.synchronize()
+        sharded = D.ViewShardedFit(dm, rank, world)
+        mine = D.views_for_rank(views, rank, world)
+        camc = [c.c() for c in cams]
+        pat = P.DilationPattern(1, 0, 0, W, H).c()
+        loss_dev = torch.zeros(views, device="cuda")
+        h_targets = [targets[v].cpu().pin_memory() for v in range(views)]
+        h_loss = torch.zeros(views).pin_memory()
+
+        def batched_step(it, tptrs, lbase):
+            for v in mine:
+                ctx.check(ctx.L.tgsx_view_accumulate3d(ctx.h, dm.h, C.byref(camc[v]), C.byref(pat), bg,
+                                                       C.c_void_p(tptrs[v]), C.c_void_p(lbase + 4 * v)))
+            if world > 1:
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(sharded._tensor())
+            a = P._lib.Adam3dArgs(it + 1, 10000, 3.0)
+            ctx.check(ctx.L.tgsx_apply_step3d(ctx.h, dm.h, views, C.byref(a)))
+
+        d_ptrs = [t.data_ptr() for t in targets]
+        h_ptrs = [t.data_ptr() for t in h_targets]
+        step_fn = lambda it: batched_step(it, d_ptrs, loss_dev.data_ptr())  # noqa: E731
+        e2e_fn = lambda it: batched_step(it, h_ptrs, h_loss.data_ptr())  # noqa: E731
+        e2e_bytes = (W * H * 12 * len(mine), 4 * len(mine))
         units = 1
     elif args.config in ("c2", "c3"):
         target = noisy(rank) if world > 1 else base.contiguous()
@@ -463,7 +504,7 @@ def run_tgsx(args, cfg):
     clocks = clk.summary()
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if args.config == "c5" else "weak",
+            "higher_is_better": True, "scaling": "strong" if args.config in ("c5", "c7") else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["workload"] + (f"; dense loss (1-{args.ssim}) L1 + {args.ssim} (1-SSIM)"
                                                       if args.ssim > 0 and p == 1 else ""),
