@@ -303,8 +303,9 @@ bool force_onesweep() {
 }
 
 // Per-tile sort of the slabs for lists up to `cap` entries (the template is chosen from it).
-int32_t slab_sort(tgsx_ctx* ctx, int64_t n, int tiles, uint64_t cap) {
-    {
+// pair_base: write each record's first pair slot (not needed when the preprocess fused the scan)
+int32_t slab_sort(tgsx_ctx* ctx, int64_t n, int tiles, uint64_t cap, bool pair_base = false) {
+    if (pair_base) {
         StageTimer t(ctx, kStDuplicate);
         CK(launch_pair_base(ctx, n));
     }
@@ -338,16 +339,16 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
         if (m->order_dirty) CK(launch_sort_depth(ctx, m));
         CK(model_to_blend_order(ctx, m));
     }
-    {
-        StageTimer t(ctx, kStPreprocess);
-        CK(launch_preprocess(ctx, m, lowpass_p, W, H));
-    }
     unsigned long long* counters = ws.counters.as<unsigned long long>();
     uint32_t* d_total = reinterpret_cast<uint32_t*>(counters + 3);
+    {
+        // rows are in blend order here: the pair-offset scan is fused into the preprocess
+        StageTimer t(ctx, kStPreprocess);
+        CK(launch_preprocess(ctx, m, lowpass_p, W, H, d_total));
+    }
     const int tiles = ws.tiles_x * ws.tiles_y;
     {
         StageTimer t(ctx, kStScan);
-        CK(launch_exclusive_scan(ctx, ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(), m->n, d_total));
         CK(launch_slab_finalize(ctx, tiles));
     }
     CK(cudaMemcpyAsync(ws.h_scratch, counters, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -760,18 +761,17 @@ int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, in
     }
     uint32_t* k = ws.keys[0].as<uint32_t>();
     uint32_t* v = ws.vals[0].as<uint32_t>();
+    unsigned long long* counters = ws.counters.as<unsigned long long>();
+    uint32_t* d_total = reinterpret_cast<uint32_t*>(counters + 3);
     {
         // blend order of this view: ascending camera depth, ties by row (stable LSD passes)
         StageTimer t(ctx, kStDepthSort);
         CK(sort_pairs(ctx, k, v, ws.keys[1].as<uint32_t>(), ws.vals[1].as<uint32_t>(), n, 32, nullptr));
-        CK(launch_bin3d(ctx, m, k, v, W, H));
+        CK(launch_bin3d(ctx, m, k, v, W, H, d_total));
     }
-    unsigned long long* counters = ws.counters.as<unsigned long long>();
-    uint32_t* d_total = reinterpret_cast<uint32_t*>(counters + 3);
     const int tiles = ws.tiles_x * ws.tiles_y;
     {
         StageTimer t(ctx, kStScan);
-        CK(launch_exclusive_scan(ctx, ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(), n, d_total));
         CK(launch_slab_finalize(ctx, tiles));
     }
     CK(cudaMemcpyAsync(ws.h_scratch, counters, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,

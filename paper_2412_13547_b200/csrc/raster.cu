@@ -21,25 +21,20 @@ namespace {
 constexpr int kFillStride = 32;
 
 // ------------------------------------------------------------------ preprocess
-__global__ void __launch_bounds__(256) preprocess_kernel(
-    const float* __restrict__ params, int64_t cap, int64_t n,
-    const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ perm, int blend_phys,
-    int lowpass_p, int W, int H, int tiles_x,
-    Prepared* __restrict__ prep, uint32_t* __restrict__ touched, uint32_t* __restrict__ fill,
-    uint32_t* __restrict__ slab, unsigned long long* err) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    // row i is rank i when the model is stored in blend order (logical index perm[i])
-    const uint32_t rank = blend_phys ? (uint32_t)i : rank_of[i];
-    const uint32_t orig = blend_phys ? perm[i] : (uint32_t)i;
+// One Gaussian (row i, blend rank `rank`): the prepared record, the number of tiles it touches
+// and (slab binning) its slot claims. Returns the tile count; 0 on an error (raised in err).
+__device__ __forceinline__ uint32_t prepare_one(const float* __restrict__ params, int64_t cap, int64_t i,
+                                                uint32_t rank, uint32_t orig, int lowpass_p, int W, int H,
+                                                int tiles_x, Prepared& o, uint32_t* __restrict__ fill,
+                                                uint32_t* __restrict__ slab, unsigned long long* err) {
     const float px = params[i], py = params[cap + i], rot = params[2 * cap + i];
     const float lx = params[3 * cap + i], ly = params[4 * cap + i], rop = params[5 * cap + i];
     const float cr = params[6 * cap + i], cg = params[7 * cap + i], cb = params[8 * cap + i];
+    o.d = make_uint4(0u, 0u, 0u, 0u);
     // covariance_from_params (gaussian.hpp:63-78)
     if (!isfinite(rot) || !isfinite(lx) || !isfinite(ly)) {
         raise_error(err, rank, 1);
-        touched[rank] = 0;
-        return;
+        return 0;
     }
     float sn, c;
     cr_sincosf(rot, &sn, &c);
@@ -56,10 +51,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     const float det = fsub(fmul(s00, s11), fmul(s01, s01));
     if (!(det > 0.0f) || !isfinite(det)) {
         raise_error(err, rank, 2);
-        touched[rank] = 0;
-        return;
+        return 0;
     }
-    Prepared o;
     o.a = make_float4(px, py, fdiv_pos(s11, det), fdiv_pos(-s01, det));
     const float rx = fmul(kCullSigmas, __fsqrt_rn(s00));
     const float ry = fmul(kCullSigmas, __fsqrt_rn(s11));
@@ -91,11 +84,52 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                         slab[(size_t)tt[u] * kSegCap + pos[u]] = rank;
             }
         }
-    } else {
-        o.d = make_uint4(0u, 0u, 0u, 0u);
     }
+    return tiles;
+}
+
+__global__ void __launch_bounds__(256) preprocess_kernel(
+    const float* __restrict__ params, int64_t cap, int64_t n,
+    const uint32_t* __restrict__ rank_of, const uint32_t* __restrict__ perm, int blend_phys,
+    int lowpass_p, int W, int H, int tiles_x,
+    Prepared* __restrict__ prep, uint32_t* __restrict__ touched, uint32_t* __restrict__ fill,
+    uint32_t* __restrict__ slab, unsigned long long* err) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    // row i is rank i when the model is stored in blend order (logical index perm[i])
+    const uint32_t rank = blend_phys ? (uint32_t)i : rank_of[i];
+    const uint32_t orig = blend_phys ? perm[i] : (uint32_t)i;
+    Prepared o;
+    const uint32_t tiles = prepare_one(params, cap, i, rank, orig, lowpass_p, W, H, tiles_x, o, fill, slab, err);
     prep[rank] = o;
     touched[rank] = tiles;
+}
+
+// Rows in blend order (rank == row), with the pair-offset scan fused in: blocks take
+// launch-ordered tickets, reduce their tile counts and find their prefix by decoupled look-back
+// (block_scan_lookback), so each record leaves with its first pair slot (d.z) and pair_off /
+// touched / the total K are written here: the separate scan and pair-base passes over the
+// Gaussians disappear from the step.
+__global__ void __launch_bounds__(256) preprocess_scan_kernel(
+    const float* __restrict__ params, int64_t cap, int64_t n, const uint32_t* __restrict__ perm,
+    int lowpass_p, int W, int H, int tiles_x, Prepared* __restrict__ prep, uint32_t* __restrict__ touched,
+    uint32_t* __restrict__ pair_off, uint32_t* __restrict__ fill, uint32_t* __restrict__ slab,
+    unsigned long long* err, unsigned long long* status, uint32_t* ticket, uint32_t* d_total) {
+    __shared__ uint32_t s_bid;
+    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t bid = s_bid;
+    const int64_t i = (int64_t)bid * 256 + threadIdx.x;
+    Prepared o;
+    uint32_t tiles = 0;
+    if (i < n) tiles = prepare_one(params, cap, i, (uint32_t)i, perm[i], lowpass_p, W, H, tiles_x, o, fill, slab, err);
+    const uint32_t excl = block_scan_lookback(tiles, bid, n, status, d_total);
+    if (i < n) {
+        o.d.z = excl;
+        prep[i] = o;
+        touched[i] = tiles;
+        pair_off[i] = excl;
+    }
 }
 
 // ------------------------------------------------------------------ key duplication
@@ -274,7 +308,7 @@ int key_bits_for(int tiles) {
     return b;
 }
 
-cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H) {
+cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t* d_total) {
     Workspace& ws = ctx->ws;
     const int64_t n = m->n;
     cudaError_t e;
@@ -287,7 +321,26 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
     if ((e = ws.tile_fill.ensure(tiles * 4 * kFillStride))) return e;
     if ((e = ws.tile_slab.ensure(tiles * 4 * kSegCap))) return e;
     if ((e = cudaMemsetAsync(ws.tile_fill.p, 0, tiles * 4 * kFillStride, ctx->stream))) return e;
-    if (n == 0) return cudaSuccess;
+    if (n == 0) {
+        if (d_total) return cudaMemsetAsync(d_total, 0, sizeof(uint32_t), ctx->stream);
+        return cudaSuccess;
+    }
+    if (d_total) {
+        // fused pair-offset scan: rows must be in blend order
+        if (!m->blend_phys) return cudaErrorInvalidValue;
+        const int64_t blocks = grid_for(n, 256);
+        const size_t need = 64 + (size_t)blocks * sizeof(unsigned long long);
+        if ((e = ws.scan_tmp.ensure(need))) return e;
+        if ((e = cudaMemsetAsync(ws.scan_tmp.p, 0, need, ctx->stream))) return e;
+        preprocess_scan_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(
+            m->params.as<float>(), m->cap, n, m->perm.as<uint32_t>(), lowpass_p, W, H, ws.tiles_x,
+            ws.prep.as<Prepared>(), ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(),
+            ws.tile_fill.as<uint32_t>(), ws.tile_slab.as<uint32_t>(), ws.counters.as<unsigned long long>(),
+            reinterpret_cast<unsigned long long*>(ws.scan_tmp.as<char>() + 64), ws.scan_tmp.as<uint32_t>(),
+            d_total);
+        ctx->launches++;
+        return cudaGetLastError();
+    }
     preprocess_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
         m->params.as<float>(), m->cap, n, m->rank_of.as<uint32_t>(), m->perm.as<uint32_t>(),
         m->blend_phys ? 1 : 0, lowpass_p, W, H, ws.tiles_x,

@@ -225,25 +225,32 @@ __global__ void __launch_bounds__(256) preprocess3d_kernel(
 }
 
 // ------------------------------------------------------------------ rank-order gather + binning
+// One thread per blend rank (blocks ticket-ordered): gathers the row's record, claims its slab
+// slots like the 2-D preprocess, and runs the pair-offset scan fused in (block_scan_lookback):
+// pair_off / touched / the record's first pair slot / the total K leave this kernel.
 __global__ void __launch_bounds__(256) bin3d_kernel(
     const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals, int64_t n,
     const Prepared* __restrict__ prep_row, int W, int H, int tiles_x, Prepared* __restrict__ prep,
-    uint32_t* __restrict__ touched, uint32_t* __restrict__ fill, uint32_t* __restrict__ slab,
-    uint32_t* __restrict__ perm, uint32_t* __restrict__ rank_of) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const uint32_t row = svals[r];
-    perm[r] = row;
-    rank_of[row] = (uint32_t)r;
-    if (skeys[r] == kCulledKey) {
-        touched[r] = 0;
-        prep[r].d = make_uint4(0u, 0u, 0u, 0u);
-        return;
-    }
-    Prepared o = prep_row[row];
-    int tx0, tx1, ty0, ty1;
+    uint32_t* __restrict__ touched, uint32_t* __restrict__ pair_off, uint32_t* __restrict__ fill,
+    uint32_t* __restrict__ slab, uint32_t* __restrict__ perm, uint32_t* __restrict__ rank_of,
+    unsigned long long* status, uint32_t* ticket, uint32_t* d_total) {
+    __shared__ uint32_t s_bid;
+    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t bid = s_bid;
+    const int64_t r = (int64_t)bid * 256 + threadIdx.x;
+    Prepared o;
+    o.d = make_uint4(0u, 0u, 0u, 0u);
     uint32_t tiles = 0;
-    if (tile_rect(o.a.x, o.a.y, o.b.z, o.b.w, W, H, tx0, tx1, ty0, ty1)) {
+    const bool live = r < n && skeys[r] != kCulledKey;
+    if (r < n) {
+        const uint32_t row = svals[r];
+        perm[r] = row;
+        rank_of[row] = (uint32_t)r;
+        if (live) o = prep_row[row];
+    }
+    int tx0, tx1, ty0, ty1;
+    if (live && tile_rect(o.a.x, o.a.y, o.b.z, o.b.w, W, H, tx0, tx1, ty0, ty1)) {
         tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
         o.d = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16),
                          0u, tiles);
@@ -264,8 +271,14 @@ __global__ void __launch_bounds__(256) bin3d_kernel(
     } else {
         o.d = make_uint4(0u, 0u, 0u, 0u);
     }
-    prep[r] = o;
-    touched[r] = tiles;
+    const uint32_t excl = block_scan_lookback(tiles, bid, n, status, d_total);
+    if (r < n) {
+        o.d.z = excl;
+        if (live) prep[r] = o;
+        else prep[r].d = o.d;
+        touched[r] = tiles;
+        pair_off[r] = excl;
+    }
 }
 
 // ------------------------------------------------------------------ chain rule (+ Adam)
@@ -704,14 +717,20 @@ cudaError_t launch_preprocess3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam,
 }
 
 cudaError_t launch_bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const uint32_t* skeys, const uint32_t* svals,
-                         int W, int H) {
+                         int W, int H, uint32_t* d_total) {
     Workspace& ws = ctx->ws;
     const int64_t n = m->n;
-    if (n == 0) return cudaSuccess;
-    bin3d_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+    if (n == 0) return cudaMemsetAsync(d_total, 0, sizeof(uint32_t), ctx->stream);
+    const int64_t blocks = grid_for(n, 256);
+    const size_t need = 64 + (size_t)blocks * sizeof(unsigned long long);
+    cudaError_t e;
+    if ((e = ws.scan_tmp.ensure(need))) return e;
+    if ((e = cudaMemsetAsync(ws.scan_tmp.p, 0, need, ctx->stream))) return e;
+    bin3d_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(
         skeys, svals, n, m->prep_row.as<Prepared>(), W, H, ws.tiles_x, ws.prep.as<Prepared>(),
-        ws.touched.as<uint32_t>(), ws.tile_fill.as<uint32_t>(), ws.tile_slab.as<uint32_t>(),
-        m->perm.as<uint32_t>(), m->rank_of.as<uint32_t>());
+        ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(), ws.tile_fill.as<uint32_t>(),
+        ws.tile_slab.as<uint32_t>(), m->perm.as<uint32_t>(), m->rank_of.as<uint32_t>(),
+        reinterpret_cast<unsigned long long*>(ws.scan_tmp.as<char>() + 64), ws.scan_tmp.as<uint32_t>(), d_total);
     ctx->launches++;
     return cudaGetLastError();
 }

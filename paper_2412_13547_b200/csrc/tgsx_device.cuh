@@ -104,6 +104,68 @@ __device__ __forceinline__ uint32_t orderable_key(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// ------------------------------------------------------------------ fused block scan
+// Exclusive prefix of `v` over a launch-ordered sequence of 256-thread blocks (block `bid`, all
+// threads call it): block scan + decoupled look-back over status[] (flag 2 bits | value 62 bits,
+// zeroed before the launch; bid from an atomic ticket so a block only waits on resident blocks).
+// The block holding element n-1 writes the grand total to *d_total.
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbIncl = 2ull << 62, kLbMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint32_t block_scan_lookback(uint32_t v, uint32_t bid, int64_t n,
+                                                        unsigned long long* status, uint32_t* d_total) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ unsigned long long s_prefix;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < 8 ? s_warp[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int d = 1; d < 8; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, wi, d);
+            if (lane >= d) wi += t;
+        }
+        if (lane < 8) s_warp[lane] = wi - w;
+        const unsigned long long block_total = __shfl_sync(0xffffffffu, wi, 7);
+        unsigned long long prefix = 0;
+        if (bid == 0) {
+            if (lane == 0) atomicExch(&status[0], kLbIncl | block_total);
+        } else {
+            if (lane == 0) atomicExch(&status[bid], kLbAgg | block_total);
+            int64_t j = (int64_t)bid - 1 - lane;
+            while (true) {
+                unsigned long long s = kLbIncl;  // virtual inclusive zero before block 0
+                if (j >= 0) {
+                    do {
+                        s = *reinterpret_cast<volatile unsigned long long*>(&status[j]);
+                    } while ((s >> 62) == 0);
+                }
+                const uint32_t im = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+                unsigned long long val = (!im || lane <= __ffs(im) - 1) ? (s & kLbMask) : 0ull;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) val += __shfl_xor_sync(0xffffffffu, val, d);
+                prefix += val;
+                if (im) break;
+                j -= 32;
+            }
+            if (lane == 0) atomicExch(&status[bid], kLbIncl | (prefix + block_total));
+        }
+        if (lane == 0) {
+            s_prefix = prefix;
+            if ((int64_t)(bid + 1) * 256 >= n) *d_total = (uint32_t)(prefix + block_total);
+        }
+    }
+    __syncthreads();
+    return (uint32_t)s_prefix + s_warp[warp] + (incl - v);
+}
+
 // ------------------------------------------------------------------ prepared splat record
 // 64 B per splat, blend (rank) order:
 //   a = (mean x, mean y, inv00, inv01)   b = (inv11, alpha, rx, ry)

@@ -186,7 +186,10 @@ struct RenderArgs {
 };
 
 cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m);
-cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H);
+// d_total non-null: the pair-offset scan is fused in (rows must be in blend order): pair_off,
+// the records' first pair slot and the total pair count K are written by the same kernel
+cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H,
+                              uint32_t* d_total = nullptr);
 cudaError_t launch_exclusive_scan(tgsx_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n,
                                   uint32_t* d_total);
 cudaError_t launch_duplicate(tgsx_ctx* ctx, int64_t n, int key_bits);
@@ -232,8 +235,9 @@ struct Adam3dCfg {
 };
 constexpr int k3dParams = 59;
 cudaError_t launch_preprocess3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int W, int H);
+// gather into blend order + slot claims + the fused pair-offset scan (total K to d_total)
 cudaError_t launch_bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const uint32_t* skeys, const uint32_t* svals,
-                         int W, int H);
+                         int W, int H, uint32_t* d_total);
 // mode: 0 gradients out, 1 fused Adam, 2 accumulate into the batched step buffer
 cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int mode,
                            bool update_stats, float* grads, float* screen, const Adam3dCfg* cfg);
