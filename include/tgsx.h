@@ -371,10 +371,12 @@ int32_t tgsx_view_accumulate3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera
                                const float bg[3], const float* target, float* out_loss);
 float* tgsx_step_buffer3d(tgsx_model3d* m, int64_t* out_floats);
 int32_t tgsx_apply_step3d(tgsx_ctx* ctx, tgsx_model3d* m, int32_t batch_views, const tgsx_adam3d_args* a);
-/* Parity stage: the blend-ordered 64-B records (Prepared layout, raster.cu) of all n ranks and
- * the sorted depth keys (culled rows last with key 0xffffffff). */
+/* Parity stage: the 64-B records (Prepared layout, raster.cu) of all n Gaussians and their
+ * orderable depth keys (culled: 0xffffffff), in the order the binning produced them:
+ * *out_blend_ordered = 0 -> row order (per-tile path: each tile list is sorted by (key, row)),
+ * 1 -> blend order (global-sort fallback for lists longer than a slab). */
 int32_t tgsx_stage_prepare3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, int32_t lowpass_p,
-                             float* out_records, uint32_t* out_keys);
+                             float* out_records, uint32_t* out_keys, int32_t* out_blend_ordered);
 
 #ifdef __cplusplus
 }

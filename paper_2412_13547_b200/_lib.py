@@ -151,7 +151,7 @@ SIGNATURES = {
                                     vp, vp, C.c_int32]),
     "tgsx_adam3d_step": (C.c_int32, [vp, vp, vp, P(Adam3dArgs)]),
     "tgsx_fit_step3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, vp, P(Adam3dArgs), vp]),
-    "tgsx_stage_prepare3d": (C.c_int32, [vp, vp, P(Camera3), C.c_int32, vp, vp]),
+    "tgsx_stage_prepare3d": (C.c_int32, [vp, vp, P(Camera3), C.c_int32, vp, vp, P(C.c_int32)]),
     "tgsx_view_accumulate3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, vp, vp]),
     "tgsx_step_buffer3d": (vp, [vp, i64p]),
     "tgsx_apply_step3d": (C.c_int32, [vp, vp, C.c_int32, P(Adam3dArgs)]),

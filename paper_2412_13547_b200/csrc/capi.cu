@@ -755,6 +755,43 @@ int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, in
     ws.have_forward = false;
     const int64_t n = m->n;
     CK(reset_counters(ctx));
+    unsigned long long* counters0 = ws.counters.as<unsigned long long>();
+    const int ntiles = ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+    if (!force_onesweep()) {
+        // per-tile path: no global depth sort. Rows claim their tiles' slab slots, the per-tile
+        // warp sort orders every list by (depth key, row) = the blend order inside the tile.
+        {
+            StageTimer t(ctx, kStPreprocess);
+            CK(launch_preprocess3d_bin(ctx, m, cam, lowpass_p, W, H, reinterpret_cast<uint32_t*>(counters0 + 3)));
+        }
+        {
+            StageTimer t(ctx, kStScan);
+            CK(launch_slab_finalize(ctx, ntiles));
+        }
+        CK(cudaMemcpyAsync(ws.h_scratch, counters0, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->prof.enabled) ctx->prof.harvest();
+        int32_t rc0 = check_kernel_error3d(ctx, ws.h_scratch[0]);
+        if (rc0) return rc0;
+        const uint64_t max_list = ws.h_scratch[5];
+        if (max_list <= (uint64_t)kSegCap) {
+            const int64_t K = (int64_t)(uint32_t)(ws.h_scratch[3] & 0xffffffffull);
+            ws.K = K;
+            CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
+            ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
+            {
+                StageTimer t(ctx, kStSort);
+                CK(launch_seg_sort3d(ctx, ntiles, (int64_t)max_list));
+            }
+            m->rank_ordered = false;
+            *items = ws.tile_slab.as<uint32_t>();
+            return TGSX_OK;
+        }
+        // a list longer than a slab: the global-sort path below
+        CK(reset_counters(ctx));
+    }
+    m->rank_ordered = true;
     {
         StageTimer t(ctx, kStPreprocess);
         CK(launch_preprocess3d(ctx, m, cam, lowpass_p, W, H));
@@ -768,6 +805,9 @@ int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, in
         StageTimer t(ctx, kStDepthSort);
         CK(sort_pairs(ctx, k, v, ws.keys[1].as<uint32_t>(), ws.vals[1].as<uint32_t>(), n, 32, nullptr));
         CK(launch_bin3d(ctx, m, k, v, W, H, d_total));
+        // the onesweep binning below reuses the key buffers: keep the sorted depth keys
+        CK(m->skeys.ensure((size_t)std::max<int64_t>(n, 1) * 4));
+        if (n) CK(cudaMemcpyAsync(m->skeys.p, k, (size_t)n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     }
     const int tiles = ws.tiles_x * ws.tiles_y;
     {
@@ -1389,7 +1429,7 @@ int32_t tgsx_model3d_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model3d** out)
 void tgsx_model3d_destroy(tgsx_model3d* m) {
     if (!m) return;
     DevBuf* bufs[] = {&m->params, &m->m1, &m->m2, &m->pos_acc, &m->col_acc, &m->visit,
-                      &m->perm, &m->rank_of, &m->prep_row, &m->gbuf, &m->step};
+                      &m->perm, &m->rank_of, &m->prep_row, &m->gbuf, &m->step, &m->skeys};
     for (DevBuf* b : bufs) b->release();
     delete m;
 }
@@ -1604,7 +1644,7 @@ static int32_t fused_view3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* c
 }
 
 int32_t tgsx_stage_prepare3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, int32_t lowpass_p,
-                             float* out_records, uint32_t* out_keys) {
+                             float* out_records, uint32_t* out_keys, int32_t* out_blend_ordered) {
     if (!ctx || !m || lowpass_p < 1) return TGSX_EINVAL;
     Cam3 c3;
     int32_t rc = make_cam3(ctx, cam, nullptr, &c3);
@@ -1614,8 +1654,11 @@ int32_t tgsx_stage_prepare3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* 
     const int64_t n = m->n;
     if (n && out_records) CK(cudaMemcpyAsync(out_records, ctx->ws.prep.p, (size_t)n * sizeof(Prepared),
                                              cudaMemcpyDefault, ctx->stream));
-    // sorted depth keys of the blend order (culled rows last, key 0xffffffff)
-    if (n && out_keys) CK(cudaMemcpyAsync(out_keys, ctx->ws.keys[0].p, (size_t)n * 4, cudaMemcpyDefault, ctx->stream));
+    // depth keys in the records' order (culled rows: key 0xffffffff)
+    if (n && out_keys)
+        CK(cudaMemcpyAsync(out_keys, m->rank_ordered ? m->skeys.p : ctx->ws.keys[0].p, (size_t)n * 4,
+                           cudaMemcpyDefault, ctx->stream));
+    if (out_blend_ordered) *out_blend_ordered = m->rank_ordered ? 1 : 0;
     CK(cudaStreamSynchronize(ctx->stream));
     return TGSX_OK;
 }

@@ -157,13 +157,13 @@ __device__ __forceinline__ void view_dir(const Cam3& cam, const float (&mu)[3], 
 __device__ __forceinline__ float sigmoidf(float x) { return 1.0f / (1.0f + expf(-x)); }
 
 // ------------------------------------------------------------------ preprocess
-__global__ void __launch_bounds__(256) preprocess3d_kernel(
-    const float* __restrict__ params, int64_t cap, int64_t n, Cam3 cam, float bump,
-    Prepared* __restrict__ prep_row, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-    unsigned long long* err) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    vals[i] = (uint32_t)i;
+// One Gaussian (row i): the 2-D record (d left zero) and its orderable depth key. Returns false
+// when culled (near plane) or invalid (error raised).
+__device__ __forceinline__ bool prepare3d_one(const float* __restrict__ params, int64_t cap, int64_t i,
+                                              const Cam3& cam, float bump, Prepared& o, uint32_t& key,
+                                              unsigned long long* err) {
+    key = kCulledKey;
+    o.d = make_uint4(0u, 0u, 0u, 0u);
     float mu[3], q[4], ls[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) mu[k] = __ldg(params + k * cap + i);
@@ -186,19 +186,14 @@ __global__ void __launch_bounds__(256) preprocess3d_kernel(
     finite &= (q[0] != 0.f || q[1] != 0.f || q[2] != 0.f || q[3] != 0.f);
     if (!finite) {
         raise_error(err, (uint32_t)i, 1);
-        keys[i] = kCulledKey;
-        return;
+        return false;
     }
     Geo3 g;
-    if (!geometry(cam, bump, mu, q, ls, g)) {
-        keys[i] = kCulledKey;
-        return;
-    }
+    if (!geometry(cam, bump, mu, q, ls, g)) return false;
     const float det = g.s00 * g.s11 - g.s01 * g.s01;
     if (!(det > 0.0f) || !isfinite(det)) {
         raise_error(err, (uint32_t)i, 2);
-        keys[i] = kCulledKey;
-        return;
+        return false;
     }
     float d[3], ilen;
     view_dir(cam, mu, d, ilen);
@@ -213,15 +208,157 @@ __global__ void __launch_bounds__(256) preprocess3d_kernel(
         rgb[c] = fmaxf(acc, 0.0f);
     }
     const float idet = 1.0f / det;
-    Prepared o;
     o.a = make_float4(cam.fx * g.tc[0] * g.iz + cam.cx, cam.fy * g.tc[1] * g.iz + cam.cy,
                       g.s11 * idet, -g.s01 * idet);
     o.b = make_float4(g.s00 * idet, sigmoidf(rop), kCullSigmas * sqrtf(g.s00),
                       kCullSigmas * sqrtf(g.s11));
     o.c = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float((uint32_t)i));
-    o.d = make_uint4(0u, 0u, 0u, 0u);
-    prep_row[i] = o;
-    keys[i] = __float_as_uint(g.tc[2]) | 0x80000000u;  // positive depth: orderable key
+    key = __float_as_uint(g.tc[2]) | 0x80000000u;  // positive depth: orderable key
+    return true;
+}
+
+// Slab claims of one visible record (the 2-D preprocess's claim loop), slot value `v`.
+__device__ __forceinline__ uint32_t claim3d(Prepared& o, int W, int H, int tiles_x, uint32_t v,
+                                            uint32_t* __restrict__ fill, uint32_t* __restrict__ slab) {
+    int tx0, tx1, ty0, ty1;
+    if (!tile_rect(o.a.x, o.a.y, o.b.z, o.b.w, W, H, tx0, tx1, ty0, ty1)) {
+        o.d = make_uint4(0u, 0u, 0u, 0u);
+        return 0;
+    }
+    const uint32_t tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+    o.d = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16), 0u, tiles);
+    const int w = tx1 - tx0 + 1, cnt = (int)tiles;
+    for (int q0 = 0; q0 < cnt; q0 += 4) {
+        uint32_t pos[4], tt[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (q0 + u < cnt) {
+                const int q = q0 + u;
+                tt[u] = (uint32_t)((ty0 + q / w) * tiles_x + tx0 + q % w);
+                pos[u] = atomicAdd(&fill[(size_t)tt[u] * kFillStride], 1u);
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (q0 + u < cnt && pos[u] < (uint32_t)kSegCap) slab[(size_t)tt[u] * kSegCap + pos[u]] = v;
+    }
+    return tiles;
+}
+
+// Global-sort path: records in row order + (depth key, row) pairs for the blend sort.
+__global__ void __launch_bounds__(256) preprocess3d_kernel(
+    const float* __restrict__ params, int64_t cap, int64_t n, Cam3 cam, float bump,
+    Prepared* __restrict__ prep_row, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+    unsigned long long* err) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    vals[i] = (uint32_t)i;
+    Prepared o;
+    uint32_t key;
+    if (prepare3d_one(params, cap, i, cam, bump, o, key, err)) prep_row[i] = o;
+    keys[i] = key;
+}
+
+// Per-tile path (no global sort): records stay in ROW order; every visible row claims its slab
+// slots with its row index, the pair-offset scan runs fused (ticket-ordered blocks), and the
+// per-tile warp sort (seg_sort3d_kernel) orders each list by (depth key, row) — the blend order
+// restricted to the tile, which is all the blend kernels read.
+__global__ void __launch_bounds__(256) preprocess3d_bin_kernel(
+    const float* __restrict__ params, int64_t cap, int64_t n, Cam3 cam, float bump, int W, int H,
+    int tiles_x, Prepared* __restrict__ prep, uint32_t* __restrict__ keys, uint32_t* __restrict__ touched,
+    uint32_t* __restrict__ pair_off, uint32_t* __restrict__ fill, uint32_t* __restrict__ slab,
+    unsigned long long* err, unsigned long long* status, uint32_t* ticket, uint32_t* d_total) {
+    __shared__ uint32_t s_bid;
+    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t bid = s_bid;
+    const int64_t i = (int64_t)bid * 256 + threadIdx.x;
+    Prepared o;
+    uint32_t key = kCulledKey, tiles = 0;
+    bool live = false;
+    if (i < n) {
+        live = prepare3d_one(params, cap, i, cam, bump, o, key, err);
+        if (live) tiles = claim3d(o, W, H, tiles_x, (uint32_t)i, fill, slab);
+    }
+    const uint32_t excl = block_scan_lookback(tiles, bid, n, status, d_total);
+    if (i < n) {
+        o.d.z = excl;
+        if (live) prep[i] = o;
+        else prep[i].d = make_uint4(0u, 0u, excl, 0u);
+        keys[i] = key;
+        touched[i] = tiles;
+        pair_off[i] = excl;
+    }
+}
+
+// Bitonic sort of 32*E 64-bit keys held by one warp (lane L owns positions L*E .. L*E+E-1).
+template <int E>
+__device__ __forceinline__ void warp_bitonic64(unsigned long long (&x)[E], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= E) {
+                const int lm = j / E;
+                const bool lower = (lane & lm) == 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const unsigned long long y = __shfl_xor_sync(0xffffffffu, x[e], lm);
+                    const bool asc = ((lane * E + e) & k) == 0;
+                    x[e] = (asc == lower) ? min(x[e], y) : max(x[e], y);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if ((e & j) == 0) {
+                        const bool asc = ((lane * E + e) & k) == 0;
+                        const unsigned long long a = x[e], b = x[e | j];
+                        x[e] = asc ? min(a, b) : max(a, b);
+                        x[e | j] = asc ? max(a, b) : min(a, b);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void warp_sort_rows(uint32_t* __restrict__ list, int n, const uint32_t* __restrict__ keys,
+                                               int lane) {
+    unsigned long long x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int t = lane * E + e;
+        if (t < n) {
+            const uint32_t row = list[t];
+            x[e] = ((unsigned long long)__ldg(keys + row) << 32) | row;
+        } else {
+            x[e] = ~0ull;
+        }
+    }
+    warp_bitonic64<E>(x, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        if (lane * E + e < n) list[lane * E + e] = (uint32_t)x[e];
+}
+
+// One warp per tile: the tile's rows (claimed in arbitrary order) sorted by (depth key, row).
+template <int MAXE>
+__global__ void __launch_bounds__(256) seg_sort3d_kernel(const uint2* __restrict__ ranges, int tiles,
+                                                         uint32_t* __restrict__ items,
+                                                         const uint32_t* __restrict__ keys) {
+    const int lane = threadIdx.x & 31;
+    const int tile = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (tile >= tiles) return;
+    const uint2 rg = ranges[tile];
+    const int n = (int)(rg.y - rg.x);
+    uint32_t* list = items + rg.x;
+    if (n <= 1) return;
+    if (n <= 32) warp_sort_rows<1>(list, n, keys, lane);
+    else if (n <= 64) warp_sort_rows<2>(list, n, keys, lane);
+    else if (n <= 128) warp_sort_rows<4>(list, n, keys, lane);
+    else if (MAXE <= 8 || n <= 256) warp_sort_rows<MAXE < 8 ? MAXE : 8>(list, n, keys, lane);
+    else if (MAXE <= 16 || n <= 512) warp_sort_rows<MAXE < 16 ? MAXE : 16>(list, n, keys, lane);
+    else warp_sort_rows<MAXE>(list, n, keys, lane);
 }
 
 // ------------------------------------------------------------------ rank-order gather + binning
@@ -249,28 +386,7 @@ __global__ void __launch_bounds__(256) bin3d_kernel(
         rank_of[row] = (uint32_t)r;
         if (live) o = prep_row[row];
     }
-    int tx0, tx1, ty0, ty1;
-    if (live && tile_rect(o.a.x, o.a.y, o.b.z, o.b.w, W, H, tx0, tx1, ty0, ty1)) {
-        tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-        o.d = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16),
-                         0u, tiles);
-        const int w = tx1 - tx0 + 1, cnt = (int)tiles;
-        for (int q0 = 0; q0 < cnt; q0 += 4) {
-            uint32_t pos[4], tt[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (q0 + u < cnt) {
-                    const int q = q0 + u;
-                    tt[u] = (uint32_t)((ty0 + q / w) * tiles_x + tx0 + q % w);
-                    pos[u] = atomicAdd(&fill[(size_t)tt[u] * kFillStride], 1u);
-                }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (q0 + u < cnt && pos[u] < (uint32_t)kSegCap) slab[(size_t)tt[u] * kSegCap + pos[u]] = (uint32_t)r;
-        }
-    } else {
-        o.d = make_uint4(0u, 0u, 0u, 0u);
-    }
+    if (live) tiles = claim3d(o, W, H, tiles_x, (uint32_t)r, fill, slab);
     const uint32_t excl = block_scan_lookback(tiles, bid, n, status, d_total);
     if (r < n) {
         o.d.z = excl;
@@ -458,7 +574,8 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
     if (i >= cp.n) return;
     const int64_t cap = cp.cap;
     const float* __restrict__ P = cp.params;
-    const uint32_t r = __ldg(cp.rank_of + i);
+    // per-tile path: pair slots by row; global-sort path: by blend rank
+    const uint32_t r = cp.rank_of ? __ldg(cp.rank_of + i) : (uint32_t)i;
     const uint32_t cnt = __ldg(cp.touched + r);
     float s[10];
 #pragma unroll
@@ -687,12 +804,10 @@ cudaError_t launch_adam3d(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, co
     return cudaGetLastError();
 }
 
-cudaError_t launch_preprocess3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p,
-                                int W, int H) {
+static cudaError_t prepare3d_buffers(tgsx_ctx* ctx, tgsx_model3d* m, int W, int H) {
     Workspace& ws = ctx->ws;
-    const int64_t n = m->n;
+    const int64_t c = std::max<int64_t>(m->n, 1);
     cudaError_t e;
-    const int64_t c = std::max<int64_t>(n, 1);
     if ((e = ws.prep.ensure(c * sizeof(Prepared)))) return e;
     if ((e = m->prep_row.ensure(c * sizeof(Prepared)))) return e;
     if ((e = ws.touched.ensure((c + 1) * 4))) return e;
@@ -706,12 +821,57 @@ cudaError_t launch_preprocess3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam,
     const size_t tiles = (size_t)std::max(ws.tiles_x * ws.tiles_y, 1);
     if ((e = ws.tile_fill.ensure(tiles * 4 * kFillStride))) return e;
     if ((e = ws.tile_slab.ensure(tiles * 4 * kSegCap))) return e;
-    if ((e = cudaMemsetAsync(ws.tile_fill.p, 0, tiles * 4 * kFillStride, ctx->stream))) return e;
+    return cudaMemsetAsync(ws.tile_fill.p, 0, tiles * 4 * kFillStride, ctx->stream);
+}
+
+cudaError_t launch_preprocess3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p,
+                                int W, int H) {
+    Workspace& ws = ctx->ws;
+    const int64_t n = m->n;
+    cudaError_t e;
+    if ((e = prepare3d_buffers(ctx, m, W, H))) return e;
     if (n == 0) return cudaSuccess;
     const float bump = 0.3f + 0.5f * (float)(lowpass_p - 1);
     preprocess3d_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
         m->params.as<float>(), m->cap, n, cam, bump, m->prep_row.as<Prepared>(),
         ws.keys[0].as<uint32_t>(), ws.vals[0].as<uint32_t>(), ws.counters.as<unsigned long long>());
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess3d_bin(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int W, int H,
+                                    uint32_t* d_total) {
+    Workspace& ws = ctx->ws;
+    cudaError_t e;
+    if ((e = prepare3d_buffers(ctx, m, W, H))) return e;
+    const int64_t n = m->n;
+    if (n == 0) return cudaMemsetAsync(d_total, 0, sizeof(uint32_t), ctx->stream);
+    const int64_t blocks = grid_for(n, 256);
+    const size_t need = 64 + (size_t)blocks * sizeof(unsigned long long);
+    if ((e = ws.scan_tmp.ensure(need))) return e;
+    if ((e = cudaMemsetAsync(ws.scan_tmp.p, 0, need, ctx->stream))) return e;
+    const float bump = 0.3f + 0.5f * (float)(lowpass_p - 1);
+    preprocess3d_bin_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(
+        m->params.as<float>(), m->cap, n, cam, bump, W, H, ws.tiles_x, ws.prep.as<Prepared>(),
+        ws.keys[0].as<uint32_t>(), ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(),
+        ws.tile_fill.as<uint32_t>(), ws.tile_slab.as<uint32_t>(), ws.counters.as<unsigned long long>(),
+        reinterpret_cast<unsigned long long*>(ws.scan_tmp.as<char>() + 64), ws.scan_tmp.as<uint32_t>(), d_total);
+    ctx->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seg_sort3d(tgsx_ctx* ctx, int tiles, int64_t max_list) {
+    if (tiles == 0) return cudaSuccess;
+    const uint2* rg = ctx->ws.ranges.as<uint2>();
+    uint32_t* items = ctx->ws.tile_slab.as<uint32_t>();
+    const uint32_t* keys = ctx->ws.keys[0].as<uint32_t>();
+    const unsigned grid = grid_for(tiles, 8);
+    if (max_list <= 256)
+        seg_sort3d_kernel<8><<<grid, 256, 0, ctx->stream>>>(rg, tiles, items, keys);
+    else if (max_list <= 512)
+        seg_sort3d_kernel<16><<<grid, 256, 0, ctx->stream>>>(rg, tiles, items, keys);
+    else
+        seg_sort3d_kernel<32><<<grid, 256, 0, ctx->stream>>>(rg, tiles, items, keys);
     ctx->launches++;
     return cudaGetLastError();
 }
@@ -745,7 +905,7 @@ cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int 
     cp.n = m->n;
     cp.cam = cam;
     cp.bump = 0.3f + 0.5f * (float)(lowpass_p - 1);
-    cp.rank_of = m->rank_of.as<uint32_t>();
+    cp.rank_of = m->rank_ordered ? m->rank_of.as<uint32_t>() : nullptr;
     cp.pair_off = ctx->ws.pair_off.as<uint32_t>();
     cp.touched = ctx->ws.touched.as<uint32_t>();
     cp.partial = Partials::at(ctx->ws.partial.p, ctx->ws.pair_cap);

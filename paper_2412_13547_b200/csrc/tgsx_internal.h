@@ -157,6 +157,9 @@ struct tgsx_model3d {
     tgsx::DevBuf gbuf;              // float[17][n] chain-rule output of the fused step (scene3d.cu)
     tgsx::DevBuf step;              // float[62][cap] batched-view step buffer (all-reduced across ranks)
     int64_t step_views = 0;
+    tgsx::DevBuf skeys;             // u32[cap] sorted depth keys of the global-sort path (parity stage)
+    bool rank_ordered = false;      // last binning: records / pair slots by blend rank (global-sort
+                                    // path) rather than by row (per-tile path)
 };
 
 // physical row order of the model (capi.cu): blend order for the hot path, logical (creation)
@@ -235,6 +238,11 @@ struct Adam3dCfg {
 };
 constexpr int k3dParams = 59;
 cudaError_t launch_preprocess3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int W, int H);
+// per-tile path: records by row, slab claims by row, fused pair-offset scan (K to d_total)
+cudaError_t launch_preprocess3d_bin(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int W, int H,
+                                    uint32_t* d_total);
+// per-tile (depth key, row) sort of the slabs (keys = ws.keys[0] by row)
+cudaError_t launch_seg_sort3d(tgsx_ctx* ctx, int tiles, int64_t max_list);
 // gather into blend order + slot claims + the fused pair-offset scan (total K to d_total)
 cudaError_t launch_bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const uint32_t* skeys, const uint32_t* svals,
                          int W, int H, uint32_t* d_total);

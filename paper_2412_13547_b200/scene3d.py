@@ -250,14 +250,20 @@ class DeviceModel3D:
         n = self.size()
         rec = np.zeros((max(n, 1), 16), np.float32)
         keys = np.zeros(max(n, 1), np.uint32)
+        ordered = C.c_int32()
         self.ctx.check(self.ctx.L.tgsx_stage_prepare3d(self.ctx.h, self.h, C.byref(cam.c()), lowpass_p,
-                                                       _ptr(rec), _ptr(keys)))
-        nv = int(np.count_nonzero(keys[:n] != 0xFFFFFFFF))
+                                                       _ptr(rec), _ptr(keys), C.byref(ordered)))
+        rec, keys = rec[:n], keys[:n]
+        if not ordered.value:  # row order: the blend order is (depth key, row)
+            rows = np.arange(n, dtype=np.uint64)
+            order = np.argsort((keys.astype(np.uint64) << np.uint64(32)) | rows, kind="stable")
+            rec, keys = rec[order], keys[order]
+        nv = int(np.count_nonzero(keys != 0xFFFFFFFF))
         r = rec[:nv]  # Prepared: (mx, my, i00, i01) (i11, alpha, rx, ry) (r, g, b, orig) (rect)
         out = {"mx": r[:, 0], "my": r[:, 1], "i00": r[:, 2], "i01": r[:, 3], "i11": r[:, 4],
                "alpha": r[:, 5], "rx": r[:, 6], "ry": r[:, 7], "c0": r[:, 8], "c1": r[:, 9],
                "c2": r[:, 10], "orig": r[:, 11].view(np.uint32).copy(),
-               "depth": (keys[:nv] & 0x7FFFFFFF).view(np.float32).copy()}
+               "depth": (keys[:nv] & 0x7FFFFFFF).view(np.float32).copy(), "blend_ordered": bool(ordered.value)}
         return out
 
 
