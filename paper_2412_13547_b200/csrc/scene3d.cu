@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256) preprocess3d_kernel(
 // slots with its row index, the pair-offset scan runs fused (ticket-ordered blocks), and the
 // per-tile warp sort (seg_sort3d_kernel) orders each list by (depth key, row) — the blend order
 // restricted to the tile, which is all the blend kernels read.
-__global__ void __launch_bounds__(256) preprocess3d_bin_kernel(
+__global__ void __launch_bounds__(256, 3) preprocess3d_bin_kernel(
     const float* __restrict__ params, int64_t cap, int64_t n, Cam3 cam, float bump, int W, int H,
     int tiles_x, Prepared* __restrict__ prep, uint32_t* __restrict__ keys, uint32_t* __restrict__ touched,
     uint32_t* __restrict__ pair_off, uint32_t* __restrict__ fill, uint32_t* __restrict__ slab,
@@ -353,10 +353,9 @@ __global__ void __launch_bounds__(256) seg_sort3d_kernel(const uint2* __restrict
     const int n = (int)(rg.y - rg.x);
     uint32_t* list = items + rg.x;
     if (n <= 1) return;
-    if (n <= 32) warp_sort_rows<1>(list, n, keys, lane);
-    else if (n <= 64) warp_sort_rows<2>(list, n, keys, lane);
-    else if (n <= 128) warp_sort_rows<4>(list, n, keys, lane);
-    else if (MAXE <= 8 || n <= 256) warp_sort_rows<MAXE < 8 ? MAXE : 8>(list, n, keys, lane);
+    // three network sizes only: the fully unrolled 64-bit networks are large, and warps of one SM
+    // running many different sizes thrash the instruction cache (ncu: no_instruction stalls)
+    if (n <= 64) warp_sort_rows<2>(list, n, keys, lane);
     else if (MAXE <= 16 || n <= 512) warp_sort_rows<MAXE < 16 ? MAXE : 16>(list, n, keys, lane);
     else warp_sort_rows<MAXE>(list, n, keys, lane);
 }
