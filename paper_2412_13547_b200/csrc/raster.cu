@@ -256,10 +256,9 @@ __global__ void __launch_bounds__(256) seg_sort_kernel(const uint2* __restrict__
     const int n = (int)(rg.y - rg.x);
     uint32_t* list = items + rg.x;
     if (n <= 1) return;
-    if (n <= 32) warp_sort_list<1>(list, n, lane);
-    else if (n <= 64) warp_sort_list<2>(list, n, lane);
-    else if (n <= 128) warp_sort_list<4>(list, n, lane);
-    else if (MAXE <= 8 || n <= 256) warp_sort_list<MAXE < 8 ? MAXE : 8>(list, n, lane);
+    // three network sizes: warps of one SM running many different fully unrolled networks
+    // thrash the instruction cache
+    if (n <= 64) warp_sort_list<2>(list, n, lane);
     else if (MAXE <= 16 || n <= 512) warp_sort_list<MAXE < 16 ? MAXE : 16>(list, n, lane);
     else warp_sort_list<MAXE>(list, n, lane);
 }
