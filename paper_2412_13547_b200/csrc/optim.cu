@@ -129,8 +129,25 @@ __global__ void __launch_bounds__(256, 4) chain_kernel(ChainParams cp) {
             vv0[q] = cp.m2[o];
         }
     }
-    // two slots per step (the loads of both in flight together); sums in slot order
+    // four / two slots per step (their loads in flight together); sums in slot order
     uint32_t t = 0;
+    for (; t + 3 < cnt; t += 4) {
+        float4 a[4], b[4];
+        float2 c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = pa[t + u];
+            b[u] = pb[t + u];
+            c[u] = pc[t + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            s[0] += a[u].x; s[1] += a[u].y; s[2] += a[u].z; s[3] += a[u].w;
+            s[4] += b[u].x; s[5] += b[u].y; s[6] += b[u].z; s[7] += b[u].w;
+            s[8] += c[u].x;
+            s[9] = fmaxf(s[9], c[u].y);
+        }
+    }
     for (; t + 1 < cnt; t += 2) {
         const float4 a0 = pa[t], b0 = pb[t], a1 = pa[t + 1], b1 = pb[t + 1];
         const float2 c0 = pc[t], c1 = pc[t + 1];
