@@ -95,7 +95,9 @@ class ClockSampler:
     def sample_nvml(self):
         N = self.nvml
         sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
-        mx = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        if getattr(self, "_max", None) is None:  # constant: queried once
+            self._max = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        mx = self._max
         bits = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         rs = [name for name, attr in self.REASONS if bits & getattr(N, attr, 0)]
         return sm, mx, rs
@@ -118,7 +120,7 @@ class ClockSampler:
                 self.samples.append(self.sample_nvml() if self.nvml else self.sample_smi())
             except Exception:
                 pass
-            self.stop.wait(0.01 if self.nvml else 0.1)
+            self.stop.wait(0.005 if self.nvml else 0.1)
 
     def __enter__(self):
         self.th.start()
@@ -510,7 +512,9 @@ def run_tgsx(args, cfg):
                                                       if args.ssim > 0 and p == 1 else ""),
                        "gaussians": n, "width": W, "height": H, "p": p,
                        "views_per_step": units if args.config in ("c2", "c3", "c6") else cfg.get("views", 1),
-                       "l2": "per-step working set > 126 MB L2 (no explicit flush)"},
+                       "l2": "per-step working set > 126 MB L2 (no explicit flush)",
+                       "trajectory": "every timed phase starts from the same initial model; the per-step "
+                                     "work changes as the fit proceeds, so the average depends on steps"},
             "clocks": clocks,
             "gpu_launches": launches,
             "roofline": roofline(stages, counters, clocks, n, args.config),
@@ -544,7 +548,8 @@ def run_tgsx(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    # 200 C2 steps ~ 0.3 s timed: long enough for >= 10 clock samples inside the timed region
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="tgsx", choices=["tgsx", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
