@@ -256,14 +256,31 @@ def measured_traffic(config, kernel):
         return None
 
 
-def roofline(stages, counters, clocks, n, config):
+def measure_fp32_peak(ctx):
+    """Measured FP32 FMA throughput (TFLOP/s) of this GPU: scalar FFMA and packed FFMA2."""
+    a, b = C.c_double(), C.c_double()
+    try:
+        ctx.check(ctx.L.tgsx_measure_fp32_peak(ctx.h, C.byref(a), C.byref(b)))
+        return {"ffma": a.value, "ffma2": b.value}
+    except Exception:
+        return None
+
+
+def roofline(stages, counters, clocks, n, config, fp32_meas=None):
     peaks = measured_peaks()
     per = {k: (v[0] / max(v[1], 1), v[1]) for k, v in stages.items() if v[1]}
     dom = max(per, key=lambda k: per[k][0] * per[k][1])
     dom_ms = per[dom][0]
     E, Bl, K = counters["evals"], counters["blend_ops"], counters["pairs"]
     f_mhz = clocks.get("sm_mhz") or peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1342.0)
-    fp32_peak = 148 * 128 * 2 * f_mhz * 1e6 / 1e12  # TFLOP/s at the sampled SM clock
+    fp32_nominal = 148 * 128 * 2 * f_mhz * 1e6 / 1e12  # TFLOP/s at the sampled SM clock
+    if fp32_meas:
+        fp32_peak = max(fp32_meas["ffma"], fp32_meas["ffma2"])
+        note = (f"measured on this GPU (tgsx_measure_fp32_peak): FFMA {fp32_meas['ffma']:.1f}, packed FFMA2 "
+                f"{fp32_meas['ffma2']:.1f} TFLOP/s; nominal 148 SM x 128 lanes x 2 x clock = {fp32_nominal:.1f}")
+    else:
+        fp32_peak = fp32_nominal
+        note = "148 SM x 128 FP32 lanes x 2 x median sampled SM clock (MEASURED_PEAKS.json has no FP32 figure)"
     if dom in ("blend_backward", "blend_forward"):
         per_blend = 77 if dom == "blend_backward" else 20
         achieved = (2 * E + per_blend * Bl) / (dom_ms / 1e3) / 1e12
@@ -271,8 +288,7 @@ def roofline(stages, counters, clocks, n, config):
                 "unit": "TFLOP/s", "frac": achieved / fp32_peak,
                 "traffic": measured_traffic(config, dom),
                 "ms_per_launch": dom_ms,
-                "peak_note": "148 SM x 128 FP32 lanes x 2 x median sampled SM clock "
-                             "(MEASURED_PEAKS.json has no FP32 figure)",
+                "peak_note": note,
                 "work_note": f"algorithmic flops per launch 2E+{per_blend}Bl with E={E} evaluations, "
                              f"Bl={Bl} blends (SURVEY.md §8d)"}
     if config in ("c6", "c7"):  # 3-D: chain3d + Adam streams 59 params, 2 moments (r+w), partials
@@ -498,6 +514,7 @@ def run_tgsx(args, cfg):
             e2e_fn(i)
         ctx.synchronize()
         e2e_ms = timer.run(e2e_fn, args.steps, args.warmup, ctx)
+    fp32_meas = measure_fp32_peak(ctx)  # after the timed regions
     if rank != 0:
         dist.barrier()
         dist.destroy_process_group()
@@ -517,7 +534,7 @@ def run_tgsx(args, cfg):
                                      "work changes as the fit proceeds, so the average depends on steps"},
             "clocks": clocks,
             "gpu_launches": launches,
-            "roofline": roofline(stages, counters, clocks, n, args.config),
+            "roofline": roofline(stages, counters, clocks, n, args.config, fp32_meas),
             "stages_ms_per_step": {k: v[0] / prof_steps for k, v in stages.items() if v[1]},
             "counters": counters}
     if e2e_ms is not None:

@@ -378,6 +378,11 @@ int32_t tgsx_apply_step3d(tgsx_ctx* ctx, tgsx_model3d* m, int32_t batch_views, c
 int32_t tgsx_stage_prepare3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, int32_t lowpass_p,
                              float* out_records, uint32_t* out_keys, int32_t* out_blend_ordered);
 
+/* Diagnostics: measured FP32 throughput of this GPU (8 independent FMA chains per thread, one
+ * launch of 8 CTAs x 256 threads per SM) with scalar FFMA and packed FFMA2, in TFLOP/s (FMA = 2
+ * flops) — the roofline denominator of the blend kernels. */
+int32_t tgsx_measure_fp32_peak(tgsx_ctx* ctx, double* out_ffma_tflops, double* out_ffma2_tflops);
+
 #ifdef __cplusplus
 }
 #endif

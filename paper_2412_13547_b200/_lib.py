@@ -155,6 +155,7 @@ SIGNATURES = {
     "tgsx_view_accumulate3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, vp, vp]),
     "tgsx_step_buffer3d": (vp, [vp, i64p]),
     "tgsx_apply_step3d": (C.c_int32, [vp, vp, C.c_int32, P(Adam3dArgs)]),
+    "tgsx_measure_fp32_peak": (C.c_int32, [vp, f64p, f64p]),
 }
 
 _LIB = None

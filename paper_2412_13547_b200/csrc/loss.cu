@@ -275,3 +275,69 @@ cudaError_t launch_loss_finalize(tgsx_ctx* ctx, const float* l1_part, int n1, fl
 }
 
 }  // namespace tgsx
+
+// ---------------------------------------------------------------- FP32 peak microbenchmark
+// Roofline denominator for the blend kernels ("add a measured FFMA
+// microbenchmark peak"): 8 independent FMA chains per thread, scalar FFMA or packed FFMA2,
+// grid = 8 CTAs x 256 threads per SM; timed with CUDA events on the context stream.
+namespace tgsx {
+namespace {
+template <bool PACKED>
+__global__ void __launch_bounds__(256) fp32_peak_kernel(float* out, int iters, float a, float b) {
+    float2 x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = make_float2((float)(threadIdx.x + j), (float)(blockIdx.x - j));
+    const float2 av = make_float2(a, a), bv = make_float2(b, b);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (PACKED) {
+                x[j] = __ffma2_rn(x[j], av, bv);
+            } else {
+                x[j].x = __fmaf_rn(x[j].x, a, b);
+                x[j].y = __fmaf_rn(x[j].y, a, b);
+            }
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += x[j].x + x[j].y;
+    if (s == 1234.5f) out[0] = s;  // never true: keeps the chains live
+}
+}  // namespace
+}  // namespace tgsx
+
+extern "C" int32_t tgsx_measure_fp32_peak(tgsx_ctx* ctx, double* out_ffma_tflops, double* out_ffma2_tflops) {
+    using namespace tgsx;
+    if (!ctx) return TGSX_EINVAL;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return TGSX_ECUDA;
+    if (ctx->ws.generic.ensure(64) != cudaSuccess) return TGSX_ECUDA;
+    float* out = ctx->ws.generic.as<float>();
+    const unsigned blocks = (unsigned)sms * 8u;
+    const int iters = 4096;
+    const double flops = 2.0 * 16.0 * iters * (double)blocks * 256.0;  // 16 FMAs per iteration
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double res[2] = {0.0, 0.0};
+    for (int packed = 0; packed < 2; ++packed) {
+        for (int rep = 0; rep < 3; ++rep) {  // first repetition warms up
+            cudaEventRecord(e0, ctx->stream);
+            if (packed) fp32_peak_kernel<true><<<blocks, 256, 0, ctx->stream>>>(out, iters, 0.999f, 1e-3f);
+            else fp32_peak_kernel<false><<<blocks, 256, 0, ctx->stream>>>(out, iters, 0.999f, 1e-3f);
+            cudaEventRecord(e1, ctx->stream);
+            ctx->launches++;
+            if (cudaEventSynchronize(e1) != cudaSuccess) return TGSX_ECUDA;
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep) res[packed] = std::max(res[packed], flops / (ms * 1e-3) / 1e12);
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (out_ffma_tflops) *out_ffma_tflops = res[0];
+    if (out_ffma2_tflops) *out_ffma2_tflops = res[1];
+    return cudaGetLastError() == cudaSuccess ? TGSX_OK : TGSX_ECUDA;
+}
