@@ -173,6 +173,10 @@ def run_reference(args, cfg):
     rank, world, _ = env_rank()
     if rank != 0:
         return
+    if cfg.get("three_d"):
+        print(json.dumps({"impl": "reference", "unavailable": "the reference is a 2-D analog of 3DGS: "
+                          "it has no 3-D front end (SURVEY.md §0)"}), flush=True)
+        return
     B, impl, threads, s, target = _ref_setup(cfg)
     m1 = np.zeros((9, s.n), np.float32)
     m2 = np.zeros((9, s.n), np.float32)

@@ -139,6 +139,11 @@ int32_t tgsx_loss(tgsx_ctx* ctx, const tgsx_pattern* pat, const float* rgb, cons
 /* lambda_ssim of the fused fit views below on dense patterns (default 0: L1 only; the trainer
  * uses its config's value, SPEC.md DESIGN DECISIONS 0.2). */
 int32_t tgsx_set_ssim_weight(tgsx_ctx* ctx, float ssim_weight);
+/* Binning path: 0 (default) slab binning with per-tile sorts (2-D and 3-D), falling back to the
+ * onesweep paths for lists longer than a slab; 1 always the onesweep paths (2-D: key
+ * duplication + radix sort; 3-D: global depth sort + rank gather + onesweep). Both give identical
+ * per-tile lists (tests compare them at full size). */
+int32_t tgsx_set_binning(tgsx_ctx* ctx, int32_t mode);
 
 /* One fused fit iteration on one view: render -> loss (L1 over active pixels; plus the SSIM
  * term on dense views when tgsx_set_ssim_weight > 0)

@@ -100,6 +100,7 @@ SIGNATURES = {
     "tgsx_fit_step": (C.c_int32, [vp, vp, P(Pattern), f32p, vp, P(AdamArgs), vp]),
     "tgsx_loss": (C.c_int32, [vp, P(Pattern), vp, vp, C.c_float, vp, vp]),
     "tgsx_set_ssim_weight": (C.c_int32, [vp, C.c_float]),
+    "tgsx_set_binning": (C.c_int32, [vp, C.c_int32]),
     "tgsx_view_accumulate": (C.c_int32, [vp, vp, P(Pattern), f32p, vp, vp]),
     "tgsx_step_buffer": (vp, [vp, i64p]),
     "tgsx_apply_step": (C.c_int32, [vp, vp, C.c_int32, P(AdamArgs)]),

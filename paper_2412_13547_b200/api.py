@@ -263,6 +263,10 @@ class Context:
     def profile(self, enable: bool = True):
         self.check(self.L.tgsx_profile(self.h, 1 if enable else 0))
 
+    def set_binning(self, mode: int):
+        """0: slab binning with per-tile sorts (default); 1: always the onesweep paths."""
+        self.check(self.L.tgsx_set_binning(self.h, int(mode)))
+
     def set_ssim_weight(self, weight: float):
         """lambda_ssim of dense fused fit views (0 = L1 only)."""
         self.check(self.L.tgsx_set_ssim_weight(self.h, float(weight)))

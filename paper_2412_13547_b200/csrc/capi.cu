@@ -294,12 +294,14 @@ cudaError_t reset_counters(tgsx_ctx* ctx) {
     return cudaMemsetAsync(ws.counters.p, 0xff, sizeof(unsigned long long), ctx->stream);
 }
 
-bool force_onesweep() {
+// TGSX_BINNING=onesweep (process-wide) or tgsx_set_binning(ctx, 1): onesweep tile binning for
+// 2-D views, the global depth sort + onesweep binning for 3-D views (the fallback paths)
+bool force_onesweep(const tgsx_ctx* ctx) {
     static const bool v = [] {
         const char* s = std::getenv("TGSX_BINNING");
         return s && std::string(s) == "onesweep";
     }();
-    return v;
+    return v || (ctx && ctx->binning_mode == 1);
 }
 
 // Per-tile sort of the slabs for lists up to `cap` entries (the template is chosen from it).
@@ -353,7 +355,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
     }
     CK(cudaMemcpyAsync(ws.h_scratch, counters, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        ctx->stream));
-    if (defer && !sorted_keys && !force_onesweep() && !debug_checks()) {
+    if (defer && !sorted_keys && !force_onesweep(ctx) && !debug_checks()) {
         if (!ctx->bin_event) CK(cudaEventCreateWithFlags(&ctx->bin_event, cudaEventDisableTiming));
         CK(cudaEventRecord(ctx->bin_event, ctx->stream));
         const uint64_t guess = std::min<uint64_t>(kSegCap, ctx->bin_max_hint + ctx->bin_max_hint / 4);
@@ -374,7 +376,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
     ctx->bin_max_hint = max_list;
     CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
     ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
-    if (max_list <= (uint64_t)kSegCap && !force_onesweep()) {
+    if (max_list <= (uint64_t)kSegCap && !force_onesweep(ctx)) {
         // slab binning: every tile's list was claimed by preprocess into its slab; sort each slab
         // back into blend order (one warp per tile)
         rc = slab_sort(ctx, m->n, tiles, max_list);
@@ -757,7 +759,7 @@ int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, in
     CK(reset_counters(ctx));
     unsigned long long* counters0 = ws.counters.as<unsigned long long>();
     const int ntiles = ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
-    if (!force_onesweep()) {
+    if (!force_onesweep(ctx)) {
         // per-tile path: no global depth sort. Rows claim their tiles' slab slots, the per-tile
         // warp sort orders every list by (depth key, row) = the blend order inside the tile.
         {
@@ -825,7 +827,7 @@ int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, in
     ws.K = K;
     CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
     ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
-    if (max_list <= (uint64_t)kSegCap && !force_onesweep()) {
+    if (max_list <= (uint64_t)kSegCap && !force_onesweep(ctx)) {
         rc = slab_sort(ctx, n, tiles, max_list);
         if (rc) return rc;
         *items = ws.tile_slab.as<uint32_t>();
@@ -1233,6 +1235,13 @@ float* tgsx_step_buffer(tgsx_model* m, int64_t* out_floats) {
     if (!m) return nullptr;
     if (out_floats) *out_floats = (int64_t)kStepFloats * m->cap;
     return m->step.as<float>();
+}
+
+int32_t tgsx_set_binning(tgsx_ctx* ctx, int32_t mode) {
+    if (!ctx || mode < 0 || mode > 1) return TGSX_EINVAL;
+    ctx->binning_mode = mode;
+    ctx->bin_valid = false;
+    return TGSX_OK;
 }
 
 int32_t tgsx_set_ssim_weight(tgsx_ctx* ctx, float ssim_weight) {

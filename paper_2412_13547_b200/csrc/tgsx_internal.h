@@ -97,6 +97,7 @@ struct tgsx_ctx {
     // tile lists do not depend on the dilation offset). Any entry point that changes the
     // parameters, the row order or the binning workspace clears bin_valid.
     float ssim_weight = 0.f;  // lambda_ssim of dense fused views (tgsx_set_ssim_weight)
+    int binning_mode = 0;     // 0 slab / per-tile binning with fallback, 1 force the onesweep paths
     bool bin_valid = false;
     uint64_t bin_model = 0;
     int bin_lowpass = 0, bin_W = 0, bin_H = 0;
