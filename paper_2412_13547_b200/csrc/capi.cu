@@ -305,12 +305,9 @@ bool force_onesweep(const tgsx_ctx* ctx) {
 }
 
 // Per-tile sort of the slabs for lists up to `cap` entries (the template is chosen from it).
-// pair_base: write each record's first pair slot (not needed when the preprocess fused the scan)
-int32_t slab_sort(tgsx_ctx* ctx, int64_t n, int tiles, uint64_t cap, bool pair_base = false) {
-    if (pair_base) {
-        StageTimer t(ctx, kStDuplicate);
-        CK(launch_pair_base(ctx, n));
-    }
+// Per-tile sort of the slabs for lists up to `cap` entries (the template is chosen from it). The
+// records already carry their first pair slot (the preprocess runs the pair-offset scan fused).
+int32_t slab_sort(tgsx_ctx* ctx, int tiles, uint64_t cap) {
     {
         StageTimer t(ctx, kStSort);
         CK(launch_seg_sort(ctx, ctx->ws.tile_slab.as<uint32_t>(), tiles, (int64_t)cap));
@@ -359,7 +356,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
         if (!ctx->bin_event) CK(cudaEventCreateWithFlags(&ctx->bin_event, cudaEventDisableTiming));
         CK(cudaEventRecord(ctx->bin_event, ctx->stream));
         const uint64_t guess = std::min<uint64_t>(kSegCap, ctx->bin_max_hint + ctx->bin_max_hint / 4);
-        int32_t rc = slab_sort(ctx, m->n, tiles, guess);
+        int32_t rc = slab_sort(ctx, tiles, guess);
         if (rc) return rc;
         ctx->bin_pending = true;
         *items = ws.tile_slab.as<uint32_t>();
@@ -379,7 +376,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
     if (max_list <= (uint64_t)kSegCap && !force_onesweep(ctx)) {
         // slab binning: every tile's list was claimed by preprocess into its slab; sort each slab
         // back into blend order (one warp per tile)
-        rc = slab_sort(ctx, m->n, tiles, max_list);
+        rc = slab_sort(ctx, tiles, max_list);
         if (rc) return rc;
         *items = ws.tile_slab.as<uint32_t>();
         if (sorted_keys) *sorted_keys = nullptr;
@@ -411,7 +408,7 @@ int32_t bin_settle(tgsx_ctx* ctx, tgsx_model* m, int W, int H, uint32_t** items,
     if (max_list <= (uint64_t)ctx->bin_sort_cap) return TGSX_OK;
     *redo = true;
     if (max_list <= (uint64_t)kSegCap) {
-        rc = slab_sort(ctx, m->n, ws.tiles_x * ws.tiles_y, max_list);
+        rc = slab_sort(ctx, ws.tiles_x * ws.tiles_y, max_list);
         if (rc) return rc;
         *items = ws.tile_slab.as<uint32_t>();
     } else {
@@ -828,7 +825,7 @@ int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, in
     CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
     ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
     if (max_list <= (uint64_t)kSegCap && !force_onesweep(ctx)) {
-        rc = slab_sort(ctx, n, tiles, max_list);
+        rc = slab_sort(ctx, tiles, max_list);
         if (rc) return rc;
         *items = ws.tile_slab.as<uint32_t>();
         return TGSX_OK;

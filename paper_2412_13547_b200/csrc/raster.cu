@@ -192,13 +192,6 @@ __global__ void slab_finalize_kernel(const uint32_t* __restrict__ fill, int tile
     if ((threadIdx.x & 31) == 0 && c) atomicMax(max_cnt, (unsigned long long)c);
 }
 
-// first partial slot of each splat (rank-major pair order) into its prepared record
-__global__ void pair_base_kernel(Prepared* __restrict__ prep, const uint32_t* __restrict__ pair_off,
-                                 int64_t n) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) prep[r].d.z = pair_off[r];
-}
-
 // Bitonic sort of 32*E keys held by one warp, lane L owning positions L*E .. L*E+E-1:
 // partners closer than E are in-register compare-exchanges, farther ones one shuffle.
 template <int E>
@@ -274,15 +267,6 @@ cudaError_t launch_slab_finalize(tgsx_ctx* ctx, int tiles) {
     if (tiles == 0) return cudaSuccess;
     slab_finalize_kernel<<<grid_for(tiles, 256), 256, 0, ctx->stream>>>(
         ws.tile_fill.as<uint32_t>(), tiles, ws.ranges.as<uint2>(), ws.counters.as<unsigned long long>() + 5);
-    ctx->launches++;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_pair_base(tgsx_ctx* ctx, int64_t n) {
-    Workspace& ws = ctx->ws;
-    if (n == 0) return cudaSuccess;
-    pair_base_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(ws.prep.as<Prepared>(),
-                                                                ws.pair_off.as<uint32_t>(), n);
     ctx->launches++;
     return cudaGetLastError();
 }

@@ -412,16 +412,6 @@ __device__ __forceinline__ void adam3d_math(float& th, float& m, float& v, float
     if (clamp) th = th < -c.raw_cap ? -c.raw_cap : (c.raw_cap < th ? c.raw_cap : th);
 }
 
-__device__ __forceinline__ void adam3d_one(float* __restrict__ params, float* __restrict__ m1,
-                                           float* __restrict__ m2, int64_t o, float g, float lr,
-                                           bool clamp, const Adam3dCfg& c) {
-    float th = params[o], m = m1[o], v = m2[o];
-    adam3d_math(th, m, v, g, lr, clamp, c);
-    m1[o] = m;
-    m2[o] = v;
-    params[o] = th;
-}
-
 // Adam over components K0 .. K0+NK-1 of row i: all 3*NK loads issued before any store (the
 // streams are independent; the restrict pointers let the loads run ahead).
 template <int K0, int NK, typename GradFn>

@@ -205,7 +205,6 @@ cudaError_t launch_ranges(tgsx_ctx* ctx, const uint32_t* keys, int64_t K, int ti
 // per-tile warp register sort (lists up to kSegCap; longer lists take the onesweep path)
 constexpr int kSegCap = 1024;
 cudaError_t launch_slab_finalize(tgsx_ctx* ctx, int tiles);
-cudaError_t launch_pair_base(tgsx_ctx* ctx, int64_t n);
 cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles, int64_t max_list);
 cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
                            bool fused_loss);
