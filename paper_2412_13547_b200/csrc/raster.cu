@@ -21,6 +21,28 @@ namespace {
 constexpr int kFillStride = 32;
 
 // ------------------------------------------------------------------ preprocess
+// Slab binning: claim a slot in every tile of the record's rectangle (d = packed rect, tiles):
+// kSegCap entries per tile, arbitrary order inside a tile (the per-tile sort restores blend
+// order). Four claims in flight per step: the returning atomics' latency dominates.
+__device__ __forceinline__ void claim_slots(const uint4& d, int tiles_x, uint32_t v, uint32_t* __restrict__ fill,
+                                            uint32_t* __restrict__ slab) {
+    const int tx0 = d.x & 0xffff, tx1 = d.x >> 16, ty0 = d.y & 0xffff;
+    const int w = tx1 - tx0 + 1, cnt = (int)d.w;
+    for (int q0 = 0; q0 < cnt; q0 += 4) {
+        uint32_t pos[4], tt[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (q0 + u < cnt) {
+                const int q = q0 + u;
+                tt[u] = (uint32_t)((ty0 + q / w) * tiles_x + tx0 + q % w);
+                pos[u] = atomicAdd(&fill[(size_t)tt[u] * kFillStride], 1u);
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (q0 + u < cnt && pos[u] < (uint32_t)kSegCap) slab[(size_t)tt[u] * kSegCap + pos[u]] = v;
+    }
+}
+
 // One Gaussian (row i, blend rank `rank`): the prepared record, the number of tiles it touches
 // and (slab binning) its slot claims. Returns the tile count; 0 on an error (raised in err).
 __device__ __forceinline__ uint32_t prepare_one(const float* __restrict__ params, int64_t cap, int64_t i,
@@ -64,26 +86,7 @@ __device__ __forceinline__ uint32_t prepare_one(const float* __restrict__ params
         tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
         o.d = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16),
                          0u, tiles);
-        if (fill) {
-            // slab binning: claim a slot in every touched tile's slab (kSegCap entries per tile,
-            // arbitrary order inside a tile; the per-tile sort restores blend order). Four claims
-            // in flight per step: the returning atomics' latency dominates.
-            const int w = tx1 - tx0 + 1, cnt = (int)tiles;
-            for (int q0 = 0; q0 < cnt; q0 += 4) {
-                uint32_t pos[4], tt[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (q0 + u < cnt) {
-                        const int q = q0 + u;
-                        tt[u] = (uint32_t)((ty0 + q / w) * tiles_x + tx0 + q % w);
-                        pos[u] = atomicAdd(&fill[(size_t)tt[u] * kFillStride], 1u);
-                    }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (q0 + u < cnt && pos[u] < (uint32_t)kSegCap)
-                        slab[(size_t)tt[u] * kSegCap + pos[u]] = rank;
-            }
-        }
+        if (fill) claim_slots(o.d, tiles_x, rank, fill, slab);
     }
     return tiles;
 }
@@ -122,13 +125,15 @@ __global__ void __launch_bounds__(256) preprocess_scan_kernel(
     const int64_t i = (int64_t)bid * 256 + threadIdx.x;
     Prepared o;
     uint32_t tiles = 0;
-    if (i < n) tiles = prepare_one(params, cap, i, (uint32_t)i, perm[i], lowpass_p, W, H, tiles_x, o, fill, slab, err);
+    // the slot claims come after the scan: the block barrier never waits on their atomics
+    if (i < n) tiles = prepare_one(params, cap, i, (uint32_t)i, perm[i], lowpass_p, W, H, tiles_x, o, nullptr, slab, err);
     const uint32_t excl = block_scan_lookback(tiles, bid, n, status, d_total);
     if (i < n) {
         o.d.z = excl;
         prep[i] = o;
         touched[i] = tiles;
         pair_off[i] = excl;
+        if (tiles) claim_slots(o.d, tiles_x, (uint32_t)i, fill, slab);
     }
 }
 

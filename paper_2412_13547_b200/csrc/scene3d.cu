@@ -217,9 +217,8 @@ __device__ __forceinline__ bool prepare3d_one(const float* __restrict__ params, 
     return true;
 }
 
-// Slab claims of one visible record (the 2-D preprocess's claim loop), slot value `v`.
-__device__ __forceinline__ uint32_t claim3d(Prepared& o, int W, int H, int tiles_x, uint32_t v,
-                                            uint32_t* __restrict__ fill, uint32_t* __restrict__ slab) {
+// Tile rectangle of a visible record into o.d (rect packed, tiles); returns the tile count.
+__device__ __forceinline__ uint32_t rect3d(Prepared& o, int W, int H) {
     int tx0, tx1, ty0, ty1;
     if (!tile_rect(o.a.x, o.a.y, o.b.z, o.b.w, W, H, tx0, tx1, ty0, ty1)) {
         o.d = make_uint4(0u, 0u, 0u, 0u);
@@ -227,7 +226,14 @@ __device__ __forceinline__ uint32_t claim3d(Prepared& o, int W, int H, int tiles
     }
     const uint32_t tiles = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
     o.d = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16), 0u, tiles);
-    const int w = tx1 - tx0 + 1, cnt = (int)tiles;
+    return tiles;
+}
+
+// Slab claims of one record (the 2-D preprocess's claim loop), slot value `v`.
+__device__ __forceinline__ void claim3d(const uint4& d, int tiles_x, uint32_t v, uint32_t* __restrict__ fill,
+                                        uint32_t* __restrict__ slab) {
+    const int tx0 = d.x & 0xffff, tx1 = d.x >> 16, ty0 = d.y & 0xffff;
+    const int w = tx1 - tx0 + 1, cnt = (int)d.w;
     for (int q0 = 0; q0 < cnt; q0 += 4) {
         uint32_t pos[4], tt[4];
 #pragma unroll
@@ -241,7 +247,6 @@ __device__ __forceinline__ uint32_t claim3d(Prepared& o, int W, int H, int tiles
         for (int u = 0; u < 4; ++u)
             if (q0 + u < cnt && pos[u] < (uint32_t)kSegCap) slab[(size_t)tt[u] * kSegCap + pos[u]] = v;
     }
-    return tiles;
 }
 
 // Global-sort path: records in row order + (depth key, row) pairs for the blend sort.
@@ -277,7 +282,7 @@ __global__ void __launch_bounds__(256, 3) preprocess3d_bin_kernel(
     bool live = false;
     if (i < n) {
         live = prepare3d_one(params, cap, i, cam, bump, o, key, err);
-        if (live) tiles = claim3d(o, W, H, tiles_x, (uint32_t)i, fill, slab);
+        if (live) tiles = rect3d(o, W, H);
     }
     const uint32_t excl = block_scan_lookback(tiles, bid, n, status, d_total);
     if (i < n) {
@@ -287,6 +292,8 @@ __global__ void __launch_bounds__(256, 3) preprocess3d_bin_kernel(
         keys[i] = key;
         touched[i] = tiles;
         pair_off[i] = excl;
+        // claims after the scan: the block barrier never waits on their atomics
+        if (tiles) claim3d(o.d, tiles_x, (uint32_t)i, fill, slab);
     }
 }
 
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(256) bin3d_kernel(
         rank_of[row] = (uint32_t)r;
         if (live) o = prep_row[row];
     }
-    if (live) tiles = claim3d(o, W, H, tiles_x, (uint32_t)r, fill, slab);
+    if (live) tiles = rect3d(o, W, H);
     const uint32_t excl = block_scan_lookback(tiles, bid, n, status, d_total);
     if (r < n) {
         o.d.z = excl;
@@ -393,6 +400,7 @@ __global__ void __launch_bounds__(256) bin3d_kernel(
         else prep[r].d = o.d;
         touched[r] = tiles;
         pair_off[r] = excl;
+        if (tiles) claim3d(o.d, tiles_x, (uint32_t)r, fill, slab);
     }
 }
 
