@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .api import Context, DilationPattern, GradientSet, RenderOptions, RenderOutput, default_context
+from .api import Context, DilationPattern, RenderOptions, RenderOutput, default_context
 
 N_PARAMS = 59
 ROW_MEAN, ROW_QUAT, ROW_LOGSCALE, ROW_OPACITY, ROW_SH = 0, 3, 7, 10, 11
@@ -267,4 +267,4 @@ class DeviceModel3D:
         return out
 
 
-__all__ = ["Camera", "GaussianModel3D", "DeviceModel3D", "N_PARAMS", "SH_C0", "GradientSet"]
+__all__ = ["Camera", "GaussianModel3D", "DeviceModel3D", "N_PARAMS", "SH_C0"]
