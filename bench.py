@@ -428,7 +428,8 @@ def run_tgsx(args, cfg):
         h_target = target.cpu().pin_memory()
         h_loss = torch.zeros(1).pin_memory()
         e2e_fn = lambda it: one_step(it, C.c_void_p(h_target.data_ptr()), C.c_void_p(h_loss.data_ptr()))  # noqa: E731
-        e2e_bytes = (W * H * 12, 4)
+        # a dilated view stages only its active rows of the host target (1/p of the image)
+        e2e_bytes = (W * ((H + p - 1) // p) * 12, 4)
         units = world  # views per step over all ranks
     elif args.config == "c4":
         n_targets = 200
@@ -480,7 +481,7 @@ def run_tgsx(args, cfg):
         h_ptrs = [t.data_ptr() for t in h_targets]
         step_fn = lambda it: batched_step(it, d_ptrs, loss_dev.data_ptr(), 4)  # noqa: E731
         e2e_fn = lambda it: batched_step(it, h_ptrs, h_loss.data_ptr(), 4)  # noqa: E731
-        e2e_bytes = (W * H * 12 * len(mine), 4 * len(mine))
+        e2e_bytes = (W * ((H + p - 1) // p) * 12 * len(mine), 4 * len(mine))
         units = 1  # one batched step = one fit iteration of the whole job (strong scaling)
 
     # The fit changes the model (and so the per-step work) every iteration: each timed phase

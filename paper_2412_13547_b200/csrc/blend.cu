@@ -56,6 +56,7 @@ struct BlendParams {
     uint32_t* last;
     unsigned long long* counters;  // [1] blend ops, [2] evaluations
     const float* target;           // fused L1 (forward)
+    int target_rows;               // > 1: target holds only the active rows (dilated host targets)
     float* dLdC;
     float* block_loss;
     float loss_scale;
@@ -268,7 +269,8 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_pairs_kernel(BlendPara
         prm.last[r] = last;
         ev += done ? last : (uint32_t)count;
         if (prm.target) {
-            const float* tg = prm.target + 3 * ((int64_t)y * prm.W + x);
+            const int ty = prm.target_rows > 1 ? (y - prm.oy) / prm.target_rows : y;  // staged rows only
+            const float* tg = prm.target + 3 * ((int64_t)ty * prm.W + x);
             const float d0 = c0 - tg[0], d1 = c1 - tg[1], d2 = c2 - tg[2];
             lsum += fabsf(d0) + fabsf(d1) + fabsf(d2);
             const float sc = prm.loss_scale;
@@ -758,6 +760,7 @@ cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* 
     BlendParams prm = make_params(ctx, ra, items);
     if (fused_loss) {
         prm.target = ra.target;
+        prm.target_rows = ra.target_rows;
         prm.loss_scale = ra.P > 0 ? (float)((double)ra.l1_weight / (3.0 * (double)ra.P)) : 0.f;
     } else {
         prm.target = nullptr;

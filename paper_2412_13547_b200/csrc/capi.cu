@@ -596,11 +596,18 @@ bool is_pinned_host_ptr(const void* p) {
 // filled on the copy stream, so the H2D of this view overlaps the previous view's kernels (the
 // compute stream waits for the copy; the next copy into a buffer waits for the forward that
 // read it, see mark_target_consumed).
-int32_t stage_target(tgsx_ctx* ctx, const float* src, size_t bytes, const float** out) {
+// Host targets of a dilated view (p > 1) only stage the active rows y = oy, oy + p, ... (the fused
+// L1 reads nothing else): a pitched copy of 1/p of the image, indexed by the kernel as row
+// (y - oy) / p (ra->target_rows = p). Device targets are used in place (full image).
+int32_t stage_target(tgsx_ctx* ctx, const float* src, size_t bytes, const float** out,
+                     RenderArgs* ra = nullptr) {
     if (is_device_ptr(src)) {
         *out = src;
         return TGSX_OK;
     }
+    const bool rows_only = ra && ra->p > 1 && ra->rows > 0;
+    const size_t row_bytes = ra ? (size_t)ra->W * 12 : 0;
+    if (rows_only) bytes = row_bytes * (size_t)ra->rows;
     if (!ctx->copy_stream) {
         CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         for (int i = 0; i < 2; ++i) {
@@ -617,7 +624,13 @@ int32_t stage_target(tgsx_ctx* ctx, const float* src, size_t bytes, const float*
         CK(b.ensure(bytes));
     }
     if (ctx->stage_used[k]) CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->consumed[k], 0));
-    CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+    if (rows_only) {
+        CK(cudaMemcpy2DAsync(b.p, row_bytes, src + (size_t)ra->oy * ra->W * 3, row_bytes * (size_t)ra->p,
+                             row_bytes, (size_t)ra->rows, cudaMemcpyHostToDevice, ctx->copy_stream));
+        ra->target_rows = ra->p;
+    } else {
+        CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->copy_stream));
+    }
     CK(cudaEventRecord(ctx->staged[k], ctx->copy_stream));
     CK(cudaStreamWaitEvent(ctx->stream, ctx->staged[k], 0));
     ctx->stage_pending = k;
@@ -668,7 +681,7 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
     const float lam = (pat->p == 1 && ctx->ssim_weight > 0.f) ? ctx->ssim_weight : 0.f;
     ra.l1_weight = 1.0f - lam;
     Workspace& ws = ctx->ws;
-    rc = stage_target(ctx, target, (size_t)ra.W * ra.H * 12, &ra.target);
+    rc = stage_target(ctx, target, (size_t)ra.W * ra.H * 12, &ra.target, &ra);
     if (rc) return rc;
     uint32_t* items = nullptr;
     rc = render_core(ctx, m, ra, true, &items, true);  // forward + fused (1 - lam) L1
@@ -1613,7 +1626,7 @@ static int32_t fused_view3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* c
     const float lam = (pat->p == 1 && ctx->ssim_weight > 0.f) ? ctx->ssim_weight : 0.f;
     ra.l1_weight = 1.0f - lam;
     Workspace& ws = ctx->ws;
-    if ((rc = stage_target(ctx, target, (size_t)ra.W * ra.H * 12, &ra.target))) return rc;
+    if ((rc = stage_target(ctx, target, (size_t)ra.W * ra.H * 12, &ra.target, &ra))) return rc;
     uint32_t* items = nullptr;
     if ((rc = render3d_core(ctx, m, c3, ra, true, &items))) return rc;
     int nsb = 0;

@@ -187,6 +187,7 @@ struct RenderArgs {
     int lowpass_p;
     const float* target;  // fused L1 target (device, W*H*3) or null
     float l1_weight;      // weight of the L1 term (1 - lambda_ssim on dense SSIM iterations)
+    int target_rows = 1;  // > 1: the target holds only the active rows (row (y - oy) / p)
 };
 
 cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m);

@@ -277,3 +277,25 @@ def test_fullsize_c3_fit_step_runs(P, ctx):
         ox, oy = P.next_offsets(2, it)
         losses.append(dm.fit_step(P.DilationPattern(2, ox, oy, W, H), (0, 0, 0), target, it + 1, 1000, diag))
     assert all(np.isfinite(losses)) and np.mean(losses[4:]) < np.mean(losses[:4])
+
+
+@pytest.mark.parametrize("p,ox,oy", [(2, 1, 1), (3, 2, 2), (3, 0, 1)])
+def test_dilated_host_target_stages_active_rows(P, ctx, p, ox, oy):
+    """A host target of a dilated view is staged as its active rows only (1/p of the image over
+    PCIe); the fused step must equal the same step with the full device-resident target, bit for
+    bit (odd heights: the last active row)."""
+    import torch
+    W, H, n = 70, 53, 800
+    s = B.synthetic_scene(3, n, W, H).ensure_stats()
+    target = target_image(4, n, W, H)
+    pat = P.DilationPattern(p, ox, oy, W, H)
+    diag = math.hypot(W, H)
+    a = P.DeviceModel.from_host(model_from_scene(s), ctx)
+    b = P.DeviceModel.from_host(model_from_scene(s), ctx)
+    la = a.fit_step(pat, (0, 0, 0), np.ascontiguousarray(target), 1, 100, diag)   # host: rows only
+    dev = torch.from_numpy(np.ascontiguousarray(target)).cuda()
+    torch.cuda.synchronize()
+    lb = b.fit_step(pat, (0, 0, 0), dev.data_ptr(), 1, 100, diag)                # device: full image
+    assert la == lb
+    ha, hb = a.download(), b.download()
+    assert np.array_equal(ha.params.view(np.uint32), hb.params.view(np.uint32))
