@@ -520,6 +520,18 @@ def run_tgsx(args, cfg):
         ctx.synchronize()
         e2e_ms = timer.run(e2e_fn, args.steps, args.warmup, ctx)
     fp32_meas = measure_fp32_peak(ctx)  # after the timed regions
+    consistent = None
+    if world > 1:
+        # every rank must hold bit-identical parameters after the all-reduced
+        # steps (identical Adam / densify decisions): compare a hash of the downloaded model
+        import hashlib
+        h = dm.download()
+        arr = h.params if hasattr(h, "params") else None
+        digest = hashlib.sha256(np.ascontiguousarray(arr).tobytes()).digest()[:8]
+        mine = torch.tensor([int.from_bytes(digest, "little", signed=True)], dtype=torch.int64, device="cuda")
+        allh = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allh, mine)
+        consistent = len({int(t.item()) for t in allh}) == 1
     if rank != 0:
         dist.barrier()
         dist.destroy_process_group()
@@ -547,6 +559,8 @@ def run_tgsx(args, cfg):
                        "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1]}
     else:
         line["e2e"] = {"value": None, "unit": "iters/s", "note": "fit loop runs device-resident targets"}
+    if consistent is not None:
+        line["ranks_bit_identical"] = consistent  # model hash equal on every rank after the run
     if args.config == "c4":
         reps = extra["reports"]
         line["fit_loop"] = {"iterations": [reps[0].iteration, reps[-1].iteration],
