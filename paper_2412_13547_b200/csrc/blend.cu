@@ -770,7 +770,7 @@ cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* 
     if (ra.p == 1) {
         forward_pairs_kernel<2, 2, 256><<<tiles, 128, 0, ctx->stream>>>(prm);
     } else {
-        forward_pairs_kernel<1, 1, 128><<<tiles, 32, 0, ctx->stream>>>(prm);
+        forward_pairs_kernel<1, 1, 32><<<tiles, 32, 0, ctx->stream>>>(prm);
     }
     ctx->launches++;
     return cudaGetLastError();
