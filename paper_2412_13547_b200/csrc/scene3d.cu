@@ -668,18 +668,18 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
 }
 
 // Adam over one group of components of every Gaussian (grid.y = group, kAdamGroups groups):
-// group 0 = rows 0..5 (mean, quaternion w x y), group 1 = rows 6..10 (quaternion z, log-scales,
-// opacity), group 2 + j = SH functions 2j, 2j+1, all three channels (rows 11 + 6j ..). <= 6
-// components per thread: small register footprint, full occupancy for the streams.
-constexpr int kAdamGroups = 10;
+// groups 0..3 = rows 0-2, 3-5, 6-8, 9-10 (mean, quaternion, log-scales, opacity); group 4 + k = SH
+// function k, all three channels (rows 11 + 3k ..). <= 3 components per thread: small register
+// footprint, full occupancy for the streams.
+constexpr int kAdamGroups = 20;
 
 template <int G>
 __device__ __forceinline__ void adam3d_group_apply(float* __restrict__ P, float* __restrict__ M1,
                                                    float* __restrict__ M2, int64_t cap, int64_t n,
                                                    int64_t i, const float* __restrict__ GB,
                                                    const Adam3dCfg& c) {
-    if (G < 2) {
-        constexpr int K0 = G == 0 ? 0 : 6, NK = G == 0 ? 6 : 5;
+    if (G < 4) {
+        constexpr int K0 = 3 * G, NK = G == 3 ? 2 : 3;
         float gg[NK];
 #pragma unroll
         for (int k = 0; k < NK; ++k) gg[k] = GB[(int64_t)(K0 + k) * n + i];
@@ -692,13 +692,13 @@ __device__ __forceinline__ void adam3d_group_apply(float* __restrict__ P, float*
             d[k] = GB[(int64_t)(14 + k) * n + i];
         }
         sh_basis(d[0], d[1], d[2], b);
-        constexpr int K0 = 11 + 6 * (G - 2);
-        adam3d_chunk<K0, 6>(P, M1, M2, cap, i,
+        constexpr int K0 = 11 + 3 * (G - 4);
+        adam3d_chunk<K0, 3>(P, M1, M2, cap, i,
                             [&](int k) { return fmul(b[(k - 11) / 3], dcol[(k - 11) % 3]); }, c);
     }
 }
 
-__global__ void __launch_bounds__(256, 3) adam3d_apply_kernel(float* __restrict__ P, float* __restrict__ M1,
+__global__ void __launch_bounds__(256) adam3d_apply_kernel(float* __restrict__ P, float* __restrict__ M1,
                                                            float* __restrict__ M2, int64_t cap, int64_t n,
                                                            const float* __restrict__ GB, Adam3dCfg c) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -713,7 +713,17 @@ __global__ void __launch_bounds__(256, 3) adam3d_apply_kernel(float* __restrict_
         case 6: adam3d_group_apply<6>(P, M1, M2, cap, n, i, GB, c); break;
         case 7: adam3d_group_apply<7>(P, M1, M2, cap, n, i, GB, c); break;
         case 8: adam3d_group_apply<8>(P, M1, M2, cap, n, i, GB, c); break;
-        default: adam3d_group_apply<9>(P, M1, M2, cap, n, i, GB, c); break;
+        case 9: adam3d_group_apply<9>(P, M1, M2, cap, n, i, GB, c); break;
+        case 10: adam3d_group_apply<10>(P, M1, M2, cap, n, i, GB, c); break;
+        case 11: adam3d_group_apply<11>(P, M1, M2, cap, n, i, GB, c); break;
+        case 12: adam3d_group_apply<12>(P, M1, M2, cap, n, i, GB, c); break;
+        case 13: adam3d_group_apply<13>(P, M1, M2, cap, n, i, GB, c); break;
+        case 14: adam3d_group_apply<14>(P, M1, M2, cap, n, i, GB, c); break;
+        case 15: adam3d_group_apply<15>(P, M1, M2, cap, n, i, GB, c); break;
+        case 16: adam3d_group_apply<16>(P, M1, M2, cap, n, i, GB, c); break;
+        case 17: adam3d_group_apply<17>(P, M1, M2, cap, n, i, GB, c); break;
+        case 18: adam3d_group_apply<18>(P, M1, M2, cap, n, i, GB, c); break;
+        default: adam3d_group_apply<19>(P, M1, M2, cap, n, i, GB, c); break;
     }
 }
 
@@ -785,7 +795,7 @@ inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / b
 
 cudaError_t launch_adam3d_step(tgsx_ctx* ctx, tgsx_model3d* m, int batch_views, const Adam3dCfg& cfg) {
     if (m->n == 0) return cudaSuccess;
-    adam3d_step_kernel<<<dim3(grid_for(m->n, 256), kAdamGroups), 256, 0, ctx->stream>>>(
+    adam3d_step_kernel<<<dim3(grid_for(m->n, 256), 10), 256, 0, ctx->stream>>>(
         m->params.as<float>(), m->m1.as<float>(), m->m2.as<float>(), m->cap, m->n, m->step.as<float>(),
         (float)(batch_views > 0 ? batch_views : 1), m->pos_acc.as<float>(), m->col_acc.as<float>(),
         m->visit.as<int32_t>(), cfg);
@@ -795,7 +805,7 @@ cudaError_t launch_adam3d_step(tgsx_ctx* ctx, tgsx_model3d* m, int batch_views, 
 
 cudaError_t launch_adam3d(tgsx_ctx* ctx, tgsx_model3d* m, const float* grads, const Adam3dCfg& cfg) {
     if (m->n == 0) return cudaSuccess;
-    adam3d_kernel<<<dim3(grid_for(m->n, 256), kAdamGroups), 256, 0, ctx->stream>>>(m->params.as<float>(), m->m1.as<float>(),
+    adam3d_kernel<<<dim3(grid_for(m->n, 256), 10), 256, 0, ctx->stream>>>(m->params.as<float>(), m->m1.as<float>(),
                                                                 m->m2.as<float>(), m->cap, m->n, grads, cfg);
     ctx->launches++;
     return cudaGetLastError();
