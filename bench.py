@@ -154,19 +154,57 @@ def _ref_setup(cfg):
     W, H, n = cfg["W"], cfg["H"], cfg["n"]
     impl = "ref_native" if B.ref_available() else "oracle"
     B.set_math(False)
-    s = B.synthetic_scene(1, n, W, H)
+    s = B.synthetic_scene(1, n, W, H).ensure_stats()
     t = B.synthetic_scene(2, n, W, H)
     target, _, _, _ = B.render(t, 1, 0, 0, W, H, impl=impl, threads=threads)
     return B, impl, threads, s, target.reshape(H, W, 3)
 
 
-def _ref_step(B, impl, threads, s, target, m1, m2, cfg, it):
-    W, H, p = cfg["W"], cfg["H"], cfg["p"]
-    ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
-    rgb, _, _, _ = B.render(s, p, ox, oy, W, H, impl=impl, threads=threads)
-    _, dl = B.l1_loss(rgb, p, ox, oy, W, H, target)
-    g, _ = B.backward(s, p, ox, oy, W, H, dl, impl=impl, threads=threads)
-    B.adam_step(s, g, m1, m2, B.adam_config(it + 1, 10000, math.hypot(W, H)))
+class RefArm:
+    """The reference CPU fit iteration: ONE persistent reference GaussianModel (oracle/_ref,
+    B.RefSession) rendered and back-propagated by the unmodified tgs::render / tgs::backward on
+    all host threads, the restated L1 and Adam (oracle) on its parameters, written back in place.
+    The blend order stays cached across iterations as in the reference (model.hpp:105-119); its
+    one-off sort is timed separately (`first_call_sort_s`)."""
+
+    def __init__(self, cfg):
+        self.cfg = cfg
+        self.B, self.impl, self.threads, self.s, self.target = _ref_setup(cfg)
+        n = self.s.n
+        self.m1 = np.zeros((9, n), np.float32)
+        self.m2 = np.zeros((9, n), np.float32)
+        self.sess = None
+        self.sort_s = None
+        if self.impl != "oracle":
+            self.sess = self.B.RefSession(self.s, self.impl)
+            t0 = time.perf_counter()
+            self.sess.sort()
+            self.sort_s = time.perf_counter() - t0
+
+    def step(self, it):
+        B, cfg = self.B, self.cfg
+        W, H, p = cfg["W"], cfg["H"], cfg["p"]
+        ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
+        if self.sess is not None:
+            rgb, _, _ = self.sess.render(p, ox, oy, W, H, threads=self.threads)
+            _, dl = B.l1_loss(rgb, p, ox, oy, W, H, self.target)
+            g = self.sess.backward(p, ox, oy, W, H, dl, threads=self.threads)
+        else:
+            rgb, _, _, _ = B.render(self.s, p, ox, oy, W, H, impl=self.impl, threads=self.threads)
+            _, dl = B.l1_loss(rgb, p, ox, oy, W, H, self.target)
+            g, _ = B.backward(self.s, p, ox, oy, W, H, dl, impl=self.impl, threads=self.threads)
+        B.adam_step(self.s, g, self.m1, self.m2, B.adam_config(it + 1, 10000, math.hypot(W, H)))
+        if self.sess is not None:
+            self.sess.push()
+
+    @property
+    def kind(self):
+        return "reference" if self.impl != "oracle" else "port"
+
+    def describe(self, what):
+        d = (f"{what} on {self.threads} host threads: one persistent reference GaussianModel "
+             "(oracle/_ref render+backward, cached blend order) + restated L1 and Adam")
+        return d if self.impl != "oracle" else what + " (oracle C restatement, single thread)"
 
 
 def run_reference(args, cfg):
@@ -177,49 +215,43 @@ def run_reference(args, cfg):
         print(json.dumps({"impl": "reference", "unavailable": "the reference is a 2-D analog of 3DGS: "
                           "it has no 3-D front end (SURVEY.md §0)"}), flush=True)
         return
-    B, impl, threads, s, target = _ref_setup(cfg)
-    m1 = np.zeros((9, s.n), np.float32)
-    m2 = np.zeros((9, s.n), np.float32)
-    # one full iteration takes ~2 s (C2) on the host: bound the sample so the arm ends within a
-    # few minutes whatever --steps / --warmup the caller passes
+    arm = RefArm(cfg)
+    # one full iteration takes ~1-2 s (C2) on the host: bound the sample so the arm ends within
+    # a few minutes whatever --steps / --warmup the caller passes
     warm = min(args.warmup, 1)
     steps = max(1, min(args.steps, 10 if cfg["n"] <= 1_000_000 else 4))
     for i in range(warm):
-        _ref_step(B, impl, threads, s, target, m1, m2, cfg, i)
+        arm.step(i)
     t0 = time.perf_counter()
     for i in range(steps):
-        _ref_step(B, impl, threads, s, target, m1, m2, cfg, warm + i)
+        arm.step(warm + i)
     dt = time.perf_counter() - t0
     v = steps / dt
-    kind = "reference" if impl != "oracle" else "port"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s",
             "n_gpus": world, "steps": steps, "warmup": warm,
             "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["workload"], "gaussians": cfg["n"], "width": cfg["W"],
                        "height": cfg["H"], "p": cfg["p"]},
-            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": threads, "kind": kind,
-                             "sample": f"{steps} full fit iterations (after {warm} warm-up) on {threads} host threads "
-                                       "(reference render+backward from oracle/_ref, restated L1+Adam)"},
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": arm.threads, "kind": arm.kind,
+                             "sample": arm.describe(f"{steps} full fit iterations (after {warm} warm-up)"),
+                             "first_call_sort_s": arm.sort_s},
             "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_sample(cfg, iters=2):
     """Bounded CPU sample of the same workload (oracle/_ref, all host threads)."""
-    B, impl, threads, s, target = _ref_setup(cfg)
-    m1 = np.zeros((9, s.n), np.float32)
-    m2 = np.zeros((9, s.n), np.float32)
+    arm = RefArm(cfg)
     times = []
     for it in range(iters + 1):
         t0 = time.perf_counter()
-        _ref_step(B, impl, threads, s, target, m1, m2, cfg, it)
+        arm.step(it)
         times.append(time.perf_counter() - t0)
-    med = statistics.median(times[1:])  # the first iteration absorbs the blend-order sort
-    return {"value": 1.0 / med, "unit": "iters/s", "cores": threads,
-            "kind": "reference" if impl != "oracle" else "port",
-            "sample": f"median of {iters} full fit iterations after 1 warm-up, same config "
-                      "(reference render+backward from oracle/_ref, restated L1+Adam)"}
+    med = statistics.median(times[1:])
+    return {"value": 1.0 / med, "unit": "iters/s", "cores": arm.threads, "kind": arm.kind,
+            "sample": arm.describe(f"median of {iters} full fit iterations after 1 warm-up, same config"),
+            "first_call_sort_s": arm.sort_s}
 
 
 # ---------------------------------------------------------------------------- tgsx arm

@@ -385,6 +385,81 @@ def backward(s: Scene, p, ox, oy, W, H, dLdC, bg=(0, 0, 0), lowpass_p=0, impl="o
     return grads[:, :n], None
 
 
+class RefSession:
+    """One persistent tgs::GaussianModel<float> of the unmodified reference (oracle/_ref), kept
+    across fit iterations so its cached blend order (model.hpp:105-119) is reused the way the
+    reference's own trainer would reuse it; parameters are written in place between iterations.
+    Used by bench.py's reference arm. The scene `s` stays the SoA source of truth for the
+    restated optimizer (adam_step); push() copies its 9 parameters into the model."""
+
+    def __init__(self, s: Scene, impl="ref_native"):
+        self.h = None
+        self.L = ref_lib(impl.split("_", 1)[1])
+        L = self.L
+        L.ref_session_create_f32.restype = C.c_void_p
+        L.ref_session_create_f32.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
+        L.ref_session_destroy.argtypes = [C.c_void_p]
+        L.ref_session_sort.argtypes = [C.c_void_p]
+        L.ref_session_set_params_f32.argtypes = [C.c_void_p, C.c_void_p]
+        L.ref_session_render_f32.argtypes = [C.c_void_p] + [C.c_int] * 5 + [
+            C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p, C.c_int]
+        L.ref_session_backward_f32.argtypes = [C.c_void_p] + [C.c_int] * 5 + [
+            C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_char_p, C.c_int]
+        L.ref_session_visits.argtypes = [C.c_void_p, C.c_void_p]
+        self.s = s
+        keep: list = []
+        err = C.create_string_buffer(256)
+        self.h = L.ref_session_create_f32(C.byref(_ref_scene(s, np.float32, keep)), err, 256)
+        if not self.h:
+            raise OracleError(3, err.value.decode())
+
+    def close(self):
+        if self.h:
+            self.L.ref_session_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def sort(self):
+        self.L.ref_session_sort(self.h)
+
+    def push(self):
+        arrs = [np.ascontiguousarray(getattr(self.s, f), np.float32) for f in PARAM_FIELDS]
+        ptrs = (C.c_void_p * 9)(*[a.ctypes.data for a in arrs])
+        self.L.ref_session_set_params_f32(self.h, ptrs)
+
+    def render(self, p, ox, oy, W, H, bg=(0, 0, 0), threads=1):
+        Pn = active_count(p, ox, oy, W, H)
+        rgb = np.zeros((Pn, 3), np.float32)
+        T = np.zeros(Pn, np.float32)
+        ops = C.c_uint64(0)
+        bgv = np.asarray(bg, np.float32)
+        err = C.create_string_buffer(256)
+        rc = self.L.ref_session_render_f32(self.h, p, ox, oy, W, H, bgv.ctypes.data, threads,
+                                           rgb.ctypes.data, T.ctypes.data, C.byref(ops), err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return rgb, T, ops.value
+
+    def backward(self, p, ox, oy, W, H, dLdC, bg=(0, 0, 0), threads=1):
+        n = self.s.n
+        grads = np.zeros((9, max(n, 1)), np.float32)
+        gp = (C.c_void_p * 9)(*[grads[q].ctypes.data for q in range(9)])
+        dLdC = np.ascontiguousarray(dLdC, np.float32)
+        bgv = np.asarray(bg, np.float32)
+        err = C.create_string_buffer(256)
+        rc = self.L.ref_session_backward_f32(self.h, p, ox, oy, W, H, bgv.ctypes.data, dLdC.ctypes.data,
+                                             C.c_int64(dLdC.size // 3), threads, gp, err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return grads[:, :n]
+
+    def visits(self):
+        out = np.zeros(max(self.s.n, 1), np.int64)
+        self.L.ref_session_visits(self.h, out.ctypes.data)
+        return out[:self.s.n]
+
+
 PREP_FIELDS = ("mx", "my", "i00", "i01", "i11", "alpha", "c0", "c1", "c2", "rx", "ry")
 
 

@@ -238,6 +238,102 @@ int ref_sorted_order_f32(const RefSceneF32* s, uint32_t* out, char* err, int err
         err, errlen);
 }
 
+// ---------------------------------------------------------------- persistent model session
+// The reference arm of bench.py: ONE tgs::GaussianModel<float> kept across fit iterations, as
+// the reference's own trainer would hold it, so GaussianModel::sorted_order stays cached until a
+// structural change (model.hpp:105-119: add/compact set order_dirty_; parameter writes through
+// operator[] do not). Parameters are written in place between iterations (the optimizer step);
+// the DensifyStats accumulate inside the model across backward calls (rasterizer.cpp:350-358).
+struct RefSession {
+    tgs::GaussianModel<float> model;
+};
+
+void* ref_session_create_f32(const RefSceneF32* s, char* err, int errlen) {
+    RefSession* h = nullptr;
+    const int rc = guarded([&] { h = new RefSession{build_model(*s)}; }, err, errlen);
+    return rc ? nullptr : h;
+}
+
+void ref_session_destroy(void* h) { delete static_cast<RefSession*>(h); }
+
+// Forces the blend-order sort (the first-call cost the cached order amortises).
+int ref_session_sort(void* h) {
+    (void)static_cast<RefSession*>(h)->model.sorted_order();
+    return 0;
+}
+
+// Overwrites the 9 optimised parameters (pos x/y, rot, log-scale x/y, raw opacity, raw rgb) in
+// place, model index order; depth_key and id are untouched, so the cached order stays valid.
+int ref_session_set_params_f32(void* h, const float* const* f) {
+    auto& m = static_cast<RefSession*>(h)->model;
+    const size_t n = m.size();
+    for (size_t i = 0; i < n; ++i) {
+        auto& g = m[i];
+        g.position = {f[0][i], f[1][i]};
+        g.rotation = f[2][i];
+        g.log_scales = {f[3][i], f[4][i]};
+        g.raw_opacity = f[5][i];
+        g.color = {f[6][i], f[7][i], f[8][i]};
+    }
+    return 0;
+}
+
+int ref_session_render_f32(void* h, int p, int ox, int oy, int W, int H, const float* bg, int threads,
+                           float* out_rgb, float* out_T, uint64_t* out_ops, char* err, int errlen) {
+    auto& m = static_cast<RefSession*>(h)->model;
+    return guarded(
+        [&] {
+            tgs::DilationPattern pat(p, ox, oy, W, H);
+            tgs::RenderOptions opts;
+            opts.threads = threads;
+            auto out = tgs::render<float>(m, pat, tgs::Vec3<float>(bg[0], bg[1], bg[2]), opts);
+            for (size_t i = 0; i < out.colors.size(); ++i) {
+                out_rgb[3 * i + 0] = out.colors[i].x;
+                out_rgb[3 * i + 1] = out.colors[i].y;
+                out_rgb[3 * i + 2] = out.colors[i].z;
+                out_T[i] = out.final_transmittance[i];
+            }
+            *out_ops = out.blend_op_count;
+        },
+        err, errlen);
+}
+
+int ref_session_backward_f32(void* h, int p, int ox, int oy, int W, int H, const float* bg,
+                             const float* dLdC, int64_t dLdC_count, int threads, float* const* grads,
+                             char* err, int errlen) {
+    auto& m = static_cast<RefSession*>(h)->model;
+    return guarded(
+        [&] {
+            tgs::DilationPattern pat(p, ox, oy, W, H);
+            tgs::RenderOptions opts;
+            opts.threads = threads;
+            std::vector<tgs::Vec3<float>> g((size_t)dLdC_count);
+            for (size_t i = 0; i < g.size(); ++i)
+                g[i] = tgs::Vec3<float>(dLdC[3 * i], dLdC[3 * i + 1], dLdC[3 * i + 2]);
+            auto gs = tgs::backward<float>(m, pat, tgs::Vec3<float>(bg[0], bg[1], bg[2]), g, opts);
+            const size_t n = m.size();
+            for (size_t i = 0; i < n; ++i) {
+                grads[0][i] = gs.position[i].x;
+                grads[1][i] = gs.position[i].y;
+                grads[2][i] = gs.rotation[i];
+                grads[3][i] = gs.log_scales[i].x;
+                grads[4][i] = gs.log_scales[i].y;
+                grads[5][i] = gs.raw_opacity[i];
+                grads[6][i] = gs.color[i].x;
+                grads[7][i] = gs.color[i].y;
+                grads[8][i] = gs.color[i].z;
+            }
+        },
+        err, errlen);
+}
+
+// visit_count of the persistent model's DensifyStats (model index order)
+int ref_session_visits(void* h, int64_t* out) {
+    const auto& st = static_cast<RefSession*>(h)->model.stats();
+    for (size_t i = 0; i < st.visit_count.size(); ++i) out[i] = st.visit_count[i];
+    return 0;
+}
+
 // KdTree2<float>::knn (kdtree.hpp) of every point, excluding itself: out[i*k + j] = the j-th
 // nearest (ascending (dist2, index)); missing neighbours (n - 1 < k) are UINT32_MAX.
 int ref_knn_f32(const float* xy, int64_t n, int k, uint32_t* out, char* err, int errlen) {
