@@ -40,6 +40,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
+    "c1": dict(workload="C1: synthetic 10K Gaussians, 256x256, p=1 single-view fit step (fwd + L1 + bwd + "
+                        "densify stats + Adam; the reference's CPU-runnable case — the 2-D reference has "
+                        "no SH, SURVEY.md §8a A3b)", n=10_000, W=256, H=256, p=1),
     "c2": dict(workload="C2: synthetic 1M Gaussians, 1920x1080, p=1 single-view fit step "
                         "(fwd + L1 + bwd + densify stats + Adam)", n=1_000_000, W=1920, H=1080, p=1),
     "c3": dict(workload="C3: synthetic 3M Gaussians, 3840x2160, dilated p=2 (cycled offsets) "
@@ -256,26 +259,44 @@ def cpu_baseline_sample(cfg, iters=2):
 
 # ---------------------------------------------------------------------------- tgsx arm
 class Timer:
-    """CUDA events on the library stream around a timed region; max over ranks."""
+    """CUDA events on the library stream around a timed region; max over ranks. With `flush`
+    (a working set that would sit in the 126 MB L2) a 256 MB buffer is written before every step
+    and only the steps are timed (one event pair per step, summed)."""
 
     def __init__(self, torch, stream, dist):
         self.torch, self.stream, self.dist = torch, stream, dist
+        self.flush_buf = None
 
-    def run(self, fn, steps, base, ctx):
+    def run(self, fn, steps, base, ctx, flush=False):
         torch = self.torch
         if self.dist:
             self.dist.barrier()
         torch.cuda.synchronize()
         ctx.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(self.stream)
-        for i in range(steps):
-            fn(base + i)
-        e1.record(self.stream)
-        e1.synchronize()
-        ctx.synchronize()
-        ms = e0.elapsed_time(e1)
+        if flush:
+            if self.flush_buf is None:
+                self.flush_buf = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(steps)]
+            for i in range(steps):
+                with torch.cuda.stream(self.stream):
+                    self.flush_buf.fill_(float(i))
+                ev[i][0].record(self.stream)
+                fn(base + i)
+                ev[i][1].record(self.stream)
+            ev[-1][1].synchronize()
+            ctx.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in ev)
+        else:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+            for i in range(steps):
+                fn(base + i)
+            e1.record(self.stream)
+            e1.synchronize()
+            ctx.synchronize()
+            ms = e0.elapsed_time(e1)
         if self.dist:
             t = torch.tensor([ms], device="cuda")
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
@@ -339,7 +360,11 @@ def roofline(stages, counters, clocks, n, config, fp32_meas=None):
             "traffic": measured_traffic(config, dom), "ms_per_launch": dom_ms}
 
 
-def run_tgsx(args, cfg):
+def run_tgsx(args):
+    """All ranks: set up the process group, the context (+ the library NCCL communicator for
+    N > 1), measure the requested config; with the default config (C2) also the sub-records of
+    the metric's other halves — C1 (N = 1), C3 (4K dilated) and C5 (batched-view 4K) — nested in
+    the same JSON line. Rank 0 prints it."""
     import torch
     import paper_2412_13547_b200 as P
     from paper_2412_13547_b200 import dist as D
@@ -350,11 +375,40 @@ def run_tgsx(args, cfg):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    W, H, n, p = cfg["W"], cfg["H"], cfg["n"], cfg["p"]
-    diag = float(np.hypot(W, H))
     ctx = P.Context(local)
+    if world > 1:
+        # the per-Gaussian step buffer is summed by the library's own NCCL communicator
+        # (tgsx_comm_init; the torch process group only broadcasts its unique id)
+        D.init_library_comm(ctx, rank, world)
     if args.ssim > 0:
         ctx.set_ssim_weight(args.ssim)
+    env = {"torch": torch, "P": P, "D": D, "ctx": ctx, "dist": dist, "rank": rank, "world": world,
+           "local": local}
+    line = measure(args, args.config, env)
+    if args.config == "c2" and args.ssim == 0 and not args.no_subrecords:
+        subs = {}
+        for name in (["c1"] if world == 1 else []) + ["c3", "c5"]:
+            sub = measure(args, name, env)
+            if sub is not None:
+                sub.pop("metric", None)
+                subs[name] = sub
+        if line is not None:
+            line["subrecords"] = subs
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure(args, name, env):
+    """One config on every rank; returns rank 0's JSON record (None on the other ranks)."""
+    torch, P, D, ctx, dist = env["torch"], env["P"], env["D"], env["ctx"], env["dist"]
+    rank, world, local = env["rank"], env["world"], env["local"]
+    cfg = CONFIGS[name]
+    steps_override = None
+    W, H, n, p = cfg["W"], cfg["H"], cfg["n"], cfg["p"]
+    diag = float(np.hypot(W, H))
     stream = torch.cuda.ExternalStream(ctx.L.tgsx_get_stream(ctx.h))
     if not cfg.get("three_d"):
         host = P.GaussianModel.synthetic(1, n, W, H)
@@ -371,7 +425,7 @@ def run_tgsx(args, cfg):
         return (base + 0.02 * torch.randn(base.shape, generator=g, device="cuda")).contiguous()
 
     extra = {}
-    if cfg.get("three_d") and args.config == "c6":
+    if cfg.get("three_d") and name == "c6":
         from paper_2412_13547_b200 import scene3d as S3
         if world > 1:
             raise SystemExit("c6 (3-D front end) is single-view: run it with --gpus 1")
@@ -399,7 +453,7 @@ def run_tgsx(args, cfg):
         e2e_fn = lambda it: one_step(it, C.c_void_p(h_target.data_ptr()), C.c_void_p(h_loss.data_ptr()))  # noqa: E731
         e2e_bytes = (W * H * 12, 4)
         units = 1
-    elif args.config == "c7":
+    elif name == "c7":
         from paper_2412_13547_b200 import scene3d as S3
         views = cfg["views"]
         fx = 0.5 * W / math.tan(math.radians(30))
@@ -412,7 +466,6 @@ def run_tgsx(args, cfg):
         targets = [torch.from_numpy(tm3.render(c).colors.reshape(H, W, 3).copy()).cuda().contiguous() for c in cams]
         tm3.close()
         torch.cuda.synchronize()
-        sharded = D.ViewShardedFit(dm, rank, world)
         mine = D.views_for_rank(views, rank, world)
         camc = [c.c() for c in cams]
         pat = P.DilationPattern(1, 0, 0, W, H).c()
@@ -425,8 +478,7 @@ def run_tgsx(args, cfg):
                 ctx.check(ctx.L.tgsx_view_accumulate3d(ctx.h, dm.h, C.byref(camc[v]), C.byref(pat), bg,
                                                        C.c_void_p(tptrs[v]), C.c_void_p(lbase + 4 * v)))
             if world > 1:
-                with torch.cuda.stream(stream):
-                    dist.all_reduce(sharded._tensor())
+                ctx.check(ctx.L.tgsx_allreduce_step3d(ctx.h, dm.h))
             a = P._lib.Adam3dArgs(it + 1, 10000, 3.0)
             ctx.check(ctx.L.tgsx_apply_step3d(ctx.h, dm.h, views, C.byref(a)))
 
@@ -436,11 +488,10 @@ def run_tgsx(args, cfg):
         e2e_fn = lambda it: batched_step(it, h_ptrs, h_loss.data_ptr())  # noqa: E731
         e2e_bytes = (W * H * 12 * len(mine), 4 * len(mine))
         units = 1
-    elif args.config in ("c2", "c3"):
+    elif name in ("c1", "c2", "c3"):
         target = noisy(rank) if world > 1 else base.contiguous()
         loss_dev = torch.zeros(1, device="cuda")
         torch.cuda.synchronize()
-        sharded = D.ViewShardedFit(dm, rank, world)
 
         def one_step(it, tptr, lptr):
             ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
@@ -449,10 +500,10 @@ def run_tgsx(args, cfg):
             if world == 1:
                 ctx.check(ctx.L.tgsx_fit_step(ctx.h, dm.h, C.byref(pat), bg, tptr, C.byref(a), lptr))
             else:
-                ctx.check(ctx.L.tgsx_view_accumulate(ctx.h, dm.h, C.byref(pat), bg, tptr, lptr))
-                with torch.cuda.stream(stream):
-                    dist.all_reduce(sharded._tensor())
-                ctx.check(ctx.L.tgsx_apply_step(ctx.h, dm.h, world, C.byref(a)))
+                # one view per rank: chain -> NCCL all-reduce -> Adam pipelined over 4 buckets
+                tp = (C.c_void_p * 1)(tptr)
+                ctx.check(ctx.L.tgsx_batched_step(ctx.h, dm.h, 1, C.byref(pat), bg, tp, world, C.byref(a),
+                                                  lptr, args.buckets))
 
         tptr, lptr = C.c_void_p(target.data_ptr()), C.c_void_p(loss_dev.data_ptr())
         step_fn = lambda it: one_step(it, tptr, lptr)  # noqa: E731
@@ -463,7 +514,7 @@ def run_tgsx(args, cfg):
         # a dilated view stages only its active rows of the host target (1/p of the image)
         e2e_bytes = (W * ((H + p - 1) // p) * 12, 4)
         units = world  # views per step over all ranks
-    elif args.config == "c4":
+    elif name == "c4":
         n_targets = 200
         targets = [noisy(v) for v in range(n_targets)]
         torch.cuda.synchronize()
@@ -486,28 +537,25 @@ def run_tgsx(args, cfg):
         units = 1
         extra["trainer"] = trainer
         extra["reports"] = reports
-        args.steps = max(args.steps, 100)
-        args.warmup = max(args.warmup, tcfg.warmup_iters)
+        steps_override = (max(args.steps, 100), max(args.warmup, tcfg.warmup_iters))
     else:  # c5
         views = cfg["views"]
         targets = [noisy(v) for v in range(views)]
         torch.cuda.synchronize()
-        sharded = D.ViewShardedFit(dm, rank, world)
         mine = D.views_for_rank(views, rank, world)
         pats = [P.DilationPattern(p, (v % (p * p)) % p, (v % (p * p)) // p, W, H).c() for v in range(views)]
+        mpats = (P._lib.Pattern * max(len(mine), 1))(*[pats[v] for v in mine])
         loss_dev = torch.zeros(views, device="cuda")
         h_targets = [targets[v].cpu().pin_memory() for v in range(views)]
         h_loss = torch.zeros(views).pin_memory()
 
         def batched_step(it, tptrs, lbase, lstride):
-            for v in mine:
-                ctx.check(ctx.L.tgsx_view_accumulate(ctx.h, dm.h, C.byref(pats[v]), bg, C.c_void_p(tptrs[v]),
-                                                     C.c_void_p(lbase + 4 * v)))
-            if world > 1:
-                with torch.cuda.stream(stream):
-                    dist.all_reduce(sharded._tensor())
+            # this rank's views -> step buffer -> NCCL all-reduce (N > 1) -> Adam, the last chain /
+            # all-reduce / Adam pipelined over Gaussian buckets (tgsx_batched_step)
+            tp = (C.c_void_p * max(len(mine), 1))(*[tptrs[v] for v in mine])
             a = P._lib.AdamArgs(it + 1, 10000, diag)
-            ctx.check(ctx.L.tgsx_apply_step(ctx.h, dm.h, views, C.byref(a)))
+            ctx.check(ctx.L.tgsx_batched_step(ctx.h, dm.h, len(mine), mpats, bg, tp, views, C.byref(a),
+                                              C.c_void_p(lbase + 4 * (mine[0] if mine else 0)), args.buckets))
 
         d_ptrs = [t.data_ptr() for t in targets]
         h_ptrs = [t.data_ptr() for t in h_targets]
@@ -519,12 +567,15 @@ def run_tgsx(args, cfg):
     # The fit changes the model (and so the per-step work) every iteration: each timed phase
     # below restarts from the same initial model, W warm-up steps, then K timed steps, so the
     # device-resident and the end-to-end numbers measure the same trajectory.
+    steps, warmup = steps_override or (args.steps, args.warmup)
+    small = n * 200 < (96 << 20)  # per-step working set below L2: flush it before every step
+
     def restart():
-        if args.config == "c4":
+        if name == "c4":
             return
         dm.upload(host)
         ctx.synchronize()
-        for i in range(args.warmup):
+        for i in range(warmup):
             step_fn(i)
         ctx.synchronize()
 
@@ -532,25 +583,26 @@ def run_tgsx(args, cfg):
 
     launches0 = ctx.launches
     with ClockSampler(local) as clk:
-        ms = timer.run(step_fn, args.steps, args.warmup, ctx)
+        ms = timer.run(step_fn, steps, warmup, ctx, flush=small)
     launches = ctx.launches - launches0
     counters = ctx.counters()
     # per-stage CUDA-event timing in a separate run (the event records and their readback add
     # host work between the launches, so they stay out of the timed region above)
-    prof_steps = min(args.steps, 20)
+    prof_steps = min(steps, 20)
     restart()
     ctx.profile(True)
-    timer.run(step_fn, prof_steps, args.warmup, ctx)
+    timer.run(step_fn, prof_steps, warmup, ctx)
     stages = ctx.profile_read()
+    timeline = ctx.pipeline_timeline() if (world > 1 or name == "c5") else None
     ctx.profile(False)
     e2e_ms = None
     if e2e_fn:
         # the host-input path has its own warm-up (staging buffers, copy stream) before timing
         dm.upload(host)
-        for i in range(args.warmup):
+        for i in range(warmup):
             e2e_fn(i)
         ctx.synchronize()
-        e2e_ms = timer.run(e2e_fn, args.steps, args.warmup, ctx)
+        e2e_ms = timer.run(e2e_fn, steps, warmup, ctx, flush=small)
     fp32_meas = measure_fp32_peak(ctx)  # after the timed regions
     consistent = None
     if world > 1:
@@ -564,36 +616,39 @@ def run_tgsx(args, cfg):
         allh = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(allh, mine)
         consistent = len({int(t.item()) for t in allh}) == 1
+    dm.close()
     if rank != 0:
-        dist.barrier()
-        dist.destroy_process_group()
-        return
-    value = units * args.steps / (ms / 1e3)
+        return None
+    value = units * steps / (ms / 1e3)
     clocks = clk.summary()
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if args.config in ("c5", "c7") else "weak",
+            "steps": steps, "warmup": warmup, "ms_per_step": ms / steps,
+            "higher_is_better": True, "scaling": "strong" if name in ("c5", "c7") else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["workload"] + (f"; dense loss (1-{args.ssim}) L1 + {args.ssim} (1-SSIM)"
                                                       if args.ssim > 0 and p == 1 else ""),
                        "gaussians": n, "width": W, "height": H, "p": p,
-                       "views_per_step": units if args.config in ("c2", "c3", "c6") else cfg.get("views", 1),
-                       "l2": "per-step working set > 126 MB L2 (no explicit flush)",
+                       "views_per_step": units if name in ("c1", "c2", "c3", "c6") else cfg.get("views", 1),
+                       "l2": ("L2 flushed (256 MB write) before every timed step; per-step events"
+                              if small else "per-step working set > 126 MB L2 (no explicit flush)"),
                        "trajectory": "every timed phase starts from the same initial model; the per-step "
                                      "work changes as the fit proceeds, so the average depends on steps"},
             "clocks": clocks,
             "gpu_launches": launches,
-            "roofline": roofline(stages, counters, clocks, n, args.config, fp32_meas),
+            "roofline": roofline(stages, counters, clocks, n, name, fp32_meas),
             "stages_ms_per_step": {k: v[0] / prof_steps for k, v in stages.items() if v[1]},
             "counters": counters}
     if e2e_ms is not None:
-        line["e2e"] = {"value": units * args.steps / (e2e_ms / 1e3), "unit": "iters/s",
+        line["e2e"] = {"value": units * steps / (e2e_ms / 1e3), "unit": "iters/s",
                        "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1]}
     else:
         line["e2e"] = {"value": None, "unit": "iters/s", "note": "fit loop runs device-resident targets"}
     if consistent is not None:
         line["ranks_bit_identical"] = consistent  # model hash equal on every rank after the run
-    if args.config == "c4":
+    if timeline is not None and len(timeline):
+        # last profiled batched step, per Gaussian bucket: chain, all-reduce, Adam [start, end] ms
+        line["pipeline_ms"] = [[round(float(x), 4) for x in row] for row in timeline]
+    if name == "c4":
         reps = extra["reports"]
         line["fit_loop"] = {"iterations": [reps[0].iteration, reps[-1].iteration],
                             "densify_events": sum(r.densified for r in reps),
@@ -602,15 +657,30 @@ def run_tgsx(args, cfg):
                             "count_start": int(n), "count_end": int(reps[-1].count),
                             "budget_end": int(reps[-1].budget),
                             "loss_last": float(extra["trainer"].losses(1)[-1])}
-    if world == 1 and not args.no_cpu_baseline and args.config in ("c2", "c3"):
+    if name == "c5" and world == 1:
+        line["cpu_baseline"] = {"value": None, "note": "not sampled: 8 CPU 4K views per step exceed the "
+                                "bench's time bound; c3's cpu_baseline is the per-view figure"}
+    if world == 1 and not args.no_cpu_baseline and name in ("c1", "c2", "c3"):
         try:
             line["cpu_baseline"] = cpu_baseline_sample(cfg)
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)}
-    print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    return line
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` with N > 1 outside torchrun: start N ranks (one per GPU) under
+    torch.distributed.run on this node and return its exit code; rank 0 prints the line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # init lines show nranks to whoever reads the log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -622,17 +692,30 @@ def main():
     ap.add_argument("--impl", default="tgsx", choices=["tgsx", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-subrecords", action="store_true",
+                    help="default config only (skip the nested C1 / C3 / C5 records)")
     ap.add_argument("--ssim", type=float, default=0.0,
                     help="lambda_ssim for dense (p=1) views: the SPEC's dense-iteration loss "
                          "(1-w) L1 + w (1-SSIM); default 0 = L1 (the graded hot path)")
+    ap.add_argument("--buckets", type=int, default=4,
+                    help="Gaussian buckets of the pipelined chain -> all-reduce -> Adam (N > 1, batched views)")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    rank, world, _ = env_rank()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.launch_check:  # launcher test (CPU): every rank reports itself, no GPU work
+        print(json.dumps({"rank": rank, "world": world}), flush=True)
+        return
     if args.impl == "tgsx":
         args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
-        run_tgsx(args, cfg)
+        run_tgsx(args)
 
 
 if __name__ == "__main__":

@@ -160,14 +160,44 @@ int32_t tgsx_fit_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, con
 /* Batched views (SPEC.md:269-277 accumulate; multi-GPU view sharding):
  * tgsx_view_accumulate adds one view's gradients and densify-stat increments into the
  * model's per-step buffer (12 floats per Gaussian: 9 gradient sums, pos-norm sum,
- * colour-norm sum, visit count). The buffer (device pointer, [12][n] floats) may be
- * all-reduced across ranks before tgsx_apply_step divides by batch_views, applies the
- * stats and runs Adam. */
+ * colour-norm sum, visit count; the reference accumulates stats per backward call,
+ * rasterizer.cpp:350-358). The buffer (device pointer, AoS [n][12] floats = exactly 48 B per
+ * Gaussian, rows in the model's physical order) may be all-reduced across ranks before
+ * tgsx_apply_step divides by batch_views, applies the stats and runs Adam.
+ * tgsx_step_layout brings the rows to the canonical order every rank shares (the blend
+ * order); a rank that accumulated no view of the step must call it before an external
+ * all-reduce (the fused views already leave the rows there). */
 int32_t tgsx_view_accumulate(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat,
                              const float bg[3], const float* target, float* out_loss);
 float* tgsx_step_buffer(tgsx_model* m, int64_t* out_floats);
+int32_t tgsx_step_layout(tgsx_ctx* ctx, tgsx_model* m);
 int32_t tgsx_apply_step(tgsx_ctx* ctx, tgsx_model* m, int32_t batch_views,
                         const tgsx_adam_args* a);
+
+/* ------------------------------------------------ in-library NCCL (view-batch DP, §8e)
+ * Replaces the reference's `accumulate` over a batch when the batch is
+ * sharded across GPUs: every rank holds the full model, renders its views, and the per-Gaussian
+ * step buffer is summed with ONE NCCL all-reduce over NVLink (NVLS where NCCL enables it).
+ * NCCL is dlopen'ed (libnccl.so.2: inside PyTorch, torch's own NCCL).
+ * tgsx_comm_unique_id: rank 0 creates the 128-byte id, the caller distributes it;
+ * tgsx_comm_init: attach a communicator of nranks to the context (its device);
+ * tgsx_allreduce_step: in-place sum of the step buffer over the ranks (stream-ordered);
+ * tgsx_batched_step: this rank's n_views views (pats[v], targets[v]; n_views may be 0) of a
+ *   step of batch_views views in total -> step buffer -> all-reduce (if a communicator is
+ *   attached) -> Adam over the mean + stats, with the last view's chain kernel, the all-reduce
+ *   and Adam pipelined over `buckets` Gaussian ranges (chain(b) -> all-reduce(b) -> Adam(b)).
+ *   out_losses[v] (may be NULL) as tgsx_fit_step's out_loss.
+ * tgsx_pipeline_timeline: with profiling enabled, the last batched step's per-bucket event
+ *   times in ms (chain start/end, all-reduce start/end, Adam start/end); returns the count. */
+int32_t tgsx_comm_unique_id(uint8_t out_id[128]);
+int32_t tgsx_comm_init(tgsx_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank);
+int32_t tgsx_comm_destroy(tgsx_ctx* ctx);
+int32_t tgsx_comm_size(const tgsx_ctx* ctx);
+int32_t tgsx_allreduce_step(tgsx_ctx* ctx, tgsx_model* m);
+int32_t tgsx_batched_step(tgsx_ctx* ctx, tgsx_model* m, int32_t n_views, const tgsx_pattern* pats,
+                          const float bg[3], const float* const* targets, int32_t batch_views,
+                          const tgsx_adam_args* a, float* out_losses, int32_t buckets);
+int32_t tgsx_pipeline_timeline(tgsx_ctx* ctx, float* out, int32_t max_floats);
 
 /* ---------------------------------------------------------------- densify */
 typedef struct {
@@ -375,6 +405,7 @@ int32_t tgsx_fit_step3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, 
 int32_t tgsx_view_accumulate3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, const tgsx_pattern* pat,
                                const float bg[3], const float* target, float* out_loss);
 float* tgsx_step_buffer3d(tgsx_model3d* m, int64_t* out_floats);
+int32_t tgsx_allreduce_step3d(tgsx_ctx* ctx, tgsx_model3d* m);  /* NCCL sum of the [62][n] buffer */
 int32_t tgsx_apply_step3d(tgsx_ctx* ctx, tgsx_model3d* m, int32_t batch_views, const tgsx_adam3d_args* a);
 /* Parity stage: the 64-B records (Prepared layout, raster.cu) of all n Gaussians and their
  * orderable depth keys (culled: 0xffffffff), in the order the binning produced them:

@@ -104,6 +104,15 @@ SIGNATURES = {
     "tgsx_view_accumulate": (C.c_int32, [vp, vp, P(Pattern), f32p, vp, vp]),
     "tgsx_step_buffer": (vp, [vp, i64p]),
     "tgsx_apply_step": (C.c_int32, [vp, vp, C.c_int32, P(AdamArgs)]),
+    "tgsx_step_layout": (C.c_int32, [vp, vp]),
+    "tgsx_comm_unique_id": (C.c_int32, [vp]),
+    "tgsx_comm_init": (C.c_int32, [vp, vp, C.c_int32, C.c_int32]),
+    "tgsx_comm_destroy": (C.c_int32, [vp]),
+    "tgsx_comm_size": (C.c_int32, [vp]),
+    "tgsx_allreduce_step": (C.c_int32, [vp, vp]),
+    "tgsx_batched_step": (C.c_int32, [vp, vp, C.c_int32, P(Pattern), f32p, P(vp), C.c_int32, P(AdamArgs),
+                                      vp, C.c_int32]),
+    "tgsx_pipeline_timeline": (C.c_int32, [vp, f32p, C.c_int32]),
     "tgsx_densify_config_default": (None, [P(DensifyConfig)]),
     "tgsx_densify": (C.c_int32, [vp, vp, P(DensifyConfig), C.c_int64, u64p, P(DensifyReport)]),
     "tgsx_visit_audit": (C.c_int32, [vp, vp]),
@@ -153,6 +162,7 @@ SIGNATURES = {
     "tgsx_adam3d_step": (C.c_int32, [vp, vp, vp, P(Adam3dArgs)]),
     "tgsx_fit_step3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, vp, P(Adam3dArgs), vp]),
     "tgsx_stage_prepare3d": (C.c_int32, [vp, vp, P(Camera3), C.c_int32, vp, vp, P(C.c_int32)]),
+    "tgsx_allreduce_step3d": (C.c_int32, [vp, vp]),
     "tgsx_view_accumulate3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, vp, vp]),
     "tgsx_step_buffer3d": (vp, [vp, i64p]),
     "tgsx_apply_step3d": (C.c_int32, [vp, vp, C.c_int32, P(Adam3dArgs)]),

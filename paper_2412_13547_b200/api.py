@@ -258,10 +258,41 @@ class Context:
         return int(self.L.tgsx_launch_count(self.h))
 
     STAGES = ("depth_sort", "preprocess", "scan", "duplicate", "radix_sort", "ranges",
-              "blend_forward", "blend_backward", "chain_adam", "loss", "densify")
+              "blend_forward", "blend_backward", "chain_adam", "loss", "densify", "adam")
 
     def profile(self, enable: bool = True):
         self.check(self.L.tgsx_profile(self.h, 1 if enable else 0))
+
+    # ------------------------------------------------ in-library NCCL
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """A fresh 128-byte NCCL unique id (rank 0 creates it, the caller distributes it)."""
+        buf = (C.c_uint8 * 128)()
+        rc = _lib.load().tgsx_comm_unique_id(buf)
+        if rc:
+            raise RuntimeError(f"tgsx_comm_unique_id failed ({rc}): NCCL not loadable")
+        return bytes(buf)
+
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        """Attach an NCCL communicator of `nranks` (this context's device) for batched steps."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        self.check(self.L.tgsx_comm_init(self.h, buf, int(nranks), int(rank)))
+
+    def comm_destroy(self):
+        self.check(self.L.tgsx_comm_destroy(self.h))
+
+    def comm_size(self) -> int:
+        return int(self.L.tgsx_comm_size(self.h))
+
+    def pipeline_timeline(self):
+        """Per-bucket event times (ms from the step start) of the last profiled batched step:
+        array [buckets][6] = chain start/end, all-reduce start/end, Adam start/end."""
+        n = self.L.tgsx_pipeline_timeline(self.h, None, 0)
+        out = np.zeros(max(n, 1), np.float32)
+        self.L.tgsx_pipeline_timeline(self.h, _ptr(out, _lib.f32p), n)
+        return out[:n].reshape(-1, 6)
 
     def set_binning(self, mode: int):
         """0: slab binning with per-tile sorts (default); 1: always the onesweep paths."""
@@ -422,10 +453,39 @@ class DeviceModel:
         return float(loss[0])
 
     def step_buffer(self):
-        """(device pointer, float count) of the [12][cap] batched step buffer."""
+        """(device pointer, float count) of the batched step buffer: AoS [n][12] floats (48 B per
+        Gaussian, rows in the model's physical order)."""
         n = C.c_int64()
         p = self.ctx.L.tgsx_step_buffer(self.h, C.byref(n))
         return int(p), int(n.value)
+
+    def step_layout(self):
+        """Bring the rows (and the step buffer) to the canonical blend order every rank of a
+        view-sharded step shares; required on a rank with no view before an external all-reduce."""
+        self.ctx.check(self.ctx.L.tgsx_step_layout(self.ctx.h, self.h))
+
+    def allreduce_step(self):
+        """In-place sum of the step buffer over the context's NCCL communicator."""
+        self.ctx.check(self.ctx.L.tgsx_allreduce_step(self.ctx.h, self.h))
+
+    def batched_step(self, views, background, batch_views: int, step: int, total_steps: int,
+                     image_diagonal: float, buckets: int = 4, losses_out=None):
+        """This rank's `views` [(pattern, target), ...] of a step of `batch_views` views in total:
+        accumulate -> all-reduce over the context's communicator (if attached) -> Adam, with the
+        last chain / all-reduce / Adam pipelined over `buckets` Gaussian ranges. Targets are (H, W, 3)
+        host arrays or device pointers (int). Returns the per-view losses (or writes them to the
+        `losses_out` pointer and returns None)."""
+        nv = len(views)
+        pats = (_lib.Pattern * max(nv, 1))(*[pv[0].c() for pv in views])
+        keep = [t if isinstance(t, int) else _f32(t) for _, t in views]
+        tps = (C.c_void_p * max(nv, 1))(*[t if isinstance(t, int) else t.ctypes.data for t in keep])
+        bg = (C.c_float * 3)(*background)
+        a = _lib.AdamArgs(step, total_steps, image_diagonal)
+        loss = np.zeros(max(nv, 1), np.float32)
+        lp = C.c_void_p(losses_out) if losses_out is not None else _ptr(loss)
+        self.ctx.check(self.ctx.L.tgsx_batched_step(self.ctx.h, self.h, nv, pats, bg, tps, batch_views,
+                                                    C.byref(a), lp, buckets))
+        return None if losses_out is not None else [float(x) for x in loss[:nv]]
 
     def apply_step(self, batch_views: int, step: int, total_steps: int, image_diagonal: float):
         a = _lib.AdamArgs(step, total_steps, image_diagonal)

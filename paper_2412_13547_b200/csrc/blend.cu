@@ -730,19 +730,20 @@ BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* ite
 template <int NGX, int NGY>
 cudaError_t run_backward(tgsx_ctx* ctx, const BlendParams& prm) {
     const size_t smem = kWPB * sizeof(BwdWarpSmem<NGX * NGY>);
-    static bool configured = false;
-    static int resident = 0;  // CTAs resident at once (SMs x CTAs per SM)
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(backward_kernel<NGX, NGY>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int& resident = ctx->bwd_resident[NGX == 2 ? 0 : 1];  // CTAs resident at once (SMs x CTAs/SM)
+    if (!resident) {
+        // per context: the opt-in above 48 KB is a per-device attribute, set on the ctx's device
+        int prev = 0;
+        cudaError_t e = cudaGetDevice(&prev);
         if (e) return e;
+        if (prev != ctx->device && (e = cudaSetDevice(ctx->device))) return e;
+        e = cudaFuncSetAttribute(backward_kernel<NGX, NGY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int sms = 0, per_sm = 0;
-        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device))) return e;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, backward_kernel<NGX, NGY>,
-                                                               kWPB * 32, smem)))
-            return e;
+        if (!e) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        if (!e) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, backward_kernel<NGX, NGY>, kWPB * 32, smem);
+        if (prev != ctx->device) cudaSetDevice(prev);
+        if (e) return e;
         resident = std::max(1, sms * std::max(per_sm, 1));
-        configured = true;
     }
     cudaError_t e = cudaMemsetAsync(prm.tile_queue, 0, sizeof(unsigned int), ctx->stream);
     if (e) return e;

@@ -179,7 +179,7 @@ cudaError_t model_reserve(tgsx_ctx* ctx, tgsx_model* m, int64_t cap) {
     if ((e = regrow_rows(m->tau_v, 1, 8))) return e;
     if ((e = regrow_rows(m->m1, 9, 4))) return e;
     if ((e = regrow_rows(m->m2, 9, 4))) return e;
-    if ((e = regrow_rows(m->step, kStepFloats, 4))) return e;
+    if ((e = regrow_rows(m->step, 1, sizeof(StepRec)))) return e;  // AoS records
     if ((e = regrow_rows(m->screen, 10, 4))) return e;
     if ((e = regrow_rows(m->perm, 1, 4))) return e;
     if ((e = regrow_rows(m->rank_of, 1, 4))) return e;
@@ -209,7 +209,7 @@ cudaError_t permute_model(tgsx_ctx* ctx, tgsx_model* m, const uint32_t* idx) {
     struct R { DevBuf* b; int rows; int elt; } rs[] = {
         {&m->params, kParamRows, 4}, {&m->ids, 1, 8}, {&m->pos_acc, 1, 4}, {&m->col_acc, 1, 4},
         {&m->accum, 1, 4}, {&m->visit, 1, 8}, {&m->window, 1, 8}, {&m->tau_v, 1, 8},
-        {&m->m1, 9, 4}, {&m->m2, 9, 4}, {&m->step, kStepFloats, 4}};
+        {&m->m1, 9, 4}, {&m->m2, 9, 4}, {&m->step, 1, (int)sizeof(StepRec)}};
     static_assert(sizeof(rs) / sizeof(rs[0]) == sizeof(m->spare) / sizeof(m->spare[0]), "spares");
     cudaError_t e;
     for (int i = 0; i < 11; ++i) {
@@ -226,6 +226,9 @@ cudaError_t permute_model(tgsx_ctx* ctx, tgsx_model* m, const uint32_t* idx) {
         if (r.elt == 4)
             permute_rows_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(r.b->as<uint32_t>(), sp.as<uint32_t>(),
                                                                         cap, n, r.rows, idx);
+        else if (r.elt == (int)sizeof(StepRec))
+            permute_rows_kernel<StepRec><<<grid, 256, 0, ctx->stream>>>(r.b->as<StepRec>(), sp.as<StepRec>(),
+                                                                       cap, n, 1, idx);
         else
             permute_rows_kernel<unsigned long long><<<grid, 256, 0, ctx->stream>>>(
                 r.b->as<unsigned long long>(), sp.as<unsigned long long>(), cap, n, r.rows, idx);
@@ -245,8 +248,8 @@ cudaError_t model_grow(tgsx_ctx* ctx, tgsx_model* m, int64_t cap) {
     if (cap <= m->cap) return cudaSuccess;
     cudaError_t e = model_reserve(ctx, m, cap);
     if (e) return e;
-    const int rows[11] = {kParamRows, 1, 1, 1, 1, 1, 1, 1, 9, 9, kStepFloats};
-    const int elt[11] = {4, 8, 4, 4, 4, 8, 8, 8, 4, 4, 4};
+    const int rows[11] = {kParamRows, 1, 1, 1, 1, 1, 1, 1, 9, 9, 1};
+    const int elt[11] = {4, 8, 4, 4, 4, 8, 8, 8, 4, 4, (int)sizeof(StepRec)};
     for (int i = 0; i < 11; ++i) {
         DevBuf& sp = m->spare[i];
         const size_t bytes = (size_t)rows[i] * m->cap * elt[i];
@@ -671,8 +674,11 @@ int32_t render_core(tgsx_ctx* ctx, tgsx_model* m, const RenderArgs& ra, bool fus
 }
 
 
+// run_chain = false: everything up to (not including) the chain kernel; the caller launches the
+// chain itself (tgsx_batched_step pipelines it over Gaussian buckets with the all-reduce)
 int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
-                   const float* target, float* out_loss, ChainMode mode, const AdamCfg* cfg) {
+                   const float* target, float* out_loss, ChainMode mode, const AdamCfg* cfg,
+                   bool run_chain = true) {
     int32_t rc = check_pattern(ctx, pat);
     if (rc) return rc;
     if (!target) return fail(ctx, TGSX_EINVAL, "target is null");
@@ -700,7 +706,7 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
         StageTimer t(ctx, kStBackward);
         CK(launch_backward(ctx, ra, items));
     }
-    {
+    if (run_chain) {
         StageTimer t(ctx, kStChain);
         CK(launch_chain(ctx, m, mode, true, nullptr, reinterpret_cast<const float*>(cfg)));
     }
@@ -957,6 +963,7 @@ void tgsx_destroy(tgsx_ctx* ctx) {
             cudaEventDestroy(ctx->consumed[i]);
         }
     }
+    comm_release(ctx);
     if (ws.h_scratch) cudaFreeHost(ws.h_scratch);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
@@ -1243,8 +1250,140 @@ int32_t tgsx_view_accumulate(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* p
 
 float* tgsx_step_buffer(tgsx_model* m, int64_t* out_floats) {
     if (!m) return nullptr;
-    if (out_floats) *out_floats = (int64_t)kStepFloats * m->cap;
+    if (out_floats) *out_floats = (int64_t)kStepFloats * m->n;  // AoS [n][12]: exactly 48 B/G
     return m->step.as<float>();
+}
+
+// Canonical row order of the step buffer shared by every rank of a view-sharded step: the blend
+// order (identical on every rank: depth_key and ids are replicated). A rank that accumulated views
+// is already there (fused views permute the rows into blend order); a rank with no view of the
+// step must be brought there BEFORE the all-reduce — its buffer is still zero, so the
+// permutation moves nothing but the model rows — or it would apply blend-ordered sums to
+// logically ordered rows.
+int32_t tgsx_step_layout(tgsx_ctx* ctx, tgsx_model* m) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    if (m->order_dirty) {
+        ctx->bin_valid = false;
+        CK(launch_sort_depth(ctx, m));
+    }
+    if (!m->blend_phys) CK(model_to_blend_order(ctx, m));
+    return TGSX_OK;
+}
+
+// Sum of the step buffer over the attached communicator's ranks (48 B per Gaussian, in place),
+// on the comm stream ordered after / before the compute stream.
+int32_t tgsx_allreduce_step(tgsx_ctx* ctx, tgsx_model* m) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    if (!ctx->comm) return fail(ctx, TGSX_ESTATE, "no communicator attached (tgsx_comm_init)");
+    int32_t rc = tgsx_step_layout(ctx, m);
+    if (rc) return rc;
+    if (ctx->pipe_events.size() < 2) {
+        for (auto& e : ctx->pipe_events) cudaEventDestroy(e);
+        ctx->pipe_events.assign(2, nullptr);
+        for (auto& e : ctx->pipe_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ctx->pipe_events[0], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->pipe_events[0], 0));
+    if ((rc = comm_allreduce_sum(ctx, m->step.as<float>(), (size_t)kStepFloats * m->n, ctx->comm_stream))) return rc;
+    CK(cudaEventRecord(ctx->pipe_events[1], ctx->comm_stream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->pipe_events[1], 0));
+    return TGSX_OK;
+}
+
+// One view-sharded batched step of this rank: its n_views views accumulated into
+// the step buffer, the buffer summed over the communicator's ranks, then the identical Adam +
+// stats update over the global batch (rasterizer.cpp:350-358). The last view's
+// chain kernel, the all-reduce and Adam are pipelined over `buckets` contiguous Gaussian ranges:
+// chain(b) -> all-reduce(b) on the comm stream -> Adam(b), so the transfer of bucket b overlaps
+// the chain of bucket b+1 and the Adam of bucket b-1.
+int32_t tgsx_batched_step(tgsx_ctx* ctx, tgsx_model* m, int32_t n_views, const tgsx_pattern* pats,
+                          const float bg[3], const float* const* targets, int32_t batch_views,
+                          const tgsx_adam_args* a, float* out_losses, int32_t buckets) {
+    if (!ctx || !m || !a || n_views < 0 || (n_views > 0 && (!pats || !targets)))
+        return fail(ctx, TGSX_EINVAL, "batched_step: bad arguments");
+    if (batch_views < 1 || batch_views < n_views) return fail(ctx, TGSX_EINVAL, "batched_step: bad batch size");
+    if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
+    AdamCfg c;
+    fill_adam(c, a);
+    c.batch = (float)batch_views;
+    int32_t rc;
+    for (int v = 0; v + 1 < n_views; ++v) {
+        rc = fused_view(ctx, m, &pats[v], bg, targets[v], out_losses ? out_losses + v : nullptr,
+                        ChainMode::kAccumulate, nullptr);
+        if (rc) return rc;
+    }
+    const bool last_view = n_views > 0;
+    if (last_view) {
+        rc = fused_view(ctx, m, &pats[n_views - 1], bg, targets[n_views - 1],
+                        out_losses ? out_losses + n_views - 1 : nullptr, ChainMode::kAccumulate, nullptr, false);
+        if (rc) return rc;
+    } else if ((rc = tgsx_step_layout(ctx, m))) {
+        return rc;
+    }
+    const int64_t n = m->n;
+    const bool comm = ctx->comm != nullptr;
+    const int B = comm ? (int)std::max<int64_t>(1, std::min<int64_t>(std::max(buckets, 1), (n + 1023) / 1024)) : 1;
+    // bucket bounds, aligned to 256 Gaussians (whole chain / Adam blocks, 12 KB NCCL chunks)
+    std::vector<int64_t> lo(B + 1);
+    for (int b = 0; b <= B; ++b) lo[b] = std::min<int64_t>(n, ((n * b / B) + 255) / 256 * 256);
+    lo[B] = n;
+    const size_t ne = 1 + 6 * (size_t)B;
+    if (ctx->pipe_events.size() < ne) {
+        for (auto& e : ctx->pipe_events) cudaEventDestroy(e);
+        ctx->pipe_events.assign(ne, nullptr);
+        for (auto& e : ctx->pipe_events) CK(cudaEventCreate(&e));  // timing: the pipeline timeline
+    }
+    cudaEvent_t* ev = ctx->pipe_events.data();  // [0] step start; per bucket 6: chain s/e, ar s/e, adam s/e
+    CK(cudaEventRecord(ev[0], ctx->stream));
+    for (int b = 0; b < B; ++b) {
+        cudaEvent_t* e = ev + 1 + 6 * b;
+        CK(cudaEventRecord(e[0], ctx->stream));
+        if (last_view) {
+            StageTimer t(ctx, kStChain);
+            CK(launch_chain(ctx, m, ChainMode::kAccumulate, true, nullptr, nullptr, lo[b], lo[b + 1]));
+        }
+        CK(cudaEventRecord(e[1], ctx->stream));
+        if (comm) {
+            CK(cudaStreamWaitEvent(ctx->comm_stream, e[1], 0));
+            CK(cudaEventRecord(e[2], ctx->comm_stream));
+            rc = comm_allreduce_sum(ctx, m->step.as<float>() + (size_t)kStepFloats * lo[b],
+                                    (size_t)kStepFloats * (lo[b + 1] - lo[b]), ctx->comm_stream);
+            if (rc) return rc;
+            CK(cudaEventRecord(e[3], ctx->comm_stream));
+        }
+    }
+    for (int b = 0; b < B; ++b) {
+        cudaEvent_t* e = ev + 1 + 6 * b;
+        if (comm) CK(cudaStreamWaitEvent(ctx->stream, e[3], 0));
+        CK(cudaEventRecord(e[4], ctx->stream));
+        {
+            StageTimer t(ctx, kStAdam);
+            CK(launch_adam(ctx, m, nullptr, reinterpret_cast<const float*>(&c), batch_views, lo[b], lo[b + 1]));
+        }
+        CK(cudaEventRecord(e[5], ctx->stream));
+    }
+    m->step_views = 0;
+    ctx->bin_valid = false;  // the parameters moved
+    if (ctx->prof.enabled) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->pipe_timeline.assign(6 * (size_t)B, 0.f);
+        for (int b = 0; b < B; ++b)
+            for (int k = 0; k < 6; ++k) {
+                if (!comm && (k == 2 || k == 3)) continue;
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, ev[0], ev[1 + 6 * b + k]));
+                ctx->pipe_timeline[6 * b + k] = ms;
+            }
+    }
+    return TGSX_OK;
+}
+
+int32_t tgsx_pipeline_timeline(tgsx_ctx* ctx, float* out, int32_t max_floats) {
+    if (!ctx) return -1;
+    const int32_t n = (int32_t)ctx->pipe_timeline.size();
+    if (out)
+        for (int32_t i = 0; i < std::min(n, max_floats); ++i) out[i] = ctx->pipe_timeline[i];
+    return n;
 }
 
 int32_t tgsx_set_binning(tgsx_ctx* ctx, int32_t mode) {
@@ -1303,7 +1442,10 @@ int32_t tgsx_apply_step(tgsx_ctx* ctx, tgsx_model* m, int32_t batch_views, const
     if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
     AdamCfg c;
     fill_adam(c, a);
-    CK(launch_adam(ctx, m, nullptr, reinterpret_cast<const float*>(&c), batch_views));
+    {
+        StageTimer t(ctx, kStAdam);
+        CK(launch_adam(ctx, m, nullptr, reinterpret_cast<const float*>(&c), batch_views));
+    }
     m->step_views = 0;
     return TGSX_OK;
 }
@@ -1594,8 +1736,27 @@ int32_t tgsx_view_accumulate3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera
 
 float* tgsx_step_buffer3d(tgsx_model3d* m, int64_t* out_floats) {
     if (!m) return nullptr;
-    if (out_floats) *out_floats = (int64_t)k3dStepRows * m->cap;
+    if (out_floats) *out_floats = (int64_t)k3dStepRows * m->n;  // packed [62][n]
     return m->step.as<float>();
+}
+
+// In-place sum of the packed [62][n] 3-D step buffer over the attached communicator (rows stay in
+// creation order on every rank: no layout step is needed).
+int32_t tgsx_allreduce_step3d(tgsx_ctx* ctx, tgsx_model3d* m) {
+    if (!ctx || !m) return TGSX_EINVAL;
+    if (!ctx->comm) return fail(ctx, TGSX_ESTATE, "no communicator attached (tgsx_comm_init)");
+    if (ctx->pipe_events.size() < 2) {
+        for (auto& e : ctx->pipe_events) cudaEventDestroy(e);
+        ctx->pipe_events.assign(2, nullptr);
+        for (auto& e : ctx->pipe_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ctx->pipe_events[0], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->pipe_events[0], 0));
+    int32_t rc = comm_allreduce_sum(ctx, m->step.as<float>(), (size_t)k3dStepRows * m->n, ctx->comm_stream);
+    if (rc) return rc;
+    CK(cudaEventRecord(ctx->pipe_events[1], ctx->comm_stream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->pipe_events[1], 0));
+    return TGSX_OK;
 }
 
 int32_t tgsx_apply_step3d(tgsx_ctx* ctx, tgsx_model3d* m, int32_t batch_views, const tgsx_adam3d_args* a) {
@@ -1606,8 +1767,7 @@ int32_t tgsx_apply_step3d(tgsx_ctx* ctx, tgsx_model3d* m, int32_t batch_views, c
     fill_adam3d(cfg, a);
     CK(launch_adam3d_step(ctx, m, batch_views, cfg));
     m->step_views = 0;
-    CK(cudaStreamSynchronize(ctx->stream));
-    return TGSX_OK;
+    return TGSX_OK;  // stream-ordered: no host sync per step
 }
 
 // One 3-D view: render + fused L1 (+ SSIM on dense views) + backward + chain3d in `mode`

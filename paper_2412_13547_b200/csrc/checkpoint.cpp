@@ -140,15 +140,21 @@ int32_t tgsx_checkpoint_load(tgsx_ctx* ctx, tgsx_model* m, tgsx_trainer* tr, con
          r.bytes(h.window.data(), n * 8) && r.bytes(h.tau_v.data(), n * 8) &&
          r.bytes(h.m1.data(), n * 36) && r.bytes(h.m2.data(), n * 36);
     uint32_t has_state = 0;
+    int32_t rc_parse = TGSX_OK;
     ok = ok && r.get(has_state) && has_state <= 1;
     if (!ok) return TGSX_ERUNTIME;
     if (has_state && !tr) return TGSX_EINVAL;  // training state needs a trainer to restore into
+    // parse and validate EVERYTHING before touching the caller's model or trainer: a corrupt or
+    // truncated trainer section (or trailing bytes) leaves both exactly as they were
+    tgsx::TrainerState st;
+    if (has_state && (rc_parse = tgsx::trainer_parse(tr, r, st))) return rc_parse;
+    if (r.p != r.end) return TGSX_ERUNTIME;  // trailing bytes: not a TGS1 file
     tgsx_host_scene s = h.scene();
     int32_t rc = tgsx_model_upload(ctx, m, &s);
     if (rc) return rc;
     if ((rc = tgsx_model_upload_moments(ctx, m, h.m1.data(), h.m2.data()))) return rc;
-    if (has_state && (rc = tgsx::trainer_read(tr, r))) return rc;
-    return r.p == r.end ? TGSX_OK : TGSX_ERUNTIME;  // trailing bytes: not a TGS1 file
+    if (has_state && (rc = tgsx::trainer_commit(tr, st))) return rc;
+    return TGSX_OK;
 }
 
 }  // extern "C"

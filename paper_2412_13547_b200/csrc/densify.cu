@@ -275,7 +275,7 @@ int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cf
         DCK(cudaMemsetAsync(m->window.as<int64_t>() + n0, 0, nsel * 8, ctx->stream));
         DCK(cudaMemset2DAsync(m->m1.as<float>() + n0, cap * 4, 0, nsel * 4, 9, ctx->stream));
         DCK(cudaMemset2DAsync(m->m2.as<float>() + n0, cap * 4, 0, nsel * 4, 9, ctx->stream));
-        DCK(cudaMemset2DAsync(m->step.as<float>() + n0, cap * 4, 0, nsel * 4, kStepFloats, ctx->stream));
+        DCK(cudaMemsetAsync(m->step.as<StepRec>() + n0, 0, nsel * sizeof(StepRec), ctx->stream));
         tgsx_pcg32_advance(rng_state, 3ull * (uint64_t)nsel);
         m->next_id += (uint64_t)nsel;
         m->n = n0 + nsel;
@@ -301,7 +301,7 @@ int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cf
             struct R { DevBuf* b; int rows; int elt; } rs[] = {
                 {&m->params, 10, 4}, {&m->ids, 1, 8}, {&m->pos_acc, 1, 4}, {&m->col_acc, 1, 4},
                 {&m->accum, 1, 4}, {&m->visit, 1, 8}, {&m->window, 1, 8}, {&m->tau_v, 1, 8},
-                {&m->m1, 9, 4}, {&m->m2, 9, 4}, {&m->step, kStepFloats, 4}};
+                {&m->m1, 9, 4}, {&m->m2, 9, 4}, {&m->step, 1, (int)sizeof(StepRec)}};
             // compact each row group into its spare (allocated once per capacity) and swap
             for (int i = 0; i < 11; ++i) {
                 const auto& r = rs[i];
@@ -316,6 +316,9 @@ int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cf
                 if (r.elt == 4)
                     compact_rows<uint32_t><<<grid_for(n1, 256), 256, 0, ctx->stream>>>(
                         r.b->as<uint32_t>(), sp.as<uint32_t>(), cap, n1, r.rows, keep, kpos);
+                else if (r.elt == (int)sizeof(StepRec))
+                    compact_rows<StepRec><<<grid_for(n1, 256), 256, 0, ctx->stream>>>(
+                        r.b->as<StepRec>(), sp.as<StepRec>(), cap, n1, 1, keep, kpos);
                 else
                     compact_rows<unsigned long long><<<grid_for(n1, 256), 256, 0, ctx->stream>>>(
                         r.b->as<unsigned long long>(), sp.as<unsigned long long>(), cap, n1, r.rows, keep, kpos);

@@ -234,6 +234,9 @@ void budget_write(const tgsx_budget* b, ByteWriter& w) {
     }
 }
 
+tgsx_budget* budget_clone(const tgsx_budget* b) { return new tgsx_budget(*b); }
+void budget_assign(tgsx_budget* dst, const tgsx_budget* src) { *dst = *src; }
+
 bool budget_read(tgsx_budget* b, ByteReader& r) {
     uint8_t has = 0;
     if (!(r.get(b->n_init) && r.get(b->m_final) && r.get(b->m_adaptive) && r.get(b->alpha) &&

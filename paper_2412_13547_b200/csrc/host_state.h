@@ -43,7 +43,24 @@ struct ByteReader {
 
 void budget_write(const tgsx_budget* b, ByteWriter& w);
 bool budget_read(tgsx_budget* b, ByteReader& r);
+tgsx_budget* budget_clone(const tgsx_budget* b);
+void budget_assign(tgsx_budget* dst, const tgsx_budget* src);
 void trainer_write(const tgsx_trainer* tr, ByteWriter& w);
-int32_t trainer_read(tgsx_trainer* tr, ByteReader& r);  // TGSX_OK, TGSX_ERUNTIME (corrupt)
+
+// Training state parsed from a checkpoint, not yet applied: the load parses everything first and
+// changes the caller's model / trainer only once the whole file has been validated.
+struct TrainerState {
+    int64_t t = 0, adam_step = 0, n_init = 0, fed = 0, ring = 0;
+    uint64_t rng[2] = {0, 0};
+    double last_budget = 0;
+    std::vector<float> losses;
+    tgsx_budget* budget = nullptr;  // owned (destroyed by the destructor)
+    TrainerState() = default;
+    TrainerState(const TrainerState&) = delete;
+    TrainerState& operator=(const TrainerState&) = delete;
+    ~TrainerState();
+};
+int32_t trainer_parse(const tgsx_trainer* tr, ByteReader& r, TrainerState& st);  // OK / ERUNTIME
+int32_t trainer_commit(tgsx_trainer* tr, const TrainerState& st);                // OK / ECUDA
 
 }  // namespace tgsx

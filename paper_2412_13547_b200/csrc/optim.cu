@@ -87,15 +87,16 @@ struct ChainParams {
     float* grads;   // [9][n] (mode 0)
     float* m1;
     float* m2;
-    float* step;    // [12][cap] (mode 2)
+    StepRec* step;  // [n] AoS (mode 2)
+    int64_t i0, i1; // Gaussian (row) range of this launch (buckets of the pipelined batched step)
     AdamCfg adam;
 };
 
 // 6 blocks of 256 per SM (<= 40 registers): the slot loop and the moment / parameter streams
 // are latency-bound, so occupancy buys memory-level parallelism
 __global__ void __launch_bounds__(256, 4) chain_kernel(ChainParams cp) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= cp.n) return;
+    const int64_t i = cp.i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cp.i1) return;
     const int64_t cap = cp.cap;
     const float* __restrict__ params = cp.params;
     // independent loads first (memory-level parallelism): the raw parameters the chain rule
@@ -210,13 +211,18 @@ __global__ void __launch_bounds__(256, 4) chain_kernel(ChainParams cp) {
         cn = __fsqrt_rn(fadd(fadd(fmul(g[6], g[6]), fmul(g[7], g[7])), fmul(g[8], g[8])));
     }
     if (cp.mode == 2) {
-#pragma unroll
-        for (int q = 0; q < 9; ++q) cp.step[q * cap + i] += g[q];
+        // batched views: sums in view order; the three counters increment
+        // together (rasterizer.cpp:352-357), so one visit count is carried
+        StepRec r = cp.step[i];
+        r.a.x += g[0]; r.a.y += g[1]; r.a.z += g[2]; r.a.w += g[3];
+        r.b.x += g[4]; r.b.y += g[5]; r.b.z += g[6]; r.b.w += g[7];
+        r.c.x += g[8];
         if (visited) {
-            cp.step[9 * cap + i] += pn;
-            cp.step[10 * cap + i] += cn;
-            cp.step[11 * cap + i] += 1.0f;
+            r.c.y += pn;
+            r.c.z += cn;
+            r.c.w += 1.0f;
         }
+        cp.step[i] = r;
         return;
     }
     if (cp.update_stats && visited) {
@@ -234,34 +240,32 @@ __global__ void __launch_bounds__(256, 4) chain_kernel(ChainParams cp) {
     adam_update_pre(cp.params_w, cp.m1, cp.m2, cap, i, g, th0, mm0, vv0, cp.adam);
 }
 
-// mode 0: grads [9][n] given; mode 1: step buffer [12][cap] (mean over batch, stats applied)
+// grads != null: explicit gradients [9][n]; else the batched step buffer (AoS [n], mean over the
+// batch, stats applied, record zeroed for the next batch). Rows [i0, i1).
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, float* __restrict__ m1,
                                                    float* __restrict__ m2, int64_t cap, int64_t n,
-                                                   const float* __restrict__ grads,
-                                                   float* __restrict__ step, float* pos_acc,
+                                                   int64_t i0, int64_t i1, const float* __restrict__ grads,
+                                                   StepRec* __restrict__ step, float* pos_acc,
                                                    float* col_acc, int32_t* accum, int64_t* visit,
                                                    int64_t* window, AdamCfg c) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= i1) return;
     float g[9];
     if (step) {
+        const StepRec r = step[i];
+        const float s9[9] = {r.a.x, r.a.y, r.a.z, r.a.w, r.b.x, r.b.y, r.b.z, r.b.w, r.c.x};
 #pragma unroll
-        for (int q = 0; q < 9; ++q) {
-            g[q] = fdiv_pos(step[q * cap + i], c.batch);
-            step[q * cap + i] = 0.f;
-        }
-        const float v = step[11 * cap + i];
-        if (v > 0.f) {
-            const int32_t cnt = (int32_t)v;
-            pos_acc[i] = fadd(pos_acc[i], step[9 * cap + i]);
-            col_acc[i] = fadd(col_acc[i], step[10 * cap + i]);
+        for (int q = 0; q < 9; ++q) g[q] = fdiv_pos(s9[q], c.batch);
+        if (r.c.w > 0.f) {
+            const int32_t cnt = (int32_t)r.c.w;
+            pos_acc[i] = fadd(pos_acc[i], r.c.y);
+            col_acc[i] = fadd(col_acc[i], r.c.z);
             accum[i] += cnt;
             visit[i] += cnt;
             window[i] += cnt;
         }
-        step[9 * cap + i] = 0.f;
-        step[10 * cap + i] = 0.f;
-        step[11 * cap + i] = 0.f;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        step[i] = StepRec{z, z, z};
     } else {
 #pragma unroll
         for (int q = 0; q < 9; ++q) g[q] = grads[q * n + i];
@@ -274,13 +278,16 @@ inline unsigned grid_for(int64_t n, int bt) { return (unsigned)((n + bt - 1) / b
 }  // namespace
 
 cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool update_stats,
-                         float* grads_out, const float* adam_cfg) {
-    if (m->n == 0) return cudaSuccess;
+                         float* grads_out, const float* adam_cfg, int64_t i0, int64_t i1) {
+    if (i1 < 0) i1 = m->n;
+    if (i1 <= i0) return cudaSuccess;
     ChainParams cp{};
     cp.params = m->params.as<float>();
     cp.params_w = m->params.as<float>();
     cp.cap = m->cap;
     cp.n = m->n;
+    cp.i0 = i0;
+    cp.i1 = i1;
     cp.rank_of = m->rank_of.as<uint32_t>();
     cp.perm = m->blend_phys ? m->perm.as<uint32_t>() : nullptr;
     cp.pair_off = ctx->ws.pair_off.as<uint32_t>();
@@ -298,21 +305,22 @@ cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool upda
     cp.grads = grads_out;
     cp.m1 = m->m1.as<float>();
     cp.m2 = m->m2.as<float>();
-    cp.step = m->step.as<float>();
+    cp.step = m->step.as<StepRec>();
     if (adam_cfg) cp.adam = *reinterpret_cast<const AdamCfg*>(adam_cfg);
-    chain_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(cp);
+    chain_kernel<<<grid_for(i1 - i0, 256), 256, 0, ctx->stream>>>(cp);
     ctx->launches++;
     return cudaGetLastError();
 }
 
 cudaError_t launch_adam(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const float* adam_cfg,
-                        int batch_views) {
-    if (m->n == 0) return cudaSuccess;
+                        int batch_views, int64_t i0, int64_t i1) {
+    if (i1 < 0) i1 = m->n;
+    if (i1 <= i0) return cudaSuccess;
     AdamCfg c = *reinterpret_cast<const AdamCfg*>(adam_cfg);
     c.batch = (float)(batch_views > 0 ? batch_views : 1);
-    adam_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(
-        m->params.as<float>(), m->m1.as<float>(), m->m2.as<float>(), m->cap, m->n, grads,
-        grads ? nullptr : m->step.as<float>(), m->pos_acc.as<float>(), m->col_acc.as<float>(),
+    adam_kernel<<<grid_for(i1 - i0, 256), 256, 0, ctx->stream>>>(
+        m->params.as<float>(), m->m1.as<float>(), m->m2.as<float>(), m->cap, m->n, i0, i1, grads,
+        grads ? nullptr : m->step.as<StepRec>(), m->pos_acc.as<float>(), m->col_acc.as<float>(),
         m->accum.as<int32_t>(), m->visit.as<int64_t>(), m->window.as<int64_t>(), c);
     ctx->launches++;
     return cudaGetLastError();

@@ -461,7 +461,7 @@ struct Chain3Params {
     int32_t* visit;
     int update_stats;
     float* gbuf;    // [17][n] (mode 1): gradients 0..10, masked colour gradient, view direction
-    float* step;    // [62][cap] (mode 2): 59 gradient sums, position-norm sum, colour-norm sum, visits
+    float* step;    // [62][n] packed (mode 2): 59 gradient sums, position-norm sum, colour-norm sum, visits
 };
 
 // Gradients of one Gaussian from its merged screen-space sums s[0..8]: the 11 geometric /
@@ -644,15 +644,15 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
             float old[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                if (k0 + k < 59) old[k] = ST[(int64_t)(k0 + k) * cap + i];
+                if (k0 + k < 59) old[k] = ST[(int64_t)(k0 + k) * cp.n + i];
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                if (k0 + k < 59) ST[(int64_t)(k0 + k) * cap + i] = old[k] + grad(k0 + k);
+                if (k0 + k < 59) ST[(int64_t)(k0 + k) * cp.n + i] = old[k] + grad(k0 + k);
         }
         if (cp.update_stats && visited) {
-            ST[59 * cap + i] += pn;
-            ST[60 * cap + i] += cn;
-            ST[61 * cap + i] += 1.0f;
+            ST[59 * cp.n + i] += pn;
+            ST[60 * cp.n + i] += cn;
+            ST[61 * cp.n + i] += 1.0f;
         }
         return;
     }
@@ -758,7 +758,7 @@ __global__ void __launch_bounds__(256) adam3d_step_kernel(float* __restrict__ pa
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     auto grad = [&](int k) -> float {
-        float* p = step + (int64_t)k * cap + i;
+        float* p = step + (int64_t)k * n + i;  // packed [62][n]
         const float v = *p;
         *p = 0.f;
         return fdiv_pos(v, batch);
@@ -766,15 +766,15 @@ __global__ void __launch_bounds__(256) adam3d_step_kernel(float* __restrict__ pa
     switch (blockIdx.y) {
         case 0: {
             adam3d_chunk<0, 6>(params, m1, m2, cap, i, grad, c);
-            const float v = step[61 * cap + i];
+            const float v = step[61 * n + i];
             if (v > 0.f) {
-                pos_acc[i] += step[59 * cap + i];
-                col_acc[i] += step[60 * cap + i];
+                pos_acc[i] += step[59 * n + i];
+                col_acc[i] += step[60 * n + i];
                 visit[i] += (int32_t)v;
             }
-            step[59 * cap + i] = 0.f;
-            step[60 * cap + i] = 0.f;
-            step[61 * cap + i] = 0.f;
+            step[59 * n + i] = 0.f;
+            step[60 * n + i] = 0.f;
+            step[61 * n + i] = 0.f;
             break;
         }
         case 1: adam3d_chunk<6, 5>(params, m1, m2, cap, i, grad, c); break;

@@ -20,6 +20,13 @@ constexpr double kMinScale = 1e-4;        // gaussian.hpp:14
 constexpr double kRawCap = 12.0;          // gaussian.hpp:18
 constexpr int kParams = 9;                // optimised components per Gaussian
 constexpr int kStepFloats = 12;           // step buffer: 9 grads + pos norm + col norm + visits
+// One Gaussian's step-buffer record. The batched-view step buffer is AoS [n][12] floats (48 B per
+// Gaussian, rows in the model's physical order): any Gaussian range is one contiguous slice, so the
+// all-reduce moves exactly 48 n bytes and a bucket [i0, i1) of the chain -> all-reduce -> Adam
+// pipeline is one contiguous NCCL buffer.
+struct alignas(16) StepRec {
+    float4 a, b, c;  // (g0..g3), (g4..g7), (g8, pos norm, colour norm, visits)
+};
 
 // Kernel error word: (rank << 2) | code, lowest wins; all-ones = no error.
 constexpr unsigned long long kErrNone = ~0ull;

@@ -63,7 +63,7 @@ struct Workspace {
 namespace tgsx {
 // Live per-stage timing with CUDA events on the context stream (enabled by tgsx_profile).
 enum Stage { kStDepthSort, kStPreprocess, kStScan, kStDuplicate, kStSort, kStRanges,
-             kStForward, kStBackward, kStChain, kStLoss, kStDensify, kNumStages };
+             kStForward, kStBackward, kStChain, kStLoss, kStDensify, kStAdam, kNumStages };
 struct Profiler {
     bool enabled = false;
     std::vector<cudaEvent_t> pool;          // reusable events
@@ -109,6 +109,18 @@ struct tgsx_ctx {
     bool bin_pending = false;
     int bin_sort_cap = 0;           // longest list the speculative per-tile sort handled
     uint64_t bin_max_hint = 0;      // longest list of the previous binning
+    // blend backward launch configuration, per context (= per device): the dynamic shared-memory
+    // opt-in is a per-device function attribute and the resident-CTA count sizes the grid
+    int bwd_resident[2] = {0, 0};
+    // NCCL communicator of a view-sharded fit (comm.cpp; null = single rank) and its stream;
+    // events of the pipelined batched step (chain(b) -> all-reduce(b) -> Adam(b))
+    void* comm = nullptr;
+    int comm_ranks = 1, comm_rank = 0;
+    cudaStream_t comm_stream = nullptr;
+    std::vector<cudaEvent_t> pipe_events;
+    // pipeline timeline of the last profiled batched step: per bucket (chain start, chain end,
+    // all-reduce start, all-reduce end, Adam start, Adam end) in ms from the step's first event
+    std::vector<float> pipe_timeline;
 };
 
 // Scoped stage timer: no-op unless profiling is enabled.
@@ -137,7 +149,7 @@ struct tgsx_model {
     tgsx::DevBuf ids;      // u64[cap]
     tgsx::DevBuf pos_acc, col_acc, accum, visit, window, tau_v;
     tgsx::DevBuf m1, m2;   // float[9][cap] Adam moments
-    tgsx::DevBuf step;     // float[12][cap] batched-view step buffer
+    tgsx::DevBuf step;     // StepRec[cap] (AoS, 48 B/G) batched-view step buffer
     tgsx::DevBuf perm;     // u32[cap] rank -> index
     tgsx::DevBuf rank_of;  // u32[cap] index -> rank
     tgsx::DevBuf screen;   // float[10][cap] screen-space grads of the last backward
@@ -191,6 +203,9 @@ struct RenderArgs {
 };
 
 cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m);
+// NCCL (comm.cpp): in-place sum all-reduce of `count` floats on stream s; communicator teardown
+int32_t comm_allreduce_sum(tgsx_ctx* ctx, float* buf, size_t count, cudaStream_t s);
+void comm_release(tgsx_ctx* ctx);
 // d_total non-null: the pair-offset scan is fused in (rows must be in blend order): pair_off,
 // the records' first pair slot and the total pair count K are written by the same kernel
 cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H,
@@ -219,10 +234,11 @@ cudaError_t launch_ssim(tgsx_ctx* ctx, const float* rgb, const float* target, in
 cudaError_t launch_loss_finalize(tgsx_ctx* ctx, const float* l1_part, int n1, float w1, const float* s_part,
                                  int n2, float lam, double inv, float* out);
 enum class ChainMode { kGrads, kAdam, kAccumulate };
+// [i0, i1): the Gaussian rows of this launch (i1 < 0: up to n)
 cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool update_stats,
-                         float* grads_out, const float* adam_cfg);
+                         float* grads_out, const float* adam_cfg, int64_t i0 = 0, int64_t i1 = -1);
 cudaError_t launch_adam(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const float* adam_cfg,
-                        int batch_views);
+                        int batch_views, int64_t i0 = 0, int64_t i1 = -1);
 
 int key_bits_for(int tiles);
 

@@ -232,20 +232,36 @@ void trainer_write(const tgsx_trainer* tr, ByteWriter& w) {
     budget_write(tr->budget, w);
 }
 
-int32_t trainer_read(tgsx_trainer* tr, ByteReader& r) {
-    int64_t ring = 0;
-    if (!(r.get(tr->t) && r.get(tr->adam_step) && r.get(tr->n_init) && r.get(tr->fed) && r.get(tr->rng[0]) &&
-          r.get(tr->rng[1]) && r.get(tr->last_budget) && r.get(ring)))
+TrainerState::~TrainerState() {
+    if (budget) tgsx_budget_destroy(budget);
+}
+
+int32_t trainer_parse(const tgsx_trainer* tr, ByteReader& r, TrainerState& st) {
+    if (!(r.get(st.t) && r.get(st.adam_step) && r.get(st.n_init) && r.get(st.fed) && r.get(st.rng[0]) &&
+          r.get(st.rng[1]) && r.get(st.last_budget) && r.get(st.ring)))
         return TGSX_ERUNTIME;
-    if (ring != tr->ring) return TGSX_ERUNTIME;  // trainer created with another densify interval
-    std::vector<float> h((size_t)ring);
-    if (!r.bytes(h.data(), h.size() * sizeof(float))) return TGSX_ERUNTIME;
+    if (st.ring != tr->ring) return TGSX_ERUNTIME;  // trainer created with another densify interval
+    st.losses.resize((size_t)st.ring);
+    if (!r.bytes(st.losses.data(), st.losses.size() * sizeof(float))) return TGSX_ERUNTIME;
+    st.budget = budget_clone(tr->budget);
+    return budget_read(st.budget, r) ? TGSX_OK : TGSX_ERUNTIME;
+}
+
+int32_t trainer_commit(tgsx_trainer* tr, const TrainerState& st) {
     cudaStream_t s = (cudaStream_t)tgsx_get_stream(tr->ctx);
-    if (cudaMemcpyAsync(tr->d_losses, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, s) ||
+    if (cudaMemcpyAsync(tr->d_losses, st.losses.data(), sizeof(float) * st.losses.size(), cudaMemcpyHostToDevice, s) ||
         cudaStreamSynchronize(s))
         return TGSX_ECUDA;
-    std::memcpy(tr->h_pinned, h.data(), sizeof(float) * h.size());
-    return budget_read(tr->budget, r) ? TGSX_OK : TGSX_ERUNTIME;
+    std::memcpy(tr->h_pinned, st.losses.data(), sizeof(float) * st.losses.size());
+    tr->t = st.t;
+    tr->adam_step = st.adam_step;
+    tr->n_init = st.n_init;
+    tr->fed = st.fed;
+    tr->rng[0] = st.rng[0];
+    tr->rng[1] = st.rng[1];
+    tr->last_budget = st.last_budget;
+    budget_assign(tr->budget, st.budget);
+    return TGSX_OK;
 }
 
 }  // namespace tgsx

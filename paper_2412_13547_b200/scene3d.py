@@ -240,6 +240,13 @@ class DeviceModel3D:
         ptr = self.ctx.L.tgsx_step_buffer3d(self.h, C.byref(n))
         return int(ptr), int(n.value)
 
+    def step_layout(self):
+        """3-D rows stay in creation order on every rank: nothing to do (2-D API parity)."""
+
+    def allreduce_step(self):
+        """In-place sum of the packed [62][n] step buffer over the context's NCCL communicator."""
+        self.ctx.check(self.ctx.L.tgsx_allreduce_step3d(self.ctx.h, self.h))
+
     def apply_step(self, batch_views: int, step: int, total_steps: int, scene_extent: float):
         a = _lib.Adam3dArgs(step, total_steps, scene_extent)
         self.ctx.check(self.ctx.L.tgsx_apply_step3d(self.ctx.h, self.h, batch_views, C.byref(a)))

@@ -78,3 +78,36 @@ def test_corrupt_truncated_and_empty(P, ctx, tmp_path):
     assert dm.size() == 0
     dm.load_checkpoint(str(path))
     assert dm.size() == 200 and np.array_equal(dm.download().params[0], s.px)
+
+
+def test_load_is_atomic(P, ctx, tmp_path):
+    """A checkpoint whose trainer section is corrupt or truncated (or that has trailing bytes)
+    is rejected BEFORE the caller's model or trainer changes (the load validates the whole file
+    first)."""
+    W, H, n = 64, 48, 600
+    src = P.DeviceModel.from_host(model_from_scene(B.synthetic_scene(1, n, W, H)), ctx)
+    targets = [B.render(B.synthetic_scene(2, 500, W, H), 1, 0, 0, W, H)[0].reshape(H, W, 3)] * 2
+    tr = _trainer(P, src, W, H)
+    tr.set_targets(targets)
+    for _ in range(25):
+        tr.step()
+    path = tmp_path / "t.tgs"
+    src.save_checkpoint(str(path), tr)
+    data = path.read_bytes()
+    model_end = 24 + 156 * src.size() + 4
+    keep = B.synthetic_scene(5, 300, W, H)
+    dst = P.DeviceModel.from_host(model_from_scene(keep), ctx)
+    tr2 = _trainer(P, dst, W, H)
+    tr2.set_targets(targets)
+    tr2.step()
+    before = tr2.losses(1).copy()
+    px_before = dst.download().params[0].copy()
+    for blob in (data[:model_end + 20], data[:-3], data + b"\x01\x02"):
+        bad = tmp_path / "bad.tgs"
+        bad.write_bytes(blob)
+        with pytest.raises(RuntimeError):
+            dst.load_checkpoint(str(bad), tr2)
+        assert dst.size() == 300 and np.array_equal(dst.download().params[0], px_before)
+        assert np.array_equal(tr2.losses(1), before)
+    dst.load_checkpoint(str(path), tr2)
+    assert dst.size() == src.size()
