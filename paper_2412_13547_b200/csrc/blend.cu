@@ -119,6 +119,121 @@ __device__ __forceinline__ float2 pair_quad(const float4& a, float kc, float fx,
 }
 
 
+// One chunk (<= 32 staged records at cbase, list positions lbase-1 ...) of walk_pixel
+// (rasterizer.cpp:108-136) for the lane's two pixels of the 8x8 block (bx, by) of active pixels:
+// masks transposed (lane c < 16 holds the chunk's splats passing active column c, lane 16 + r
+// those passing row r; a pixel's pass set is column & row), then the union of the lane's two
+// pass sets front to back, two splats per iteration, packed FP32x2. Returns true when every
+// pixel of the warp has terminated.
+__device__ __forceinline__ bool walk_chunk(uint32_t cbase, int ccount, uint32_t lbase, int bx, int by, float fx,
+                                           float fyA, float fyB, float2& T, float2& C0, float2& C1, float2& C2,
+                                           uint32_t& lastA, uint32_t& lastB, uint32_t& ops, bool& doneA,
+                                           bool& doneB) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t bits = transpose32(lane < ccount ? __float_as_uint(lds_f1(cbase + lane * kRec + 36)) : 0u);
+    const uint32_t X = __shfl_sync(kFull, bits, bx * 8 + (lane & 7));
+    uint32_t colA = X & __shfl_sync(kFull, bits, 16 + by * 8 + 2 * (lane >> 3));
+    uint32_t colB = X & __shfl_sync(kFull, bits, 17 + by * 8 + 2 * (lane >> 3));
+    if (doneA) colA = 0;
+    if (doneB) colB = 0;
+    const uint32_t colA0 = colA, colB0 = colB;
+    int termA = 32, termB = 32;  // bit of each pixel's terminating blend, 32 = none
+    uint32_t colU = colA | colB;
+    // branch-free: a lane whose walk is over runs on record 0 with both pixels masked
+    // (sigma = 0 changes nothing)
+    // Two splats (k1 < k2) per iteration: their Gaussians are independent (ILP), the
+    // blends are applied in order and a ray that terminates at k1 does not blend k2.
+    while (__any_sync(kFull, colU)) {
+        const int k1 = colU ? __ffs(colU) - 1 : 0;
+        const uint32_t bit1 = colU ? 1u << k1 : 0u;
+        const uint32_t rem = colU & ~bit1;
+        const int k2 = rem ? __ffs(rem) - 1 : 0;
+        const uint32_t bit2 = rem ? 1u << k2 : 0u;
+        const bool hA1 = (colA & bit1) != 0u, hB1 = (colB & bit1) != 0u;
+        const bool hA2 = (colA & bit2) != 0u, hB2 = (colB & bit2) != 0u;
+        const uint32_t ad1 = cbase + k1 * kRec, ad2 = cbase + k2 * kRec;
+        const float4 a1 = lds_f4(ad1), b1 = lds_f4(ad1 + 16);
+        const float4 a2 = lds_f4(ad2), b2 = lds_f4(ad2 + 16);
+        const float cz1 = lds_f1(ad1 + 32), cz2 = lds_f1(ad2 + 32);
+        const float2 q1 = pair_quad(a1, b1.x, fx, fyA, fyB);
+        const float2 q2 = pair_quad(a2, b2.x, fx, fyA, fyB);
+        const float2 e1 = make_float2(fast_exp2(q1.x), fast_exp2(q1.y));
+        const float2 e2 = make_float2(fast_exp2(q2.x), fast_exp2(q2.y));
+        // a pixel that does not pass the splat gets sigma = 0 (T, colour unchanged)
+        const float2 s1 = make_float2(hA1 ? __fmul_rn(b1.y, e1.x) : 0.f, hB1 ? __fmul_rn(b1.y, e1.y) : 0.f);
+        const float2 w1 = __fmul2_rn(s1, T);
+        // 1 - sigma with one rounding, exactly as the scalar subtraction
+        T = __fmul2_rn(T, __ffma2_rn(s1, make_float2(-1.0f, -1.0f), make_float2(1.0f, 1.0f)));
+        C0 = __ffma2_rn(w1, make_float2(b1.z, b1.z), C0);
+        C1 = __ffma2_rn(w1, make_float2(b1.w, b1.w), C1);
+        C2 = __ffma2_rn(w1, make_float2(cz1, cz1), C2);
+        const bool tA1 = hA1 && T.x < kTermT, tB1 = hB1 && T.y < kTermT;  // ray ends at k1
+        const bool gA2 = hA2 && !tA1, gB2 = hB2 && !tB1;
+        const float2 s2 = make_float2(gA2 ? __fmul_rn(b2.y, e2.x) : 0.f, gB2 ? __fmul_rn(b2.y, e2.y) : 0.f);
+        const float2 w2 = __fmul2_rn(s2, T);
+        T = __fmul2_rn(T, __ffma2_rn(s2, make_float2(-1.0f, -1.0f), make_float2(1.0f, 1.0f)));
+        C0 = __ffma2_rn(w2, make_float2(b2.z, b2.z), C0);
+        C1 = __ffma2_rn(w2, make_float2(b2.w, b2.w), C1);
+        C2 = __ffma2_rn(w2, make_float2(cz2, cz2), C2);
+        const bool tA2 = gA2 && T.x < kTermT, tB2 = gB2 && T.y < kTermT;
+        colA &= ~(bit1 | bit2);
+        colB &= ~(bit1 | bit2);
+        if (tA1 || tA2) {  // ray A terminates (break after blending)
+            termA = tA1 ? k1 : k2;
+            colA = 0;
+        }
+        if (tB1 || tB2) {
+            termB = tB1 ? k1 : k2;
+            colB = 0;
+        }
+        colU = colA | colB;
+    }
+    if (colA0) {
+        const uint32_t used = termA < 32 ? (colA0 & (kFull >> (31 - termA))) : colA0;
+        ops += __popc(used);
+        lastA = lbase + 31 - __clz(used);
+        if (termA < 32) doneA = true;
+    }
+    if (colB0) {
+        const uint32_t used = termB < 32 ? (colB0 & (kFull >> (31 - termB))) : colB0;
+        ops += __popc(used);
+        lastB = lbase + 31 - __clz(used);
+        if (termB < 32) doneB = true;
+    }
+    return __all_sync(kFull, doneA && doneB);
+}
+
+// Pixel epilogue of walk_pixel / render (rasterizer.cpp:131-133, 180-182): background term,
+// outputs by dense rank, evaluation count, fused L1 value and dL/dC.
+__device__ __forceinline__ void finish_pixel(const BlendParams& prm, bool valid, int x, int y, float Tp, float c0,
+                                             float c1, float c2, uint32_t last, bool done, int count,
+                                             unsigned long long& ev, float& lsum) {
+    if (!valid) return;
+    const int p = prm.p;
+    c0 = __fmaf_rn(Tp, prm.bg0, c0);
+    c1 = __fmaf_rn(Tp, prm.bg1, c1);
+    c2 = __fmaf_rn(Tp, prm.bg2, c2);
+    const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
+    if (prm.rgb) {
+        prm.rgb[3 * r] = c0;
+        prm.rgb[3 * r + 1] = c1;
+        prm.rgb[3 * r + 2] = c2;
+    }
+    prm.T[r] = Tp;
+    prm.last[r] = last;
+    ev += done ? last : (uint32_t)count;
+    if (prm.target) {
+        const int ty = prm.target_rows > 1 ? (y - prm.oy) / prm.target_rows : y;  // staged rows only
+        const float* tg = prm.target + 3 * ((int64_t)ty * prm.W + x);
+        const float d0 = c0 - tg[0], d1 = c1 - tg[1], d2 = c2 - tg[2];
+        lsum += fabsf(d0) + fabsf(d1) + fabsf(d2);
+        const float sc = prm.loss_scale;
+        prm.dLdC[3 * r] = d0 > 0.f ? sc : (d0 < 0.f ? -sc : 0.f);
+        prm.dLdC[3 * r + 1] = d1 > 0.f ? sc : (d1 < 0.f ? -sc : 0.f);
+        prm.dLdC[3 * r + 2] = d2 > 0.f ? sc : (d2 < 0.f ? -sc : 0.f);
+    }
+}
+
 // One CTA per tile, one warp per 8x8 block of active pixels, TWO vertically adjacent pixels per
 // lane (rows 2r and 2r+1 of the block). The lane walks the union of its two pixels' passing
 // splats front to back; the two Gaussians / blends of a splat run as packed FP32x2 (FMUL2 /
@@ -170,82 +285,8 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_pairs_kernel(BlendPara
         __syncthreads();
         if (warp_done) continue;
         for (int c0 = 0; c0 < bcount; c0 += 32) {
-            const int j = c0 + lane;
-            // masks transposed: lane c < 16 holds the chunk's splats passing active column c,
-            // lane 16 + r those passing row r; a pixel's pass set is column & row
-            const uint32_t bits = transpose32(j < bcount ? __float_as_uint(lds_f1(sbase + j * kRec + 36)) : 0u);
-            const uint32_t X = __shfl_sync(kFull, bits, bx * 8 + (lane & 7));
-            uint32_t colA = X & __shfl_sync(kFull, bits, 16 + by * 8 + 2 * (lane >> 3));
-            uint32_t colB = X & __shfl_sync(kFull, bits, 17 + by * 8 + 2 * (lane >> 3));
-            if (doneA) colA = 0;
-            if (doneB) colB = 0;
-            const uint32_t colA0 = colA, colB0 = colB;
-            const uint32_t cbase = sbase + c0 * kRec;
-            const uint32_t lbase = (uint32_t)(bstart + c0 + 1);
-            int termA = 32, termB = 32;  // bit of each pixel's terminating blend, 32 = none
-            uint32_t colU = colA | colB;
-            // branch-free: a lane whose walk is over runs on record 0 with both pixels masked
-            // (sigma = 0 changes nothing)
-            // Two splats (k1 < k2) per iteration: their Gaussians are independent (ILP), the
-            // blends are applied in order and a ray that terminates at k1 does not blend k2.
-            while (__any_sync(kFull, colU)) {
-                const int k1 = colU ? __ffs(colU) - 1 : 0;
-                const uint32_t bit1 = colU ? 1u << k1 : 0u;
-                const uint32_t rem = colU & ~bit1;
-                const int k2 = rem ? __ffs(rem) - 1 : 0;
-                const uint32_t bit2 = rem ? 1u << k2 : 0u;
-                const bool hA1 = (colA & bit1) != 0u, hB1 = (colB & bit1) != 0u;
-                const bool hA2 = (colA & bit2) != 0u, hB2 = (colB & bit2) != 0u;
-                const uint32_t ad1 = cbase + k1 * kRec, ad2 = cbase + k2 * kRec;
-                const float4 a1 = lds_f4(ad1), b1 = lds_f4(ad1 + 16);
-                const float4 a2 = lds_f4(ad2), b2 = lds_f4(ad2 + 16);
-                const float cz1 = lds_f1(ad1 + 32), cz2 = lds_f1(ad2 + 32);
-                const float2 q1 = pair_quad(a1, b1.x, fx, fyA, fyB);
-                const float2 q2 = pair_quad(a2, b2.x, fx, fyA, fyB);
-                const float2 e1 = make_float2(fast_exp2(q1.x), fast_exp2(q1.y));
-                const float2 e2 = make_float2(fast_exp2(q2.x), fast_exp2(q2.y));
-                // a pixel that does not pass the splat gets sigma = 0 (T, colour unchanged)
-                const float2 s1 = make_float2(hA1 ? __fmul_rn(b1.y, e1.x) : 0.f, hB1 ? __fmul_rn(b1.y, e1.y) : 0.f);
-                const float2 w1 = __fmul2_rn(s1, T);
-                // 1 - sigma with one rounding, exactly as the scalar subtraction
-                T = __fmul2_rn(T, __ffma2_rn(s1, make_float2(-1.0f, -1.0f), make_float2(1.0f, 1.0f)));
-                C0 = __ffma2_rn(w1, make_float2(b1.z, b1.z), C0);
-                C1 = __ffma2_rn(w1, make_float2(b1.w, b1.w), C1);
-                C2 = __ffma2_rn(w1, make_float2(cz1, cz1), C2);
-                const bool tA1 = hA1 && T.x < kTermT, tB1 = hB1 && T.y < kTermT;  // ray ends at k1
-                const bool gA2 = hA2 && !tA1, gB2 = hB2 && !tB1;
-                const float2 s2 = make_float2(gA2 ? __fmul_rn(b2.y, e2.x) : 0.f, gB2 ? __fmul_rn(b2.y, e2.y) : 0.f);
-                const float2 w2 = __fmul2_rn(s2, T);
-                T = __fmul2_rn(T, __ffma2_rn(s2, make_float2(-1.0f, -1.0f), make_float2(1.0f, 1.0f)));
-                C0 = __ffma2_rn(w2, make_float2(b2.z, b2.z), C0);
-                C1 = __ffma2_rn(w2, make_float2(b2.w, b2.w), C1);
-                C2 = __ffma2_rn(w2, make_float2(cz2, cz2), C2);
-                const bool tA2 = gA2 && T.x < kTermT, tB2 = gB2 && T.y < kTermT;
-                colA &= ~(bit1 | bit2);
-                colB &= ~(bit1 | bit2);
-                if (tA1 || tA2) {  // ray A terminates (break after blending)
-                    termA = tA1 ? k1 : k2;
-                    colA = 0;
-                }
-                if (tB1 || tB2) {
-                    termB = tB1 ? k1 : k2;
-                    colB = 0;
-                }
-                colU = colA | colB;
-            }
-            if (colA0) {
-                const uint32_t used = termA < 32 ? (colA0 & (kFull >> (31 - termA))) : colA0;
-                ops += __popc(used);
-                lastA = lbase + 31 - __clz(used);
-                if (termA < 32) doneA = true;
-            }
-            if (colB0) {
-                const uint32_t used = termB < 32 ? (colB0 & (kFull >> (31 - termB))) : colB0;
-                ops += __popc(used);
-                lastB = lbase + 31 - __clz(used);
-                if (termB < 32) doneB = true;
-            }
-            if (__all_sync(kFull, doneA && doneB)) {
+            if (walk_chunk(sbase + c0 * kRec, min(32, bcount - c0), (uint32_t)(bstart + c0 + 1), bx, by,
+                           fx, fyA, fyB, T, C0, C1, C2, lastA, lastB, ops, doneA, doneB)) {
                 warp_done = true;
                 break;
             }
@@ -254,33 +295,8 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_pairs_kernel(BlendPara
 
     float lsum = 0.f;
     unsigned long long ev = 0;
-    auto finish = [&](bool valid, int y, float Tp, float c0, float c1, float c2, uint32_t last, bool done) {
-        if (!valid) return;
-        c0 = __fmaf_rn(Tp, prm.bg0, c0);
-        c1 = __fmaf_rn(Tp, prm.bg1, c1);
-        c2 = __fmaf_rn(Tp, prm.bg2, c2);
-        const int r = ((y - prm.oy) / p) * prm.cols + (x - prm.ox) / p;
-        if (prm.rgb) {
-            prm.rgb[3 * r] = c0;
-            prm.rgb[3 * r + 1] = c1;
-            prm.rgb[3 * r + 2] = c2;
-        }
-        prm.T[r] = Tp;
-        prm.last[r] = last;
-        ev += done ? last : (uint32_t)count;
-        if (prm.target) {
-            const int ty = prm.target_rows > 1 ? (y - prm.oy) / prm.target_rows : y;  // staged rows only
-            const float* tg = prm.target + 3 * ((int64_t)ty * prm.W + x);
-            const float d0 = c0 - tg[0], d1 = c1 - tg[1], d2 = c2 - tg[2];
-            lsum += fabsf(d0) + fabsf(d1) + fabsf(d2);
-            const float sc = prm.loss_scale;
-            prm.dLdC[3 * r] = d0 > 0.f ? sc : (d0 < 0.f ? -sc : 0.f);
-            prm.dLdC[3 * r + 1] = d1 > 0.f ? sc : (d1 < 0.f ? -sc : 0.f);
-            prm.dLdC[3 * r + 2] = d2 > 0.f ? sc : (d2 < 0.f ? -sc : 0.f);
-        }
-    };
-    finish(vA, yA, T.x, C0.x, C1.x, C2.x, lastA, doneA);
-    finish(vB, yB, T.y, C0.y, C1.y, C2.y, lastB, doneB);
+    finish_pixel(prm, vA, x, yA, T.x, C0.x, C1.x, C2.x, lastA, doneA, count, ev, lsum);
+    finish_pixel(prm, vB, x, yB, T.y, C0.y, C1.y, C2.y, lastB, doneB, count, ev, lsum);
     unsigned long long o = ops;
 #pragma unroll
     for (int sft = 16; sft > 0; sft >>= 1) {
@@ -318,6 +334,12 @@ __device__ __forceinline__ uint32_t pair_slot(const Prepared& P, int tx, int ty)
 }
 
 constexpr int kSubRows = 16;  // union rows per phase-1 / phase-2 round
+
+#ifdef TGSX_BWD_STATS
+// debug build only (A/B experiments): [0] group-chunks with work, [1] padded rows, [2] blended
+// (splat, pixel) pairs, [3] U0 + U1, [4] phase-2 rounds, [5] chunks
+__device__ unsigned long long g_bwd_stats[16];
+#endif
 
 // Per-warp shared memory of the backward. Pixel layout of an 8x8 group: lane l owns the two
 // vertically adjacent pixels (col l&7, rows 2(l>>3), 2(l>>3)+1) = pixel slots 2l (A), 2l+1 (B).
@@ -508,6 +530,9 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
         // masks transposed: lane c < 16 holds the chunk's splats passing active column c, lane
         // 16 + r those passing row r (rasterizer.cpp:116-118); a pixel's pass set is column & row
         const uint32_t bits = transpose32(__float_as_uint(lds_f1(myrec + 36)));
+#ifdef TGSX_BWD_STATS
+        if (lane == 0) atomicAdd(&g_bwd_stats[5], 1ull);
+#endif
         float m0 = 0.f, mx1 = 0.f, my1 = 0.f, mxx = 0.f, mxy = 0.f, myy = 0.f;
         float q0 = 0.f, q1 = 0.f, q2 = 0.f;
         uint32_t vism = 0;
@@ -522,6 +547,9 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
             const uint32_t X = __shfl_sync(kFull, bits, gx * 8 + cxl);
             uint32_t colA = X & __shfl_sync(kFull, bits, 16 + gy * 8 + ryl);
             uint32_t colB = X & __shfl_sync(kFull, bits, 17 + gy * 8 + ryl);
+#ifdef TGSX_BWD_STATS
+            const uint32_t boxA = colA, boxB = colB;
+#endif
             cp_async_wait<1>();
             __syncwarp();
             const uint32_t lgc = lgbase + 1024u * (uint32_t)cur + 8u * (uint32_t)lane;
@@ -543,6 +571,35 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
             // rows are visited in pairs: an odd count is padded with a filler row (each half then
             // has a splat outside its union, as U <= 31)
             const int U = (max(U0, U1) + 1) & ~1;
+#ifdef TGSX_BWD_STATS
+            {
+                const unsigned nb = __reduce_add_sync(kFull, (unsigned)(__popc(colA) + __popc(colB)));
+                if (lane == 0) {
+                    atomicAdd(&g_bwd_stats[0], 1ull);
+                    atomicAdd(&g_bwd_stats[1], (unsigned long long)U);
+                    atomicAdd(&g_bwd_stats[2], (unsigned long long)nb);
+                    atomicAdd(&g_bwd_stats[3], (unsigned long long)(U0 + U1));
+                    atomicAdd(&g_bwd_stats[4], (unsigned long long)((U + kSubRows - 1) / kSubRows));
+                }
+                // [6] box-only blends (termination ignored; invalid pixels have T = 1 and are
+                // never limited, so count only lanes whose pixels are valid via lastp != 0)
+                const unsigned nbox = __reduce_add_sync(kFull, (unsigned)(__popc(boxA) + __popc(boxB)));
+                // [7] rows if 4x4 quarters (lanes {0-3, 8-11} etc.) ran in lockstep
+                uint32_t q = cu;
+                q |= __shfl_xor_sync(kFull, q, 1);
+                q |= __shfl_xor_sync(kFull, q, 2);
+                q |= __shfl_xor_sync(kFull, q, 8);
+                const unsigned qmax = __reduce_max_sync(kFull, (unsigned)__popc(q));
+                const unsigned lmax = __reduce_max_sync(kFull, (unsigned)__popc(cu));
+                const unsigned lsum = __reduce_add_sync(kFull, (unsigned)__popc(cu));
+                if (lane == 0) {
+                    atomicAdd(&g_bwd_stats[8], (unsigned long long)lmax);
+                    atomicAdd(&g_bwd_stats[9], (unsigned long long)lsum);
+                    atomicAdd(&g_bwd_stats[6], (unsigned long long)nbox);
+                    atomicAdd(&g_bwd_stats[7], (unsigned long long)qmax);
+                }
+            }
+#endif
             const float2 g0p = lds_f2(lgc + 256), g1p = lds_f2(lgc + 512), g2p = lds_f2(lgc + 768);
             const float4 st = S.st[g][lane];
             float2 T = make_float2(st.x, st.z), gS = make_float2(st.y, st.w);
@@ -756,6 +813,15 @@ cudaError_t run_backward(tgsx_ctx* ctx, const BlendParams& prm) {
 
 }  // namespace
 
+#ifdef TGSX_BWD_STATS
+extern "C" int tgsx_debug_bwd_stats(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_bwd_stats, sizeof(unsigned long long) * 16);
+    unsigned long long z[16] = {};
+    return (int)cudaMemcpyToSymbol(g_bwd_stats, z, sizeof(z));
+}
+#endif
+
 cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items,
                            bool fused_loss) {
     BlendParams prm = make_params(ctx, ra, items);
@@ -770,7 +836,7 @@ cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* 
     const unsigned tiles = (unsigned)prm.tiles;
     if (ra.p == 1) {
         forward_pairs_kernel<2, 2, 256><<<tiles, 128, 0, ctx->stream>>>(prm);
-    } else {
+    } else {  // dilated: a tile's <= 8x8 active pixels are one warp's block
         forward_pairs_kernel<1, 1, 32><<<tiles, 32, 0, ctx->stream>>>(prm);
     }
     ctx->launches++;
