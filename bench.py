@@ -493,12 +493,14 @@ def measure(args, name, env):
         loss_dev = torch.zeros(1, device="cuda")
         torch.cuda.synchronize()
 
-        def one_step(it, tptr, lptr):
+        def one_step(it, tptr, lptr, graph=False):
             ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
             pat = P.DilationPattern(p, ox, oy, W, H).c()
             a = P._lib.AdamArgs(it + 1, 10000, diag)
             if world == 1:
-                ctx.check(ctx.L.tgsx_fit_step(ctx.h, dm.h, C.byref(pat), bg, tptr, C.byref(a), lptr))
+                # graph: the step replayed from a CUDA graph (one launch; verified a step behind)
+                fit = ctx.L.tgsx_fit_graph_step if graph else ctx.L.tgsx_fit_step
+                ctx.check(fit(ctx.h, dm.h, C.byref(pat), bg, tptr, C.byref(a), lptr))
             else:
                 # one view per rank: chain -> NCCL all-reduce -> Adam pipelined over 4 buckets
                 tp = (C.c_void_p * 1)(tptr)
@@ -506,11 +508,19 @@ def measure(args, name, env):
                                                   lptr, args.buckets))
 
         tptr, lptr = C.c_void_p(target.data_ptr()), C.c_void_p(loss_dev.data_ptr())
-        step_fn = lambda it: one_step(it, tptr, lptr)  # noqa: E731
+        use_graph = world == 1 and not args.no_graph
+        step_fn = lambda it: one_step(it, tptr, lptr, use_graph)  # noqa: E731
+        extra["eager_fn"] = (lambda it: one_step(it, tptr, lptr)) if use_graph else None  # noqa: E731
         views_per_step = world
         h_target = target.cpu().pin_memory()
         h_loss = torch.zeros(1).pin_memory()
-        e2e_fn = lambda it: one_step(it, C.c_void_p(h_target.data_ptr()), C.c_void_p(h_loss.data_ptr()))  # noqa: E731
+        # host targets: the eager step stages the H2D copy on a copy stream overlapping the
+        # previous step's kernels; the graph copies inside the step (no overlap): measured slower
+        # end to end even at C1 (6.2k vs 7.5k it/s), so the host path is the eager step
+        e2e_graph = False
+        e2e_fn = lambda it: one_step(it, C.c_void_p(h_target.data_ptr()), C.c_void_p(h_loss.data_ptr()), e2e_graph)  # noqa: E731
+        extra["api"] = {"value": "tgsx_fit_graph_step" if use_graph else "tgsx_fit_step",
+                        "e2e": "tgsx_fit_graph_step" if e2e_graph else "tgsx_fit_step"}
         # a dilated view stages only its active rows of the host target (1/p of the image)
         e2e_bytes = (W * ((H + p - 1) // p) * 12, 4)
         units = world  # views per step over all ranks
@@ -586,6 +596,10 @@ def measure(args, name, env):
         ms = timer.run(step_fn, steps, warmup, ctx, flush=small)
     launches = ctx.launches - launches0
     counters = ctx.counters()
+    eager_ms = None
+    if extra.get("eager_fn"):  # the same steps through the eager tgsx_fit_step, for comparison
+        restart()
+        eager_ms = timer.run(extra["eager_fn"], steps, warmup, ctx, flush=small)
     # per-stage CUDA-event timing in a separate run (the event records and their readback add
     # host work between the launches, so they stay out of the timed region above)
     prof_steps = min(steps, 20)
@@ -638,6 +652,13 @@ def measure(args, name, env):
             "roofline": roofline(stages, counters, clocks, n, name, fp32_meas),
             "stages_ms_per_step": {k: v[0] / prof_steps for k, v in stages.items() if v[1]},
             "counters": counters}
+    if "api" in extra:
+        line["config"]["api"] = extra["api"]
+        if extra["api"]["value"] == "tgsx_fit_graph_step":
+            caps, replays, reruns = ctx.graph_stats()
+            line["config"]["graph"] = {"captures": caps, "replays": replays, "eager_reruns": reruns}
+    if eager_ms is not None:
+        line["eager_value"] = units * steps / (eager_ms / 1e3)  # same steps, eager tgsx_fit_step
     if e2e_ms is not None:
         line["e2e"] = {"value": units * steps / (e2e_ms / 1e3), "unit": "iters/s",
                        "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1]}
@@ -692,6 +713,8 @@ def main():
     ap.add_argument("--impl", default="tgsx", choices=["tgsx", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time the eager tgsx_fit_step instead of the CUDA-graph replayed step")
     ap.add_argument("--no-subrecords", action="store_true",
                     help="default config only (skip the nested C1 / C3 / C5 records)")
     ap.add_argument("--ssim", type=float, default=0.0,

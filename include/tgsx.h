@@ -156,6 +156,20 @@ int32_t tgsx_set_binning(tgsx_ctx* ctx, int32_t mode);
  * Equivalent to render + L1 + backward + tgsx_adam_step with the same args. */
 int32_t tgsx_fit_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
                       const float* target, const tgsx_adam_args* a, float* out_loss);
+/* tgsx_fit_step replayed from a CUDA graph: the first call with a given model
+ * / pattern / background / target / loss pointer runs eagerly and captures the step; later
+ * calls launch the graph (one launch, no host wait) with this call's Adam arguments. The
+ * binning capacities are frozen at capture and checked on the device; a step that exceeds them
+ * (or raises a kernel error) and its successor are re-run eagerly, so the model sequence is
+ * exactly that of tgsx_fit_step. Steps are verified one call behind: errors of a replayed step
+ * are returned by a later call (this, tgsx_synchronize or any call that touches the model), and
+ * target / *out_loss must be device or pinned host memory that stays unchanged until the call
+ * after next returns (other targets run eagerly). Not used while profiling is enabled. */
+int32_t tgsx_fit_graph_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
+                            const float* target, const tgsx_adam_args* a, float* out_loss);
+/* Graph statistics: captures, replayed launches, eager re-runs after a device-side fault. */
+int32_t tgsx_fit_graph_stats(const tgsx_ctx* ctx, uint64_t* out_captures, uint64_t* out_replays,
+                             uint64_t* out_reruns);
 
 /* Batched views (SPEC.md:269-277 accumulate; multi-GPU view sharding):
  * tgsx_view_accumulate adds one view's gradients and densify-stat increments into the

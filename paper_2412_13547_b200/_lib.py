@@ -98,6 +98,8 @@ SIGNATURES = {
                                   C.c_int32]),
     "tgsx_adam_step": (C.c_int32, [vp, vp, vp, P(AdamArgs)]),
     "tgsx_fit_step": (C.c_int32, [vp, vp, P(Pattern), f32p, vp, P(AdamArgs), vp]),
+    "tgsx_fit_graph_step": (C.c_int32, [vp, vp, P(Pattern), f32p, vp, P(AdamArgs), vp]),
+    "tgsx_fit_graph_stats": (C.c_int32, [vp, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]),
     "tgsx_loss": (C.c_int32, [vp, P(Pattern), vp, vp, C.c_float, vp, vp]),
     "tgsx_set_ssim_weight": (C.c_int32, [vp, C.c_float]),
     "tgsx_set_binning": (C.c_int32, [vp, C.c_int32]),

@@ -309,6 +309,12 @@ class Context:
         self.check(self.L.tgsx_profile_read(self.h, ms, cnt, n))
         return {s: (ms[i], cnt[i]) for i, s in enumerate(self.STAGES)}
 
+    def graph_stats(self):
+        """(captures, replayed launches, eager re-runs) of tgsx_fit_graph_step on this context."""
+        c, r, e = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.check(self.L.tgsx_fit_graph_stats(self.h, C.byref(c), C.byref(r), C.byref(e)))
+        return c.value, r.value, e.value
+
     def counters(self):
         ops, ev, pairs = C.c_uint64(), C.c_uint64(), C.c_uint64()
         self.check(self.L.tgsx_stage_counters(self.h, C.byref(ops), C.byref(ev), C.byref(pairs)))
@@ -443,6 +449,18 @@ class DeviceModel:
         self.ctx.check(self.ctx.L.tgsx_fit_step(self.ctx.h, self.h, C.byref(pattern.c()), bg, tp,
                                                 C.byref(a), _ptr(loss)))
         return float(loss[0])
+
+    def fit_graph_step(self, pattern: DilationPattern, background, target: int, step: int,
+                       total_steps: int, image_diagonal: float, loss_ptr: int = 0):
+        """fit_step replayed from a CUDA graph (tgsx_fit_graph_step): `target` and `loss_ptr`
+        are device (or pinned host) pointers that stay valid for two further steps; the loss is
+        written there in stream order. Errors of a replayed step surface one call later (or at
+        Context.synchronize)."""
+        a = _lib.AdamArgs(step, total_steps, image_diagonal)
+        bg = (C.c_float * 3)(*background)
+        self.ctx.check(self.ctx.L.tgsx_fit_graph_step(self.ctx.h, self.h, C.byref(pattern.c()), bg,
+                                                      C.c_void_p(target), C.byref(a),
+                                                      C.c_void_p(loss_ptr) if loss_ptr else None))
 
     def view_accumulate(self, pattern: DilationPattern, background, target) -> float:
         bg = (C.c_float * 3)(*background)

@@ -62,6 +62,11 @@ struct BlendParams {
     float loss_scale;
     Partials partial;              // backward output, one entry per pair slot
     unsigned int* tile_queue;      // backward: next tile to take (zeroed before the launch)
+    // graph-replayed steps (graph.cpp): the backward checks the binning counters against the
+    // capacities the graph was captured with; a violation (or a kernel error) sets *fault, which
+    // turns this and every later replayed step into a no-op until the host re-runs them eagerly
+    unsigned* fault;
+    uint32_t guard_pairs, guard_list;
 };
 
 struct TileGeo {
@@ -745,6 +750,15 @@ __global__ void __launch_bounds__(kWPB * 32, TGSX_BWD_MINB) backward_kernel(Blen
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto& S = reinterpret_cast<BwdWarpSmem<NG>*>(smem_raw)[warp];
+    if (prm.fault) {
+        const unsigned long long* c = prm.counters;
+        const bool bad = *reinterpret_cast<const volatile unsigned*>(prm.fault) != 0u || c[0] != kErrNone ||
+                         (c[3] & 0xffffffffull) > prm.guard_pairs || c[5] > prm.guard_list;
+        if (bad) {
+            if (threadIdx.x == 0) atomicOr(prm.fault, 1u);
+            return;
+        }
+    }
     for (;;) {
         int tile = 0;
         if (lane == 0) tile = (int)atomicAdd(prm.tile_queue, 1u);
@@ -781,6 +795,11 @@ BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* ite
     prm.partial = Partials::at(ws.partial.p, ws.pair_cap);
     // counters slot 7 (u32): the backward's tile queue
     prm.tile_queue = reinterpret_cast<unsigned int*>(ws.counters.as<unsigned long long>() + 7);
+    if (ctx->graph_capturing) {
+        prm.fault = ctx->graph_fault;
+        prm.guard_pairs = (uint32_t)std::min<int64_t>(std::min(ws.pair_cap, ctx->graph_guard_pairs), 0xffffffffll);
+        prm.guard_list = (uint32_t)ctx->bin_sort_cap;
+    }
     return prm;
 }
 

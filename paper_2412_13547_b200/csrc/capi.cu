@@ -357,7 +357,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
                        ctx->stream));
     if (defer && !sorted_keys && !force_onesweep(ctx) && !debug_checks()) {
         if (!ctx->bin_event) CK(cudaEventCreateWithFlags(&ctx->bin_event, cudaEventDisableTiming));
-        CK(cudaEventRecord(ctx->bin_event, ctx->stream));
+        if (!ctx->graph_capturing) CK(cudaEventRecord(ctx->bin_event, ctx->stream));
         const uint64_t guess = std::min<uint64_t>(kSegCap, ctx->bin_max_hint + ctx->bin_max_hint / 4);
         int32_t rc = slab_sort(ctx, tiles, guess);
         if (rc) return rc;
@@ -395,6 +395,9 @@ int32_t bin_settle(tgsx_ctx* ctx, tgsx_model* m, int W, int H, uint32_t** items,
     *redo = false;
     if (!ctx->bin_pending) return TGSX_OK;
     ctx->bin_pending = false;
+    // a captured step never waits on the host: the backward checks the counters against the
+    // capture-time capacities on the device (graph.cpp)
+    if (ctx->graph_capturing) return TGSX_OK;
     Workspace& ws = ctx->ws;
     CK(cudaEventSynchronize(ctx->bin_event));
     int32_t rc = check_kernel_error(ctx, ws.h_scratch[0]);
@@ -565,6 +568,15 @@ void fill_adam(AdamCfg& c, const tgsx_adam_args* a) {
     c.batch = 1.0f;
 }
 
+}  // namespace
+
+void tgsx::adam_cfg_from_args(AdamCfg& c, const tgsx_adam_args* a) { fill_adam(c, a); }
+bool tgsx::graph_eligible_binning(const tgsx_ctx* ctx) {
+    return !force_onesweep(ctx) && !debug_checks() && ctx->bin_max_hint <= (uint64_t)kSegCap;
+}
+
+namespace {
+
 bool is_device_ptr(const void* p) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -611,6 +623,21 @@ int32_t stage_target(tgsx_ctx* ctx, const float* src, size_t bytes, const float*
     const bool rows_only = ra && ra->p > 1 && ra->rows > 0;
     const size_t row_bytes = ra ? (size_t)ra->W * 12 : 0;
     if (rows_only) bytes = row_bytes * (size_t)ra->rows;
+    if (ctx->graph_capturing) {
+        // a graph-replayed step copies its (pinned) host target on the compute stream into the
+        // workspace (sized before the capture): the copy is a node of the step's graph
+        DevBuf& b = ctx->ws.target;
+        if (b.bytes < bytes) CK(b.ensure(bytes));
+        if (rows_only) {
+            CK(cudaMemcpy2DAsync(b.p, row_bytes, src + (size_t)ra->oy * ra->W * 3, row_bytes * (size_t)ra->p,
+                                 row_bytes, (size_t)ra->rows, cudaMemcpyHostToDevice, ctx->stream));
+            ra->target_rows = ra->p;
+        } else {
+            CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        *out = b.as<float>();
+        return TGSX_OK;
+    }
     if (!ctx->copy_stream) {
         CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         for (int i = 0; i < 2; ++i) {
@@ -682,6 +709,7 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
     int32_t rc = check_pattern(ctx, pat);
     if (rc) return rc;
     if (!target) return fail(ctx, TGSX_EINVAL, "target is null");
+    if (!ctx->graph_capturing && !ctx->graph_replaying && (rc = graph_flush(ctx))) return rc;
     RenderArgs ra = make_args(pat, bg, 0);
     // compute_loss: dense views add the SSIM term, dilated views are L1 only
     const float lam = (pat->p == 1 && ctx->ssim_weight > 0.f) ? ctx->ssim_weight : 0.f;
@@ -709,6 +737,13 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
     if (run_chain) {
         StageTimer t(ctx, kStChain);
         CK(launch_chain(ctx, m, mode, true, nullptr, reinterpret_cast<const float*>(cfg)));
+        if (ctx->graph_capturing) {  // the chain node: its Adam arguments change per replay
+            cudaStreamCaptureStatus st;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t nd = 0;
+            CK(cudaStreamGetCaptureInfo(ctx->stream, &st, nullptr, nullptr, &deps, &nd));
+            ctx->graph_chain_node = nd == 1 ? (void*)deps[0] : nullptr;
+        }
     }
     if (mode == ChainMode::kAdam) ctx->bin_valid = false;  // the parameters moved
     const int tiles = ws.tiles_x * ws.tiles_y;
@@ -947,6 +982,7 @@ void tgsx_destroy(tgsx_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    graph_release(ctx);
     Workspace& ws = ctx->ws;
     DevBuf* bufs[] = {&ws.prep, &ws.touched, &ws.pair_off, &ws.scan_tmp, &ws.keys[0], &ws.keys[1],
                       &ws.vals[0], &ws.vals[1], &ws.sort_tmp, &ws.ranges, &ws.partial, &ws.rgb,
@@ -971,6 +1007,7 @@ void tgsx_destroy(tgsx_ctx* ctx) {
 
 int32_t tgsx_set_stream(tgsx_ctx* ctx, void* stream) {
     if (!ctx) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
     return TGSX_OK;
 }
@@ -980,6 +1017,7 @@ void* tgsx_get_stream(tgsx_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr
 const char* tgsx_last_error(const tgsx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int32_t tgsx_synchronize(tgsx_ctx* ctx) {
+    if (int32_t rc = graph_flush(ctx)) return rc;
     CK(cudaStreamSynchronize(ctx->stream));
     return TGSX_OK;
 }
@@ -1036,6 +1074,7 @@ void tgsx_model_destroy(tgsx_model* m) {
 
 int32_t tgsx_model_reserve(tgsx_ctx* ctx, tgsx_model* m, int64_t capacity) {
     if (!ctx || !m || capacity < 0) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     ctx->bin_valid = false;
     CK(model_grow(ctx, m, capacity));
     // per-Gaussian workspace (prepared records, counts, offsets, depth-sort and densify scratch)
@@ -1055,6 +1094,7 @@ uint64_t tgsx_model_next_id(const tgsx_model* m) { return m ? m->next_id : 0; }
 
 int32_t tgsx_model_upload(tgsx_ctx* ctx, tgsx_model* m, const tgsx_host_scene* h) {
     if (!ctx || !m || !h || h->n < 0) return fail(ctx, TGSX_EINVAL, "bad upload arguments");
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     ctx->bin_valid = false;
     const int64_t n = h->n;
     CK(model_reserve(ctx, m, n));
@@ -1113,6 +1153,7 @@ int32_t tgsx_model_upload(tgsx_ctx* ctx, tgsx_model* m, const tgsx_host_scene* h
 
 int32_t tgsx_model_download(tgsx_ctx* ctx, tgsx_model* m, tgsx_host_scene* h) {
     if (!ctx || !m || !h) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     CK(model_to_logical_order(ctx, m));
     const int64_t n = m->n, cap = m->cap;
     cudaStream_t s = ctx->stream;
@@ -1135,6 +1176,7 @@ int32_t tgsx_model_download(tgsx_ctx* ctx, tgsx_model* m, tgsx_host_scene* h) {
 
 int32_t tgsx_model_download_moments(tgsx_ctx* ctx, tgsx_model* m, float* m1, float* m2) {
     if (!ctx || !m) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     CK(model_to_logical_order(ctx, m));
     const int64_t n = m->n, cap = m->cap;
     if (n) {
@@ -1147,6 +1189,7 @@ int32_t tgsx_model_download_moments(tgsx_ctx* ctx, tgsx_model* m, float* m1, flo
 
 int32_t tgsx_model_upload_moments(tgsx_ctx* ctx, tgsx_model* m, const float* m1, const float* m2) {
     if (!ctx || !m) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     CK(model_to_logical_order(ctx, m));
     const int64_t n = m->n, cap = m->cap;
     if (n) {
@@ -1161,6 +1204,7 @@ int32_t tgsx_model_upload_moments(tgsx_ctx* ctx, tgsx_model* m, const float* m1,
 int32_t tgsx_render(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
                     int32_t lowpass_p, float* out_rgb, float* out_T, uint64_t* out_blend_ops) {
     if (!ctx || !m) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     int32_t rc = check_pattern(ctx, pat);
     if (rc) return rc;
     RenderArgs ra = make_args(pat, bg, lowpass_p);
@@ -1183,6 +1227,7 @@ int32_t tgsx_backward(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, con
                       int32_t lowpass_p, const float* dLdC, int64_t dLdC_count, float* out_grads,
                       int32_t update_stats) {
     if (!ctx || !m) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     int32_t rc = check_pattern(ctx, pat);
     if (rc) return rc;
     RenderArgs ra = make_args(pat, bg, lowpass_p);
@@ -1218,6 +1263,7 @@ int32_t tgsx_backward(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, con
 // ---------------------------------------------------------------- fit step
 int32_t tgsx_adam_step(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const tgsx_adam_args* a) {
     if (!ctx || !m || !grads || !a) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
     ctx->bin_valid = false;
     AdamCfg c;
@@ -1262,6 +1308,7 @@ float* tgsx_step_buffer(tgsx_model* m, int64_t* out_floats) {
 // logically ordered rows.
 int32_t tgsx_step_layout(tgsx_ctx* ctx, tgsx_model* m) {
     if (!ctx || !m) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     if (m->order_dirty) {
         ctx->bin_valid = false;
         CK(launch_sort_depth(ctx, m));
@@ -1301,6 +1348,7 @@ int32_t tgsx_batched_step(tgsx_ctx* ctx, tgsx_model* m, int32_t n_views, const t
                           const tgsx_adam_args* a, float* out_losses, int32_t buckets) {
     if (!ctx || !m || !a || n_views < 0 || (n_views > 0 && (!pats || !targets)))
         return fail(ctx, TGSX_EINVAL, "batched_step: bad arguments");
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     if (batch_views < 1 || batch_views < n_views) return fail(ctx, TGSX_EINVAL, "batched_step: bad batch size");
     if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
     AdamCfg c;
@@ -1437,6 +1485,7 @@ int32_t tgsx_loss(tgsx_ctx* ctx, const tgsx_pattern* pat, const float* rgb, cons
 
 int32_t tgsx_apply_step(tgsx_ctx* ctx, tgsx_model* m, int32_t batch_views, const tgsx_adam_args* a) {
     if (!ctx || !m || !a) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     if (batch_views < 1) return fail(ctx, TGSX_EINVAL, "accumulate: empty batch");
     ctx->bin_valid = false;  // parameters change
     if (a->step < 1) return fail(ctx, TGSX_EINVAL, "adam step must be >= 1");
@@ -1453,6 +1502,7 @@ int32_t tgsx_apply_step(tgsx_ctx* ctx, tgsx_model* m, int32_t batch_views, const
 // ---------------------------------------------------------------- stage access
 int32_t tgsx_stage_prepare(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, float* out, uint32_t* orig) {
     if (!ctx || !m || lowpass_p < 1) return fail(ctx, TGSX_EINVAL, "bad arguments");
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     ctx->bin_valid = false;
     CK(reset_counters(ctx));
     if (m->order_dirty) CK(launch_sort_depth(ctx, m));
@@ -1480,6 +1530,7 @@ int32_t tgsx_stage_prepare(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, floa
 
 int32_t tgsx_stage_sorted_order(tgsx_ctx* ctx, tgsx_model* m, uint32_t* perm) {
     if (!ctx || !m) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     ctx->bin_valid = false;
     if (m->order_dirty) CK(launch_sort_depth(ctx, m));
     if (m->n && perm) CK(cudaMemcpyAsync(perm, m->perm.p, m->n * 4, cudaMemcpyDefault, ctx->stream));
@@ -1491,6 +1542,7 @@ int32_t tgsx_stage_tile_lists(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, i
                               int32_t height, uint32_t* offsets, uint32_t* items,
                               int64_t items_cap, int64_t* out_k) {
     if (!ctx || !m || lowpass_p < 1 || width < 1 || height < 1) return fail(ctx, TGSX_EINVAL, "bad arguments");
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     uint32_t* it = nullptr;
     uint32_t* keys = nullptr;
     int32_t rc = bin(ctx, m, lowpass_p, width, height, &it, &keys);
@@ -1529,6 +1581,7 @@ int32_t tgsx_stage_tile_lists(tgsx_ctx* ctx, tgsx_model* m, int32_t lowpass_p, i
 
 int32_t tgsx_stage_screen_grads(tgsx_ctx* ctx, tgsx_model* m, float* out) {
     if (!ctx || !m || !out) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     if (m->n) CK(cudaMemcpy2DAsync(out, m->n * 4, m->screen.p, m->cap * 4, m->n * 4, 10, cudaMemcpyDefault, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return TGSX_OK;

@@ -199,6 +199,7 @@ void tgsx_densify_config_default(tgsx_densify_config* c) {
 int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cfg, int64_t budget,
                      uint64_t rng_state[2], tgsx_densify_report* out) {
     if (!ctx || !m || !cfg || !rng_state) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     StageTimer timer(ctx, kStDensify);
     // selection ties, spawn order and compaction follow the logical (creation) order
     DCK(model_to_logical_order(ctx, m));
@@ -346,6 +347,7 @@ int32_t tgsx_densify(tgsx_ctx* ctx, tgsx_model* m, const tgsx_densify_config* cf
 
 int32_t tgsx_visit_audit(tgsx_ctx* ctx, tgsx_model* m) {
     if (!ctx || !m) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     if (m->n) {
         visit_audit_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(m->window.as<int64_t>(),
                                                                          m->tau_v.as<double>(), m->n);

@@ -90,6 +90,7 @@ struct ChainParams {
     StepRec* step;  // [n] AoS (mode 2)
     int64_t i0, i1; // Gaussian (row) range of this launch (buckets of the pipelined batched step)
     AdamCfg adam;
+    const unsigned* fault;  // graph-replayed steps (graph.cpp): non-zero => the step is a no-op
 };
 
 // 6 blocks of 256 per SM (<= 40 registers): the slot loop and the moment / parameter streams
@@ -97,6 +98,7 @@ struct ChainParams {
 __global__ void __launch_bounds__(256, 4) chain_kernel(ChainParams cp) {
     const int64_t i = cp.i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cp.i1) return;
+    if (cp.fault && *reinterpret_cast<const volatile unsigned*>(cp.fault)) return;
     const int64_t cap = cp.cap;
     const float* __restrict__ params = cp.params;
     // independent loads first (memory-level parallelism): the raw parameters the chain rule
@@ -307,9 +309,24 @@ cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool upda
     cp.m2 = m->m2.as<float>();
     cp.step = m->step.as<StepRec>();
     if (adam_cfg) cp.adam = *reinterpret_cast<const AdamCfg*>(adam_cfg);
+    cp.fault = ctx->graph_capturing ? ctx->graph_fault : nullptr;
     chain_kernel<<<grid_for(i1 - i0, 256), 256, 0, ctx->stream>>>(cp);
     ctx->launches++;
     return cudaGetLastError();
+}
+
+// Per-launch Adam hyper-parameters of a captured chain kernel node (graph.cpp): the node's
+// ChainParams as captured with only `adam` replaced, for the next launches of `exec`.
+cudaError_t chain_node_set_adam(cudaGraphExec_t exec, cudaGraphNode_t node, const AdamCfg& c) {
+    cudaKernelNodeParams kp{};
+    cudaError_t e = cudaGraphKernelNodeGetParams(node, &kp);
+    if (e) return e;
+    ChainParams cp = *reinterpret_cast<const ChainParams*>(kp.kernelParams[0]);
+    cp.adam = c;
+    void* args[1] = {&cp};
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    return cudaGraphExecKernelNodeSetParams(exec, node, &kp);
 }
 
 cudaError_t launch_adam(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const float* adam_cfg,

@@ -121,6 +121,14 @@ struct tgsx_ctx {
     // pipeline timeline of the last profiled batched step: per bucket (chain start, chain end,
     // all-reduce start, all-reduce end, Adam start, Adam end) in ms from the step's first event
     std::vector<float> pipe_timeline;
+    // CUDA-graph replay of the fused fit step (graph.cpp, tgsx_fit_graph_step): while capturing,
+    // the backward / chain kernels get the fault word and the capture-time capacities as guards
+    bool graph_capturing = false, graph_replaying = false;
+    unsigned* graph_fault = nullptr;    // device word, sticky until the host re-runs the steps
+    unsigned* h_graph_fault = nullptr;  // pinned [2]: the fault word after each slot's last launch
+    int64_t graph_guard_pairs = 0;      // pair count the captured step may produce (<= pair_cap)
+    void* graph_chain_node = nullptr;   // cudaGraphNode_t of the captured chain kernel
+    void* graph = nullptr;              // tgsx::FitGraph
 };
 
 // Scoped stage timer: no-op unless profiling is enabled.
@@ -174,6 +182,13 @@ struct tgsx_model3d {
     bool rank_ordered = false;      // last binning: records / pair slots by blend rank (global-sort
                                     // path) rather than by row (per-tile path)
 };
+
+namespace tgsx {
+// graph.cpp: verifies every in-flight graph-replayed fit step (re-running a faulted one and its
+// successors eagerly); called by every entry point that reads or changes the model
+int32_t graph_flush(tgsx_ctx* ctx);
+void graph_release(tgsx_ctx* ctx);
+}  // namespace tgsx
 
 // physical row order of the model (capi.cu): blend order for the hot path, logical (creation)
 // order for densify / download / explicit-gradient APIs
@@ -239,6 +254,11 @@ cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool upda
                          float* grads_out, const float* adam_cfg, int64_t i0 = 0, int64_t i1 = -1);
 cudaError_t launch_adam(tgsx_ctx* ctx, tgsx_model* m, const float* grads, const float* adam_cfg,
                         int batch_views, int64_t i0 = 0, int64_t i1 = -1);
+// graph.cpp helpers: the Adam hyper-parameters of a step (capi.cu fill_adam) and the per-launch
+// update of a captured chain kernel node (optim.cu)
+void adam_cfg_from_args(AdamCfg& c, const tgsx_adam_args* a);
+cudaError_t chain_node_set_adam(cudaGraphExec_t exec, cudaGraphNode_t node, const AdamCfg& c);
+bool graph_eligible_binning(const tgsx_ctx* ctx);
 
 int key_bits_for(int tiles);
 
