@@ -62,6 +62,12 @@ CONFIGS = {
                         "per step accumulated + one Adam step; cameras sharded across ranks with an NCCL "
                         "all-reduce of the [62][N] step buffer", n=1_000_000, W=1920, H=1080, p=1,
                three_d=True, views=8),
+    "c8": dict(workload="C8: full Turbo-GS fit at 4K — 3M initial Gaussians, 16 synthetic 3840x2160 views, "
+                        "1000 iterations of the SPEC schedule (warm-up 100, dilated p=2 cycled offsets, densify "
+                        "every 20 until 600 with the convergence-aware budget M = 1.5 N0 (tau_pos 5e-8), "
+                        "post-densify random dilation with dense L1 + 0.2 SSIM iterations, batched finale of "
+                        "100 iterations x 4 views); the whole schedule is one timed region",
+               n=3_000_000, W=3840, H=2160, p=2, iters=1000, views=16),
 }
 METRIC = "fit iters/sec (fwd+bwd+Adam) at 1080p and 4K dilated, 1M–3M Gaussians"
 
@@ -360,6 +366,62 @@ def roofline(stages, counters, clocks, n, config, fp32_meas=None):
             "traffic": measured_traffic(config, dom), "ms_per_launch": dom_ms}
 
 
+def measure_fit4k(args, env):
+    """C8: the whole 4K Turbo-GS schedule (trainer.cpp) as one timed region on one GPU: fit
+    time, iterations/s over the schedule, densify events with budget compliance, final loss and
+    PSNR of the fitted model against the clean scene (the 4K quality check against the reference
+    schedule runs at reduced N in tests/test_gpu_fit4k.py)."""
+    torch, P, ctx = env["torch"], env["P"], env["ctx"]
+    cfg = CONFIGS["c8"]
+    W, H, n, p, iters = cfg["W"], cfg["H"], cfg["n"], cfg["p"], cfg["iters"]
+    host = P.GaussianModel.synthetic(1, n, W, H)
+    tm = P.DeviceModel.from_host(P.GaussianModel.synthetic(2, n, W, H), ctx)
+    clean = torch.from_numpy(tm.render(P.DilationPattern(1, 0, 0, W, H)).colors.reshape(H, W, 3)).cuda()
+    tm.close()
+    targets = []
+    for v in range(cfg["views"]):
+        g = torch.Generator(device="cuda").manual_seed(2000 + v)
+        targets.append((clean + 0.02 * torch.randn(clean.shape, generator=g, device="cuda")).clamp(0, 1).contiguous())
+    tcfg = P.train_config(total_iters=iters, warmup_iters=100, densify_interval=20, densify_until=600,
+                          batch_final_iters=100, batch_size=4, dilation_p=p, n_views=cfg["views"],
+                          m_final=1.5 * n, seed=1)
+    tcfg.densify.tau_pos = 5e-8  # ~90th percentile of the mean position-gradient norm (see c4)
+    dm = P.DeviceModel.from_host(host, ctx)
+    trainer = P.Trainer(dm, W, H, tcfg)
+    trainer.set_targets([t.data_ptr() for t in targets])
+    stream = torch.cuda.ExternalStream(ctx.L.tgsx_get_stream(ctx.h))
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    reports = []
+    launches0 = ctx.launches
+    with ClockSampler(env["local"]) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            reports.append(trainer.step())
+        e1.record(stream)
+        e1.synchronize()
+        ctx.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - launches0
+    losses = trainer.losses(100)
+    final = torch.from_numpy(dm.render(P.DilationPattern(1, 0, 0, W, H)).colors.reshape(H, W, 3)).cuda()
+    mse = float(((final - clean) ** 2).mean())
+    events = [(r.iteration, r.budget, r.count, r.spawned, r.pruned) for r in reports if r.densified]
+    dm.close()
+    return {"value": iters / (ms / 1e3), "unit": "iters/s", "n_gpus": 1, "steps": iters, "warmup": 0,
+            "ms_per_step": ms / iters, "fit_seconds": ms / 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "gaussians": n, "width": W, "height": H, "p": p,
+                       "views": cfg["views"], "l2": "per-step working set > 126 MB L2 (no explicit flush)"},
+            "clocks": clk.summary(), "gpu_launches": launches,
+            "fit": {"densify_events": len(events), "budget_respected": all(c <= b for _, b, c, _, _ in events),
+                    "count_start": n, "count_end": int(reports[-1].count), "spawned": int(sum(e[3] for e in events)),
+                    "pruned": int(sum(e[4] for e in events)), "loss_last": float(losses[-1]),
+                    "psnr_db": 10.0 * math.log10(1.0 / mse) if mse > 0 else None,
+                    "events_first_last": [events[0], events[-1]] if events else []}}
+
+
 def run_tgsx(args):
     """All ranks: set up the process group, the context (+ the library NCCL communicator for
     N > 1), measure the requested config; with the default config (C2) also the sub-records of
@@ -384,11 +446,16 @@ def run_tgsx(args):
         ctx.set_ssim_weight(args.ssim)
     env = {"torch": torch, "P": P, "D": D, "ctx": ctx, "dist": dist, "rank": rank, "world": world,
            "local": local}
-    line = measure(args, args.config, env)
+    if args.config == "c8":
+        if world > 1:
+            raise SystemExit("c8 (the whole 4K fit schedule) runs on one GPU: --gpus 1")
+        line = dict(metric=METRIC, **measure_fit4k(args, env))
+    else:
+        line = measure(args, args.config, env)
     if args.config == "c2" and args.ssim == 0 and not args.no_subrecords:
         subs = {}
-        for name in (["c1"] if world == 1 else []) + ["c3", "c5"]:
-            sub = measure(args, name, env)
+        for name in (["c1"] if world == 1 else []) + ["c3", "c5"] + (["c8"] if world == 1 else []):
+            sub = measure_fit4k(args, env) if name == "c8" else measure(args, name, env)
             if sub is not None:
                 sub.pop("metric", None)
                 subs[name] = sub

@@ -282,6 +282,9 @@ int32_t tgsx_trainer_step(tgsx_trainer* tr, const float* const* targets, int64_t
 /* Losses of the most recent iterations (oldest first), up to max_out. */
 int32_t tgsx_trainer_losses(tgsx_trainer* tr, float* out, int64_t max_out, int64_t* out_n);
 const tgsx_budget* tgsx_trainer_budget(const tgsx_trainer* tr);
+/* The trainer's PCG32 state (state, inc): offset coin -> colour coin -> spawn jitter stream
+ * (SPEC.md:604), e.g. to drive a reference run of the schedule with the same draws. */
+int32_t tgsx_trainer_rng(const tgsx_trainer* tr, uint64_t out_state[2]);
 
 /* ---------------------------------------------------------------- TGS1 checkpoint */
 /* "TGS1", u32 version, u64 count, u64 next_id, the parameter arrays in declared field order,

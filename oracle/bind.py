@@ -241,6 +241,9 @@ class Pcg32:
     def state(self):
         return (self.c.state, self.c.inc)
 
+    def set_state(self, st) -> None:
+        self.c.state, self.c.inc = int(st[0]), int(st[1])
+
 
 # ------------------------------------------------------------------ render / backward
 def active_count(p, ox, oy, W, H):

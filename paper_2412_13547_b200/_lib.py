@@ -132,6 +132,7 @@ SIGNATURES = {
     "tgsx_trainer_step": (C.c_int32, [vp, P(vp), C.c_int64, P(TrainReport)]),
     "tgsx_trainer_losses": (C.c_int32, [vp, f32p, C.c_int64, i64p]),
     "tgsx_trainer_budget": (vp, [vp]),
+    "tgsx_trainer_rng": (C.c_int32, [vp, P(C.c_uint64)]),
     "tgsx_checkpoint_save": (C.c_int32, [vp, vp, vp, C.c_char_p]),
     "tgsx_checkpoint_load": (C.c_int32, [vp, vp, vp, C.c_char_p]),
     "tgsx_knn": (C.c_int32, [vp, vp, C.c_int64, C.c_int32, vp, vp]),

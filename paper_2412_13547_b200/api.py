@@ -705,6 +705,12 @@ class Trainer:
         self.dm.ctx.check(self.dm.ctx.L.tgsx_trainer_losses(self.h, _ptr(out, _lib.f32p), max_n, C.byref(n)))
         return out[:n.value]
 
+    def rng_state(self):
+        """(state, inc) of the trainer's PCG32 stream (SPEC.md:604 draw order)."""
+        st = (C.c_uint64 * 2)()
+        self.dm.ctx.check(self.dm.ctx.L.tgsx_trainer_rng(self.h, st))
+        return int(st[0]), int(st[1])
+
     def budget_state(self):
         b = self.dm.ctx.L.tgsx_trainer_budget(self.h)
         out = (C.c_double * 5)()

@@ -208,6 +208,12 @@ int32_t tgsx_trainer_losses(tgsx_trainer* tr, float* out, int64_t max_out, int64
 }
 
 const tgsx_budget* tgsx_trainer_budget(const tgsx_trainer* tr) { return tr ? tr->budget : nullptr; }
+int32_t tgsx_trainer_rng(const tgsx_trainer* tr, uint64_t out_state[2]) {
+    if (!tr || !out_state) return TGSX_EINVAL;
+    out_state[0] = tr->rng[0];
+    out_state[1] = tr->rng[1];
+    return TGSX_OK;
+}
 
 }  // extern "C"
 
