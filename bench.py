@@ -313,10 +313,52 @@ class Timer:
 def measured_traffic(config, kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic_r01.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic_r02.json")) as f:
             return json.load(f).get(config, {}).get(kernel)
     except Exception:
         return None
+
+
+def sass_weights(config):
+    """Per-blend instruction / FP32-flop / shared-wavefront weights of the blend kernels, recounted
+    from the executed SASS of one ncu capture (tools/freeze_weights.py -> profiles/weights_r02.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "weights_r02.json")) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
+def blend_pipes(stages, counters, f_mhz, fp32_peak, config):
+    """Issue-slot, executed-FP32 and shared-memory-wavefront fractions of the blend kernels: the
+    frozen per-blend SASS weights x this run's blend count, over this run's per-launch time."""
+    w = sass_weights(config)
+    if not w:
+        return None
+    out = {}
+    f = f_mhz * 1e6
+    for k in ("blend_forward", "blend_backward"):
+        if k not in w or k not in stages or not stages[k][1]:
+            continue
+        ms = stages[k][0] / stages[k][1]
+        pb = w[k]["per_blend"]
+        bl = counters["blend_ops"]
+        inst = pb["warp_inst"] * bl
+        fl = pb["fp32_flops"] * bl
+        wf = pb["smem_wavefronts"] * bl
+        out[k] = {"ms_per_launch": ms,
+                  "warp_inst_per_blend": pb["warp_inst"], "fp32_flops_per_blend": pb["fp32_flops"],
+                  "smem_wavefronts_per_blend": pb["smem_wavefronts"],
+                  # 4 schedulers x 148 SMs issue one warp instruction per cycle each
+                  "issue_frac": inst / (ms / 1e3 * 592 * f),
+                  "fp32_executed_tflops": fl / (ms / 1e3) / 1e12,
+                  "fp32_executed_frac": fl / (ms / 1e3) / 1e12 / fp32_peak,
+                  # one shared-memory wavefront per SM per cycle
+                  "smem_wavefront_frac": wf / (ms / 1e3 * 148 * f)}
+    out["note"] = ("weights recounted from the executed SASS of one ncu capture (profiles/weights_r02.json, "
+                   "tools/freeze_weights.py) x this run's blend count; issue slots = 592 schedulers x SM clock, "
+                   "shared memory = 1 wavefront / SM / cycle")
+    return out
 
 
 def measure_fp32_peak(ctx):
@@ -353,7 +395,8 @@ def roofline(stages, counters, clocks, n, config, fp32_meas=None):
                 "ms_per_launch": dom_ms,
                 "peak_note": note,
                 "work_note": f"algorithmic flops per launch 2E+{per_blend}Bl with E={E} evaluations, "
-                             f"Bl={Bl} blends (SURVEY.md §8d)"}
+                             f"Bl={Bl} blends (SURVEY.md §8d)",
+                "pipes": blend_pipes(stages, counters, f_mhz, fp32_peak, config)}
     if config in ("c6", "c7"):  # 3-D: chain3d + Adam streams 59 params, 2 moments (r+w), partials
         nb = {"chain_adam": (59 * 4 * 6 + 24) * n + 40 * K, "preprocess": (59 * 4 + 64 + 8) * n,
               "depth_sort": 4 * 24 * n + (64 + 64 + 16) * n}.get(dom, 0)
