@@ -135,7 +135,9 @@ __device__ __forceinline__ bool walk_chunk(uint32_t cbase, int ccount, uint32_t 
                                            uint32_t& lastA, uint32_t& lastB, uint32_t& ops, bool& doneA,
                                            bool& doneB) {
     const int lane = threadIdx.x & 31;
-    const uint32_t bits = transpose32(lane < ccount ? __float_as_uint(lds_f1(cbase + lane * kRec + 36)) : 0u);
+    // bit-reversed pass sets (bit 31 - k = splat k): the next splat front to back is one FLO (clz)
+    const uint32_t bits =
+        __brev(transpose32(lane < ccount ? __float_as_uint(lds_f1(cbase + lane * kRec + 36)) : 0u));
     const uint32_t X = __shfl_sync(kFull, bits, bx * 8 + (lane & 7));
     uint32_t colA = X & __shfl_sync(kFull, bits, 16 + by * 8 + 2 * (lane >> 3));
     uint32_t colB = X & __shfl_sync(kFull, bits, 17 + by * 8 + 2 * (lane >> 3));
@@ -143,17 +145,19 @@ __device__ __forceinline__ bool walk_chunk(uint32_t cbase, int ccount, uint32_t 
     if (doneB) colB = 0;
     const uint32_t colA0 = colA, colB0 = colB;
     int termA = 32, termB = 32;  // bit of each pixel's terminating blend, 32 = none
+    const int kmax = ccount - 1;
     uint32_t colU = colA | colB;
     // branch-free: a lane whose walk is over runs on record 0 with both pixels masked
     // (sigma = 0 changes nothing)
     // Two splats (k1 < k2) per iteration: their Gaussians are independent (ILP), the
     // blends are applied in order and a ray that terminates at k1 does not blend k2.
     while (__any_sync(kFull, colU)) {
-        const int k1 = colU ? __ffs(colU) - 1 : 0;
-        const uint32_t bit1 = colU ? 1u << k1 : 0u;
+        // an empty set reads the chunk's last staged record with a zero bit (pixels masked)
+        const int k1 = min(__clz(colU), kmax);
+        const uint32_t bit1 = (0x80000000u >> k1) & colU;
         const uint32_t rem = colU & ~bit1;
-        const int k2 = rem ? __ffs(rem) - 1 : 0;
-        const uint32_t bit2 = rem ? 1u << k2 : 0u;
+        const int k2 = min(__clz(rem), kmax);
+        const uint32_t bit2 = (0x80000000u >> k2) & rem;
         const bool hA1 = (colA & bit1) != 0u, hB1 = (colB & bit1) != 0u;
         const bool hA2 = (colA & bit2) != 0u, hB2 = (colB & bit2) != 0u;
         const uint32_t ad1 = cbase + k1 * kRec, ad2 = cbase + k2 * kRec;
@@ -193,16 +197,18 @@ __device__ __forceinline__ bool walk_chunk(uint32_t cbase, int ccount, uint32_t 
         }
         colU = colA | colB;
     }
+    // (bit-reversed: positions 0..term are bits 31..31-term; the last used position is the
+    // lowest set bit)
     if (colA0) {
-        const uint32_t used = termA < 32 ? (colA0 & (kFull >> (31 - termA))) : colA0;
+        const uint32_t used = termA < 32 ? (colA0 & ~(0x7fffffffu >> termA)) : colA0;
         ops += __popc(used);
-        lastA = lbase + 31 - __clz(used);
+        lastA = lbase + 32 - __ffs(used);
         if (termA < 32) doneA = true;
     }
     if (colB0) {
-        const uint32_t used = termB < 32 ? (colB0 & (kFull >> (31 - termB))) : colB0;
+        const uint32_t used = termB < 32 ? (colB0 & ~(0x7fffffffu >> termB)) : colB0;
         ops += __popc(used);
-        lastB = lbase + 31 - __clz(used);
+        lastB = lbase + 32 - __ffs(used);
         if (termB < 32) doneB = true;
     }
     return __all_sync(kFull, doneA && doneB);
@@ -326,6 +332,109 @@ __global__ void __launch_bounds__(NWX * NWY * 32) forward_pairs_kernel(BlendPara
         if (to) atomicAdd(&prm.counters[1], to);
         if (te) atomicAdd(&prm.counters[2], te);
         if (prm.block_loss) prm.block_loss[tile] = tl;
+    }
+}
+
+// 16-byte global -> shared async copy (LDGSTS, L2 only), zero-fill when src_bytes == 0
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Dilated forward (p >= 2: a tile's <= 8x8 active pixels are one warp's block): one warp per
+// tile, independent warps (no block barriers). The list is consumed in chunks of 32; the raw
+// 64-B prepared records of chunk c+1 are gathered by asynchronous copies (each lane copies its
+// own list entry's record, four 16-B LDGSTS) while chunk c is walked, so the record gathers —
+// the 3M-splat record array does not fit in L2 — do not stall the walk. Each lane then stages
+// its own record of the arrived chunk (box mask, pre-scaled conic) exactly as the p = 1 kernel.
+struct FwdWarpSmem {
+    unsigned char raw[2][32 * sizeof(Prepared)];
+    unsigned char rec[32 * kRec];
+};
+
+__global__ void __launch_bounds__(32, 32) forward_dilated_kernel(BlendParams prm) {
+    __shared__ __align__(128) FwdWarpSmem S;
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x;
+    TileGeo geo;
+    geo.init(prm, tile);
+    const int p = prm.p;
+    const int lx = lane & 7, lyA = 2 * (lane >> 3);
+    const bool vA = lx < geo.acols && lyA < geo.arows;
+    const bool vB = lx < geo.acols && lyA + 1 < geo.arows;
+    const int x = geo.ax + lx * p, yA = geo.ay + lyA * p, yB = yA + p;
+    const float fx = (float)x + 0.5f, fyA = (float)yA + 0.5f, fyB = (float)yB + 0.5f;
+    const uint2 range = prm.ranges[tile];
+    const int count = (int)(range.y - range.x);
+    const int nch = (count + 31) >> 5;
+    const uint32_t rawbase = smem_addr(S.raw), recbase = smem_addr(S.rec);
+    const uint32_t myraw = rawbase + lane * (uint32_t)sizeof(Prepared);
+    // chunk c's gathers: lane copies its entry's record into raw[c & 1] (nothing past the list)
+    auto issue = [&](int c, uint32_t item) {
+        const uint32_t nb = c * 32 + lane < count ? 16u : 0u;
+        const char* src = reinterpret_cast<const char*>(prm.prep + item);
+        const uint32_t dst = myraw + (uint32_t)(c & 1) * (32u * sizeof(Prepared));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cp_async16(dst + 16 * q, src + 16 * q, nb);
+        cp_async_commit_();
+    };
+
+    float2 T = make_float2(1.0f, 1.0f);
+    float2 C0 = make_float2(0.f, 0.f), C1 = C0, C2 = C0;
+    uint32_t lastA = 0, lastB = 0, ops = 0;
+    bool doneA = !vA, doneB = !vB;
+    bool warp_done = __all_sync(kFull, doneA && doneB);
+    uint32_t item = 0;
+    if (!warp_done && nch > 0) {
+        issue(0, lane < count ? prm.items[range.x + lane] : 0u);
+        item = 32 + lane < count ? prm.items[range.x + 32 + lane] : 0u;
+    }
+    for (int c = 0; c < nch && !warp_done; ++c) {
+        if (c + 1 < nch) {
+            issue(c + 1, item);
+            const int j = (c + 2) * 32 + lane;
+            item = j < count ? prm.items[range.x + j] : 0u;
+            cp_async_wait_<1>();
+        } else {
+            cp_async_wait_<0>();
+        }
+        const int n = min(32, count - c * 32);
+        const uint32_t dst = recbase + lane * kRec;
+        if (lane < n) {
+            const uint32_t src = myraw + (uint32_t)(c & 1) * (32u * sizeof(Prepared));
+            const float4 a = lds_f4(src), b = lds_f4(src + 16), cc = lds_f4(src + 32);
+            const uint32_t mask = box_mask(a.x, b.z, geo.ax, p, geo.acols) |
+                                  (box_mask(a.y, b.w, geo.ay, p, geo.arows) << 16);
+            sts_f4(dst, make_float4(a.x, a.y, __fmul_rn(a.z, kNegHalfLog2e), __fmul_rn(a.w * 2.0f, kNegHalfLog2e)));
+            sts_f4(dst + 16, make_float4(__fmul_rn(b.x, kNegHalfLog2e), b.y, cc.x, cc.y));
+            sts_f4(dst + 32, make_float4(cc.z, __uint_as_float(mask), 0.f, 0.f));
+        }
+        __syncwarp();
+        warp_done = walk_chunk(recbase, n, (uint32_t)(c * 32 + 1), 0, 0, fx, fyA, fyB, T, C0, C1, C2, lastA, lastB,
+                               ops, doneA, doneB);
+    }
+    cp_async_wait_<0>();  // copies still in flight must land before the CTA exits
+
+    float lsum = 0.f;
+    unsigned long long ev = 0;
+    finish_pixel(prm, vA, x, yA, T.x, C0.x, C1.x, C2.x, lastA, doneA, count, ev, lsum);
+    finish_pixel(prm, vB, x, yB, T.y, C0.y, C1.y, C2.y, lastB, doneB, count, ev, lsum);
+    unsigned long long o = ops;
+#pragma unroll
+    for (int sft = 16; sft > 0; sft >>= 1) {
+        o += __shfl_xor_sync(kFull, o, sft);
+        ev += __shfl_xor_sync(kFull, ev, sft);
+        lsum += __shfl_xor_sync(kFull, lsum, sft);
+    }
+    if (lane == 0) {
+        if (o) atomicAdd(&prm.counters[1], o);
+        if (ev) atomicAdd(&prm.counters[2], ev);
+        if (prm.block_loss) prm.block_loss[tile] = lsum;
     }
 }
 
@@ -856,7 +965,7 @@ cudaError_t launch_forward(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* 
     if (ra.p == 1) {
         forward_pairs_kernel<2, 2, 256><<<tiles, 128, 0, ctx->stream>>>(prm);
     } else {  // dilated: a tile's <= 8x8 active pixels are one warp's block
-        forward_pairs_kernel<1, 1, 32><<<tiles, 32, 0, ctx->stream>>>(prm);
+        forward_dilated_kernel<<<tiles, 32, 0, ctx->stream>>>(prm);
     }
     ctx->launches++;
     return cudaGetLastError();

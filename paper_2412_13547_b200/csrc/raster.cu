@@ -133,7 +133,9 @@ __global__ void __launch_bounds__(256) preprocess_scan_kernel(
         prep[i] = o;
         touched[i] = tiles;
         pair_off[i] = excl;
+#ifndef TGSX_PRE_NOCLAIM
         if (tiles) claim_slots(o.d, tiles_x, (uint32_t)i, fill, slab);
+#endif
     }
 }
 
