@@ -114,7 +114,8 @@ std::vector<uintptr_t> make_key(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern
     put(k, m->uid);
     put(k, m->n);
     put(k, m->cap);
-    put(k, (int)m->blend_phys + 2 * (int)m->order_dirty);
+    put(k, (int)m->blend_phys + 2 * (int)m->order_dirty + 4 * (int)m->spatial_valid);
+    put(k, m->spatial.p);
     for (const DevBuf* b : {&m->params, &m->ids, &m->pos_acc, &m->col_acc, &m->accum, &m->visit, &m->window,
                             &m->tau_v, &m->m1, &m->m2, &m->step, &m->perm, &m->rank_of, &m->screen})
         put(k, b->p);

@@ -133,10 +133,74 @@ __global__ void __launch_bounds__(256) preprocess_scan_kernel(
         prep[i] = o;
         touched[i] = tiles;
         pair_off[i] = excl;
-#ifndef TGSX_PRE_NOCLAIM
-        if (tiles) claim_slots(o.d, tiles_x, (uint32_t)i, fill, slab);
-#endif
+        if (tiles && fill) claim_slots(o.d, tiles_x, (uint32_t)i, fill, slab);
     }
+}
+
+// ------------------------------------------------------------------ slot claims
+// Slab slot claims of every (tile, splat) pair, taken in SPATIAL order: thread i handles blend
+// rank spatial[i] (ranks ordered by the top-left tile of their rectangle), so a warp's pairs fall
+// on a handful of tiles. The warp flattens its 32 splats' pairs (exclusive scan of the tile
+// counts), takes them 32 at a time (lane j: pair base + j, its owner found by a 5-step binary
+// search over the scan), groups equal tiles with match.any and claims one run of slots per
+// distinct tile with a single atomic. A slot's position inside its tile is arbitrary (the
+// per-tile sort restores blend order), so the claim order changes nothing but the atomic count:
+// in blend (depth) order neighbouring threads hit unrelated tiles and every pair was one
+// contended L2 atomic.
+__global__ void __launch_bounds__(256) claim_kernel(const uint32_t* __restrict__ spatial,
+                                                    const Prepared* __restrict__ prep, int64_t n, int tiles_x,
+                                                    uint32_t* __restrict__ fill, uint32_t* __restrict__ slab) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    uint32_t rank = 0;
+    uint4 d = make_uint4(0u, 0u, 0u, 0u);
+    if (i < n) {
+        rank = spatial[i];
+        d = __ldg(&prep[rank].d);
+    }
+    const uint32_t cnt = d.w;
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const uint32_t excl = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t tx0 = d.x & 0xffffu, ty0 = d.y & 0xffffu, w = (d.x >> 16) - tx0 + 1u;
+    const uint32_t lt = lanemask_lt();
+    for (uint32_t base = 0; base < total; base += 32) {
+        const uint32_t j = base + (uint32_t)lane;
+        int o = 0;  // owner: the last lane whose exclusive offset is <= j (it has j inside its run)
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, excl, o + s);
+            if (e <= j) o += s;
+        }
+        const uint32_t q = j - __shfl_sync(0xffffffffu, excl, o);
+        const uint32_t orank = __shfl_sync(0xffffffffu, rank, o);
+        const uint32_t otx0 = __shfl_sync(0xffffffffu, tx0, o), oty0 = __shfl_sync(0xffffffffu, ty0, o);
+        const uint32_t ow = __shfl_sync(0xffffffffu, w, o);
+        const bool valid = j < total;
+        const uint32_t qy = valid ? q / ow : 0u;
+        const uint32_t tile = valid ? (oty0 + qy) * (uint32_t)tiles_x + otx0 + (q - qy * ow) : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, tile);
+        const int leader = __ffs(peers) - 1;
+        uint32_t pos = 0;
+        if (valid && lane == leader) pos = atomicAdd(&fill[(size_t)tile * kFillStride], (uint32_t)__popc(peers));
+        pos = __shfl_sync(0xffffffffu, pos, leader) + (uint32_t)__popc(peers & lt);
+        if (valid && pos < (uint32_t)kSegCap) slab[(size_t)tile * kSegCap + pos] = orank;
+    }
+}
+
+// spatial order key of blend rank r: the top-left tile of its rectangle (unbinned: last)
+__global__ void spatial_keys_kernel(const Prepared* __restrict__ prep, int64_t n, int tiles_x, uint32_t* __restrict__ keys,
+                                    uint32_t* __restrict__ vals) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint4 d = __ldg(&prep[r].d);
+    keys[r] = d.w ? (d.y & 0xffffu) * (uint32_t)tiles_x + (d.x & 0xffffu) : 0x7fffffffu;
+    vals[r] = (uint32_t)r;
 }
 
 // ------------------------------------------------------------------ key duplication
@@ -292,10 +356,48 @@ cudaError_t launch_seg_sort(tgsx_ctx* ctx, uint32_t* items, int tiles, int64_t m
     return cudaGetLastError();
 }
 
+
 int key_bits_for(int tiles) {
     int b = 0;
     while ((1ll << b) < (long long)tiles) ++b;
     return b;
+}
+
+// Spatial claim order of the model's blend ranks (claim_kernel): ranks sorted by the top-left
+// tile of their rectangles in the records of the current preprocess. Rebuilt when the blend
+// ranks change (depth sort) and every kSpatialRefresh binnings (splats move while fitting; any
+// permutation is correct, the order only sets how many atomics the claims need).
+constexpr int kSpatialRefresh = 64;
+
+cudaError_t launch_claims(tgsx_ctx* ctx, tgsx_model* m) {
+    Workspace& ws = ctx->ws;
+    const int64_t n = m->n;
+    cudaError_t e;
+    if (n == 0) return cudaSuccess;
+    const int tiles = ws.tiles_x * ws.tiles_y;
+    if (!m->spatial_valid || (m->spatial_age >= kSpatialRefresh && !ctx->graph_capturing)) {
+        if ((e = m->spatial.ensure((size_t)m->cap * 4))) return e;
+        for (int b = 0; b < 2; ++b) {
+            if ((e = ws.keys[b].ensure(n * 4))) return e;
+            if ((e = ws.vals[b].ensure(n * 4))) return e;
+        }
+        ctx->bin_valid = false;  // the sort reuses the binning buffers
+        uint32_t *k = ws.keys[0].as<uint32_t>(), *v = ws.vals[0].as<uint32_t>();
+        spatial_keys_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(ws.prep.as<Prepared>(), n, ws.tiles_x, k, v);
+        ctx->launches++;
+        if ((e = sort_pairs(ctx, k, v, ws.keys[1].as<uint32_t>(), ws.vals[1].as<uint32_t>(), n,
+                            key_bits_for(tiles + 1), nullptr)))
+            return e;
+        if ((e = cudaMemcpyAsync(m->spatial.p, v, n * 4, cudaMemcpyDeviceToDevice, ctx->stream))) return e;
+        m->spatial_valid = true;
+        m->spatial_age = 0;
+    }
+    ++m->spatial_age;
+    claim_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(m->spatial.as<uint32_t>(), ws.prep.as<Prepared>(), n,
+                                                            ws.tiles_x, ws.tile_fill.as<uint32_t>(),
+                                                            ws.tile_slab.as<uint32_t>());
+    ctx->launches++;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t* d_total) {
@@ -324,12 +426,13 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
         if ((e = cudaMemsetAsync(ws.scan_tmp.p, 0, need, ctx->stream))) return e;
         preprocess_scan_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(
             m->params.as<float>(), m->cap, n, m->perm.as<uint32_t>(), lowpass_p, W, H, ws.tiles_x,
-            ws.prep.as<Prepared>(), ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(),
-            ws.tile_fill.as<uint32_t>(), ws.tile_slab.as<uint32_t>(), ws.counters.as<unsigned long long>(),
+            ws.prep.as<Prepared>(), ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(), nullptr,
+            ws.tile_slab.as<uint32_t>(), ws.counters.as<unsigned long long>(),
             reinterpret_cast<unsigned long long*>(ws.scan_tmp.as<char>() + 64), ws.scan_tmp.as<uint32_t>(),
             d_total);
         ctx->launches++;
-        return cudaGetLastError();
+        if ((e = cudaGetLastError())) return e;
+        return launch_claims(ctx, m);
     }
     preprocess_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
         m->params.as<float>(), m->cap, n, m->rank_of.as<uint32_t>(), m->perm.as<uint32_t>(),

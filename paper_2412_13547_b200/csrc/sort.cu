@@ -407,6 +407,7 @@ cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m) {
         m->perm.as<uint32_t>(), m->rank_of.as<uint32_t>(), n);
     ctx->launches++;
     m->order_dirty = false;
+    m->spatial_valid = false;  // the ranks changed: the claim order is rebuilt at the next binning
     return cudaGetLastError();
 }
 

@@ -162,6 +162,9 @@ struct tgsx_model {
     tgsx::DevBuf rank_of;  // u32[cap] index -> rank
     tgsx::DevBuf screen;   // float[10][cap] screen-space grads of the last backward
     tgsx::DevBuf spare[11];  // prune compaction targets (swapped with the live rows; no per-event malloc)
+    tgsx::DevBuf spatial;    // u32[cap] blend ranks in slot-claim (spatial) order (raster.cu launch_claims)
+    bool spatial_valid = false;
+    int spatial_age = 0;
     int64_t step_views = 0;
 };
 
