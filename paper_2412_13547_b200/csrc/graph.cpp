@@ -120,7 +120,7 @@ std::vector<uintptr_t> make_key(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern
                             &m->tau_v, &m->m1, &m->m2, &m->step, &m->perm, &m->rank_of, &m->screen})
         put(k, b->p);
     const Workspace& ws = ctx->ws;
-    for (const DevBuf* b : {&ws.prep, &ws.touched, &ws.pair_off, &ws.scan_tmp, &ws.ranges, &ws.tile_fill,
+    for (const DevBuf* b : {&ws.prep, &ws.touched, &ws.pair_off, &ws.rect, &ws.scan_tmp, &ws.ranges, &ws.tile_fill,
                             &ws.tile_slab, &ws.partial, &ws.rgb, &ws.T, &ws.last, &ws.dLdC, &ws.target,
                             &ws.block_loss, &ws.ssim_abc, &ws.ssim_part, &ws.counters})
         put(k, b->p);

@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(256) preprocess_scan_kernel(
     const float* __restrict__ params, int64_t cap, int64_t n, const uint32_t* __restrict__ perm,
     int lowpass_p, int W, int H, int tiles_x, Prepared* __restrict__ prep, uint32_t* __restrict__ touched,
     uint32_t* __restrict__ pair_off, uint32_t* __restrict__ fill, uint32_t* __restrict__ slab,
-    unsigned long long* err, unsigned long long* status, uint32_t* ticket, uint32_t* d_total) {
+    unsigned long long* err, unsigned long long* status, uint32_t* ticket, uint32_t* d_total,
+    uint2* __restrict__ rect) {
     __shared__ uint32_t s_bid;
     if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
     __syncthreads();
@@ -133,6 +134,8 @@ __global__ void __launch_bounds__(256) preprocess_scan_kernel(
         prep[i] = o;
         touched[i] = tiles;
         pair_off[i] = excl;
+        // compact rectangle for the claim kernel (an empty rectangle has tiles == 0: tx1 < tx0)
+        if (rect) rect[i] = tiles ? make_uint2(o.d.x, o.d.y) : make_uint2(1u, 1u);
         if (tiles && fill) claim_slots(o.d, tiles_x, (uint32_t)i, fill, slab);
     }
 }
@@ -148,17 +151,18 @@ __global__ void __launch_bounds__(256) preprocess_scan_kernel(
 // in blend (depth) order neighbouring threads hit unrelated tiles and every pair was one
 // contended L2 atomic.
 __global__ void __launch_bounds__(256) claim_kernel(const uint32_t* __restrict__ spatial,
-                                                    const Prepared* __restrict__ prep, int64_t n, int tiles_x,
+                                                    const uint2* __restrict__ rect, int64_t n, int tiles_x,
                                                     uint32_t* __restrict__ fill, uint32_t* __restrict__ slab) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     uint32_t rank = 0;
-    uint4 d = make_uint4(0u, 0u, 0u, 0u);
+    uint2 d = make_uint2(1u, 1u);  // empty
     if (i < n) {
         rank = spatial[i];
-        d = __ldg(&prep[rank].d);
+        d = __ldg(&rect[rank]);
     }
-    const uint32_t cnt = d.w;
+    const int rw = (int)(d.x >> 16) - (int)(d.x & 0xffffu) + 1, rh = (int)(d.y >> 16) - (int)(d.y & 0xffffu) + 1;
+    const uint32_t cnt = rw > 0 && rh > 0 ? (uint32_t)(rw * rh) : 0u;
     uint32_t incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -194,12 +198,13 @@ __global__ void __launch_bounds__(256) claim_kernel(const uint32_t* __restrict__
 }
 
 // spatial order key of blend rank r: the top-left tile of its rectangle (unbinned: last)
-__global__ void spatial_keys_kernel(const Prepared* __restrict__ prep, int64_t n, int tiles_x, uint32_t* __restrict__ keys,
+__global__ void spatial_keys_kernel(const uint2* __restrict__ rect, int64_t n, int tiles_x, uint32_t* __restrict__ keys,
                                     uint32_t* __restrict__ vals) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
-    const uint4 d = __ldg(&prep[r].d);
-    keys[r] = d.w ? (d.y & 0xffffu) * (uint32_t)tiles_x + (d.x & 0xffffu) : 0x7fffffffu;
+    const uint2 d = __ldg(&rect[r]);
+    const bool empty = (d.x >> 16) < (d.x & 0xffffu);
+    keys[r] = empty ? 0x7fffffffu : (d.y & 0xffffu) * (uint32_t)tiles_x + (d.x & 0xffffu);
     vals[r] = (uint32_t)r;
 }
 
@@ -383,7 +388,7 @@ cudaError_t launch_claims(tgsx_ctx* ctx, tgsx_model* m) {
         }
         ctx->bin_valid = false;  // the sort reuses the binning buffers
         uint32_t *k = ws.keys[0].as<uint32_t>(), *v = ws.vals[0].as<uint32_t>();
-        spatial_keys_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(ws.prep.as<Prepared>(), n, ws.tiles_x, k, v);
+        spatial_keys_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(ws.rect.as<uint2>(), n, ws.tiles_x, k, v);
         ctx->launches++;
         if ((e = sort_pairs(ctx, k, v, ws.keys[1].as<uint32_t>(), ws.vals[1].as<uint32_t>(), n,
                             key_bits_for(tiles + 1), nullptr)))
@@ -393,7 +398,7 @@ cudaError_t launch_claims(tgsx_ctx* ctx, tgsx_model* m) {
         m->spatial_age = 0;
     }
     ++m->spatial_age;
-    claim_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(m->spatial.as<uint32_t>(), ws.prep.as<Prepared>(), n,
+    claim_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(m->spatial.as<uint32_t>(), ws.rect.as<uint2>(), n,
                                                             ws.tiles_x, ws.tile_fill.as<uint32_t>(),
                                                             ws.tile_slab.as<uint32_t>());
     ctx->launches++;
@@ -407,6 +412,7 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
     if ((e = ws.prep.ensure(std::max<int64_t>(n, 1) * sizeof(Prepared)))) return e;
     if ((e = ws.touched.ensure((n + 1) * 4))) return e;
     if ((e = ws.pair_off.ensure((n + 1) * 4))) return e;
+    if ((e = ws.rect.ensure((n + 1) * 8))) return e;
     ws.tiles_x = (W + kTile - 1) / kTile;
     ws.tiles_y = (H + kTile - 1) / kTile;
     const size_t tiles = (size_t)std::max(ws.tiles_x * ws.tiles_y, 1);
@@ -429,7 +435,7 @@ cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W
             ws.prep.as<Prepared>(), ws.touched.as<uint32_t>(), ws.pair_off.as<uint32_t>(), nullptr,
             ws.tile_slab.as<uint32_t>(), ws.counters.as<unsigned long long>(),
             reinterpret_cast<unsigned long long*>(ws.scan_tmp.as<char>() + 64), ws.scan_tmp.as<uint32_t>(),
-            d_total);
+            d_total, ws.rect.as<uint2>());
         ctx->launches++;
         if ((e = cudaGetLastError())) return e;
         return launch_claims(ctx, m);

@@ -35,6 +35,7 @@ struct Workspace {
     DevBuf prep;        // Prepared[n]
     DevBuf touched;     // u32[n + 1] tiles touched per rank
     DevBuf pair_off;    // u32[n + 1] exclusive scan of touched
+    DevBuf rect;        // uint2[n] tile rectangle per rank (tx0 | tx1 << 16, ty0 | ty1 << 16) for the claims
     DevBuf scan_tmp;    // look-back status
     // binning
     DevBuf keys[2], vals[2];  // u32[K] ping-pong
