@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) claim_kernel(const uint32_t* __restrict__
     uint32_t rank = 0;
     uint2 d = make_uint2(1u, 1u);  // empty
     if (i < n) {
-        rank = spatial[i];
+        rank = __ldcs(spatial + i);
         d = __ldg(&rect[rank]);
     }
     const int rw = (int)(d.x >> 16) - (int)(d.x & 0xffffu) + 1, rh = (int)(d.y >> 16) - (int)(d.y & 0xffffu) + 1;
