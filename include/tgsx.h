@@ -431,6 +431,26 @@ int32_t tgsx_apply_step3d(tgsx_ctx* ctx, tgsx_model3d* m, int32_t batch_views, c
 int32_t tgsx_stage_prepare3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* cam, int32_t lowpass_p,
                              float* out_records, uint32_t* out_keys, int32_t* out_blend_ordered);
 
+/* Densification of the 3-D model (north_star item 4 on the 3-D path). The reference has only the
+ * 2-D densifier; this is the same event on the 3-D parameters, with the SPEC's
+ * statistics mapped to the 3-D front end's (screen-space position-gradient norm, SH-DC colour
+ * norm, visits; accum = visits since the last event, window = visits since the last audit):
+ * colour coin -> select (visits > tau_v, sigmoid(opacity) >= mask floor, averaged position norm >
+ * tau_pos or coin and averaged colour norm > 0.01 tau_pos) -> cap to budget - count (top-k by
+ * averaged position norm, ties by index) -> spawn (child at a point uniform in the parent's
+ * 1-sigma ellipsoid, log-scales - ln 2, quaternion and SH copied, opacity 0.1, 3 PCG32 draws per
+ * child in parent order) -> prune (sigmoid(opacity) < prune floor, order-preserving compaction)
+ * -> reset. Restated in FP64 by oracle/ewa3d.c (or3d_densify_event); no reference code exists
+ * for it. Fails with TGSX_ESTATE while a batched step (tgsx_view_accumulate3d) is pending. */
+int32_t tgsx_densify3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_densify_config* c, int64_t budget,
+                       uint64_t rng_state[2], tgsx_densify_report* out);
+/* update_visit_thresholds on the visits since the last audit. */
+int32_t tgsx_visit_audit3d(tgsx_ctx* ctx, tgsx_model3d* m);
+/* Densification state per Gaussian (any pointer may be NULL): stable ids (0..n-1 at upload,
+ * children numbered from next_id), tau_v, the visit count at the last event / audit. */
+int32_t tgsx_model3d_download_state(tgsx_ctx* ctx, tgsx_model3d* m, uint64_t* ids, double* tau_v,
+                                    int32_t* visit_evt, int32_t* visit_aud, uint64_t* next_id);
+
 /* Diagnostics: measured FP32 throughput of this GPU (8 independent FMA chains per thread, one
  * launch of 8 CTAs x 256 threads per SM) with scalar FFMA and packed FFMA2, in TFLOP/s (FMA = 2
  * flops) — the roofline denominator of the blend kernels. */

@@ -835,3 +835,57 @@ def adam3d_step(params, grads, m, v, cfg: OrAdam3dCfg):
         assert a.dtype == np.float32 and a.flags.c_contiguous
     lib().or3d_adam_step(_ptr(params, f32p), _ptr(grads, f32p), _ptr(m, f32p), _ptr(v, f32p),
                          C.c_int64(n), C.byref(cfg))
+
+
+# ------------------------------------------------------------------ 3-D densification (ewa3d.c)
+class Or3dModel(C.Structure):
+    _fields_ = [("n", C.c_int64), ("cap", C.c_int64), ("params", f32p), ("m1", f32p), ("m2", f32p),
+                ("pos_acc", f32p), ("col_acc", f32p), ("visit", C.POINTER(C.c_int32)),
+                ("visit_evt", C.POINTER(C.c_int32)), ("visit_aud", C.POINTER(C.c_int32)),
+                ("id", C.POINTER(C.c_uint64)), ("tau_v", f64p), ("next_id", C.c_uint64)]
+
+
+def densify3d_event(state: dict, cfg, budget: int, rng: Pcg32):
+    """One 3-D densify event on `state` (dict of numpy arrays: params/m1/m2 [59][n], pos_acc,
+    col_acc f32[n], visit, visit_evt, visit_aud i32[n], ids u64[n], tau_v f64[n], next_id) —
+    or3d_densify_event, the restatement tgsx_densify3d is checked against. Returns the new state
+    (length-n arrays) and (spawned, pruned, candidates, coin)."""
+    n = state["params"].shape[1]
+    cap = n + max(int(budget) - n, 0) + 1
+    pad = lambda a, dt: np.concatenate([np.asarray(a, dt), np.zeros(cap - n, dt)])  # noqa: E731
+    rows = lambda a: np.ascontiguousarray(  # noqa: E731
+        np.concatenate([np.asarray(a, np.float32), np.zeros((N3D, cap - n), np.float32)], axis=1))
+    P_, M1, M2 = rows(state["params"]), rows(state["m1"]), rows(state["m2"])
+    pa, ca = pad(state["pos_acc"], np.float32), pad(state["col_acc"], np.float32)
+    vi, ve, va = (pad(state[k], np.int32) for k in ("visit", "visit_evt", "visit_aud"))
+    ids, tv = pad(state["ids"], np.uint64), pad(state["tau_v"], np.float64)
+    I32 = C.POINTER(C.c_int32)
+    m = Or3dModel(n, cap, _ptr(P_, f32p), _ptr(M1, f32p), _ptr(M2, f32p), _ptr(pa, f32p), _ptr(ca, f32p),
+                  vi.ctypes.data_as(I32), ve.ctypes.data_as(I32), va.ctypes.data_as(I32),
+                  ids.ctypes.data_as(C.POINTER(C.c_uint64)), _ptr(tv, f64p), int(state["next_id"]))
+    sp, pr, nc = C.c_int64(), C.c_int64(), C.c_int64()
+    coin = C.c_int()
+    L = lib()
+    L.or3d_densify_event.restype = C.c_int64
+    L.or3d_densify_event.argtypes = [P(Or3dModel), P(OrDensifyCfg), C.c_int64, P(OrPcg), P(C.c_int64),
+                                     P(C.c_int64), P(C.c_int64), P(C.c_int)]
+    L.or3d_densify_event(C.byref(m), C.byref(cfg), int(budget), C.byref(rng.c), C.byref(sp), C.byref(pr),
+                         C.byref(nc), C.byref(coin))
+    k = m.n
+    out = {"params": P_[:, :k].copy(), "m1": M1[:, :k].copy(), "m2": M2[:, :k].copy(), "pos_acc": pa[:k].copy(),
+           "col_acc": ca[:k].copy(), "visit": vi[:k].copy(), "visit_evt": ve[:k].copy(),
+           "visit_aud": va[:k].copy(), "ids": ids[:k].copy(), "tau_v": tv[:k].copy(), "next_id": m.next_id}
+    return out, (sp.value, pr.value, nc.value, coin.value)
+
+
+def visit_audit3d(state: dict):
+    n = state["params"].shape[1]
+    vi, va = np.ascontiguousarray(state["visit"], np.int32), np.ascontiguousarray(state["visit_aud"], np.int32).copy()
+    tv = np.ascontiguousarray(state["tau_v"], np.float64).copy()
+    I32 = C.POINTER(C.c_int32)
+    dummy = np.zeros(1, np.float32)
+    m = Or3dModel(n, n, _ptr(dummy, f32p), _ptr(dummy, f32p), _ptr(dummy, f32p), _ptr(dummy, f32p),
+                  _ptr(dummy, f32p), vi.ctypes.data_as(I32), vi.ctypes.data_as(I32), va.ctypes.data_as(I32),
+                  None, _ptr(tv, f64p), 0)
+    lib().or3d_visit_audit(C.byref(m))
+    return tv, va

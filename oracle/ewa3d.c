@@ -424,3 +424,138 @@ void or3d_adam_step(float* params, const float* grads, float* m, float* v, int64
         }
     }
 }
+
+/* ---------------------------------------------------------------- 3-D densification
+ * The 2-D densify event (tgs_oracle.c or_densify_event) restated on the 3-D
+ * parameters, the specification the GPU's tgsx_densify3d (csrc/densify3d.cu) is checked
+ * against. No reference code exists for it (the reference densifier is 2-D and missing):
+ *   coin (one draw) -> select: accum = visit - visit_evt > 0, visit > tau_v, activate(raw
+ *   opacity) >= mask floor, averaged position norm > tau_pos or (coin and averaged colour norm >
+ *   tau_color) -> cap to budget - n (top-k by averaged position norm, ties by lower index) ->
+ *   spawn in parent-index order, 3 draws per child: radius cbrt(u1), z = 1 - 2 u2, phi = 2 pi
+ *   u3 -> a point uniform in the unit ball, mapped through R(q) diag(exp(log-scales)) (the
+ *   parent's 1-sigma ellipsoid; double arithmetic, rounded to float at the end); log-scales -
+ *   ln 2 (float), quaternion and SH copied, raw opacity = inverse_activate(0.1), id = next_id++,
+ *   tau_v = tau_v_init, zero statistics and moments -> prune activate(raw opacity) < prune
+ *   floor, order-preserving over every array -> reset (sums zero, visit_evt = visit). */
+static const float* g3_key;
+static int cmp3_desc_key(const void* a, const void* b) {
+    const int64_t i = *(const int64_t*)a, j = *(const int64_t*)b;
+    if (g3_key[i] != g3_key[j]) return g3_key[i] > g3_key[j] ? -1 : 1;
+    return i < j ? -1 : (i > j ? 1 : 0);
+}
+
+static void or3d_copy_row(or3d_model* s, int64_t dst, int64_t src) {
+    const int64_t cap = s->cap;
+    for (int k = 0; k < OR3D_PARAMS; ++k) {
+        s->params[k * cap + dst] = s->params[k * cap + src];
+        s->m1[k * cap + dst] = s->m1[k * cap + src];
+        s->m2[k * cap + dst] = s->m2[k * cap + src];
+    }
+    s->pos_acc[dst] = s->pos_acc[src];
+    s->col_acc[dst] = s->col_acc[src];
+    s->visit[dst] = s->visit[src];
+    s->visit_evt[dst] = s->visit_evt[src];
+    s->visit_aud[dst] = s->visit_aud[src];
+    s->id[dst] = s->id[src];
+    s->tau_v[dst] = s->tau_v[src];
+}
+
+int64_t or3d_densify_event(or3d_model* s, const or_densify_cfg* c, int64_t budget, or_pcg32* rng,
+                           int64_t* out_spawned, int64_t* out_pruned, int64_t* out_candidates,
+                           int* out_coin) {
+    const int64_t cap = s->cap, n0 = s->n;
+    const int coin = or_pcg32_uniform(rng) < (double)c->color_branch_prob;
+    uint8_t* cand = (uint8_t*)calloc((size_t)(n0 ? n0 : 1), 1);
+    float* key = (float*)calloc((size_t)(n0 ? n0 : 1), sizeof(float));
+    int64_t nc = 0;
+    for (int64_t i = 0; i < n0; ++i) {
+        const int32_t cnt = s->visit[i] - s->visit_evt[i];
+        if (cnt > 0 && (double)s->visit[i] > s->tau_v[i] &&
+            or_activatef(s->params[10 * cap + i]) >= c->opacity_mask_floor) {
+            const float cf = (float)cnt;
+            const float ap = s->pos_acc[i] / cf, ac = s->col_acc[i] / cf;
+            key[i] = ap;
+            cand[i] = (ap > c->tau_pos) || (coin && ac > c->tau_color);
+            nc += cand[i];
+        }
+    }
+    int64_t remaining = budget - n0;
+    if (remaining < 0) remaining = 0;
+    if (nc > remaining) {
+        int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)nc);
+        int64_t w = 0;
+        for (int64_t i = 0; i < n0; ++i)
+            if (cand[i]) idx[w++] = i;
+        g3_key = key;
+        qsort(idx, (size_t)nc, sizeof(int64_t), cmp3_desc_key);
+        for (int64_t i = remaining; i < nc; ++i) cand[idx[i]] = 0;
+        free(idx);
+    }
+    const double two_pi = 6.28318530717958647692;
+    const float ln2 = 0.693147180559945309f;
+    int64_t w = n0;
+    for (int64_t i = 0; i < n0; ++i) {
+        if (!cand[i] || w >= cap) continue;
+        const double u1 = or_pcg32_uniform(rng), u2 = or_pcg32_uniform(rng), u3 = or_pcg32_uniform(rng);
+        const double rad = cbrt(u1), z = 1.0 - 2.0 * u2;
+        const double rxy = sqrt(fmax(0.0, 1.0 - z * z)), ph = two_pi * u3;
+        const double e[3] = {rad * rxy * cos(ph), rad * rxy * sin(ph), rad * z};
+        const double qw = s->params[3 * cap + i], qx = s->params[4 * cap + i], qy = s->params[5 * cap + i],
+                     qz = s->params[6 * cap + i];
+        const double qn = sqrt((qw * qw + qx * qx) + (qy * qy + qz * qz));
+        const double r = qw / qn, x = qx / qn, y = qy / qn, zq = qz / qn;
+        const double Q[3][3] = {{1 - 2 * (y * y + zq * zq), 2 * (x * y - r * zq), 2 * (x * zq + r * y)},
+                                {2 * (x * y + r * zq), 1 - 2 * (x * x + zq * zq), 2 * (y * zq - r * x)},
+                                {2 * (x * zq - r * y), 2 * (y * zq + r * x), 1 - 2 * (x * x + y * y)}};
+        double d[3];
+        for (int k = 0; k < 3; ++k) d[k] = exp((double)s->params[(7 + k) * cap + i]) * e[k];
+        for (int k = 0; k < 3; ++k) {
+            const double o = Q[k][0] * d[0] + Q[k][1] * d[1] + Q[k][2] * d[2];
+            s->params[k * cap + w] = (float)((double)s->params[k * cap + i] + o);
+        }
+        for (int k = 3; k < 7; ++k) s->params[k * cap + w] = s->params[k * cap + i];
+        for (int k = 7; k < 10; ++k) s->params[k * cap + w] = s->params[k * cap + i] - ln2;
+        s->params[10 * cap + w] = c->child_raw_opacity;
+        for (int k = 11; k < OR3D_PARAMS; ++k) s->params[k * cap + w] = s->params[k * cap + i];
+        for (int k = 0; k < OR3D_PARAMS; ++k) s->m1[k * cap + w] = s->m2[k * cap + w] = 0.f;
+        s->pos_acc[w] = s->col_acc[w] = 0.f;
+        s->visit[w] = s->visit_evt[w] = s->visit_aud[w] = 0;
+        s->id[w] = s->next_id++;
+        s->tau_v[w] = c->tau_v_init;
+        ++w;
+    }
+    free(cand);
+    free(key);
+    const int64_t spawned = w - n0;
+    s->n = w;
+    int64_t kept = 0;
+    for (int64_t r = 0; r < s->n; ++r) {
+        if (or_activatef(s->params[10 * cap + r]) < c->opacity_prune_floor) continue;
+        if (kept != r) or3d_copy_row(s, kept, r);
+        ++kept;
+    }
+    const int64_t pruned = s->n - kept;
+    s->n = kept;
+    for (int64_t i = 0; i < s->n; ++i) {
+        s->pos_acc[i] = 0.f;
+        s->col_acc[i] = 0.f;
+        s->visit_evt[i] = s->visit[i];
+    }
+    if (out_spawned) *out_spawned = spawned;
+    if (out_pruned) *out_pruned = pruned;
+    if (out_candidates) *out_candidates = nc;
+    if (out_coin) *out_coin = coin;
+    return s->n;
+}
+
+/* update_visit_thresholds SPEC.md:349-357 on the visits since the last audit. */
+void or3d_visit_audit(or3d_model* s) {
+    for (int64_t i = 0; i < s->n; ++i) {
+        if (s->visit[i] - s->visit_aud[i] < 5) {
+            const double t = s->tau_v[i] * 0.5;
+            s->tau_v[i] = t < 1.0 ? 1.0 : t;
+        }
+        s->visit_aud[i] = s->visit[i];
+    }
+}

@@ -125,6 +125,7 @@ int or_sorted_order(const or_scene* s, uint32_t* perm) {
  * rx/ry rasterizer.cpp:40-41. Returns 0, 1 (invalid_argument: non-finite rotation/log-scale,
  * gaussian.hpp:64-68; bad p, dilation.hpp:75) or 2 (runtime_error: det<=0, gaussian.hpp:84-86). */
 static float activate(float raw) { return 1.0f / (1.0f + m_expf(-raw)); }
+float or_activatef(float raw) { return activate(raw); }
 
 static int prepare_one(const or_scene* s, uint32_t idx, int lowpass_p, float* o /*11*/) {
     const float rot = s->rot[idx], lx = s->lsx[idx], ly = s->lsy[idx];

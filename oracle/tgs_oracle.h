@@ -165,6 +165,29 @@ void or3d_adam_config(or3d_adam_cfg* c, int64_t step, int64_t total_steps, doubl
 float or3d_lr(const or3d_adam_cfg* c, int k);
 void or3d_adam_step(float* params, const float* grads, float* m, float* v, int64_t n,
                     const or3d_adam_cfg* c);
+/* activate (gaussian.hpp:47-49) in float with the oracle's expf (libm or correctly rounded) */
+float or_activatef(float raw);
+/* Densification of the 3-D model (the 2-D densify event of SPEC.md:300-383 on the 3-D
+ * parameters; the GPU counterpart is tgsx_densify3d). Arrays are capacity-strided like the
+ * device model ([59][cap] params and moments); accum = visit - visit_evt. */
+typedef struct {
+    int64_t n, cap;
+    float* params;          /* [59][cap] */
+    float* m1;              /* [59][cap] */
+    float* m2;              /* [59][cap] */
+    float* pos_acc;
+    float* col_acc;
+    int32_t* visit;
+    int32_t* visit_evt;
+    int32_t* visit_aud;
+    uint64_t* id;
+    double* tau_v;
+    uint64_t next_id;
+} or3d_model;
+int64_t or3d_densify_event(or3d_model* s, const or_densify_cfg* c, int64_t budget, or_pcg32* rng,
+                           int64_t* out_spawned, int64_t* out_pruned, int64_t* out_candidates,
+                           int* out_coin);
+void or3d_visit_audit(or3d_model* s);
 
 #ifdef __cplusplus
 }

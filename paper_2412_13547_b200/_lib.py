@@ -159,6 +159,9 @@ SIGNATURES = {
     "tgsx_model3d_upload": (C.c_int32, [vp, vp, vp, C.c_int64]),
     "tgsx_model3d_download": (C.c_int32, [vp, vp, vp, vp, vp, vp]),
     "tgsx_model3d_download_moments": (C.c_int32, [vp, vp, vp, vp]),
+    "tgsx_model3d_download_state": (C.c_int32, [vp, vp, vp, vp, vp, vp, u64p]),
+    "tgsx_densify3d": (C.c_int32, [vp, vp, P(DensifyConfig), C.c_int64, u64p, P(DensifyReport)]),
+    "tgsx_visit_audit3d": (C.c_int32, [vp, vp]),
     "tgsx_render3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, C.c_int32, vp, vp, u64p]),
     "tgsx_backward3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, C.c_int32, vp, C.c_int64,
                                     vp, vp, C.c_int32]),

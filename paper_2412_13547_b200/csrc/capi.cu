@@ -948,6 +948,10 @@ cudaError_t model3d_reserve(tgsx_ctx* ctx, tgsx_model3d* m, int64_t cap, bool ke
     if ((e = regrow(m->col_acc, 1, 4))) return e;
     if ((e = regrow(m->visit, 1, 4))) return e;
     if ((e = regrow(m->step, k3dStepRows, 4))) return e;
+    if ((e = regrow(m->ids, 1, 8))) return e;
+    if ((e = regrow(m->tau_v, 1, 8))) return e;
+    if ((e = regrow(m->visit_evt, 1, 4))) return e;
+    if ((e = regrow(m->visit_aud, 1, 4))) return e;
     if ((e = m->perm.ensure(nc * 4))) return e;
     if ((e = m->rank_of.ensure(nc * 4))) return e;
     if ((e = m->prep_row.ensure(nc * sizeof(Prepared)))) return e;
@@ -956,6 +960,8 @@ cudaError_t model3d_reserve(tgsx_ctx* ctx, tgsx_model3d* m, int64_t cap, bool ke
 }
 
 }  // namespace
+
+cudaError_t model3d_grow(tgsx_ctx* ctx, tgsx_model3d* m, int64_t cap) { return model3d_reserve(ctx, m, cap, true); }
 
 // ============================================================================ C ABI
 extern "C" {
@@ -1642,9 +1648,11 @@ int32_t tgsx_model3d_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model3d** out)
 
 void tgsx_model3d_destroy(tgsx_model3d* m) {
     if (!m) return;
-    DevBuf* bufs[] = {&m->params, &m->m1, &m->m2, &m->pos_acc, &m->col_acc, &m->visit,
-                      &m->perm, &m->rank_of, &m->prep_row, &m->gbuf, &m->step, &m->skeys};
+    DevBuf* bufs[] = {&m->params, &m->m1,    &m->m2,       &m->pos_acc,   &m->col_acc, &m->visit,
+                      &m->perm,   &m->rank_of, &m->prep_row, &m->gbuf,      &m->step,    &m->skeys,
+                      &m->ids,    &m->tau_v, &m->visit_evt, &m->visit_aud};
     for (DevBuf* b : bufs) b->release();
+    for (DevBuf& b : m->spare) b.release();
     delete m;
 }
 
@@ -1664,6 +1672,10 @@ int32_t tgsx_model3d_upload(tgsx_ctx* ctx, tgsx_model3d* m, const float* params,
     CK(cudaMemsetAsync(m->col_acc.p, 0, m->col_acc.bytes, s));
     CK(cudaMemsetAsync(m->visit.p, 0, m->visit.bytes, s));
     CK(cudaMemsetAsync(m->step.p, 0, m->step.bytes, s));
+    CK(cudaMemsetAsync(m->visit_evt.p, 0, m->visit_evt.bytes, s));
+    CK(cudaMemsetAsync(m->visit_aud.p, 0, m->visit_aud.bytes, s));
+    CK(densify3d_init_rows(ctx, m, 0, n));  // ids 0..n-1, tau_v = tau_v_init default
+    m->next_id = (uint64_t)n;
     m->step_views = 0;
     CK(cudaStreamSynchronize(s));
     return TGSX_OK;

@@ -185,6 +185,15 @@ struct tgsx_model3d {
     tgsx::DevBuf skeys;             // u32[cap] sorted depth keys of the global-sort path (parity stage)
     bool rank_ordered = false;      // last binning: records / pair slots by blend rank (global-sort
                                     // path) rather than by row (per-tile path)
+    // densification state (densify3d.cu; the 2-D DensifyStats analogues):
+    // stable ids, per-Gaussian visit threshold, and the visit count at the last densify event /
+    // visit audit (accum = visit - visit_evt, window = visit - visit_aud: the fit kernels only
+    // ever increment `visit`)
+    tgsx::DevBuf ids;               // u64[cap]
+    tgsx::DevBuf tau_v;             // f64[cap]
+    tgsx::DevBuf visit_evt, visit_aud;  // i32[cap]
+    uint64_t next_id = 0;
+    tgsx::DevBuf spare[11];         // prune compaction targets (swapped with the live rows)
 };
 
 namespace tgsx {
@@ -197,6 +206,9 @@ void graph_release(tgsx_ctx* ctx);
 // physical row order of the model (capi.cu): blend order for the hot path, logical (creation)
 // order for densify / download / explicit-gradient APIs
 cudaError_t model_to_blend_order(tgsx_ctx* ctx, tgsx_model* m);
+cudaError_t model3d_grow(tgsx_ctx* ctx, tgsx_model3d* m, int64_t cap);  // keeps the live rows
+// ids = i, tau_v = SPEC default tau_v_init for rows [i0, i1) of a freshly uploaded 3-D model
+cudaError_t densify3d_init_rows(tgsx_ctx* ctx, tgsx_model3d* m, int64_t i0, int64_t i1);
 cudaError_t model_to_logical_order(tgsx_ctx* ctx, tgsx_model* m);
 // capacity growth keeping contents, spare row buffers sized alongside (capi.cu)
 cudaError_t model_grow(tgsx_ctx* ctx, tgsx_model* m, int64_t cap);

@@ -164,6 +164,33 @@ class DeviceModel3D:
         self.ctx.check(self.ctx.L.tgsx_model3d_download_moments(self.ctx.h, self.h, _ptr(m1), _ptr(m2)))
         return m1, m2
 
+    def densify_state(self):
+        """(ids u64[n], tau_v f64[n], visit count at the last densify event i32[n], at the last
+        audit i32[n], next id) — tgsx_model3d_download_state."""
+        n = self.size()
+        ids, tau = np.zeros(n, np.uint64), np.zeros(n, np.float64)
+        ve, va = np.zeros(n, np.int32), np.zeros(n, np.int32)
+        nxt = C.c_uint64()
+        self.ctx.check(self.ctx.L.tgsx_model3d_download_state(self.ctx.h, self.h, _ptr(ids), _ptr(tau), _ptr(ve),
+                                                              _ptr(va), C.byref(nxt)))
+        return ids, tau, ve, va, int(nxt.value)
+
+    def densify(self, budget: int, rng_state: np.ndarray, config=None):
+        """One densify event on the 3-D model (tgsx_densify3d: the SPEC's 2-D event on the 3-D
+        parameters — select, top-k under the budget, spawn inside the parent's 1-sigma ellipsoid,
+        prune, reset). rng_state (uint64[2], PCG32) is advanced in place."""
+        from .api import densify_config
+        cfg = config or densify_config()
+        rep = _lib.DensifyReport()
+        st = np.ascontiguousarray(rng_state, np.uint64)
+        self.ctx.check(self.ctx.L.tgsx_densify3d(self.ctx.h, self.h, C.byref(cfg), int(budget),
+                                                 st.ctypes.data_as(_lib.u64p), C.byref(rep)))
+        rng_state[:] = st
+        return rep
+
+    def visit_audit(self):
+        self.ctx.check(self.ctx.L.tgsx_visit_audit3d(self.ctx.h, self.h))
+
     def close(self):
         if getattr(self, "h", None):
             self.ctx.L.tgsx_model3d_destroy(self.h)

@@ -218,3 +218,58 @@ def test_adam3d_first_step_moves_by_lr():
     assert p[10, 0] == pytest.approx(-5e-2, rel=1e-5)
     assert p[11, 0] == pytest.approx(-2.5e-3, rel=1e-5)
     assert p[20, 0] == pytest.approx(-2.5e-3 / 20, rel=1e-5)
+
+
+# ---------------------------------------------------------------- 3-D densify (SPEC examples)
+def _dstate(n, seed=0, pos=1e-2, visits=10):
+    rng = np.random.default_rng(seed)
+    P = rng.normal(size=(59, n)).astype(np.float32)
+    P[3] = 1.0 + np.abs(P[3])
+    P[10] = 1.0  # opacity 0.73: above both floors
+    return {"params": P, "m1": np.zeros((59, n), np.float32), "m2": np.zeros((59, n), np.float32),
+            "pos_acc": rng.uniform(0.5, 1.0, n).astype(np.float32) * pos,
+            "col_acc": np.zeros(n, np.float32), "visit": np.full(n, visits, np.int32),
+            "visit_evt": np.zeros(n, np.int32), "visit_aud": np.zeros(n, np.int32),
+            "ids": np.arange(n, dtype=np.uint64), "tau_v": np.full(n, 5.0), "next_id": n}
+
+
+def test_densify3d_spec_examples():
+    """SPEC.md:330-347 examples on the 3-D restatement: budget 0 -> unchanged; 10 candidates,
+    budget 4 -> the 4 highest averaged position norms spawn; one candidate -> one child inside
+    the parent's 1-sigma ellipsoid at half scale; all below the prune floor -> empty."""
+    B.set_math(True)
+    cfg = B.densify_config(2e-4)
+    s = _dstate(10)
+    out, (sp, pr, nc, _) = B.densify3d_event(s, cfg, 10, B.Pcg32(1, 1))
+    assert (sp, pr, nc) == (0, 0, 10) and np.array_equal(out["params"], s["params"])
+    out, (sp, _, _, _) = B.densify3d_event(s, cfg, 14, B.Pcg32(1, 1))
+    top = np.argsort(-(s["pos_acc"] / 10.0), kind="stable")[:4]
+    assert sp == 4 and out["params"].shape[1] == 14
+    assert np.array_equal(np.sort(np.nonzero(np.isin(np.arange(10), top))[0]),
+                          np.sort([int(np.nonzero((out["params"][11:, 10 + j][:, None] == s["params"][11:]).all(0))[0][0])
+                                   for j in range(4)]))
+    one = _dstate(1, seed=3)
+    out, (sp, _, _, _) = B.densify3d_event(one, cfg, 100, B.Pcg32(2, 1))
+    assert sp == 1
+    th, ch = one["params"][:, 0].astype(np.float64), out["params"][:, 1].astype(np.float64)
+    w, x, y, z = th[3:7] / np.linalg.norm(th[3:7])
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                  [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                  [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+    d = R.T @ (ch[:3] - th[:3]) / np.exp(th[7:10])
+    assert np.linalg.norm(d) <= 1.0 + 1e-6
+    assert np.allclose(ch[7:10], th[7:10] - np.log(2.0), atol=1e-6)
+    assert abs(1.0 / (1.0 + np.exp(-ch[10])) - 0.1) < 1e-6 and out["ids"][1] == 1 and out["next_id"] == 2
+    low = _dstate(5)
+    low["params"][10] = -8.0
+    out, (_, pr, _, _) = B.densify3d_event(low, cfg, 100, B.Pcg32(1, 1))
+    assert pr == 5 and out["params"].shape[1] == 0
+
+
+def test_visit_audit3d_spec_examples():
+    """v = 10, tau 8 -> 8; v = 3, tau 8 -> 4; v = 0, tau 1 -> 1."""
+    s = _dstate(3)
+    s["visit"] = np.array([10, 3, 0], np.int32)
+    s["tau_v"] = np.array([8.0, 8.0, 1.0])
+    tv, va = B.visit_audit3d(s)
+    assert list(tv) == [8.0, 4.0, 1.0] and list(va) == [10, 3, 0]
