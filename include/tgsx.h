@@ -392,6 +392,8 @@ typedef struct {
 int32_t tgsx_model3d_create(tgsx_ctx* ctx, int64_t capacity, tgsx_model3d** out);
 void tgsx_model3d_destroy(tgsx_model3d* m);
 int64_t tgsx_model3d_size(const tgsx_model3d* m);
+/* Grows the capacity (rows kept) so later densify events allocate nothing. */
+int32_t tgsx_model3d_reserve(tgsx_ctx* ctx, tgsx_model3d* m, int64_t capacity);
 /* params host or device float[59][n]; zeroes the Adam moments and statistics. */
 int32_t tgsx_model3d_upload(tgsx_ctx* ctx, tgsx_model3d* m, const float* params, int64_t n);
 /* Any pointer may be NULL. Statistics: screen-space position-gradient norm sum, SH-DC
@@ -446,6 +448,22 @@ int32_t tgsx_densify3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_densify_config
                        uint64_t rng_state[2], tgsx_densify_report* out);
 /* update_visit_thresholds on the visits since the last audit. */
 int32_t tgsx_visit_audit3d(tgsx_ctx* ctx, tgsx_model3d* m);
+/* The SPEC fit loop (tgsx_trainer_*) over a set of cameras of a 3-D model:
+ * view (t - 1) mod n_cams at iteration t; dilated warm-up with cycled offsets; densify every
+ * densify_interval with the convergence-aware budget (tgsx_densify3d); after densify_until a
+ * dilation coin per iteration, dense iterations with the SSIM term; the last batch_final_iters
+ * iterations accumulate batch_size distinct cameras and take one Adam step on the mean; visit
+ * audits every n_views iterations. Adam: tgsx_adam3d_args with scene_extent. targets[v]: the
+ * full-resolution RGB of camera v (host or device), n_targets == n_cams. */
+typedef struct tgsx_trainer3d tgsx_trainer3d;
+int32_t tgsx_trainer3d_create(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_train_config* cfg,
+                              const tgsx_camera* cams, int32_t n_cams, double scene_extent,
+                              tgsx_trainer3d** out);
+void tgsx_trainer3d_destroy(tgsx_trainer3d* tr);
+int32_t tgsx_trainer3d_step(tgsx_trainer3d* tr, const float* const* targets, int64_t n_targets,
+                            tgsx_train_report* report);
+/* Per-iteration losses of the last min(ring, t) iterations, oldest first. */
+int32_t tgsx_trainer3d_losses(tgsx_trainer3d* tr, float* out, int64_t max_out, int64_t* out_n);
 /* Densification state per Gaussian (any pointer may be NULL): stable ids (0..n-1 at upload,
  * children numbered from next_id), tau_v, the visit count at the last event / audit. */
 int32_t tgsx_model3d_download_state(tgsx_ctx* ctx, tgsx_model3d* m, uint64_t* ids, double* tau_v,

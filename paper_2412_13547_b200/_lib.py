@@ -162,6 +162,11 @@ SIGNATURES = {
     "tgsx_model3d_download_state": (C.c_int32, [vp, vp, vp, vp, vp, vp, u64p]),
     "tgsx_densify3d": (C.c_int32, [vp, vp, P(DensifyConfig), C.c_int64, u64p, P(DensifyReport)]),
     "tgsx_visit_audit3d": (C.c_int32, [vp, vp]),
+    "tgsx_model3d_reserve": (C.c_int32, [vp, vp, C.c_int64]),
+    "tgsx_trainer3d_create": (C.c_int32, [vp, vp, P(TrainConfig), P(Camera3), C.c_int32, C.c_double, P(vp)]),
+    "tgsx_trainer3d_destroy": (None, [vp]),
+    "tgsx_trainer3d_step": (C.c_int32, [vp, P(vp), C.c_int64, P(TrainReport)]),
+    "tgsx_trainer3d_losses": (C.c_int32, [vp, f32p, C.c_int64, i64p]),
     "tgsx_render3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, C.c_int32, vp, vp, u64p]),
     "tgsx_backward3d": (C.c_int32, [vp, vp, P(Camera3), P(Pattern), f32p, C.c_int32, vp, C.c_int64,
                                     vp, vp, C.c_int32]),

@@ -1658,6 +1658,14 @@ void tgsx_model3d_destroy(tgsx_model3d* m) {
 
 int64_t tgsx_model3d_size(const tgsx_model3d* m) { return m ? m->n : 0; }
 
+int32_t tgsx_model3d_reserve(tgsx_ctx* ctx, tgsx_model3d* m, int64_t capacity) {
+    if (!ctx || !m || capacity < 0) return TGSX_EINVAL;
+    if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
+    ctx->bin_valid = false;
+    CK(model3d_reserve(ctx, m, capacity, true));
+    return TGSX_OK;
+}
+
 int32_t tgsx_model3d_upload(tgsx_ctx* ctx, tgsx_model3d* m, const float* params, int64_t n) {
     if (!ctx || !m || n < 0 || (n && !params)) return fail(ctx, TGSX_EINVAL, "bad 3-D upload arguments");
     ctx->bin_valid = false;

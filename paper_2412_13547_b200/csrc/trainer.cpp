@@ -41,9 +41,29 @@ struct tgsx_trainer {
     double last_budget = 0;
 };
 
+// The same schedule over a set of cameras of a 3-D model (tgsx_trainer3d_*).
+struct tgsx_trainer3d {
+    tgsx_ctx* ctx = nullptr;
+    tgsx_model3d* m = nullptr;
+    tgsx_train_config cfg{};
+    std::vector<tgsx_camera> cams;
+    double extent = 1.0;
+    tgsx_budget* budget = nullptr;
+    uint64_t rng[2] = {0, 0};
+    int64_t t = 0;
+    int64_t adam_step = 0;
+    int64_t n_init = 0;
+    float* d_losses = nullptr;
+    int64_t ring = 0;
+    int64_t fed = 0;
+    float* h_pinned = nullptr;
+    double last_budget = 0;
+};
+
 namespace {
 
-int32_t feed_losses(tgsx_trainer* tr) {
+template <typename TR>
+int32_t feed_losses(TR* tr) {
     const int64_t pending = tr->t - tr->fed;
     if (pending <= 0) return TGSX_OK;
     if (cudaMemcpyAsync(tr->h_pinned, tr->d_losses, sizeof(float) * tr->ring, cudaMemcpyDeviceToHost,
@@ -212,6 +232,134 @@ int32_t tgsx_trainer_rng(const tgsx_trainer* tr, uint64_t out_state[2]) {
     if (!tr || !out_state) return TGSX_EINVAL;
     out_state[0] = tr->rng[0];
     out_state[1] = tr->rng[1];
+    return TGSX_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- 3-D trainer
+extern "C" {
+
+int32_t tgsx_trainer3d_create(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_train_config* cfg,
+                              const tgsx_camera* cams, int32_t n_cams, double scene_extent,
+                              tgsx_trainer3d** out) {
+    if (!ctx || !m || !cfg || !cams || n_cams < 1 || !out || !(scene_extent > 0)) return TGSX_EINVAL;
+    if (cfg->dilation_p < 1 || cfg->batch_size < 1 || cfg->densify_interval < 1) return TGSX_EINVAL;
+    if (!(cfg->ssim_weight >= 0.f && cfg->ssim_weight <= 1.f)) return TGSX_EINVAL;
+    if (!(cfg->warmup_iters <= cfg->densify_until && cfg->densify_until <= cfg->total_iters)) return TGSX_EINVAL;
+    for (int32_t v = 0; v < n_cams; ++v)
+        if (cams[v].width < 1 || cams[v].height < 1) return TGSX_EINVAL;
+    tgsx_trainer3d* tr = new (std::nothrow) tgsx_trainer3d();
+    if (!tr) return TGSX_ENOMEM;
+    tr->ctx = ctx;
+    tr->m = m;
+    tr->cfg = *cfg;
+    tr->cams.assign(cams, cams + n_cams);
+    tr->extent = scene_extent;
+    tr->n_init = tgsx_model3d_size(m);
+    const double mf = cfg->m_final > 0 ? cfg->m_final : 1.5 * (double)tr->n_init;
+    tgsx_budget_create((double)tr->n_init, mf, &tr->budget);
+    if (cfg->densify_until > cfg->warmup_iters) {
+        const int32_t rc = tgsx_model3d_reserve(ctx, m, (int64_t)std::ceil(1.5 * mf) + 1024);
+        if (rc) {
+            tgsx_budget_destroy(tr->budget);
+            delete tr;
+            return rc;
+        }
+    }
+    tgsx_pcg32_init(tr->rng, cfg->seed, 1);
+    tr->ring = std::max<int64_t>(cfg->densify_interval, 1) * 4 + 64;
+    if (cudaMalloc(&tr->d_losses, sizeof(float) * tr->ring) != cudaSuccess ||
+        cudaMallocHost(&tr->h_pinned, sizeof(float) * tr->ring) != cudaSuccess) {
+        tgsx_trainer3d_destroy(tr);
+        return TGSX_ECUDA;
+    }
+    cudaMemset(tr->d_losses, 0, sizeof(float) * tr->ring);
+    *out = tr;
+    return TGSX_OK;
+}
+
+void tgsx_trainer3d_destroy(tgsx_trainer3d* tr) {
+    if (!tr) return;
+    if (tr->budget) tgsx_budget_destroy(tr->budget);
+    if (tr->d_losses) cudaFree(tr->d_losses);
+    if (tr->h_pinned) cudaFreeHost(tr->h_pinned);
+    delete tr;
+}
+
+int32_t tgsx_trainer3d_step(tgsx_trainer3d* tr, const float* const* targets, int64_t n_targets,
+                            tgsx_train_report* rep) {
+    if (!tr || !targets || n_targets != (int64_t)tr->cams.size()) return TGSX_EINVAL;
+    const tgsx_train_config& c = tr->cfg;
+    const int64_t t = tr->t + 1;
+    const int64_t nv = (int64_t)tr->cams.size();
+    const float* bg = c.background;
+    tgsx_train_report r{};
+    r.iteration = t;
+    const int64_t final_start = c.total_iters - c.batch_final_iters;
+    float* dloss = tr->d_losses + (t - 1) % tr->ring;
+    int32_t rc = TGSX_OK;
+    const int p = c.dilation_p;
+    if (t > final_start && c.batch_size > 1) {
+        // batched finale: batch_size distinct cameras (cycled offsets), mean, one Adam step
+        for (int32_t b = 0; b < c.batch_size; ++b) {
+            const int64_t k = (t - 1) * c.batch_size + b;
+            const tgsx_camera& cam = tr->cams[k % nv];
+            const int64_t idx = k % ((int64_t)p * p);
+            tgsx_pattern pat{p, (int32_t)(idx % p), (int32_t)(idx / p), cam.width, cam.height};
+            if ((rc = tgsx_view_accumulate3d(tr->ctx, tr->m, &cam, &pat, bg, targets[k % nv], b == 0 ? dloss : nullptr)))
+                return rc;
+        }
+        tgsx_adam3d_args a{++tr->adam_step, c.total_iters, tr->extent};
+        if ((rc = tgsx_apply_step3d(tr->ctx, tr->m, c.batch_size, &a))) return rc;
+        r.dilated = 1;
+    } else {
+        int dilate = 1;
+        if (t > c.densify_until) dilate = tgsx_pcg32_uniform(tr->rng) < (double)c.post_densify_dilation_prob;
+        const int pp = dilate ? p : 1;
+        const tgsx_camera& cam = tr->cams[(t - 1) % nv];
+        const int64_t idx = ((t - 1) / nv) % ((int64_t)pp * pp);  // offsets cycle per pass over the cameras
+        tgsx_pattern pat{pp, (int32_t)(idx % pp), (int32_t)(idx / pp), cam.width, cam.height};
+        tgsx_adam3d_args a{++tr->adam_step, c.total_iters, tr->extent};
+        if ((rc = tgsx_set_ssim_weight(tr->ctx, pp == 1 ? c.ssim_weight : 0.f))) return rc;
+        rc = tgsx_fit_step3d(tr->ctx, tr->m, &cam, &pat, bg, targets[(t - 1) % nv], &a, dloss);
+        tgsx_set_ssim_weight(tr->ctx, 0.f);
+        if (rc) return rc;
+        r.dilated = dilate;
+    }
+    tr->t = t;
+    if (tr->t - tr->fed >= tr->ring / 2 && (rc = feed_losses(tr))) return rc;
+    if (t > c.warmup_iters && t <= c.densify_until && t % c.densify_interval == 0) {
+        if ((rc = feed_losses(tr))) return rc;
+        tgsx_budget_update(tr->budget, t);
+        const double tn = tgsx_budget_t_norm(t, c.warmup_iters, c.densify_until);
+        const int64_t B = tgsx_budget_at(tr->budget, tn);
+        tgsx_densify_report dr{};
+        if ((rc = tgsx_densify3d(tr->ctx, tr->m, &c.densify, B, tr->rng, &dr))) return rc;
+        r.densified = 1;
+        r.budget = B;
+        r.spawned = dr.spawned;
+        r.pruned = dr.pruned;
+        tr->last_budget = (double)B;
+    }
+    if (c.n_views > 0 && t % c.n_views == 0) {
+        if ((rc = tgsx_visit_audit3d(tr->ctx, tr->m))) return rc;
+    }
+    r.count = tgsx_model3d_size(tr->m);
+    r.budget = r.budget ? r.budget : (int64_t)tr->last_budget;
+    if (rep) *rep = r;
+    return TGSX_OK;
+}
+
+int32_t tgsx_trainer3d_losses(tgsx_trainer3d* tr, float* out, int64_t max_out, int64_t* out_n) {
+    if (!tr) return TGSX_EINVAL;
+    if (feed_losses(tr)) return TGSX_ECUDA;
+    const int64_t n = std::min<int64_t>(std::min<int64_t>(tr->t, tr->ring), max_out);
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t it = tr->t - n + 1 + k;
+        out[k] = tr->h_pinned[(it - 1) % tr->ring];
+    }
+    if (out_n) *out_n = n;
     return TGSX_OK;
 }
 

@@ -302,3 +302,50 @@ class DeviceModel3D:
 
 
 __all__ = ["Camera", "GaussianModel3D", "DeviceModel3D", "N_PARAMS", "SH_C0"]
+
+
+class Trainer3D:
+    """The SPEC fit loop (warm-up, densify every 20 with the convergence-aware budget, post-densify
+    random dilation with SSIM on dense iterations, batched finale, visit audits) over a set of
+    cameras of a DeviceModel3D (libtgsx tgsx_trainer3d_*, csrc/trainer.cpp)."""
+
+    def __init__(self, dm: DeviceModel3D, cameras, scene_extent: float, config=None, **kw):
+        from .api import train_config
+        self.dm = dm
+        self.cfg = config or train_config(**kw)
+        self.cams = (_lib.Camera3 * len(cameras))(*[c.c() for c in cameras])
+        h = C.c_void_p()
+        dm.ctx.check(dm.ctx.L.tgsx_trainer3d_create(dm.ctx.h, dm.h, C.byref(self.cfg), self.cams, len(cameras),
+                                                    float(scene_extent), C.byref(h)))
+        self.h = h
+        self._targets = None
+
+    def set_targets(self, targets):
+        """targets[v]: camera v's (H, W, 3) float32 host array or device pointer (int)."""
+        self._keep = [t if isinstance(t, int) else _f32(t) for t in targets]
+        ptrs = [t if isinstance(t, int) else t.ctypes.data for t in self._keep]
+        self._targets = (C.c_void_p * len(ptrs))(*ptrs)
+
+    def step(self) -> _lib.TrainReport:
+        rep = _lib.TrainReport()
+        self.dm.ctx.check(self.dm.ctx.L.tgsx_trainer3d_step(self.h, self._targets, len(self._targets),
+                                                            C.byref(rep)))
+        return rep
+
+    def losses(self, max_n: int = 4096) -> np.ndarray:
+        out = np.zeros(max_n, np.float32)
+        n = C.c_int64()
+        self.dm.ctx.check(self.dm.ctx.L.tgsx_trainer3d_losses(self.h, out.ctypes.data_as(_lib.f32p), max_n,
+                                                              C.byref(n)))
+        return out[:n.value]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.dm.ctx.L.tgsx_trainer3d_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
