@@ -68,6 +68,12 @@ CONFIGS = {
                         "post-densify random dilation with dense L1 + 0.2 SSIM iterations, batched finale of "
                         "100 iterations x 4 views); the whole schedule is one timed region",
                n=3_000_000, W=3840, H=2160, p=2, iters=1000, views=16),
+    "c9": dict(workload="C9-3D: full Turbo-GS fit schedule on the 3-D front end — 1M initial 3-D Gaussians SH3, 8 "
+                        "distinct 1080p cameras, 600 iterations (warm-up 100 dilated p=2, densify every 20 until 400 "
+                        "with the convergence-aware budget M = 1.5 N0 (tau_pos 6e-8, ~90th percentile of the averaged "
+                        "screen-space position norm), post-densify random dilation with dense L1 + 0.2 SSIM, batched "
+                        "finale of 50 iterations x 4 cameras); the whole schedule is one timed region",
+               n=1_000_000, W=1920, H=1080, p=2, iters=600, views=8, three_d=True),
 }
 METRIC = "fit iters/sec (fwd+bwd+Adam) at 1080p and 4K dilated, 1M–3M Gaussians"
 
@@ -466,6 +472,61 @@ def measure_fit4k(args, env):
                     "events_first_last": [events[0], events[-1]] if events else []}}
 
 
+def measure_fit3d(args, env):
+    """C9: the SPEC fit schedule on the 3-D front end (tgsx_trainer3d_*: 3-D densification with the
+    budget controller) as one timed region on one GPU; final PSNR against the target renders."""
+    torch, P, ctx = env["torch"], env["P"], env["ctx"]
+    from paper_2412_13547_b200 import scene3d as S3
+    cfg = CONFIGS["c9"]
+    W, H, n, p, iters, views = cfg["W"], cfg["H"], cfg["n"], cfg["p"], cfg["iters"], cfg["views"]
+    fx = 0.5 * W / math.tan(math.radians(30))
+    cams = [S3.Camera.look_at((0.3 * math.cos(a), 0.2 * math.sin(a), 0.0), (0.0, 0.0, 4.5), (0, -1, 0), 60.0, W, H)
+            for a in np.linspace(0, 2 * math.pi, views, endpoint=False)]
+    cam0 = S3.Camera(np.eye(3), np.zeros(3), fx, fx, W / 2, H / 2, W, H)
+    dm = S3.DeviceModel3D.from_host(S3.GaussianModel3D.synthetic(1, n, cam0), ctx)
+    tm = S3.DeviceModel3D.from_host(S3.GaussianModel3D.synthetic(2, n, cam0), ctx)
+    targets = [torch.from_numpy(tm.render(c).colors.reshape(H, W, 3).copy()).cuda().contiguous() for c in cams]
+    tm.close()
+    tcfg = P.train_config(total_iters=iters, warmup_iters=100, densify_interval=20, densify_until=400,
+                          batch_final_iters=50, batch_size=4, dilation_p=p, n_views=views, m_final=1.5 * n, seed=1)
+    tcfg.densify.tau_pos = 6e-8
+    trainer = S3.Trainer3D(dm, cams, 3.0, tcfg)
+    trainer.set_targets([t.data_ptr() for t in targets])
+    stream = torch.cuda.ExternalStream(ctx.L.tgsx_get_stream(ctx.h))
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    reports = []
+    launches0 = ctx.launches
+    with ClockSampler(env["local"]) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            reports.append(trainer.step())
+        e1.record(stream)
+        e1.synchronize()
+        ctx.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - launches0
+    losses = trainer.losses(100)
+    mse = float(np.mean([float(((torch.from_numpy(dm.render(c).colors.reshape(H, W, 3).copy()).cuda() - t) ** 2).mean())
+                         for c, t in zip(cams, targets)]))
+    events = [(r.iteration, r.budget, r.count, r.spawned, r.pruned) for r in reports if r.densified]
+    trainer.close()
+    dm.close()
+    return {"value": iters / (ms / 1e3), "unit": "iters/s", "n_gpus": 1, "steps": iters, "warmup": 0,
+            "ms_per_step": ms / iters, "fit_seconds": ms / 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "gaussians": n, "width": W, "height": H, "p": p,
+                       "views": views, "l2": "per-step working set > 126 MB L2 (no explicit flush)"},
+            "clocks": clk.summary(), "gpu_launches": launches,
+            "e2e": {"value": None, "unit": "iters/s", "note": "the fit loop runs device-resident targets"},
+            "fit": {"densify_events": len(events), "budget_respected": all(c <= b for _, b, c, _, _ in events),
+                    "count_start": n, "count_end": int(reports[-1].count), "spawned": int(sum(e[3] for e in events)),
+                    "pruned": int(sum(e[4] for e in events)), "loss_first": float(losses[0]),
+                    "loss_last": float(losses[-1]), "psnr_db": 10.0 * math.log10(1.0 / mse) if mse > 0 else None,
+                    "events_first_last": [events[0], events[-1]] if events else []}}
+
+
 def run_tgsx(args):
     """All ranks: set up the process group, the context (+ the library NCCL communicator for
     N > 1), measure the requested config; with the default config (C2) also the sub-records of
@@ -494,13 +555,19 @@ def run_tgsx(args):
         if world > 1:
             raise SystemExit("c8 (the whole 4K fit schedule) runs on one GPU: --gpus 1")
         line = dict(metric=METRIC, **measure_fit4k(args, env))
+    elif args.config == "c9":
+        if world > 1:
+            raise SystemExit("c9 (the 3-D fit schedule) runs on one GPU: --gpus 1")
+        line = dict(metric=METRIC, **measure_fit3d(args, env))
     else:
         line = measure(args, args.config, env)
     if args.config == "c2" and args.ssim == 0 and not args.no_subrecords:
         subs = {}
-        for name in (["c1"] if world == 1 else []) + ["c3", "c5"] + (["c8", "c2_ssim"] if world == 1 else []):
+        for name in (["c1"] if world == 1 else []) + ["c3", "c5"] + (["c8", "c9", "c2_ssim"] if world == 1 else []):
             if name == "c8":
                 sub = measure_fit4k(args, env)
+            elif name == "c9":
+                sub = measure_fit3d(args, env)
             elif name == "c2_ssim":
                 # the dense iteration of the SPEC's compute_loss: (1 - 0.2) L1 + 0.2 (1 - SSIM)
                 import copy

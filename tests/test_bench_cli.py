@@ -16,7 +16,7 @@ def _run(*args):
 
 
 def test_reference_arm_3d_configs_report_unavailable():
-    for cfg in ("c6", "c7"):
+    for cfg in ("c6", "c7", "c9"):
         lines = _run("--impl", "reference", "--config", cfg)
         assert len(lines) == 1
         assert lines[0]["impl"] == "reference" and "unavailable" in lines[0]
@@ -26,7 +26,7 @@ def test_help_lists_configs():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--help"], capture_output=True,
                          text=True, timeout=60, cwd=ROOT)
     assert out.returncode == 0
-    for cfg in ("c2", "c3", "c4", "c5", "c6", "c7"):
+    for cfg in ("c2", "c3", "c4", "c5", "c6", "c7", "c8", "c9"):
         assert cfg in out.stdout
 
 
