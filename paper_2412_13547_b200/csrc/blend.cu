@@ -622,19 +622,23 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
     const uint32_t lgbase = smem_addr(S.lg);
     // dense rank of active pixel (lx, ly) = rank0 + ly * cols + lx (ax, ay are active pixels)
     const int rank0 = ((geo.ay - prm.oy) / p) * prm.cols + (geo.ax - prm.ox) / p;
+    // Slot s of a plane holds pixel (lane s >> 1, A/B = s & 1); this lane fetches slots `lane` and
+    // 32 + lane (contiguous 4-B destinations: no bank conflicts), i.e. the pixels of lanes
+    // lane >> 1 and 16 + (lane >> 1), row offset lane & 1.
+    const int fcol = (lane >> 1) & 7, frow = 2 * (lane >> 4) + (lane & 1);  // slot `lane`
     auto prefetch = [&](int g, int buf) {
-        const int lx = (g % NGX) * 8 + cxl, lyA = (g / NGX) * 8 + ryl;
-        const bool vA = lx < geo.acols && lyA < geo.arows, vB = lx < geo.acols && lyA + 1 < geo.arows;
-        const int rA = vA ? rank0 + lyA * prm.cols + lx : 0;
-        const int rB = vB ? rA + prm.cols : 0;
-        const uint32_t nA = vA ? 4u : 0u, nB = vB ? 4u : 0u;
-        const uint32_t d = lgbase + 1024u * (uint32_t)buf + 8u * (uint32_t)lane;
-        cp_async4(d, prm.last + rA, nA);
-        cp_async4(d + 4, prm.last + rB, nB);
+        const int lx = (g % NGX) * 8 + fcol, ly0 = (g / NGX) * 8 + frow, ly1 = ly0 + 4;  // slot 32+lane: 4 rows down
+        const bool v0 = lx < geo.acols && ly0 < geo.arows, v1 = lx < geo.acols && ly1 < geo.arows;
+        const int r0 = v0 ? rank0 + ly0 * prm.cols + lx : 0;
+        const int r1 = v1 ? rank0 + ly1 * prm.cols + lx : 0;
+        const uint32_t n0 = v0 ? 4u : 0u, n1 = v1 ? 4u : 0u;
+        const uint32_t d = lgbase + 1024u * (uint32_t)buf + 4u * (uint32_t)lane;
+        cp_async4(d, prm.last + r0, n0);
+        cp_async4(d + 128, prm.last + r1, n1);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            cp_async4(d + 256 * (c + 1), prm.dLdC + 3 * rA + c, nA);
-            cp_async4(d + 256 * (c + 1) + 4, prm.dLdC + 3 * rB + c, nB);
+            cp_async4(d + 256 * (c + 1), prm.dLdC + 3 * r0 + c, n0);
+            cp_async4(d + 256 * (c + 1) + 128, prm.dLdC + 3 * r1 + c, n1);
         }
         cp_async_commit();
     };
