@@ -87,7 +87,7 @@ def main():
         cfg, rep, log = spec.split(":")
         cnt = [json.loads(l) for l in open(log) if l.startswith("{")]
         cnt = [c for c in cnt if not c["warmup"]][0]
-        out[cfg] = {"blend_forward": kernel_weights(rep, "forward_pairs", cnt),
+        out[cfg] = {"blend_forward": kernel_weights(rep, "forward_(pairs|dilated)", cnt),
                     "blend_backward": kernel_weights(rep, "backward_kernel", cnt)}
     json.dump(out, open(sys.argv[1], "w"), indent=1)
     print(json.dumps(out, indent=1)[:3000])
