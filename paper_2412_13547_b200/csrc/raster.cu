@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     touched[rank] = tiles;
 }
 
-// Rows in blend order (rank == row), with the pair-offset scan fused in: blocks take
-// launch-ordered tickets, reduce their tile counts and find their prefix by decoupled look-back
+// Rows in blend order (rank == row), with the pair-offset scan fused in: blocks (in dispatch
+// order, lookback_block) reduce their tile counts and find their prefix by decoupled look-back
 // (block_scan_lookback), so each record leaves with its first pair slot (d.z) and pair_off /
 // touched / the total K are written here: the separate scan and pair-base passes over the
 // Gaussians disappear from the step.
@@ -119,10 +119,7 @@ __global__ void __launch_bounds__(256) preprocess_scan_kernel(
     uint32_t* __restrict__ pair_off, uint32_t* __restrict__ fill, uint32_t* __restrict__ slab,
     unsigned long long* err, unsigned long long* status, uint32_t* ticket, uint32_t* d_total,
     uint2* __restrict__ rect) {
-    __shared__ uint32_t s_bid;
-    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t bid = s_bid;
+    const uint32_t bid = lookback_block(ticket);
     const int64_t i = (int64_t)bid * 256 + threadIdx.x;
     Prepared o;
     uint32_t tiles = 0;

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(256) preprocess3d_kernel(
 }
 
 // Per-tile path (no global sort): records stay in ROW order; every visible row claims its slab
-// slots with its row index, the pair-offset scan runs fused (ticket-ordered blocks), and the
+// slots with its row index, the pair-offset scan runs fused (blocks in dispatch order), and the
 // per-tile warp sort (seg_sort3d_kernel) orders each list by (depth key, row) — the blend order
 // restricted to the tile, which is all the blend kernels read.
 __global__ void __launch_bounds__(256, 3) preprocess3d_bin_kernel(
@@ -272,10 +272,7 @@ __global__ void __launch_bounds__(256, 3) preprocess3d_bin_kernel(
     int tiles_x, Prepared* __restrict__ prep, uint32_t* __restrict__ keys, uint32_t* __restrict__ touched,
     uint32_t* __restrict__ pair_off, uint32_t* __restrict__ fill, uint32_t* __restrict__ slab,
     unsigned long long* err, unsigned long long* status, uint32_t* ticket, uint32_t* d_total) {
-    __shared__ uint32_t s_bid;
-    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t bid = s_bid;
+    const uint32_t bid = lookback_block(ticket);
     const int64_t i = (int64_t)bid * 256 + threadIdx.x;
     Prepared o;
     uint32_t key = kCulledKey, tiles = 0;
@@ -368,7 +365,7 @@ __global__ void __launch_bounds__(256) seg_sort3d_kernel(const uint2* __restrict
 }
 
 // ------------------------------------------------------------------ rank-order gather + binning
-// One thread per blend rank (blocks ticket-ordered): gathers the row's record, claims its slab
+// One thread per blend rank (blocks in dispatch order): gathers the row's record, claims its slab
 // slots like the 2-D preprocess, and runs the pair-offset scan fused in (block_scan_lookback):
 // pair_off / touched / the record's first pair slot / the total K leave this kernel.
 __global__ void __launch_bounds__(256) bin3d_kernel(
@@ -377,10 +374,7 @@ __global__ void __launch_bounds__(256) bin3d_kernel(
     uint32_t* __restrict__ touched, uint32_t* __restrict__ pair_off, uint32_t* __restrict__ fill,
     uint32_t* __restrict__ slab, uint32_t* __restrict__ perm, uint32_t* __restrict__ rank_of,
     unsigned long long* status, uint32_t* ticket, uint32_t* d_total) {
-    __shared__ uint32_t s_bid;
-    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t bid = s_bid;
+    const uint32_t bid = lookback_block(ticket);
     const int64_t r = (int64_t)bid * 256 + threadIdx.x;
     Prepared o;
     o.d = make_uint4(0u, 0u, 0u, 0u);
