@@ -53,18 +53,15 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
 }
 
 // ------------------------------------------------------------------ exclusive scan
-// status[b]: flag (2 bits) | value (62 bits); ticket gives blocks a launch-order id so a
+// status[b]: flag (2 bits) | value (62 bits); blocks look back in dispatch order (lookback_block) so a
 // block only ever waits on blocks that are already resident.
 __global__ void __launch_bounds__(kScanBT) exclusive_scan_kernel(
     const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t n,
     unsigned long long* status, uint32_t* ticket, uint32_t* d_total) {
-    __shared__ uint32_t s_bid;
     __shared__ unsigned long long s_warp[kScanBT / 32];
     __shared__ unsigned long long s_prefix;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_bid = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t bid = s_bid;
+    const uint32_t bid = lookback_block(ticket);
     const int64_t base = (int64_t)bid * kScanTile + (int64_t)tid * kScanIT;
 
     uint32_t v[kScanIT];
@@ -181,10 +178,8 @@ __global__ void __launch_bounds__(kSortBT) onesweep_pass(
     __shared__ uint32_t s_warp[kSortBT / 32][kRadix];
     __shared__ uint32_t s_base[kRadix];
     __shared__ uint32_t s_wsum[kSortBT / 32];
-    __shared__ uint32_t s_bid;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < (kSortBT / 32) * kRadix; i += kSortBT) (&s_warp[0][0])[i] = 0;
-    if (tid == 0) s_bid = atomicAdd(ticket, 1u);
     // global digit offsets: exclusive scan of this pass's histogram (thread tid = digit)
     const uint32_t hcount = hist[tid];
     uint32_t hincl = hcount;
@@ -198,7 +193,7 @@ __global__ void __launch_bounds__(kSortBT) onesweep_pass(
     uint32_t wpre = 0;
     for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
     const uint32_t g_off = wpre + hincl - hcount;
-    const uint32_t bid = s_bid;
+    const uint32_t bid = lookback_block(ticket);
 
     const int64_t base = (int64_t)bid * kSortTile + (int64_t)warp * (32 * kSortIT) + lane;
     uint32_t k[kSortIT], v[kSortIT];
