@@ -527,6 +527,50 @@ def measure_fit3d(args, env):
                     "events_first_last": [events[0], events[-1]] if events else []}}
 
 
+def measure_shim(args, env):
+    """C2 through the C++ drop-in path (tools/shim_bench.cpp, built against the reference headers
+    by __graft_entry__.build()): a reference-API fit loop — tgs::render<float>, host L1,
+    tgs::backward<float>, host Adam — with only the rasterizer translation unit swapped for the
+    shim. Every call marshals the reference's AoS GaussianModel, uploads it and reads the results
+    back, exactly what a drop-in caller pays. None when the binary is absent."""
+    import tempfile
+    binp = os.path.join(ROOT, "tests", "_bin", "shim_bench")
+    if not os.path.exists(binp):
+        return None
+    P = env["P"]
+    cfg = CONFIGS["c2"]
+    W, H, n, p = cfg["W"], cfg["H"], cfg["n"], cfg["p"]
+    host = P.GaussianModel.synthetic(1, n, W, H)
+    tm = P.DeviceModel.from_host(P.GaussianModel.synthetic(2, n, W, H), env["ctx"])
+    tgt = np.ascontiguousarray(tm.render(P.DilationPattern(1, 0, 0, W, H)).colors.reshape(H, W, 3), np.float32)
+    tm.close()
+    steps, warm = 5, 1
+    with tempfile.TemporaryDirectory() as d:
+        pp, tp = os.path.join(d, "params.f32"), os.path.join(d, "target.f32")
+        np.ascontiguousarray(host.params, np.float32).tofile(pp)
+        tgt.tofile(tp)
+        t0 = time.time()
+        out = subprocess.run([binp, pp, str(n), tp, str(W), str(H), str(p), str(warm), str(steps)],
+                             capture_output=True, text=True, timeout=900)
+        wall = time.time() - t0
+    if out.returncode != 0:
+        return {"unavailable": f"shim_bench exit {out.returncode}: {out.stderr[-300:]}"}
+    r = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    return {"value": r["iters_per_s"], "unit": "iters/s", "n_gpus": 1, "steps": steps, "warmup": warm,
+            "ms_per_step": 1e3 / r["iters_per_s"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 through the C++ drop-in boundary: tools/shim_bench.cpp runs the reference "
+                                   "API loop (tgs::render<float> + host L1 + tgs::backward<float> + host Adam, one "
+                                   "thread) with rasterizer.cpp replaced by shim/tgs_gpu_rasterizer.cpp; per call "
+                                   "the reference's AoS model is marshalled, uploaded and read back",
+                       "gaussians": n, "width": W, "height": H, "p": p},
+            "timing": "host wall clock (std::chrono) around each part: the whole loop runs on the host thread",
+            "parts_s_per_step": {k: r[k] for k in ("render_s", "host_loss_s", "backward_s", "host_adam_s")},
+            "e2e": {"value": r["iters_per_s"], "unit": "iters/s", "note": "host-resident model and target: "
+                    "every byte crosses PCIe inside the shim calls"},
+            "process_wall_s": wall}
+
+
 def run_tgsx(args):
     """All ranks: set up the process group, the context (+ the library NCCL communicator for
     N > 1), measure the requested config; with the default config (C2) also the sub-records of
@@ -563,9 +607,11 @@ def run_tgsx(args):
         line = measure(args, args.config, env)
     if args.config == "c2" and args.ssim == 0 and not args.no_subrecords:
         subs = {}
-        for name in (["c1"] if world == 1 else []) + ["c3", "c5"] + (["c8", "c9", "c2_ssim"] if world == 1 else []):
+        for name in (["c1"] if world == 1 else []) + ["c3", "c5"] + (["c8", "c9", "c2_ssim", "c2_shim"] if world == 1 else []):
             if name == "c8":
                 sub = measure_fit4k(args, env)
+            elif name == "c2_shim":
+                sub = measure_shim(args, env)
             elif name == "c9":
                 sub = measure_fit3d(args, env)
             elif name == "c2_ssim":
