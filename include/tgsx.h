@@ -25,6 +25,7 @@
 #define TGSX_H
 
 #include <stdint.h>
+#include <stddef.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -73,6 +74,10 @@ int32_t tgsx_set_stream(tgsx_ctx* ctx, void* stream);
 void* tgsx_get_stream(tgsx_ctx* ctx);
 const char* tgsx_last_error(const tgsx_ctx* ctx);
 int32_t tgsx_synchronize(tgsx_ctx* ctx);
+/* Page-locked host memory (cudaHostAlloc) for staging buffers a host caller reuses across calls:
+ * copies from / to it run at full PCIe speed. */
+int32_t tgsx_host_alloc(size_t bytes, void** out);
+void tgsx_host_free(void* p);
 /* Counters of this library's kernel launches on ctx (for the bench's gpu_launches claim). */
 uint64_t tgsx_launch_count(const tgsx_ctx* ctx);
 /* Live per-stage timing: CUDA events recorded on the context stream around each stage

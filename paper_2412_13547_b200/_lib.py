@@ -81,6 +81,8 @@ SIGNATURES = {
     "tgsx_get_stream": (vp, [vp]),
     "tgsx_last_error": (C.c_char_p, [vp]),
     "tgsx_synchronize": (C.c_int32, [vp]),
+    "tgsx_host_alloc": (C.c_int32, [C.c_size_t, P(vp)]),
+    "tgsx_host_free": (None, [vp]),
     "tgsx_launch_count": (C.c_uint64, [vp]),
     "tgsx_profile": (C.c_int32, [vp, C.c_int32]),
     "tgsx_profile_read": (C.c_int32, [vp, f64p, i64p, C.c_int32]),

@@ -1022,6 +1022,17 @@ void* tgsx_get_stream(tgsx_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr
 
 const char* tgsx_last_error(const tgsx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+int32_t tgsx_host_alloc(size_t bytes, void** out) {
+    if (!out) return TGSX_EINVAL;
+    *out = nullptr;
+    if (bytes == 0) return TGSX_OK;
+    return cudaHostAlloc(out, bytes, cudaHostAllocDefault) == cudaSuccess ? TGSX_OK : TGSX_ENOMEM;
+}
+
+void tgsx_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 int32_t tgsx_synchronize(tgsx_ctx* ctx) {
     if (int32_t rc = graph_flush(ctx)) return rc;
     CK(cudaStreamSynchronize(ctx->stream));
