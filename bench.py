@@ -560,8 +560,8 @@ def measure_shim(args, env):
             "ms_per_step": 1e3 / r["iters_per_s"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "C2 through the C++ drop-in boundary: tools/shim_bench.cpp runs the reference "
-                                   "API loop (tgs::render<float> + host L1 + tgs::backward<float> + host Adam, one "
-                                   "thread) with rasterizer.cpp replaced by shim/tgs_gpu_rasterizer.cpp; per call "
+                                   "API loop (tgs::render<float> + host L1 + tgs::backward<float> + host Adam on all host "
+                                   "threads) with rasterizer.cpp replaced by shim/tgs_gpu_rasterizer.cpp; per call "
                                    "the reference's AoS model is marshalled, uploaded and read back",
                        "gaussians": n, "width": W, "height": H, "p": p},
             "timing": "host wall clock (std::chrono) around each part: the whole loop runs on the host thread",

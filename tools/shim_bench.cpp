@@ -2,9 +2,9 @@
 // translation unit is swapped for the shim (paper_2412_13547_b200/shim/tgs_gpu_rasterizer.cpp).
 // Per iteration, exactly what a caller of the reference's public API does:
 //   tgs::render<float>(model, pattern, bg)           (shim: AoS -> SoA marshal, upload, GPU render)
-//   L1 dL/dC on the host                              (per-pixel normalised)
+//   L1 dL/dC on the host threads                      (per-pixel normalised)
 //   tgs::backward<float>(model, pattern, bg, dLdC)    (shim: marshal, upload, GPU backward, stats back)
-//   Adam on the host                                  (one thread)
+//   Adam on the host threads
 // The model is the reference's own GaussianModel<float>, filled with GaussianModel::add from a
 // float[10][n] parameter file (bench.py writes the same synthetic scene it times), the target an
 // (H, W, 3) float file. Prints one JSON line: iterations/s and the per-part host-side times.
@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <thread>
 #include <vector>
 
 #include "tgs/rasterizer.hpp"
@@ -30,6 +31,16 @@ std::vector<float> read_f32(const char* path, size_t count) {
     }
     std::fclose(f);
     return v;
+}
+
+// the harness's own host loops (L1, Adam) on all host threads, as a reference trainer would run
+// them on its ThreadPool (threading.hpp)
+template <typename F>
+void parallel_for(size_t n, F&& f) {
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(), 32));
+    std::vector<std::thread> ts;
+    for (size_t t = 0; t < nt; ++t) ts.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt, t); });
+    for (auto& th : ts) th.join();
 }
 
 double now_s() {
@@ -75,15 +86,21 @@ int main(int argc, char** argv) {
         const int Pn = pat.active_count();
         std::vector<tgs::Vec3<float>> dl(Pn);
         const float sc = (float)(1.0 / (3.0 * (double)Pn));
+        std::vector<double> lsum(64, 0.0);
+        parallel_for((size_t)Pn, [&](size_t rb, size_t re, size_t tid) {
+            double ls = 0;
+            for (size_t r = rb; r < re; ++r) {
+                const int y = pat.offset_y() + ((int)r / pat.cols()) * p, x = pat.offset_x() + ((int)r % pat.cols()) * p;
+                const float* t = &target[3 * ((size_t)y * W + x)];
+                const float d0 = out.colors[r].x - t[0], d1 = out.colors[r].y - t[1], d2 = out.colors[r].z - t[2];
+                ls += std::fabs(d0) + std::fabs(d1) + std::fabs(d2);
+                auto sg = [&](float d) { return d > 0.f ? sc : (d < 0.f ? -sc : 0.f); };
+                dl[r] = tgs::Vec3<float>(sg(d0), sg(d1), sg(d2));
+            }
+            lsum[tid] = ls;
+        });
         double ls = 0;
-        for (int r = 0; r < Pn; ++r) {
-            const int y = pat.offset_y() + (r / pat.cols()) * p, x = pat.offset_x() + (r % pat.cols()) * p;
-            const float* t = &target[3 * ((size_t)y * W + x)];
-            const float d0 = out.colors[r].x - t[0], d1 = out.colors[r].y - t[1], d2 = out.colors[r].z - t[2];
-            ls += std::fabs(d0) + std::fabs(d1) + std::fabs(d2);
-            auto sg = [&](float d) { return d > 0.f ? sc : (d < 0.f ? -sc : 0.f); };
-            dl[r] = tgs::Vec3<float>(sg(d0), sg(d1), sg(d2));
-        }
+        for (double v : lsum) ls += v;
         loss = ls / (3.0 * Pn);
         a = now_s();
         t_loss += a - b;
@@ -97,7 +114,8 @@ int main(int argc, char** argv) {
                              (float)(1.6e-4 * std::hypot((double)W, (double)H) * std::pow(0.01, tn)),
                              1e-3f, 5e-3f, 5e-3f, 5e-2f, 2.5e-3f, 2.5e-3f, 2.5e-3f};
         const float bc1 = (float)(1.0 - std::pow(0.9, it + 1)), bc2 = (float)(1.0 - std::pow(0.999, it + 1));
-        for (size_t i = 0; i < n; ++i) {
+        parallel_for(n, [&](size_t ib, size_t ie, size_t) {
+          for (size_t i = ib; i < ie; ++i) {
             auto& g = model[i];
             float* th[9] = {&g.position.x, &g.position.y, &g.rotation, &g.log_scales.x, &g.log_scales.y,
                             &g.raw_opacity, &g.color.x, &g.color.y, &g.color.z};
@@ -111,7 +129,8 @@ int main(int argc, char** argv) {
                 vv = 0.999f * vv + 0.001f * gr[q] * gr[q];
                 *th[q] -= lr[q] * (mm / bc1) / (std::sqrt(vv / bc2) + 1e-15f);
             }
-        }
+          }
+        });
         t_adam += now_s() - b;
     }
     const double total = now_s() - t0;
