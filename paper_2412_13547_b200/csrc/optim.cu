@@ -93,9 +93,14 @@ struct ChainParams {
     const unsigned* fault;  // graph-replayed steps (graph.cpp): non-zero => the step is a no-op
 };
 
-// 6 blocks of 256 per SM (<= 40 registers): the slot loop and the moment / parameter streams
-// are latency-bound, so occupancy buys memory-level parallelism
-__global__ void __launch_bounds__(256, 4) chain_kernel(ChainParams cp) {
+// The slot loop and the parameter / moment / statistics streams are latency-bound: every load
+// that does not depend on the merge (raw parameters, Adam state, densify statistics) is issued
+// before it, which needs ~80 registers — 3 blocks of 256 per SM (4 forces spills; measured C3
+// 0.293 -> 0.278 ms with the statistics prefetched at 3 blocks, 6 blocks without prefetch 0.34 ms).
+#ifndef TGSX_CHAIN_MINB
+#define TGSX_CHAIN_MINB 3
+#endif
+__global__ void __launch_bounds__(256, TGSX_CHAIN_MINB) chain_kernel(ChainParams cp) {
     const int64_t i = cp.i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cp.i1) return;
     if (cp.fault && *reinterpret_cast<const volatile unsigned*>(cp.fault)) return;
@@ -123,6 +128,18 @@ __global__ void __launch_bounds__(256, 4) chain_kernel(ChainParams cp) {
     const float2* __restrict__ pc = cp.partial.c + base;
     // fused Adam: its state streams (theta, m, v) do not depend on the merge; issue them first
     float th0[9], mm0[9], vv0[9];
+    // densify statistics of a visited Gaussian: loaded up front as well (the increments below
+    // would otherwise add a third dependent memory round trip after the merge)
+    float pa0 = 0.f, ca0 = 0.f;
+    int32_t ac0 = 0;
+    int64_t vi0 = 0, wi0 = 0;
+    if (cp.update_stats && cp.mode != 2 && cnt) {
+        pa0 = cp.pos_acc[i];
+        ca0 = cp.col_acc[i];
+        ac0 = cp.accum[i];
+        vi0 = cp.visit[i];
+        wi0 = cp.window[i];
+    }
     if (cp.mode == 1) {
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
@@ -228,11 +245,11 @@ __global__ void __launch_bounds__(256, 4) chain_kernel(ChainParams cp) {
         return;
     }
     if (cp.update_stats && visited) {
-        cp.pos_acc[i] = fadd(cp.pos_acc[i], pn);
-        cp.col_acc[i] = fadd(cp.col_acc[i], cn);
-        cp.accum[i] += 1;
-        cp.visit[i] += 1;
-        cp.window[i] += 1;
+        cp.pos_acc[i] = fadd(pa0, pn);
+        cp.col_acc[i] = fadd(ca0, cn);
+        cp.accum[i] = ac0 + 1;
+        cp.visit[i] = vi0 + 1;
+        cp.window[i] = wi0 + 1;
     }
     if (cp.mode == 0) {
 #pragma unroll
