@@ -307,3 +307,34 @@ def test_binning_stress_random_shapes(P):
     oracle on every iteration (tests/stress_binning.py)."""
     from tests import stress_binning
     assert stress_binning.main(60) == 0
+
+
+def test_tile_lists_across_claim_order_refresh_and_densify(P, ctx):
+    """The slab claims run in a spatial order of the blend ranks (raster.cu launch_claims) that
+    is rebuilt after every depth sort and every 64 binnings while the splats move. Any order must
+    give the reference's lists: checked after 70 fit steps (one refresh on moved splats), after a
+    densify event (new ranks) and after the next fit steps."""
+    from tests.helpers import scene_from_model
+    B.set_math(True)
+    W, H, n = 400, 300, 20000
+    s = B.synthetic_scene(21, n, W, H)
+    dm = P.DeviceModel.from_host(model_from_scene(s), ctx)
+    tgt = np.full((H, W, 3), 0.4, np.float32)
+    diag = float(np.hypot(W, H))
+
+    def check():
+        host = scene_from_model(dm.download())
+        off, items = dm.stage_tile_lists(1, W, H)
+        roff, ritems = B.tile_grid(host, 1, W, H)
+        assert np.array_equal(off, roff) and np.array_equal(items, ritems)
+
+    for t in range(70):
+        dm.fit_step(P.DilationPattern(1, 0, 0, W, H), (0.0, 0.0, 0.0), tgt, t + 1, 1000, diag)
+    check()
+    st = np.array(B.Pcg32(3, 1).state, np.uint64)
+    rep = dm.densify(n + 2000, st, P.densify_config(tau_pos=1e-9))
+    assert rep.spawned > 0
+    check()
+    for t in range(5):
+        dm.fit_step(P.DilationPattern(2, t % 2, 0, W, H), (0.0, 0.0, 0.0), tgt, 71 + t, 1000, diag)
+    check()
