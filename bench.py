@@ -377,6 +377,37 @@ def measure_fp32_peak(ctx):
         return None
 
 
+def stage_rooflines(per, E, Bl, K, n, hbm_gbs, fp32_peak, config):
+    """Every 2-D stage of the step against its own roofline: algorithmic bytes
+    for the HBM-bound stages, SURVEY.md §8d flops for the blend kernels; `traffic` = the ncu DRAM
+    bytes of the committed capture where one exists (profiles/traffic_r02.json)."""
+    if config in ("c6", "c7"):
+        return None
+    hbm = {  # algorithmic bytes per launch
+        # params 40 + perm 4 read, record 64 + touched 4 + pair offset 4 + rectangle 8 written;
+        # claims: spatial order 4 + rectangle 8 read, 4 B per slab slot
+        "preprocess": 136 * n + 4 * K,
+        "radix_sort": 8 * K,  # per-tile sort: every list entry read and written once
+        # partials 40 B / pair; theta, m, v (9 floats each) and the statistics (28 B) read + written,
+        # pair offset + count 8 B
+        "chain_adam": (2 * (3 * 36 + 28) + 8) * n + 40 * K,
+    }
+    out = {}
+    for k, (ms, _) in per.items():
+        if k in hbm:
+            gbs = hbm[k] / (ms / 1e3) / 1e9
+            out[k] = {"bound": "hbm", "ms_per_launch": ms, "algorithmic_bytes": hbm[k], "achieved": gbs,
+                      "unit": "GB/s", "peak": hbm_gbs, "frac": gbs / hbm_gbs,
+                      "traffic": measured_traffic(config, k)}
+        elif k in ("blend_forward", "blend_backward"):
+            fl = 2 * E + (77 if k == "blend_backward" else 20) * Bl
+            tf = fl / (ms / 1e3) / 1e12
+            out[k] = {"bound": "fp32", "ms_per_launch": ms, "algorithmic_flops": fl, "achieved": tf,
+                      "unit": "TFLOP/s", "peak": fp32_peak, "frac": tf / fp32_peak,
+                      "traffic": measured_traffic(config, k)}
+    return out
+
+
 def roofline(stages, counters, clocks, n, config, fp32_meas=None):
     peaks = measured_peaks()
     per = {k: (v[0] / max(v[1], 1), v[1]) for k, v in stages.items() if v[1]}
@@ -402,7 +433,8 @@ def roofline(stages, counters, clocks, n, config, fp32_meas=None):
                 "peak_note": note,
                 "work_note": f"algorithmic flops per launch 2E+{per_blend}Bl with E={E} evaluations, "
                              f"Bl={Bl} blends (SURVEY.md §8d)",
-                "pipes": blend_pipes(stages, counters, f_mhz, fp32_peak, config)}
+                "pipes": blend_pipes(stages, counters, f_mhz, fp32_peak, config),
+                "stages": stage_rooflines(per, E, Bl, K, n, peaks["hbm_gbs"], fp32_peak, config)}
     if config in ("c6", "c7"):  # 3-D: chain3d + Adam streams 59 params, 2 moments (r+w), partials
         nb = {"chain_adam": (59 * 4 * 6 + 24) * n + 40 * K, "preprocess": (59 * 4 + 64 + 8) * n,
               "depth_sort": 4 * 24 * n + (64 + 64 + 16) * n}.get(dom, 0)
