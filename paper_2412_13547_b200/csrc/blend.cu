@@ -568,10 +568,15 @@ __device__ __forceinline__ void half_sums(uint32_t rowp, int ukey, uint32_t gbas
     acc[8] += c2p.x + c2p.y;
 }
 
-template <int NGX, int NGY>
+// CTA = true: the tile's NG groups are walked by NG warps of one CTA in parallel (warp w takes
+// group w; each warp stages the chunk itself; the per-splat moment sums of the NG groups are added
+// in group order through `red` [2][NG][32][10] floats before one warp writes the pair slots) —
+// for views with too few tiles to fill the GPU with one warp per tile (C1: 256 tiles).
+template <int NGX, int NGY, bool CTA = false>
 __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSmem<NGX * NGY>& S,
-                                              int tile, int lane) {
+                                              int tile, int lane, float* red = nullptr) {
     constexpr int NG = NGX * NGY;
+    const int gsel = CTA ? (int)(threadIdx.x >> 5) : 0;
     TileGeo geo;
     geo.init(prm, tile);
     const int p = prm.p;
@@ -584,7 +589,7 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
 
     uint32_t maxlast = 0;
 #pragma unroll 1
-    for (int g = 0; g < NG; ++g) {
+    for (int g = CTA ? gsel : 0; g < (CTA ? gsel + 1 : NG); ++g) {
         const int lx = (g % NGX) * 8 + cxl, lyA = (g / NGX) * 8 + ryl;
         float4 st = make_float4(1.f, 0.f, 1.f, 0.f);
 #pragma unroll
@@ -605,6 +610,13 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
         S.st[g][lane] = st;
     }
     maxlast = __reduce_max_sync(kFull, maxlast);
+    if (CTA) {  // every warp walks the same chunks: the tile-wide last contributor
+        __shared__ uint32_t s_max[NG];
+        if (lane == 0) s_max[gsel] = maxlast;
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < NG; ++w) maxlast = max(maxlast, s_max[w]);
+    }
     // moments about the tile's active-pixel centre (pixel-centre coordinates): active pixel
     // (cx, cy) sits at (ctr_x + (cx - hx) p, ctr_y + (cy - hy) p)
     constexpr float hx = 0.5f * (NGX * 8 - 1), hy = 0.5f * (NGY * 8 - 1);
@@ -615,7 +627,7 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
     const float fyl = (float)(geo.ay + ryl * p) + 0.5f;
 
     // list entries past every pixel's last contributor: zero partials
-    for (int j = (int)maxlast + lane; j < count; j += 32) {
+    for (int j = (int)maxlast + lane; j < (CTA && gsel ? 0 : count); j += 32) {
         const uint32_t slot = pair_slot(prm.prep[prm.items[range.x + j]], geo.tx, geo.ty);
         prm.partial.a[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
         prm.partial.b[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -647,7 +659,7 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
         cp_async_commit();
     };
     int buf = 0;
-    prefetch(0, 0);
+    prefetch(gsel, 0);  // (CTA: the warp's only group, loaded once for the whole tile)
 
     // phase-1 record offsets of this lane's slot pair in a row r: chunk (lane >> 1) ^ (r & 3)
     const uint32_t soff0 = (uint32_t)((lane >> 1) << 4) + (uint32_t)((lane & 1) << 3);
@@ -685,12 +697,15 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
         float q0 = 0.f, q1 = 0.f, q2 = 0.f;
         uint32_t vism = 0;
 #pragma unroll 1
-        for (int g = 0; g < NG; ++g) {
+        for (int gi = 0; gi < (CTA ? 1 : NG); ++gi) {
+            const int g = CTA ? gsel : gi;
             const int gx = g % NGX, gy = g / NGX;
-            const int cur = buf;
-            buf ^= 1;
+            const int cur = CTA ? 0 : buf;
             __syncwarp();  // the previous group's phase 2 is done with the rows and lg[buf]
-            prefetch(g + 1 < NG ? g + 1 : 0, buf);
+            if (!CTA) {
+                buf ^= 1;
+                prefetch(g + 1 < NG ? g + 1 : 0, buf);
+            }
             // pass sets of the lane's pixels A / B in this group
             const uint32_t X = __shfl_sync(kFull, bits, gx * 8 + cxl);
             uint32_t colA = X & __shfl_sync(kFull, bits, 16 + gy * 8 + ryl);
@@ -698,7 +713,8 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
 #ifdef TGSX_BWD_STATS
             const uint32_t boxA = colA, boxB = colB;
 #endif
-            cp_async_wait<1>();
+            if (CTA) cp_async_wait<0>();
+            else cp_async_wait<1>();
             __syncwarp();
             const uint32_t lgc = lgbase + 1024u * (uint32_t)cur + 8u * (uint32_t)lane;
             const float2 lastp = lds_f2(lgc);
@@ -858,6 +874,27 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
             S.st[g][lane] = make_float4(T.x, gS.x, T.y, gS.y);
             vism |= __reduce_or_sync(kFull, visb);
         }
+        if (CTA) {
+            // group sums -> red[ch & 1][gsel][lane]; warp 0 adds them in group order
+            float* rb = red + ((ch & 1) * NG + gsel) * 32 * 10 + lane * 10;
+            rb[0] = m0; rb[1] = mx1; rb[2] = my1; rb[3] = mxx; rb[4] = mxy; rb[5] = myy;
+            rb[6] = q0; rb[7] = q1; rb[8] = q2;
+            rb[9] = __uint_as_float((vism >> lane) & 1u);
+            __syncthreads();
+            if (gsel != 0) continue;
+            const float* r0p = red + (ch & 1) * NG * 32 * 10 + lane * 10;
+            m0 = r0p[0]; mx1 = r0p[1]; my1 = r0p[2]; mxx = r0p[3]; mxy = r0p[4]; myy = r0p[5];
+            q0 = r0p[6]; q1 = r0p[7]; q2 = r0p[8];
+            uint32_t vb = __float_as_uint(r0p[9]);
+#pragma unroll
+            for (int w = 1; w < NG; ++w) {
+                const float* rw = r0p + w * 32 * 10;
+                m0 += rw[0]; mx1 += rw[1]; my1 += rw[2]; mxx += rw[3]; mxy += rw[4]; myy += rw[5];
+                q0 += rw[6]; q1 += rw[7]; q2 += rw[8];
+                vb |= __float_as_uint(rw[9]);
+            }
+            vism = vb << lane;
+        }
         if (jvalid) {
             float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
             const uint32_t slot = __float_as_uint(lds_f1(myrec + 40));
@@ -919,6 +956,26 @@ __global__ void __launch_bounds__(kWPB * 32, TGSX_BWD_MINB) backward_kernel(Blen
     }
 }
 
+// One CTA per tile, one warp per group (backward_tile<..., true>): views with few tiles.
+template <int NGX, int NGY>
+__global__ void __launch_bounds__(NGX * NGY * 32) backward_cta_kernel(BlendParams prm) {
+    constexpr int NG = NGX * NGY;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto& S = reinterpret_cast<BwdWarpSmem<NG>*>(smem_raw)[warp];
+    float* red = reinterpret_cast<float*>(smem_raw + NG * sizeof(BwdWarpSmem<NG>));
+    if (prm.fault) {
+        const unsigned long long* c = prm.counters;
+        const bool bad = *reinterpret_cast<const volatile unsigned*>(prm.fault) != 0u || c[0] != kErrNone ||
+                         (c[3] & 0xffffffffull) > prm.guard_pairs || c[5] > prm.guard_list;
+        if (bad) {
+            if (threadIdx.x == 0) atomicOr(prm.fault, 1u);
+            return;
+        }
+    }
+    backward_tile<NGX, NGY, true>(prm, S, (int)blockIdx.x, lane, red);
+}
+
 BlendParams make_params(tgsx_ctx* ctx, const RenderArgs& ra, const uint32_t* items) {
     Workspace& ws = ctx->ws;
     BlendParams prm{};
@@ -970,6 +1027,26 @@ cudaError_t run_backward(tgsx_ctx* ctx, const BlendParams& prm) {
         if (prev != ctx->device) cudaSetDevice(prev);
         if (e) return e;
         resident = std::max(1, sms * std::max(per_sm, 1));
+    }
+    if (NGX * NGY > 1 && (int64_t)prm.tiles * 2 < (int64_t)resident * kWPB) {
+        // too few tiles to occupy every resident warp slot with one warp per tile: one CTA per tile,
+        // its groups walked in parallel
+        constexpr int NG = NGX * NGY;
+        const size_t smem_cta = NG * sizeof(BwdWarpSmem<NG>) + 2 * NG * 32 * 10 * sizeof(float);
+        int& cfg_done = ctx->bwd_resident[2];
+        if (!cfg_done) {
+            int prev = 0;
+            cudaError_t e = cudaGetDevice(&prev);
+            if (e) return e;
+            if (prev != ctx->device && (e = cudaSetDevice(ctx->device))) return e;
+            e = cudaFuncSetAttribute(backward_cta_kernel<NGX, NGY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_cta);
+            if (prev != ctx->device) cudaSetDevice(prev);
+            if (e) return e;
+            cfg_done = 1;
+        }
+        backward_cta_kernel<NGX, NGY><<<(unsigned)prm.tiles, NG * 32, smem_cta, ctx->stream>>>(prm);
+        return cudaGetLastError();
     }
     cudaError_t e = cudaMemsetAsync(prm.tile_queue, 0, sizeof(unsigned int), ctx->stream);
     if (e) return e;

@@ -112,7 +112,7 @@ struct tgsx_ctx {
     uint64_t bin_max_hint = 0;      // longest list of the previous binning
     // blend backward launch configuration, per context (= per device): the dynamic shared-memory
     // opt-in is a per-device function attribute and the resident-CTA count sizes the grid
-    int bwd_resident[2] = {0, 0};
+    int bwd_resident[3] = {0, 0, 0};  // [0] / [1] resident CTAs of backward_kernel<2,2> / <1,1>; [2] CTA variant configured
     // NCCL communicator of a view-sharded fit (comm.cpp; null = single rank) and its stream;
     // events of the pipelined batched step (chain(b) -> all-reduce(b) -> Adam(b))
     void* comm = nullptr;
