@@ -568,6 +568,22 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
     // per-tile path: pair slots by row; global-sort path: by blend rank
     const uint32_t r = cp.rank_of ? __ldg(cp.rank_of + i) : (uint32_t)i;
     const uint32_t cnt = __ldg(cp.touched + r);
+    // the geometric parameters and the statistics do not depend on the merge: issued first
+    float mu[3], q[4], ls[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mu[k] = __ldg(P + k * cap + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = __ldg(P + (3 + k) * cap + i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ls[k] = __ldg(P + (7 + k) * cap + i);
+    const float rop = __ldg(P + 10 * cap + i);
+    float pa0 = 0.f, ca0 = 0.f;
+    int32_t vi0 = 0;
+    if (cp.update_stats && cp.mode != 2) {
+        pa0 = cp.pos_acc[i];
+        ca0 = cp.col_acc[i];
+        vi0 = cp.visit[i];
+    }
     float s[10];
 #pragma unroll
     for (int k = 0; k < 10; ++k) s[k] = 0.f;
@@ -590,14 +606,6 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
 #pragma unroll
         for (int k = 0; k < 10; ++k) cp.screen[(int64_t)k * cp.n + i] = s[k];
     }
-    float mu[3], q[4], ls[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) mu[k] = __ldg(P + k * cap + i);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = __ldg(P + (3 + k) * cap + i);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) ls[k] = __ldg(P + (7 + k) * cap + i);
-    const float rop = __ldg(P + 10 * cap + i);
     Geo3 g;
     float gg[11], b[16], dcol[3], dir[3] = {0.f, 0.f, 1.f};
     bool visited = false;
@@ -612,9 +620,9 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
             cn = SH_C0 * sqrtf(dcol[0] * dcol[0] + dcol[1] * dcol[1] + dcol[2] * dcol[2]);
         }
         if (cp.update_stats && visited && cp.mode != 2) {
-            cp.pos_acc[i] += pn;
-            cp.col_acc[i] += cn;
-            cp.visit[i] += 1;
+            cp.pos_acc[i] = pa0 + pn;
+            cp.col_acc[i] = ca0 + cn;
+            cp.visit[i] = vi0 + 1;
         }
     } else {
 #pragma unroll
