@@ -72,10 +72,10 @@ struct Pinned {
     T* get(size_t count) {
         const size_t need = std::max<size_t>(count, 1) * sizeof(T);
         if (need > bytes) {
+            const size_t nb = std::max(need, bytes + bytes / 2);
             tgsx_host_free(p);
             p = nullptr;
             bytes = 0;
-            const size_t nb = std::max(need, bytes + bytes / 2);
             if (tgsx_host_alloc(nb, &p) != TGSX_OK) throw std::runtime_error("tgsx: pinned host allocation failed");
             bytes = nb;
         }
