@@ -167,3 +167,22 @@ def test_batched_step_after_densify(P, S, ctx):
     losses = [dm.view_accumulate(c, None, (0.0, 0.0, 0.0), t) for c, t in zip(cams[:2], targets[:2])]
     dm.apply_step(2, 50, 100, 3.0)
     assert all(np.isfinite(losses)) and np.all(np.isfinite(dm.download().params))
+
+
+def test_densify3d_error_paths(P, S, ctx):
+    """tgsx_densify3d refuses a model with a batched step in progress (TGSX_ESTATE) and bad
+    arguments (TGSX_EINVAL); Trainer3D rejects an inconsistent schedule."""
+    cams = _cams(S)
+    m = S.GaussianModel3D.synthetic(9, 500, cams[0])
+    dm = S.DeviceModel3D.from_host(m, ctx)
+    tgt = np.full((cams[0].height, cams[0].width, 3), 0.3, np.float32)
+    dm.view_accumulate(cams[0], None, (0.0, 0.0, 0.0), tgt)
+    st = np.array(B.Pcg32(1, 1).state, np.uint64)
+    with pytest.raises(Exception):
+        dm.densify(1000, st, P.densify_config())
+    dm.apply_step(1, 1, 10, 3.0)
+    rep = dm.densify(1000, st, P.densify_config())  # allowed again once the step is applied
+    assert rep.count_after == dm.size()
+    bad = P.train_config(total_iters=100, warmup_iters=50, densify_until=20)  # warmup > densify_until
+    with pytest.raises(Exception):
+        S.Trainer3D(dm, cams, 3.0, bad)
