@@ -97,10 +97,10 @@ struct ChainParams {
 // that does not depend on the merge (raw parameters, Adam state, densify statistics) is issued
 // before it, which needs ~80 registers — 3 blocks of 256 per SM (4 forces spills; measured C3
 // 0.293 -> 0.278 ms with the statistics prefetched at 3 blocks, 6 blocks without prefetch 0.34 ms).
-#ifndef TGSX_CHAIN_MINB
-#define TGSX_CHAIN_MINB 3
-#endif
-__global__ void __launch_bounds__(256, TGSX_CHAIN_MINB) chain_kernel(ChainParams cp) {
+// MODE (= cp.mode) is a template parameter: the gradient-only and accumulate variants carry none
+// of the Adam prefetch registers and keep 4 blocks per SM.
+template <int MODE>
+__global__ void __launch_bounds__(256, MODE == 1 ? 3 : 4) chain_kernel(ChainParams cp) {
     const int64_t i = cp.i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cp.i1) return;
     if (cp.fault && *reinterpret_cast<const volatile unsigned*>(cp.fault)) return;
@@ -133,14 +133,14 @@ __global__ void __launch_bounds__(256, TGSX_CHAIN_MINB) chain_kernel(ChainParams
     float pa0 = 0.f, ca0 = 0.f;
     int32_t ac0 = 0;
     int64_t vi0 = 0, wi0 = 0;
-    if (cp.update_stats && cp.mode != 2 && cnt) {
+    if (cp.update_stats && MODE != 2 && cnt) {
         pa0 = cp.pos_acc[i];
         ca0 = cp.col_acc[i];
         ac0 = cp.accum[i];
         vi0 = cp.visit[i];
         wi0 = cp.window[i];
     }
-    if (cp.mode == 1) {
+    if (MODE == 1) {
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
             const int64_t o = (int64_t)q * cap + i;
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256, TGSX_CHAIN_MINB) chain_kernel(ChainParams
         pn = __fsqrt_rn(fadd(fmul(g[0], g[0]), fmul(g[1], g[1])));
         cn = __fsqrt_rn(fadd(fadd(fmul(g[6], g[6]), fmul(g[7], g[7])), fmul(g[8], g[8])));
     }
-    if (cp.mode == 2) {
+    if (MODE == 2) {
         // batched views: sums in view order; the three counters increment
         // together (rasterizer.cpp:352-357), so one visit count is carried
         StepRec r = cp.step[i];
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256, TGSX_CHAIN_MINB) chain_kernel(ChainParams
         cp.visit[i] = vi0 + 1;
         cp.window[i] = wi0 + 1;
     }
-    if (cp.mode == 0) {
+    if (MODE == 0) {
 #pragma unroll
         for (int q = 0; q < 9; ++q) cp.grads[q * cp.n + li] = g[q];
         return;
@@ -327,7 +327,12 @@ cudaError_t launch_chain(tgsx_ctx* ctx, tgsx_model* m, ChainMode mode, bool upda
     cp.step = m->step.as<StepRec>();
     if (adam_cfg) cp.adam = *reinterpret_cast<const AdamCfg*>(adam_cfg);
     cp.fault = ctx->graph_capturing ? ctx->graph_fault : nullptr;
-    chain_kernel<<<grid_for(i1 - i0, 256), 256, 0, ctx->stream>>>(cp);
+    if (cp.mode == 1)
+        chain_kernel<1><<<grid_for(i1 - i0, 256), 256, 0, ctx->stream>>>(cp);
+    else if (cp.mode == 2)
+        chain_kernel<2><<<grid_for(i1 - i0, 256), 256, 0, ctx->stream>>>(cp);
+    else
+        chain_kernel<0><<<grid_for(i1 - i0, 256), 256, 0, ctx->stream>>>(cp);
     ctx->launches++;
     return cudaGetLastError();
 }
