@@ -265,8 +265,19 @@ class Context:
 
     # ------------------------------------------------ in-library NCCL
     @staticmethod
+    def _nccl_from_torch():
+        """libtgsx dlopens "libnccl.so.2" on first use; inside a Python process that library must
+        be PyTorch's own NCCL (torch's CUDA library needs its NCCL's symbols — a system NCCL loaded
+        first would shadow it and break a later `import torch`). Importing torch loads it."""
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
+
+    @staticmethod
     def comm_unique_id() -> bytes:
         """A fresh 128-byte NCCL unique id (rank 0 creates it, the caller distributes it)."""
+        Context._nccl_from_torch()
         buf = (C.c_uint8 * 128)()
         rc = _lib.load().tgsx_comm_unique_id(buf)
         if rc:
@@ -277,6 +288,7 @@ class Context:
         """Attach an NCCL communicator of `nranks` (this context's device) for batched steps."""
         if len(unique_id) != 128:
             raise ValueError("NCCL unique id must be 128 bytes")
+        Context._nccl_from_torch()
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         self.check(self.L.tgsx_comm_init(self.h, buf, int(nranks), int(rank)))
 

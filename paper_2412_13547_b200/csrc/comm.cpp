@@ -7,7 +7,8 @@
 //
 // NCCL is loaded with dlopen("libnccl.so.2") on first use instead of being linked: inside a
 // PyTorch process that resolves to the NCCL torch already loaded (one NCCL per process, no ABI
-// mix), elsewhere to the system library. Only the stable core API is used (unique id, init,
+// mix; the Python front end imports torch before the first communicator call so that it is
+// loaded), elsewhere to the system library. Only the stable core API is used (unique id, init,
 // all-reduce, destroy, error string), declared here with their C types. NVLink SHARP (NVLS) is
 // NCCL's own choice for all-reduce on NVSwitch systems (NCCL_NVLS_ENABLE, default on).
 #include <dlfcn.h>

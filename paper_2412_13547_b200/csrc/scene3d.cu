@@ -560,7 +560,11 @@ __device__ __forceinline__ void chain3d_grads(const Cam3& cam, const Geo3& g, co
     for (int k = 0; k < 4; ++k) gg[3 + k] = (dq[k] - g.qn[k] * qd) * g.qinv;
 }
 
-__global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
+// MODE (= cp.mode) as a template parameter: each variant keeps only its own output path live.
+// The accumulate variant (batched multi-camera steps) runs at 3 blocks per SM (C7 chain 1.72 ->
+// 1.57 ms per step); the fused variant keeps 2 (3 forces spills: C6 0.389 -> 0.41 ms).
+template <int MODE>
+__global__ void __launch_bounds__(256, MODE == 2 ? 3 : 2) chain3d_kernel(Chain3Params cp) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cp.n) return;
     const int64_t cap = cp.cap;
@@ -579,7 +583,7 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
     const float rop = __ldg(P + 10 * cap + i);
     float pa0 = 0.f, ca0 = 0.f;
     int32_t vi0 = 0;
-    if (cp.update_stats && cp.mode != 2) {
+    if (cp.update_stats && MODE != 2) {
         pa0 = cp.pos_acc[i];
         ca0 = cp.col_acc[i];
         vi0 = cp.visit[i];
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
             pn = sqrtf(s[0] * s[0] + s[1] * s[1]);
             cn = SH_C0 * sqrtf(dcol[0] * dcol[0] + dcol[1] * dcol[1] + dcol[2] * dcol[2]);
         }
-        if (cp.update_stats && visited && cp.mode != 2) {
+        if (cp.update_stats && visited && MODE != 2) {
             cp.pos_acc[i] = pa0 + pn;
             cp.col_acc[i] = ca0 + cn;
             cp.visit[i] = vi0 + 1;
@@ -631,9 +635,9 @@ __global__ void __launch_bounds__(256) chain3d_kernel(Chain3Params cp) {
         for (int k = 0; k < 16; ++k) b[k] = 0.f;
         dcol[0] = dcol[1] = dcol[2] = 0.f;
     }
-    if (cp.mode != 1) {
+    if (MODE != 1) {
         auto grad = [&](int k) -> float { return k < 11 ? gg[k] : fmul(b[(k - 11) / 3], dcol[(k - 11) % 3]); };
-        if (cp.mode == 0) {
+        if (MODE == 0) {
             float* __restrict__ G = cp.grads;
 #pragma unroll
             for (int k = 0; k < 59; ++k) G[(int64_t)k * cp.n + i] = grad(k);
@@ -931,7 +935,12 @@ cudaError_t launch_chain3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int 
         if ((e = m->gbuf.ensure((size_t)std::max<int64_t>(m->n, 1) * 17 * 4))) return e;
         cp.gbuf = m->gbuf.as<float>();
     }
-    chain3d_kernel<<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(cp);
+    if (mode == 1)
+        chain3d_kernel<1><<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(cp);
+    else if (mode == 2)
+        chain3d_kernel<2><<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(cp);
+    else
+        chain3d_kernel<0><<<grid_for(m->n, 256), 256, 0, ctx->stream>>>(cp);
     ctx->launches++;
     if (adam) {
         adam3d_apply_kernel<<<dim3(grid_for(m->n, 256), kAdamGroups), 256, 0, ctx->stream>>>(
