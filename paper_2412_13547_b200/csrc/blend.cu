@@ -11,11 +11,16 @@
 // the list order and box-failing splats contribute nothing, exactly as in walk_pixel
 // (rasterizer.cpp:108-136).
 //
-// forward_pairs_kernel (one CTA per tile, one warp per 8x8 block, two pixels per lane as packed
-//   FP32x2): walk_pixel + render (rasterizer.cpp:144-184), optional fused L1 epilogue
-//   (SPEC.md:562-570). Records per pixel the final T and the last blended list position.
-// backward_kernel (ONE WARP PER TILE, independent warps, no block barriers): backward tile
-//   phase (rasterizer.cpp:234-292), per chunk and 8x4 pixel group:
+// forward_pairs_kernel (p = 1: one CTA per tile, one warp per 8x8 block, two pixels per lane as
+//   packed FP32x2, 256-record staging batches): walk_pixel + render (rasterizer.cpp:144-184),
+//   optional fused L1 epilogue. Records per pixel the final T and the last
+//   blended list position.
+// forward_dilated_kernel (p >= 2: one warp per tile, the next chunk's records gathered by
+//   cp.async while the current chunk is walked): the same walk for the tile's <= 8x8 active pixels.
+// backward_kernel (ONE WARP PER TILE from a tile queue, independent warps, no block barriers;
+//   backward_cta_kernel for views with few tiles: one CTA per tile, a warp per 8x8 group, the
+//   group sums added through shared memory): backward tile phase (rasterizer.cpp:234-292), per
+//   chunk and 8x4 pixel group:
 //   1. per pixel, back to front over the union of the group's walked splats (all lanes on the
 //      same splat): T_i = T_{i+1} / (1 - sigma_i) with sigma recomputed bit-identically to the
 //      forward; g.dC/dsigma_i = T_i (g.c_i) - (g.S_i)/(1 - sigma_i) with the reference's exact
