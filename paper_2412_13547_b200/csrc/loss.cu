@@ -25,6 +25,13 @@ namespace {
 constexpr int kR = 5;                 // window radius (11 taps)
 constexpr int kTW = 32, kTH = 16;     // output tile
 constexpr int kHW = kTW + 2 * kR, kHH = kTH + 2 * kR;
+// Bank-conflict-free shared-memory strides: horizontal work item = (row yy = lane, column group
+// = warp; lanes 26-31 idle), so a warp walks down the rows of one column group; with odd row
+// strides (43 / 33 elements) its 4-B and 8-B accesses fall in distinct banks. The vertical pass
+// reads a row's 32 consecutive columns.
+static_assert(kTW / 4 == 256 / 32 && kHH <= 32, "one warp per 4-column group, one lane per haloed row");
+constexpr int kSW = kHW + 1;
+constexpr int kPW = kTW + 1;
 
 __constant__ float c_win[2 * kR + 1];
 
@@ -56,83 +63,105 @@ __global__ void __launch_bounds__(256) l1_kernel(const float* __restrict__ rgb, 
     }
 }
 
-// Separable windowed sums of NM maps over a haloed tile: in[m][kHH][kHW] -> out[m][kTH][kTW].
-// Register blocking: a horizontal work item produces 4 consecutive outputs from 14 loads, a
-// thread's vertical pass produces 2 consecutive rows from 12 loads (the shared-memory pipe, not
-// the FMA pipe, bounds the naive one-load-per-tap form).
-template <int NM>
-__device__ __forceinline__ void window_sums(const float (*in)[kHH][kHW], float (*hs)[kHH][kTW],
-                                            int tid, float (&out)[2][NM]) {
-    constexpr int kQ = kTW / 4;  // 4-wide column groups per row
-    for (int i = tid; i < kHH * kQ; i += 256) {
-        const int yy = i / kQ, x0 = 4 * (i % kQ);
-#pragma unroll
-        for (int m = 0; m < NM; ++m) {
-            float v[4 + 2 * kR];
-#pragma unroll
-            for (int j = 0; j < 4 + 2 * kR; ++j) v[j] = in[m][yy][x0 + j];
-#pragma unroll
-            for (int o = 0; o < 4; ++o) {
-                float acc = 0.f;
-#pragma unroll
-                for (int k = 0; k <= 2 * kR; ++k) acc = fmaf(c_win[k], v[o + k], acc);
-                hs[m][yy][x0 + o] = acc;
-            }
-        }
-    }
-    __syncthreads();
-    // each thread: two vertically consecutive output pixels (rows 2 ty, 2 ty + 1)
-    const int tx = tid % kTW, ty = tid / kTW;
-#pragma unroll
-    for (int m = 0; m < NM; ++m) {
-        float v[2 + 2 * kR];
-#pragma unroll
-        for (int j = 0; j < 2 + 2 * kR; ++j) v[j] = hs[m][2 * ty + j][tx];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            float acc = 0.f;
-#pragma unroll
-            for (int k = 0; k <= 2 * kR; ++k) acc = fmaf(c_win[k], v[h + k], acc);
-            out[h][m] = acc;
-        }
-    }
-}
+// Window taps as FP32x2 operands (the packed FFMA2 of a map pair takes the weight twice).
+__device__ __forceinline__ float2 wpair(int k) { return make_float2(c_win[k], c_win[k]); }
 
+// Shared-memory layout of the SSIM passes. Maps are carried in pairs where two of them share a
+// pass (packed FP32x2: (mu_x, mu_y), (x^2, y^2) sums; (a, b) adjoints) plus one single map
+// (x y sums; c adjoint); each tap is then one FFMA2 + one FFMA for three maps. A horizontal work
+// item produces 4 consecutive outputs of one haloed row from 14 loads, a thread's vertical pass
+// 2 consecutive rows (rows 2 ty, 2 ty + 1, column tx) from 12 loads. Tap order and FMA chains are
+// those of the plain per-map form (k = 0..10, acc = fma(w_k, v_k, acc)): identical results.
+struct SsimPass {
+    float2 hp[kHH][kPW];  // horizontal sums of the pair map
+    float2 hq[kHH][kPW];  // (stats only) the second pair map
+    float hs[kHH][kPW];   // the single map
+};
+
+// ssim_stats: in[ch][yy][xx] = (x, y) of the haloed tile for all three channels, loaded once;
+// per channel the horizontal pass forms x^2, y^2, x y on the fly from the (x, y) pairs.
 __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict__ rgb,
                                                          const float* __restrict__ target, int W, int H,
                                                          float* __restrict__ abc, float* __restrict__ block_sum) {
-    __shared__ float in[5][kHH][kHW];  // x, y, x^2, y^2, x y
-    __shared__ float hs[5][kHH][kTW];
+    __shared__ float2 in[3][kHH][kSW];
+    __shared__ SsimPass sp;
     __shared__ float red[8];
     const int tid = threadIdx.x;
     const int x0 = blockIdx.x * kTW - kR, y0 = blockIdx.y * kTH - kR;
+    const int64_t HW = (int64_t)W * H;
     const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
+#pragma unroll
+    for (int t = 0; t < (kHH * kHW + 255) / 256; ++t) {  // unrolled: every load issued up front
+        const int i = tid + 256 * t;
+        const int yy = i / kHW, xx = i - yy * kHW, gx = x0 + xx, gy = y0 + yy;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f;
+        if (i >= kHH * kHW) break;
+        if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+            const int64_t q = 3 * ((int64_t)gy * W + gx);
+            a0 = __ldg(rgb + q); a1 = __ldg(rgb + q + 1); a2 = __ldg(rgb + q + 2);
+            b0 = __ldg(target + q); b1 = __ldg(target + q + 1); b2 = __ldg(target + q + 2);
+        }
+        in[0][yy][xx] = make_float2(a0, b0);
+        in[1][yy][xx] = make_float2(a1, b1);
+        in[2][yy][xx] = make_float2(a2, b2);
+    }
+    __syncthreads();
+    const int tx = tid % kTW, ty = tid / kTW;
     float ssum = 0.f;
     for (int ch = 0; ch < 3; ++ch) {
-        for (int i = tid; i < kHH * kHW; i += 256) {
-            const int yy = i / kHW, xx = i % kHW, gx = x0 + xx, gy = y0 + yy;
-            float a = 0.f, b = 0.f;
-            if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
-                const int64_t q = 3 * ((int64_t)gy * W + gx) + ch;
-                a = rgb[q];
-                b = target[q];
+        if ((tid & 31) < kHH) {
+            const int yy = tid & 31, xb = 4 * (tid >> 5);
+            // streamed over the 14 inputs: output o takes tap k = j - o of input j (k ascending)
+            float2 am[4], aq[4];
+            float as[4];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) am[o] = aq[o] = make_float2(0.f, 0.f), as[o] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4 + 2 * kR; ++j) {
+                const float2 v = in[ch][yy][xb + j];
+                const float2 q = __fmul2_rn(v, v);
+                const float r = __fmul_rn(v.x, v.y);
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                    if (j - o < 0 || j - o > 2 * kR) continue;
+                    am[o] = __ffma2_rn(wpair(j - o), v, am[o]);
+                    aq[o] = __ffma2_rn(wpair(j - o), q, aq[o]);
+                    as[o] = fmaf(c_win[j - o], r, as[o]);
+                }
             }
-            in[0][yy][xx] = a;
-            in[1][yy][xx] = b;
-            in[2][yy][xx] = a * a;
-            in[3][yy][xx] = b * b;
-            in[4][yy][xx] = a * b;
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                sp.hp[yy][xb + o] = am[o];
+                sp.hq[yy][xb + o] = aq[o];
+                sp.hs[yy][xb + o] = as[o];
+            }
         }
         __syncthreads();
-        float st[2][5];
-        window_sums<5>(in, hs, tid, st);
-        const int tx = tid % kTW, ty = tid / kTW;
+        float2 mm[2], qq[2];
+        float ss[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) mm[h] = qq[h] = make_float2(0.f, 0.f), ss[h] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2 + 2 * kR; ++j) {
+            const float2 vm = sp.hp[2 * ty + j][tx], vq = sp.hq[2 * ty + j][tx];
+            const float vs = sp.hs[2 * ty + j][tx];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (j - h < 0 || j - h > 2 * kR) continue;
+                mm[h] = __ffma2_rn(wpair(j - h), vm, mm[h]);
+                qq[h] = __ffma2_rn(wpair(j - h), vq, qq[h]);
+                ss[h] = fmaf(c_win[j - h], vs, ss[h]);
+            }
+        }
+        __syncthreads();  // sp is rewritten by the next channel's horizontal pass
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
+            const float2 m = mm[h], sq = qq[h];
+            const float sxyr = ss[h];
             const int gx = blockIdx.x * kTW + tx, gy = blockIdx.y * kTH + 2 * ty + h;
             if (gx >= W || gy >= H) continue;
-            const float mx = st[h][0], my = st[h][1];
-            const float sxx = st[h][2] - mx * mx, syy = st[h][3] - my * my, sxy = st[h][4] - mx * my;
+            const float mx = m.x, my = m.y;
+            const float sxx = sq.x - mx * mx, syy = sq.y - my * my, sxy = sxyr - mx * my;
             const float A1 = 2.f * mx * my + C1, A2 = 2.f * sxy + C2;
             const float B1 = mx * mx + my * my + C1, B2 = sxx + syy + C2;
             const float iB = 1.f / (B1 * B2);
@@ -140,12 +169,12 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict
             ssum += S;
             const float dmu = 2.f * my * A2 * iB - 2.f * mx * S / B1;
             const float dsxx = -S / B2, dsxy = 2.f * A1 * iB;
-            float* o = abc + 9 * ((int64_t)gy * W + gx) + 3 * ch;
+            // planar adjoints: abc[(3 ch + k) H W + pixel], k = (a, b, c)
+            float* o = abc + (int64_t)(3 * ch) * HW + (int64_t)gy * W + gx;
             o[0] = dmu - 2.f * mx * dsxx - my * dsxy;
-            o[1] = dsxx;
-            o[2] = dsxy;
+            o[HW] = dsxx;
+            o[2 * HW] = dsxy;
         }
-        __syncthreads();
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
@@ -158,64 +187,152 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict
     }
 }
 
-__global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict__ rgb,
+// ssim_grad: per channel the haloed planar adjoints ((a, b) pairs + c; the next channel's are
+// fetched into registers while this one is filtered), G*a, G*b, G*c, then dL/dx for the
+// thread's two pixels.
+__global__ void __launch_bounds__(256, 4) ssim_grad_kernel(const float* __restrict__ rgb,
                                                         const float* __restrict__ target, int W, int H,
                                                         const float* __restrict__ abc, float scale,
                                                         float* __restrict__ dLdC) {
-    __shared__ float in[3][kHH][kHW];
-    __shared__ float hs[3][kHH][kTW];
+    constexpr int kPer = (kHH * kHW + 255) / 256;  // haloed pixels per thread
+    __shared__ float2 ab[kHH][kSW];
+    __shared__ float cc[kHH][kSW];
+    __shared__ SsimPass sp;  // (hq unused)
     const int tid = threadIdx.x;
     const int x0 = blockIdx.x * kTW - kR, y0 = blockIdx.y * kTH - kR;
-    for (int ch = 0; ch < 3; ++ch) {
-        for (int i = tid; i < kHH * kHW; i += 256) {
-            const int yy = i / kHW, xx = i % kHW, gx = x0 + xx, gy = y0 + yy;
-            float a = 0.f, b = 0.f, c = 0.f;
-            if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
-                const float* s = abc + 9 * ((int64_t)gy * W + gx) + 3 * ch;
-                a = s[0];
-                b = s[1];
-                c = s[2];
+    const int64_t HW = (int64_t)W * H;
+    float pa[kPer], pb[kPer], pc[kPer];
+    auto fetch = [&](int ch) {
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int i = tid + 256 * t;
+            const int yy = i / kHW, xx = i - yy * kHW, gx = x0 + xx, gy = y0 + yy;
+            pa[t] = pb[t] = pc[t] = 0.f;
+            if (i < kHH * kHW && gx >= 0 && gx < W && gy >= 0 && gy < H) {
+                const float* s = abc + (int64_t)(3 * ch) * HW + (int64_t)gy * W + gx;
+                pa[t] = __ldg(s);
+                pb[t] = __ldg(s + HW);
+                pc[t] = __ldg(s + 2 * HW);
             }
-            in[0][yy][xx] = a;
-            in[1][yy][xx] = b;
-            in[2][yy][xx] = c;
+        }
+    };
+    fetch(0);
+    const int tx = tid % kTW, ty = tid / kTW;
+    float gsum[2][3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        // (the previous channel's horizontal pass is past the barrier below: ab / cc are free)
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int i = tid + 256 * t;
+            if (i < kHH * kHW) {
+                const int yy = i / kHW, xx = i - yy * kHW;
+                ab[yy][xx] = make_float2(pa[t], pb[t]);
+                cc[yy][xx] = pc[t];
+            }
+        }
+        __syncthreads();  // also orders the previous channel's vertical reads before sp is rewritten
+        if (ch < 2) fetch(ch + 1);
+        if ((tid & 31) < kHH) {
+            const int yy = tid & 31, xb = 4 * (tid >> 5);
+            float2 am[4];
+            float as[4];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) am[o] = make_float2(0.f, 0.f), as[o] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4 + 2 * kR; ++j) {
+                const float2 v = ab[yy][xb + j];
+                const float r = cc[yy][xb + j];
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                    if (j - o < 0 || j - o > 2 * kR) continue;
+                    am[o] = __ffma2_rn(wpair(j - o), v, am[o]);
+                    as[o] = fmaf(c_win[j - o], r, as[o]);
+                }
+            }
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                sp.hp[yy][xb + o] = am[o];
+                sp.hs[yy][xb + o] = as[o];
+            }
         }
         __syncthreads();
-        float g[2][3];
-        window_sums<3>(in, hs, tid, g);
-        const int tx = tid % kTW, ty = tid / kTW;
+        float2 gg[2];
+        float gcc[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) gg[h] = make_float2(0.f, 0.f), gcc[h] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2 + 2 * kR; ++j) {
+            const float2 vm = sp.hp[2 * ty + j][tx];
+            const float vs = sp.hs[2 * ty + j][tx];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (j - h < 0 || j - h > 2 * kR) continue;
+                gg[h] = __ffma2_rn(wpair(j - h), vm, gg[h]);
+                gcc[h] = fmaf(c_win[j - h], vs, gcc[h]);
+            }
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
+            const float2 g = gg[h];
+            const float gc = gcc[h];
+            gsum[h][ch] = 0.f;
             const int gx = blockIdx.x * kTW + tx, gy = blockIdx.y * kTH + 2 * ty + h;
             if (gx >= W || gy >= H) continue;
             const int64_t q = 3 * ((int64_t)gy * W + gx) + ch;
-            dLdC[q] -= scale * (g[h][0] + 2.f * rgb[q] * g[h][1] + target[q] * g[h][2]);
+            gsum[h][ch] = g.x + 2.f * __ldg(rgb + q) * g.y + __ldg(target + q) * gc;
         }
-        __syncthreads();
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int gx = blockIdx.x * kTW + tx, gy = blockIdx.y * kTH + 2 * ty + h;
+        if (gx >= W || gy >= H) continue;
+        float* d = dLdC + 3 * ((int64_t)gy * W + gx);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) d[ch] -= scale * gsum[h][ch];
     }
 }
 
-// loss = w1 * sum(|d|) + lam * (1 - inv * sum(S)), sums in a fixed order (double)
-__global__ void loss_finalize_kernel(const float* __restrict__ l1_part, int n1, float w1,
-                                     const float* __restrict__ s_part, int n2, float lam, double inv,
-                                     float* __restrict__ out) {
-    __shared__ double sa[256], sb[256];
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < n1; i += 256) a += (double)l1_part[i];
-    for (int i = threadIdx.x; i < n2; i += 256) b += (double)s_part[i];
-    sa[threadIdx.x] = a;
-    sb[threadIdx.x] = b;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if ((int)threadIdx.x < w) {
-            sa[threadIdx.x] += sa[threadIdx.x + w];
-            sb[threadIdx.x] += sb[threadIdx.x + w];
+// loss = w1 * sum(|d|) + lam * (1 - inv * sum(S)), sums in a fixed order (double). One block of
+// 1024 threads; each thread keeps 8 independent running sums (8 partial loads in flight instead of
+// one dependent load-add chain: 32400 C3 tiles took 15 us that way), then warp shuffles.
+constexpr int kFinThreads = 1024, kFinUnroll = 8;
+__device__ __forceinline__ double block_sum_f64(const float* __restrict__ v, int n, double* red) {
+    double acc[kFinUnroll];
+#pragma unroll
+    for (int u = 0; u < kFinUnroll; ++u) acc[u] = 0.0;
+    for (int i = threadIdx.x; i < n; i += kFinThreads * kFinUnroll) {
+#pragma unroll
+        for (int u = 0; u < kFinUnroll; ++u) {
+            const int j = i + u * kFinThreads;
+            if (j < n) acc[u] += (double)__ldg(v + j);
         }
-        __syncthreads();
     }
+    double a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = a;
+    __syncthreads();
+    if (w == 0) {
+        a = red[l];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    }
+    __syncthreads();  // red is reused by the next sum
+    return a;         // (valid in warp 0)
+}
+
+__global__ void __launch_bounds__(kFinThreads) loss_finalize_kernel(const float* __restrict__ l1_part, int n1,
+                                                                   float w1, const float* __restrict__ s_part,
+                                                                   int n2, float lam, double inv,
+                                                                   float* __restrict__ out) {
+    __shared__ double red[kFinThreads / 32];
+    const double sa = block_sum_f64(l1_part, n1, red);
+    const double sb = block_sum_f64(s_part, n2, red);
     if (threadIdx.x == 0) {
-        double l = (double)w1 * sa[0];
-        if (n2 > 0) l += (double)lam * (1.0 - inv * sb[0]);
+        double l = (double)w1 * sa;
+        if (n2 > 0) l += (double)lam * (1.0 - inv * sb);
         out[0] = (float)l;
     }
 }
@@ -269,7 +386,7 @@ cudaError_t launch_ssim(tgsx_ctx* ctx, const float* rgb, const float* target, in
 
 cudaError_t launch_loss_finalize(tgsx_ctx* ctx, const float* l1_part, int n1, float w1, const float* s_part,
                                  int n2, float lam, double inv, float* out) {
-    loss_finalize_kernel<<<1, 256, 0, ctx->stream>>>(l1_part, n1, w1, s_part, n2, lam, inv, out);
+    loss_finalize_kernel<<<1, kFinThreads, 0, ctx->stream>>>(l1_part, n1, w1, s_part, n2, lam, inv, out);
     ctx->launches++;
     return cudaGetLastError();
 }
