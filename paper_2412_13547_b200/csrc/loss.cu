@@ -33,7 +33,13 @@ static_assert(kTW / 4 == 256 / 32 && kHH <= 32, "one warp per 4-column group, on
 constexpr int kSW = kHW + 1;
 constexpr int kPW = kTW + 1;
 
-__constant__ float c_win[2 * kR + 1];
+// The 11-tap window w_i = float(g_i / sum g), g_i = exp(-i^2 / (2 * 1.5^2)) in double, i = -5..5
+// (summed in order; oracle/tgs_oracle.c or_loss forms it the same way). Module-initialised
+// constant memory: valid on every device and inside graph captures without an upload
+// (tests/test_ssim_window.py recomputes these literals).
+__constant__ float c_win[2 * kR + 1] = {
+    0x1.0d956cp-10f, 0x1.f1fe02p-8f, 0x1.26eb18p-5f, 0x1.bff0fep-4f, 0x1.b43c40p-3f, 0x1.106560p-2f,
+    0x1.b43c40p-3f,  0x1.bff0fep-4f, 0x1.26eb18p-5f, 0x1.f1fe02p-8f, 0x1.0d956cp-10f};
 
 __global__ void __launch_bounds__(256) l1_kernel(const float* __restrict__ rgb, const float* __restrict__ target,
                                                  int p, int ox, int oy, int W, int cols, int64_t P,
@@ -337,22 +343,6 @@ __global__ void __launch_bounds__(kFinThreads) loss_finalize_kernel(const float*
     }
 }
 
-bool g_window_ready = false;
-
-cudaError_t upload_window() {
-    if (g_window_ready) return cudaSuccess;
-    float w[2 * kR + 1];
-    double g[2 * kR + 1], s = 0.0;
-    for (int i = -kR; i <= kR; ++i) {
-        g[i + kR] = std::exp(-(double)(i * i) / (2.0 * 1.5 * 1.5));
-        s += g[i + kR];
-    }
-    for (int i = 0; i <= 2 * kR; ++i) w[i] = (float)(g[i] / s);
-    cudaError_t e = cudaMemcpyToSymbol(c_win, w, sizeof(w));
-    if (!e) g_window_ready = true;
-    return e;
-}
-
 }  // namespace
 
 cudaError_t launch_l1(tgsx_ctx* ctx, const RenderArgs& ra, const float* rgb, float scale, float* dLdC,
@@ -372,8 +362,7 @@ size_t ssim_blocks(int W, int H) {
 
 cudaError_t launch_ssim(tgsx_ctx* ctx, const float* rgb, const float* target, int W, int H, float lam,
                         float* abc, float* block_sum, float* dLdC) {
-    cudaError_t e = upload_window();
-    if (e) return e;
+    cudaError_t e;
     const dim3 grid((W + kTW - 1) / kTW, (H + kTH - 1) / kTH);
     ssim_stats_kernel<<<grid, 256, 0, ctx->stream>>>(rgb, target, W, H, abc, block_sum);
     ctx->launches++;
