@@ -577,6 +577,23 @@ bool tgsx::graph_eligible_binning(const tgsx_ctx* ctx) {
 
 namespace {
 
+// rows of a dilated view's target into the workspace (StageRowsArgs); 16-B vectors when every
+// address allows (the source moves per graph replay, so the check is made per launch)
+__global__ void __launch_bounds__(256) stage_rows_kernel(StageRowsArgs a) {
+    const bool vec = ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15u) == 0 &&
+                     (a.row_floats & 3) == 0 && (a.pitch_floats & 3) == 0;
+    const int64_t per_row = vec ? a.row_floats / 4 : a.row_floats;
+    const int64_t total = per_row * a.rows;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / per_row, c = i - r * per_row;
+        if (vec)
+            reinterpret_cast<float4*>(a.dst + r * a.row_floats)[c] =
+                __ldg(reinterpret_cast<const float4*>(a.src + r * a.pitch_floats) + c);
+        else
+            a.dst[r * a.row_floats + c] = __ldg(a.src + r * a.pitch_floats + c);
+    }
+}
+
 bool is_device_ptr(const void* p) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -616,28 +633,44 @@ bool is_pinned_host_ptr(const void* p) {
 // (y - oy) / p (ra->target_rows = p). Device targets are used in place (full image).
 int32_t stage_target(tgsx_ctx* ctx, const float* src, size_t bytes, const float** out,
                      RenderArgs* ra = nullptr) {
+    const bool rows_only = ra && ra->p > 1 && ra->rows > 0;
+    const size_t row_bytes = ra ? (size_t)ra->W * 12 : 0;
+    if (ctx->graph_capturing && (ctx->graph_stage_targets || !is_device_ptr(src))) {
+        // a graph-replayed step copies its target (pinned host, or device once the fit uses more
+        // than one target; a dilated view only its active rows) on the compute stream into the
+        // workspace (sized before the capture): the copy is a node of the step's graph whose
+        // source is set per replay, so one graph serves every target of the same pattern
+        // (graph.cpp)
+        if (rows_only) bytes = row_bytes * (size_t)ra->rows;
+        DevBuf& b = ctx->ws.target;
+        if (b.bytes < bytes) CK(b.ensure(bytes));
+        const size_t off = rows_only ? (size_t)ra->oy * ra->W * 3 : 0;
+        if (rows_only) {  // a kernel node (its source can be re-targeted in the exec, a 2-D copy's not)
+            StageRowsArgs a{b.as<float>(), src + off, (int64_t)ra->W * 3, (int64_t)ra->W * 3 * ra->p, ra->rows};
+            stage_rows_kernel<<<(unsigned)std::min<int64_t>(4 * 148, (int64_t)ra->rows * 8), 256, 0, ctx->stream>>>(a);
+            ctx->launches++;
+            CK(cudaGetLastError());
+            ctx->graph_stage_args = a;
+            ctx->graph_target_kind = 2;
+            ra->target_rows = ra->p;
+        } else {
+            CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyDefault, ctx->stream));
+            ctx->graph_target_kind = 1;
+        }
+        cudaStreamCaptureStatus st;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        CK(cudaStreamGetCaptureInfo(ctx->stream, &st, nullptr, nullptr, &deps, &nd));
+        ctx->graph_target_node = nd == 1 ? (void*)deps[0] : nullptr;
+        ctx->graph_target_off = (int64_t)off;
+        *out = b.as<float>();
+        return TGSX_OK;
+    }
     if (is_device_ptr(src)) {
         *out = src;
         return TGSX_OK;
     }
-    const bool rows_only = ra && ra->p > 1 && ra->rows > 0;
-    const size_t row_bytes = ra ? (size_t)ra->W * 12 : 0;
     if (rows_only) bytes = row_bytes * (size_t)ra->rows;
-    if (ctx->graph_capturing) {
-        // a graph-replayed step copies its (pinned) host target on the compute stream into the
-        // workspace (sized before the capture): the copy is a node of the step's graph
-        DevBuf& b = ctx->ws.target;
-        if (b.bytes < bytes) CK(b.ensure(bytes));
-        if (rows_only) {
-            CK(cudaMemcpy2DAsync(b.p, row_bytes, src + (size_t)ra->oy * ra->W * 3, row_bytes * (size_t)ra->p,
-                                 row_bytes, (size_t)ra->rows, cudaMemcpyHostToDevice, ctx->stream));
-            ra->target_rows = ra->p;
-        } else {
-            CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
-        }
-        *out = b.as<float>();
-        return TGSX_OK;
-    }
     if (!ctx->copy_stream) {
         CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         for (int i = 0; i < 2; ++i) {
@@ -759,8 +792,16 @@ int32_t fused_view(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const 
         // device and pinned host destinations are written in stream order (read the pinned
         // value after tgsx_synchronize); pageable host memory is written before returning
         CK(cudaMemcpyAsync(out_loss, dloss, 4, cudaMemcpyDefault, ctx->stream));
-        if (!is_device_ptr(out_loss) && !is_pinned_host_ptr(out_loss))
+        if (ctx->graph_capturing) {  // the loss copy node: its destination is set per replay
+            cudaStreamCaptureStatus st;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t nd = 0;
+            CK(cudaStreamGetCaptureInfo(ctx->stream, &st, nullptr, nullptr, &deps, &nd));
+            ctx->graph_loss_node = nd == 1 ? (void*)deps[0] : nullptr;
+            ctx->graph_loss_src = dloss;
+        } else if (!is_device_ptr(out_loss) && !is_pinned_host_ptr(out_loss)) {
             CK(cudaStreamSynchronize(ctx->stream));
+        }
     }
     return TGSX_OK;
 }

@@ -16,9 +16,12 @@
 //    re-run eagerly in order, the fault cleared and the graph recaptured on the next call, so
 //    the sequence of model updates is exactly that of eager steps.
 //  * Per-step arguments: the Adam hyper-parameters (step count, learning-rate decay) are set on
-//    the captured chain kernel node of the exec before each launch; everything else (pattern,
-//    background, target / loss pointers, model and workspace buffers, sizes) is part of the key
-//    the graph was captured for — a different key re-runs eagerly and recaptures.
+//    the captured chain kernel node, the loss destination on the captured loss-copy node and the
+//    target on the captured target-copy node (the graph stages the target — only the active
+//    rows of a dilated view — into the workspace) of the exec before each launch; everything
+//    else (pattern, background, SSIM weight, memory types, model and workspace buffers, sizes)
+//    is part of the key the graph was captured for — a different key re-runs eagerly and
+//    recaptures.
 //
 // Every other entry point that reads or changes the model first calls graph_flush, so callers
 // observe the same state as after eager steps. Targets passed to replayed steps must stay
@@ -42,6 +45,14 @@ struct Entry {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec[2] = {nullptr, nullptr};  // per slot: the fault copy goes to h_fault[slot]
     cudaGraphNode_t chain = nullptr;
+    cudaGraphNode_t loss = nullptr;  // the out_loss copy (destination set per replay)
+    const void* loss_src = nullptr;
+    cudaGraphNode_t target = nullptr;  // the target staging into the workspace (source set per replay)
+    int target_kind = 0;               // 1: 1-D memcpy node, 2: stage-rows kernel node
+    cudaMemcpy3DParms target_parms{};
+    cudaKernelNodeParams target_kernel{};
+    StageRowsArgs target_args{};
+    int64_t target_off = 0;
     uint64_t kernels = 0;  // kernel launches per replay (counted at capture)
     uint64_t used = 0;     // last use (LRU)
     void release() {
@@ -64,9 +75,11 @@ struct FitGraph {
         const float* target = nullptr;
         tgsx_adam_args a{};
         float* out_loss = nullptr;
+        float ssim_weight = 0.f;
     } pend[2];
     uint64_t seq = 0;
     uint64_t captures = 0, replays = 0, reruns = 0;
+    const float* first_target = nullptr;  // the first device target replayed
 
     void drop_graphs() {
         for (auto& e : entries) e.release();
@@ -96,6 +109,15 @@ bool device_or_pinned(const void* p) {
         return false;
     }
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged || at.type == cudaMemoryTypeHost;
+}
+
+cudaMemoryType mem_type(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return cudaMemoryTypeUnregistered;
+    }
+    return at.type;
 }
 
 template <typename T>
@@ -132,8 +154,14 @@ std::vector<uintptr_t> make_key(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern
     put(k, pat->width);
     put(k, pat->height);
     for (int i = 0; i < 3; ++i) put(k, bg[i]);
-    put(k, target);
-    put(k, out_loss);
+    // a staged target (pinned host, or any target once several device targets were seen) is a
+    // per-replay argument; a device target read in place is part of the key
+    const cudaMemoryType tt = target ? mem_type(target) : cudaMemoryTypeUnregistered;
+    if (tt == cudaMemoryTypeDevice && !ctx->graph_stage_targets) put(k, target);
+    else put(k, 1 + (int)tt);
+    put(k, ctx->graph_stage_targets);
+    // the loss destination is a per-replay argument; its memory type is fixed by the copy node
+    put(k, out_loss ? 1 + (int)mem_type(out_loss) : 0);
     put(k, ctx->ssim_weight);
     put(k, ctx->binning_mode);
     put(k, ctx->stream);
@@ -151,12 +179,15 @@ int32_t rerun_from(tgsx_ctx* ctx, FitGraph& G, int s) {
     GK(cudaMemsetAsync(ctx->graph_fault, 0, sizeof(unsigned), ctx->stream));
     G.drop_graphs();  // outgrown capacities (or a kernel error): recapture on the next call
     ctx->graph_replaying = true;
+    const float w0 = ctx->ssim_weight;
     int32_t rc = TGSX_OK;
     for (auto& p : todo) {
         G.reruns++;
+        ctx->ssim_weight = p.ssim_weight;  // the weight the replayed step was captured with
         rc = tgsx_fit_step(ctx, p.m, &p.pat, p.bg, p.target, &p.a, p.out_loss);
         if (rc) break;
     }
+    ctx->ssim_weight = w0;
     ctx->graph_replaying = false;
     return rc;
 }
@@ -216,6 +247,9 @@ int32_t capture(tgsx_ctx* ctx, FitGraph& G, tgsx_model* m, const tgsx_pattern* p
     GK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     ctx->graph_capturing = true;
     ctx->graph_chain_node = nullptr;
+    ctx->graph_loss_node = nullptr;
+    ctx->graph_target_node = nullptr;
+    ctx->graph_target_kind = 0;
     int32_t rc = tgsx_fit_step(ctx, m, pat, bg, target, a, out_loss);
     cudaGraphNode_t fault_copy = nullptr;
     if (!rc) {
@@ -233,7 +267,7 @@ int32_t capture(tgsx_ctx* ctx, FitGraph& G, tgsx_model* m, const tgsx_pattern* p
     const cudaError_t ee = cudaStreamEndCapture(ctx->stream, &g);
     const uint64_t kernels = ctx->launches - launches0;
     ctx->launches = launches0;
-    if (rc || ee || !g || !fault_copy || !ctx->graph_chain_node) {
+    if (rc || ee || !g || !fault_copy || !ctx->graph_chain_node || (out_loss && !ctx->graph_loss_node)) {
         if (g) cudaGraphDestroy(g);
         cudaGetLastError();
         return rc ? rc : (ee ? cuda_err(ctx, ee, "cudaStreamEndCapture") : TGSX_OK);
@@ -248,9 +282,18 @@ int32_t capture(tgsx_ctx* ctx, FitGraph& G, tgsx_model* m, const tgsx_pattern* p
     Entry en;
     en.graph = g;
     en.chain = static_cast<cudaGraphNode_t>(ctx->graph_chain_node);
+    en.loss = out_loss ? static_cast<cudaGraphNode_t>(ctx->graph_loss_node) : nullptr;
+    en.loss_src = ctx->graph_loss_src;
+    en.target = static_cast<cudaGraphNode_t>(ctx->graph_target_node);
+    en.target_off = ctx->graph_target_off;
+    en.target_kind = en.target ? ctx->graph_target_kind : 0;
+    en.target_args = ctx->graph_stage_args;
+    cudaError_t e = cudaSuccess;
+    if (en.target_kind == 1) e = cudaGraphMemcpyNodeGetParams(en.target, &en.target_parms);
+    if (en.target_kind == 2) e = cudaGraphKernelNodeGetParams(en.target, &en.target_kernel);
     en.kernels = kernels;
     en.used = G.seq;
-    cudaError_t e = cudaGraphInstantiate(&en.exec[0], g, 0);
+    if (!e) e = cudaGraphInstantiate(&en.exec[0], g, 0);
     if (!e) e = cudaGraphInstantiate(&en.exec[1], g, 0);
     if (!e)
         e = cudaGraphExecMemcpyNodeSetParams1D(en.exec[1], fault_copy, ctx->h_graph_fault + 1, ctx->graph_fault,
@@ -310,6 +353,17 @@ int32_t tgsx_fit_graph_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pa
         if ((rc = check(ctx, G, false))) return rc;
         return tgsx_fit_step(ctx, m, pat, bg, target, a, out_loss);
     }
+    // a second device target: from now on targets are staged by a graph node (per-replay source)
+    // instead of being part of the key, so a multi-view fit keeps one graph per pattern
+    if (!ctx->graph_stage_targets && mem_type(target) == cudaMemoryTypeDevice) {
+        if (!G.first_target) {
+            G.first_target = target;
+        } else if (target != G.first_target) {
+            if ((rc = check(ctx, G, false))) return rc;
+            G.drop_graphs();
+            ctx->graph_stage_targets = true;
+        }
+    }
     const std::vector<uintptr_t> key = make_key(ctx, m, pat, bg, target, out_loss);
     Entry* en = nullptr;
     for (auto& e : G.entries)
@@ -328,6 +382,22 @@ int32_t tgsx_fit_graph_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pa
     AdamCfg c;
     adam_cfg_from_args(c, a);
     GK(chain_node_set_adam(en->exec[slot], en->chain, c));
+    if (en->loss)
+        GK(cudaGraphExecMemcpyNodeSetParams1D(en->exec[slot], en->loss, out_loss, en->loss_src, 4,
+                                              cudaMemcpyDefault));
+    if (en->target_kind == 1) {
+        cudaMemcpy3DParms tp = en->target_parms;
+        tp.srcPtr.ptr = const_cast<float*>(target + en->target_off);
+        GK(cudaGraphExecMemcpyNodeSetParams(en->exec[slot], en->target, &tp));
+    } else if (en->target_kind == 2) {
+        StageRowsArgs sa = en->target_args;
+        sa.src = target + en->target_off;
+        void* args[1] = {&sa};
+        cudaKernelNodeParams kp = en->target_kernel;
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        GK(cudaGraphExecKernelNodeSetParams(en->exec[slot], en->target, &kp));
+    }
     GK(cudaGraphLaunch(en->exec[slot], ctx->stream));
     GK(cudaEventRecord(G.done[slot], ctx->stream));
     en->used = G.seq;
@@ -341,6 +411,7 @@ int32_t tgsx_fit_graph_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pa
     p.target = target;
     p.a = *a;
     p.out_loss = out_loss;
+    p.ssim_weight = ctx->ssim_weight;
     G.replays++;
     return TGSX_OK;
 }

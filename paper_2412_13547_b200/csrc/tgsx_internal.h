@@ -25,6 +25,16 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
+// Arguments of the target-rows staging kernel of graph-captured dilated steps (capi.cu): rows
+// r = 0..rows-1 of row_floats floats from src + r * pitch_floats to dst + r * row_floats. A graph
+// replay re-targets src per step (graph.cpp: a 2-D memcpy node cannot be updated in an exec).
+struct StageRowsArgs {
+    float* dst;
+    const float* src;
+    int64_t row_floats, pitch_floats;
+    int32_t rows;
+};
+
 struct Status {
     int32_t code = TGSX_OK;
     std::string msg;
@@ -129,6 +139,13 @@ struct tgsx_ctx {
     unsigned* h_graph_fault = nullptr;  // pinned [2]: the fault word after each slot's last launch
     int64_t graph_guard_pairs = 0;      // pair count the captured step may produce (<= pair_cap)
     void* graph_chain_node = nullptr;   // cudaGraphNode_t of the captured chain kernel
+    void* graph_loss_node = nullptr;    // cudaGraphNode_t of the captured loss copy (out_loss), if any
+    const void* graph_loss_src = nullptr;  // its device source (the step's loss word)
+    bool graph_stage_targets = false;   // set once a fit replays steps for several device targets
+    void* graph_target_node = nullptr;  // cudaGraphNode_t of the captured target staging
+    int graph_target_kind = 0;          // 1: 1-D memcpy node, 2: stage-rows kernel node
+    int64_t graph_target_off = 0;       // its source offset (floats) from the target's base
+    tgsx::StageRowsArgs graph_stage_args{};  // kind 2: the kernel's captured arguments
     void* graph = nullptr;              // tgsx::FitGraph
 };
 

@@ -15,6 +15,7 @@
 // (the controller only reads them there), so the loop never waits on a loss readback.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -39,6 +40,7 @@ struct tgsx_trainer {
     std::vector<float> h_losses;
     float* h_pinned = nullptr;
     double last_budget = 0;
+    bool use_graph = true;           // TGSX_TRAINER_GRAPH=0: every step eager (A/B)
 };
 
 // The same schedule over a set of cameras of a 3-D model (tgsx_trainer3d_*).
@@ -66,6 +68,8 @@ template <typename TR>
 int32_t feed_losses(TR* tr) {
     const int64_t pending = tr->t - tr->fed;
     if (pending <= 0) return TGSX_OK;
+    // graph-replayed steps are verified first (a faulted one is re-run and rewrites its loss)
+    if (int32_t rc = tgsx_synchronize(tr->ctx)) return rc;
     if (cudaMemcpyAsync(tr->h_pinned, tr->d_losses, sizeof(float) * tr->ring, cudaMemcpyDeviceToHost,
                         (cudaStream_t)tgsx_get_stream(tr->ctx)) != cudaSuccess)
         return TGSX_ECUDA;
@@ -128,6 +132,7 @@ int32_t tgsx_trainer_create(tgsx_ctx* ctx, tgsx_model* m, const tgsx_train_confi
         }
     }
     tgsx_pcg32_init(tr->rng, cfg->seed, 1);
+    if (const char* e = std::getenv("TGSX_TRAINER_GRAPH")) tr->use_graph = std::strcmp(e, "0") != 0;
     tr->ring = std::max<int64_t>(cfg->densify_interval, 1) * 4 + 64;
     if (cudaMalloc(&tr->d_losses, sizeof(float) * tr->ring) != cudaSuccess ||
         cudaMallocHost(&tr->h_pinned, sizeof(float) * tr->ring) != cudaSuccess) {
@@ -183,7 +188,15 @@ int32_t tgsx_trainer_step(tgsx_trainer* tr, const float* const* targets, int64_t
         tgsx_adam_args a{++tr->adam_step, c.total_iters, std::hypot((double)tr->W, (double)tr->H)};
         // compute_loss: dense iterations add the SSIM term
         if ((rc = tgsx_set_ssim_weight(tr->ctx, pp == 1 ? c.ssim_weight : 0.f))) return rc;
-        rc = tgsx_fit_step(tr->ctx, tr->m, &pat, bg, targets[(t - 1) % n_targets], &a, dloss);
+        // While the model keeps its size (warm-up, and after the densification window) the step
+        // is replayed from a CUDA graph, one per pattern (graph.cpp stages the view's target by a
+        // node of the graph): the host only launches it. Inside the window every event resizes
+        // the model and would force p^2 + 1 recaptures per event, so those steps run eagerly.
+        const bool steady = t <= c.warmup_iters || t > c.densify_until;
+        if (steady && (int64_t)p * p + 1 <= 12 && tr->use_graph)
+            rc = tgsx_fit_graph_step(tr->ctx, tr->m, &pat, bg, targets[(t - 1) % n_targets], &a, dloss);
+        else
+            rc = tgsx_fit_step(tr->ctx, tr->m, &pat, bg, targets[(t - 1) % n_targets], &a, dloss);
         tgsx_set_ssim_weight(tr->ctx, 0.f);
         if (rc) return rc;
         r.dilated = dilate;

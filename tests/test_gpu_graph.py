@@ -120,3 +120,45 @@ def test_graph_then_eager_entry_points_flush(P, torch):
     dm.close()
     ref.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("p,steps", [(1, 9), (2, 13)])
+def test_graph_per_replay_targets_and_losses(P, torch, p, steps):
+    """A fit over several device targets with a new loss destination every step (the trainer's
+    loss ring): after the second distinct target the graphs stage the target through a copy node
+    whose source is set per replay, and the loss-copy node gets each step's destination — one
+    graph per pattern, every loss and the final model bit-identical to eager steps."""
+    ctx = P.Context(0)
+    n, W, H = 20_000, 384, 256
+    diag = float(np.hypot(W, H))
+    tgts = []
+    for s in (2, 3, 4):
+        tm = P.DeviceModel.from_host(P.GaussianModel.synthetic(s, n, W, H), ctx)
+        tgts.append(tm.render(P.DilationPattern(1, 0, 0, W, H)).colors.reshape(H, W, 3).astype(np.float32))
+        tm.close()
+    dev = [torch.from_numpy(t).cuda() for t in tgts]
+    ring = torch.zeros(steps, device="cuda")
+    torch.cuda.synchronize()
+    runs = []
+    for graph in (False, True):
+        dm = P.DeviceModel.from_host(P.GaussianModel.synthetic(1, n, W, H), ctx)
+        losses = []
+        for it in range(steps):
+            ox, oy = (it % (p * p)) % p, (it % (p * p)) // p
+            pat = P.DilationPattern(p, ox, oy, W, H)
+            if graph:
+                dm.fit_graph_step(pat, (0.0, 0.0, 0.0), dev[it % 3].data_ptr(), it + 1, 1000, diag,
+                                  ring[it:it + 1].data_ptr())
+            else:
+                losses.append(dm.fit_step(pat, (0.0, 0.0, 0.0), tgts[it % 3], it + 1, 1000, diag))
+        ctx.synchronize()
+        out = dm.download()
+        m1, m2 = dm.moments()
+        runs.append((out, m1, m2, losses if not graph else ring.cpu().numpy().tolist()))
+        dm.close()
+    (ea, e1, e2, el), (ga, g1, g2, gl) = runs
+    _same((ea, e1, e2, el[-1]), (ga, g1, g2, gl[-1]))
+    assert np.array_equal(np.float32(el), np.float32(gl))
+    caps, replays, reruns = ctx.graph_stats()
+    assert caps == 1 + p * p and replays == steps - caps and reruns == 0
+    ctx.close()
