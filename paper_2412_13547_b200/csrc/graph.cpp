@@ -102,16 +102,8 @@ int32_t cuda_err(tgsx_ctx* ctx, cudaError_t e, const char* where) {
         if (_e != cudaSuccess) return cuda_err(ctx, _e, #expr); \
     } while (0)
 
-bool device_or_pinned(const void* p) {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged || at.type == cudaMemoryTypeHost;
-}
-
 cudaMemoryType mem_type(const void* p) {
+    if (!p) return cudaMemoryTypeUnregistered;
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
         cudaGetLastError();
@@ -129,8 +121,13 @@ void put(std::vector<uintptr_t>& k, T v) {
 }
 
 // Everything the eager step's launch sequence depends on besides the device data.
+bool device_or_pinned(cudaMemoryType t) {
+    return t == cudaMemoryTypeDevice || t == cudaMemoryTypeManaged || t == cudaMemoryTypeHost;
+}
+
+// (target / loss memory types are looked up once per call by the caller)
 std::vector<uintptr_t> make_key(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pat, const float bg[3],
-                                const float* target, float* out_loss) {
+                                const float* target, float* out_loss, cudaMemoryType tt, cudaMemoryType lt) {
     std::vector<uintptr_t> k;
     put(k, m);
     put(k, m->uid);
@@ -156,12 +153,11 @@ std::vector<uintptr_t> make_key(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern
     for (int i = 0; i < 3; ++i) put(k, bg[i]);
     // a staged target (pinned host, or any target once several device targets were seen) is a
     // per-replay argument; a device target read in place is part of the key
-    const cudaMemoryType tt = target ? mem_type(target) : cudaMemoryTypeUnregistered;
     if (tt == cudaMemoryTypeDevice && !ctx->graph_stage_targets) put(k, target);
     else put(k, 1 + (int)tt);
     put(k, ctx->graph_stage_targets);
     // the loss destination is a per-replay argument; its memory type is fixed by the copy node
-    put(k, out_loss ? 1 + (int)mem_type(out_loss) : 0);
+    put(k, out_loss ? 1 + (int)lt : 0);
     put(k, ctx->ssim_weight);
     put(k, ctx->binning_mode);
     put(k, ctx->stream);
@@ -304,7 +300,7 @@ int32_t capture(tgsx_ctx* ctx, FitGraph& G, tgsx_model* m, const tgsx_pattern* p
         en.release();
         return cuda_err(ctx, e, "graph instantiate");
     }
-    en.key = make_key(ctx, m, pat, bg, target, out_loss);
+    en.key = make_key(ctx, m, pat, bg, target, out_loss, mem_type(target), mem_type(out_loss));
     G.entries.push_back(std::move(en));
     G.captures++;
     return TGSX_OK;
@@ -347,15 +343,16 @@ int32_t tgsx_fit_graph_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pa
     const int slot = (int)(G.seq & 1);
     int32_t rc = check(ctx, G, true);  // retires the step that last used `slot`
     if (rc) return rc;
+    const cudaMemoryType tt = mem_type(target), lt = mem_type(out_loss);
     const bool eligible = target && m->n > 0 && !ctx->prof.enabled && graph_eligible_binning(ctx) &&
-                          device_or_pinned(target) && (!out_loss || device_or_pinned(out_loss));
+                          device_or_pinned(tt) && (!out_loss || device_or_pinned(lt));
     if (!eligible) {
         if ((rc = check(ctx, G, false))) return rc;
         return tgsx_fit_step(ctx, m, pat, bg, target, a, out_loss);
     }
     // a second device target: from now on targets are staged by a graph node (per-replay source)
     // instead of being part of the key, so a multi-view fit keeps one graph per pattern
-    if (!ctx->graph_stage_targets && mem_type(target) == cudaMemoryTypeDevice) {
+    if (!ctx->graph_stage_targets && tt == cudaMemoryTypeDevice) {
         if (!G.first_target) {
             G.first_target = target;
         } else if (target != G.first_target) {
@@ -364,7 +361,7 @@ int32_t tgsx_fit_graph_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pa
             ctx->graph_stage_targets = true;
         }
     }
-    const std::vector<uintptr_t> key = make_key(ctx, m, pat, bg, target, out_loss);
+    const std::vector<uintptr_t> key = make_key(ctx, m, pat, bg, target, out_loss, tt, lt);
     Entry* en = nullptr;
     for (auto& e : G.entries)
         if (e.key == key) en = &e;
