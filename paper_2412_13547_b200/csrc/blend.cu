@@ -150,19 +150,18 @@ __device__ __forceinline__ bool walk_chunk(uint32_t cbase, int ccount, uint32_t 
     if (doneB) colB = 0;
     const uint32_t colA0 = colA, colB0 = colB;
     int termA = 32, termB = 32;  // bit of each pixel's terminating blend, 32 = none
-    const int kmax = ccount - 1;
     uint32_t colU = colA | colB;
-    // branch-free: a lane whose walk is over runs on record 0 with both pixels masked
-    // (sigma = 0 changes nothing)
+    // branch-free: a lane whose walk is over runs on record 32 (a spare slot past the chunk,
+    // whatever it holds) with both pixels masked (sigma = 0 changes nothing)
     // Two splats (k1 < k2) per iteration: their Gaussians are independent (ILP), the
     // blends are applied in order and a ray that terminates at k1 does not blend k2.
     while (__any_sync(kFull, colU)) {
-        // an empty set reads the chunk's last staged record with a zero bit (pixels masked)
-        const int k1 = min(__clz(colU), kmax);
-        const uint32_t bit1 = (0x80000000u >> k1) & colU;
+        // clz of an empty set is 32: the clamped funnel shift then gives a zero bit
+        const int k1 = __clz(colU);
+        const uint32_t bit1 = __funnelshift_rc(0x80000000u, 0u, (unsigned)k1);
         const uint32_t rem = colU & ~bit1;
-        const int k2 = min(__clz(rem), kmax);
-        const uint32_t bit2 = (0x80000000u >> k2) & rem;
+        const int k2 = __clz(rem);
+        const uint32_t bit2 = __funnelshift_rc(0x80000000u, 0u, (unsigned)k2);
         const bool hA1 = (colA & bit1) != 0u, hB1 = (colB & bit1) != 0u;
         const bool hA2 = (colA & bit2) != 0u, hB2 = (colB & bit2) != 0u;
         const uint32_t ad1 = cbase + k1 * kRec, ad2 = cbase + k2 * kRec;
@@ -263,7 +262,7 @@ template <int NWX, int NWY, int BATCH>
 #endif
 __global__ void __launch_bounds__(NWX * NWY * 32, TGSX_FWD_MINB) forward_pairs_kernel(BlendParams prm) {
     constexpr int NW = NWX * NWY, NT = NW * 32;
-    __shared__ __align__(16) unsigned char s_rec[BATCH * kRec];
+    __shared__ __align__(16) unsigned char s_rec[(BATCH + 1) * kRec];  // + the walk's spare slot
     __shared__ unsigned long long s_red[2][NW];
     __shared__ float s_loss[NW];
 
@@ -291,7 +290,17 @@ __global__ void __launch_bounds__(NWX * NWY * 32, TGSX_FWD_MINB) forward_pairs_k
     for (int bstart = 0; bstart < count; bstart += BATCH) {
         if (__syncthreads_and(warp_done)) break;
         const int bcount = min(BATCH, count - bstart);
-        for (int j = threadIdx.x; j < bcount; j += NT) {
+        // records past the list up to the last chunk's spare slot (c0 + 32) are zeroed: the
+        // walk reads that slot for an empty pass set (masked, but its colour must be finite)
+        const int bfill = min(BATCH, (bcount + 31) & ~31) + 1;
+        for (int j = threadIdx.x; j < bfill; j += NT) {
+            if (j >= bcount) {
+                const uint32_t dst = sbase + j * kRec;
+                sts_f4(dst, make_float4(0.f, 0.f, 0.f, 0.f));
+                sts_f4(dst + 16, make_float4(0.f, 0.f, 0.f, 0.f));
+                sts_f4(dst + 32, make_float4(0.f, 0.f, 0.f, 0.f));
+                continue;
+            }
             const Prepared& P = prm.prep[prm.items[range.x + bstart + j]];
             const float4 a = P.a, b = P.b, c = P.c;
             const uint32_t mask = box_mask(a.x, b.z, geo.ax, p, geo.acols) |
@@ -363,7 +372,7 @@ __device__ __forceinline__ void cp_async_wait_() {
 // its own record of the arrived chunk (box mask, pre-scaled conic) exactly as the p = 1 kernel.
 struct FwdWarpSmem {
     unsigned char raw[2][32 * sizeof(Prepared)];
-    unsigned char rec[32 * kRec];
+    unsigned char rec[33 * kRec];  // 32 records + the walk's spare slot
 };
 
 template <int NWX, int NWY>
@@ -402,6 +411,7 @@ __global__ void __launch_bounds__(NWX * NWY * 32, 32 / (NWX * NWY)) forward_dila
     bool doneA = !vA, doneB = !vB;
     bool warp_done = __all_sync(kFull, doneA && doneB);
     uint32_t item = 0;
+    if (lane < 3) sts_f4(recbase + 32 * kRec + 16 * lane, make_float4(0.f, 0.f, 0.f, 0.f));  // spare slot
     if (!warp_done && nch > 0) {
         issue(0, lane < count ? prm.items[range.x + lane] : 0u);
         item = 32 + lane < count ? prm.items[range.x + 32 + lane] : 0u;
