@@ -79,7 +79,14 @@ struct FitGraph {
     } pend[2];
     uint64_t seq = 0;
     uint64_t captures = 0, replays = 0, reruns = 0;
-    const float* first_target = nullptr;  // the first device target replayed
+    // per model (uid): the first device target replayed, and whether the model's fit has seen a
+    // second one (its graphs then stage the target through a node with a per-replay source)
+    struct TargetUse {
+        uint64_t uid;
+        const float* first;
+        bool staging;
+    };
+    std::vector<TargetUse> targets;
 
     void drop_graphs() {
         for (auto& e : entries) e.release();
@@ -350,17 +357,26 @@ int32_t tgsx_fit_graph_step(tgsx_ctx* ctx, tgsx_model* m, const tgsx_pattern* pa
         if ((rc = check(ctx, G, false))) return rc;
         return tgsx_fit_step(ctx, m, pat, bg, target, a, out_loss);
     }
-    // a second device target: from now on targets are staged by a graph node (per-replay source)
-    // instead of being part of the key, so a multi-view fit keeps one graph per pattern
-    if (!ctx->graph_stage_targets && tt == cudaMemoryTypeDevice) {
-        if (!G.first_target) {
-            G.first_target = target;
-        } else if (target != G.first_target) {
+    // a model's second device target: from now on its targets are staged by a graph node
+    // (per-replay source) instead of being part of the key, so a multi-view fit keeps one graph
+    // per pattern (a single-target fit reads its target in place, no copy)
+    FitGraph::TargetUse* tu = nullptr;
+    for (auto& u : G.targets)
+        if (u.uid == m->uid) tu = &u;
+    if (!tu) {
+        if (G.targets.size() >= 64) G.targets.erase(G.targets.begin());
+        G.targets.push_back({m->uid, nullptr, false});
+        tu = &G.targets.back();
+    }
+    if (!tu->staging && tt == cudaMemoryTypeDevice) {
+        if (!tu->first) {
+            tu->first = target;
+        } else if (target != tu->first) {
             if ((rc = check(ctx, G, false))) return rc;
-            G.drop_graphs();
-            ctx->graph_stage_targets = true;
+            tu->staging = true;
         }
     }
+    ctx->graph_stage_targets = tu->staging;
     const std::vector<uintptr_t> key = make_key(ctx, m, pat, bg, target, out_loss, tt, lt);
     Entry* en = nullptr;
     for (auto& e : G.entries)

@@ -141,7 +141,7 @@ struct tgsx_ctx {
     void* graph_chain_node = nullptr;   // cudaGraphNode_t of the captured chain kernel
     void* graph_loss_node = nullptr;    // cudaGraphNode_t of the captured loss copy (out_loss), if any
     const void* graph_loss_src = nullptr;  // its device source (the step's loss word)
-    bool graph_stage_targets = false;   // set once a fit replays steps for several device targets
+    bool graph_stage_targets = false;   // this call's model has replayed steps for several device targets
     void* graph_target_node = nullptr;  // cudaGraphNode_t of the captured target staging
     int graph_target_kind = 0;          // 1: 1-D memcpy node, 2: stage-rows kernel node
     int64_t graph_target_off = 0;       // its source offset (floats) from the target's base
