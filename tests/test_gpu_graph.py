@@ -122,14 +122,16 @@ def test_graph_then_eager_entry_points_flush(P, torch):
     ctx.close()
 
 
-@pytest.mark.parametrize("p,steps", [(1, 9), (2, 13)])
-def test_graph_per_replay_targets_and_losses(P, torch, p, steps):
+@pytest.mark.parametrize("p,steps,W,H", [(1, 9, 384, 256), (2, 13, 384, 256), (2, 9, 250, 131),
+                                          (3, 14, 250, 131)])
+def test_graph_per_replay_targets_and_losses(P, torch, p, steps, W, H):
     """A fit over several device targets with a new loss destination every step (the trainer's
     loss ring): after the second distinct target the graphs stage the target through a copy node
     whose source is set per replay, and the loss-copy node gets each step's destination — one
-    graph per pattern, every loss and the final model bit-identical to eager steps."""
+    graph per pattern, every loss and the final model bit-identical to eager steps. Widths not
+    divisible by 4 take the staging kernel's scalar path (dilated views stage active rows)."""
     ctx = P.Context(0)
-    n, W, H = 20_000, 384, 256
+    n = 20_000
     diag = float(np.hypot(W, H))
     tgts = []
     for s in (2, 3, 4):
