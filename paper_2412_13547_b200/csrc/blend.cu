@@ -140,28 +140,27 @@ __device__ __forceinline__ bool walk_chunk(uint32_t cbase, int ccount, uint32_t 
                                            uint32_t& lastA, uint32_t& lastB, uint32_t& ops, bool& doneA,
                                            bool& doneB) {
     const int lane = threadIdx.x & 31;
-    // bit-reversed pass sets (bit 31 - k = splat k): the next splat front to back is one FLO (clz)
-    const uint32_t bits =
-        __brev(transpose32(lane < ccount ? __float_as_uint(lds_f1(cbase + lane * kRec + 36)) : 0u));
+    // pass sets: bit k = splat k of the chunk
+    const uint32_t bits = transpose32(lane < ccount ? __float_as_uint(lds_f1(cbase + lane * kRec + 36)) : 0u);
     const uint32_t X = __shfl_sync(kFull, bits, bx * 8 + (lane & 7));
     uint32_t colA = X & __shfl_sync(kFull, bits, 16 + by * 8 + 2 * (lane >> 3));
     uint32_t colB = X & __shfl_sync(kFull, bits, 17 + by * 8 + 2 * (lane >> 3));
     if (doneA) colA = 0;
     if (doneB) colB = 0;
     const uint32_t colA0 = colA, colB0 = colB;
-    int termA = 32, termB = 32;  // bit of each pixel's terminating blend, 32 = none
+    int termA = 32, termB = 32;  // splat of each pixel's terminating blend, 32 = none
     uint32_t colU = colA | colB;
-    // branch-free: a lane whose walk is over runs on record 32 (a spare slot past the chunk,
-    // whatever it holds) with both pixels masked (sigma = 0 changes nothing)
-    // Two splats (k1 < k2) per iteration: their Gaussians are independent (ILP), the
-    // blends are applied in order and a ray that terminates at k1 does not blend k2.
+    // Two splats (k1 < k2) per iteration, lowest first (x & -x, its index one FLO): their
+    // Gaussians are independent (ILP), the blends are applied in order and a ray that terminates
+    // at k1 does not blend k2. Branch-free: an empty set gives a zero bit and index -1, the spare
+    // record slot in front of the chunk (finite contents, both pixels masked: sigma = 0 changes
+    // nothing).
     while (__any_sync(kFull, colU)) {
-        // clz of an empty set is 32: the clamped funnel shift then gives a zero bit
-        const int k1 = __clz(colU);
-        const uint32_t bit1 = __funnelshift_rc(0x80000000u, 0u, (unsigned)k1);
-        const uint32_t rem = colU & ~bit1;
-        const int k2 = __clz(rem);
-        const uint32_t bit2 = __funnelshift_rc(0x80000000u, 0u, (unsigned)k2);
+        const uint32_t bit1 = colU & (0u - colU);
+        const int k1 = 31 - __clz(bit1);
+        const uint32_t rem = colU ^ bit1;
+        const uint32_t bit2 = rem & (0u - rem);
+        const int k2 = 31 - __clz(bit2);
         const bool hA1 = (colA & bit1) != 0u, hB1 = (colB & bit1) != 0u;
         const bool hA2 = (colA & bit2) != 0u, hB2 = (colB & bit2) != 0u;
         const uint32_t ad1 = cbase + k1 * kRec, ad2 = cbase + k2 * kRec;
@@ -201,18 +200,17 @@ __device__ __forceinline__ bool walk_chunk(uint32_t cbase, int ccount, uint32_t 
         }
         colU = colA | colB;
     }
-    // (bit-reversed: positions 0..term are bits 31..31-term; the last used position is the
-    // lowest set bit)
+    // blended splats: the pass set up to the terminating one; the last is the highest set bit
     if (colA0) {
-        const uint32_t used = termA < 32 ? (colA0 & ~(0x7fffffffu >> termA)) : colA0;
+        const uint32_t used = termA < 32 ? (colA0 & (0xffffffffu >> (31 - termA))) : colA0;
         ops += __popc(used);
-        lastA = lbase + 32 - __ffs(used);
+        lastA = lbase + 31 - __clz(used);
         if (termA < 32) doneA = true;
     }
     if (colB0) {
-        const uint32_t used = termB < 32 ? (colB0 & ~(0x7fffffffu >> termB)) : colB0;
+        const uint32_t used = termB < 32 ? (colB0 & (0xffffffffu >> (31 - termB))) : colB0;
         ops += __popc(used);
-        lastB = lbase + 32 - __ffs(used);
+        lastB = lbase + 31 - __clz(used);
         if (termB < 32) doneB = true;
     }
     return __all_sync(kFull, doneA && doneB);
@@ -262,7 +260,7 @@ template <int NWX, int NWY, int BATCH>
 #endif
 __global__ void __launch_bounds__(NWX * NWY * 32, TGSX_FWD_MINB) forward_pairs_kernel(BlendParams prm) {
     constexpr int NW = NWX * NWY, NT = NW * 32;
-    __shared__ __align__(16) unsigned char s_rec[(BATCH + 1) * kRec];  // + the walk's spare slot
+    __shared__ __align__(16) unsigned char s_rec[(BATCH + 1) * kRec];  // the walk's spare slot + BATCH
     __shared__ unsigned long long s_red[2][NW];
     __shared__ float s_loss[NW];
 
@@ -279,7 +277,8 @@ __global__ void __launch_bounds__(NWX * NWY * 32, TGSX_FWD_MINB) forward_pairs_k
     const float fx = (float)x + 0.5f, fyA = (float)yA + 0.5f, fyB = (float)yB + 0.5f;
     const uint2 range = prm.ranges[tile];
     const int count = (int)(range.y - range.x);
-    const uint32_t sbase = smem_addr(s_rec);
+    const uint32_t sbase = smem_addr(s_rec) + kRec;  // record j at sbase + j kRec; spare slot (-1) zeroed
+    if (threadIdx.x < 3) sts_f4(sbase - kRec + 16 * threadIdx.x, make_float4(0.f, 0.f, 0.f, 0.f));
 
     float2 T = make_float2(1.0f, 1.0f);
     float2 C0 = make_float2(0.f, 0.f), C1 = C0, C2 = C0;
@@ -290,17 +289,7 @@ __global__ void __launch_bounds__(NWX * NWY * 32, TGSX_FWD_MINB) forward_pairs_k
     for (int bstart = 0; bstart < count; bstart += BATCH) {
         if (__syncthreads_and(warp_done)) break;
         const int bcount = min(BATCH, count - bstart);
-        // records past the list up to the last chunk's spare slot (c0 + 32) are zeroed: the
-        // walk reads that slot for an empty pass set (masked, but its colour must be finite)
-        const int bfill = min(BATCH, (bcount + 31) & ~31) + 1;
-        for (int j = threadIdx.x; j < bfill; j += NT) {
-            if (j >= bcount) {
-                const uint32_t dst = sbase + j * kRec;
-                sts_f4(dst, make_float4(0.f, 0.f, 0.f, 0.f));
-                sts_f4(dst + 16, make_float4(0.f, 0.f, 0.f, 0.f));
-                sts_f4(dst + 32, make_float4(0.f, 0.f, 0.f, 0.f));
-                continue;
-            }
+        for (int j = threadIdx.x; j < bcount; j += NT) {
             const Prepared& P = prm.prep[prm.items[range.x + bstart + j]];
             const float4 a = P.a, b = P.b, c = P.c;
             const uint32_t mask = box_mask(a.x, b.z, geo.ax, p, geo.acols) |
@@ -372,7 +361,7 @@ __device__ __forceinline__ void cp_async_wait_() {
 // its own record of the arrived chunk (box mask, pre-scaled conic) exactly as the p = 1 kernel.
 struct FwdWarpSmem {
     unsigned char raw[2][32 * sizeof(Prepared)];
-    unsigned char rec[33 * kRec];  // 32 records + the walk's spare slot
+    unsigned char rec[33 * kRec];  // the walk's spare slot + 32 records
 };
 
 template <int NWX, int NWY>
@@ -393,7 +382,7 @@ __global__ void __launch_bounds__(NWX * NWY * 32, 32 / (NWX * NWY)) forward_dila
     const uint2 range = prm.ranges[tile];
     const int count = (int)(range.y - range.x);
     const int nch = (count + 31) >> 5;
-    const uint32_t rawbase = smem_addr(S.raw), recbase = smem_addr(S.rec);
+    const uint32_t rawbase = smem_addr(S.raw), recbase = smem_addr(S.rec) + kRec;  // spare slot at -1
     const uint32_t myraw = rawbase + lane * (uint32_t)sizeof(Prepared);
     // chunk c's gathers: lane copies its entry's record into raw[c & 1] (nothing past the list)
     auto issue = [&](int c, uint32_t item) {
@@ -411,7 +400,7 @@ __global__ void __launch_bounds__(NWX * NWY * 32, 32 / (NWX * NWY)) forward_dila
     bool doneA = !vA, doneB = !vB;
     bool warp_done = __all_sync(kFull, doneA && doneB);
     uint32_t item = 0;
-    if (lane < 3) sts_f4(recbase + 32 * kRec + 16 * lane, make_float4(0.f, 0.f, 0.f, 0.f));  // spare slot
+    if (lane < 3) sts_f4(recbase - kRec + 16 * lane, make_float4(0.f, 0.f, 0.f, 0.f));  // spare slot
     if (!warp_done && nch > 0) {
         issue(0, lane < count ? prm.items[range.x + lane] : 0u);
         item = 32 + lane < count ? prm.items[range.x + 32 + lane] : 0u;
