@@ -841,11 +841,16 @@ int32_t check_kernel_error3d(tgsx_ctx* ctx, unsigned long long err) {
     return fail(ctx, TGSX_ERUNTIME, "projected covariance numerically degenerate (row " + std::to_string(row) + ")");
 }
 
+// defer (fused 3-D views): as the 2-D bin_compute — the per-tile sort is launched for lists up to
+// the previous 3-D binning's longest (x1.25) without waiting for the counters; the caller queues
+// its forward and bin3d_settle() checks them, redoing the lists when the guess was short. The
+// host then never stalls the stream between the preprocess and the blend kernels.
 int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int W, int H,
-              uint32_t** items) {
+              uint32_t** items, bool defer = false) {
     Workspace& ws = ctx->ws;
     ctx->bin_valid = false;  // the 2-D path's binning reuse never sees these buffers as its own
     ctx->bin_pending = false;
+    ctx->bin3d_pending = false;
     ws.have_forward = false;
     const int64_t n = m->n;
     CK(reset_counters(ctx));
@@ -864,11 +869,26 @@ int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, in
         }
         CK(cudaMemcpyAsync(ws.h_scratch, counters0, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            ctx->stream));
+        if (defer && ctx->bin3d_max_hint > 0 && !debug_checks()) {
+            if (!ctx->bin_event) CK(cudaEventCreateWithFlags(&ctx->bin_event, cudaEventDisableTiming));
+            CK(cudaEventRecord(ctx->bin_event, ctx->stream));
+            const uint64_t guess = std::min<uint64_t>(kSegCap, ctx->bin3d_max_hint + ctx->bin3d_max_hint / 4);
+            ctx->bin3d_sort_cap = guess <= 256 ? 256 : (guess <= 512 ? 512 : kSegCap);
+            {
+                StageTimer t(ctx, kStSort);
+                CK(launch_seg_sort3d(ctx, ntiles, (int64_t)guess));
+            }
+            m->rank_ordered = false;
+            ctx->bin3d_pending = true;
+            *items = ws.tile_slab.as<uint32_t>();
+            return TGSX_OK;
+        }
         CK(cudaStreamSynchronize(ctx->stream));
         if (ctx->prof.enabled) ctx->prof.harvest();
         int32_t rc0 = check_kernel_error3d(ctx, ws.h_scratch[0]);
         if (rc0) return rc0;
         const uint64_t max_list = ws.h_scratch[5];
+        ctx->bin3d_max_hint = max_list;
         if (max_list <= (uint64_t)kSegCap) {
             const int64_t K = (int64_t)(uint32_t)(ws.h_scratch[3] & 0xffffffffull);
             ws.K = K;
@@ -928,13 +948,53 @@ int32_t bin3d(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, in
     return bin_onesweep(ctx, nullptr, n, W, H, K, items, nullptr);
 }
 
+// Completes a deferred 3-D binning (bin3d with defer): waits for the counters (normally long
+// complete), reports kernel errors, sizes the per-pair partials and, when the speculative per-tile
+// sort was too short (or a list outgrew its slab: the global-sort path), redoes the lists; *redo
+// tells the caller to rerun its forward.
+int32_t bin3d_settle(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, int lowpass_p, int W, int H,
+                     uint32_t** items, bool* redo) {
+    *redo = false;
+    if (!ctx->bin3d_pending) return TGSX_OK;
+    ctx->bin3d_pending = false;
+    Workspace& ws = ctx->ws;
+    CK(cudaEventSynchronize(ctx->bin_event));
+    int32_t rc = check_kernel_error3d(ctx, ws.h_scratch[0]);
+    if (rc) return rc;
+    const int64_t K = (int64_t)(uint32_t)(ws.h_scratch[3] & 0xffffffffull);
+    const uint64_t max_list = ws.h_scratch[5];
+    ctx->bin3d_max_hint = max_list;
+    if (max_list > (uint64_t)kSegCap) {  // a list longer than a slab: bin again on the global-sort path
+        *redo = true;
+        return bin3d(ctx, m, cam, lowpass_p, W, H, items, false);
+    }
+    ws.K = K;
+    CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
+    ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
+    if (max_list <= (uint64_t)ctx->bin3d_sort_cap) return TGSX_OK;
+    *redo = true;
+    {
+        StageTimer t(ctx, kStSort);
+        CK(launch_seg_sort3d(ctx, ((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile), (int64_t)max_list));
+    }
+    *items = ws.tile_slab.as<uint32_t>();
+    return TGSX_OK;
+}
+
 int32_t render3d_core(tgsx_ctx* ctx, tgsx_model3d* m, const Cam3& cam, const RenderArgs& ra,
-                      bool fused_loss, uint32_t** items_out) {
+                      bool fused_loss, uint32_t** items_out, bool defer = false) {
     uint32_t* items = nullptr;
-    int32_t rc = bin3d(ctx, m, cam, ra.lowpass_p, ra.W, ra.H, &items);
+    int32_t rc = bin3d(ctx, m, cam, ra.lowpass_p, ra.W, ra.H, &items, defer);
     if (rc) return rc;
     CK(ensure_pixels(ctx, ra));
     {
+        StageTimer t(ctx, kStForward);
+        CK(launch_forward(ctx, ra, items, fused_loss));
+    }
+    bool redo = false;
+    if ((rc = bin3d_settle(ctx, m, cam, ra.lowpass_p, ra.W, ra.H, &items, &redo))) return rc;
+    if (redo) {  // the speculative lists were short: forward again on the settled ones
+        CK(reset_counters(ctx));
         StageTimer t(ctx, kStForward);
         CK(launch_forward(ctx, ra, items, fused_loss));
     }
@@ -1913,7 +1973,7 @@ static int32_t fused_view3d(tgsx_ctx* ctx, tgsx_model3d* m, const tgsx_camera* c
     Workspace& ws = ctx->ws;
     if ((rc = stage_target(ctx, target, (size_t)ra.W * ra.H * 12, &ra.target, &ra))) return rc;
     uint32_t* items = nullptr;
-    if ((rc = render3d_core(ctx, m, c3, ra, true, &items))) return rc;
+    if ((rc = render3d_core(ctx, m, c3, ra, true, &items, true))) return rc;
     int nsb = 0;
     if (lam > 0.f && ra.P > 0) {
         StageTimer t(ctx, kStLoss);

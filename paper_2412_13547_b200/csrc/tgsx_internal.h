@@ -120,6 +120,9 @@ struct tgsx_ctx {
     bool bin_pending = false;
     int bin_sort_cap = 0;           // longest list the speculative per-tile sort handled
     uint64_t bin_max_hint = 0;      // longest list of the previous binning
+    uint64_t bin3d_max_hint = 0;    // 3-D views: the previous binning's longest list
+    int bin3d_sort_cap = 0;         // 3-D: longest list the speculative per-tile sort handled
+    bool bin3d_pending = false;     // 3-D: a deferred binning awaits bin3d_settle
     // blend backward launch configuration, per context (= per device): the dynamic shared-memory
     // opt-in is a per-device function attribute and the resident-CTA count sizes the grid
     int bwd_resident[3] = {0, 0, 0};  // [0] / [1] resident CTAs of backward_kernel<2,2> / <1,1>; [2] CTA variant configured
