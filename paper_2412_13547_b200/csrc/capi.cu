@@ -9,16 +9,50 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
 namespace tgsx {
 
+// Buffers outgrown in the middle of a fit are not freed on the spot: cudaFree synchronises the
+// whole device (the queued work of this and the next step drains) and unmapping can take tens of
+// milliseconds, which showed up as 50-200 ms stalls of the first step after a densify event.
+// They are retired here and freed at the next explicit synchronisation point (tgsx_synchronize,
+// tgsx_destroy) — or at once when more than kGraveCap bytes are waiting.
+static std::mutex g_grave_mu;
+static std::vector<void*> g_grave;
+static size_t g_grave_bytes = 0;
+constexpr size_t kGraveCap = size_t(4) << 30;
+
+static void drain_graveyard_locked() {
+    for (void* q : g_grave) cudaFree(q);
+    g_grave.clear();
+    g_grave_bytes = 0;
+}
+
+static void retire(void* q, size_t nb) {
+    std::lock_guard<std::mutex> lock(g_grave_mu);
+    g_grave.push_back(q);
+    g_grave_bytes += nb;
+    if (g_grave_bytes > kGraveCap) drain_graveyard_locked();
+}
+
+void drain_graveyard() {
+    std::lock_guard<std::mutex> lock(g_grave_mu);
+    drain_graveyard_locked();
+}
+
 cudaError_t DevBuf::ensure(size_t need) {
     if (need <= bytes && p) return cudaSuccess;
-    release();
+    const bool growing = p != nullptr;
+    if (p) retire(p, bytes);
+    p = nullptr;
+    bytes = 0;
     size_t nb = std::max<size_t>(need, 256);
-    nb = nb + nb / 4;  // headroom: K and P drift between iterations
+    // headroom: K and P drift between iterations; a buffer that had to grow (a fit whose model
+    // grows) gets more, so a growing fit reallocates rarely
+    nb = growing ? nb + nb / 2 : nb + nb / 4;
     cudaError_t e = cudaMalloc(&p, nb);
     if (e) {
         p = nullptr;
@@ -40,7 +74,7 @@ cudaError_t DevBuf::grow_keep(size_t need, size_t keep_bytes, cudaStream_t s) {
         if (e) return e;
         cudaStreamSynchronize(s);
     }
-    release();
+    if (p) retire(p, bytes);
     p = np;
     bytes = nb;
     return cudaSuccess;
@@ -1095,8 +1129,9 @@ void tgsx_destroy(tgsx_ctx* ctx) {
                       &ws.vals[0], &ws.vals[1], &ws.sort_tmp, &ws.ranges, &ws.partial, &ws.rgb,
                       &ws.T, &ws.last, &ws.dLdC, &ws.target, &ws.block_loss, &ws.counters,
                       &ws.generic, &ws.tile_fill, &ws.tile_slab, &ws.ssim_abc, &ws.ssim_part,
-                      &ws.loss_grad};
+                      &ws.loss_grad, &ws.rect};
     for (DevBuf* b : bufs) b->release();
+    drain_graveyard();
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);
         cudaStreamDestroy(ctx->copy_stream);
@@ -1137,6 +1172,7 @@ void tgsx_host_free(void* p) {
 int32_t tgsx_synchronize(tgsx_ctx* ctx) {
     if (int32_t rc = graph_flush(ctx)) return rc;
     CK(cudaStreamSynchronize(ctx->stream));
+    drain_graveyard();  // outgrown buffers (the stream is idle here)
     return TGSX_OK;
 }
 
@@ -1775,6 +1811,20 @@ int32_t tgsx_model3d_reserve(tgsx_ctx* ctx, tgsx_model3d* m, int64_t capacity) {
     if (int32_t rc_ = tgsx::graph_flush(ctx)) return rc_;
     ctx->bin_valid = false;
     CK(model3d_reserve(ctx, m, capacity, true));
+    // the prune compaction's spare row buffers (densify3d.cu, same order and sizes), allocated now
+    // instead of inside the first densify event (a GB-scale cudaMalloc in the middle of a fit)
+    const int rows[10] = {k3dParams, k3dParams, k3dParams, 1, 1, 1, 1, 1, 1, 1};
+    const int elt[10] = {4, 4, 4, 4, 4, 4, 4, 4, 8, 8};
+    for (int i = 0; i < 10; ++i) {
+        DevBuf& sp = m->spare[i];
+        const size_t bytes = (size_t)rows[i] * m->cap * elt[i];
+        if (sp.bytes < bytes) {
+            CK(cudaStreamSynchronize(ctx->stream));
+            sp.release();
+            CK(cudaMalloc(&sp.p, bytes));
+            sp.bytes = bytes;
+        }
+    }
     return TGSX_OK;
 }
 

@@ -35,6 +35,9 @@ struct StageRowsArgs {
     int32_t rows;
 };
 
+// frees the buffers DevBuf::ensure / grow_keep retired while growing (capi.cu)
+void drain_graveyard();
+
 struct Status {
     int32_t code = TGSX_OK;
     std::string msg;
