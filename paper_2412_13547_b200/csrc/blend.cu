@@ -856,11 +856,48 @@ __device__ __forceinline__ void backward_tile(const BlendParams& prm, BwdWarpSme
                 // hand each half-row's sums to lane j = its splat (from up to two lanes)
                 const bool m0h = in0 && row0 >= rb && row0 < re, m1h = in1 && row1 >= rb && row1 < re;
                 const int src0 = m0h ? 2 * (row0 - rb) : 0, src1 = m1h ? 2 * (row1 - rb) + 1 : 1;
+#ifndef TGSX_BWD_SMEM_HANDOFF
+#define TGSX_BWD_SMEM_HANDOFF 1
+#endif
+#if TGSX_BWD_SMEM_HANDOFF
+                // through the (now read) rows of rec_u: 3 stores + up to 6 loads instead of 18
+                // shuffles (lane l's sums at 48 l: conflict-free stores)
+                __syncwarp();
+                {
+                    const uint32_t hb = ubase + 48u * (uint32_t)lane;
+                    sts_f4(hb, make_float4(acc[0], acc[1], acc[2], acc[3]));
+                    sts_f4(hb + 16, make_float4(acc[4], acc[5], acc[6], acc[7]));
+                    sts_f1(hb + 32, acc[8]);
+                }
+                __syncwarp();
+                if (m0h || m1h) {
+                    float v0[9], v1[9];
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) v0[q] = v1[q] = 0.f;
+                    if (m0h) {
+                        const uint32_t a = ubase + 48u * (uint32_t)src0;
+                        const float4 x = lds_f4(a), y = lds_f4(a + 16);
+                        v0[0] = x.x; v0[1] = x.y; v0[2] = x.z; v0[3] = x.w;
+                        v0[4] = y.x; v0[5] = y.y; v0[6] = y.z; v0[7] = y.w;
+                        v0[8] = lds_f1(a + 32);
+                    }
+                    if (m1h) {
+                        const uint32_t a = ubase + 48u * (uint32_t)src1;
+                        const float4 x = lds_f4(a), y = lds_f4(a + 16);
+                        v1[0] = x.x; v1[1] = x.y; v1[2] = x.z; v1[3] = x.w;
+                        v1[4] = y.x; v1[5] = y.y; v1[6] = y.z; v1[7] = y.w;
+                        v1[8] = lds_f1(a + 32);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) acc[q] = v0[q] + v1[q];
+                }
+#else
 #pragma unroll
                 for (int q = 0; q < 9; ++q) {
                     const float v0 = __shfl_sync(kFull, acc[q], src0), v1 = __shfl_sync(kFull, acc[q], src1);
                     acc[q] = (m0h ? v0 : 0.f) + (m1h ? v1 : 0.f);
                 }
+#endif
                 if (m0h || m1h) {
                     const float a0 = acc[0], ax1 = acc[1], ay1 = acc[2];
                     m0 += a0;
