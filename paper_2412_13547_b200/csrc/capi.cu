@@ -323,6 +323,14 @@ int32_t check_kernel_error(tgsx_ctx* ctx, unsigned long long err) {
                 "covariance numerically degenerate (det <= 0) (blend rank " + std::to_string(rank) + ")");
 }
 
+// per-pair partial slots to reserve for K pairs of an n-splat model of capacity cap: scaled by
+// cap / n (a fit growing its model towards a reserved budget keeps one allocation)
+int64_t pair_capacity(int64_t K, int64_t n, int64_t cap) {
+    const int64_t k = std::max<int64_t>(K, 1);
+    if (n <= 0 || cap <= n) return k;
+    return k + (int64_t)((double)k * (double)(cap - n) / (double)n);
+}
+
 cudaError_t reset_counters(tgsx_ctx* ctx) {
     Workspace& ws = ctx->ws;
     cudaError_t e = ws.counters.ensure(8 * sizeof(unsigned long long));
@@ -408,7 +416,7 @@ int32_t bin_compute(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, u
     const uint64_t max_list = ws.h_scratch[5];
     ws.K = K;
     ctx->bin_max_hint = max_list;
-    CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
+    CK(ws.partial.ensure(pair_capacity(K, m->n, m->cap) * 40));
     ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
     if (max_list <= (uint64_t)kSegCap && !force_onesweep(ctx)) {
         // slab binning: every tile's list was claimed by preprocess into its slab; sort each slab
@@ -443,7 +451,7 @@ int32_t bin_settle(tgsx_ctx* ctx, tgsx_model* m, int W, int H, uint32_t** items,
     const uint64_t max_list = ws.h_scratch[5];
     ws.K = K;
     ctx->bin_max_hint = max_list;
-    CK(ws.partial.ensure(std::max<int64_t>(K, 1) * 40));
+    CK(ws.partial.ensure(pair_capacity(K, m->n, m->cap) * 40));
     ws.pair_cap = (int64_t)(ws.partial.bytes / 40);
     if (max_list <= (uint64_t)ctx->bin_sort_cap) return TGSX_OK;
     *redo = true;

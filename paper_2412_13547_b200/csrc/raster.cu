@@ -380,8 +380,8 @@ cudaError_t launch_claims(tgsx_ctx* ctx, tgsx_model* m) {
     if (!m->spatial_valid || (m->spatial_age >= kSpatialRefresh && !ctx->graph_capturing)) {
         if ((e = m->spatial.ensure((size_t)m->cap * 4))) return e;
         for (int b = 0; b < 2; ++b) {
-            if ((e = ws.keys[b].ensure(n * 4))) return e;
-            if ((e = ws.vals[b].ensure(n * 4))) return e;
+            if ((e = ws.keys[b].ensure(std::max<int64_t>(m->cap, n) * 4))) return e;
+            if ((e = ws.vals[b].ensure(std::max<int64_t>(m->cap, n) * 4))) return e;
         }
         ctx->bin_valid = false;  // the sort reuses the binning buffers
         uint32_t *k = ws.keys[0].as<uint32_t>(), *v = ws.vals[0].as<uint32_t>();
@@ -405,11 +405,14 @@ cudaError_t launch_claims(tgsx_ctx* ctx, tgsx_model* m) {
 cudaError_t launch_preprocess(tgsx_ctx* ctx, tgsx_model* m, int lowpass_p, int W, int H, uint32_t* d_total) {
     Workspace& ws = ctx->ws;
     const int64_t n = m->n;
+    // per-splat buffers sized by the model's capacity: a fit that grows its model (densify up to
+    // a reserved budget) never reallocates them mid-run
+    const int64_t nc = std::max<int64_t>(m->cap, n);
     cudaError_t e;
-    if ((e = ws.prep.ensure(std::max<int64_t>(n, 1) * sizeof(Prepared)))) return e;
-    if ((e = ws.touched.ensure((n + 1) * 4))) return e;
-    if ((e = ws.pair_off.ensure((n + 1) * 4))) return e;
-    if ((e = ws.rect.ensure((n + 1) * 8))) return e;
+    if ((e = ws.prep.ensure(std::max<int64_t>(nc, 1) * sizeof(Prepared)))) return e;
+    if ((e = ws.touched.ensure((nc + 1) * 4))) return e;
+    if ((e = ws.pair_off.ensure((nc + 1) * 4))) return e;
+    if ((e = ws.rect.ensure((nc + 1) * 8))) return e;
     ws.tiles_x = (W + kTile - 1) / kTile;
     ws.tiles_y = (H + kTile - 1) / kTile;
     const size_t tiles = (size_t)std::max(ws.tiles_x * ws.tiles_y, 1);

@@ -373,8 +373,8 @@ cudaError_t launch_sort_depth(tgsx_ctx* ctx, tgsx_model* m) {
     if ((e = model_to_logical_order(ctx, m))) return e;
     ctx->bin_valid = false;  // the sort reuses the binning buffers
     for (int i = 0; i < 2; ++i) {
-        if ((e = ws.keys[i].ensure(n * 4))) return e;
-        if ((e = ws.vals[i].ensure(n * 4))) return e;
+        if ((e = ws.keys[i].ensure(std::max<int64_t>(m->cap, n) * 4))) return e;  // by capacity (growing fits)
+        if ((e = ws.vals[i].ensure(std::max<int64_t>(m->cap, n) * 4))) return e;
     }
     uint32_t* k = ws.keys[0].as<uint32_t>();
     uint32_t* v = ws.vals[0].as<uint32_t>();
