@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -21,19 +22,27 @@ namespace tgsx {
 // They are retired here and freed at the next explicit synchronisation point (tgsx_synchronize,
 // tgsx_destroy) — or at once when more than kGraveCap bytes are waiting.
 static std::mutex g_grave_mu;
-static std::vector<void*> g_grave;
+static std::vector<std::pair<int, void*>> g_grave;  // (device current at retirement, pointer)
 static size_t g_grave_bytes = 0;
 constexpr size_t kGraveCap = size_t(4) << 30;
 
 static void drain_graveyard_locked() {
-    for (void* q : g_grave) cudaFree(q);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (const auto& q : g_grave) {
+        if (q.first != cur) cudaSetDevice(q.first);
+        cudaFree(q.second);
+        if (q.first != cur) cudaSetDevice(cur);
+    }
     g_grave.clear();
     g_grave_bytes = 0;
 }
 
 static void retire(void* q, size_t nb) {
+    int dev = 0;
+    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(g_grave_mu);
-    g_grave.push_back(q);
+    g_grave.emplace_back(dev, q);
     g_grave_bytes += nb;
     if (g_grave_bytes > kGraveCap) drain_graveyard_locked();
 }
