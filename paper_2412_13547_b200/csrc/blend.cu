@@ -26,11 +26,12 @@
 //      forward; g.dC/dsigma_i = T_i (g.c_i) - (g.S_i)/(1 - sigma_i) with the reference's exact
 //      suffix S_i (rasterizer.cpp:266-287) carried as the scalar g.S; records u = dL/dsigma * G
 //      and the blend weight w per (splat, pixel) in a dense shared-memory row per splat;
-//   2. per splat (lane = row), dense over the group's 32 pixels: every position / covariance
-//      gradient of rasterizer.cpp:276-285 is linear in the moments sum(u), sum(u dx), sum(u dy),
-//      sum(u dx^2), sum(u dx dy), sum(u dy^2) and the colour gradient is sum(g w); with fixed
-//      pixel offsets these are FFMA-with-immediate sums, accumulated across the tile's groups in
-//      lane j's registers. After the chunk lane j converts them to the 9 screen-space gradients
+//   2. per record row and half (lane 2i + h), dense over the half's 32 pixels: every position /
+//      covariance gradient of rasterizer.cpp:276-285 is linear in the moments sum(u), sum(u dx),
+//      sum(u dy), sum(u dx^2), sum(u dx dy), sum(u dy^2) and the colour gradient is sum(g w);
+//      with fixed pixel offsets these are packed FADD2 / FFMA2 sums, handed (through the just
+//      read rows) to lane j = the row's splat and accumulated across the tile's groups in its
+//      registers. After the chunk lane j converts them to the 9 screen-space gradients
 //      and writes its (tile, splat) pair slot once — no reductions, no atomics, deterministic;
 //      the per-Gaussian merge in optim.cu walks the slots in tile order like
 //      rasterizer.cpp:301-319.
